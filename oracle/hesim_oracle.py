@@ -1,0 +1,480 @@
+"""oracle/hesim_oracle.py -- TEST INFRASTRUCTURE ONLY.
+
+numpy restatement of the reference `hesim` slot simulator for the hot path
+(the cleartext/slot-level oracle).  Every function cites the reference
+file:line it follows; tests/test_oracle_hesim.py pins it against the
+reference's own known-answer tests (proj/tests/*.cpp).  Only tests/,
+__graft_entry__.smoke() and bench.py's cpu_baseline leg may import this.
+
+Parity status: pinned (slot values, HOP counts, stage labels) against the
+reference's golden expectations; the reference itself cannot be built here
+(Eigen3 + vendor/ absent).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+CIPHERTEXT, PLAINTEXT = "ct", "pt"
+
+
+class CapacityError(RuntimeError):
+    """proj/include/hesim/errors.hpp:9-12"""
+
+
+class ShapeError(RuntimeError):
+    """proj/include/hesim/errors.hpp:14-17"""
+
+
+# ----------------------------------------------------------------- meter ---
+@dataclass
+class OpTally:
+    """proj/include/hesim/meter.hpp:12-31"""
+    add_pc: int = 0
+    add_cc: int = 0
+    mul_pc: int = 0
+    mul_cc: int = 0
+    rot: int = 0
+
+    def total(self):
+        return self.add_pc + self.add_cc + self.mul_pc + self.mul_cc + self.rot
+
+    def as_tuple(self):
+        return (self.add_pc, self.add_cc, self.mul_pc, self.mul_cc, self.rot)
+
+
+@dataclass
+class MeterContext:
+    """proj/include/hesim/meter.hpp:36-70 (begin_stage re-enters rows)."""
+    tally: OpTally = field(default_factory=OpTally)
+    stages: list = field(default_factory=list)
+    _cur: int = -1
+
+    def begin_stage(self, label):
+        for i, (name, _) in enumerate(self.stages):
+            if name == label:
+                self._cur = i
+                return
+        self.stages.append((label, OpTally()))
+        self._cur = len(self.stages) - 1
+
+    def bump(self, f):
+        setattr(self.tally, f, getattr(self.tally, f) + 1)
+        if self._cur >= 0:
+            t = self.stages[self._cur][1]
+            setattr(t, f, getattr(t, f) + 1)
+
+
+# --------------------------------------------------------------- slotvec ---
+def is_power_of_two(x):
+    return x > 0 and (x & (x - 1)) == 0
+
+
+class SlotVector:
+    """proj/include/hesim/slotvec.hpp:14-33; ctor proj/src/slotvec.cpp:12-18"""
+
+    def __init__(self, slots, kind):
+        slots = np.asarray(slots, dtype=np.float64)
+        if not is_power_of_two(slots.size):
+            raise ShapeError(f"slot count must be a power of two, got {slots.size}")
+        self.slots = slots
+        self.kind = kind
+
+    @property
+    def n_slots(self):
+        return self.slots.size
+
+    def __getitem__(self, i):
+        return self.slots[i]
+
+    def is_zero(self):
+        return not np.any(self.slots)
+
+    def masked_prefix(self, keep):  # proj/src/slotvec.cpp:20-24
+        out = self.slots.copy()
+        out[keep:] = 0.0
+        return SlotVector(out, self.kind)
+
+
+def pack(values, n_slots, kind):
+    """proj/src/slotvec.cpp:26-36"""
+    values = np.asarray(values, dtype=np.float64).ravel()
+    if values.size > n_slots:
+        raise CapacityError(f"pack: {values.size} values exceed {n_slots} slots")
+    s = np.zeros(n_slots)
+    s[: values.size] = values
+    return SlotVector(s, kind)
+
+
+def zeros(n_slots, kind):
+    """proj/src/slotvec.cpp:38-40"""
+    return SlotVector(np.zeros(n_slots), kind)
+
+
+def rotate_right(v, r, ctx):
+    """proj/src/slotvec.cpp:42-57: out[j] = v[(j - r) mod N]; r=0 free;
+    only ciphertext rotations are metered."""
+    n = v.n_slots
+    if r < 0 or r >= n:
+        raise IndexError(f"rotate: amount {r} outside [0, {n})")
+    if r == 0:
+        return v
+    if v.kind == CIPHERTEXT:
+        ctx.bump("rot")
+    return SlotVector(np.roll(v.slots, r), v.kind)
+
+
+def rotate_left(v, r, ctx):
+    """proj/src/slotvec.cpp:59-66"""
+    n = v.n_slots
+    if r < 0 or r >= n:
+        raise IndexError(f"rotate: amount {r} outside [0, {n})")
+    return rotate_right(v, 0 if r == 0 else n - r, ctx)
+
+
+def _meter_binary(a, b, ctx, cc, pc):
+    """proj/src/slotvec.cpp:76-86"""
+    n_ct = (a.kind == CIPHERTEXT) + (b.kind == CIPHERTEXT)
+    if n_ct == 2:
+        ctx.bump(cc)
+    elif n_ct == 1:
+        ctx.bump(pc)
+
+
+def _result_kind(a, b):
+    return CIPHERTEXT if CIPHERTEXT in (a.kind, b.kind) else PLAINTEXT
+
+
+def _check_shapes(a, b):  # proj/src/slotvec.cpp:88-93
+    if a.n_slots != b.n_slots:
+        raise ShapeError(f"slot count mismatch: {a.n_slots} vs {b.n_slots}")
+
+
+def add(a, b, ctx):
+    """proj/src/slotvec.cpp:97-102"""
+    _check_shapes(a, b)
+    _meter_binary(a, b, ctx, "add_cc", "add_pc")
+    return SlotVector(a.slots + b.slots, _result_kind(a, b))
+
+
+def mul(a, b, ctx):
+    """proj/src/slotvec.cpp:104-109"""
+    _check_shapes(a, b)
+    _meter_binary(a, b, ctx, "mul_cc", "mul_pc")
+    return SlotVector(a.slots * b.slots, _result_kind(a, b))
+
+
+# ---------------------------------------------------------------- matvec ---
+def next_power_of_two(x):
+    """proj/src/matvec.cpp:10-14"""
+    p = 1
+    while p < x:
+        p <<= 1
+    return p
+
+
+def _ceil_div(a, b):
+    return (a + b - 1) // b
+
+
+def _ceil_log2(x):
+    b = 0
+    while (1 << b) < x:
+        b += 1
+    return b
+
+
+def plain_branch_fits(m, n, n_slots):
+    """proj/src/matvec.cpp:29-33"""
+    if n_slots < m + n - 1:
+        return False
+    b = _ceil_log2(_ceil_div(m + n - 1, m))
+    return (m << b) <= n_slots
+
+
+def _check_dims(m, n, n_slots):  # proj/src/matvec.cpp:35-41
+    if m > n_slots or n > n_slots:
+        raise CapacityError(f"matrix {m}x{n} exceeds {n_slots} slots")
+
+
+def extract_diagonals(A, n_slots):
+    """proj/src/matvec.cpp:45-65 -> (m_eff, masks[m_eff][n_slots])"""
+    A = np.asarray(A, dtype=np.float64)
+    m, n = A.shape
+    _check_dims(m, n, n_slots)
+    m_eff = m if plain_branch_fits(m, n, n_slots) else next_power_of_two(m)
+    if m_eff > n_slots:
+        raise CapacityError(f"padded row count {m_eff} exceeds {n_slots} slots")
+    masks = np.zeros((m_eff, n_slots))
+    j = np.arange(n)
+    for i in range(m_eff):
+        row = (i + j) % m_eff
+        ok = row < m
+        masks[i, j[ok]] = A[row[ok], j[ok]]
+    return m_eff, masks
+
+
+def hs_folds(m, n, n_slots, m_eff):
+    """fold count of proj/src/matvec.cpp:88-91"""
+    padded = m_eff != m or not plain_branch_fits(m, n, n_slots)
+    return _ceil_log2(n_slots // m_eff) if padded else _ceil_log2(_ceil_div(m + n - 1, m))
+
+
+def rotate_and_sum(v, span, block, ctx):
+    """proj/src/matvec.cpp:67-80"""
+    if block < 1 or block > v.n_slots:
+        raise IndexError("rotate_and_sum: block out of range")
+    folds = _ceil_log2(_ceil_div(span, block))
+    s = v
+    for t in range(folds - 1, -1, -1):
+        s = add(s, rotate_left(s, block << t, ctx), ctx)
+    return s
+
+
+def hs_matvec(A, v, ctx, skip_zero_diagonals=True):
+    """proj/src/matvec.cpp:82-105"""
+    A = np.asarray(A, dtype=np.float64)
+    m, n = A.shape
+    N = v.n_slots
+    _check_dims(m, n, N)
+    m_eff, masks = extract_diagonals(A, N)
+    folds = hs_folds(m, n, N, m_eff)
+    s = zeros(N, CIPHERTEXT)
+    first = True
+    for i in range(m_eff):
+        if skip_zero_diagonals and not np.any(masks[i]):
+            continue
+        t = rotate_right(mul(SlotVector(masks[i], PLAINTEXT), v, ctx), i, ctx)
+        s = t if first else add(s, t, ctx)
+        first = False
+    for t in range(folds - 1, -1, -1):
+        s = add(s, rotate_left(s, m_eff << t, ctx), ctx)
+    return s
+
+
+def predict_hs(m, n, n_slots):
+    """proj/src/matvec.cpp:168-187 -> (rotations, multiplications, additions)"""
+    _check_dims(m, n, n_slots)
+    if plain_branch_fits(m, n, n_slots):
+        folds = _ceil_log2(_ceil_div(m + n - 1, m))
+        return (m - 1 + folds, m, m - 1 + folds)
+    mp = next_power_of_two(m)
+    if mp > n_slots:
+        raise CapacityError("padded row count exceeds slot count")
+    folds = _ceil_log2(n_slots // mp)
+    return (mp - 1 + folds, mp, mp - 1 + folds)
+
+
+# -------------------------------------------------------------- convlower ---
+@dataclass
+class ConvShape:
+    """proj/include/hesim/convlower.hpp:13-17"""
+    d_in: int
+    c_in: int
+    kernel_k: int
+    stride: int
+    c_out: int
+
+    def d_out(self):
+        return (self.d_in - self.kernel_k) // self.stride + 1
+
+
+def conv_pack(image, shape, n_slots):
+    """proj/src/convlower.cpp:9-37; image [c][h][w]; tap t=(ci*k+ky)*k+kx"""
+    image = np.asarray(image, dtype=np.float64)
+    d_out = shape.d_out()
+    if d_out * d_out > n_slots:
+        raise CapacityError("conv_pack: output positions exceed slots")
+    if image.shape[0] != shape.c_in or image.shape[1] != shape.d_in:
+        raise ShapeError("conv_pack: image does not match shape")
+    k, s = shape.kernel_k, shape.stride
+    taps = []
+    o = np.arange(d_out) * s
+    for ci in range(shape.c_in):
+        for ky in range(k):
+            for kx in range(k):
+                v = np.zeros(n_slots)
+                v[: d_out * d_out] = image[ci][np.ix_(o + ky, o + kx)].ravel()
+                taps.append(SlotVector(v, CIPHERTEXT))
+    return taps
+
+
+def conv_packed_forward(taps, weights, bias, shape, ctx):
+    """proj/src/convlower.cpp:39-74; weights [c_out][c_in][k][k]"""
+    k = shape.kernel_k
+    n_taps = k * k * shape.c_in
+    weights = np.asarray(weights, dtype=np.float64)
+    if len(taps) != n_taps or weights.shape != (shape.c_out, shape.c_in, k, k):
+        raise ShapeError("conv_packed_forward: filter/tap shape mismatch")
+    N = taps[0].n_slots
+    w = shape.d_out() ** 2
+    maps = []
+    for co in range(shape.c_out):
+        acc = None
+        for t in range(n_taps):
+            ci, ky, kx = t // (k * k), (t // k) % k, t % k
+            pt = np.zeros(N)
+            pt[:w] = weights[co, ci, ky, kx]
+            prod = mul(SlotVector(pt, PLAINTEXT), taps[t], ctx)
+            acc = prod if t == 0 else add(acc, prod, ctx)
+        bpt = np.zeros(N)
+        bpt[:w] = bias[co] if bias is not None and len(bias) else 0.0
+        maps.append(add(acc, SlotVector(bpt, PLAINTEXT), ctx))
+    return maps
+
+
+def conv_to_matrix(shape, weights):
+    """proj/src/convlower.cpp:76-102 (dense form)"""
+    weights = np.asarray(weights, dtype=np.float64)
+    d_out, d_in, k, s = shape.d_out(), shape.d_in, shape.kernel_k, shape.stride
+    A = np.zeros((d_out * d_out * shape.c_out, d_in * d_in * shape.c_in))
+    for co in range(shape.c_out):
+        for oy in range(d_out):
+            for ox in range(d_out):
+                r = (co * d_out + oy) * d_out + ox
+                for ci in range(shape.c_in):
+                    for ky in range(k):
+                        for kx in range(k):
+                            col = (ci * d_in + oy * s + ky) * d_in + ox * s + kx
+                            A[r, col] += weights[co, ci, ky, kx]
+    return A
+
+
+def conv_bias_vector(shape, bias):
+    """proj/src/convlower.cpp:104-113"""
+    w = shape.d_out() ** 2
+    return np.repeat(np.asarray(bias, dtype=np.float64), w)
+
+
+def square_layer(v, ctx):
+    """proj/src/convlower.cpp:141-143"""
+    return mul(v, v, ctx)
+
+
+def merge_maps(maps, w, ctx):
+    """proj/src/convlower.cpp:145-160"""
+    if not maps:
+        raise ShapeError("merge_maps: no maps")
+    N = maps[0].n_slots
+    c = len(maps)
+    if c * w > N:
+        raise CapacityError(f"merge_maps: {c} maps of {w} slots exceed {N} slots")
+    out = maps[0]
+    for j in range(1, c):
+        out = add(out, rotate_right(maps[j], j * w, ctx), ctx)
+    return out
+
+
+# -------------------------------------------------------------- refmodel ---
+def ref_conv(x, weights, bias, stride):
+    """proj/src/refmodel.cpp:21-46 (same accumulation order)"""
+    x = np.asarray(x, dtype=np.float64)
+    weights = np.asarray(weights, dtype=np.float64)
+    c_out, c_in, k, _ = weights.shape
+    if x.shape[0] != c_in:
+        raise ShapeError("conv: channel mismatch")
+    if k > x.shape[1]:
+        raise ShapeError("window larger than input")
+    d_out = (x.shape[1] - k) // stride + 1
+    out = np.zeros((c_out, d_out, d_out))
+    for co in range(c_out):
+        for oy in range(d_out):
+            for ox in range(d_out):
+                acc = bias[co] if bias is not None and len(bias) else 0.0
+                for ci in range(c_in):
+                    for ky in range(k):
+                        for kx in range(k):
+                            acc += weights[co, ci, ky, kx] * x[ci, oy * stride + ky, ox * stride + kx]
+                out[co, oy, ox] = acc
+    return out
+
+
+def ref_square(x):
+    """proj/src/refmodel.cpp:68-72"""
+    return np.asarray(x) * np.asarray(x)
+
+
+def ref_dense(v, W, b):
+    """proj/src/refmodel.cpp:74-80"""
+    W = np.asarray(W, dtype=np.float64)
+    if W.shape[1] != len(v) or W.shape[0] != len(b):
+        raise ShapeError("dense: dimension mismatch")
+    return W @ v + b
+
+
+# -------------------------------------------------- the CNN (stage driver) ---
+@dataclass
+class CnnSpec:
+    """The hot-path model family: Conv(k, s, c_out) -> Square -> Dense(m1) ->
+    Square -> Dense(m2) (BASELINE configs 0/2/3; the cryptonets-style L' net
+    after fusion, proj/src/netcompile.cpp:106-213)."""
+    in_c: int
+    in_d: int
+    k: int
+    s: int
+    c_out: int
+    dense: tuple
+    n_slots: int
+
+    def shape(self):
+        return ConvShape(self.in_d, self.in_c, self.k, self.s, self.c_out)
+
+    def stage_labels(self):
+        """lower() output for this layer list (netcompile.cpp:106-213)."""
+        labels = ["Conv1", "Flat1"]
+        for i, _ in enumerate(self.dense):
+            labels.append(f"Square{i + 1}")
+            labels.append(f"Dense{i + 1}")
+        return labels
+
+
+def execute(spec, weights, image, ctx):
+    """proj/src/netcompile.cpp:291-446 restricted to ConvPack / Merge /
+    Square / Linear(HS) stages.  weights = dict(conv_w, conv_b, dense=[(W,b)])
+    Returns the logits (first m_last slots of the output ciphertext)."""
+    shape = spec.shape()
+    N = spec.n_slots
+    ctx.begin_stage("Conv1")
+    taps = conv_pack(image, shape, N)
+    maps = conv_packed_forward(taps, weights["conv_w"], weights["conv_b"], shape, ctx)
+    ctx.begin_stage("Flat1")
+    ct = merge_maps(maps, shape.d_out() ** 2, ctx)
+    for i, (W, b) in enumerate(weights["dense"]):
+        ctx.begin_stage(f"Square{i + 1}")
+        ct = square_layer(ct, ctx)
+        ctx.begin_stage(f"Dense{i + 1}")
+        out = hs_matvec(W, ct, ctx)
+        out = add(out, pack(b, N, PLAINTEXT), ctx)
+        ct = out.masked_prefix(np.asarray(W).shape[0])
+    return ct.slots[: np.asarray(weights["dense"][-1][0]).shape[0]].copy()
+
+
+def ref_forward(spec, weights, image):
+    """proj/src/netcompile.cpp:448-503 for the same layer list."""
+    t = ref_conv(image, weights["conv_w"], weights["conv_b"], spec.s)
+    flat = None
+    for i, (W, b) in enumerate(weights["dense"]):
+        if flat is None:
+            t = ref_square(t)
+            flat = t.ravel()
+        else:
+            flat = ref_square(flat)
+        flat = ref_dense(flat, W, b)
+    return flat
+
+
+def golden_stage_tallies(spec):
+    """Closed-form per-stage HOPs (add_pc, add_cc, mul_pc, mul_cc, rot) for
+    dense weights with no zero diagonals."""
+    shape = spec.shape()
+    taps = shape.kernel_k ** 2 * shape.c_in
+    rows = {"Conv1": (shape.c_out, (taps - 1) * shape.c_out, taps * shape.c_out, 0, 0),
+            "Flat1": (0, shape.c_out - 1, 0, 0, shape.c_out - 1)}
+    n = shape.c_out * shape.d_out() ** 2
+    for i, m in enumerate(spec.dense):
+        rows[f"Square{i + 1}"] = (0, 0, 0, 1, 0)
+        rot, mul_, add_ = predict_hs(m, n, spec.n_slots)
+        rows[f"Dense{i + 1}"] = (1, add_, mul_, 0, rot)
+        n = m
+    return rows

@@ -1,0 +1,92 @@
+"""Seeded synthetic workloads for the BASELINE.json configs.
+
+There is no public dataset on this path (BASELINE.json names "MNIST-sized"
+and "CIFAR-10-shaped synthetic" inputs only); these generators stand in with
+the stated shapes and distributions:
+  - images U[0,1], MNIST 28x28 zero-padded bottom/right to 29x29
+    (proj/src/netcompile.cpp:571 pads to 29 without naming the side);
+  - weights N(0, sigma^2) (0.05 MNIST-sized, 0.02 CIFAR-shaped), biases
+    N(0, 0.01^2), all rounded to f32 like the reference weight format
+    (proj/src/modelio.cpp:54-70 reads little-endian f32 as double).
+numpy's PCG64 is used so every host produces identical values.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class NetConfig:
+    name: str
+    in_c: int
+    img_d: int        # unpadded image side
+    in_d: int         # padded side fed to the conv
+    k: int
+    s: int
+    c_out: int
+    dense: tuple      # output units of the HS layers
+    log_n: int        # ring degree N = 2^log_n; slots S = N/2
+    qbits: tuple      # Q chain (q_0 first); len-1 rescales
+    pbits: int        # special prime P
+    w_sigma: float
+    b_sigma: float = 0.01
+    log_scale: int = 40
+
+    @property
+    def n_slots(self):
+        return 1 << (self.log_n - 1)
+
+    @property
+    def d_out(self):
+        return (self.in_d - self.k) // self.s + 1
+
+    @property
+    def n_taps(self):
+        return self.k * self.k * self.in_c
+
+
+# BASELINE.json configs[0] (and [2] = 64 of these)
+CFG0 = NetConfig("cfg0-mnist", 1, 28, 29, 5, 2, 5, (100, 10), 13,
+                 (60, 40, 40, 40, 40, 40), 60, 0.05)
+# BASELINE.json configs[3]
+CFG3 = NetConfig("cfg3-cifar", 3, 32, 32, 5, 2, 32, (256, 10), 14,
+                 (60, 40, 40, 40, 40, 40), 60, 0.02)
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def net_weights(cfg: NetConfig, seed: int):
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 0x5EED]))
+    w = {
+        "conv_w": f32(rng.normal(0.0, cfg.w_sigma, (cfg.c_out, cfg.in_c, cfg.k, cfg.k))),
+        "conv_b": f32(rng.normal(0.0, cfg.b_sigma, cfg.c_out)),
+        "dense": [],
+    }
+    n = cfg.c_out * cfg.d_out ** 2
+    for m in cfg.dense:
+        W = f32(rng.normal(0.0, cfg.w_sigma, (m, n)))
+        b = f32(rng.normal(0.0, cfg.b_sigma, m))
+        w["dense"].append((W, b))
+        n = m
+    return w
+
+
+def net_image(cfg: NetConfig, seed: int):
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 0x1A6E]))
+    img = np.zeros((cfg.in_c, cfg.in_d, cfg.in_d))
+    img[:, : cfg.img_d, : cfg.img_d] = f32(rng.uniform(0.0, 1.0, (cfg.in_c, cfg.img_d, cfg.img_d)))
+    return img
+
+
+def cfg0_weights_and_image(seed: int = 0):
+    return net_weights(CFG0, seed), net_image(CFG0, seed)
+
+
+def hs_sweep_case(m: int, n: int, seed: int = 0):
+    """BASELINE.json configs[1]: A ~ N(0, 0.05^2) (m x n), v ~ U[-1, 1]^n."""
+    rng = np.random.default_rng(np.random.SeedSequence([seed, m, n]))
+    return f32(rng.normal(0.0, 0.05, (m, n))), f32(rng.uniform(-1.0, 1.0, n))
