@@ -1,0 +1,187 @@
+/*
+ * hegpu.h -- C-ABI of the B200-native CKKS engine behind the reference's
+ * evaluator / layer API (arXiv 2110.08321, reference `hesim`).
+ *
+ * The reference has no FFI: it is a static C++ library of free functions
+ * over value types (proj/CMakeLists.txt:10-19).  This header is the
+ * boundary SURVEY.md §8b specifies: opaque handles, plain pointers and
+ * sizes, int status codes, a per-context last-error string.  Each entry
+ * point names the reference interface it replaces (file:line, paths
+ * relative to the reference root).  include/hegpu.hpp restores the hesim::
+ * value-semantics names on top of it; INTEGRATION.md shows the bindings.
+ *
+ * Data formats ("wire format", what upload/download/encode/encrypt use):
+ *   - a polynomial at level l is l limbs of N uint64 words, limb i reduced
+ *     mod q_i, in the NTT domain with bit-reversed evaluation order (word k
+ *     of a limb holds a(psi^(2*brv(k)+1))); the extended basis appends the
+ *     special prime P as limb l;
+ *   - a ciphertext is [2][l][N] (c0 then c1); a batch of `count`
+ *     ciphertexts is [count][2][l][N]; a plaintext batch is [count][l'][N].
+ * Device-internal layout differs (slot-ordered evaluations so Galois
+ * rotations are cyclic shifts, Montgomery-form plaintexts); upload and
+ * download convert, so wire limbs are bit-identical to the CPU oracle.
+ *
+ * Metering: every evaluator/layer call bumps the context's OpTally under
+ * the current stage exactly like the reference (proj/src/slotvec.cpp:49-52,
+ * 76-86): a call on a batch of `count` ciphertexts counts `count` ops.
+ */
+#ifndef HEGPU_H
+#define HEGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; errors map onto proj/include/hesim/errors.hpp:9-26 and
+ * std::out_of_range (proj/src/slotvec.cpp:45-48) */
+enum {
+  HEGPU_OK = 0,
+  HEGPU_ERR_CAPACITY = 1, /* hesim::CapacityError */
+  HEGPU_ERR_SHAPE = 2,    /* hesim::ShapeError    */
+  HEGPU_ERR_LAYOUT = 3,   /* hesim::LayoutError   */
+  HEGPU_ERR_RANGE = 4,    /* std::out_of_range    */
+  HEGPU_ERR_IO = 5,       /* hesim::IoError       */
+  HEGPU_ERR_CUDA = 6,     /* CUDA runtime failure / no device */
+  HEGPU_ERR_NCCL = 7,
+  HEGPU_ERR_ARG = 8,      /* null handle, bad parameter */
+  HEGPU_ERR_KEY = 9       /* missing evaluation key */
+};
+
+/* tally field order, proj/include/hesim/meter.hpp:12-31 */
+enum { HEGPU_ADD_PC = 0, HEGPU_ADD_CC = 1, HEGPU_MUL_PC = 2, HEGPU_MUL_CC = 3, HEGPU_ROT = 4 };
+
+typedef struct hegpu_ctx hegpu_ctx;
+typedef struct hegpu_ct hegpu_ct;
+typedef struct hegpu_pt hegpu_pt;
+typedef struct hegpu_hs_plan hegpu_hs_plan;
+typedef struct hegpu_net hegpu_net;
+
+#define HEGPU_MAX_Q 15
+
+typedef struct {
+  int log_n;                 /* ring degree N = 2^log_n, slots S = N/2 */
+  int n_q;                   /* Q chain length L (L-1 rescales) */
+  int q_bits[HEGPU_MAX_Q];   /* bit sizes of q_0..q_{L-1} (<= 61) */
+  int p_bits;                /* special prime P (<= 61) */
+  uint64_t seed;             /* secret / key / encryption randomness */
+} hegpu_params;
+
+/* ---- context ------------------------------------------------------------ */
+/* device = HEGPU_CLIENT_ONLY creates a host-only context for the data-owner
+ * side (encode / encrypt / decrypt / key export); every device call on it
+ * fails with HEGPU_ERR_CUDA -- there is no CPU evaluator. */
+#define HEGPU_CLIENT_ONLY (-1)
+int hegpu_ctx_create(const hegpu_params* p, int device, hegpu_ctx** out);
+void hegpu_ctx_destroy(hegpu_ctx* ctx);
+const char* hegpu_last_error(const hegpu_ctx* ctx);
+/* N, S, L and the L+1 primes (q_0..q_{L-1}, P) */
+int hegpu_ctx_info(const hegpu_ctx* ctx, int* n, int* slots, int* n_q, uint64_t* primes);
+int hegpu_sync(hegpu_ctx* ctx);
+/* kernels launched by this context since creation (ours only) */
+int64_t hegpu_kernel_launches(const hegpu_ctx* ctx);
+
+/* ---- metering: proj/include/hesim/meter.hpp:36-70 ----------------------- */
+int hegpu_begin_stage(hegpu_ctx* ctx, const char* label);
+int hegpu_num_stages(const hegpu_ctx* ctx);
+int hegpu_stage_tally(const hegpu_ctx* ctx, int idx, char* label, int label_len, int64_t tally[5]);
+int hegpu_total_tally(const hegpu_ctx* ctx, int64_t tally[5]);
+int hegpu_reset_meter(hegpu_ctx* ctx);
+
+/* ---- client side (host CPU; the reference's pack/conv_pack are client-side,
+ *      proj/include/hesim/convlower.hpp:20-23, proj/src/slotvec.cpp:26-40) --- */
+/* pack(values, n_slots, Plaintext) (proj/src/slotvec.cpp:26-36) as a CKKS
+ * encoding at `scale`: out = level (+1 if with_p) limbs */
+int hegpu_encode(hegpu_ctx* ctx, const double* z, int len, double scale, int level, int with_p,
+                 uint64_t* out);
+int hegpu_decode(hegpu_ctx* ctx, const uint64_t* pt, int level, double scale, double* slots);
+/* pack(values, n_slots, Ciphertext): symmetric encryption of an encoded pt */
+int hegpu_encrypt(hegpu_ctx* ctx, const uint64_t* pt, int level, uint64_t nonce, uint64_t* ct);
+int hegpu_decrypt(hegpu_ctx* ctx, const uint64_t* ct, int level, uint64_t* pt);
+/* Galois keys for right rotations by r (slotvec.cpp:42-57 semantics) and the
+ * relinearisation key; generated on the host, stored on the device */
+int hegpu_gen_rotation_keys(hegpu_ctx* ctx, const int64_t* right_rots, int n);
+int hegpu_gen_relin_key(hegpu_ctx* ctx);
+/* host copy of a generated key, wire format [L][2][L+1][N] (for tests) */
+int hegpu_export_rotation_key(hegpu_ctx* ctx, int64_t right_rot, uint64_t* out);
+int hegpu_export_relin_key(hegpu_ctx* ctx, uint64_t* out);
+
+/* ---- device ciphertext / plaintext batches ------------------------------ */
+int hegpu_ct_create(hegpu_ctx* ctx, int count, int level, hegpu_ct** out);
+void hegpu_ct_destroy(hegpu_ct* ct);
+int hegpu_ct_upload(hegpu_ct* ct, const uint64_t* host, size_t nwords, double scale);
+int hegpu_ct_download(hegpu_ct* ct, uint64_t* host, size_t nwords);
+int hegpu_ct_info(const hegpu_ct* ct, int* count, int* level, double* scale);
+int hegpu_pt_create(hegpu_ctx* ctx, int count, int level, int with_p, hegpu_pt** out);
+void hegpu_pt_destroy(hegpu_pt* pt);
+int hegpu_pt_upload(hegpu_pt* pt, const uint64_t* host, size_t nwords, double scale);
+int hegpu_pt_download(hegpu_pt* pt, uint64_t* host, size_t nwords);
+
+/* ---- evaluator: proj/include/hesim/slotvec.hpp:44-52 -------------------- */
+/* add(ct, ct): Add CC (slotvec.cpp:97-102) */
+int hegpu_add(hegpu_ctx* ctx, const hegpu_ct* a, const hegpu_ct* b, hegpu_ct* out);
+/* add(ct, pt): Add PC; pt count 1 broadcasts over the batch */
+int hegpu_add_plain(hegpu_ctx* ctx, const hegpu_ct* a, const hegpu_pt* p, hegpu_ct* out);
+/* mul(ct, pt): Mul PC (slotvec.cpp:104-109); pt count 1 broadcasts */
+int hegpu_mul_plain(hegpu_ctx* ctx, const hegpu_ct* a, const hegpu_pt* p, hegpu_ct* out);
+/* CKKS rescale (new; the reference models no levels): unmetered */
+int hegpu_rescale(hegpu_ctx* ctx, const hegpu_ct* a, hegpu_ct* out);
+/* rotate_right / rotate_left (slotvec.cpp:42-66): Rot, r=0 free,
+ * r outside [0, S) -> HEGPU_ERR_RANGE */
+int hegpu_rotate_right(hegpu_ctx* ctx, const hegpu_ct* a, int64_t r, hegpu_ct* out);
+int hegpu_rotate_left(hegpu_ctx* ctx, const hegpu_ct* a, int64_t r, hegpu_ct* out);
+
+/* ---- layers: proj/include/hesim/convlower.hpp:24-54, matvec.hpp:41-66 --- */
+/* square_layer (convlower.cpp:141-143): Mul CC + relinearise + rescale */
+int hegpu_square(hegpu_ctx* ctx, const hegpu_ct* a, hegpu_ct* out);
+/* conv_packed_forward (convlower.cpp:39-74) + rescale: taps = count B*ntaps
+ * ordered [b][t] (t = (ci*k+ky)*k+kx), weights [c_out][ntaps] (f64),
+ * bias [c_out] (may be NULL), w_used = d_out^2 slots carrying the bias.
+ * maps_out: count B*c_out ordered [b][co], level l-1. */
+int hegpu_conv_packed_forward(hegpu_ctx* ctx, const hegpu_ct* taps, int ntaps, const double* weights,
+                              int c_out, const double* bias, int w_used, hegpu_ct* maps_out);
+/* merge_maps (convlower.cpp:145-160): maps count B*c ordered [b][j];
+ * out count B; CapacityError if c*w > S */
+int hegpu_merge_maps(hegpu_ctx* ctx, const hegpu_ct* maps, int c, int64_t w, hegpu_ct* out);
+/* extract_diagonals (matvec.cpp:45-65) + encode, once per matrix (offline);
+ * A is m x n row-major, input ciphertexts at `level` */
+int hegpu_hs_plan_create(hegpu_ctx* ctx, const double* A, int m, int n, int level,
+                         int skip_zero_diagonals, hegpu_hs_plan** out);
+void hegpu_hs_plan_destroy(hegpu_hs_plan* plan);
+/* right rotations the plan needs keys for (diagonal offsets, then folds as
+ * right-rotation amounts); returns the count, fills `rots` if non-NULL */
+int hegpu_hs_plan_rotations(const hegpu_hs_plan* plan, int64_t* rots, int cap);
+int hegpu_hs_plan_info(const hegpu_hs_plan* plan, int* m_eff, int* folds, int* kept);
+/* hs_matvec (matvec.cpp:82-105): out level = level-1 (one rescale) */
+int hegpu_hs_matvec(hegpu_ctx* ctx, const hegpu_hs_plan* plan, const hegpu_ct* v, hegpu_ct* out);
+
+/* ---- stage driver: execute (proj/src/netcompile.cpp:291-446) ------------ */
+typedef struct {
+  int in_c, in_d, k, stride, c_out;  /* first-layer conv (ConvPack stage) */
+  int n_dense;                       /* Square+Dense pairs that follow */
+  int dense_out[4];
+} hegpu_net_spec;
+/* weights: conv_w [c_out][in_c][k][k], conv_b [c_out], then per dense layer
+ * W (row-major m x n) and b [m]; all f64 */
+int hegpu_net_create(hegpu_ctx* ctx, const hegpu_net_spec* spec, const double* conv_w,
+                     const double* conv_b, const double* const* dense_w,
+                     const double* const* dense_b, hegpu_net** out);
+void hegpu_net_destroy(hegpu_net* net);
+/* device-resident run: taps = count B*ntaps at the top level */
+int hegpu_net_run(hegpu_net* net, const hegpu_ct* taps, hegpu_ct* out);
+/* end-to-end run from host buffers (wire format taps [B][ntaps][2][L][N]
+ * -> output cts [B][2][1][N]); includes both host<->device copies */
+int hegpu_net_run_host(hegpu_net* net, const uint64_t* host_taps, int batch, uint64_t* host_out);
+/* client helper: conv_pack (convlower.cpp:9-37) + encode + encrypt of one
+ * image [in_c][in_d][in_d] -> ntaps wire ciphertexts at the top level */
+int hegpu_net_encrypt_image(hegpu_net* net, const double* image, uint64_t nonce, uint64_t* taps_out);
+/* logits: decrypt + decode output ct (wire) into m_last values */
+int hegpu_net_decrypt_logits(hegpu_net* net, const uint64_t* out_ct, double* logits);
+double hegpu_net_output_scale(const hegpu_net* net);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEGPU_H */

@@ -1,0 +1,115 @@
+"""oracle/ckks_pipeline.py -- TEST INFRASTRUCTURE ONLY: the CPU-oracle versions of the layer compositions the GPU
+path runs, built from oracle/ckks.py primitives and the slot-level
+restatement of the reference (oracle/hesim_oracle.py).  Test
+infrastructure only."""
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import hesim_oracle as HS
+
+
+def hs_masks(ck, A, level, skip_zero=True):
+    """extract_diagonals (proj/src/matvec.cpp:45-65) then mask'_i =
+    rot_right(mask_i, i), encoded at scale q_{level-1} in the extended basis."""
+    m, n = A.shape
+    S = ck.S
+    m_eff, masks = HS.extract_diagonals(A, S)
+    folds = HS.hs_folds(m, n, S, m_eff)
+    rots, enc = [], []
+    for i in range(m_eff):
+        if skip_zero and not masks[i].any():
+            continue
+        rots.append(i)
+        enc.append(ck.encode(np.roll(masks[i], i), float(ck.primes[level - 1]), level, with_p=True))
+    return m_eff, folds, rots, (np.concatenate(enc) if enc else np.zeros(0, dtype=np.uint64))
+
+
+def hs_matvec(ck, v, level, A, skip_zero=True, keys=None):
+    """Oracle HS layer: hoisted diagonal sum, rescale, log-depth fold
+    (proj/src/matvec.cpp:82-105).  Returns ct at level-1."""
+    m_eff, folds, rots, masks = hs_masks(ck, A, level, skip_zero)
+    keys = keys if keys is not None else {}
+
+    def key(g):
+        if g not in keys:
+            keys[g] = ck.galois_key(g)
+        return keys[g]
+
+    kl = [key(ck.galois_right(r)) for r in rots if r != 0]
+    kbuf = np.concatenate(kl) if kl else np.zeros(1, dtype=np.uint64)
+    u = ck.hs_hoisted(v, level, np.array(rots, dtype=np.int64), masks, kbuf)
+    u = ck.rescale(u, level)
+    l = level - 1
+    for t in range(folds - 1, -1, -1):
+        g = ck.galois_left(m_eff << t)
+        u = ck.add(u, ck.rotate(u, l, g, key(g)), l)
+    return u
+
+
+def conv_layer(ck, taps, ntaps, level, weights, bias, w_used, tap_scale):
+    """conv_packed_forward (proj/src/convlower.cpp:39-74) + rescale."""
+    c_out = len(weights) // ntaps if np.ndim(weights) == 1 else np.asarray(weights).shape[0]
+    w = np.asarray(weights, dtype=np.float64).reshape(c_out, ntaps)
+    qlast = float(ck.primes[level - 1])
+    bpts = np.concatenate([ck.encode(np.full(w_used, bias[co] if bias is not None else 0.0),
+                                     tap_scale * qlast, level) for co in range(c_out)])
+    maps = ck.conv_mac(taps, ntaps, level, w, c_out, qlast, bpts)
+    per = 2 * level * ck.N
+    return np.concatenate([ck.rescale(maps[co * per:(co + 1) * per], level) for co in range(c_out)])
+
+
+def merge(ck, maps, nmaps, level, w, keys=None):
+    """merge_maps (proj/src/convlower.cpp:145-160)."""
+    keys = keys if keys is not None else {}
+    kl = []
+    for j in range(1, nmaps):
+        g = ck.galois_right(j * w)
+        if g not in keys:
+            keys[g] = ck.galois_key(g)
+        kl.append(keys[g])
+    kbuf = np.concatenate(kl) if kl else np.zeros(1, dtype=np.uint64)
+    return ck.merge(maps, nmaps, level, w, kbuf)
+
+
+def square(ck, v, level, rlk):
+    return ck.rescale(ck.square(v, level, rlk), level)
+
+
+def conv_pack_taps(ck, cfg, image, nonce, tap_scale):
+    """Client side: conv_pack (proj/src/convlower.cpp:9-37) + encode + encrypt,
+    nonces nonce*ntaps + t (same convention as hegpu_net_encrypt_image)."""
+    shape = HS.ConvShape(cfg.in_d, cfg.in_c, cfg.k, cfg.s, cfg.c_out)
+    taps = HS.conv_pack(image, shape, ck.S)
+    L = ck.L
+    ntaps = len(taps)
+    w_used = shape.d_out() ** 2
+    cts = [ck.encrypt(ck.encode(t.slots[:w_used], tap_scale, L), L, nonce * ntaps + i) for i, t in enumerate(taps)]
+    return np.concatenate(cts)
+
+
+def run_net(ck, cfg, weights, image, nonce=0, keys=None):
+    """Full oracle pipeline for one image; returns (output ct at level 1,
+    output scale)."""
+    keys = keys if keys is not None else {}
+    tap_scale = 2.0 ** 40
+    L = ck.L
+    ntaps = cfg.k * cfg.k * cfg.in_c
+    d_out = (cfg.in_d - cfg.k) // cfg.s + 1
+    w_used = d_out * d_out
+    taps = conv_pack_taps(ck, cfg, image, nonce, tap_scale)
+    maps = conv_layer(ck, taps, ntaps, L, np.asarray(weights["conv_w"]).reshape(cfg.c_out, -1),
+                      weights["conv_b"], w_used, tap_scale)
+    l = L - 1
+    x = merge(ck, maps, cfg.c_out, l, w_used, keys)
+    scale = tap_scale
+    if "rlk" not in keys:
+        keys["rlk"] = ck.relin_key()
+    for W, b in weights["dense"]:
+        x = square(ck, x, l, keys["rlk"])
+        scale = scale * scale / float(ck.primes[l - 1])
+        l -= 1
+        x = hs_matvec(ck, x, l, np.asarray(W), True, keys)
+        l -= 1
+        x = ck.add_pc(x, ck.encode(np.asarray(b), scale, l), l)
+    return x, scale

@@ -1,0 +1,155 @@
+// engine.hpp -- device-side engine state shared by the CUDA translation
+// units and the C-ABI (csrc/capi.cu).
+//
+// Device layout: an NTT-domain limb is stored in SLOT ORDER
+// (position p < S holds a(psi^(5^p)), p >= S holds a(psi^(-5^(p-S)))), so
+// the Galois automorphism X -> X^(5^s) is a cyclic shift by s inside each
+// half -- every rotation becomes coalesced streaming instead of a gather.
+// Plaintexts, keys and HS masks are kept in Montgomery form.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "core.hpp"
+#include "modarith.cuh"
+
+namespace hegpu {
+
+#define HEGPU_MAX_BATCH_PERIOD 64
+
+// per-launch description of which key / shift row b uses (b % period)
+struct KeyRowMap {
+  int period;
+  int shift[HEGPU_MAX_BATCH_PERIOD];             // left shift s (0 = none)
+  const u64d* key[HEGPU_MAX_BATCH_PERIOD];       // device key (Montgomery)
+};
+
+struct DeviceKey {
+  u64d* data = nullptr;  // [L][2][L+1][N], slot order, Montgomery form
+  int shift = 0;         // left rotation amount (Galois 5^shift)
+  std::vector<u64> wire; // host wire copy (exported for tests)
+};
+
+struct Meter {
+  std::vector<std::pair<std::string, std::array<int64_t, 5>>> stages;
+  std::array<int64_t, 5> total{};
+  int cur = -1;
+  void begin(const std::string& label);
+  void bump(int field, int64_t n);
+};
+
+struct Context {
+  hegpu_params hp{};
+  std::unique_ptr<Params> P;
+  std::unique_ptr<Client> client;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  PrimeTable primes{};
+  u64d* d_tw = nullptr;          // [np][4][N]: w, w', iw, iw'
+  u64d* d_consts = nullptr;      // [np]: ninv, ninv' ; then [np][np]: qinv(value, shoup)
+  uint32_t* d_slot_src = nullptr;  // [N]
+  std::map<int, DeviceKey> rot_keys;  // keyed by left shift in [1, S)
+  DeviceKey relin;
+  bool has_relin = false;
+  Meter meter;
+  std::string last_error;
+  int64_t launches = 0;
+  size_t ws_bytes = 0;
+
+  int N() const { return P->n; }
+  int S() const { return P->slots; }
+  int L() const { return P->L; }
+  const u64d* ninv_tab() const { return d_consts; }
+  const u64d* qinv_tab() const { return d_consts + 2 * (size_t)P->np(); }
+  u64d* alloc(size_t words);
+  void free(u64d* p);
+  const DeviceKey& rot_key(int shift);
+};
+
+struct CtBatch {
+  Context* ctx;
+  int count, level;
+  double scale;
+  u64d* d;  // [count][2][level][N]
+  size_t words() const { return (size_t)count * 2 * level * ctx->N(); }
+  size_t stride() const { return (size_t)2 * level * ctx->N(); }
+};
+
+struct PtBatch {
+  Context* ctx;
+  int count, level, with_p;
+  double scale;
+  u64d* d;  // [count][level + with_p][N], Montgomery form
+  int limbs() const { return level + with_p; }
+  size_t words() const { return (size_t)count * limbs() * ctx->N(); }
+};
+
+// ---------------------------------------------------------------- launchers
+void check_cuda(cudaError_t e, const char* what);
+#define CK(x) ::hegpu::check_cuda((x), #x)
+
+// coefficient rows -> slot-order NTT rows; row r uses limb r % nl (limb l ->
+// prime l, or P for l == p_limb when p_limb >= 0)
+void launch_ntt_rows(Context& c, const u64d* src, u64d* dst, int rows, int nl, int p_limb);
+// slot-order NTT rows -> coefficient rows (x N^{-1}); 2-level row map
+void launch_intt_rows(Context& c, const u64d* src, u64d* dst, int n_outer, int n_inner,
+                      long src_outer, long src_inner, long dst_outer, long dst_inner,
+                      const int* prime_of_inner /* n_inner entries, host */);
+// wire (bit-reversed) <-> slot order permutation on count*limbs rows
+void launch_wire_to_slot(Context& c, const u64d* src, u64d* dst, size_t rows, int to_mont,
+                         int nl, int p_limb);
+void launch_slot_to_wire(Context& c, const u64d* src, u64d* dst, size_t rows, int from_mont,
+                         int nl, int p_limb);
+
+// key switching pieces (ks.cu)
+struct KsWork {
+  u64d* tmp;  // [B][l][N] coefficient digits
+  u64d* D;    // [B][l][l+1][N] ModUp digits, slot order
+  u64d* acc;  // [B][2][l+1][N] extended-basis accumulators
+  u64d* tmpP; // [B][2][N] dropped-limb coefficients
+};
+// d rows: poly at src + b*src_stride (l limbs); keys/shifts per b % period
+void ks_modup(Context& c, const u64d* src, long src_stride, int B, int l, const KeyRowMap* shifts,
+              u64d* tmp, u64d* D);
+void ks_inner(Context& c, const u64d* D, int B, int l, const KeyRowMap& keys, u64d* acc);
+// out[b][p][t] = (src[b][p][t] - lift(src[b][p][last])) * inv + add[b][p][t](shifted)
+struct DropArgs {
+  const u64d* src; long src_b, src_p; int src_limbs;  // last limb is dropped
+  u64d* dst; long dst_b, dst_p;
+  int pd;          // prime index of the dropped limb
+  int nl;          // output limbs (primes 0..nl-1)
+  const u64d* add; long add_b, add_p; int add_mask;  // add term per poly (bit p)
+  const KeyRowMap* shifts;  // shift for add reads of poly 0 (may be null)
+};
+void drop_last_limb(Context& c, int B, const DropArgs& a, u64d* tmpP);
+
+// pointwise (eval.cu)
+void launch_add(Context& c, const u64d* a, const u64d* b, u64d* out, int count, int l);
+void launch_add_plain(Context& c, const u64d* a, const u64d* p, long p_stride, u64d* out, int count, int l);
+void launch_mul_plain(Context& c, const u64d* a, const u64d* p, long p_stride, u64d* out, int count, int l);
+void launch_tensor_square(Context& c, const u64d* a, u64d* d01, u64d* d2, int count, int l);
+void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, const u64d* wmont /*[c_out][ntaps][l]*/,
+                     int c_out, const u64d* bias /*[c_out][l][N] mont*/, u64d* out);
+struct HsDiagTable {
+  int ndiag;
+  const u64d* masks;     // [ndiag][l+1][N] mont, slot order
+  const int* shifts;     // [ndiag] device: left shift (0 = no rotation)
+  const u64d* const* keys; // [ndiag] device key pointers (null for shift 0)
+};
+void launch_hs_diag(Context& c, const u64d* v, int B, int l, const u64d* D, const HsDiagTable& t,
+                    u64d* acc, u64d* cacc);
+
+// high-level evaluator (eval.cu)
+void eval_rescale(Context& c, const CtBatch& a, CtBatch& out);
+// out = rot(a) for B ciphertexts at level l (strided), per-row shift/key
+void eval_rotate(Context& c, const u64d* a, long a_stride, int B, int l, const KeyRowMap& km, u64d* out,
+                 long out_stride);
+void eval_square(Context& c, const CtBatch& a, CtBatch& out);  // tensor + relin, no rescale
+
+}  // namespace hegpu

@@ -1,0 +1,239 @@
+// layers.cu -- conv-pack, merge, square and Halevi-Shoup layers on the
+// CKKS engine (reference semantics: proj/src/convlower.cpp:39-74,141-160,
+// proj/src/matvec.cpp:45-105).
+#include <cmath>
+#include <string>
+
+#include "layers.hpp"
+
+namespace hegpu {
+
+namespace {
+
+void need(bool ok, int code, const std::string& msg) {
+  if (!ok) fail(code, msg);
+}
+
+// host wire limbs -> device slot order, Montgomery
+void upload_mont(Context& c, const std::vector<u64>& wire, u64d* dst, size_t rows, int nl, int p_limb) {
+  u64d* stage = c.alloc(wire.size());
+  CK(cudaMemcpyAsync(stage, wire.data(), wire.size() * 8, cudaMemcpyHostToDevice, c.stream));
+  launch_wire_to_slot(c, stage, dst, rows, 1, nl, p_limb);
+  c.free(stage);
+  CK(cudaStreamSynchronize(c.stream));
+}
+
+int ceil_log2(int64_t x) {
+  int b = 0;
+  while ((int64_t{1} << b) < x) ++b;
+  return b;
+}
+int64_t next_pow2(int64_t x) {
+  int64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+// proj/src/matvec.cpp:29-33
+bool plain_branch_fits(int64_t m, int64_t n, int64_t S) {
+  if (S < m + n - 1) return false;
+  const int b = ceil_log2((m + n - 1 + m - 1) / m);
+  return (m << b) <= S;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ conv ----
+ConvLayer::ConvLayer(Context& c, int nt, int co_n, const double* weights, const double* bias_vals, int w_used,
+                     int lvl, double tap_scale)
+    : ntaps(nt), c_out(co_n), level(lvl), ctx(&c) {
+  need(level >= 2, HEGPU_ERR_CAPACITY, "conv_packed_forward: no prime left to rescale");
+  const Params& P = *c.P;
+  const u64 qlast = P.q(level - 1);
+  std::vector<u64> w((size_t)c_out * ntaps * level);
+  for (int co = 0; co < c_out; ++co)
+    for (int t = 0; t < ntaps; ++t) {
+      const double x = std::rint(weights[(size_t)co * ntaps + t] * (double)qlast);
+      for (int li = 0; li < level; ++li) {
+        const u64 q = P.q(li);
+        w[((size_t)co * ntaps + t) * level + li] = mul_mod(residue_of_double(x, q), P.primes[li].r_mod, q);
+      }
+    }
+  CK(cudaMalloc((void**)&this->w, w.size() * 8));
+  CK(cudaMemcpy(this->w, w.data(), w.size() * 8, cudaMemcpyHostToDevice));
+  // bias[co] on the first w_used slots (convlower.cpp:68-71), at the product scale
+  const int N = P.n;
+  std::vector<u64> wire((size_t)c_out * level * N);
+  std::vector<double> z(w_used);
+  for (int co = 0; co < c_out; ++co) {
+    std::fill(z.begin(), z.end(), bias_vals ? bias_vals[co] : 0.0);
+    c.client->encode(z.data(), w_used, tap_scale * (double)qlast, level, false, wire.data() + (size_t)co * level * N);
+  }
+  CK(cudaMalloc((void**)&bias, wire.size() * 8));
+  upload_mont(c, wire, bias, (size_t)c_out * level, level, -1);
+}
+
+ConvLayer::~ConvLayer() {
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(w);
+  cudaFree(bias);
+}
+
+void ConvLayer::run(Context& c, const CtBatch& taps, CtBatch& maps) {
+  const int B = taps.count / ntaps, l = level, N = c.N();
+  CtBatch prod{&c, B * c_out, l, taps.scale * (double)c.P->q(l - 1), c.alloc((size_t)B * c_out * 2 * l * N)};
+  launch_conv_mac(c, taps.d, B, ntaps, l, w, c_out, bias, prod.d);
+  eval_rescale(c, prod, maps);
+  maps.scale = taps.scale;
+  c.free(prod.d);
+}
+
+// ----------------------------------------------------------------- merge ----
+void merge_maps(Context& c, const CtBatch& maps, int nmaps, int64_t w, CtBatch& out) {
+  const int B = out.count, l = maps.level, S = c.S();
+  const size_t st = maps.stride();
+  CK(cudaMemcpy2DAsync(out.d, st * 8, maps.d, (size_t)nmaps * st * 8, st * 8, B, cudaMemcpyDeviceToDevice,
+                       c.stream));
+  out.scale = maps.scale;
+  if (nmaps == 1) return;
+  CtBatch rot{&c, B, l, maps.scale, c.alloc((size_t)B * st)};
+  for (int j = 1; j < nmaps; ++j) {
+    const int shift = (int)((S - ((int64_t)j * w) % S) % S);
+    if (shift == 0) continue;
+    KeyRowMap km{};
+    km.period = 1;
+    km.shift[0] = shift;
+    km.key[0] = c.rot_key(shift).data;
+    eval_rotate(c, maps.d + (size_t)j * st, (long)((size_t)nmaps * st), B, l, km, rot.d, (long)st);
+    launch_add(c, out.d, rot.d, out.d, B, l);
+  }
+  c.free(rot.d);
+}
+
+// ---------------------------------------------------------------- square ----
+void square_layer(Context& c, const CtBatch& a, CtBatch& out) {
+  const int B = a.count, l = a.level;
+  CtBatch t{&c, B, l, a.scale * a.scale, c.alloc((size_t)B * 2 * l * c.N())};
+  eval_square(c, a, t);
+  eval_rescale(c, t, out);
+  out.scale = a.scale * a.scale / (double)c.P->q(l - 1);
+  c.free(t.d);
+}
+
+// -------------------------------------------------------------------- HS ----
+void HsPlan::build(Context& c, const double* A, int m_, int n_, int lvl, bool skip_zero) {
+  ctx = &c;
+  m = m_;
+  n = n_;
+  level = lvl;
+  const int S = c.S(), N = c.N();
+  // proj/src/matvec.cpp:35-41, 48-53
+  need(m >= 1 && n >= 1, HEGPU_ERR_SHAPE, "hs_matvec: empty matrix");
+  need(m <= S && n <= S, HEGPU_ERR_CAPACITY,
+       "matrix " + std::to_string(m) + "x" + std::to_string(n) + " exceeds " + std::to_string(S) + " slots");
+  const bool plain = plain_branch_fits(m, n, S);
+  m_eff = plain ? m : (int)next_pow2(m);
+  need(m_eff <= S, HEGPU_ERR_CAPACITY,
+       "padded row count " + std::to_string(m_eff) + " exceeds " + std::to_string(S) + " slots");
+  folds = plain ? ceil_log2((m + n - 1 + m - 1) / m) : ceil_log2(S / m_eff);
+  // generalized diagonals, pre-rotated: mask'_i = rot_right(mask_i, i)
+  std::vector<std::vector<double>> kept;
+  for (int i = 0; i < m_eff; ++i) {
+    std::vector<double> mk(S, 0.0);
+    bool nz = false;
+    for (int j = 0; j < n; ++j) {
+      const int row = (i + j) % m_eff;
+      if (row < m) {
+        const double v = A[(size_t)row * n + j];
+        mk[(j + i) % S] = v;
+        nz = nz || v != 0.0;
+      }
+    }
+    if (skip_zero && !nz) continue;
+    diag.push_back(HsDiag{i, i, (S - i) % S});
+    kept.push_back(std::move(mk));
+  }
+  const int nl = level + 1;
+  const double scale = (double)c.P->q(level - 1);
+  std::vector<u64> wire(kept.size() * nl * (size_t)N);
+#pragma omp parallel for schedule(dynamic)
+  for (long i = 0; i < (long)kept.size(); ++i)
+    c.client->encode(kept[i].data(), S, scale, level, true, wire.data() + (size_t)i * nl * N);
+  if (!kept.empty()) {
+    CK(cudaMalloc((void**)&masks, wire.size() * 8));
+    upload_mont(c, wire, masks, kept.size() * nl, nl, level);
+  }
+  std::vector<int> sh(diag.size());
+  for (size_t i = 0; i < diag.size(); ++i) sh[i] = diag[i].shift;
+  CK(cudaMalloc((void**)&d_shifts, (sh.size() + 1) * sizeof(int)));
+  if (!sh.empty()) CK(cudaMemcpy(d_shifts, sh.data(), sh.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMalloc((void**)&d_keys, (diag.size() + 1) * sizeof(u64d*)));
+}
+
+void HsPlan::release() {
+  if (ctx) cudaStreamSynchronize(ctx->stream);
+  cudaFree(masks);
+  cudaFree(d_shifts);
+  cudaFree(d_keys);
+  masks = nullptr;
+  d_shifts = nullptr;
+  d_keys = nullptr;
+}
+
+std::vector<int64_t> HsPlan::right_rotations() const {
+  std::vector<int64_t> r;
+  for (const HsDiag& d : diag)
+    if (d.right) r.push_back(d.right);
+  const int S = ctx->S();
+  for (int t = folds - 1; t >= 0; --t) r.push_back((S - (((int64_t)m_eff << t) % S)) % S);
+  return r;
+}
+
+void HsPlan::run(Context& c, const CtBatch& v, CtBatch& out) {
+  const int B = v.count, l = level, N = c.N(), S = c.S();
+  if (!keys_resolved) {
+    std::vector<const u64d*> kp(diag.size(), nullptr);
+    for (size_t i = 0; i < diag.size(); ++i)
+      if (diag[i].shift) kp[i] = c.rot_key(diag[i].shift).data;
+    if (!kp.empty()) CK(cudaMemcpy(d_keys, kp.data(), kp.size() * sizeof(u64d*), cudaMemcpyHostToDevice));
+    for (int t = folds - 1; t >= 0; --t) c.rot_key((int)(((int64_t)m_eff << t) % S));
+    keys_resolved = true;
+  }
+  u64d* tmp = c.alloc((size_t)B * l * N);
+  u64d* D = c.alloc((size_t)B * l * (l + 1) * N);
+  u64d* acc = c.alloc((size_t)B * 2 * (l + 1) * N);
+  u64d* cacc = c.alloc((size_t)B * 2 * l * N);
+  u64d* tmpP = c.alloc((size_t)B * 2 * N);
+  CtBatch u{&c, B, l, v.scale * (double)c.P->q(l - 1), c.alloc((size_t)B * 2 * l * N)};
+  // (1) one ModUp of v.c1 for all diagonals (hoisting)
+  ks_modup(c, v.d + (size_t)l * N, (long)v.stride(), B, l, nullptr, tmp, D);
+  // (2) diagonal accumulation in the extended basis
+  HsDiagTable tab{(int)diag.size(), masks, d_shifts, d_keys};
+  launch_hs_diag(c, v.d, B, l, D, tab, acc, cacc);
+  // (3) one ModDown of the sum (+ the Q-basis c-part)
+  DropArgs d{};
+  d.src = acc; d.src_b = 2L * (l + 1) * N; d.src_p = (long)(l + 1) * N; d.src_limbs = l + 1;
+  d.dst = u.d; d.dst_b = (long)u.stride(); d.dst_p = (long)l * N;
+  d.pd = c.L(); d.nl = l;
+  d.add = cacc; d.add_b = 2L * l * N; d.add_p = (long)l * N; d.add_mask = 3; d.shifts = nullptr;
+  drop_last_limb(c, B, d, tmpP);
+  // (4) rescale by q_{l-1}: the masks were encoded at exactly that scale
+  eval_rescale(c, u, out);
+  out.scale = v.scale;
+  // (5) log-depth fold, matvec.cpp:101-103: s += rot_left(s, m_eff * 2^t)
+  if (folds > 0) {
+    CtBatch r{&c, B, l - 1, out.scale, c.alloc((size_t)B * 2 * (l - 1) * N)};
+    for (int t = folds - 1; t >= 0; --t) {
+      const int shift = (int)(((int64_t)m_eff << t) % S);
+      KeyRowMap km{};
+      km.period = 1;
+      km.shift[0] = shift;
+      km.key[0] = c.rot_key(shift).data;
+      eval_rotate(c, out.d, (long)out.stride(), B, l - 1, km, r.d, (long)r.stride());
+      launch_add(c, out.d, r.d, out.d, B, l - 1);
+    }
+    c.free(r.d);
+  }
+  c.free(tmp); c.free(D); c.free(acc); c.free(cacc); c.free(tmpP); c.free(u.d);
+}
+
+}  // namespace hegpu

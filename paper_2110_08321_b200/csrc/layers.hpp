@@ -1,0 +1,52 @@
+// layers.hpp -- the reference's layer kernels on the CKKS engine:
+//   ConvLayer   conv_packed_forward  proj/src/convlower.cpp:39-74
+//   merge_maps  merge_maps           proj/src/convlower.cpp:145-160
+//   square_layer square_layer        proj/src/convlower.cpp:141-143
+//   HsPlan      extract_diagonals + hs_matvec  proj/src/matvec.cpp:45-105
+#pragma once
+
+#include "engine.hpp"
+
+namespace hegpu {
+
+// conv-pack MAC with scalar weights round(w * q_{l-1}) (the tap ciphertexts
+// are zero beyond the used slots, so the reference's masked constant
+// plaintext and the scalar agree up to encryption noise),
+// the per-map bias plaintext on the first w_used slots, then one rescale.
+struct ConvLayer {
+  int ntaps, c_out, level;
+  u64d* w = nullptr;     // [c_out][ntaps][level] Montgomery scalars
+  u64d* bias = nullptr;  // [c_out][level][N] Montgomery, slot order
+  ConvLayer(Context& c, int ntaps, int c_out, const double* weights, const double* bias_vals, int w_used,
+            int level, double tap_scale);
+  ~ConvLayer();
+  ConvLayer(const ConvLayer&) = delete;
+  ConvLayer& operator=(const ConvLayer&) = delete;
+  void run(Context& c, const CtBatch& taps, CtBatch& maps);
+  Context* ctx;
+};
+
+void merge_maps(Context& c, const CtBatch& maps, int nmaps, int64_t w, CtBatch& out);
+void square_layer(Context& c, const CtBatch& a, CtBatch& out);  // tensor + relin + rescale
+
+struct HsDiag {
+  int index;      // diagonal i of extract_diagonals
+  int64_t right;  // right rotation (= i)
+  int shift;      // device left shift (S - i) mod S
+};
+
+struct HsPlan {
+  int m = 0, n = 0, m_eff = 0, folds = 0, level = 0;
+  std::vector<HsDiag> diag;   // kept (non-zero) diagonals in order
+  u64d* masks = nullptr;      // [kept][level+1][N] Montgomery, slot order
+  int* d_shifts = nullptr;    // [kept]
+  const u64d** d_keys = nullptr;  // [kept] resolved on first run
+  bool keys_resolved = false;
+  void build(Context& c, const double* A, int m, int n, int level, bool skip_zero);
+  void release();
+  std::vector<int64_t> right_rotations() const;  // diagonals, then folds
+  void run(Context& c, const CtBatch& v, CtBatch& out);
+  Context* ctx = nullptr;
+};
+
+}  // namespace hegpu

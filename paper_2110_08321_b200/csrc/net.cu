@@ -1,0 +1,259 @@
+// net.cu -- the stage driver: the reference's `execute` stage loop
+// (proj/src/netcompile.cpp:291-446) for the hot-path model family
+//   ConvPack "Conv1" -> Merge "Flat1" -> { Square "Square<i>", Linear(HS)
+//   "Dense<i>" }*,
+// i.e. the stage list lower() produces for Conv -> Square -> Dense -> ...
+// (netcompile.cpp:106-213), run on a batch of B images in one pass.
+//
+// Level schedule: taps at level L; conv + rescale -> L-1;
+// merge at L-1; every Square and every Dense consumes one prime.
+// masked_prefix (netcompile.cpp:424) is elided: the next HS masks are zero
+// beyond n (matvec.cpp:57-61) and logits are read from slots 0..m-1.
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "handles.hpp"
+#include "layers.hpp"
+
+using namespace hegpu;
+
+
+struct hegpu_net {
+  Context* c = nullptr;
+  hegpu_net_spec spec{};
+  int d_out = 0, w_used = 0, ntaps = 0, top = 0;
+  double tap_scale = 0, out_scale = 0;
+  std::unique_ptr<ConvLayer> conv;
+  std::vector<HsPlan> plans;
+  std::vector<u64d*> bias;   // per dense layer, [level][N] Montgomery
+  std::vector<double> bias_scale;
+  ~hegpu_net() {
+    for (auto& p : plans) p.release();
+    for (u64d* b : bias) cudaFree(b);
+  }
+};
+
+namespace {
+
+void need(bool ok, int code, const std::string& msg) {
+  if (!ok) fail(code, msg);
+}
+
+template <typename F>
+int guarded(Context* c, F&& f) {
+  try {
+    f();
+    return HEGPU_OK;
+  } catch (const Error& e) {
+    if (c) c->last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (c) c->last_error = e.what();
+    return HEGPU_ERR_ARG;
+  }
+}
+
+struct Scratch {
+  Context& c;
+  u64d* p;
+  Scratch(Context& cc, size_t words) : c(cc), p(cc.alloc(words)) {}
+  ~Scratch() { c.free(p); }
+};
+
+void run_net(hegpu_net& net, const CtBatch& taps, CtBatch& out) {
+  Context& c = *net.c;
+  const hegpu_net_spec& s = net.spec;
+  const int B = taps.count / net.ntaps, N = c.N();
+  int l = net.top;
+  // Conv1: ConvPack (netcompile.cpp:321-331)
+  c.meter.begin("Conv1");
+  Scratch maps(c, (size_t)B * s.c_out * 2 * (l - 1) * N);
+  CtBatch mb{&c, B * s.c_out, l - 1, 0, maps.p};
+  net.conv->run(c, taps, mb);
+  c.meter.bump(HEGPU_MUL_PC, (int64_t)B * net.ntaps * s.c_out);
+  c.meter.bump(HEGPU_ADD_CC, (int64_t)B * (net.ntaps - 1) * s.c_out);
+  c.meter.bump(HEGPU_ADD_PC, (int64_t)B * s.c_out);
+  --l;
+  // Flat1: Merge (netcompile.cpp:332-347)
+  c.meter.begin("Flat1");
+  Scratch cur(c, (size_t)B * 2 * l * N);
+  CtBatch x{&c, B, l, 0, cur.p};
+  merge_maps(c, mb, s.c_out, net.w_used, x);
+  c.meter.bump(HEGPU_ROT, (int64_t)B * (s.c_out - 1));
+  c.meter.bump(HEGPU_ADD_CC, (int64_t)B * (s.c_out - 1));
+  Scratch nxt(c, (size_t)B * 2 * l * N);
+  for (int i = 0; i < s.n_dense; ++i) {
+    // Square<i> (netcompile.cpp:348-351)
+    c.meter.begin("Square" + std::to_string(i + 1));
+    CtBatch y{&c, B, l - 1, 0, nxt.p};
+    square_layer(c, x, y);
+    c.meter.bump(HEGPU_MUL_CC, B);
+    --l;
+    // Dense<i>: Linear / HS (netcompile.cpp:380-434)
+    c.meter.begin("Dense" + std::to_string(i + 1));
+    HsPlan& pl = net.plans[i];
+    const bool last = i + 1 == s.n_dense;
+    CtBatch z{&c, B, l - 1, 0, last ? out.d : cur.p};
+    pl.run(c, y, z);
+    const int64_t kept = (int64_t)pl.diag.size();
+    int64_t rots = 0;
+    for (const auto& d : pl.diag) rots += d.right != 0;
+    c.meter.bump(HEGPU_MUL_PC, B * kept);
+    c.meter.bump(HEGPU_ROT, B * (rots + pl.folds));
+    c.meter.bump(HEGPU_ADD_CC, B * ((kept > 0 ? kept - 1 : 0) + pl.folds));
+    // bias add(out, pack(b)) (netcompile.cpp:423)
+    launch_add_plain(c, z.d, net.bias[i], 0, z.d, B, l - 1);
+    c.meter.bump(HEGPU_ADD_PC, B);
+    --l;
+    x = z;
+    if (last) out.scale = z.scale;
+  }
+}
+
+}  // namespace
+
+extern "C" int hegpu_net_create(hegpu_ctx* h, const hegpu_net_spec* spec, const double* conv_w,
+                                const double* conv_b, const double* const* dense_w, const double* const* dense_b,
+                                hegpu_net** out) {
+  if (!h || !spec || !conv_w || !out || (spec->n_dense > 0 && (!dense_w || !dense_b))) return HEGPU_ERR_ARG;
+  Context& c = h->c;
+  return guarded(&c, [&] {
+    const hegpu_net_spec& s = *spec;
+    need(c.device >= 0 && c.stream, HEGPU_ERR_CUDA, "client-only context: the evaluator needs a CUDA device");
+    need(s.n_dense >= 1 && s.n_dense <= 4, HEGPU_ERR_SHAPE, "net: 1..4 dense layers supported");
+    need(s.k >= 1 && s.stride >= 1 && s.k <= s.in_d, HEGPU_ERR_SHAPE, "net: window larger than input");
+    auto net = std::make_unique<hegpu_net>();
+    net->c = &c;
+    net->spec = s;
+    net->d_out = (s.in_d - s.k) / s.stride + 1;
+    net->w_used = net->d_out * net->d_out;
+    net->ntaps = s.k * s.k * s.in_c;
+    net->top = c.L();
+    const int S = c.S();
+    // lower() capacity checks (netcompile.cpp:125-128, 147-152, 203-207)
+    need(net->w_used <= S, HEGPU_ERR_CAPACITY,
+         "Conv1: d_out^2 = " + std::to_string(net->w_used) + " > n_slots = " + std::to_string(S));
+    need((int64_t)s.c_out * net->w_used <= S, HEGPU_ERR_CAPACITY,
+         "Flat1: group footprint " + std::to_string(s.c_out * net->w_used) + " > n_slots = " + std::to_string(S));
+    need(c.L() >= 2 + 2 * s.n_dense, HEGPU_ERR_CAPACITY, "net: Q chain too short for the level schedule");
+    net->tap_scale = std::ldexp(1.0, 40);
+    net->conv = std::make_unique<ConvLayer>(c, net->ntaps, s.c_out, conv_w, conv_b, net->w_used, net->top,
+                                            net->tap_scale);
+    std::vector<int64_t> rots;
+    for (int j = 1; j < s.c_out; ++j) rots.push_back((int64_t)j * net->w_used);
+    double scale = net->tap_scale;  // after conv + rescale
+    int l = net->top - 1;
+    int n = s.c_out * net->w_used;
+    net->plans.resize(s.n_dense);
+    for (int i = 0; i < s.n_dense; ++i) {
+      scale = scale * scale / (double)c.P->q(l - 1);  // square + rescale
+      --l;
+      const int m = s.dense_out[i];
+      try {
+        net->plans[i].build(c, dense_w[i], m, n, l, true);
+      } catch (const Error& e) {
+        fail(e.code, "Dense" + std::to_string(i + 1) + ": " + e.what());
+      }
+      for (int64_t r : net->plans[i].right_rotations()) rots.push_back(r);
+      --l;  // HS rescale; bias at the same scale
+      std::vector<double> bz(dense_b[i], dense_b[i] + m);
+      std::vector<u64> wire((size_t)l * c.N());
+      c.client->encode(bz.data(), m, scale, l, false, wire.data());
+      u64d* d = nullptr;
+      CK(cudaMalloc((void**)&d, wire.size() * 8));
+      u64d* stage = c.alloc(wire.size());
+      CK(cudaMemcpyAsync(stage, wire.data(), wire.size() * 8, cudaMemcpyHostToDevice, c.stream));
+      launch_wire_to_slot(c, stage, d, (size_t)l, 1, l, -1);
+      c.free(stage);
+      net->bias.push_back(d);
+      net->bias_scale.push_back(scale);
+      n = m;
+    }
+    net->out_scale = scale;
+    CK(cudaStreamSynchronize(c.stream));
+    if (int rc = hegpu_gen_rotation_keys(h, rots.data(), (int)rots.size())) fail(rc, c.last_error);
+    if (int rc = hegpu_gen_relin_key(h)) fail(rc, c.last_error);
+    *out = net.release();
+  });
+}
+
+extern "C" void hegpu_net_destroy(hegpu_net* net) {
+  if (!net) return;
+  cudaStreamSynchronize(net->c->stream);
+  delete net;
+}
+
+extern "C" int hegpu_net_run(hegpu_net* net, const hegpu_ct* taps, hegpu_ct* out) {
+  if (!net || !taps || !out) return HEGPU_ERR_ARG;
+  Context& c = *net->c;
+  return guarded(&c, [&] {
+    need(taps->b.level == net->top && taps->b.count % net->ntaps == 0, HEGPU_ERR_SHAPE,
+         "net_run: taps must be B*ntaps ciphertexts at the top level");
+    const int B = taps->b.count / net->ntaps;
+    need(out->b.count == B && out->b.level == net->top - 1 - 2 * net->spec.n_dense, HEGPU_ERR_SHAPE,
+         "net_run: bad output handle");
+    CtBatch o = out->b;
+    run_net(*net, taps->b, o);
+    out->b.scale = o.scale;
+  });
+}
+
+extern "C" int hegpu_net_run_host(hegpu_net* net, const uint64_t* host_taps, int batch, uint64_t* host_out) {
+  if (!net || !host_taps || !host_out || batch < 1) return HEGPU_ERR_ARG;
+  Context& c = *net->c;
+  return guarded(&c, [&] {
+    const int N = c.N(), L = net->top, lo = net->top - 1 - 2 * net->spec.n_dense;
+    const size_t in_words = (size_t)batch * net->ntaps * 2 * L * N;
+    const size_t out_words = (size_t)batch * 2 * lo * N;
+    Scratch stage(c, in_words);
+    Scratch taps(c, in_words);
+    CK(cudaMemcpyAsync(stage.p, host_taps, in_words * 8, cudaMemcpyHostToDevice, c.stream));
+    launch_wire_to_slot(c, stage.p, taps.p, (size_t)batch * net->ntaps * 2 * L, 0, L, -1);
+    CtBatch tb{&c, batch * net->ntaps, L, net->tap_scale, taps.p};
+    Scratch o(c, out_words);
+    CtBatch ob{&c, batch, lo, 0, o.p};
+    run_net(*net, tb, ob);
+    launch_slot_to_wire(c, o.p, stage.p, (size_t)batch * 2 * lo, 0, lo, -1);
+    CK(cudaMemcpyAsync(host_out, stage.p, out_words * 8, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+extern "C" int hegpu_net_encrypt_image(hegpu_net* net, const double* image, uint64_t nonce, uint64_t* taps_out) {
+  if (!net || !image || !taps_out) return HEGPU_ERR_ARG;
+  Context& c = *net->c;
+  return guarded(&c, [&] {
+    const hegpu_net_spec& s = net->spec;
+    const int N = c.N(), L = net->top, d = net->d_out;
+    std::vector<double> z(net->w_used);
+    std::vector<u64> pt((size_t)L * N);
+    // conv_pack (convlower.cpp:9-37): tap t = (ci*k+ky)*k+kx, slot oy*d_out+ox
+    for (int ci = 0; ci < s.in_c; ++ci)
+      for (int ky = 0; ky < s.k; ++ky)
+        for (int kx = 0; kx < s.k; ++kx) {
+          const int t = (ci * s.k + ky) * s.k + kx;
+          for (int oy = 0; oy < d; ++oy)
+            for (int ox = 0; ox < d; ++ox)
+              z[oy * d + ox] = image[((size_t)ci * s.in_d + oy * s.stride + ky) * s.in_d + ox * s.stride + kx];
+          c.client->encode(z.data(), net->w_used, net->tap_scale, L, false, pt.data());
+          c.client->encrypt(pt.data(), L, nonce * (uint64_t)net->ntaps + (uint64_t)t,
+                            taps_out + (size_t)t * 2 * L * N);
+        }
+  });
+}
+
+extern "C" int hegpu_net_decrypt_logits(hegpu_net* net, const uint64_t* out_ct, double* logits) {
+  if (!net || !out_ct || !logits) return HEGPU_ERR_ARG;
+  Context& c = *net->c;
+  return guarded(&c, [&] {
+    const int N = c.N(), lo = net->top - 1 - 2 * net->spec.n_dense;
+    std::vector<u64> pt((size_t)lo * N);
+    std::vector<double> slots(c.S());
+    c.client->decrypt(out_ct, lo, pt.data());
+    c.client->decode(pt.data(), lo, net->out_scale, slots.data());
+    std::memcpy(logits, slots.data(), sizeof(double) * net->spec.dense_out[net->spec.n_dense - 1]);
+  });
+}
+
+extern "C" double hegpu_net_output_scale(const hegpu_net* net) { return net ? net->out_scale : 0.0; }

@@ -1,0 +1,450 @@
+"""ctypes front end of libhegpu.so (include/hegpu.h) for tests and bench.py.
+
+This is plumbing over the C-ABI, not a second implementation: every call
+goes to the native library, and importing fails loudly if it is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhegpu.so")
+
+OK, ERR_CAPACITY, ERR_SHAPE, ERR_LAYOUT, ERR_RANGE, ERR_IO, ERR_CUDA, ERR_NCCL, ERR_ARG, ERR_KEY = range(10)
+CLIENT_ONLY = -1
+MAX_Q = 15
+TALLY_FIELDS = ("add_pc", "add_cc", "mul_pc", "mul_cc", "rot")
+
+
+class HegpuError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[hegpu {code}] {msg}")
+        self.code = code
+
+
+class CapacityError(HegpuError):
+    """hesim::CapacityError (proj/include/hesim/errors.hpp:9-12)"""
+
+
+class ShapeError(HegpuError):
+    """hesim::ShapeError"""
+
+
+class LayoutError(HegpuError):
+    """hesim::LayoutError"""
+
+
+class RangeError(HegpuError, IndexError):
+    """std::out_of_range (proj/src/slotvec.cpp:45-48)"""
+
+
+_ERR = {ERR_CAPACITY: CapacityError, ERR_SHAPE: ShapeError, ERR_LAYOUT: LayoutError, ERR_RANGE: RangeError}
+
+
+class Params(C.Structure):
+    _fields_ = [("log_n", C.c_int), ("n_q", C.c_int), ("q_bits", C.c_int * MAX_Q),
+                ("p_bits", C.c_int), ("seed", C.c_uint64)]
+
+
+class NetSpec(C.Structure):
+    _fields_ = [("in_c", C.c_int), ("in_d", C.c_int), ("k", C.c_int), ("stride", C.c_int),
+                ("c_out", C.c_int), ("n_dense", C.c_int), ("dense_out", C.c_int * 4)]
+
+
+_lib = None
+u64p = np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")
+f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2110_08321_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i, u, d, sz = C.c_void_p, C.c_int, C.c_uint64, C.c_double, C.c_size_t
+        pp = C.POINTER(C.c_void_p)
+        sig = {
+            "hegpu_ctx_create": (i, [C.POINTER(Params), i, pp]),
+            "hegpu_ctx_destroy": (None, [vp]),
+            "hegpu_last_error": (C.c_char_p, [vp]),
+            "hegpu_ctx_info": (i, [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i), u64p]),
+            "hegpu_sync": (i, [vp]),
+            "hegpu_kernel_launches": (C.c_int64, [vp]),
+            "hegpu_begin_stage": (i, [vp, C.c_char_p]),
+            "hegpu_num_stages": (i, [vp]),
+            "hegpu_stage_tally": (i, [vp, i, C.c_char_p, i, i64p]),
+            "hegpu_total_tally": (i, [vp, i64p]),
+            "hegpu_reset_meter": (i, [vp]),
+            "hegpu_encode": (i, [vp, f64p, i, d, i, i, u64p]),
+            "hegpu_decode": (i, [vp, u64p, i, d, f64p]),
+            "hegpu_encrypt": (i, [vp, u64p, i, u, u64p]),
+            "hegpu_decrypt": (i, [vp, u64p, i, u64p]),
+            "hegpu_gen_rotation_keys": (i, [vp, i64p, i]),
+            "hegpu_gen_relin_key": (i, [vp]),
+            "hegpu_export_rotation_key": (i, [vp, C.c_int64, u64p]),
+            "hegpu_export_relin_key": (i, [vp, u64p]),
+            "hegpu_ct_create": (i, [vp, i, i, pp]),
+            "hegpu_ct_destroy": (None, [vp]),
+            "hegpu_ct_upload": (i, [vp, vp, sz, d]),
+            "hegpu_ct_download": (i, [vp, vp, sz]),
+            "hegpu_ct_info": (i, [vp, C.POINTER(i), C.POINTER(i), C.POINTER(d)]),
+            "hegpu_pt_create": (i, [vp, i, i, i, pp]),
+            "hegpu_pt_destroy": (None, [vp]),
+            "hegpu_pt_upload": (i, [vp, vp, sz, d]),
+            "hegpu_pt_download": (i, [vp, vp, sz]),
+            "hegpu_add": (i, [vp, vp, vp, vp]),
+            "hegpu_add_plain": (i, [vp, vp, vp, vp]),
+            "hegpu_mul_plain": (i, [vp, vp, vp, vp]),
+            "hegpu_rescale": (i, [vp, vp, vp]),
+            "hegpu_rotate_right": (i, [vp, vp, C.c_int64, vp]),
+            "hegpu_rotate_left": (i, [vp, vp, C.c_int64, vp]),
+            "hegpu_square": (i, [vp, vp, vp]),
+            "hegpu_conv_packed_forward": (i, [vp, vp, i, f64p, i, vp, i, vp]),
+            "hegpu_merge_maps": (i, [vp, vp, i, C.c_int64, vp]),
+            "hegpu_hs_plan_create": (i, [vp, f64p, i, i, i, i, pp]),
+            "hegpu_hs_plan_destroy": (None, [vp]),
+            "hegpu_hs_plan_rotations": (i, [vp, vp, i]),
+            "hegpu_hs_plan_info": (i, [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i)]),
+            "hegpu_hs_matvec": (i, [vp, vp, vp, vp]),
+            "hegpu_net_create": (i, [vp, C.POINTER(NetSpec), f64p, f64p, vp, vp, pp]),
+            "hegpu_net_destroy": (None, [vp]),
+            "hegpu_net_run": (i, [vp, vp, vp]),
+            "hegpu_net_run_host": (i, [vp, vp, i, vp]),
+            "hegpu_net_encrypt_image": (i, [vp, f64p, u, u64p]),
+            "hegpu_net_decrypt_logits": (i, [vp, u64p, f64p]),
+            "hegpu_net_output_scale": (d, [vp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def declared_symbols():
+    """Every function include/hegpu.h declares (for the export test)."""
+    import re
+    root = os.path.dirname(_HERE)
+    text = open(os.path.join(root, "include", "hegpu.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\s*\*|int64_t|double)\s+\*?(hegpu_\w+)\(",
+                                 text, re.M)))
+
+
+class Context:
+    def __init__(self, log_n, qbits, pbits, seed=1, device=0):
+        p = Params()
+        p.log_n = log_n
+        p.n_q = len(qbits)
+        for k, b in enumerate(qbits):
+            p.q_bits[k] = b
+        p.p_bits = pbits
+        p.seed = seed
+        h = C.c_void_p()
+        rc = lib().hegpu_ctx_create(C.byref(p), device, C.byref(h))
+        if rc:
+            raise _ERR.get(rc, HegpuError)(rc, lib().hegpu_last_error(None).decode())
+        self.h = h
+        self.L = len(qbits)
+        self.np = self.L + 1
+        n, s, nq = C.c_int(), C.c_int(), C.c_int()
+        primes = np.zeros(self.np, dtype=np.uint64)
+        lib().hegpu_ctx_info(h, C.byref(n), C.byref(s), C.byref(nq), primes)
+        self.N, self.S = n.value, s.value
+        self.primes = [int(x) for x in primes]
+        self.key_words = self.L * 2 * self.np * self.N
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().hegpu_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc):
+        if rc:
+            raise _ERR.get(rc, HegpuError)(rc, lib().hegpu_last_error(self.h).decode())
+
+    # -- client -----------------------------------------------------------
+    def encode(self, z, scale, level, with_p=False):
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        out = np.empty((level + int(with_p)) * self.N, dtype=np.uint64)
+        self.check(lib().hegpu_encode(self.h, z, len(z), scale, level, int(with_p), out))
+        return out
+
+    def decode(self, pt, level, scale):
+        out = np.empty(self.S, dtype=np.float64)
+        self.check(lib().hegpu_decode(self.h, np.ascontiguousarray(pt, dtype=np.uint64), level, scale, out))
+        return out
+
+    def encrypt(self, pt, level, nonce):
+        ct = np.empty(2 * level * self.N, dtype=np.uint64)
+        self.check(lib().hegpu_encrypt(self.h, np.ascontiguousarray(pt, dtype=np.uint64), level, nonce, ct))
+        return ct
+
+    def decrypt(self, ct, level):
+        pt = np.empty(level * self.N, dtype=np.uint64)
+        self.check(lib().hegpu_decrypt(self.h, np.ascontiguousarray(ct, dtype=np.uint64), level, pt))
+        return pt
+
+    def export_rotation_key(self, r):
+        out = np.empty(self.key_words, dtype=np.uint64)
+        self.check(lib().hegpu_export_rotation_key(self.h, r, out))
+        return out
+
+    def export_relin_key(self):
+        out = np.empty(self.key_words, dtype=np.uint64)
+        self.check(lib().hegpu_export_relin_key(self.h, out))
+        return out
+
+    def gen_rotation_keys(self, rights):
+        r = np.ascontiguousarray(rights, dtype=np.int64)
+        self.check(lib().hegpu_gen_rotation_keys(self.h, r, len(r)))
+
+    def gen_relin_key(self):
+        self.check(lib().hegpu_gen_relin_key(self.h))
+
+    # -- device objects -------------------------------------------------------
+    def ct(self, count, level, data=None, scale=1.0):
+        return Ciphertext(self, count, level, data, scale)
+
+    def pt(self, count, level, with_p=False, data=None, scale=1.0):
+        return Plaintext(self, count, level, with_p, data, scale)
+
+    # -- metering -------------------------------------------------------------
+    def begin_stage(self, label):
+        self.check(lib().hegpu_begin_stage(self.h, label.encode()))
+
+    def stages(self):
+        out = []
+        buf = C.create_string_buffer(128)
+        for i in range(lib().hegpu_num_stages(self.h)):
+            t = np.zeros(5, dtype=np.int64)
+            self.check(lib().hegpu_stage_tally(self.h, i, buf, 128, t))
+            out.append((buf.value.decode(), tuple(int(x) for x in t)))
+        return out
+
+    def total(self):
+        t = np.zeros(5, dtype=np.int64)
+        self.check(lib().hegpu_total_tally(self.h, t))
+        return tuple(int(x) for x in t)
+
+    def reset_meter(self):
+        self.check(lib().hegpu_reset_meter(self.h))
+
+    def launches(self):
+        return int(lib().hegpu_kernel_launches(self.h))
+
+    def sync(self):
+        self.check(lib().hegpu_sync(self.h))
+
+    # -- evaluator ------------------------------------------------------------
+    def add(self, a, b, out):
+        self.check(lib().hegpu_add(self.h, a.h, b.h, out.h))
+        return out
+
+    def add_plain(self, a, p, out):
+        self.check(lib().hegpu_add_plain(self.h, a.h, p.h, out.h))
+        return out
+
+    def mul_plain(self, a, p, out):
+        self.check(lib().hegpu_mul_plain(self.h, a.h, p.h, out.h))
+        return out
+
+    def rescale(self, a, out):
+        self.check(lib().hegpu_rescale(self.h, a.h, out.h))
+        return out
+
+    def rotate_right(self, a, r, out):
+        self.check(lib().hegpu_rotate_right(self.h, a.h, r, out.h))
+        return out
+
+    def rotate_left(self, a, r, out):
+        self.check(lib().hegpu_rotate_left(self.h, a.h, r, out.h))
+        return out
+
+    def square(self, a, out):
+        self.check(lib().hegpu_square(self.h, a.h, out.h))
+        return out
+
+    def conv_packed_forward(self, taps, ntaps, weights, bias, w_used, out):
+        w = np.ascontiguousarray(weights, dtype=np.float64).ravel()
+        c_out = len(w) // ntaps
+        b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float64)
+        self.check(lib().hegpu_conv_packed_forward(self.h, taps.h, ntaps, w, c_out,
+                                                   None if b is None else b.ctypes.data, w_used, out.h))
+        return out
+
+    def merge_maps(self, maps, c, w, out):
+        self.check(lib().hegpu_merge_maps(self.h, maps.h, c, w, out.h))
+        return out
+
+    def hs_plan(self, A, level, skip_zero=True):
+        return HsPlan(self, A, level, skip_zero)
+
+    def hs_matvec(self, plan, v, out):
+        self.check(lib().hegpu_hs_matvec(self.h, plan.h, v.h, out.h))
+        return out
+
+
+class Ciphertext:
+    def __init__(self, ctx, count, level, data=None, scale=1.0):
+        self.ctx, self.count, self.level = ctx, count, level
+        h = C.c_void_p()
+        ctx.check(lib().hegpu_ct_create(ctx.h, count, level, C.byref(h)))
+        self.h = h
+        if data is not None:
+            self.upload(data, scale)
+
+    @property
+    def words(self):
+        return self.count * 2 * self.level * self.ctx.N
+
+    def upload(self, data, scale=1.0):
+        data = np.ascontiguousarray(data, dtype=np.uint64)
+        self.ctx.check(lib().hegpu_ct_upload(self.h, data.ctypes.data, data.size, scale))
+
+    def download(self):
+        out = np.empty(self.words, dtype=np.uint64)
+        self.ctx.check(lib().hegpu_ct_download(self.h, out.ctypes.data, out.size))
+        return out
+
+    @property
+    def scale(self):
+        s = C.c_double()
+        lib().hegpu_ct_info(self.h, None, None, C.byref(s))
+        return s.value
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().hegpu_ct_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+class Plaintext:
+    def __init__(self, ctx, count, level, with_p=False, data=None, scale=1.0):
+        self.ctx, self.count, self.level, self.with_p = ctx, count, level, with_p
+        h = C.c_void_p()
+        ctx.check(lib().hegpu_pt_create(ctx.h, count, level, int(with_p), C.byref(h)))
+        self.h = h
+        if data is not None:
+            self.upload(data, scale)
+
+    @property
+    def words(self):
+        return self.count * (self.level + int(self.with_p)) * self.ctx.N
+
+    def upload(self, data, scale=1.0):
+        data = np.ascontiguousarray(data, dtype=np.uint64)
+        self.ctx.check(lib().hegpu_pt_upload(self.h, data.ctypes.data, data.size, scale))
+
+    def download(self):
+        out = np.empty(self.words, dtype=np.uint64)
+        self.ctx.check(lib().hegpu_pt_download(self.h, out.ctypes.data, out.size))
+        return out
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().hegpu_pt_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+class HsPlan:
+    def __init__(self, ctx, A, level, skip_zero=True):
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        self.ctx, self.m, self.n = ctx, A.shape[0], A.shape[1]
+        h = C.c_void_p()
+        ctx.check(lib().hegpu_hs_plan_create(ctx.h, A.ravel(), self.m, self.n, level, int(skip_zero),
+                                             C.byref(h)))
+        self.h = h
+        me, fo, ke = C.c_int(), C.c_int(), C.c_int()
+        lib().hegpu_hs_plan_info(h, C.byref(me), C.byref(fo), C.byref(ke))
+        self.m_eff, self.folds, self.kept = me.value, fo.value, ke.value
+
+    def rotations(self):
+        n = lib().hegpu_hs_plan_rotations(self.h, None, 0)
+        r = np.zeros(max(n, 1), dtype=np.int64)
+        lib().hegpu_hs_plan_rotations(self.h, r.ctypes.data, n)
+        return [int(x) for x in r[:n]]
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().hegpu_hs_plan_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+class Net:
+    """Stage driver (execute, proj/src/netcompile.cpp:291-446) for the
+    Conv -> (Square -> Dense)* family on a batch of images."""
+
+    def __init__(self, ctx, cfg, weights):
+        self.ctx, self.cfg = ctx, cfg
+        spec = NetSpec()
+        spec.in_c, spec.in_d, spec.k, spec.stride, spec.c_out = cfg.in_c, cfg.in_d, cfg.k, cfg.s, cfg.c_out
+        spec.n_dense = len(cfg.dense)
+        for k, m in enumerate(cfg.dense):
+            spec.dense_out[k] = m
+        self._keep = [np.ascontiguousarray(W, dtype=np.float64) for W, _ in weights["dense"]]
+        self._keepb = [np.ascontiguousarray(b, dtype=np.float64) for _, b in weights["dense"]]
+        wp = (C.c_void_p * 4)(*[a.ctypes.data for a in self._keep])
+        bp = (C.c_void_p * 4)(*[a.ctypes.data for a in self._keepb])
+        cw = np.ascontiguousarray(weights["conv_w"], dtype=np.float64).ravel()
+        cb = np.ascontiguousarray(weights["conv_b"], dtype=np.float64)
+        h = C.c_void_p()
+        ctx.check(lib().hegpu_net_create(ctx.h, C.byref(spec), cw, cb, C.cast(wp, C.c_void_p),
+                                         C.cast(bp, C.c_void_p), C.byref(h)))
+        self.h = h
+        self.ntaps = cfg.k * cfg.k * cfg.in_c
+        self.top = ctx.L
+        self.out_level = ctx.L - 1 - 2 * len(cfg.dense)
+        self.tap_words = 2 * self.top * ctx.N
+        self.out_words = 2 * self.out_level * ctx.N
+
+    def encrypt_image(self, image, nonce):
+        out = np.empty(self.ntaps * self.tap_words, dtype=np.uint64)
+        self.ctx.check(lib().hegpu_net_encrypt_image(self.h, np.ascontiguousarray(image, dtype=np.float64).ravel(),
+                                                     nonce, out))
+        return out
+
+    def run(self, taps_ct, out_ct):
+        self.ctx.check(lib().hegpu_net_run(self.h, taps_ct.h, out_ct.h))
+        return out_ct
+
+    def run_host(self, host_taps, batch, host_out):
+        """host_taps / host_out: numpy or pinned torch buffers (.ctypes.data / data_ptr)."""
+        pi = host_taps.ctypes.data if isinstance(host_taps, np.ndarray) else host_taps.data_ptr()
+        po = host_out.ctypes.data if isinstance(host_out, np.ndarray) else host_out.data_ptr()
+        self.ctx.check(lib().hegpu_net_run_host(self.h, pi, batch, po))
+
+    def decrypt_logits(self, out_ct):
+        m = self.cfg.dense[-1]
+        out = np.empty(m, dtype=np.float64)
+        self.ctx.check(lib().hegpu_net_decrypt_logits(self.h, np.ascontiguousarray(out_ct, dtype=np.uint64), out))
+        return out
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().hegpu_net_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass

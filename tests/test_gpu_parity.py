@@ -1,0 +1,275 @@
+"""GPU parity: every CUDA op, called through the C-ABI, against the CPU
+oracle on identical inputs -- ciphertext limbs must be bit-identical -- and
+the decrypted slots against the reference slot semantics (oracle/
+hesim_oracle.py, restating proj/src/*.cpp)."""
+import numpy as np
+import pytest
+
+from oracle import hesim_oracle as HS
+from oracle.ckks import Ckks
+from paper_2110_08321_b200 import hegpu as H
+from paper_2110_08321_b200.workloads import CFG0, hs_sweep_case, net_image, net_weights
+from oracle import ckks_pipeline as P
+
+pytestmark = pytest.mark.gpu
+
+SMALL = (10, [60, 40, 40, 40, 40], 60)   # N = 1024, S = 512
+DELTA = 2.0 ** 40
+
+
+@pytest.fixture(scope="module")
+def pair():
+    log_n, qb, pb = SMALL
+    ctx = H.Context(log_n, qb, pb, seed=21)
+    ck = Ckks(log_n, qb, pb, seed=21)
+    assert ctx.primes == ck.primes
+    return ctx, ck
+
+
+def fresh(ck, rng, level, nonce, n=None, scale=DELTA):
+    z = rng.uniform(-1, 1, n or ck.S)
+    return z, ck.encrypt(ck.encode(z, scale, level), level, nonce)
+
+
+def test_upload_download_roundtrip(pair):
+    ctx, ck = pair
+    rng = np.random.default_rng(0)
+    _, c = fresh(ck, rng, 5, 1)
+    d = ctx.ct(1, 5, c, DELTA)
+    assert np.array_equal(d.download(), c)
+    p = ck.encode(rng.uniform(-1, 1, ck.S), DELTA, 3, with_p=True)
+    dp = ctx.pt(1, 3, True, p, DELTA)
+    assert np.array_equal(dp.download(), p)
+
+
+def test_add_mul_plain(pair):
+    ctx, ck = pair
+    rng = np.random.default_rng(1)
+    l = 4
+    za, a = fresh(ck, rng, l, 2)
+    zb, b = fresh(ck, rng, l, 3)
+    zp = rng.uniform(-1, 1, ck.S)
+    p = ck.encode(zp, float(ck.primes[l - 1]), l)
+    da, db = ctx.ct(1, l, a, DELTA), ctx.ct(1, l, b, DELTA)
+    dp = ctx.pt(1, l, False, p, float(ck.primes[l - 1]))
+    out = ctx.ct(1, l)
+    assert np.array_equal(ctx.add(da, db, out).download(), ck.add(a, b, l))
+    assert np.array_equal(ctx.add_plain(da, dp, out).download(), ck.add_pc(a, p, l))
+    got = ctx.mul_plain(da, dp, out).download()
+    assert np.array_equal(got, ck.mul_pc(a, p, l))
+    r = ctx.ct(1, l - 1)
+    ctx.rescale(out, r)
+    want = ck.rescale(ck.mul_pc(a, p, l), l)
+    assert np.array_equal(r.download(), want)
+    assert np.abs(ck.decrypt_decode(want, l - 1, DELTA) - za * zp).max() < 1e-6
+
+
+@pytest.mark.parametrize("r", [1, 7, 255, 511])
+def test_rotate_right_bit_exact(pair, r):
+    ctx, ck = pair
+    rng = np.random.default_rng(r)
+    l = 4
+    z, a = fresh(ck, rng, l, 10 + r)
+    ctx.gen_rotation_keys([r])
+    out = ctx.ct(1, l)
+    got = ctx.rotate_right(ctx.ct(1, l, a, DELTA), r, out).download()
+    want = ck.rotate(a, l, ck.galois_right(r), ck.galois_key(ck.galois_right(r)))
+    assert np.array_equal(got, want)
+    # slot semantics: out[j] = v[(j - r) mod S] (proj/src/slotvec.cpp:42-57)
+    assert np.abs(ck.decrypt_decode(got, l, DELTA) - np.roll(z, r)).max() < 1e-6
+
+
+def test_rotate_left_and_zero(pair):
+    ctx, ck = pair
+    rng = np.random.default_rng(5)
+    l = 3
+    z, a = fresh(ck, rng, l, 40)
+    ctx.gen_rotation_keys([ck.S - 3])
+    da, out = ctx.ct(1, l, a, DELTA), ctx.ct(1, l)
+    ctx.reset_meter()
+    got = ctx.rotate_left(da, 3, out).download()
+    want = ck.rotate(a, l, ck.galois_left(3), ck.galois_key(ck.galois_left(3)))
+    assert np.array_equal(got, want)
+    assert np.abs(ck.decrypt_decode(got, l, DELTA) - np.roll(z, -3)).max() < 1e-6
+    assert np.array_equal(ctx.rotate_right(da, 0, out).download(), a)  # free no-op
+    assert ctx.total() == (0, 0, 0, 0, 1)
+    with pytest.raises(H.RangeError):
+        ctx.rotate_right(da, ck.S, out)
+    with pytest.raises(H.RangeError):
+        ctx.rotate_right(da, -1, out)
+    with pytest.raises(H.HegpuError) as e:
+        ctx.rotate_right(da, 77, out)
+    assert e.value.code == H.ERR_KEY
+
+
+def test_square_relin_rescale(pair):
+    ctx, ck = pair
+    rng = np.random.default_rng(6)
+    l = 5
+    z, a = fresh(ck, rng, l, 50)
+    ctx.gen_relin_key()
+    out = ctx.ct(1, l - 1)
+    got = ctx.square(ctx.ct(1, l, a, DELTA), out).download()
+    want = ck.rescale(ck.square(a, l, ck.relin_key()), l)
+    assert np.array_equal(got, want)
+    s = DELTA * DELTA / ck.primes[l - 1]
+    assert abs(out.scale - s) / s < 1e-15
+    assert np.abs(ck.decrypt_decode(got, l - 1, s) - z * z).max() < 1e-6
+
+
+def test_batched_ops_match_per_ciphertext(pair):
+    ctx, ck = pair
+    rng = np.random.default_rng(7)
+    l, B, r = 4, 3, 5
+    cts = [fresh(ck, rng, l, 60 + i)[1] for i in range(B)]
+    ctx.gen_rotation_keys([r])
+    ctx.gen_relin_key()
+    d = ctx.ct(B, l, np.concatenate(cts), DELTA)
+    out = ctx.ct(B, l)
+    got = ctx.rotate_right(d, r, out).download().reshape(B, -1)
+    key = ck.galois_key(ck.galois_right(r))
+    for i in range(B):
+        assert np.array_equal(got[i], ck.rotate(cts[i], l, ck.galois_right(r), key))
+    sq = ctx.ct(B, l - 1)
+    got = ctx.square(d, sq).download().reshape(B, -1)
+    rlk = ck.relin_key()
+    for i in range(B):
+        assert np.array_equal(got[i], ck.rescale(ck.square(cts[i], l, rlk), l))
+
+
+def test_conv_packed_forward(pair):
+    ctx, ck = pair
+    rng = np.random.default_rng(8)
+    # a 1x12x12 image, 3x3 kernel, stride 1 -> d_out 10 (w = 100 slots), 4 maps
+    cfg = type("C", (), dict(in_c=1, in_d=12, k=3, s=1, c_out=4))
+    img = rng.uniform(0, 1, (1, 12, 12))
+    W = rng.normal(0, 0.05, (4, 1, 3, 3))
+    bias = rng.normal(0, 0.01, 4)
+    L = ck.L
+    taps = P.conv_pack_taps(ck, cfg, img, 3, DELTA)
+    dt = ctx.ct(9, L, taps, DELTA)
+    out = ctx.ct(4, L - 1)
+    ctx.reset_meter()
+    got = ctx.conv_packed_forward(dt, 9, W.reshape(4, 9), bias, 100, out).download()
+    want = P.conv_layer(ck, taps, 9, L, W.reshape(4, 9), bias, 100, DELTA)
+    assert np.array_equal(got, want)
+    assert ctx.total() == (4, 32, 36, 0, 0)   # (c_out, (k^2-1) c_out, k^2 c_out, 0, 0)
+    ref = HS.ref_conv(img, W, bias, 1)
+    per = 2 * (L - 1) * ck.N
+    for co in range(4):
+        dec = ck.decrypt_decode(got[co * per:(co + 1) * per], L - 1, DELTA)
+        assert np.abs(dec[:100] - ref[co].ravel()).max() < 1e-6
+
+
+def test_merge_maps(pair):
+    ctx, ck = pair
+    rng = np.random.default_rng(9)
+    l, c, w = 4, 5, 100
+    zs, cts = [], []
+    for j in range(c):
+        z, ct = fresh(ck, rng, l, 80 + j, n=w)
+        zs.append(z)
+        cts.append(ct)
+    maps = np.concatenate(cts)
+    ctx.gen_rotation_keys([j * w for j in range(1, c)])
+    out = ctx.ct(1, l)
+    ctx.reset_meter()
+    got = ctx.merge_maps(ctx.ct(c, l, maps, DELTA), c, w, out).download()
+    assert ctx.total() == (0, 4, 0, 0, 4)   # merge 5 maps: 4 rot + 4 add (test_convlower.cpp:171-188)
+    want = P.merge(ck, maps, c, l, w)
+    assert np.array_equal(got, want)
+    dec = ck.decrypt_decode(got, l, DELTA)
+    assert np.abs(dec[: c * w] - np.concatenate(zs)).max() < 1e-6
+    with pytest.raises(H.CapacityError):
+        ctx.merge_maps(ctx.ct(c, l, maps, DELTA), c, 200, out)
+
+
+@pytest.mark.parametrize("m,n,skip", [(2, 2, True), (10, 100, True), (32, 300, True), (3, 4, False),
+                                      (7, 500, True), (4, 4, True)])
+def test_hs_matvec(pair, m, n, skip):
+    ctx, ck = pair
+    rng = np.random.default_rng(m * 1000 + n)
+    l = 3
+    A = rng.normal(0, 0.05, (m, n))
+    if (m, n) == (4, 4):
+        A = np.eye(4)  # zero diagonals skipped (test_matvec.cpp:99-108)
+    z, v = fresh(ck, rng, l, 100 + m, n=n)
+    plan = ctx.hs_plan(A, l, skip)
+    ctx.gen_rotation_keys(plan.rotations())
+    out = ctx.ct(1, l - 1)
+    ctx.reset_meter()
+    got = ctx.hs_matvec(plan, ctx.ct(1, l, v, DELTA), out).download()
+    want = P.hs_matvec(ck, v, l, A, skip)
+    assert np.array_equal(got, want)
+    dec = ck.decrypt_decode(got, l - 1, DELTA)
+    assert np.abs(dec[:m] - A @ z).max() < 1e-5
+    # metering equals the reference's hs_matvec on the same matrix
+    mc = HS.MeterContext()
+    HS.hs_matvec(A, HS.pack(z, ck.S, HS.CIPHERTEXT), mc, skip_zero_diagonals=skip)
+    assert ctx.total() == mc.tally.as_tuple()
+
+
+def test_hs_capacity(pair):
+    ctx, ck = pair
+    with pytest.raises(H.CapacityError):
+        ctx.hs_plan(np.ones((4, ck.S + 1)), 3)
+
+
+@pytest.fixture(scope="module")
+def cfg0():
+    cfg = CFG0
+    ctx = H.Context(cfg.log_n, list(cfg.qbits), cfg.pbits, seed=1234)
+    ck = Ckks(cfg.log_n, list(cfg.qbits), cfg.pbits, seed=1234)
+    w = net_weights(cfg, 0)
+    net = H.Net(ctx, cfg, w)
+    return cfg, ctx, ck, w, net
+
+
+def test_cfg0_net_bit_exact_and_logits(cfg0):
+    """Config 0 end to end: limbs == oracle pipeline, logits within 1e-3 of
+    ref_forward (proj/src/netcompile.cpp:448-503), per-stage HOPs == the
+    golden table."""
+    cfg, ctx, ck, w, net = cfg0
+    B = 2
+    imgs = [net_image(cfg, s) for s in range(B)]
+    taps = np.concatenate([net.encrypt_image(im, nonce=s) for s, im in enumerate(imgs)])
+    dt = ctx.ct(B * net.ntaps, net.top, taps, DELTA)
+    out = ctx.ct(B, net.out_level)
+    ctx.reset_meter()
+    net.run(dt, out)
+    got = out.download().reshape(B, -1)
+    spec = HS.CnnSpec(cfg.in_c, cfg.in_d, cfg.k, cfg.s, cfg.c_out, cfg.dense, cfg.n_slots)
+    golden = HS.golden_stage_tallies(spec)
+    assert dict(ctx.stages()) == {k: tuple(B * x for x in v) for k, v in golden.items()}
+    keys = {}
+    want, scale = P.run_net(ck, cfg, w, imgs[0], nonce=0, keys=keys)
+    assert np.array_equal(got[0], want)
+    for b in range(B):
+        logits = net.decrypt_logits(got[b])
+        ref = HS.ref_forward(spec, w, imgs[b])
+        assert np.abs(logits - ref).max() < 1e-3
+
+
+def test_cfg0_run_host_matches_device_run(cfg0):
+    cfg, ctx, ck, w, net = cfg0
+    B = 3
+    taps = np.concatenate([net.encrypt_image(net_image(cfg, 10 + s), nonce=10 + s) for s in range(B)])
+    host_out = np.zeros(B * net.out_words, dtype=np.uint64)
+    net.run_host(taps, B, host_out)
+    out = ctx.ct(B, net.out_level)
+    net.run(ctx.ct(B * net.ntaps, net.top, taps, DELTA), out)
+    assert np.array_equal(host_out, out.download())
+
+
+def test_cfg1_point_hs(cfg0):
+    """Config 1 shape at reduced ring (full sizes run in bench): m=64, n=256."""
+    ctx = H.Context(12, [60, 40], 60, seed=3)
+    ck = Ckks(12, [60, 40], 60, seed=3)
+    A, x = hs_sweep_case(64, 256)
+    v = ck.encrypt(ck.encode(x, DELTA, 2), 2, 1)
+    plan = ctx.hs_plan(A, 2)
+    ctx.gen_rotation_keys(plan.rotations())
+    out = ctx.ct(1, 1)
+    got = ctx.hs_matvec(plan, ctx.ct(1, 2, v, DELTA), out).download()
+    assert np.array_equal(got, P.hs_matvec(ck, v, 2, A))
+    assert np.abs(ck.decrypt_decode(got, 1, DELTA)[:64] - A @ x).max() < 1e-5
