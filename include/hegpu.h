@@ -82,6 +82,19 @@ int hegpu_ctx_info(const hegpu_ctx* ctx, int* n, int* slots, int* n_q, uint64_t*
 int hegpu_sync(hegpu_ctx* ctx);
 /* kernels launched by this context since creation (ours only) */
 int64_t hegpu_kernel_launches(const hegpu_ctx* ctx);
+/* per-kernel timing: bracket every launch of kernel `name` (e.g.
+ * "k_hs_diag") with CUDA events on the context stream; NULL disables.
+ * _read synchronises, returns the summed device time, launch count and
+ * algorithmic HBM bytes since the timer was (re)armed, and
+ * re-arms it. */
+int hegpu_kernel_timer(hegpu_ctx* ctx, const char* name);
+int hegpu_kernel_timer_read(hegpu_ctx* ctx, double* total_ms, int64_t* launches, double* alg_bytes);
+/* the cudaStream_t every kernel of this context is launched on (for
+ * caller-side CUDA-event timing); NULL for a client-only context */
+void* hegpu_stream(const hegpu_ctx* ctx);
+/* copy a device ciphertext batch, in wire format, into caller-owned device
+ * memory (e.g. a torch.cuda tensor handed to an NCCL gather) */
+int hegpu_ct_export_device(hegpu_ct* ct, void* dev_dst, size_t nwords);
 
 /* ---- metering: proj/include/hesim/meter.hpp:36-70 ----------------------- */
 int hegpu_begin_stage(hegpu_ctx* ctx, const char* label);

@@ -88,28 +88,70 @@ def conv_pack_taps(ck, cfg, image, nonce, tap_scale):
     return np.concatenate(cts)
 
 
+class PreparedNet:
+    """Server-side offline state for one model (keys, encoded HS masks,
+    bias plaintexts) so that eval() times only the homomorphic evaluation."""
+
+    def __init__(self, ck, cfg, weights):
+        self.ck, self.cfg = ck, cfg
+        self.tap_scale = 2.0 ** 40
+        L = ck.L
+        self.ntaps = cfg.k * cfg.k * cfg.in_c
+        d_out = (cfg.in_d - cfg.k) // cfg.s + 1
+        self.w_used = d_out * d_out
+        self.conv_w = np.asarray(weights["conv_w"], dtype=np.float64).reshape(cfg.c_out, -1)
+        qlast = float(ck.primes[L - 1])
+        self.conv_bias = np.concatenate([
+            ck.encode(np.full(self.w_used, weights["conv_b"][co]), self.tap_scale * qlast, L)
+            for co in range(cfg.c_out)])
+        keys = {}
+
+        def key(g):
+            if g not in keys:
+                keys[g] = ck.galois_key(g)
+            return keys[g]
+
+        l = L - 1
+        self.merge_keys = np.concatenate([key(ck.galois_right(j * self.w_used)) for j in range(1, cfg.c_out)]) \
+            if cfg.c_out > 1 else np.zeros(1, dtype=np.uint64)
+        self.rlk = ck.relin_key()
+        scale = self.tap_scale
+        self.layers = []
+        for W, b in weights["dense"]:
+            scale = scale * scale / float(ck.primes[l - 1])
+            l -= 1
+            m_eff, folds, rots, masks = hs_masks(ck, np.asarray(W), l, True)
+            kl = [key(ck.galois_right(r)) for r in rots if r != 0]
+            kbuf = np.concatenate(kl) if kl else np.zeros(1, dtype=np.uint64)
+            fold_keys = [(ck.galois_left(m_eff << t), key(ck.galois_left(m_eff << t)))
+                         for t in range(folds - 1, -1, -1)]
+            l -= 1
+            bias = ck.encode(np.asarray(b), scale, l)
+            self.layers.append((l + 1, np.array(rots, dtype=np.int64), masks, kbuf, fold_keys, bias))
+        self.out_scale = scale
+
+    def eval(self, taps):
+        ck, cfg = self.ck, self.cfg
+        L = ck.L
+        maps = ck.conv_mac(taps, self.ntaps, L, self.conv_w, cfg.c_out, float(ck.primes[L - 1]), self.conv_bias)
+        per = 2 * L * ck.N
+        maps = np.concatenate([ck.rescale(maps[co * per:(co + 1) * per], L) for co in range(cfg.c_out)])
+        l = L - 1
+        x = ck.merge(maps, cfg.c_out, l, self.w_used, self.merge_keys)
+        for lv, rots, masks, kbuf, fold_keys, bias in self.layers:
+            x = ck.rescale(ck.square(x, l, self.rlk), l)
+            l = lv
+            u = ck.rescale(ck.hs_hoisted(x, l, rots, masks, kbuf), l)
+            l -= 1
+            for g, k in fold_keys:
+                u = ck.add(u, ck.rotate(u, l, g, k), l)
+            x = ck.add_pc(u, bias, l)
+        return x
+
+
 def run_net(ck, cfg, weights, image, nonce=0, keys=None):
-    """Full oracle pipeline for one image; returns (output ct at level 1,
-    output scale)."""
-    keys = keys if keys is not None else {}
-    tap_scale = 2.0 ** 40
-    L = ck.L
-    ntaps = cfg.k * cfg.k * cfg.in_c
-    d_out = (cfg.in_d - cfg.k) // cfg.s + 1
-    w_used = d_out * d_out
-    taps = conv_pack_taps(ck, cfg, image, nonce, tap_scale)
-    maps = conv_layer(ck, taps, ntaps, L, np.asarray(weights["conv_w"]).reshape(cfg.c_out, -1),
-                      weights["conv_b"], w_used, tap_scale)
-    l = L - 1
-    x = merge(ck, maps, cfg.c_out, l, w_used, keys)
-    scale = tap_scale
-    if "rlk" not in keys:
-        keys["rlk"] = ck.relin_key()
-    for W, b in weights["dense"]:
-        x = square(ck, x, l, keys["rlk"])
-        scale = scale * scale / float(ck.primes[l - 1])
-        l -= 1
-        x = hs_matvec(ck, x, l, np.asarray(W), True, keys)
-        l -= 1
-        x = ck.add_pc(x, ck.encode(np.asarray(b), scale, l), l)
-    return x, scale
+    """Full oracle pipeline for one image (client encryption included);
+    returns (output ct at the last level, output scale)."""
+    prep = PreparedNet(ck, cfg, weights)
+    taps = conv_pack_taps(ck, cfg, image, nonce, prep.tap_scale)
+    return prep.eval(taps), prep.out_scale

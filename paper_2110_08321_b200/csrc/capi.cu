@@ -121,16 +121,7 @@ extern "C" int hegpu_ctx_create(const hegpu_params* p, int device, hegpu_ctx** o
       const Prime& pr = c.P->primes[i];
       c.primes.p[i] = DevPrime{pr.q, pr.qneg_inv, pr.r_mod, pr.r2_mod};
     }
-    std::vector<u64> tw((size_t)np * 4 * N);
-    for (int i = 0; i < np; ++i) {
-      const Prime& pr = c.P->primes[i];
-      std::copy(pr.w.begin(), pr.w.end(), tw.begin() + ((size_t)i * 4 + 0) * N);
-      std::copy(pr.wp.begin(), pr.wp.end(), tw.begin() + ((size_t)i * 4 + 1) * N);
-      std::copy(pr.iw.begin(), pr.iw.end(), tw.begin() + ((size_t)i * 4 + 2) * N);
-      std::copy(pr.iwp.begin(), pr.iwp.end(), tw.begin() + ((size_t)i * 4 + 3) * N);
-    }
-    CK(cudaMalloc((void**)&c.d_tw, tw.size() * 8));
-    CK(cudaMemcpy(c.d_tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice));
+    upload_twiddles(c);
     std::vector<u64> consts((size_t)2 * np + (size_t)2 * np * np);
     for (int i = 0; i < np; ++i) {
       const u64 q = c.P->q(i);
@@ -189,6 +180,45 @@ extern "C" int hegpu_sync(hegpu_ctx* h) {
 }
 
 extern "C" int64_t hegpu_kernel_launches(const hegpu_ctx* h) { return h ? h->c.launches : -1; }
+
+extern "C" void* hegpu_stream(const hegpu_ctx* h) { return h ? (void*)h->c.stream : nullptr; }
+
+extern "C" int hegpu_kernel_timer(hegpu_ctx* h, const char* name) {
+  if (!h) return HEGPU_ERR_ARG;
+  h->c.ktimer_name = name ? name : "";
+  h->c.ktimer_used = 0;
+  h->c.ktimer_bytes = 0;
+  return HEGPU_OK;
+}
+
+extern "C" int hegpu_kernel_timer_read(hegpu_ctx* h, double* total_ms, int64_t* launches, double* bytes) {
+  if (!h) return HEGPU_ERR_ARG;
+  Context& c = h->c;
+  return guarded(&c, [&] {
+    need_gpu(c);
+    CK(cudaStreamSynchronize(c.stream));
+    double tot = 0;
+    for (size_t i = 0; i < c.ktimer_used; ++i) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, c.ktimer_events[i].first, c.ktimer_events[i].second));
+      tot += ms;
+    }
+    if (total_ms) *total_ms = tot;
+    if (launches) *launches = (int64_t)c.ktimer_used;
+    if (bytes) *bytes = c.ktimer_bytes;
+    c.ktimer_used = 0;
+    c.ktimer_bytes = 0;
+  });
+}
+
+extern "C" int hegpu_ct_export_device(hegpu_ct* t, void* dst, size_t nwords) {
+  if (!t || !dst) return HEGPU_ERR_ARG;
+  Context& c = *t->b.ctx;
+  return guarded(&c, [&] {
+    need(nwords == t->b.words(), HEGPU_ERR_SHAPE, "ct_export_device: word count mismatch");
+    launch_slot_to_wire(c, t->b.d, (u64d*)dst, (size_t)t->b.count * 2 * t->b.level, 0, t->b.level, -1);
+  });
+}
 
 // ============================================================== metering ====
 extern "C" int hegpu_begin_stage(hegpu_ctx* h, const char* label) {

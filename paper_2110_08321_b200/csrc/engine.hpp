@@ -51,7 +51,7 @@ struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
   PrimeTable primes{};
-  u64d* d_tw = nullptr;          // [np][4][N]: w, w', iw, iw'
+  u64d* d_tw = nullptr;          // [np][2][N] (w, w') pairs: forward, inverse
   u64d* d_consts = nullptr;      // [np]: ninv, ninv' ; then [np][np]: qinv(value, shoup)
   uint32_t* d_slot_src = nullptr;  // [N]
   std::map<int, DeviceKey> rot_keys;  // keyed by left shift in [1, S)
@@ -61,6 +61,12 @@ struct Context {
   std::string last_error;
   int64_t launches = 0;
   size_t ws_bytes = 0;
+  // per-kernel event timing (hegpu_kernel_timer): every launch of the named
+  // kernel is bracketed by two events on the context stream
+  std::string ktimer_name;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ktimer_events;
+  size_t ktimer_used = 0;
+  double ktimer_bytes = 0;
 
   int N() const { return P->n; }
   int S() const { return P->slots; }
@@ -94,6 +100,44 @@ struct PtBatch {
 void check_cuda(cudaError_t e, const char* what);
 #define CK(x) ::hegpu::check_cuda((x), #x)
 
+// Brackets one kernel launch: counts it and, when the context's kernel
+// timer names this kernel, records start/stop events around it.
+struct Launch {
+  Context& c;
+  cudaEvent_t stop = nullptr;
+  // bytes: the launch's ALGORITHMIC HBM bytes (each operand read or written
+  // once), accumulated for the timed kernel -> roofline achieved GB/s
+  Launch(Context& cc, const char* name, double bytes = 0.0) : c(cc) {
+    ++c.launches;
+    if (!c.ktimer_name.empty() && c.ktimer_name == name) {
+      c.ktimer_bytes += bytes;
+      if (c.ktimer_used == c.ktimer_events.size()) {
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        c.ktimer_events.emplace_back(a, b);
+      }
+      auto& ev = c.ktimer_events[c.ktimer_used++];
+      CK(cudaEventRecord(ev.first, c.stream));
+      stop = ev.second;
+    }
+  }
+  void end() {
+    if (stop) CK(cudaEventRecord(stop, c.stream));
+    CK(cudaGetLastError());
+  }
+};
+// LAUNCH_B(ctx, "k_name", bytes, k_name<<<grid, block, smem, ctx.stream>>>(args...));
+#define LAUNCH_B(ctx, name, bytes, ...)          \
+  do {                                           \
+    ::hegpu::Launch _launch(ctx, name, (bytes)); \
+    __VA_ARGS__;                                 \
+    _launch.end();                               \
+  } while (0)
+#define LAUNCH(ctx, name, ...) LAUNCH_B(ctx, name, 0.0, __VA_ARGS__)
+
+// twiddle tables [np][fwd, inv][N] of (w, w') pairs -> c.d_tw
+void upload_twiddles(Context& c);
 // coefficient rows -> slot-order NTT rows; row r uses limb r % nl (limb l ->
 // prime l, or P for l == p_limb when p_limb >= 0)
 void launch_ntt_rows(Context& c, const u64d* src, u64d* dst, int rows, int nl, int p_limb);
@@ -138,12 +182,17 @@ void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, cons
                      int c_out, const u64d* bias /*[c_out][l][N] mont*/, u64d* out);
 struct HsDiagTable {
   int ndiag;
-  const u64d* masks;     // [ndiag][l+1][N] mont, slot order
-  const int* shifts;     // [ndiag] device: left shift (0 = no rotation)
-  const u64d* const* keys; // [ndiag] device key pointers (null for shift 0)
+  int keyed;                 // diagonals with r > 0 (carry a fused key)
+  const int* r;              // [ndiag] device: right rotation r_i, ascending
+  const u64d* const* fkeys;  // [ndiag] device: key_i * mask_i, [l][2][l+1][N] (null for r = 0)
+  const u64d* masks;         // [ndiag][l+1][N] mont, slot order
+  int nchunk;
+  const int* chunk;          // [nchunk + 1] diagonal ranges with r span < hs_chunk_span()
 };
+int hs_chunk_span();
 void launch_hs_diag(Context& c, const u64d* v, int B, int l, const u64d* D, const HsDiagTable& t,
                     u64d* acc, u64d* cacc);
+void launch_fuse_key(Context& c, const u64d* key, const u64d* mask, int l, u64d* fk);
 
 // high-level evaluator (eval.cu)
 void eval_rescale(Context& c, const CtBatch& a, CtBatch& out);

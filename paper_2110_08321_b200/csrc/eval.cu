@@ -1,10 +1,12 @@
-// eval.cu -- pointwise RNS kernels, the key-switch inner product, and the
-// evaluator compositions (rescale, Galois rotation, square + relinearise).
+// eval.cu -- pointwise RNS kernels, the key-switch inner product, the
+// conv-pack MAC, the Halevi-Shoup diagonal accumulation, and the evaluator
+// compositions (rescale, Galois rotation, square + relinearise).
 //
 // Reference semantics: add / mul (proj/src/slotvec.cpp:97-109), rotate_right
-// / rotate_left (:42-66), square_layer (proj/src/convlower.cpp:141-143).
-// The CKKS math (hybrid key switch, alpha = 1, one special prime) is fixed
-// in DESIGN.md §3.6 and restated by oracle/ckks_oracle.c.
+// / rotate_left (:42-66), square_layer (proj/src/convlower.cpp:141-143),
+// conv_packed_forward (:39-74), hs_matvec (proj/src/matvec.cpp:82-105).  The
+// CKKS math (hybrid key switch, alpha = 1, one special prime) is fixed in
+// DESIGN.md §3 and restated by oracle/ckks_oracle.c.
 #include "engine.hpp"
 
 namespace hegpu {
@@ -18,6 +20,22 @@ __device__ __forceinline__ int shifted_pos(int p, int s, int S) {
   int j = p - h + s;
   if (j >= S) j -= S;
   return h + j;
+}
+
+// 192-bit multiply-accumulate (lo, hi, top) += a * b
+__device__ __forceinline__ void mad192(u64d& lo, u64d& hi, uint32_t& top, u64d a, u64d b) {
+  asm("mad.lo.cc.u64 %0, %3, %4, %0;\n\t"
+      "madc.hi.cc.u64 %1, %3, %4, %1;\n\t"
+      "addc.u32 %2, %2, 0;\n\t"
+      : "+l"(lo), "+l"(hi), "+r"(top)
+      : "l"(a), "l"(b));
+}
+// (top:hi:lo) * 2^-64 mod q  (the sum of products of standard x Montgomery)
+__device__ __forceinline__ u64d red192(u64d lo, u64d hi, uint32_t top, const DevPrime& pr) {
+  u64d x = mont_reduce128(hi, (u64d)top, pr.q, pr.qneg_inv);  // (top:hi) R^-1
+  x = mont_mul(x, pr.r2_mod, pr.q, pr.qneg_inv);              // (top:hi) mod q
+  const u64d y = mont_reduce128(lo, 0ull, pr.q, pr.qneg_inv); // lo R^-1
+  return add_mod_d(x, y, pr.q);
 }
 
 // elementwise over [count][2][l][N]
@@ -86,111 +104,189 @@ __global__ void k_ks_inner(PrimeTable pt, const u64d* __restrict__ D, int l, int
   const u64d* key = km.key[b % km.period];
   const size_t kp = (size_t)(L + 1) * N;  // one key poly over all primes
   u64d lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
+  uint32_t t0 = 0, t1 = 0;
   for (int j = 0; j < l; ++j) {
     const u64d d = D[(((size_t)b * l + j) * (l + 1) + t) * N + k];
     const u64d* kj = key + (size_t)j * 2 * kp + (size_t)pi * N + k;
-    mac128(lo0, hi0, d, __ldg(kj));
-    mac128(lo1, hi1, d, __ldg(kj + kp));
+    mad192(lo0, hi0, t0, d, __ldg(kj));
+    mad192(lo1, hi1, t1, d, __ldg(kj + kp));
   }
   u64d* o = acc + ((size_t)b * 2 * (l + 1) + t) * N + k;
-  o[0] = mont_reduce128(lo0, hi0, pr.q, pr.qneg_inv);
-  o[(size_t)(l + 1) * N] = mont_reduce128(lo1, hi1, pr.q, pr.qneg_inv);
+  o[0] = red192(lo0, hi0, t0, pr);
+  o[(size_t)(l + 1) * N] = red192(lo1, hi1, t1, pr);
 }
 
-// conv-pack MAC (convlower.cpp:39-74): up to 8 output maps per thread
+// conv-pack MAC (convlower.cpp:39-74): CO output maps per thread, taps
+// streamed 8 at a time so each thread keeps 8 independent loads in flight.
 template <int CO>
-__global__ void k_conv_mac(PrimeTable pt, const u64d* __restrict__ taps, int ntaps, int l, int N,
-                           const u64d* __restrict__ w, int c_out, const u64d* __restrict__ bias,
-                           u64d* __restrict__ out) {
+__global__ void __launch_bounds__(kTpb) k_conv_mac(PrimeTable pt, const u64d* __restrict__ taps, int ntaps, int l,
+                                                   int N, const u64d* __restrict__ w, int c_out,
+                                                   const u64d* __restrict__ bias, u64d* __restrict__ out) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = blockIdx.y % l, poly = blockIdx.y / l;
-  const int b = blockIdx.z / ((c_out + CO - 1) / CO), cg = blockIdx.z % ((c_out + CO - 1) / CO);
+  const int groups = (c_out + CO - 1) / CO;
+  const int b = blockIdx.z / groups, cg = blockIdx.z % groups;
   if (k >= N) return;
   const DevPrime pr = pt.p[t];
   const size_t ct_words = (size_t)2 * l * N;
   const u64d* tp = taps + (size_t)b * ntaps * ct_words + (size_t)poly * l * N + (size_t)t * N + k;
-  u64d acc[CO], lo[CO], hi[CO];
+  u64d lo[CO], hi[CO];
+  uint32_t top[CO];
 #pragma unroll
-  for (int c = 0; c < CO; ++c) acc[c] = lo[c] = hi[c] = 0;
-  for (int s0 = 0; s0 < ntaps; s0 += 7) {
-    const int s1 = s0 + 7 < ntaps ? s0 + 7 : ntaps;
-    for (int s = s0; s < s1; ++s) {
-      const u64d x = tp[(size_t)s * ct_words];
+  for (int c = 0; c < CO; ++c) lo[c] = hi[c] = 0, top[c] = 0;
+  const int nco = c_out - cg * CO < CO ? c_out - cg * CO : CO;
+  int s = 0;
+  for (; s + 8 <= ntaps; s += 8) {
+    u64d x[8];
 #pragma unroll
-      for (int c = 0; c < CO; ++c) {
-        const int co = cg * CO + c;
-        if (co < c_out) mac128(lo[c], hi[c], x, __ldg(w + ((size_t)co * ntaps + s) * l + t));
-      }
-    }
+    for (int u = 0; u < 8; ++u) x[u] = __ldg(tp + (size_t)(s + u) * ct_words);
 #pragma unroll
-    for (int c = 0; c < CO; ++c) {
-      acc[c] = add_mod_d(acc[c], mont_reduce128(lo[c], hi[c], pr.q, pr.qneg_inv), pr.q);
-      lo[c] = hi[c] = 0;
-    }
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int c = 0; c < CO; ++c)
+        if (c < nco) mad192(lo[c], hi[c], top[c], x[u], __ldg(w + ((size_t)(cg * CO + c) * ntaps + s + u) * l + t));
+  }
+  for (; s < ntaps; ++s) {
+    const u64d x = __ldg(tp + (size_t)s * ct_words);
+#pragma unroll
+    for (int c = 0; c < CO; ++c)
+      if (c < nco) mad192(lo[c], hi[c], top[c], x, __ldg(w + ((size_t)(cg * CO + c) * ntaps + s) * l + t));
   }
 #pragma unroll
   for (int c = 0; c < CO; ++c) {
+    if (c >= nco) break;
     const int co = cg * CO + c;
-    if (co >= c_out) break;
-    u64d v = acc[c];
+    u64d v = red192(lo[c], hi[c], top[c], pr);
     if (poly == 0 && bias)
       v = add_mod_d(v, mont_mul(bias[((size_t)co * l + t) * N + k], 1ull, pr.q, pr.qneg_inv), pr.q);
     out[((size_t)b * c_out + co) * ct_words + (size_t)poly * l * N + (size_t)t * N + k] = v;
   }
 }
 
+// ---------------------------------------------------------------------------
 // Halevi-Shoup diagonal accumulation over the hoisted ModUp digits D of v.c1
-// (DESIGN.md §4.3): for each diagonal i with left shift s_i and mask m_i
-//   acc (ext basis) += m_i * sum_j sigma_i(D_j) * key_i[j]
-//   cacc            += m_i * sigma_i(v.c0)         (s_i == 0: m_i * v)
-__global__ void k_hs_diag(PrimeTable pt, const u64d* __restrict__ v, const u64d* __restrict__ D, int l, int L,
-                          int N, int ndiag, const u64d* __restrict__ masks, const int* __restrict__ shifts,
-                          const u64d* const* __restrict__ keys, u64d* __restrict__ acc, u64d* __restrict__ cacc) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  const int t = blockIdx.y, b = blockIdx.z;
-  if (k >= N) return;
+// (DESIGN.md §4.3).  Diagonal i rotates right by r_i; its Galois key is
+// pre-multiplied by the (pre-rotated) mask, so per output word and image the
+// work is a pure 192-bit multiply-accumulate:
+//   acc[p][t]  += sum_j D_j[k - r_i] * (key_i[j][p][t] * m_i[t])[k]   (r_i > 0)
+//   cacc[0][t] += c0[k - r_i] * m_i[t][k]                              (t < l)
+//   r_i == 0   : cacc[p][t] += c_p[k] * m_0[t][k]
+// The diagonals of a chunk have r in [r_lo, r_hi] (< KB + CW positions), so
+// the CTA stages the D / c0 window of its k-block in shared memory once and
+// every diagonal of the chunk reads it from there.
+constexpr int kHsKB = 128;  // output positions per CTA
+constexpr int kHsCW = 128;  // max r span of a chunk
+constexpr int kHsBT = 4;    // images per thread
+
+template <int LV>
+__global__ void __launch_bounds__(kHsKB) k_hs_diag(PrimeTable pt, const u64d* __restrict__ v,
+                                                   const u64d* __restrict__ D, int B, int L, int N,
+                                                   HsDiagTable tab, u64d* __restrict__ acc,
+                                                   u64d* __restrict__ cacc) {
+  extern __shared__ u64d win[];  // [BT][LV + 1][W]
   const int S = N >> 1;
+  const int KB = kHsKB < S ? kHsKB : S;
+  const int kb = blockIdx.y, t = blockIdx.z, b0 = blockIdx.x * kHsBT;
+  const int k0 = kb * KB, k = k0 + threadIdx.x;
+  const bool active = threadIdx.x < KB;
+  const int half = k0 >= S ? S : 0;
+  const int pi = t == LV ? L : t;
+  const DevPrime pr = pt.p[pi];
+  const bool has_c = t < LV;
+  const int Wmax = KB + kHsCW;
+  const int nrow = has_c ? LV + 1 : LV;  // D digits (+ c0)
+  const size_t ln = (size_t)LV * N;
+
+  u64d a_lo[kHsBT][2], a_hi[kHsBT][2], c_lo[kHsBT][2], c_hi[kHsBT][2];
+  uint32_t a_tp[kHsBT][2], c_tp[kHsBT][2];
+#pragma unroll
+  for (int bb = 0; bb < kHsBT; ++bb)
+#pragma unroll
+    for (int p = 0; p < 2; ++p) a_lo[bb][p] = a_hi[bb][p] = c_lo[bb][p] = c_hi[bb][p] = 0, a_tp[bb][p] = c_tp[bb][p] = 0;
+
+  for (int ch = 0; ch < tab.nchunk; ++ch) {
+    const int i0 = __ldg(tab.chunk + ch), i1 = __ldg(tab.chunk + ch + 1);
+    const int r_lo = __ldg(tab.r + i0), r_hi = __ldg(tab.r + i1 - 1);
+    const int W = KB + r_hi - r_lo;
+    // stage window positions k0 - r_hi + w (mod S, inside this half)
+    __syncthreads();
+    for (int e = threadIdx.x; e < kHsBT * nrow * W; e += blockDim.x) {
+      const int w = e % W, rb = e / W, row = rb % nrow, bb = rb / nrow;
+      const int b = b0 + bb;
+      int pos = k0 - half - r_hi + w;
+      pos %= S;
+      if (pos < 0) pos += S;
+      pos += half;
+      u64d val = 0;
+      if (b < B)
+        val = row < LV ? D[(((size_t)b * LV + row) * (LV + 1) + t) * N + pos]
+                       : v[(size_t)b * 2 * ln + (size_t)t * N + pos];
+      win[(size_t)(bb * (LV + 1) + row) * Wmax + w] = val;
+    }
+    __syncthreads();
+    if (!active) continue;
+    for (int i = i0; i < i1; ++i) {
+      const int r = __ldg(tab.r + i);
+      const int wo = threadIdx.x + (r_hi - r);
+      const u64d m = has_c ? __ldg(tab.masks + ((size_t)i * (LV + 1) + t) * N + k) : 0ull;
+      if (r == 0) {
+        if (has_c) {
+#pragma unroll
+          for (int bb = 0; bb < kHsBT; ++bb) {
+            const int b = b0 + bb;
+            if (b >= B) break;
+            mad192(c_lo[bb][0], c_hi[bb][0], c_tp[bb][0], win[(size_t)(bb * (LV + 1) + LV) * Wmax + wo], m);
+            mad192(c_lo[bb][1], c_hi[bb][1], c_tp[bb][1], v[(size_t)b * 2 * ln + ln + (size_t)t * N + k], m);
+          }
+        }
+        continue;
+      }
+      const u64d* fk = tab.fkeys[i] + (size_t)t * N + k;
+      const size_t kp = (size_t)(LV + 1) * N;
+      u64d kv[LV][2];
+#pragma unroll
+      for (int j = 0; j < LV; ++j) {
+        kv[j][0] = __ldg(fk + (size_t)j * 2 * kp);
+        kv[j][1] = __ldg(fk + (size_t)j * 2 * kp + kp);
+      }
+#pragma unroll
+      for (int bb = 0; bb < kHsBT; ++bb) {
+#pragma unroll
+        for (int j = 0; j < LV; ++j) {
+          const u64d d = win[(size_t)(bb * (LV + 1) + j) * Wmax + wo];
+          mad192(a_lo[bb][0], a_hi[bb][0], a_tp[bb][0], d, kv[j][0]);
+          mad192(a_lo[bb][1], a_hi[bb][1], a_tp[bb][1], d, kv[j][1]);
+        }
+        if (has_c) mad192(c_lo[bb][0], c_hi[bb][0], c_tp[bb][0], win[(size_t)(bb * (LV + 1) + LV) * Wmax + wo], m);
+      }
+    }
+  }
+  if (!active) return;
+#pragma unroll
+  for (int bb = 0; bb < kHsBT; ++bb) {
+    const int b = b0 + bb;
+    if (b >= B) break;
+    u64d* ab = acc + (size_t)b * 2 * (LV + 1) * N + (size_t)t * N + k;
+    ab[0] = red192(a_lo[bb][0], a_hi[bb][0], a_tp[bb][0], pr);
+    ab[(size_t)(LV + 1) * N] = red192(a_lo[bb][1], a_hi[bb][1], a_tp[bb][1], pr);
+    if (has_c) {
+      u64d* cb = cacc + (size_t)b * 2 * ln + (size_t)t * N + k;
+      cb[0] = red192(c_lo[bb][0], c_hi[bb][0], c_tp[bb][0], pr);
+      cb[ln] = red192(c_lo[bb][1], c_hi[bb][1], c_tp[bb][1], pr);
+    }
+  }
+}
+
+// fused key: fk[j][p][t] = key[j][p][pi(t)] * m[t]   (t over the ext basis)
+__global__ void k_fuse_key(PrimeTable pt, const u64d* __restrict__ key, const u64d* __restrict__ m, int l, int L,
+                           int N, u64d* __restrict__ fk) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.y % (l + 1), jp = blockIdx.y / (l + 1);  // jp = j * 2 + p
+  if (k >= N) return;
   const int pi = t == l ? L : t;
   const DevPrime pr = pt.p[pi];
-  const u64d q = pr.q, qn = pr.qneg_inv;
-  const size_t kp = (size_t)(L + 1) * N;
-  const size_t ln = (size_t)l * N;
-  const u64d* Db = D + (size_t)b * l * (l + 1) * N + (size_t)t * N;
-  const u64d* c0 = v + (size_t)b * 2 * ln + (size_t)t * N;
-  const u64d* c1 = c0 + ln;
-  u64d a0 = 0, a1 = 0, x0 = 0, x1 = 0;
-  for (int i = 0; i < ndiag; ++i) {
-    const int s = __ldg(shifts + i);
-    const u64d m = __ldg(masks + ((size_t)i * (l + 1) + t) * N + k);
-    if (s == 0) {
-      if (t < l) {
-        x0 = add_mod_d(x0, mont_mul(c0[k], m, q, qn), q);
-        x1 = add_mod_d(x1, mont_mul(c1[k], m, q, qn), q);
-      }
-      continue;
-    }
-    const int ps = shifted_pos(k, s, S);
-    const u64d* key = keys[i] + (size_t)pi * N + k;
-    u64d lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
-    for (int j = 0; j < l; ++j) {
-      const u64d d = Db[(size_t)j * (l + 1) * N + ps];
-      const u64d* kj = key + (size_t)j * 2 * kp;
-      mac128(lo0, hi0, d, __ldg(kj));
-      mac128(lo1, hi1, d, __ldg(kj + kp));
-    }
-    const u64d ip0 = mont_reduce128(lo0, hi0, q, qn), ip1 = mont_reduce128(lo1, hi1, q, qn);
-    a0 = add_mod_d(a0, mont_mul(ip0, m, q, qn), q);
-    a1 = add_mod_d(a1, mont_mul(ip1, m, q, qn), q);
-    if (t < l) x0 = add_mod_d(x0, mont_mul(c0[ps], m, q, qn), q);
-  }
-  u64d* ab = acc + (size_t)b * 2 * (l + 1) * N + (size_t)t * N + k;
-  ab[0] = a0;
-  ab[(size_t)(l + 1) * N] = a1;
-  if (t < l) {
-    u64d* cb = cacc + (size_t)b * 2 * ln + (size_t)t * N + k;
-    cb[0] = x0;
-    cb[ln] = x1;
-  }
+  const u64d kv = key[((size_t)jp * (L + 1) + pi) * N + k];
+  fk[((size_t)jp * (l + 1) + t) * N + k] = mont_mul(kv, m[(size_t)t * N + k], pr.q, pr.qneg_inv);
 }
 
 unsigned grid_for(size_t total) {
@@ -198,59 +294,91 @@ unsigned grid_for(size_t total) {
   return (unsigned)(g < 148 * 16 ? (g ? g : 1) : 148 * 16);
 }
 
+template <int LV>
+void launch_hs_lv(Context& c, const u64d* v, int B, const u64d* D, const HsDiagTable& t, u64d* acc, u64d* cacc) {
+  const int N = c.N(), S = N / 2;
+  const int KB = kHsKB < S ? kHsKB : S;
+  dim3 grid((B + kHsBT - 1) / kHsBT, N / KB, LV + 1);
+  const size_t sm = (size_t)kHsBT * (LV + 1) * (KB + kHsCW) * 8;
+  static size_t done = 0;
+  if (sm > 48 * 1024 && sm > done) {
+    CK(cudaFuncSetAttribute(k_hs_diag<LV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    done = sm;
+  }
+  // fused keys + masks (c-part limbs) once; v, D read once; acc, cacc written once
+  const double NB = 8.0 * N;
+  const double bytes = NB * (t.keyed * LV * 2.0 * (LV + 1) + t.ndiag * LV + B * (LV * (LV + 1.0) + 2.0 * LV) +
+                             B * (2.0 * (LV + 1) + 2.0 * LV));
+  LAUNCH_B(c, "k_hs_diag", bytes, k_hs_diag<LV><<<grid, kHsKB, sm, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc));
+}
+
 }  // namespace
+
+int hs_chunk_span() { return kHsCW; }
 
 void launch_add(Context& c, const u64d* a, const u64d* b, u64d* out, int count, int l) {
   const size_t total = (size_t)count * 2 * l * c.N();
-  k_add<<<grid_for(total), kTpb, 0, c.stream>>>(c.primes, a, b, out, total, l, c.N());
-  c.launches++;
-  CK(cudaGetLastError());
+  LAUNCH_B(c, "k_add", 24.0 * total, k_add<<<grid_for(total), kTpb, 0, c.stream>>>(c.primes, a, b, out, total, l, c.N()));
 }
 
 void launch_add_plain(Context& c, const u64d* a, const u64d* p, long p_stride, u64d* out, int count, int l) {
   const size_t total = (size_t)count * 2 * l * c.N();
-  k_add_plain<<<grid_for(total), kTpb, 0, c.stream>>>(c.primes, a, p, p_stride, out, total, l, c.N());
-  c.launches++;
-  CK(cudaGetLastError());
+  LAUNCH_B(c, "k_add_plain", 16.0 * total + 4.0 * total / count,
+         k_add_plain<<<grid_for(total), kTpb, 0, c.stream>>>(c.primes, a, p, p_stride, out, total, l, c.N()));
 }
 
 void launch_mul_plain(Context& c, const u64d* a, const u64d* p, long p_stride, u64d* out, int count, int l) {
   const size_t total = (size_t)count * 2 * l * c.N();
-  k_mul_plain<<<grid_for(total), kTpb, 0, c.stream>>>(c.primes, a, p, p_stride, out, total, l, c.N());
-  c.launches++;
-  CK(cudaGetLastError());
+  LAUNCH_B(c, "k_mul_plain", 16.0 * total + 4.0 * total / count,
+         k_mul_plain<<<grid_for(total), kTpb, 0, c.stream>>>(c.primes, a, p, p_stride, out, total, l, c.N()));
 }
 
 void launch_tensor_square(Context& c, const u64d* a, u64d* d01, u64d* d2, int count, int l) {
   const size_t total = (size_t)count * l * c.N();
-  k_tensor_square<<<grid_for(total), kTpb, 0, c.stream>>>(c.primes, a, d01, d2, total, l, c.N());
-  c.launches++;
-  CK(cudaGetLastError());
+  LAUNCH_B(c, "k_tensor_square", 40.0 * total,
+         k_tensor_square<<<grid_for(total), kTpb, 0, c.stream>>>(c.primes, a, d01, d2, total, l, c.N()));
 }
 
 void ks_inner(Context& c, const u64d* D, int B, int l, const KeyRowMap& keys, u64d* acc) {
   dim3 grid((c.N() + kTpb - 1) / kTpb, l + 1, B);
-  k_ks_inner<<<grid, kTpb, 0, c.stream>>>(c.primes, D, l, c.L(), c.N(), keys, acc);
-  c.launches++;
-  CK(cudaGetLastError());
+  double kb = 0;  // distinct keys read once each
+  for (int i = 0; i < keys.period && i < B; ++i) kb += 8.0 * l * 2 * (l + 1) * c.N();
+  LAUNCH_B(c, "k_ks_inner", 8.0 * B * (l + 2) * (l + 1) * c.N() + kb, k_ks_inner<<<grid, kTpb, 0, c.stream>>>(c.primes, D, l, c.L(), c.N(), keys, acc));
 }
 
 void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, const u64d* w, int c_out,
                      const u64d* bias, u64d* out) {
-  const int groups = (c_out + 7) / 8;
-  dim3 grid((c.N() + kTpb - 1) / kTpb, 2 * l, B * groups);
-  k_conv_mac<8><<<grid, kTpb, 0, c.stream>>>(c.primes, taps, ntaps, l, c.N(), w, c_out, bias, out);
-  c.launches++;
-  CK(cudaGetLastError());
+  // taps read once, maps written once, bias plaintexts read once
+  const double bytes = 8.0 * c.N() * l * (2.0 * B * ntaps + 2.0 * B * c_out + c_out);
+  if (c_out <= 4) {
+    dim3 grid((c.N() + kTpb - 1) / kTpb, 2 * l, B * ((c_out + 3) / 4));
+    LAUNCH_B(c, "k_conv_mac", bytes,
+           k_conv_mac<4><<<grid, kTpb, 0, c.stream>>>(c.primes, taps, ntaps, l, c.N(), w, c_out, bias, out));
+  } else {
+    dim3 grid((c.N() + kTpb - 1) / kTpb, 2 * l, B * ((c_out + 7) / 8));
+    LAUNCH_B(c, "k_conv_mac", bytes,
+           k_conv_mac<8><<<grid, kTpb, 0, c.stream>>>(c.primes, taps, ntaps, l, c.N(), w, c_out, bias, out));
+  }
+}
+
+void launch_fuse_key(Context& c, const u64d* key, const u64d* mask, int l, u64d* fk) {
+  dim3 grid((c.N() + kTpb - 1) / kTpb, 2 * l * (l + 1));
+  LAUNCH(c, "k_fuse_key", k_fuse_key<<<grid, kTpb, 0, c.stream>>>(c.primes, key, mask, l, c.L(), c.N(), fk));
 }
 
 void launch_hs_diag(Context& c, const u64d* v, int B, int l, const u64d* D, const HsDiagTable& t, u64d* acc,
                     u64d* cacc) {
-  dim3 grid((c.N() + kTpb - 1) / kTpb, l + 1, B);
-  k_hs_diag<<<grid, kTpb, 0, c.stream>>>(c.primes, v, D, l, c.L(), c.N(), t.ndiag, t.masks, t.shifts, t.keys,
-                                         acc, cacc);
-  c.launches++;
-  CK(cudaGetLastError());
+  switch (l) {
+    case 1: launch_hs_lv<1>(c, v, B, D, t, acc, cacc); break;
+    case 2: launch_hs_lv<2>(c, v, B, D, t, acc, cacc); break;
+    case 3: launch_hs_lv<3>(c, v, B, D, t, acc, cacc); break;
+    case 4: launch_hs_lv<4>(c, v, B, D, t, acc, cacc); break;
+    case 5: launch_hs_lv<5>(c, v, B, D, t, acc, cacc); break;
+    case 6: launch_hs_lv<6>(c, v, B, D, t, acc, cacc); break;
+    case 7: launch_hs_lv<7>(c, v, B, D, t, acc, cacc); break;
+    case 8: launch_hs_lv<8>(c, v, B, D, t, acc, cacc); break;
+    default: fail(HEGPU_ERR_ARG, "hs_matvec: level above 8 not supported");
+  }
 }
 
 // ---------------------------------------------------------------- compositions

@@ -162,21 +162,33 @@ void HsPlan::build(Context& c, const double* A, int m_, int n_, int lvl, bool sk
     CK(cudaMalloc((void**)&masks, wire.size() * 8));
     upload_mont(c, wire, masks, kept.size() * nl, nl, level);
   }
-  std::vector<int> sh(diag.size());
-  for (size_t i = 0; i < diag.size(); ++i) sh[i] = diag[i].shift;
-  CK(cudaMalloc((void**)&d_shifts, (sh.size() + 1) * sizeof(int)));
-  if (!sh.empty()) CK(cudaMemcpy(d_shifts, sh.data(), sh.size() * sizeof(int), cudaMemcpyHostToDevice));
-  CK(cudaMalloc((void**)&d_keys, (diag.size() + 1) * sizeof(u64d*)));
+  // right rotations (ascending) and chunks whose r span fits one smem window
+  std::vector<int> r(diag.size()), chunk{0};
+  for (size_t i = 0; i < diag.size(); ++i) {
+    r[i] = (int)diag[i].right;
+    if (i > 0 && r[i] - r[chunk.back()] >= hs_chunk_span()) chunk.push_back((int)i);
+  }
+  chunk.push_back((int)diag.size());
+  if (diag.empty()) chunk = {0};
+  nchunk = (int)chunk.size() - 1;
+  CK(cudaMalloc((void**)&d_r, (r.size() + 1) * sizeof(int)));
+  if (!r.empty()) CK(cudaMemcpy(d_r, r.data(), r.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMalloc((void**)&d_chunk, chunk.size() * sizeof(int)));
+  CK(cudaMemcpy(d_chunk, chunk.data(), chunk.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMalloc((void**)&d_fkeys, (diag.size() + 1) * sizeof(u64d*)));
 }
 
 void HsPlan::release() {
   if (ctx) cudaStreamSynchronize(ctx->stream);
   cudaFree(masks);
-  cudaFree(d_shifts);
-  cudaFree(d_keys);
+  cudaFree(d_r);
+  cudaFree(d_chunk);
+  cudaFree(fkeys);
+  cudaFree(d_fkeys);
   masks = nullptr;
-  d_shifts = nullptr;
-  d_keys = nullptr;
+  d_r = d_chunk = nullptr;
+  fkeys = nullptr;
+  d_fkeys = nullptr;
 }
 
 std::vector<int64_t> HsPlan::right_rotations() const {
@@ -191,11 +203,23 @@ std::vector<int64_t> HsPlan::right_rotations() const {
 void HsPlan::run(Context& c, const CtBatch& v, CtBatch& out) {
   const int B = v.count, l = level, N = c.N(), S = c.S();
   if (!keys_resolved) {
-    std::vector<const u64d*> kp(diag.size(), nullptr);
-    for (size_t i = 0; i < diag.size(); ++i)
-      if (diag[i].shift) kp[i] = c.rot_key(diag[i].shift).data;
-    if (!kp.empty()) CK(cudaMemcpy(d_keys, kp.data(), kp.size() * sizeof(u64d*), cudaMemcpyHostToDevice));
+    // fuse each diagonal's Galois key with its mask once (offline work):
+    // fk_i[j][p][t] = key_i[j][p][t] * mask'_i[t] over the level-l ext basis
     for (int t = folds - 1; t >= 0; --t) c.rot_key((int)(((int64_t)m_eff << t) % S));
+    const size_t fk_words = (size_t)l * 2 * (l + 1) * N;
+    size_t nkeyed = 0;
+    for (const HsDiag& d : diag) nkeyed += d.shift != 0;
+    if (nkeyed) CK(cudaMalloc((void**)&fkeys, nkeyed * fk_words * 8));
+    std::vector<const u64d*> kp(diag.size(), nullptr);
+    size_t slot = 0;
+    for (size_t i = 0; i < diag.size(); ++i) {
+      if (!diag[i].shift) continue;
+      u64d* dst = fkeys + slot++ * fk_words;
+      launch_fuse_key(c, c.rot_key(diag[i].shift).data, masks + i * (size_t)(l + 1) * N, l, dst);
+      kp[i] = dst;
+    }
+    if (!kp.empty()) CK(cudaMemcpy(d_fkeys, kp.data(), kp.size() * sizeof(u64d*), cudaMemcpyHostToDevice));
+    CK(cudaStreamSynchronize(c.stream));
     keys_resolved = true;
   }
   u64d* tmp = c.alloc((size_t)B * l * N);
@@ -207,7 +231,9 @@ void HsPlan::run(Context& c, const CtBatch& v, CtBatch& out) {
   // (1) one ModUp of v.c1 for all diagonals (hoisting)
   ks_modup(c, v.d + (size_t)l * N, (long)v.stride(), B, l, nullptr, tmp, D);
   // (2) diagonal accumulation in the extended basis
-  HsDiagTable tab{(int)diag.size(), masks, d_shifts, d_keys};
+  int keyed = 0;
+  for (const HsDiag& dd : diag) keyed += dd.shift != 0;
+  HsDiagTable tab{(int)diag.size(), keyed, d_r, d_fkeys, masks, nchunk, d_chunk};
   launch_hs_diag(c, v.d, B, l, D, tab, acc, cacc);
   // (3) one ModDown of the sum (+ the Q-basis c-part)
   DropArgs d{};

@@ -39,8 +39,11 @@ struct HsPlan {
   int m = 0, n = 0, m_eff = 0, folds = 0, level = 0;
   std::vector<HsDiag> diag;   // kept (non-zero) diagonals in order
   u64d* masks = nullptr;      // [kept][level+1][N] Montgomery, slot order
-  int* d_shifts = nullptr;    // [kept]
-  const u64d** d_keys = nullptr;  // [kept] resolved on first run
+  int* d_r = nullptr;         // [kept] right rotations
+  int* d_chunk = nullptr;     // chunk boundaries
+  int nchunk = 0;
+  u64d* fkeys = nullptr;      // [kept][level][2][level+1][N] key_i * mask_i (first run)
+  const u64d** d_fkeys = nullptr;  // [kept]
   bool keys_resolved = false;
   void build(Context& c, const double* A, int m, int n, int level, bool skip_zero);
   void release();

@@ -1,59 +1,35 @@
 // ntt.cu -- batched negacyclic NTT / INTT over 64-bit primes (sm_100a).
 //
-// One CTA transforms one N-word limb entirely in shared memory (N <= 16384:
-// 128 KB).  Forward: Cooley-Tukey with psi powers in bit-reversed order and
-// Shoup twiddle products; inverse: Gentleman-Sande.  Loads/stores fuse the
-// surrounding RNS steps so every limb crosses HBM once per transform:
-//   - forward stores scatter into the device SLOT ORDER (engine.hpp);
-//   - the key-switch INTT loads apply the Galois shift on the fly;
-//   - ModUp loads reduce a digit mod the target prime;
-//   - the drop-limb NTT (rescale / ModDown) lifts the dropped residue,
-//     transforms it and finishes (x - X) * q_d^{-1} (+ add term) in the store.
+// One CTA transforms one N-word limb (2^5 <= N <= 2^14) held in shared
+// memory.  Each thread keeps R = 16 words in registers and runs up to 4
+// radix-2 stages per pass on them (Cooley-Tukey forward with psi powers in
+// bit-reversed order, Gentleman-Sande inverse), so an N = 8192 transform is
+// 4 register passes with 3 shared-memory exchanges instead of 13
+// stage-synchronous sweeps.  The pass schedule is resolved at compile time
+// per log2 N.  Butterflies are Harvey-lazy (values in [0, 4q), Shoup twiddle
+// products in [0, 2q)); primes < 2^61 keep 4q in a word.  Twiddles are
+// (w, w') pairs read as one 16-byte load.
+//
+// Loads and stores are functors so every limb crosses HBM once per
+// transform with the surrounding RNS step fused in:
+//   forward : store scatters to the device SLOT ORDER (engine.hpp);
+//             ModUp loads reduce a digit mod the target prime;
+//             drop-limb (rescale / ModDown) loads lift the dropped residue
+//             and the store finishes (x - X) * q_d^{-1} (+ add term);
+//   inverse : key-switch loads apply the Galois shift and emit the shifted
+//             own-prime limb for ModUp; stores multiply by N^{-1}.
 #include "engine.hpp"
 
 namespace hegpu {
 
 namespace {
 
-__device__ __forceinline__ int ntt_threads(int N) { return N / 2 < 512 ? N / 2 : 512; }
+constexpr int kLogR = 4;
+constexpr int kR = 1 << kLogR;
+constexpr int kMinLogN = 5, kMaxLogN = 14;
 
-// forward CT in smem (natural in, bit-reversed out)
-__device__ __forceinline__ void fwd_core(u64d* a, int N, int logN, const u64d* __restrict__ w,
-                                         const u64d* __restrict__ wp, u64d q) {
-  const int half = N >> 1;
-  for (int lt = logN - 1, m = 1; lt >= 0; --lt, m <<= 1) {
-    const int tmask = (1 << lt) - 1;
-    for (int b = threadIdx.x; b < half; b += blockDim.x) {
-      const int i = b >> lt, j = b & tmask;
-      const int x = (i << (lt + 1)) + j, y = x + (1 << lt);
-      const u64d W = __ldg(w + m + i), Wp = __ldg(wp + m + i);
-      const u64d U = a[x], V = shoup_mul_d(a[y], W, Wp, q);
-      a[x] = add_mod_d(U, V, q);
-      a[y] = sub_mod_d(U, V, q);
-    }
-    __syncthreads();
-  }
-}
+__device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
 
-// inverse GS in smem (bit-reversed in, natural out, without the N^{-1})
-__device__ __forceinline__ void inv_core(u64d* a, int N, const u64d* __restrict__ iw,
-                                         const u64d* __restrict__ iwp, u64d q) {
-  const int half = N >> 1;
-  for (int lt = 0, h = half; h >= 1; ++lt, h >>= 1) {
-    const int tmask = (1 << lt) - 1;
-    for (int b = threadIdx.x; b < half; b += blockDim.x) {
-      const int i = b >> lt, j = b & tmask;
-      const int x = (i << (lt + 1)) + j, y = x + (1 << lt);
-      const u64d W = __ldg(iw + h + i), Wp = __ldg(iwp + h + i);
-      const u64d U = a[x], V = a[y];
-      a[x] = add_mod_d(U, V, q);
-      a[y] = shoup_mul_d(sub_mod_d(U, V, q), W, Wp, q);
-    }
-    __syncthreads();
-  }
-}
-
-// slot position p after a left rotation by s (inside each half)
 __device__ __forceinline__ int shifted(int p, int s, int S) {
   const int h = p >= S ? S : 0;
   int j = p - h + s;
@@ -61,112 +37,298 @@ __device__ __forceinline__ int shifted(int p, int s, int S) {
   return h + j;
 }
 
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
+
 struct TwArgs {
-  const u64d* tw;
+  const ulonglong2* tw;   // [np][2][N] (w, w') forward then inverse
   const u64d* ninv;       // [np][2]
   const uint32_t* slot_src;
-  int N, logN;
 };
 
-__device__ __forceinline__ const u64d* tw_of(const TwArgs& t, int pi, int which) {
-  return t.tw + ((size_t)pi * 4 + which) * t.N;
+// ------------------------------------------------------------------ forward
+// Pass of RR stages starting at stage S0: thread element e = g * 2^RR + j sits
+// at index hi * 2^(LOGN - S0) + j * 2^LOB + lo (LOB = LOGN - S0 - RR), where
+// group grp = g * T + tid splits into (hi, lo).
+template <int LOGN, int S0, int RR>
+__device__ __forceinline__ int fwd_idx(int g, int j) {
+  constexpr int T = (1 << LOGN) / kR, LOB = LOGN - S0 - RR;
+  const int grp = g * T + (int)threadIdx.x;
+  return ((grp >> LOB) << (LOGN - S0)) + (j << LOB) + (grp & ((1 << LOB) - 1));
 }
 
-// --------------------------------------------------------------------------
-__global__ void k_ntt_rows(TwArgs ta, PrimeTable pt, const u64d* __restrict__ src,
-                           u64d* __restrict__ dst, int nl, int p_limb, int p_index) {
+template <int LOGN, int S0, int RR>
+__device__ __forceinline__ void fwd_pass(u64d (&x)[kR], const ulonglong2* __restrict__ tw, u64d q) {
+  constexpr int T = (1 << LOGN) / kR, G = kR >> RR, J = 1 << RR, LOB = LOGN - S0 - RR;
+  const u64d q2 = 2 * q;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int hi = (g * T + (int)threadIdx.x) >> LOB;
+#pragma unroll
+    for (int u = 0; u < RR; ++u) {
+      const int half = J >> (u + 1);
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        if (j & half) continue;
+        const ulonglong2 W = __ldg(tw + (1 << (S0 + u)) + (hi << u) + (j >> (RR - u)));
+        u64d a = x[g * J + j];
+        if (a >= q2) a -= q2;
+        const u64d t = shoup_mul_lazy(x[g * J + j + half], W.x, W.y, q);
+        x[g * J + j] = a + t;
+        x[g * J + j + half] = a - t + q2;
+      }
+    }
+  }
+}
+
+template <int LOGN, int S0, int RR>
+__device__ __forceinline__ void fwd_store(u64d* sm, const u64d (&x)[kR]) {
+#pragma unroll
+  for (int g = 0; g < (kR >> RR); ++g)
+#pragma unroll
+    for (int j = 0; j < (1 << RR); ++j) sm[pad(fwd_idx<LOGN, S0, RR>(g, j))] = x[g * (1 << RR) + j];
+}
+
+template <int LOGN, int S0, int RR>
+__device__ __forceinline__ void fwd_load(const u64d* sm, u64d (&x)[kR]) {
+#pragma unroll
+  for (int g = 0; g < (kR >> RR); ++g)
+#pragma unroll
+    for (int j = 0; j < (1 << RR); ++j) x[g * (1 << RR) + j] = sm[pad(fwd_idx<LOGN, S0, RR>(g, j))];
+}
+
+template <int LOGN, int S0>
+__device__ __forceinline__ void fwd_passes(u64d (&x)[kR], u64d* sm, const ulonglong2* tw, u64d q) {
+  constexpr int RR = cmin(kLogR, LOGN - S0);
+  fwd_pass<LOGN, S0, RR>(x, tw, q);
+  if constexpr (S0 + RR < LOGN) {
+    constexpr int RN = cmin(kLogR, LOGN - S0 - RR);
+    fwd_store<LOGN, S0, RR>(sm, x);
+    __syncthreads();
+    fwd_load<LOGN, S0 + RR, RN>(sm, x);
+    __syncthreads();
+    fwd_passes<LOGN, S0 + RR>(x, sm, tw, q);
+  } else {
+    const u64d q2 = 2 * q;
+#pragma unroll
+    for (int e = 0; e < kR; ++e) {
+      u64d v = x[e];
+      if (v >= q2) v -= q2;
+      if (v >= q) v -= q;
+      x[e] = v;
+    }
+    fwd_store<LOGN, S0, RR>(sm, x);
+    __syncthreads();
+  }
+}
+
+// forward NTT of the row `ld` describes; result in smem (padded, canonical,
+// bit-reversed index order), CTA synchronised on return
+template <int LOGN, class Ld>
+__device__ __forceinline__ void fwd_transform(u64d* sm, const Ld& ld, const ulonglong2* tw, u64d q) {
+  constexpr int R0 = cmin(kLogR, LOGN);
+  u64d x[kR];
+#pragma unroll
+  for (int g = 0; g < (kR >> R0); ++g)
+#pragma unroll
+    for (int j = 0; j < (1 << R0); ++j) x[g * (1 << R0) + j] = ld.load(fwd_idx<LOGN, 0, R0>(g, j));
+  fwd_passes<LOGN, 0>(x, sm, tw, q);
+}
+
+// ------------------------------------------------------------------ inverse
+// GS pass of RR stages starting at inverse stage S0 (distance 2^S0): element
+// e = g * 2^RR + j sits at hi * 2^(S0 + RR) + j * 2^S0 + lo.
+template <int LOGN, int S0, int RR>
+__device__ __forceinline__ int inv_idx(int g, int j) {
+  constexpr int T = (1 << LOGN) / kR;
+  const int grp = g * T + (int)threadIdx.x;
+  return ((grp >> S0) << (S0 + RR)) + (j << S0) + (grp & ((1 << S0) - 1));
+}
+
+template <int LOGN, int S0, int RR>
+__device__ __forceinline__ void inv_pass(u64d (&x)[kR], const ulonglong2* __restrict__ tw, u64d q) {
+  constexpr int T = (1 << LOGN) / kR, G = kR >> RR, J = 1 << RR;
+  const u64d q2 = 2 * q;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int hi = (g * T + (int)threadIdx.x) >> S0;
+#pragma unroll
+    for (int u = 0; u < RR; ++u) {
+      const int dist = 1 << u;
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        if (j & dist) continue;
+        const ulonglong2 W = __ldg(tw + (1 << (LOGN - S0 - u - 1)) + (hi << (RR - u - 1)) + (j >> (u + 1)));
+        const u64d a = x[g * J + j], b = x[g * J + j + dist];
+        u64d s = a + b;
+        if (s >= q2) s -= q2;
+        x[g * J + j] = s;
+        x[g * J + j + dist] = shoup_mul_lazy(a - b + q2, W.x, W.y, q);
+      }
+    }
+  }
+}
+
+template <int LOGN, int S0, int RR>
+__device__ __forceinline__ void inv_store(u64d* sm, const u64d (&x)[kR]) {
+#pragma unroll
+  for (int g = 0; g < (kR >> RR); ++g)
+#pragma unroll
+    for (int j = 0; j < (1 << RR); ++j) sm[pad(inv_idx<LOGN, S0, RR>(g, j))] = x[g * (1 << RR) + j];
+}
+
+template <int LOGN, int S0, int RR>
+__device__ __forceinline__ void inv_load(const u64d* sm, u64d (&x)[kR]) {
+#pragma unroll
+  for (int g = 0; g < (kR >> RR); ++g)
+#pragma unroll
+    for (int j = 0; j < (1 << RR); ++j) x[g * (1 << RR) + j] = sm[pad(inv_idx<LOGN, S0, RR>(g, j))];
+}
+
+template <int LOGN, int S0, class St>
+__device__ __forceinline__ void inv_passes(u64d (&x)[kR], u64d* sm, const ulonglong2* tw, u64d q, u64d nv,
+                                           u64d nvp, St& st) {
+  constexpr int RR = cmin(kLogR, LOGN - S0);
+  inv_pass<LOGN, S0, RR>(x, tw, q);
+  if constexpr (S0 + RR < LOGN) {
+    constexpr int RN = cmin(kLogR, LOGN - S0 - RR);
+    __syncthreads();
+    inv_store<LOGN, S0, RR>(sm, x);
+    __syncthreads();
+    inv_load<LOGN, S0 + RR, RN>(sm, x);
+    inv_passes<LOGN, S0 + RR>(x, sm, tw, q, nv, nvp, st);
+  } else {
+#pragma unroll
+    for (int g = 0; g < (kR >> RR); ++g)
+#pragma unroll
+      for (int j = 0; j < (1 << RR); ++j)
+        st.store(inv_idx<LOGN, S0, RR>(g, j), shoup_mul_d(x[g * (1 << RR) + j], nv, nvp, q));
+  }
+}
+
+// inverse NTT: input already scattered into smem (bit-reversed index order,
+// canonical) and synchronised; st.store(k, v) receives N^{-1} * INTT.
+template <int LOGN, class St>
+__device__ __forceinline__ void inv_transform(u64d* sm, St& st, const ulonglong2* tw, u64d q, u64d nv, u64d nvp) {
+  constexpr int R0 = cmin(kLogR, LOGN);
+  u64d x[kR];
+  inv_load<LOGN, 0, R0>(sm, x);
+  inv_passes<LOGN, 0>(x, sm, tw, q, nv, nvp, st);
+}
+
+// ------------------------------------------------------------ functors
+struct LdPlain {
+  const u64d* p;
+  __device__ u64d load(int k) const { return p[k]; }
+};
+struct LdReduce {
+  const u64d* p;
+  DevPrime pr;
+  __device__ u64d load(int k) const { return reduce64(p[k], pr); }
+};
+struct LdLift {  // centered lift of a residue mod qd into q
+  const u64d* p;
+  DevPrime pr;
+  u64d qd;
+  __device__ u64d load(int k) const {
+    const u64d x = p[k];
+    return x > (qd >> 1) ? sub_mod_d(0, reduce64(qd - x, pr), pr.q) : reduce64(x, pr);
+  }
+};
+struct StPlain {
+  u64d* p;
+  __device__ void store(int k, u64d v) const { p[k] = v; }
+};
+
+__device__ __forceinline__ const ulonglong2* twf(const TwArgs& t, int pi, int N) {
+  return t.tw + (size_t)pi * 2 * N;
+}
+__device__ __forceinline__ const ulonglong2* twi(const TwArgs& t, int pi, int N) {
+  return t.tw + ((size_t)pi * 2 + 1) * N;
+}
+
+#define NTT_BOUNDS __launch_bounds__((1 << LOGN) / kR)
+
+// ------------------------------------------------------------ kernels
+template <int LOGN>
+__global__ void NTT_BOUNDS k_ntt_rows(TwArgs ta, PrimeTable pt, const u64d* __restrict__ src,
+                                      u64d* __restrict__ dst, int nl, int p_limb, int p_index) {
   extern __shared__ u64d sm[];
-  const int N = ta.N, r = blockIdx.x, limb = r % nl;
+  constexpr int N = 1 << LOGN;
+  const int r = blockIdx.x, limb = r % nl;
   const int pi = (limb == p_limb) ? p_index : limb;
-  const u64d q = pt.p[pi].q;
-  const u64d* s = src + (size_t)r * N;
-  for (int k = threadIdx.x; k < N; k += blockDim.x) sm[k] = s[k];
-  __syncthreads();
-  fwd_core(sm, N, ta.logN, tw_of(ta, pi, 0), tw_of(ta, pi, 1), q);
+  fwd_transform<LOGN>(sm, LdPlain{src + (size_t)r * N}, twf(ta, pi, N), pt.p[pi].q);
   u64d* d = dst + (size_t)r * N;
-  for (int p = threadIdx.x; p < N; p += blockDim.x) d[p] = sm[__ldg(ta.slot_src + p)];
+  for (int p = threadIdx.x; p < N; p += blockDim.x) d[p] = sm[pad(__ldg(ta.slot_src + p))];
 }
 
 struct PMap {
   int8_t p[HEGPU_MAX_PRIMES];
 };
 
-__global__ void k_intt_rows(TwArgs ta, PrimeTable pt, const u64d* __restrict__ src,
-                            u64d* __restrict__ dst, int n_inner, long so, long si, long dox,
-                            long di, PMap pm) {
+template <int LOGN>
+__global__ void NTT_BOUNDS k_intt_rows(TwArgs ta, PrimeTable pt, const u64d* __restrict__ src,
+                                       u64d* __restrict__ dst, int n_inner, long so, long si, long dox, long di,
+                                       PMap pm) {
   extern __shared__ u64d sm[];
-  const int N = ta.N;
+  constexpr int N = 1 << LOGN;
   const int r = blockIdx.x, o = r / n_inner, i = r % n_inner;
   const int pi = pm.p[i];
-  const u64d q = pt.p[pi].q;
   const u64d* s = src + o * so + i * si;
-  for (int p = threadIdx.x; p < N; p += blockDim.x) sm[__ldg(ta.slot_src + p)] = s[p];
+  for (int p = threadIdx.x; p < N; p += blockDim.x) sm[pad(__ldg(ta.slot_src + p))] = s[p];
   __syncthreads();
-  inv_core(sm, N, tw_of(ta, pi, 2), tw_of(ta, pi, 3), q);
-  const u64d nv = ta.ninv[2 * pi], nvp = ta.ninv[2 * pi + 1];
-  u64d* d = dst + o * dox + i * di;
-  for (int k = threadIdx.x; k < N; k += blockDim.x) d[k] = shoup_mul_d(sm[k], nv, nvp, q);
+  StPlain st{dst + o * dox + i * di};
+  inv_transform<LOGN>(sm, st, twi(ta, pi, N), pt.p[pi].q, ta.ninv[2 * pi], ta.ninv[2 * pi + 1]);
 }
 
 // KS input: digit j of (shifted) poly b -> coefficient row tmp[b][j]; also
 // writes the shifted NTT-form limb into D[b][j][j] (ModUp's own-prime row).
-__global__ void k_ks_intt(TwArgs ta, PrimeTable pt, const u64d* __restrict__ src, long src_stride,
-                          int l, KeyRowMap km, int use_shift, u64d* __restrict__ tmp,
-                          u64d* __restrict__ D) {
+template <int LOGN>
+__global__ void NTT_BOUNDS k_ks_intt(TwArgs ta, PrimeTable pt, const u64d* __restrict__ src, long src_stride, int l,
+                                     KeyRowMap km, int use_shift, u64d* __restrict__ tmp, u64d* __restrict__ D) {
   extern __shared__ u64d sm[];
-  const int N = ta.N, S = N >> 1;
+  constexpr int N = 1 << LOGN, S = N >> 1;
   const int r = blockIdx.x, b = r / l, j = r % l;
   const int s = use_shift ? km.shift[b % km.period] : 0;
-  const u64d q = pt.p[j].q;
   const u64d* in = src + b * src_stride + (size_t)j * N;
   u64d* own = D + (((size_t)b * l + j) * (l + 1) + j) * N;
   for (int p = threadIdx.x; p < N; p += blockDim.x) {
     const u64d v = in[s ? shifted(p, s, S) : p];
     own[p] = v;
-    sm[__ldg(ta.slot_src + p)] = v;
+    sm[pad(__ldg(ta.slot_src + p))] = v;
   }
   __syncthreads();
-  inv_core(sm, N, tw_of(ta, j, 2), tw_of(ta, j, 3), q);
-  const u64d nv = ta.ninv[2 * j], nvp = ta.ninv[2 * j + 1];
-  u64d* d = tmp + ((size_t)b * l + j) * N;
-  for (int k = threadIdx.x; k < N; k += blockDim.x) d[k] = shoup_mul_d(sm[k], nv, nvp, q);
+  StPlain st{tmp + ((size_t)b * l + j) * N};
+  inv_transform<LOGN>(sm, st, twi(ta, j, N), pt.p[j].q, ta.ninv[2 * j], ta.ninv[2 * j + 1]);
 }
 
 // ModUp: rows (b, j, t') with t = t' < j ? t' : t'+1 over the extended basis
 // (t == l means P); NTT_t(tmp[b][j] mod q_t) -> D[b][j][t]
-__global__ void k_ks_modup(TwArgs ta, PrimeTable pt, const u64d* __restrict__ tmp, int l, int P_index,
-                           u64d* __restrict__ D) {
+template <int LOGN>
+__global__ void NTT_BOUNDS k_ks_modup(TwArgs ta, PrimeTable pt, const u64d* __restrict__ tmp, int l, int P_index,
+                                      u64d* __restrict__ D) {
   extern __shared__ u64d sm[];
-  const int N = ta.N;
+  constexpr int N = 1 << LOGN;
   const int r = blockIdx.x;
   const int tp = r % l, bj = r / l, j = bj % l, b = bj / l;
   const int t = tp < j ? tp : tp + 1;
   const int pi = t == l ? P_index : t;
   const DevPrime pr = pt.p[pi];
-  const u64d* s = tmp + ((size_t)b * l + j) * N;
-  for (int k = threadIdx.x; k < N; k += blockDim.x) sm[k] = reduce64(s[k], pr);
-  __syncthreads();
-  fwd_core(sm, N, ta.logN, tw_of(ta, pi, 0), tw_of(ta, pi, 1), pr.q);
+  fwd_transform<LOGN>(sm, LdReduce{tmp + ((size_t)b * l + j) * N, pr}, twf(ta, pi, N), pr.q);
   u64d* d = D + (((size_t)b * l + j) * (l + 1) + t) * N;
-  for (int p = threadIdx.x; p < N; p += blockDim.x) d[p] = sm[__ldg(ta.slot_src + p)];
+  for (int p = threadIdx.x; p < N; p += blockDim.x) d[p] = sm[pad(__ldg(ta.slot_src + p))];
 }
 
 // drop-limb NTT: rows (b, p, t < nl)
-__global__ void k_drop_ntt(TwArgs ta, PrimeTable pt, const u64d* __restrict__ qinv, int np_all,
-                           DropArgs a, const u64d* __restrict__ tmpP, KeyRowMap km, int use_shift) {
+template <int LOGN>
+__global__ void NTT_BOUNDS k_drop_ntt(TwArgs ta, PrimeTable pt, const u64d* __restrict__ qinv, int np_all,
+                                      DropArgs a, const u64d* __restrict__ tmpP, KeyRowMap km, int use_shift) {
   extern __shared__ u64d sm[];
-  const int N = ta.N, S = N >> 1;
+  constexpr int N = 1 << LOGN, S = N >> 1;
   const int r = blockIdx.x;
   const int t = r % a.nl, bp = r / a.nl, p = bp % 2, b = bp / 2;
   const DevPrime pr = pt.p[t];
-  const u64d q = pr.q, qd = pt.p[a.pd].q, half = qd >> 1;
-  const u64d* s = tmpP + ((size_t)b * 2 + p) * N;
-  for (int k = threadIdx.x; k < N; k += blockDim.x) {
-    const u64d x = s[k];
-    sm[k] = x > half ? sub_mod_d(0, reduce64(qd - x, pr), q) : reduce64(x, pr);
-  }
-  __syncthreads();
-  fwd_core(sm, N, ta.logN, tw_of(ta, t, 0), tw_of(ta, t, 1), q);
+  const u64d q = pr.q;
+  fwd_transform<LOGN>(sm, LdLift{tmpP + ((size_t)b * 2 + p) * N, pr, pt.p[a.pd].q}, twf(ta, t, N), q);
   const u64d iv = qinv[((size_t)t * np_all + a.pd) * 2], ivp = qinv[((size_t)t * np_all + a.pd) * 2 + 1];
   const u64d* in = a.src + b * a.src_b + p * a.src_p + (size_t)t * N;
   u64d* out = a.dst + b * a.dst_b + p * a.dst_p + (size_t)t * N;
@@ -174,7 +336,7 @@ __global__ void k_drop_ntt(TwArgs ta, PrimeTable pt, const u64d* __restrict__ qi
   const u64d* ad = add ? a.add + b * a.add_b + p * a.add_p + (size_t)t * N : nullptr;
   const int sh = (use_shift && p == 0) ? km.shift[b % km.period] : 0;
   for (int pos = threadIdx.x; pos < N; pos += blockDim.x) {
-    u64d v = shoup_mul_d(sub_mod_d(in[pos], sm[__ldg(ta.slot_src + pos)], q), iv, ivp, q);
+    u64d v = shoup_mul_d(sub_mod_d(in[pos], sm[pad(__ldg(ta.slot_src + pos))], q), iv, ivp, q);
     if (add) v = add_mod_d(v, ad[sh ? shifted(pos, sh, S) : pos], q);
     out[pos] = v;
   }
@@ -182,8 +344,8 @@ __global__ void k_drop_ntt(TwArgs ta, PrimeTable pt, const u64d* __restrict__ qi
 
 // wire (bit-reversed) <-> slot order, optional Montgomery conversion
 __global__ void k_wire_to_slot(const u64d* __restrict__ src, u64d* __restrict__ dst,
-                               const uint32_t* __restrict__ slot_src, PrimeTable pt, int N, int to_mont,
-                               int nl, int p_limb, int p_index) {
+                               const uint32_t* __restrict__ slot_src, PrimeTable pt, int N, int to_mont, int nl,
+                               int p_limb, int p_index) {
   const size_t r = blockIdx.y;
   const int limb = (int)(r % nl);
   const DevPrime pr = pt.p[limb == p_limb ? p_index : limb];
@@ -196,8 +358,8 @@ __global__ void k_wire_to_slot(const u64d* __restrict__ src, u64d* __restrict__ 
 }
 
 __global__ void k_slot_to_wire(const u64d* __restrict__ src, u64d* __restrict__ dst,
-                               const uint32_t* __restrict__ slot_src, PrimeTable pt, int N, int from_mont,
-                               int nl, int p_limb, int p_index) {
+                               const uint32_t* __restrict__ slot_src, PrimeTable pt, int N, int from_mont, int nl,
+                               int p_limb, int p_index) {
   const size_t r = blockIdx.y;
   const int limb = (int)(r % nl);
   const DevPrime pr = pt.p[limb == p_limb ? p_index : limb];
@@ -209,30 +371,65 @@ __global__ void k_slot_to_wire(const u64d* __restrict__ src, u64d* __restrict__ 
   }
 }
 
-TwArgs tw_args(Context& c) {
-  return TwArgs{c.d_tw, c.ninv_tab(), c.d_slot_src, c.N(), c.P->log_n};
-}
-
-int threads_for(int N) { return N / 2 < 512 ? N / 2 : 512; }
+TwArgs tw_args(Context& c) { return TwArgs{(const ulonglong2*)c.d_tw, c.ninv_tab(), c.d_slot_src}; }
+int ntt_threads(int N) { return N / kR; }
+size_t ntt_smem(int N) { return (size_t)(N + (N >> 4) + 1) * 8; }
 
 template <typename K>
-void set_smem(K kernel, size_t bytes) {
-  static size_t done = 0;
-  if (bytes > 48 * 1024 && bytes > done) {
-    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    done = bytes;
-  }
+void prep_kernel(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
+
+// one launch per op, dispatched on log2 N
+#define NTT_DISPATCH(logn, KERNEL, GRID, ...)                                                       \
+  do {                                                                                              \
+    switch (logn) {                                                                                 \
+      case 5: NTT_GO(5, KERNEL, GRID, __VA_ARGS__); break;                                          \
+      case 6: NTT_GO(6, KERNEL, GRID, __VA_ARGS__); break;                                          \
+      case 7: NTT_GO(7, KERNEL, GRID, __VA_ARGS__); break;                                          \
+      case 8: NTT_GO(8, KERNEL, GRID, __VA_ARGS__); break;                                          \
+      case 9: NTT_GO(9, KERNEL, GRID, __VA_ARGS__); break;                                          \
+      case 10: NTT_GO(10, KERNEL, GRID, __VA_ARGS__); break;                                        \
+      case 11: NTT_GO(11, KERNEL, GRID, __VA_ARGS__); break;                                        \
+      case 12: NTT_GO(12, KERNEL, GRID, __VA_ARGS__); break;                                        \
+      case 13: NTT_GO(13, KERNEL, GRID, __VA_ARGS__); break;                                        \
+      case 14: NTT_GO(14, KERNEL, GRID, __VA_ARGS__); break;                                        \
+      default: fail(HEGPU_ERR_ARG, "NTT: log2 N must be in [5, 14] on the device");                \
+    }                                                                                               \
+  } while (0)
+
+#define NTT_GO(LG, KERNEL, GRID, ...)                                                               \
+  do {                                                                                              \
+    static bool prepared = false;                                                                   \
+    const size_t smb = ntt_smem(1 << LG);                                                           \
+    if (!prepared) { prep_kernel(KERNEL<LG>, smb); prepared = true; }                                \
+    LAUNCH_B(c, #KERNEL, _ntt_bytes, KERNEL<LG><<<(GRID), (1 << LG) / kR, smb, c.stream>>>(__VA_ARGS__)); \
+  } while (0)
 
 }  // namespace
 
+void upload_twiddles(Context& c) {
+  const Params& P = *c.P;
+  const int np = P.np(), N = P.n;
+  if (P.log_n < kMinLogN || P.log_n > kMaxLogN) fail(HEGPU_ERR_ARG, "device NTT supports 2^5 <= N <= 2^14");
+  std::vector<u64> tw((size_t)np * 2 * N * 2);
+  for (int i = 0; i < np; ++i) {
+    const Prime& pr = P.primes[i];
+    for (int k = 0; k < N; ++k) {
+      tw[(((size_t)i * 2 + 0) * N + k) * 2 + 0] = pr.w[k];
+      tw[(((size_t)i * 2 + 0) * N + k) * 2 + 1] = pr.wp[k];
+      tw[(((size_t)i * 2 + 1) * N + k) * 2 + 0] = pr.iw[k];
+      tw[(((size_t)i * 2 + 1) * N + k) * 2 + 1] = pr.iwp[k];
+    }
+  }
+  CK(cudaMalloc((void**)&c.d_tw, tw.size() * 8));
+  CK(cudaMemcpy(c.d_tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice));
+}
+
 void launch_ntt_rows(Context& c, const u64d* src, u64d* dst, int rows, int nl, int p_limb) {
   if (rows <= 0) return;
-  const size_t sm = (size_t)c.N() * 8;
-  set_smem(k_ntt_rows, sm);
-  k_ntt_rows<<<rows, threads_for(c.N()), sm, c.stream>>>(tw_args(c), c.primes, src, dst, nl, p_limb, c.L());
-  c.launches++;
-  CK(cudaGetLastError());
+  const double _ntt_bytes = 16.0 * c.N() * rows;  // read + write one limb per row
+  NTT_DISPATCH(c.P->log_n, k_ntt_rows, rows, tw_args(c), c.primes, src, dst, nl, p_limb, c.L());
 }
 
 void launch_intt_rows(Context& c, const u64d* src, u64d* dst, int n_outer, int n_inner, long so, long si,
@@ -241,63 +438,49 @@ void launch_intt_rows(Context& c, const u64d* src, u64d* dst, int n_outer, int n
   if (n_inner > HEGPU_MAX_PRIMES) fail(HEGPU_ERR_ARG, "intt_rows: too many limbs");
   PMap pm{};
   for (int i = 0; i < n_inner; ++i) pm.p[i] = (int8_t)prime_of_inner[i];
-  const size_t sm = (size_t)c.N() * 8;
-  set_smem(k_intt_rows, sm);
-  k_intt_rows<<<n_outer * n_inner, threads_for(c.N()), sm, c.stream>>>(
-      tw_args(c), c.primes, src, dst, n_inner, so, si, dox, di, pm);
-  c.launches++;
-  CK(cudaGetLastError());
+  const double _ntt_bytes = 16.0 * c.N() * n_outer * n_inner;
+  NTT_DISPATCH(c.P->log_n, k_intt_rows, n_outer * n_inner, tw_args(c), c.primes, src, dst, n_inner, so, si, dox,
+               di, pm);
 }
 
 void launch_wire_to_slot(Context& c, const u64d* src, u64d* dst, size_t rows, int to_mont, int nl, int p_limb) {
   if (!rows) return;
   dim3 grid((c.N() + 255) / 256 < 8 ? (c.N() + 255) / 256 : 8, (unsigned)rows);
-  k_wire_to_slot<<<grid, 256, 0, c.stream>>>(src, dst, c.d_slot_src, c.primes, c.N(), to_mont, nl, p_limb, c.L());
-  c.launches++;
-  CK(cudaGetLastError());
+  LAUNCH(c, "k_wire_to_slot",
+         k_wire_to_slot<<<grid, 256, 0, c.stream>>>(src, dst, c.d_slot_src, c.primes, c.N(), to_mont, nl, p_limb,
+                                                    c.L()));
 }
 
 void launch_slot_to_wire(Context& c, const u64d* src, u64d* dst, size_t rows, int from_mont, int nl, int p_limb) {
   if (!rows) return;
   dim3 grid((c.N() + 255) / 256 < 8 ? (c.N() + 255) / 256 : 8, (unsigned)rows);
-  k_slot_to_wire<<<grid, 256, 0, c.stream>>>(src, dst, c.d_slot_src, c.primes, c.N(), from_mont, nl, p_limb, c.L());
-  c.launches++;
-  CK(cudaGetLastError());
+  LAUNCH(c, "k_slot_to_wire",
+         k_slot_to_wire<<<grid, 256, 0, c.stream>>>(src, dst, c.d_slot_src, c.primes, c.N(), from_mont, nl, p_limb,
+                                                    c.L()));
 }
 
-void ks_modup(Context& c, const u64d* src, long src_stride, int B, int l, const KeyRowMap* shifts,
-              u64d* tmp, u64d* D) {
-  const size_t sm = (size_t)c.N() * 8;
+void ks_modup(Context& c, const u64d* src, long src_stride, int B, int l, const KeyRowMap* shifts, u64d* tmp,
+              u64d* D) {
   KeyRowMap dummy{};
   dummy.period = 1;
-  set_smem(k_ks_intt, sm);
-  k_ks_intt<<<B * l, threads_for(c.N()), sm, c.stream>>>(tw_args(c), c.primes, src, src_stride, l,
-                                                          shifts ? *shifts : dummy, shifts != nullptr, tmp, D);
-  c.launches++;
-  CK(cudaGetLastError());
-  if (B * l * l > 0) {
-    set_smem(k_ks_modup, sm);
-    k_ks_modup<<<B * l * l, threads_for(c.N()), sm, c.stream>>>(tw_args(c), c.primes, tmp, l, c.L(), D);
-    c.launches++;
-    CK(cudaGetLastError());
-  }
+  double _ntt_bytes = 24.0 * c.N() * B * l;  // read digit, write coefficients + own-prime copy
+  NTT_DISPATCH(c.P->log_n, k_ks_intt, B * l, tw_args(c), c.primes, src, src_stride, l, shifts ? *shifts : dummy,
+               shifts != nullptr, tmp, D);
+  _ntt_bytes = 16.0 * c.N() * B * l * l;
+  if (B * l * l > 0) NTT_DISPATCH(c.P->log_n, k_ks_modup, B * l * l, tw_args(c), c.primes, tmp, l, c.L(), D);
 }
 
 void drop_last_limb(Context& c, int B, const DropArgs& a, u64d* tmpP) {
   const int N = c.N();
-  // INTT of the dropped limb of both polys -> tmpP[b][p]
   const int pmap[2] = {a.pd, a.pd};
   launch_intt_rows(c, a.src + (size_t)(a.src_limbs - 1) * N, tmpP, B, 2, a.src_b, a.src_p, 2L * N, N, pmap);
   if (a.nl <= 0) return;
-  const size_t sm = (size_t)N * 8;
   KeyRowMap dummy{};
   dummy.period = 1;
-  set_smem(k_drop_ntt, sm);
-  k_drop_ntt<<<B * 2 * a.nl, threads_for(N), sm, c.stream>>>(tw_args(c), c.primes, c.qinv_tab(), c.P->np(), a,
-                                                            tmpP, a.shifts ? *a.shifts : dummy,
-                                                            a.shifts != nullptr);
-  c.launches++;
-  CK(cudaGetLastError());
+  // read lifted residue + source limb (+ add term), write the output limb
+  const double _ntt_bytes = (24.0 + (a.add ? 8.0 : 0.0)) * N * B * 2 * a.nl;
+  NTT_DISPATCH(c.P->log_n, k_drop_ntt, B * 2 * a.nl, tw_args(c), c.primes, c.qinv_tab(), c.P->np(), a, tmpP,
+               a.shifts ? *a.shifts : dummy, a.shifts != nullptr);
 }
 
 }  // namespace hegpu

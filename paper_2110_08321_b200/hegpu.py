@@ -76,6 +76,10 @@ def lib():
             "hegpu_ctx_info": (i, [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i), u64p]),
             "hegpu_sync": (i, [vp]),
             "hegpu_kernel_launches": (C.c_int64, [vp]),
+            "hegpu_stream": (vp, [vp]),
+            "hegpu_kernel_timer": (i, [vp, C.c_char_p]),
+            "hegpu_kernel_timer_read": (i, [vp, C.POINTER(d), C.POINTER(C.c_int64), C.POINTER(d)]),
+            "hegpu_ct_export_device": (i, [vp, vp, sz]),
             "hegpu_begin_stage": (i, [vp, C.c_char_p]),
             "hegpu_num_stages": (i, [vp]),
             "hegpu_stage_tally": (i, [vp, i, C.c_char_p, i, i64p]),
@@ -133,7 +137,7 @@ def declared_symbols():
     import re
     root = os.path.dirname(_HERE)
     text = open(os.path.join(root, "include", "hegpu.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char\s*\*|int64_t|double)\s+\*?(hegpu_\w+)\(",
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char|int64_t|double)\s*\*?\s*(hegpu_\w+)\(",
                                  text, re.M)))
 
 
@@ -245,6 +249,19 @@ class Context:
     def launches(self):
         return int(lib().hegpu_kernel_launches(self.h))
 
+    def stream_ptr(self):
+        return lib().hegpu_stream(self.h) or 0
+
+    def kernel_timer(self, name):
+        """arm per-launch CUDA-event timing of one kernel (None disables)"""
+        self.check(lib().hegpu_kernel_timer(self.h, name.encode() if name else None))
+
+    def kernel_timer_read(self):
+        """(total device ms, launches, algorithmic bytes) since arming"""
+        ms, n, b = C.c_double(), C.c_int64(), C.c_double()
+        self.check(lib().hegpu_kernel_timer_read(self.h, C.byref(ms), C.byref(n), C.byref(b)))
+        return ms.value, n.value, b.value
+
     def sync(self):
         self.check(lib().hegpu_sync(self.h))
 
@@ -318,6 +335,9 @@ class Ciphertext:
         out = np.empty(self.words, dtype=np.uint64)
         self.ctx.check(lib().hegpu_ct_download(self.h, out.ctypes.data, out.size))
         return out
+
+    def export_device(self, dev_ptr):
+        self.ctx.check(lib().hegpu_ct_export_device(self.h, dev_ptr, self.words))
 
     @property
     def scale(self):
