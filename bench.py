@@ -163,6 +163,7 @@ def run_gpu(args):
     import torch
     import torch.distributed as dist
 
+    from paper_2110_08321_b200 import dist as D
     from paper_2110_08321_b200 import hegpu as H
     from paper_2110_08321_b200.workloads import CFG0, net_image, net_weights
 
@@ -174,9 +175,8 @@ def run_gpu(args):
     B = args.batch
     ctx = H.Context(cfg.log_n, list(cfg.qbits), cfg.pbits, seed=SEED, device=local)
     net = H.Net(ctx, cfg, net_weights(cfg, SEED))
-    # client side (outside the timed region): conv-pack + encrypt B images
-    first = rank * B
-    taps = np.concatenate([net.encrypt_image(net_image(cfg, first + i), nonce=first + i) for i in range(B)])
+    # client side (outside the timed region): conv-pack + encrypt this rank's images
+    taps = np.concatenate([net.encrypt_image(net_image(cfg, i), nonce=i) for i in D.image_range(rank, B)])
     dtaps = ctx.ct(B * net.ntaps, net.top, taps, 2.0 ** 40)
     out = ctx.ct(B, net.out_level)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=local)
@@ -185,10 +185,10 @@ def run_gpu(args):
 
     def step():
         net.run(dtaps, out)
-        if world > 1:  # NCCL gather of the output ciphertexts (config 2)
+        if world > 1:  # NCCL all-gather of the output ciphertexts (config 2)
             out.export_device(gather_buf.data_ptr())
             with torch.cuda.stream(stream):
-                dist.all_gather_into_tensor(gathered, gather_buf)
+                D.gather_outputs(gather_buf, world, gathered)
 
     for _ in range(args.warmup):
         step()
@@ -210,11 +210,7 @@ def run_gpu(args):
         dist.barrier()
     launches = ctx.launches() - l0
     tally = ctx.total()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    t = torch.tensor([ms], device=f"cuda:{local}")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = D.max_over_ranks(ev0.elapsed_time(ev1) / args.steps, device=f"cuda:{local}")
     value = B * world / (ms_max / 1e3)
     per_step_rot = tally[4] / args.steps
     per_step_ks = per_step_rot + ctx.total()[3] / args.steps  # rotations + relinearisations
@@ -256,11 +252,7 @@ def run_gpu(args):
         net.run_host(pin_in, B, pin_out)
     e1.record(stream)
     e1.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / args.steps
-    te = torch.tensor([e2e_ms], device=f"cuda:{local}")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_ms = float(te.item())
+    e2e_ms = D.max_over_ranks(e0.elapsed_time(e1) / args.steps, device=f"cuda:{local}")
     assert np.array_equal(pin_out.numpy().view(np.uint64), host_out), "e2e output differs from device run"
 
     line = {

@@ -246,7 +246,8 @@ __device__ __forceinline__ const ulonglong2* twi(const TwArgs& t, int pi, int N)
   return t.tw + ((size_t)pi * 2 + 1) * N;
 }
 
-#define NTT_BOUNDS __launch_bounds__((1 << LOGN) / kR)
+// two CTAs per SM for N <= 8192 (<= 64 registers per thread)
+#define NTT_BOUNDS __launch_bounds__((1 << LOGN) / kR, (LOGN <= 13 ? 2 : 1))
 
 // ------------------------------------------------------------ kernels
 template <int LOGN>

@@ -1,0 +1,37 @@
+"""Multi-GPU plumbing for the config-2 workload.
+
+Images are independent ciphertext sets, so ranks shard images (weak
+scaling: `per_rank` images each) with keys/masks replicated, and the only
+collective is an all-gather of the output ciphertexts in wire format.
+Backend-agnostic (NCCL on GPUs, gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+
+def image_range(rank: int, per_rank: int):
+    """global image indices (also the encryption nonces) owned by `rank`"""
+    return range(rank * per_rank, (rank + 1) * per_rank)
+
+
+def gather_outputs(local, world: int, out=None):
+    """all-gather the per-rank output ciphertext words (int64 view of the
+    uint64 wire words) into [world * local.numel()] ordered by rank."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return local
+    if out is None:
+        out = torch.empty(world * local.numel(), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, local.contiguous())
+    return out
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    """the step time every rank reports is the max over ranks"""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized():
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
