@@ -64,8 +64,8 @@ typedef struct hegpu_net hegpu_net;
 typedef struct {
   int log_n;                 /* ring degree N = 2^log_n, slots S = N/2 */
   int n_q;                   /* Q chain length L (L-1 rescales) */
-  int q_bits[HEGPU_MAX_Q];   /* bit sizes of q_0..q_{L-1} (<= 61) */
-  int p_bits;                /* special prime P (<= 61) */
+  int q_bits[HEGPU_MAX_Q];   /* bit sizes of q_0..q_{L-1} (<= 60) */
+  int p_bits;                /* special prime P (<= 60) */
   uint64_t seed;             /* secret / key / encryption randomness */
 } hegpu_params;
 

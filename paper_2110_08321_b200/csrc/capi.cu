@@ -86,6 +86,7 @@ void upload_key(Context& c, const std::vector<u64>& wire, DeviceKey& k) {
   if (!k.data) CK(cudaMalloc((void**)&k.data, words * 8));
   const int np = c.P->np();
   launch_wire_to_slot(c, stage, k.data, (size_t)c.L() * 2 * np, 1, np, c.L());
+  launch_split31(c, k.data, words);  // keys are only ever multiply-accumulated
   c.free(stage);
   CK(cudaStreamSynchronize(c.stream));
 }

@@ -193,6 +193,8 @@ int hs_chunk_span();
 void launch_hs_diag(Context& c, const u64d* v, int B, int l, const u64d* D, const HsDiagTable& t,
                     u64d* acc, u64d* cacc);
 void launch_fuse_key(Context& c, const u64d* key, const u64d* mask, int l, u64d* fk);
+// re-pack Montgomery multiplier words x -> (x mod 2^31) | (x >> 31) << 32
+void launch_split31(Context& c, u64d* p, size_t words);
 
 // high-level evaluator (eval.cu)
 void eval_rescale(Context& c, const CtBatch& a, CtBatch& out);

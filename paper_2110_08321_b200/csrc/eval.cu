@@ -101,19 +101,21 @@ __global__ void k_ks_inner(PrimeTable pt, const u64d* __restrict__ D, int l, int
   if (k >= N) return;
   const int pi = t == l ? L : t;
   const DevPrime pr = pt.p[pi];
-  const u64d* key = km.key[b % km.period];
-  const size_t kp = (size_t)(L + 1) * N;  // one key poly over all primes
-  u64d lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
-  uint32_t t0 = 0, t1 = 0;
+  const u64d* key = km.key[b % km.period];  // split-31 Montgomery words
+  const size_t kp = (size_t)(L + 1) * N;    // one key poly over all primes
+  Acc3 a0, a1;
+  a0.zero();
+  a1.zero();
   for (int j = 0; j < l; ++j) {
-    const u64d d = D[(((size_t)b * l + j) * (l + 1) + t) * N + k];
+    const u64d d = split31(D[(((size_t)b * l + j) * (l + 1) + t) * N + k]);
     const u64d* kj = key + (size_t)j * 2 * kp + (size_t)pi * N + k;
-    mad192(lo0, hi0, t0, d, __ldg(kj));
-    mad192(lo1, hi1, t1, d, __ldg(kj + kp));
+    a0.mad(d, __ldg(kj));
+    a1.mad(d, __ldg(kj + kp));
+    if ((j & 3) == 3) a0.fold(), a1.fold();
   }
   u64d* o = acc + ((size_t)b * 2 * (l + 1) + t) * N + k;
-  o[0] = red192(lo0, hi0, t0, pr);
-  o[(size_t)(l + 1) * N] = red192(lo1, hi1, t1, pr);
+  o[0] = a0.reduce(pr);
+  o[(size_t)(l + 1) * N] = a1.reduce(pr);
 }
 
 // conv-pack MAC (convlower.cpp:39-74): CO output maps per thread, taps
@@ -122,41 +124,47 @@ template <int CO>
 __global__ void __launch_bounds__(kTpb) k_conv_mac(PrimeTable pt, const u64d* __restrict__ taps, int ntaps, int l,
                                                    int N, const u64d* __restrict__ w, int c_out,
                                                    const u64d* __restrict__ bias, u64d* __restrict__ out) {
+  extern __shared__ u64d ws[];  // [CO][ntaps] split-31 Montgomery scalars of this (t, group)
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = blockIdx.y % l, poly = blockIdx.y / l;
   const int groups = (c_out + CO - 1) / CO;
   const int b = blockIdx.z / groups, cg = blockIdx.z % groups;
+  const int nco = c_out - cg * CO < CO ? c_out - cg * CO : CO;
+  for (int e = threadIdx.x; e < CO * ntaps; e += blockDim.x) {
+    const int c = e / ntaps, s = e % ntaps;
+    ws[e] = c < nco ? __ldg(w + ((size_t)(cg * CO + c) * ntaps + s) * l + t) : 0ull;
+  }
+  __syncthreads();
   if (k >= N) return;
   const DevPrime pr = pt.p[t];
   const size_t ct_words = (size_t)2 * l * N;
   const u64d* tp = taps + (size_t)b * ntaps * ct_words + (size_t)poly * l * N + (size_t)t * N + k;
-  u64d lo[CO], hi[CO];
-  uint32_t top[CO];
+  Acc3 acc[CO];
 #pragma unroll
-  for (int c = 0; c < CO; ++c) lo[c] = hi[c] = 0, top[c] = 0;
-  const int nco = c_out - cg * CO < CO ? c_out - cg * CO : CO;
+  for (int c = 0; c < CO; ++c) acc[c].zero();
   int s = 0;
-  for (; s + 8 <= ntaps; s += 8) {
-    u64d x[8];
+  // 4 taps in flight per thread; fold every 4 products
+  for (; s + 4 <= ntaps; s += 4) {
+    u64d x[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = __ldg(tp + (size_t)(s + u) * ct_words);
+    for (int u = 0; u < 4; ++u) x[u] = split31(__ldg(tp + (size_t)(s + u) * ct_words));
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int c = 0; c < CO; ++c) {
 #pragma unroll
-      for (int c = 0; c < CO; ++c)
-        if (c < nco) mad192(lo[c], hi[c], top[c], x[u], __ldg(w + ((size_t)(cg * CO + c) * ntaps + s + u) * l + t));
+      for (int u = 0; u < 4; ++u) acc[c].mad(x[u], ws[c * ntaps + s + u]);
+      acc[c].fold();
+    }
   }
   for (; s < ntaps; ++s) {
-    const u64d x = __ldg(tp + (size_t)s * ct_words);
+    const u64d x = split31(__ldg(tp + (size_t)s * ct_words));
 #pragma unroll
-    for (int c = 0; c < CO; ++c)
-      if (c < nco) mad192(lo[c], hi[c], top[c], x, __ldg(w + ((size_t)(cg * CO + c) * ntaps + s) * l + t));
+    for (int c = 0; c < CO; ++c) acc[c].mad(x, ws[c * ntaps + s]);
   }
 #pragma unroll
   for (int c = 0; c < CO; ++c) {
     if (c >= nco) break;
     const int co = cg * CO + c;
-    u64d v = red192(lo[c], hi[c], top[c], pr);
+    u64d v = acc[c].reduce(pr);
     if (poly == 0 && bias)
       v = add_mod_d(v, mont_mul(bias[((size_t)co * l + t) * N + k], 1ull, pr.q, pr.qneg_inv), pr.q);
     out[((size_t)b * c_out + co) * ct_words + (size_t)poly * l * N + (size_t)t * N + k] = v;
@@ -183,101 +191,94 @@ __global__ void __launch_bounds__(kHsKB) k_hs_diag(PrimeTable pt, const u64d* __
                                                    const u64d* __restrict__ D, int B, int L, int N,
                                                    HsDiagTable tab, u64d* __restrict__ acc,
                                                    u64d* __restrict__ cacc) {
-  extern __shared__ u64d win[];  // [BT][LV + 1][W]
+  extern __shared__ u64d win[];  // [BT][LV + 1][kHsW], split-31 words
+  constexpr int kW = kHsKB + kHsCW;  // window row stride (compile-time -> immediate LDS offsets)
   const int S = N >> 1;
-  const int KB = kHsKB < S ? kHsKB : S;
-  const int kb = blockIdx.y, t = blockIdx.z, b0 = blockIdx.x * kHsBT;
-  const int k0 = kb * KB, k = k0 + threadIdx.x;
-  const bool active = threadIdx.x < KB;
+  const int kb = blockIdx.y, t = blockIdx.z >> 1, p = blockIdx.z & 1, b0 = blockIdx.x * kHsBT;
+  const int k0 = kb * kHsKB, k = k0 + threadIdx.x;
   const int half = k0 >= S ? S : 0;
   const int pi = t == LV ? L : t;
   const DevPrime pr = pt.p[pi];
   const bool has_c = t < LV;
-  const int Wmax = KB + kHsCW;
-  const int nrow = has_c ? LV + 1 : LV;  // D digits (+ c0)
-  const size_t ln = (size_t)LV * N;
+  const bool do_c0 = has_c && p == 0;
+  const int nrow = do_c0 ? LV + 1 : LV;  // D digits (+ c0)
+  const int ln = LV * N, kp = (LV + 1) * N;
 
-  u64d a_lo[kHsBT][2], a_hi[kHsBT][2], c_lo[kHsBT][2], c_hi[kHsBT][2];
-  uint32_t a_tp[kHsBT][2], c_tp[kHsBT][2];
+  Acc3 a[kHsBT], c[kHsBT];
 #pragma unroll
-  for (int bb = 0; bb < kHsBT; ++bb)
-#pragma unroll
-    for (int p = 0; p < 2; ++p) a_lo[bb][p] = a_hi[bb][p] = c_lo[bb][p] = c_hi[bb][p] = 0, a_tp[bb][p] = c_tp[bb][p] = 0;
+  for (int bb = 0; bb < kHsBT; ++bb) a[bb].zero(), c[bb].zero();
 
+  const u64d* mrow = tab.masks + (size_t)t * N + k;
   for (int ch = 0; ch < tab.nchunk; ++ch) {
     const int i0 = __ldg(tab.chunk + ch), i1 = __ldg(tab.chunk + ch + 1);
     const int r_lo = __ldg(tab.r + i0), r_hi = __ldg(tab.r + i1 - 1);
-    const int W = KB + r_hi - r_lo;
-    // stage window positions k0 - r_hi + w (mod S, inside this half)
+    const int W = kHsKB + r_hi - r_lo;
+    // stage window positions k0 - r_hi + w (mod S, inside this half), split
     __syncthreads();
-    for (int e = threadIdx.x; e < kHsBT * nrow * W; e += blockDim.x) {
-      const int w = e % W, rb = e / W, row = rb % nrow, bb = rb / nrow;
-      const int b = b0 + bb;
-      int pos = k0 - half - r_hi + w;
-      pos %= S;
-      if (pos < 0) pos += S;
-      pos += half;
-      u64d val = 0;
-      if (b < B)
-        val = row < LV ? D[(((size_t)b * LV + row) * (LV + 1) + t) * N + pos]
-                       : v[(size_t)b * 2 * ln + (size_t)t * N + pos];
-      win[(size_t)(bb * (LV + 1) + row) * Wmax + w] = val;
+    for (int row = 0; row < kHsBT * nrow; ++row) {
+      const int bb = row / nrow, rr = row % nrow, b = b0 + bb;
+      const u64d* src = b >= B ? nullptr
+                        : rr < LV ? D + (((size_t)b * LV + rr) * (LV + 1) + t) * N
+                                  : v + (size_t)b * 2 * ln + (size_t)t * N;
+      u64d* dst = win + (bb * (LV + 1) + rr) * kW;
+      for (int w = threadIdx.x; w < W; w += kHsKB) {
+        int pos = k0 - half - r_hi + w;
+        if (pos < 0) pos += S;
+        dst[w] = src ? split31(src[half + pos]) : 0ull;
+      }
     }
     __syncthreads();
-    if (!active) continue;
+    const u64d* wb = win + threadIdx.x + r_hi;
     for (int i = i0; i < i1; ++i) {
       const int r = __ldg(tab.r + i);
-      const int wo = threadIdx.x + (r_hi - r);
-      const u64d m = has_c ? __ldg(tab.masks + ((size_t)i * (LV + 1) + t) * N + k) : 0ull;
-      if (r == 0) {
-        if (has_c) {
+      const u64d* wp = wb - r;  // + (bb * (LV + 1) + row) * kW, compile-time below
+      if (do_c0) {
+        const u64d m = __ldg(mrow + (size_t)i * kp);
 #pragma unroll
-          for (int bb = 0; bb < kHsBT; ++bb) {
-            const int b = b0 + bb;
-            if (b >= B) break;
-            mad192(c_lo[bb][0], c_hi[bb][0], c_tp[bb][0], win[(size_t)(bb * (LV + 1) + LV) * Wmax + wo], m);
-            mad192(c_lo[bb][1], c_hi[bb][1], c_tp[bb][1], v[(size_t)b * 2 * ln + ln + (size_t)t * N + k], m);
+        for (int bb = 0; bb < kHsBT; ++bb) c[bb].mad(wp[(bb * (LV + 1) + LV) * kW], m);
+      }
+      if (r != 0) {
+        const u64d* fk = tab.fkeys[i] + p * kp + t * N + k;
+        u64d kv[LV];
+#pragma unroll
+        for (int j = 0; j < LV; ++j) kv[j] = __ldg(fk + j * 2 * kp);
+#pragma unroll
+        for (int bb = 0; bb < kHsBT; ++bb) {
+#pragma unroll
+          for (int j = 0; j < LV; ++j) {
+            a[bb].mad(wp[(bb * (LV + 1) + j) * kW], kv[j]);
+            if ((j & 3) == 3) a[bb].fold();
           }
+          if (LV & 3) a[bb].fold();
         }
-        continue;
       }
-      const u64d* fk = tab.fkeys[i] + (size_t)t * N + k;
-      const size_t kp = (size_t)(LV + 1) * N;
-      u64d kv[LV][2];
+      if (do_c0 && ((i - i0) & 3) == 3) {
 #pragma unroll
-      for (int j = 0; j < LV; ++j) {
-        kv[j][0] = __ldg(fk + (size_t)j * 2 * kp);
-        kv[j][1] = __ldg(fk + (size_t)j * 2 * kp + kp);
-      }
-#pragma unroll
-      for (int bb = 0; bb < kHsBT; ++bb) {
-#pragma unroll
-        for (int j = 0; j < LV; ++j) {
-          const u64d d = win[(size_t)(bb * (LV + 1) + j) * Wmax + wo];
-          mad192(a_lo[bb][0], a_hi[bb][0], a_tp[bb][0], d, kv[j][0]);
-          mad192(a_lo[bb][1], a_hi[bb][1], a_tp[bb][1], d, kv[j][1]);
-        }
-        if (has_c) mad192(c_lo[bb][0], c_hi[bb][0], c_tp[bb][0], win[(size_t)(bb * (LV + 1) + LV) * Wmax + wo], m);
+        for (int bb = 0; bb < kHsBT; ++bb) c[bb].fold();
       }
     }
+#pragma unroll
+    for (int bb = 0; bb < kHsBT; ++bb) c[bb].fold();
   }
-  if (!active) return;
+  // r == 0 diagonal (if kept) is the only contributor to the c1 part
+  u64d m0 = 0;
+  const bool c1_term = has_c && p == 1 && tab.ndiag > 0 && __ldg(tab.r) == 0;
+  if (c1_term) m0 = unsplit31(__ldg(tab.masks + (size_t)t * N + k));
 #pragma unroll
   for (int bb = 0; bb < kHsBT; ++bb) {
     const int b = b0 + bb;
     if (b >= B) break;
-    u64d* ab = acc + (size_t)b * 2 * (LV + 1) * N + (size_t)t * N + k;
-    ab[0] = red192(a_lo[bb][0], a_hi[bb][0], a_tp[bb][0], pr);
-    ab[(size_t)(LV + 1) * N] = red192(a_lo[bb][1], a_hi[bb][1], a_tp[bb][1], pr);
+    acc[(size_t)b * 2 * kp + (size_t)p * kp + (size_t)t * N + k] = a[bb].reduce(pr);
     if (has_c) {
-      u64d* cb = cacc + (size_t)b * 2 * ln + (size_t)t * N + k;
-      cb[0] = red192(c_lo[bb][0], c_hi[bb][0], c_tp[bb][0], pr);
-      cb[ln] = red192(c_lo[bb][1], c_hi[bb][1], c_tp[bb][1], pr);
+      u64d* cb = cacc + (size_t)b * 2 * ln + (size_t)p * ln + (size_t)t * N + k;
+      if (p == 0) *cb = c[bb].reduce(pr);
+      else *cb = c1_term ? mont_mul(v[(size_t)b * 2 * ln + ln + (size_t)t * N + k], m0, pr.q, pr.qneg_inv) : 0ull;
     }
   }
 }
 
-// fused key: fk[j][p][t] = key[j][p][pi(t)] * m[t]   (t over the ext basis)
+// fused key: fk[j][p][t] = key[j][p][pi(t)] * m[t]   (t over the ext basis);
+// key, mask and result are split-31 Montgomery words
 __global__ void k_fuse_key(PrimeTable pt, const u64d* __restrict__ key, const u64d* __restrict__ m, int l, int L,
                            int N, u64d* __restrict__ fk) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -285,8 +286,15 @@ __global__ void k_fuse_key(PrimeTable pt, const u64d* __restrict__ key, const u6
   if (k >= N) return;
   const int pi = t == l ? L : t;
   const DevPrime pr = pt.p[pi];
-  const u64d kv = key[((size_t)jp * (L + 1) + pi) * N + k];
-  fk[((size_t)jp * (l + 1) + t) * N + k] = mont_mul(kv, m[(size_t)t * N + k], pr.q, pr.qneg_inv);
+  const u64d kv = unsplit31(key[((size_t)jp * (L + 1) + pi) * N + k]);
+  const u64d mv = unsplit31(m[(size_t)t * N + k]);
+  fk[((size_t)jp * (l + 1) + t) * N + k] = split31(mont_mul(kv, mv, pr.q, pr.qneg_inv));
+}
+
+// in-place split-31 re-packing of Montgomery multiplier tables
+__global__ void k_split31(u64d* __restrict__ p, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = split31(p[i]);
 }
 
 unsigned grid_for(size_t total) {
@@ -297,9 +305,9 @@ unsigned grid_for(size_t total) {
 template <int LV>
 void launch_hs_lv(Context& c, const u64d* v, int B, const u64d* D, const HsDiagTable& t, u64d* acc, u64d* cacc) {
   const int N = c.N(), S = N / 2;
-  const int KB = kHsKB < S ? kHsKB : S;
-  dim3 grid((B + kHsBT - 1) / kHsBT, N / KB, LV + 1);
-  const size_t sm = (size_t)kHsBT * (LV + 1) * (KB + kHsCW) * 8;
+  if (S < kHsKB) fail(HEGPU_ERR_ARG, "hs_matvec on the device needs N >= 256");
+  dim3 grid((B + kHsBT - 1) / kHsBT, N / kHsKB, 2 * (LV + 1));
+  const size_t sm = (size_t)kHsBT * (LV + 1) * (kHsKB + kHsCW) * 8;
   static size_t done = 0;
   if (sm > 48 * 1024 && sm > done) {
     CK(cudaFuncSetAttribute(k_hs_diag<LV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -350,15 +358,31 @@ void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, cons
                      const u64d* bias, u64d* out) {
   // taps read once, maps written once, bias plaintexts read once
   const double bytes = 8.0 * c.N() * l * (2.0 * B * ntaps + 2.0 * B * c_out + c_out);
-  if (c_out <= 4) {
-    dim3 grid((c.N() + kTpb - 1) / kTpb, 2 * l, B * ((c_out + 3) / 4));
-    LAUNCH_B(c, "k_conv_mac", bytes,
-           k_conv_mac<4><<<grid, kTpb, 0, c.stream>>>(c.primes, taps, ntaps, l, c.N(), w, c_out, bias, out));
-  } else {
-    dim3 grid((c.N() + kTpb - 1) / kTpb, 2 * l, B * ((c_out + 7) / 8));
-    LAUNCH_B(c, "k_conv_mac", bytes,
-           k_conv_mac<8><<<grid, kTpb, 0, c.stream>>>(c.primes, taps, ntaps, l, c.N(), w, c_out, bias, out));
+  const int co = c_out < 8 ? c_out : 8;  // output maps per thread (exact for c_out <= 8)
+  dim3 grid((c.N() + kTpb - 1) / kTpb, 2 * l, B * ((c_out + co - 1) / co));
+  const size_t sm = (size_t)co * ntaps * 8;
+  if (sm > 200 * 1024) fail(HEGPU_ERR_CAPACITY, "conv_packed_forward: too many taps");
+#define CONV_GO(CO)                                                                                        \
+  case CO: {                                                                                               \
+    static size_t done = 0;                                                                                \
+    if (sm > 48 * 1024 && sm > done) {                                                                     \
+      CK(cudaFuncSetAttribute(k_conv_mac<CO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));      \
+      done = sm;                                                                                           \
+    }                                                                                                      \
+    LAUNCH_B(c, "k_conv_mac", bytes,                                                                       \
+             k_conv_mac<CO><<<grid, kTpb, sm, c.stream>>>(c.primes, taps, ntaps, l, c.N(), w, c_out, bias, out)); \
+    break;                                                                                                 \
   }
+  switch (co) {
+    CONV_GO(1) CONV_GO(2) CONV_GO(3) CONV_GO(4) CONV_GO(5) CONV_GO(6) CONV_GO(7) CONV_GO(8)
+    default: fail(HEGPU_ERR_ARG, "conv: bad c_out");
+  }
+#undef CONV_GO
+}
+
+void launch_split31(Context& c, u64d* p, size_t words) {
+  if (!words) return;
+  LAUNCH_B(c, "k_split31", 16.0 * words, k_split31<<<grid_for(words), kTpb, 0, c.stream>>>(p, words));
 }
 
 void launch_fuse_key(Context& c, const u64d* key, const u64d* mask, int l, u64d* fk) {

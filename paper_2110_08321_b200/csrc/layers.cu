@@ -55,7 +55,8 @@ ConvLayer::ConvLayer(Context& c, int nt, int co_n, const double* weights, const 
       const double x = std::rint(weights[(size_t)co * ntaps + t] * (double)qlast);
       for (int li = 0; li < level; ++li) {
         const u64 q = P.q(li);
-        w[((size_t)co * ntaps + t) * level + li] = mul_mod(residue_of_double(x, q), P.primes[li].r_mod, q);
+        const u64 wm = mul_mod(residue_of_double(x, q), P.primes[li].r_mod, q);  // Montgomery form
+        w[((size_t)co * ntaps + t) * level + li] = (wm & 0x7FFFFFFFull) | ((wm >> 31) << 32);  // split-31
       }
     }
   CK(cudaMalloc((void**)&this->w, w.size() * 8));
@@ -161,6 +162,8 @@ void HsPlan::build(Context& c, const double* A, int m_, int n_, int lvl, bool sk
   if (!kept.empty()) {
     CK(cudaMalloc((void**)&masks, wire.size() * 8));
     upload_mont(c, wire, masks, kept.size() * nl, nl, level);
+    launch_split31(c, masks, wire.size());
+    CK(cudaStreamSynchronize(c.stream));
   }
   // right rotations (ascending) and chunks whose r span fits one smem window
   std::vector<int> r(diag.size()), chunk{0};

@@ -70,4 +70,73 @@ __device__ __forceinline__ u64d reduce64(u64d x, const DevPrime& p) {
   return mont_mul(x, p.r_mod, p.q, p.qneg_inv);
 }
 
+// Shoup product with an approximate quotient: the high word of a * w' is
+// formed from the three leading 32x32 partial products only (3 IMAD.WIDE
+// instead of a full 64x64 high product), so the quotient is low by at most
+// 2 and the result lies in [0, 4q) for any a < 2^64 (q < 2^61).
+__device__ __forceinline__ u64d shoup_mul_lazy4(u64d a, u64d w, u64d wp, u64d q) {
+  const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32);
+  const uint32_t w0 = (uint32_t)wp, w1 = (uint32_t)(wp >> 32);
+  u64d h;
+  asm("{\n\t.reg .u64 t1, t2;\n\t"
+      "mul.wide.u32 t1, %1, %3;\n\t"   // a1 * w0'
+      "mul.wide.u32 t2, %2, %4;\n\t"   // a0 * w1'
+      "shr.u64 t1, t1, 32;\n\t"
+      "shr.u64 t2, t2, 32;\n\t"
+      "add.u64 t1, t1, t2;\n\t"
+      "mad.wide.u32 %0, %1, %4, t1;\n\t"  // + a1 * w1'
+      "}"
+      : "=l"(h)
+      : "r"(a1), "r"(a0), "r"(w0), "r"(w1));
+  return a * w - h * q;
+}
+
+// ---- 31-bit split operands for multiply-accumulate ------------------------
+// A residue x < 2^61 is stored "split" as x0 | x1 << 32 with x0 = x mod 2^31,
+// x1 = x >> 31 (< 2^30).  A product of two split operands is four 32x32->64
+// IMAD.WIDE partial products accumulated carry-free:
+//   s0 += x0 y0 (< 2^62)   s1 += x0 y1 + x1 y0 (< 2^62)   s2 += x1 y1 (< 2^60)
+// so up to 4 products fit before folding into a 192-bit total.
+__device__ __forceinline__ u64d split31(u64d x) { return (x & 0x7FFFFFFFull) | ((x >> 31) << 32); }
+__device__ __forceinline__ u64d unsplit31(u64d s) { return (s & 0xFFFFFFFFull) + ((s >> 32) << 31); }
+
+struct Acc3 {  // s0 + s1 2^31 + s2 2^62 (partial), folded into lo:hi:top
+  u64d s0, s1, s2, lo, hi;
+  uint32_t top;
+  __device__ __forceinline__ void zero() { s0 = s1 = s2 = lo = hi = 0; top = 0; }
+  __device__ __forceinline__ void mad(u64d xs, u64d ys) {
+    const uint32_t x0 = (uint32_t)xs, x1 = (uint32_t)(xs >> 32);
+    const uint32_t y0 = (uint32_t)ys, y1 = (uint32_t)(ys >> 32);
+    asm("mad.wide.u32 %0, %3, %5, %0;\n\t"
+        "mad.wide.u32 %1, %3, %6, %1;\n\t"
+        "mad.wide.u32 %1, %4, %5, %1;\n\t"
+        "mad.wide.u32 %2, %4, %6, %2;\n\t"
+        : "+l"(s0), "+l"(s1), "+l"(s2)
+        : "r"(x0), "r"(x1), "r"(y0), "r"(y1));
+  }
+  __device__ __forceinline__ void fold() {
+    const u64d l1 = s1 << 31, h1 = s1 >> 33, l2 = s2 << 62, h2 = s2 >> 2;
+    asm("add.cc.u64 %0, %0, %3;\n\t"
+        "addc.cc.u64 %1, %1, 0;\n\t"
+        "addc.u32 %2, %2, 0;\n\t"
+        "add.cc.u64 %0, %0, %4;\n\t"
+        "addc.cc.u64 %1, %1, %5;\n\t"
+        "addc.u32 %2, %2, 0;\n\t"
+        "add.cc.u64 %0, %0, %6;\n\t"
+        "addc.cc.u64 %1, %1, %7;\n\t"
+        "addc.u32 %2, %2, 0;\n\t"
+        : "+l"(lo), "+l"(hi), "+r"(top)
+        : "l"(s0), "l"(l1), "l"(h1), "l"(l2), "l"(h2));
+    s0 = s1 = s2 = 0;
+  }
+  // (top:hi:lo) * 2^-64 mod q  (products of standard x Montgomery operands)
+  __device__ __forceinline__ u64d reduce(const DevPrime& pr) {
+    fold();
+    u64d x = mont_reduce128(hi, (u64d)top, pr.q, pr.qneg_inv);
+    x = mont_mul(x, pr.r2_mod, pr.q, pr.qneg_inv);
+    const u64d y = mont_reduce128(lo, 0ull, pr.q, pr.qneg_inv);
+    return add_mod_d(x, y, pr.q);
+  }
+};
+
 }  // namespace hegpu

@@ -59,7 +59,7 @@ __device__ __forceinline__ int fwd_idx(int g, int j) {
 template <int LOGN, int S0, int RR>
 __device__ __forceinline__ void fwd_pass(u64d (&x)[kR], const ulonglong2* __restrict__ tw, u64d q) {
   constexpr int T = (1 << LOGN) / kR, G = kR >> RR, J = 1 << RR, LOB = LOGN - S0 - RR;
-  const u64d q2 = 2 * q;
+  const u64d q4 = 4 * q;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const int hi = (g * T + (int)threadIdx.x) >> LOB;
@@ -70,11 +70,12 @@ __device__ __forceinline__ void fwd_pass(u64d (&x)[kR], const ulonglong2* __rest
       for (int j = 0; j < J; ++j) {
         if (j & half) continue;
         const ulonglong2 W = __ldg(tw + (1 << (S0 + u)) + (hi << u) + (j >> (RR - u)));
+        // values in [0, 8q) (q < 2^60): one conditional subtraction per butterfly
         u64d a = x[g * J + j];
-        if (a >= q2) a -= q2;
-        const u64d t = shoup_mul_lazy(x[g * J + j + half], W.x, W.y, q);
+        if (a >= q4) a -= q4;
+        const u64d t = shoup_mul_lazy4(x[g * J + j + half], W.x, W.y, q);  // [0, 4q)
         x[g * J + j] = a + t;
-        x[g * J + j + half] = a - t + q2;
+        x[g * J + j + half] = a - t + q4;
       }
     }
   }
@@ -108,10 +109,11 @@ __device__ __forceinline__ void fwd_passes(u64d (&x)[kR], u64d* sm, const ulongl
     __syncthreads();
     fwd_passes<LOGN, S0 + RR>(x, sm, tw, q);
   } else {
-    const u64d q2 = 2 * q;
+    const u64d q2 = 2 * q, q4 = 4 * q;
 #pragma unroll
-    for (int e = 0; e < kR; ++e) {
+    for (int e = 0; e < kR; ++e) {  // [0, 8q) -> [0, q)
       u64d v = x[e];
+      if (v >= q4) v -= q4;
       if (v >= q2) v -= q2;
       if (v >= q) v -= q;
       x[e] = v;
@@ -147,7 +149,7 @@ __device__ __forceinline__ int inv_idx(int g, int j) {
 template <int LOGN, int S0, int RR>
 __device__ __forceinline__ void inv_pass(u64d (&x)[kR], const ulonglong2* __restrict__ tw, u64d q) {
   constexpr int T = (1 << LOGN) / kR, G = kR >> RR, J = 1 << RR;
-  const u64d q2 = 2 * q;
+  const u64d q4 = 4 * q;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const int hi = (g * T + (int)threadIdx.x) >> S0;
@@ -158,11 +160,12 @@ __device__ __forceinline__ void inv_pass(u64d (&x)[kR], const ulonglong2* __rest
       for (int j = 0; j < J; ++j) {
         if (j & dist) continue;
         const ulonglong2 W = __ldg(tw + (1 << (LOGN - S0 - u - 1)) + (hi << (RR - u - 1)) + (j >> (u + 1)));
+        // values in [0, 4q): one conditional subtraction per butterfly
         const u64d a = x[g * J + j], b = x[g * J + j + dist];
         u64d s = a + b;
-        if (s >= q2) s -= q2;
+        if (s >= q4) s -= q4;
         x[g * J + j] = s;
-        x[g * J + j + dist] = shoup_mul_lazy(a - b + q2, W.x, W.y, q);
+        x[g * J + j + dist] = shoup_mul_lazy4(a - b + q4, W.x, W.y, q);  // [0, 4q)
       }
     }
   }

@@ -73,7 +73,8 @@ Params::Params(const hegpu_params& p) {
   // largest unused primes below 2^bits with q == 1 (mod 2N), in request order
   for (int i = 0; i <= L; ++i) {
     const int bits = i < L ? p.q_bits[i] : p.p_bits;
-    if (bits <= log_n + 1 || bits > 61) fail(HEGPU_ERR_ARG, "prime bit size out of range");
+    // <= 60 bits: the lazy NTT keeps values below 8q < 2^63
+    if (bits <= log_n + 1 || bits > 60) fail(HEGPU_ERR_ARG, "prime bit size out of range (<= 60)");
     u64 c = (1ULL << bits) - (u64)m2n + 1;
     for (;; c -= (u64)m2n) {
       bool used = false;
