@@ -120,7 +120,7 @@ extern "C" int hegpu_ctx_create(const hegpu_params* p, int device, hegpu_ctx** o
     const int np = c.P->np(), N = c.P->n;
     for (int i = 0; i < np; ++i) {
       const Prime& pr = c.P->primes[i];
-      c.primes.p[i] = DevPrime{pr.q, pr.qneg_inv, pr.r_mod, pr.r2_mod};
+      c.primes.p[i] = DevPrime{pr.q, pr.qneg_inv, pr.r_mod, pr.r2_mod, shoup_pre(1, pr.q)};
     }
     upload_twiddles(c);
     std::vector<u64> consts((size_t)2 * np + (size_t)2 * np * np);

@@ -187,7 +187,7 @@ constexpr int kHsCW = 128;  // max r span of a chunk
 constexpr int kHsBT = 4;    // images per thread
 
 template <int LV>
-__global__ void __launch_bounds__(kHsKB) k_hs_diag(PrimeTable pt, const u64d* __restrict__ v,
+__global__ void __launch_bounds__(kHsKB, 4) k_hs_diag(PrimeTable pt, const u64d* __restrict__ v,
                                                    const u64d* __restrict__ D, int B, int L, int N,
                                                    HsDiagTable tab, u64d* __restrict__ acc,
                                                    u64d* __restrict__ cacc) {
@@ -229,19 +229,35 @@ __global__ void __launch_bounds__(kHsKB) k_hs_diag(PrimeTable pt, const u64d* __
     }
     __syncthreads();
     const u64d* wb = win + threadIdx.x + r_hi;
+    // software pipeline: the fused-key words and mask of diagonal i + 1 are
+    // in flight while diagonal i is accumulated
+    u64d kn[LV], mn = 0;
+    int rn = __ldg(tab.r + i0);
+    {
+      const u64d* fk = rn ? tab.fkeys[i0] + p * kp + t * N + k : nullptr;
+#pragma unroll
+      for (int j = 0; j < LV; ++j) kn[j] = fk ? __ldg(fk + j * 2 * kp) : 0ull;
+      if (do_c0) mn = __ldg(mrow + (size_t)i0 * kp);
+    }
     for (int i = i0; i < i1; ++i) {
-      const int r = __ldg(tab.r + i);
+      const int r = rn;
+      u64d kv[LV];
+#pragma unroll
+      for (int j = 0; j < LV; ++j) kv[j] = kn[j];
+      const u64d m = mn;
+      if (i + 1 < i1) {
+        rn = __ldg(tab.r + i + 1);
+        const u64d* fk = rn ? tab.fkeys[i + 1] + p * kp + t * N + k : nullptr;
+#pragma unroll
+        for (int j = 0; j < LV; ++j) kn[j] = fk ? __ldg(fk + j * 2 * kp) : 0ull;
+        if (do_c0) mn = __ldg(mrow + (size_t)(i + 1) * kp);
+      }
       const u64d* wp = wb - r;  // + (bb * (LV + 1) + row) * kW, compile-time below
       if (do_c0) {
-        const u64d m = __ldg(mrow + (size_t)i * kp);
 #pragma unroll
         for (int bb = 0; bb < kHsBT; ++bb) c[bb].mad(wp[(bb * (LV + 1) + LV) * kW], m);
       }
       if (r != 0) {
-        const u64d* fk = tab.fkeys[i] + p * kp + t * N + k;
-        u64d kv[LV];
-#pragma unroll
-        for (int j = 0; j < LV; ++j) kv[j] = __ldg(fk + j * 2 * kp);
 #pragma unroll
         for (int bb = 0; bb < kHsBT; ++bb) {
 #pragma unroll

@@ -20,6 +20,7 @@ struct DevPrime {
   u64d qneg_inv;  // -q^{-1} mod 2^64
   u64d r_mod;     // 2^64 mod q (to_mont of 1; reduce via mont_mul(x, r_mod))
   u64d r2_mod;    // 2^128 mod q
+  u64d one_sh;    // floor(2^64 / q): Shoup companion of 1 (lazy x mod q)
 };
 
 #define HEGPU_MAX_PRIMES 16
@@ -89,6 +90,11 @@ __device__ __forceinline__ u64d shoup_mul_lazy4(u64d a, u64d w, u64d wp, u64d q)
       : "=l"(h)
       : "r"(a1), "r"(a0), "r"(w0), "r"(w1));
   return a * w - h * q;
+}
+
+// lazy reduction of any x < 2^64 into [0, 4q): x - floor~(x / q) q
+__device__ __forceinline__ u64d reduce_lazy4(u64d x, const DevPrime& p) {
+  return shoup_mul_lazy4(x, 1ull, p.one_sh, p.q);
 }
 
 // ---- 31-bit split operands for multiply-accumulate ------------------------

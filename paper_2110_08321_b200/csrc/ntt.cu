@@ -24,8 +24,10 @@ namespace hegpu {
 
 namespace {
 
-constexpr int kLogR = 4;
-constexpr int kR = 1 << kLogR;
+// registers per thread: R = 2^lr words.  R = 16 measured faster than R = 32
+// on B200 (2 CTAs x 512 threads per SM for N = 2^13 beat 2 x 256 threads
+// with 128 registers each; profiles/r01_notes.md)
+__host__ __device__ constexpr int lr_of(int logn) { return logn > 0 ? 4 : 4; }
 constexpr int kMinLogN = 5, kMaxLogN = 14;
 
 __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
@@ -51,14 +53,14 @@ struct TwArgs {
 // group grp = g * T + tid splits into (hi, lo).
 template <int LOGN, int S0, int RR>
 __device__ __forceinline__ int fwd_idx(int g, int j) {
-  constexpr int T = (1 << LOGN) / kR, LOB = LOGN - S0 - RR;
+  constexpr int T = (1 << LOGN) / (1 << lr_of(LOGN)), LOB = LOGN - S0 - RR;
   const int grp = g * T + (int)threadIdx.x;
   return ((grp >> LOB) << (LOGN - S0)) + (j << LOB) + (grp & ((1 << LOB) - 1));
 }
 
 template <int LOGN, int S0, int RR>
-__device__ __forceinline__ void fwd_pass(u64d (&x)[kR], const ulonglong2* __restrict__ tw, u64d q) {
-  constexpr int T = (1 << LOGN) / kR, G = kR >> RR, J = 1 << RR, LOB = LOGN - S0 - RR;
+__device__ __forceinline__ void fwd_pass(u64d (&x)[1 << lr_of(LOGN)], const ulonglong2* __restrict__ tw, u64d q) {
+  constexpr int T = (1 << LOGN) / (1 << lr_of(LOGN)), G = (1 << lr_of(LOGN)) >> RR, J = 1 << RR, LOB = LOGN - S0 - RR;
   const u64d q4 = 4 * q;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -82,27 +84,27 @@ __device__ __forceinline__ void fwd_pass(u64d (&x)[kR], const ulonglong2* __rest
 }
 
 template <int LOGN, int S0, int RR>
-__device__ __forceinline__ void fwd_store(u64d* sm, const u64d (&x)[kR]) {
+__device__ __forceinline__ void fwd_store(u64d* sm, const u64d (&x)[1 << lr_of(LOGN)]) {
 #pragma unroll
-  for (int g = 0; g < (kR >> RR); ++g)
+  for (int g = 0; g < ((1 << lr_of(LOGN)) >> RR); ++g)
 #pragma unroll
     for (int j = 0; j < (1 << RR); ++j) sm[pad(fwd_idx<LOGN, S0, RR>(g, j))] = x[g * (1 << RR) + j];
 }
 
 template <int LOGN, int S0, int RR>
-__device__ __forceinline__ void fwd_load(const u64d* sm, u64d (&x)[kR]) {
+__device__ __forceinline__ void fwd_load(const u64d* sm, u64d (&x)[1 << lr_of(LOGN)]) {
 #pragma unroll
-  for (int g = 0; g < (kR >> RR); ++g)
+  for (int g = 0; g < ((1 << lr_of(LOGN)) >> RR); ++g)
 #pragma unroll
     for (int j = 0; j < (1 << RR); ++j) x[g * (1 << RR) + j] = sm[pad(fwd_idx<LOGN, S0, RR>(g, j))];
 }
 
 template <int LOGN, int S0>
-__device__ __forceinline__ void fwd_passes(u64d (&x)[kR], u64d* sm, const ulonglong2* tw, u64d q) {
-  constexpr int RR = cmin(kLogR, LOGN - S0);
+__device__ __forceinline__ void fwd_passes(u64d (&x)[1 << lr_of(LOGN)], u64d* sm, const ulonglong2* tw, u64d q) {
+  constexpr int RR = cmin(lr_of(LOGN), LOGN - S0);
   fwd_pass<LOGN, S0, RR>(x, tw, q);
   if constexpr (S0 + RR < LOGN) {
-    constexpr int RN = cmin(kLogR, LOGN - S0 - RR);
+    constexpr int RN = cmin(lr_of(LOGN), LOGN - S0 - RR);
     fwd_store<LOGN, S0, RR>(sm, x);
     __syncthreads();
     fwd_load<LOGN, S0 + RR, RN>(sm, x);
@@ -111,7 +113,7 @@ __device__ __forceinline__ void fwd_passes(u64d (&x)[kR], u64d* sm, const ulongl
   } else {
     const u64d q2 = 2 * q, q4 = 4 * q;
 #pragma unroll
-    for (int e = 0; e < kR; ++e) {  // [0, 8q) -> [0, q)
+    for (int e = 0; e < (1 << lr_of(LOGN)); ++e) {  // [0, 8q) -> [0, q)
       u64d v = x[e];
       if (v >= q4) v -= q4;
       if (v >= q2) v -= q2;
@@ -127,10 +129,10 @@ __device__ __forceinline__ void fwd_passes(u64d (&x)[kR], u64d* sm, const ulongl
 // bit-reversed index order), CTA synchronised on return
 template <int LOGN, class Ld>
 __device__ __forceinline__ void fwd_transform(u64d* sm, const Ld& ld, const ulonglong2* tw, u64d q) {
-  constexpr int R0 = cmin(kLogR, LOGN);
-  u64d x[kR];
+  constexpr int R0 = cmin(lr_of(LOGN), LOGN);
+  u64d x[1 << lr_of(LOGN)];
 #pragma unroll
-  for (int g = 0; g < (kR >> R0); ++g)
+  for (int g = 0; g < ((1 << lr_of(LOGN)) >> R0); ++g)
 #pragma unroll
     for (int j = 0; j < (1 << R0); ++j) x[g * (1 << R0) + j] = ld.load(fwd_idx<LOGN, 0, R0>(g, j));
   fwd_passes<LOGN, 0>(x, sm, tw, q);
@@ -141,14 +143,14 @@ __device__ __forceinline__ void fwd_transform(u64d* sm, const Ld& ld, const ulon
 // e = g * 2^RR + j sits at hi * 2^(S0 + RR) + j * 2^S0 + lo.
 template <int LOGN, int S0, int RR>
 __device__ __forceinline__ int inv_idx(int g, int j) {
-  constexpr int T = (1 << LOGN) / kR;
+  constexpr int T = (1 << LOGN) / (1 << lr_of(LOGN));
   const int grp = g * T + (int)threadIdx.x;
   return ((grp >> S0) << (S0 + RR)) + (j << S0) + (grp & ((1 << S0) - 1));
 }
 
 template <int LOGN, int S0, int RR>
-__device__ __forceinline__ void inv_pass(u64d (&x)[kR], const ulonglong2* __restrict__ tw, u64d q) {
-  constexpr int T = (1 << LOGN) / kR, G = kR >> RR, J = 1 << RR;
+__device__ __forceinline__ void inv_pass(u64d (&x)[1 << lr_of(LOGN)], const ulonglong2* __restrict__ tw, u64d q) {
+  constexpr int T = (1 << LOGN) / (1 << lr_of(LOGN)), G = (1 << lr_of(LOGN)) >> RR, J = 1 << RR;
   const u64d q4 = 4 * q;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -172,28 +174,28 @@ __device__ __forceinline__ void inv_pass(u64d (&x)[kR], const ulonglong2* __rest
 }
 
 template <int LOGN, int S0, int RR>
-__device__ __forceinline__ void inv_store(u64d* sm, const u64d (&x)[kR]) {
+__device__ __forceinline__ void inv_store(u64d* sm, const u64d (&x)[1 << lr_of(LOGN)]) {
 #pragma unroll
-  for (int g = 0; g < (kR >> RR); ++g)
+  for (int g = 0; g < ((1 << lr_of(LOGN)) >> RR); ++g)
 #pragma unroll
     for (int j = 0; j < (1 << RR); ++j) sm[pad(inv_idx<LOGN, S0, RR>(g, j))] = x[g * (1 << RR) + j];
 }
 
 template <int LOGN, int S0, int RR>
-__device__ __forceinline__ void inv_load(const u64d* sm, u64d (&x)[kR]) {
+__device__ __forceinline__ void inv_load(const u64d* sm, u64d (&x)[1 << lr_of(LOGN)]) {
 #pragma unroll
-  for (int g = 0; g < (kR >> RR); ++g)
+  for (int g = 0; g < ((1 << lr_of(LOGN)) >> RR); ++g)
 #pragma unroll
     for (int j = 0; j < (1 << RR); ++j) x[g * (1 << RR) + j] = sm[pad(inv_idx<LOGN, S0, RR>(g, j))];
 }
 
 template <int LOGN, int S0, class St>
-__device__ __forceinline__ void inv_passes(u64d (&x)[kR], u64d* sm, const ulonglong2* tw, u64d q, u64d nv,
+__device__ __forceinline__ void inv_passes(u64d (&x)[1 << lr_of(LOGN)], u64d* sm, const ulonglong2* tw, u64d q, u64d nv,
                                            u64d nvp, St& st) {
-  constexpr int RR = cmin(kLogR, LOGN - S0);
+  constexpr int RR = cmin(lr_of(LOGN), LOGN - S0);
   inv_pass<LOGN, S0, RR>(x, tw, q);
   if constexpr (S0 + RR < LOGN) {
-    constexpr int RN = cmin(kLogR, LOGN - S0 - RR);
+    constexpr int RN = cmin(lr_of(LOGN), LOGN - S0 - RR);
     __syncthreads();
     inv_store<LOGN, S0, RR>(sm, x);
     __syncthreads();
@@ -201,7 +203,7 @@ __device__ __forceinline__ void inv_passes(u64d (&x)[kR], u64d* sm, const ulongl
     inv_passes<LOGN, S0 + RR>(x, sm, tw, q, nv, nvp, st);
   } else {
 #pragma unroll
-    for (int g = 0; g < (kR >> RR); ++g)
+    for (int g = 0; g < ((1 << lr_of(LOGN)) >> RR); ++g)
 #pragma unroll
       for (int j = 0; j < (1 << RR); ++j)
         st.store(inv_idx<LOGN, S0, RR>(g, j), shoup_mul_d(x[g * (1 << RR) + j], nv, nvp, q));
@@ -212,8 +214,8 @@ __device__ __forceinline__ void inv_passes(u64d (&x)[kR], u64d* sm, const ulongl
 // canonical) and synchronised; st.store(k, v) receives N^{-1} * INTT.
 template <int LOGN, class St>
 __device__ __forceinline__ void inv_transform(u64d* sm, St& st, const ulonglong2* tw, u64d q, u64d nv, u64d nvp) {
-  constexpr int R0 = cmin(kLogR, LOGN);
-  u64d x[kR];
+  constexpr int R0 = cmin(lr_of(LOGN), LOGN);
+  u64d x[1 << lr_of(LOGN)];
   inv_load<LOGN, 0, R0>(sm, x);
   inv_passes<LOGN, 0>(x, sm, tw, q, nv, nvp, st);
 }
@@ -223,18 +225,28 @@ struct LdPlain {
   const u64d* p;
   __device__ u64d load(int k) const { return p[k]; }
 };
-struct LdReduce {
+// NTT inputs may be lazy (< 8q), so digit lifts only reduce when the source
+// prime exceeds the target prime, and then only into [0, 4q).
+struct LdReduce {  // residue mod q_src (< q_src) into the target prime
   const u64d* p;
   DevPrime pr;
-  __device__ u64d load(int k) const { return reduce64(p[k], pr); }
+  bool need;  // q_src > q
+  __device__ u64d load(int k) const {
+    const u64d x = p[k];
+    return need ? reduce_lazy4(x, pr) : x;
+  }
 };
-struct LdLift {  // centered lift of a residue mod qd into q
+struct LdLift {  // centered lift of a residue mod qd into q: (-qd/2, qd/2] -> [0, 4q]
   const u64d* p;
   DevPrime pr;
   u64d qd;
+  bool need;  // qd / 2 >= q
   __device__ u64d load(int k) const {
     const u64d x = p[k];
-    return x > (qd >> 1) ? sub_mod_d(0, reduce64(qd - x, pr), pr.q) : reduce64(x, pr);
+    const bool neg = x > (qd >> 1);
+    u64d y = neg ? qd - x : x;
+    if (need) y = reduce_lazy4(y, pr);
+    return neg ? 4 * pr.q - y : y;
   }
 };
 struct StPlain {
@@ -250,7 +262,7 @@ __device__ __forceinline__ const ulonglong2* twi(const TwArgs& t, int pi, int N)
 }
 
 // two CTAs per SM for N <= 8192 (<= 64 registers per thread)
-#define NTT_BOUNDS __launch_bounds__((1 << LOGN) / kR, (LOGN <= 13 ? 2 : 1))
+#define NTT_BOUNDS __launch_bounds__((1 << LOGN) / (1 << lr_of(LOGN)), (LOGN <= 13 ? 2 : 1))
 
 // ------------------------------------------------------------ kernels
 template <int LOGN>
@@ -317,7 +329,7 @@ __global__ void NTT_BOUNDS k_ks_modup(TwArgs ta, PrimeTable pt, const u64d* __re
   const int t = tp < j ? tp : tp + 1;
   const int pi = t == l ? P_index : t;
   const DevPrime pr = pt.p[pi];
-  fwd_transform<LOGN>(sm, LdReduce{tmp + ((size_t)b * l + j) * N, pr}, twf(ta, pi, N), pr.q);
+  fwd_transform<LOGN>(sm, LdReduce{tmp + ((size_t)b * l + j) * N, pr, pt.p[j].q > pr.q}, twf(ta, pi, N), pr.q);
   u64d* d = D + (((size_t)b * l + j) * (l + 1) + t) * N;
   for (int p = threadIdx.x; p < N; p += blockDim.x) d[p] = sm[pad(__ldg(ta.slot_src + p))];
 }
@@ -332,7 +344,8 @@ __global__ void NTT_BOUNDS k_drop_ntt(TwArgs ta, PrimeTable pt, const u64d* __re
   const int t = r % a.nl, bp = r / a.nl, p = bp % 2, b = bp / 2;
   const DevPrime pr = pt.p[t];
   const u64d q = pr.q;
-  fwd_transform<LOGN>(sm, LdLift{tmpP + ((size_t)b * 2 + p) * N, pr, pt.p[a.pd].q}, twf(ta, t, N), q);
+  const u64d qd = pt.p[a.pd].q;
+  fwd_transform<LOGN>(sm, LdLift{tmpP + ((size_t)b * 2 + p) * N, pr, qd, (qd >> 1) >= q}, twf(ta, t, N), q);
   const u64d iv = qinv[((size_t)t * np_all + a.pd) * 2], ivp = qinv[((size_t)t * np_all + a.pd) * 2 + 1];
   const u64d* in = a.src + b * a.src_b + p * a.src_p + (size_t)t * N;
   u64d* out = a.dst + b * a.dst_b + p * a.dst_p + (size_t)t * N;
@@ -376,7 +389,7 @@ __global__ void k_slot_to_wire(const u64d* __restrict__ src, u64d* __restrict__ 
 }
 
 TwArgs tw_args(Context& c) { return TwArgs{(const ulonglong2*)c.d_tw, c.ninv_tab(), c.d_slot_src}; }
-int ntt_threads(int N) { return N / kR; }
+
 size_t ntt_smem(int N) { return (size_t)(N + (N >> 4) + 1) * 8; }
 
 template <typename K>
@@ -407,7 +420,7 @@ void prep_kernel(K kernel, size_t bytes) {
     static bool prepared = false;                                                                   \
     const size_t smb = ntt_smem(1 << LG);                                                           \
     if (!prepared) { prep_kernel(KERNEL<LG>, smb); prepared = true; }                                \
-    LAUNCH_B(c, #KERNEL, _ntt_bytes, KERNEL<LG><<<(GRID), (1 << LG) / kR, smb, c.stream>>>(__VA_ARGS__)); \
+    LAUNCH_B(c, #KERNEL, _ntt_bytes, KERNEL<LG><<<(GRID), (1 << LG) >> lr_of(LG), smb, c.stream>>>(__VA_ARGS__)); \
   } while (0)
 
 }  // namespace
