@@ -89,6 +89,14 @@ int64_t hegpu_kernel_launches(const hegpu_ctx* ctx);
  * re-arms it. */
 int hegpu_kernel_timer(hegpu_ctx* ctx, const char* name);
 int hegpu_kernel_timer_read(hegpu_ctx* ctx, double* total_ms, int64_t* launches, double* alg_bytes);
+/* CUDA-graph capture of everything the context enqueues between begin and
+ * end (e.g. one hegpu_net_run); replay with hegpu_graph_launch.  Metering
+ * and launch counters advance only while capturing. */
+typedef struct hegpu_graph hegpu_graph;
+int hegpu_capture_begin(hegpu_ctx* ctx);
+int hegpu_capture_end(hegpu_ctx* ctx, hegpu_graph** out);
+int hegpu_graph_launch(hegpu_graph* g);
+void hegpu_graph_destroy(hegpu_graph* g);
 /* the cudaStream_t every kernel of this context is launched on (for
  * caller-side CUDA-event timing); NULL for a client-only context */
 void* hegpu_stream(const hegpu_ctx* ctx);
@@ -113,6 +121,12 @@ int hegpu_decode(hegpu_ctx* ctx, const uint64_t* pt, int level, double scale, do
 /* pack(values, n_slots, Ciphertext): symmetric encryption of an encoded pt */
 int hegpu_encrypt(hegpu_ctx* ctx, const uint64_t* pt, int level, uint64_t nonce, uint64_t* ct);
 int hegpu_decrypt(hegpu_ctx* ctx, const uint64_t* ct, int level, uint64_t* pt);
+/* compact fresh ciphertext: the `level` a-stream keys (u64), then c0 limb i
+ * byte-packed in ceil(bits(q_i)/8) bytes per coefficient (wire order); c1 is
+ * regenerated from the stream keys on upload -- bit-identical to
+ * hegpu_encrypt's output, 2.9x fewer bytes for the config-0 chain */
+size_t hegpu_compact_bytes(const hegpu_ctx* ctx, int level);
+int hegpu_encrypt_compact(hegpu_ctx* ctx, const uint64_t* pt, int level, uint64_t nonce, uint8_t* out);
 /* Galois keys for right rotations by r (slotvec.cpp:42-57 semantics) and the
  * relinearisation key; generated on the host, stored on the device */
 int hegpu_gen_rotation_keys(hegpu_ctx* ctx, const int64_t* right_rots, int n);
@@ -126,6 +140,8 @@ int hegpu_ct_create(hegpu_ctx* ctx, int count, int level, hegpu_ct** out);
 void hegpu_ct_destroy(hegpu_ct* ct);
 int hegpu_ct_upload(hegpu_ct* ct, const uint64_t* host, size_t nwords, double scale);
 int hegpu_ct_download(hegpu_ct* ct, uint64_t* host, size_t nwords);
+/* upload `count` compact ciphertexts (hegpu_encrypt_compact) back to back */
+int hegpu_ct_upload_compact(hegpu_ct* ct, const uint8_t* host, size_t nbytes, double scale);
 int hegpu_ct_info(const hegpu_ct* ct, int* count, int* level, double* scale);
 int hegpu_pt_create(hegpu_ctx* ctx, int count, int level, int with_p, hegpu_pt** out);
 void hegpu_pt_destroy(hegpu_pt* pt);
@@ -190,6 +206,13 @@ int hegpu_net_run_host(hegpu_net* net, const uint64_t* host_taps, int batch, uin
 /* client helper: conv_pack (convlower.cpp:9-37) + encode + encrypt of one
  * image [in_c][in_d][in_d] -> ntaps wire ciphertexts at the top level */
 int hegpu_net_encrypt_image(hegpu_net* net, const double* image, uint64_t nonce, uint64_t* taps_out);
+/* the same taps in compact form (hegpu_net_compact_image_bytes per image) */
+size_t hegpu_net_compact_image_bytes(const hegpu_net* net);
+int hegpu_net_encrypt_image_compact(hegpu_net* net, const double* image, uint64_t nonce, uint8_t* taps_out);
+/* end-to-end run from compact host taps [batch][ntaps] -> output cts (wire);
+ * the batch is processed in chunks of `chunk` images (0 = automatic) with the
+ * next chunk's host->device copy overlapping the current chunk's compute */
+int hegpu_net_run_host_compact(hegpu_net* net, const uint8_t* host_taps, int batch, int chunk, uint64_t* host_out);
 /* logits: decrypt + decode output ct (wire) into m_last values */
 int hegpu_net_decrypt_logits(hegpu_net* net, const uint64_t* out_ct, double* logits);
 double hegpu_net_output_scale(const hegpu_net* net);

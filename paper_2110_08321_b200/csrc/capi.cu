@@ -184,6 +184,47 @@ extern "C" int64_t hegpu_kernel_launches(const hegpu_ctx* h) { return h ? h->c.l
 
 extern "C" void* hegpu_stream(const hegpu_ctx* h) { return h ? (void*)h->c.stream : nullptr; }
 
+struct hegpu_graph {
+  Context* c;
+  cudaGraph_t g;
+  cudaGraphExec_t exec;
+};
+
+extern "C" int hegpu_capture_begin(hegpu_ctx* h) {
+  if (!h) return HEGPU_ERR_ARG;
+  Context& c = h->c;
+  return guarded(&c, [&] {
+    need_gpu(c);
+    CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+  });
+}
+
+extern "C" int hegpu_capture_end(hegpu_ctx* h, hegpu_graph** out) {
+  if (!h || !out) return HEGPU_ERR_ARG;
+  Context& c = h->c;
+  return guarded(&c, [&] {
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamEndCapture(c.stream, &g));
+    cudaGraphExec_t exec = nullptr;
+    CK(cudaGraphInstantiate(&exec, g, 0));
+    *out = new hegpu_graph{&c, g, exec};
+  });
+}
+
+extern "C" int hegpu_graph_launch(hegpu_graph* gr) {
+  if (!gr) return HEGPU_ERR_ARG;
+  Context& c = *gr->c;
+  return guarded(&c, [&] { CK(cudaGraphLaunch(gr->exec, c.stream)); });
+}
+
+extern "C" void hegpu_graph_destroy(hegpu_graph* gr) {
+  if (!gr) return;
+  cudaStreamSynchronize(gr->c->stream);
+  cudaGraphExecDestroy(gr->exec);
+  cudaGraphDestroy(gr->g);
+  delete gr;
+}
+
 extern "C" int hegpu_kernel_timer(hegpu_ctx* h, const char* name) {
   if (!h) return HEGPU_ERR_ARG;
   h->c.ktimer_name = name ? name : "";
@@ -281,6 +322,19 @@ extern "C" int hegpu_decrypt(hegpu_ctx* h, const uint64_t* ct, int level, uint64
   });
 }
 
+extern "C" size_t hegpu_compact_bytes(const hegpu_ctx* h, int level) {
+  if (!h || level < 1 || level > h->c.L()) return 0;
+  return h->c.client->compact_bytes(level);
+}
+
+extern "C" int hegpu_encrypt_compact(hegpu_ctx* h, const uint64_t* pt, int level, uint64_t nonce, uint8_t* out) {
+  if (!h || !pt || !out) return HEGPU_ERR_ARG;
+  return guarded(&h->c, [&] {
+    need(level >= 1 && level <= h->c.L(), HEGPU_ERR_ARG, "encrypt_compact: bad level");
+    h->c.client->encrypt_compact(pt, level, nonce, out);
+  });
+}
+
 extern "C" int hegpu_gen_rotation_keys(hegpu_ctx* h, const int64_t* rots, int n) {
   if (!h || (n && !rots)) return HEGPU_ERR_ARG;
   Context& c = h->c;
@@ -371,6 +425,21 @@ extern "C" int hegpu_ct_download(hegpu_ct* t, uint64_t* host, size_t nwords) {
     launch_slot_to_wire(c, t->b.d, stage, (size_t)t->b.count * 2 * t->b.level, 0, t->b.level, -1);
     CK(cudaMemcpyAsync(host, stage, nwords * 8, cudaMemcpyDeviceToHost, c.stream));
     c.free(stage);
+    CK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+extern "C" int hegpu_ct_upload_compact(hegpu_ct* t, const uint8_t* host, size_t nbytes, double scale) {
+  if (!t || !host) return HEGPU_ERR_ARG;
+  Context& c = *t->b.ctx;
+  return guarded(&c, [&] {
+    const size_t per = c.client->compact_bytes(t->b.level);
+    need(nbytes == per * t->b.count, HEGPU_ERR_SHAPE, "ct_upload_compact: byte count mismatch");
+    u64d* stage = c.alloc((nbytes + 7) / 8);
+    CK(cudaMemcpyAsync(stage, host, nbytes, cudaMemcpyHostToDevice, c.stream));
+    launch_expand_compact(c, (const uint8_t*)stage, t->b.count, t->b.level, t->b.d);
+    c.free(stage);
+    t->b.scale = scale;
     CK(cudaStreamSynchronize(c.stream));
   });
 }

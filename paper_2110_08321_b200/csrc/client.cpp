@@ -181,6 +181,27 @@ void Client::encrypt(const u64* pt, int level, u64 nonce, u64* ct) const {
   }
 }
 
+size_t Client::compact_bytes(int level) const {
+  size_t n = (size_t)level * 8;
+  for (int i = 0; i < level; ++i) n += (size_t)P_.n * limb_bytes(i);
+  return n;
+}
+
+void Client::encrypt_compact(const u64* pt, int level, u64 nonce, uint8_t* out) const {
+  const int N = P_.n;
+  std::vector<u64> ct((size_t)2 * level * N);
+  encrypt(pt, level, nonce, ct.data());
+  u64* keys = reinterpret_cast<u64*>(out);
+  for (int t = 0; t < level; ++t) keys[t] = Stream(P_.seed, tag_enc(nonce, 0, (u64)t)).key;
+  uint8_t* o = out + (size_t)level * 8;
+  for (int t = 0; t < level; ++t) {
+    const int nb = limb_bytes(t);
+    const u64* c0 = ct.data() + (size_t)t * N;
+    for (int k = 0; k < N; ++k)
+      for (int b = 0; b < nb; ++b) *o++ = (uint8_t)(c0[k] >> (8 * b));
+  }
+}
+
 void Client::decrypt(const u64* ct, int level, u64* pt) const {
   const int N = P_.n;
   for (int t = 0; t < level; ++t) {

@@ -115,6 +115,13 @@ class Client {
   void encode(const double* z, int len, double scale, int level, bool with_p, u64* out) const;
   void decode(const u64* pt, int level, double scale, double* slots) const;
   void encrypt(const u64* pt, int level, u64 nonce, u64* ct) const;
+  // compact fresh ciphertext: the level a-stream keys, then
+  // c0 limb i packed in ceil(bits(q_i) / 8) bytes per coefficient; c1 = a is
+  // regenerated from the stream keys on the device.  Expands to exactly the
+  // ciphertext encrypt() produces.
+  size_t compact_bytes(int level) const;
+  void encrypt_compact(const u64* pt, int level, u64 nonce, uint8_t* out) const;
+  int limb_bytes(int i) const { return (64 - __builtin_clzll(P_.q(i)) + 7) / 8; }
   void decrypt(const u64* ct, int level, u64* pt) const;
   // key-switching key s' -> s, wire layout [L][2][L+1][N]
   void gen_ksk(u64 kind, u64 g, const u64* sprime, u64* key) const;

@@ -9,6 +9,7 @@
 // merge at L-1; every Square and every Dense consumes one prime.
 // masked_prefix (netcompile.cpp:424) is elided: the next HS masks are zero
 // beyond n (matvec.cpp:57-61) and logits are read from slots 0..m-1.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -28,9 +29,23 @@ struct hegpu_net {
   std::vector<HsPlan> plans;
   std::vector<u64d*> bias;   // per dense layer, [level][N] Montgomery
   std::vector<double> bias_scale;
+  // host-input pipeline (hegpu_net_run_host_compact): double-buffered
+  // compact staging, a copy stream and its events
+  uint8_t* stage[2] = {nullptr, nullptr};
+  size_t stage_bytes = 0;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t copied[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> sub_events;  // one per input sub-chunk
   ~hegpu_net() {
     for (auto& p : plans) p.release();
     for (u64d* b : bias) cudaFree(b);
+    for (int s = 0; s < 2; ++s) {
+      if (stage[s]) cudaFree(stage[s]);
+      if (copied[s]) cudaEventDestroy(copied[s]);
+      if (freed[s]) cudaEventDestroy(freed[s]);
+    }
+    for (cudaEvent_t e : sub_events) cudaEventDestroy(e);
+    if (copy) cudaStreamDestroy(copy);
   }
 };
 
@@ -61,20 +76,35 @@ struct Scratch {
   ~Scratch() { c.free(p); }
 };
 
-void run_net(hegpu_net& net, const CtBatch& taps, CtBatch& out) {
+// Conv1: ConvPack (netcompile.cpp:321-331); maps [B][c_out] at top-1
+void run_conv(hegpu_net& net, const CtBatch& taps, CtBatch& maps) {
   Context& c = *net.c;
   const hegpu_net_spec& s = net.spec;
-  const int B = taps.count / net.ntaps, N = c.N();
-  int l = net.top;
-  // Conv1: ConvPack (netcompile.cpp:321-331)
+  const int B = taps.count / net.ntaps;
   c.meter.begin("Conv1");
-  Scratch maps(c, (size_t)B * s.c_out * 2 * (l - 1) * N);
-  CtBatch mb{&c, B * s.c_out, l - 1, 0, maps.p};
-  net.conv->run(c, taps, mb);
+  net.conv->run(c, taps, maps);
   c.meter.bump(HEGPU_MUL_PC, (int64_t)B * net.ntaps * s.c_out);
   c.meter.bump(HEGPU_ADD_CC, (int64_t)B * (net.ntaps - 1) * s.c_out);
   c.meter.bump(HEGPU_ADD_PC, (int64_t)B * s.c_out);
-  --l;
+}
+
+void run_after_conv(hegpu_net& net, const CtBatch& mb, CtBatch& out);
+
+void run_net(hegpu_net& net, const CtBatch& taps, CtBatch& out) {
+  Context& c = *net.c;
+  const int B = taps.count / net.ntaps;
+  Scratch maps(c, (size_t)B * net.spec.c_out * 2 * (net.top - 1) * c.N());
+  CtBatch mb{&c, B * net.spec.c_out, net.top - 1, 0, maps.p};
+  run_conv(net, taps, mb);
+  run_after_conv(net, mb, out);
+}
+
+// Flat1 onwards, on the conv-layer maps
+void run_after_conv(hegpu_net& net, const CtBatch& mb, CtBatch& out) {
+  Context& c = *net.c;
+  const hegpu_net_spec& s = net.spec;
+  const int B = mb.count / s.c_out, N = c.N();
+  int l = mb.level;
   // Flat1: Merge (netcompile.cpp:332-347)
   c.meter.begin("Flat1");
   Scratch cur(c, (size_t)B * 2 * l * N);
@@ -217,6 +247,101 @@ extern "C" int hegpu_net_run_host(hegpu_net* net, const uint64_t* host_taps, int
     launch_slot_to_wire(c, o.p, stage.p, (size_t)batch * 2 * lo, 0, lo, -1);
     CK(cudaMemcpyAsync(host_out, stage.p, out_words * 8, cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+extern "C" size_t hegpu_net_compact_image_bytes(const hegpu_net* net) {
+  return net ? (size_t)net->ntaps * net->c->client->compact_bytes(net->top) : 0;
+}
+
+extern "C" int hegpu_net_run_host_compact(hegpu_net* net, const uint8_t* host, int batch, int chunk,
+                                          uint64_t* host_out) {
+  if (!net || !host || !host_out || batch < 1) return HEGPU_ERR_ARG;
+  Context& c = *net->c;
+  return guarded(&c, [&] {
+    const int N = c.N(), L = net->top, lo = net->top - 1 - 2 * net->spec.n_dense;
+    // two-level pipeline: the copy stream streams every image's compact taps
+    // in sub-chunks of c1 images; the compute stream expands + convolves each
+    // sub-chunk as soon as it lands, and runs merge..Dense on chunks of c2.
+    const int c2 = chunk > 0 ? std::min(chunk, batch) : std::min(batch, 32);
+    const int c1 = std::min(c2, 4);
+    const size_t per_img = hegpu_net_compact_image_bytes(net);
+    const size_t out_words = (size_t)2 * lo * N;
+    const size_t map_words = (size_t)2 * (L - 1) * N;
+    if (net->stage_bytes < per_img * batch) {
+      CK(cudaStreamSynchronize(c.stream));
+      if (net->stage[0]) cudaFree(net->stage[0]);
+      CK(cudaMalloc((void**)&net->stage[0], per_img * batch));
+      net->stage_bytes = per_img * batch;
+    }
+    if (!net->copy) {
+      CK(cudaStreamCreateWithFlags(&net->copy, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&net->freed[0], cudaEventDisableTiming));
+    }
+    const int nsub = (batch + c1 - 1) / c1;
+    while ((int)net->sub_events.size() < nsub) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      net->sub_events.push_back(e);
+    }
+    // staging is reused across calls: copies start once earlier compute is done
+    CK(cudaEventRecord(net->freed[0], c.stream));
+    CK(cudaStreamWaitEvent(net->copy, net->freed[0], 0));
+    for (int j = 0; j < nsub; ++j) {
+      const int b0 = j * c1, nb = std::min(c1, batch - b0);
+      CK(cudaMemcpyAsync(net->stage[0] + (size_t)b0 * per_img, host + (size_t)b0 * per_img, per_img * nb,
+                         cudaMemcpyHostToDevice, net->copy));
+      CK(cudaEventRecord(net->sub_events[j], net->copy));
+    }
+    Scratch taps(c, (size_t)c1 * net->ntaps * 2 * L * N);
+    Scratch maps(c, (size_t)c2 * net->spec.c_out * map_words);
+    Scratch o(c, (size_t)c2 * out_words);
+    Scratch wire(c, (size_t)c2 * out_words);
+    for (int m0 = 0; m0 < batch; m0 += c2) {
+      const int nm = std::min(c2, batch - m0);
+      for (int b0 = m0; b0 < m0 + nm; b0 += c1) {
+        const int nb = std::min(c1, m0 + nm - b0);
+        CK(cudaStreamWaitEvent(c.stream, net->sub_events[b0 / c1], 0));
+        launch_expand_compact(c, net->stage[0] + (size_t)b0 * per_img, nb * net->ntaps, L, taps.p);
+        CtBatch tb{&c, nb * net->ntaps, L, net->tap_scale, taps.p};
+        CtBatch mb{&c, nb * net->spec.c_out, L - 1, 0, maps.p + (size_t)(b0 - m0) * net->spec.c_out * map_words};
+        run_conv(*net, tb, mb);
+      }
+      CtBatch mb{&c, nm * net->spec.c_out, L - 1, net->tap_scale, maps.p};
+      CtBatch ob{&c, nm, lo, 0, o.p};
+      run_after_conv(*net, mb, ob);
+      launch_slot_to_wire(c, o.p, wire.p, (size_t)nm * 2 * lo, 0, lo, -1);
+      CK(cudaMemcpyAsync(host_out + (size_t)m0 * out_words, wire.p, (size_t)nm * out_words * 8,
+                         cudaMemcpyDeviceToHost, c.stream));
+    }
+    CK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+extern "C" int hegpu_net_encrypt_image_compact(hegpu_net* net, const double* image, uint64_t nonce,
+                                               uint8_t* taps_out) {
+  if (!net || !image || !taps_out) return HEGPU_ERR_ARG;
+  Context& c = *net->c;
+  return guarded(&c, [&] {
+    const int L = net->top;
+    const size_t per = c.client->compact_bytes(L);
+    // same conv_pack + encode as hegpu_net_encrypt_image, same nonces: the
+    // compact taps expand to exactly those ciphertexts
+    std::vector<double> z(net->w_used);
+    std::vector<u64> pt((size_t)L * c.N());
+    const hegpu_net_spec& s = net->spec;
+    const int d = net->d_out;
+    for (int ci = 0; ci < s.in_c; ++ci)
+      for (int ky = 0; ky < s.k; ++ky)
+        for (int kx = 0; kx < s.k; ++kx) {
+          const int t = (ci * s.k + ky) * s.k + kx;
+          for (int oy = 0; oy < d; ++oy)
+            for (int ox = 0; ox < d; ++ox)
+              z[oy * d + ox] = image[((size_t)ci * s.in_d + oy * s.stride + ky) * s.in_d + ox * s.stride + kx];
+          c.client->encode(z.data(), net->w_used, net->tap_scale, L, false, pt.data());
+          c.client->encrypt_compact(pt.data(), L, nonce * (uint64_t)net->ntaps + (uint64_t)t,
+                                    taps_out + (size_t)t * per);
+        }
   });
 }
 

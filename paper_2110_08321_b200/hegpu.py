@@ -77,6 +77,10 @@ def lib():
             "hegpu_sync": (i, [vp]),
             "hegpu_kernel_launches": (C.c_int64, [vp]),
             "hegpu_stream": (vp, [vp]),
+            "hegpu_capture_begin": (i, [vp]),
+            "hegpu_capture_end": (i, [vp, pp]),
+            "hegpu_graph_launch": (i, [vp]),
+            "hegpu_graph_destroy": (None, [vp]),
             "hegpu_kernel_timer": (i, [vp, C.c_char_p]),
             "hegpu_kernel_timer_read": (i, [vp, C.POINTER(d), C.POINTER(C.c_int64), C.POINTER(d)]),
             "hegpu_ct_export_device": (i, [vp, vp, sz]),
@@ -123,6 +127,12 @@ def lib():
             "hegpu_net_encrypt_image": (i, [vp, f64p, u, u64p]),
             "hegpu_net_decrypt_logits": (i, [vp, u64p, f64p]),
             "hegpu_net_output_scale": (d, [vp]),
+            "hegpu_compact_bytes": (sz, [vp, i]),
+            "hegpu_encrypt_compact": (i, [vp, u64p, i, u, vp]),
+            "hegpu_ct_upload_compact": (i, [vp, vp, sz, d]),
+            "hegpu_net_compact_image_bytes": (sz, [vp]),
+            "hegpu_net_encrypt_image_compact": (i, [vp, f64p, u, vp]),
+            "hegpu_net_run_host_compact": (i, [vp, vp, i, i, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -137,7 +147,7 @@ def declared_symbols():
     import re
     root = os.path.dirname(_HERE)
     text = open(os.path.join(root, "include", "hegpu.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char|int64_t|double)\s*\*?\s*(hegpu_\w+)\(",
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char|int64_t|double|size_t)\s*\*?\s*(hegpu_\w+)\(",
                                  text, re.M)))
 
 
@@ -196,6 +206,15 @@ class Context:
         self.check(lib().hegpu_encrypt(self.h, np.ascontiguousarray(pt, dtype=np.uint64), level, nonce, ct))
         return ct
 
+    def compact_bytes(self, level):
+        return int(lib().hegpu_compact_bytes(self.h, level))
+
+    def encrypt_compact(self, pt, level, nonce):
+        out = np.empty(self.compact_bytes(level), dtype=np.uint8)
+        self.check(lib().hegpu_encrypt_compact(self.h, np.ascontiguousarray(pt, dtype=np.uint64), level, nonce,
+                                               out.ctypes.data))
+        return out
+
     def decrypt(self, ct, level):
         pt = np.empty(level * self.N, dtype=np.uint64)
         self.check(lib().hegpu_decrypt(self.h, np.ascontiguousarray(ct, dtype=np.uint64), level, pt))
@@ -251,6 +270,17 @@ class Context:
 
     def stream_ptr(self):
         return lib().hegpu_stream(self.h) or 0
+
+    def capture(self, fn):
+        """capture everything fn() enqueues into a CUDA graph; returns a
+        replay callable (metering advances only during capture)"""
+        self.check(lib().hegpu_capture_begin(self.h))
+        try:
+            fn()
+        finally:
+            g = C.c_void_p()
+            self.check(lib().hegpu_capture_end(self.h, C.byref(g)))
+        return Graph(self, g)
 
     def kernel_timer(self, name):
         """arm per-launch CUDA-event timing of one kernel (None disables)"""
@@ -314,6 +344,22 @@ class Context:
         return out
 
 
+class Graph:
+    def __init__(self, ctx, h):
+        self.ctx, self.h = ctx, h
+
+    def __call__(self):
+        self.ctx.check(lib().hegpu_graph_launch(self.h))
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().hegpu_graph_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
 class Ciphertext:
     def __init__(self, ctx, count, level, data=None, scale=1.0):
         self.ctx, self.count, self.level = ctx, count, level
@@ -335,6 +381,10 @@ class Ciphertext:
         out = np.empty(self.words, dtype=np.uint64)
         self.ctx.check(lib().hegpu_ct_download(self.h, out.ctypes.data, out.size))
         return out
+
+    def upload_compact(self, data, scale=1.0):
+        data = np.ascontiguousarray(data, dtype=np.uint8)
+        self.ctx.check(lib().hegpu_ct_upload_compact(self.h, data.ctypes.data, data.size, scale))
 
     def export_device(self, dev_ptr):
         self.ctx.check(lib().hegpu_ct_export_device(self.h, dev_ptr, self.words))
@@ -454,6 +504,22 @@ class Net:
         pi = host_taps.ctypes.data if isinstance(host_taps, np.ndarray) else host_taps.data_ptr()
         po = host_out.ctypes.data if isinstance(host_out, np.ndarray) else host_out.data_ptr()
         self.ctx.check(lib().hegpu_net_run_host(self.h, pi, batch, po))
+
+    @property
+    def compact_image_bytes(self):
+        return int(lib().hegpu_net_compact_image_bytes(self.h))
+
+    def encrypt_image_compact(self, image, nonce):
+        out = np.empty(self.compact_image_bytes, dtype=np.uint8)
+        self.ctx.check(lib().hegpu_net_encrypt_image_compact(
+            self.h, np.ascontiguousarray(image, dtype=np.float64).ravel(), nonce, out.ctypes.data))
+        return out
+
+    def run_host_compact(self, host_taps, batch, host_out, chunk=0):
+        """compact taps (uint8, pinned or numpy) -> output wire cts; pipelined chunks"""
+        pi = host_taps.ctypes.data if isinstance(host_taps, np.ndarray) else host_taps.data_ptr()
+        po = host_out.ctypes.data if isinstance(host_out, np.ndarray) else host_out.data_ptr()
+        self.ctx.check(lib().hegpu_net_run_host_compact(self.h, pi, batch, chunk, po))
 
     def decrypt_logits(self, out_ct):
         m = self.cfg.dense[-1]

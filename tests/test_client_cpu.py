@@ -69,6 +69,33 @@ def test_encode_encrypt_bit_exact(log_n, qbits, pbits):
     assert np.abs(d1 - d2).max() < 1e-9
 
 
+def unpack_compact(ctx, blob, level):
+    """host-side reference unpacking of the compact format (c0 only)"""
+    off = 8 * level
+    c0 = []
+    for t in range(level):
+        nb = (int(ctx.primes[t]).bit_length() + 7) // 8
+        raw = blob[off:off + nb * ctx.N].reshape(ctx.N, nb).astype(np.uint64)
+        c0.append(sum(raw[:, b] << np.uint64(8 * b) for b in range(nb)))
+        off += nb * ctx.N
+    assert off == len(blob)
+    return np.concatenate(c0)
+
+
+@pytest.mark.parametrize("log_n,qbits,pbits", PARAMS)
+def test_compact_encryption_matches_full(log_n, qbits, pbits):
+    ctx = H.Context(log_n, qbits, pbits, seed=17, device=H.CLIENT_ONLY)
+    L = len(qbits)
+    pt = ctx.encode(np.random.default_rng(1).uniform(-1, 1, ctx.S), 2.0 ** 40, L)
+    full = ctx.encrypt(pt, L, nonce=5)
+    blob = ctx.encrypt_compact(pt, L, nonce=5)
+    assert len(blob) == ctx.compact_bytes(L)
+    assert np.array_equal(unpack_compact(ctx, blob, L), full[: L * ctx.N])
+    # config 0: 33 bytes per coefficient instead of 96
+    if qbits == [60, 40, 40, 40, 40, 40]:
+        assert len(blob) == 8 * L + ctx.N * (8 + 5 * 5)
+
+
 def test_edge_encodings():
     ctx = H.Context(6, [60, 40], 60, seed=1, device=H.CLIENT_ONLY)
     ck = Ckks(6, [60, 40], 60, seed=1)

@@ -42,6 +42,20 @@ def test_upload_download_roundtrip(pair):
     assert np.array_equal(dp.download(), p)
 
 
+def test_compact_upload_regenerates_c1(pair):
+    """compact taps (c0 + a-stream keys) expand on the device to exactly the
+    oracle's fresh ciphertexts"""
+    ctx, ck = pair
+    rng = np.random.default_rng(11)
+    L = ck.L
+    pts = [ck.encode(rng.uniform(-1, 1, ck.S), DELTA, L) for _ in range(3)]
+    blob = np.concatenate([ctx.encrypt_compact(p, L, nonce=40 + i) for i, p in enumerate(pts)])
+    d = ctx.ct(3, L)
+    d.upload_compact(blob, DELTA)
+    want = np.concatenate([ck.encrypt(p, L, 40 + i) for i, p in enumerate(pts)])
+    assert np.array_equal(d.download(), want)
+
+
 def test_add_mul_plain(pair):
     ctx, ck = pair
     rng = np.random.default_rng(1)
@@ -258,6 +272,21 @@ def test_cfg0_run_host_matches_device_run(cfg0):
     net.run_host(taps, B, host_out)
     out = ctx.ct(B, net.out_level)
     net.run(ctx.ct(B * net.ntaps, net.top, taps, DELTA), out)
+    assert np.array_equal(host_out, out.download())
+
+
+@pytest.mark.parametrize("chunk", [0, 2, 5])
+def test_cfg0_run_host_compact_pipeline(cfg0, chunk):
+    """e2e path: compact taps, chunked H2D/compute pipeline == device run"""
+    cfg, ctx, ck, w, net = cfg0
+    B = 5
+    imgs = [net_image(cfg, 30 + s) for s in range(B)]
+    compact = np.concatenate([net.encrypt_image_compact(im, nonce=30 + s) for s, im in enumerate(imgs)])
+    full = np.concatenate([net.encrypt_image(im, nonce=30 + s) for s, im in enumerate(imgs)])
+    host_out = np.zeros(B * net.out_words, dtype=np.uint64)
+    net.run_host_compact(compact, B, host_out, chunk)
+    out = ctx.ct(B, net.out_level)
+    net.run(ctx.ct(B * net.ntaps, net.top, full, DELTA), out)
     assert np.array_equal(host_out, out.download())
 
 
