@@ -694,18 +694,49 @@ void ock_conv_mac(const ock_ctx* c, const u64* taps, int ntaps, int l,
   }
 }
 
+/* merge_maps with one lazy ModDown:
+ *   out = map_0 + sum_j rot_right(map_j, j w)
+ *       = (map_0.c0 + sum_j sigma_j(map_j.c0), map_0.c1) + ModDown(sum_j IP_j)
+ * where IP_j is the extended-basis key-switch inner product of
+ * sigma_j(map_j.c1). */
 void ock_merge(const ock_ctx* c, const u64* maps, int nmaps, int l, int64_t w,
                const u64* keys, u64* out) {
-  const size_t n = 2 * (size_t)l * c->N;
-  const size_t ksz = (size_t)c->L * 2 * c->np * c->N;
-  u64* r = (u64*)malloc(sizeof(u64) * n);
+  const size_t N = c->N, n = 2 * (size_t)l * N, ne = (size_t)(l + 1) * N;
+  const size_t ksz = (size_t)c->L * 2 * c->np * N;
+  u64* ra = (u64*)malloc(sizeof(u64) * n);
+  u64* D = (u64*)malloc(sizeof(u64) * (size_t)l * ne);
+  u64* IP = (u64*)malloc(sizeof(u64) * 2 * ne);
+  u64* ACC = (u64*)calloc(2 * ne, sizeof(u64));
+  u64* md = (u64*)malloc(sizeof(u64) * n);
   memcpy(out, maps, sizeof(u64) * n);
   for (int j = 1; j < nmaps; j++) {
-    ock_rotate(c, maps + (size_t)j * n, l, ock_galois_right(c, (int64_t)j * w),
-               keys + (size_t)(j - 1) * ksz, r);
-    ock_add(c, out, r, l, out);
+    ock_automorph_ntt(c, ock_galois_right(c, (int64_t)j * w), maps + (size_t)j * n, ra, 2 * l);
+    modup(c, ra + (size_t)l * N, l, D);
+    key_inner(c, D, l, keys + (size_t)(j - 1) * ksz, IP);
+    for (int p = 0; p < 2; p++)
+      for (int t = 0; t <= l; t++) {
+        u64 q = c->q[t < l ? t : c->L];
+        for (size_t k = 0; k < N; k++) {
+          size_t i = (size_t)p * ne + (size_t)t * N + k;
+          ACC[i] = addmod(ACC[i], IP[i], q);
+        }
+      }
+    for (int t = 0; t < l; t++)
+      for (size_t k = 0; k < N; k++) {
+        size_t i = (size_t)t * N + k;
+        out[i] = addmod(out[i], ra[i], c->q[t]);
+      }
   }
-  free(r);
+  if (nmaps > 1) {
+    moddown(c, ACC, l, md);
+    for (int p = 0; p < 2; p++)
+      for (int t = 0; t < l; t++)
+        for (size_t k = 0; k < N; k++) {
+          size_t i = (size_t)p * l * N + (size_t)t * N + k;
+          out[i] = addmod(out[i], md[i], c->q[t]);
+        }
+  }
+  free(ra); free(D); free(IP); free(ACC); free(md);
 }
 
 /* Double-hoisted Halevi-Shoup diagonal sum:

@@ -28,6 +28,10 @@ struct KeyRowMap {
   int period;
   int shift[HEGPU_MAX_BATCH_PERIOD];             // left shift s (0 = none)
   const u64d* key[HEGPU_MAX_BATCH_PERIOD];       // device key (Montgomery)
+  // optional grouped input rows (merge): row b reads src + (b / grp) *
+  // grp_stride + (b % grp) * src_stride; grp = 0 means b * src_stride
+  int grp;
+  long grp_stride;
 };
 
 struct DeviceKey {
@@ -205,5 +209,6 @@ void eval_rescale(Context& c, const CtBatch& a, CtBatch& out);
 void eval_rotate(Context& c, const u64d* a, long a_stride, int B, int l, const KeyRowMap& km, u64d* out,
                  long out_stride);
 void eval_square(Context& c, const CtBatch& a, CtBatch& out);  // tensor + relin, no rescale
+void eval_merge(Context& c, const CtBatch& maps, int nmaps, const KeyRowMap& km, CtBatch& out);
 
 }  // namespace hegpu

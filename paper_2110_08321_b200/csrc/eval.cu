@@ -93,29 +93,108 @@ __global__ void k_tensor_square(PrimeTable pt, const u64d* __restrict__ a, u64d*
   }
 }
 
-// key-switch inner product: acc[b][p][t] = sum_j D[b][j][t] * key_b[j][p][pi(t)]
-__global__ void k_ks_inner(PrimeTable pt, const u64d* __restrict__ D, int l, int L, int N, KeyRowMap km,
-                           u64d* __restrict__ acc) {
+// key-switch inner product: acc[b][p][t] = sum_j D[b][j][t] * key_b[j][p][pi(t)].
+// Rows sharing a key (b = (u*KT + bb) * period + jkey) are tiled KT per
+// thread so every key word is loaded once for KT ciphertexts.
+constexpr int kKsKT = 4;
+__global__ void __launch_bounds__(kTpb) k_ks_inner(PrimeTable pt, const u64d* __restrict__ D, int B, int l, int L,
+                                                   int N, KeyRowMap km, u64d* __restrict__ acc) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  const int t = blockIdx.y, b = blockIdx.z;
+  const int t = blockIdx.y;
+  const int jkey = blockIdx.z % km.period, u = blockIdx.z / km.period;
   if (k >= N) return;
   const int pi = t == l ? L : t;
   const DevPrime pr = pt.p[pi];
-  const u64d* key = km.key[b % km.period];  // split-31 Montgomery words
-  const size_t kp = (size_t)(L + 1) * N;    // one key poly over all primes
-  Acc3 a0, a1;
-  a0.zero();
-  a1.zero();
-  for (int j = 0; j < l; ++j) {
-    const u64d d = split31(D[(((size_t)b * l + j) * (l + 1) + t) * N + k]);
-    const u64d* kj = key + (size_t)j * 2 * kp + (size_t)pi * N + k;
-    a0.mad(d, __ldg(kj));
-    a1.mad(d, __ldg(kj + kp));
-    if ((j & 3) == 3) a0.fold(), a1.fold();
+  const u64d* key = km.key[jkey] + (size_t)pi * N + k;  // split-31 Montgomery words
+  const size_t kp = (size_t)(L + 1) * N;                // one key poly over all primes
+  int rows[kKsKT];
+  Acc3 a0[kKsKT], a1[kKsKT];
+#pragma unroll
+  for (int bb = 0; bb < kKsKT; ++bb) {
+    rows[bb] = (u * kKsKT + bb) * km.period + jkey;
+    a0[bb].zero();
+    a1[bb].zero();
   }
-  u64d* o = acc + ((size_t)b * 2 * (l + 1) + t) * N + k;
-  o[0] = a0.reduce(pr);
-  o[(size_t)(l + 1) * N] = a1.reduce(pr);
+  for (int j = 0; j < l; ++j) {
+    const u64d k0 = __ldg(key + (size_t)j * 2 * kp), k1 = __ldg(key + (size_t)j * 2 * kp + kp);
+#pragma unroll
+    for (int bb = 0; bb < kKsKT; ++bb) {
+      if (rows[bb] >= B) break;
+      const u64d d = split31(D[(((size_t)rows[bb] * l + j) * (l + 1) + t) * N + k]);
+      a0[bb].mad(d, k0);
+      a1[bb].mad(d, k1);
+    }
+    if ((j & 3) == 3) {
+#pragma unroll
+      for (int bb = 0; bb < kKsKT; ++bb) a0[bb].fold(), a1[bb].fold();
+    }
+  }
+#pragma unroll
+  for (int bb = 0; bb < kKsKT; ++bb) {
+    if (rows[bb] >= B) break;
+    u64d* o = acc + ((size_t)rows[bb] * 2 * (l + 1) + t) * N + k;
+    o[0] = a0[bb].reduce(pr);
+    o[(size_t)(l + 1) * N] = a1[bb].reduce(pr);
+  }
+}
+
+// merge inner product, summed over the G rotated maps of each image:
+//   acc[img][p][t] = sum_j sum_d D[img*G + j][d][t] * key_j[d][p][pi(t)]
+__global__ void __launch_bounds__(kTpb) k_ks_inner_sum(PrimeTable pt, const u64d* __restrict__ D, int nimg, int G,
+                                                       int l, int L, int N, KeyRowMap km,
+                                                       u64d* __restrict__ acc) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.y, i0 = blockIdx.z * kKsKT;
+  if (k >= N) return;
+  const int pi = t == l ? L : t;
+  const DevPrime pr = pt.p[pi];
+  const size_t kp = (size_t)(L + 1) * N;
+  Acc3 a0[kKsKT], a1[kKsKT];
+#pragma unroll
+  for (int bb = 0; bb < kKsKT; ++bb) a0[bb].zero(), a1[bb].zero();
+  int cnt = 0;
+  for (int j = 0; j < G; ++j) {
+    const u64d* key = km.key[j] + (size_t)pi * N + k;
+    for (int d = 0; d < l; ++d) {
+      const u64d k0 = __ldg(key + (size_t)d * 2 * kp), k1 = __ldg(key + (size_t)d * 2 * kp + kp);
+#pragma unroll
+      for (int bb = 0; bb < kKsKT; ++bb) {
+        const int img = i0 + bb;
+        if (img >= nimg) break;
+        const u64d x = split31(D[((((size_t)img * G + j) * l + d) * (l + 1) + t) * N + k]);
+        a0[bb].mad(x, k0);
+        a1[bb].mad(x, k1);
+      }
+      if ((++cnt & 3) == 0) {
+#pragma unroll
+        for (int bb = 0; bb < kKsKT; ++bb) a0[bb].fold(), a1[bb].fold();
+      }
+    }
+  }
+#pragma unroll
+  for (int bb = 0; bb < kKsKT; ++bb) {
+    const int img = i0 + bb;
+    if (img >= nimg) break;
+    u64d* o = acc + ((size_t)img * 2 * (l + 1) + t) * N + k;
+    o[0] = a0[bb].reduce(pr);
+    o[(size_t)(l + 1) * N] = a1[bb].reduce(pr);
+  }
+}
+
+// merge Q-basis part: C0 = map_0.c0 + sum_j sigma_j(map_j.c0), C1 = map_0.c1
+__global__ void k_merge_c(PrimeTable pt, const u64d* __restrict__ maps, int nimg, int c, int l, int N,
+                          KeyRowMap km, u64d* __restrict__ C) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.y % l, p = blockIdx.y / l, img = blockIdx.z;
+  if (k >= N) return;
+  const int S = N >> 1;
+  const u64d q = pt.p[t].q;
+  const size_t st = (size_t)2 * l * N;
+  const u64d* m = maps + (size_t)img * c * st + (size_t)p * l * N + (size_t)t * N;
+  u64d v = m[k];
+  if (p == 0)
+    for (int j = 1; j < c; ++j) v = add_mod_d(v, m[(size_t)j * st + shifted_pos(k, km.shift[j - 1], S)], q);
+  C[(size_t)img * st + (size_t)p * l * N + (size_t)t * N + k] = v;
 }
 
 // conv-pack MAC (convlower.cpp:39-74): CO output maps per thread, taps
@@ -364,10 +443,13 @@ void launch_tensor_square(Context& c, const u64d* a, u64d* d01, u64d* d2, int co
 }
 
 void ks_inner(Context& c, const u64d* D, int B, int l, const KeyRowMap& keys, u64d* acc) {
-  dim3 grid((c.N() + kTpb - 1) / kTpb, l + 1, B);
+  const int per = keys.period, rows_per_key = (B + per - 1) / per;
+  const int tiles = (rows_per_key + kKsKT - 1) / kKsKT;
+  dim3 grid((c.N() + kTpb - 1) / kTpb, l + 1, per * tiles);
   double kb = 0;  // distinct keys read once each
-  for (int i = 0; i < keys.period && i < B; ++i) kb += 8.0 * l * 2 * (l + 1) * c.N();
-  LAUNCH_B(c, "k_ks_inner", 8.0 * B * (l + 2) * (l + 1) * c.N() + kb, k_ks_inner<<<grid, kTpb, 0, c.stream>>>(c.primes, D, l, c.L(), c.N(), keys, acc));
+  for (int i = 0; i < per && i < B; ++i) kb += 8.0 * l * 2 * (l + 1) * c.N();
+  LAUNCH_B(c, "k_ks_inner", 8.0 * B * (l + 2) * (l + 1) * c.N() + kb,
+           k_ks_inner<<<grid, kTpb, 0, c.stream>>>(c.primes, D, B, l, c.L(), c.N(), keys, acc));
 }
 
 void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, const u64d* w, int c_out,
@@ -450,6 +532,35 @@ void eval_rotate(Context& c, const u64d* a, long a_stride, int B, int l, const K
   d.add = a; d.add_b = a_stride; d.add_p = 0; d.add_mask = 1; d.shifts = &km;
   drop_last_limb(c, B, d, tmpP);
   c.free(tmp); c.free(D); c.free(acc); c.free(tmpP);
+}
+
+// merge_maps with one lazy ModDown per image; km carries
+// the nmaps-1 shifts / keys (period nmaps-1)
+void eval_merge(Context& c, const CtBatch& maps, int nmaps, const KeyRowMap& km, CtBatch& out) {
+  const int B = out.count, l = maps.level, N = c.N(), G = nmaps - 1;
+  const size_t st = maps.stride();
+  u64d* tmp = c.alloc((size_t)B * G * l * N);
+  u64d* D = c.alloc((size_t)B * G * l * (l + 1) * N);
+  u64d* acc = c.alloc((size_t)B * 2 * (l + 1) * N);
+  u64d* C = c.alloc((size_t)B * 2 * l * N);
+  u64d* tmpP = c.alloc((size_t)B * 2 * N);
+  KeyRowMap kg = km;
+  kg.grp = G;
+  kg.grp_stride = (long)(nmaps * st);
+  ks_modup(c, maps.d + st + (size_t)l * N, (long)st, B * G, l, &kg, tmp, D);
+  dim3 gi((N + kTpb - 1) / kTpb, l + 1, (B + kKsKT - 1) / kKsKT);
+  LAUNCH_B(c, "k_ks_inner", 8.0 * N * ((double)B * G * l * (l + 1) + 2.0 * G * l * (l + 1) + 2.0 * B * (l + 1)),
+           k_ks_inner_sum<<<gi, kTpb, 0, c.stream>>>(c.primes, D, B, G, l, c.L(), N, km, acc));
+  dim3 gc((N + kTpb - 1) / kTpb, 2 * l, B);
+  LAUNCH_B(c, "k_merge_c", 8.0 * N * ((double)B * (nmaps + 1) * l + 2.0 * B * l),
+           k_merge_c<<<gc, kTpb, 0, c.stream>>>(c.primes, maps.d, B, nmaps, l, N, km, C));
+  DropArgs d{};
+  d.src = acc; d.src_b = 2L * (l + 1) * N; d.src_p = (long)(l + 1) * N; d.src_limbs = l + 1;
+  d.dst = out.d; d.dst_b = (long)out.stride(); d.dst_p = (long)l * N;
+  d.pd = c.L(); d.nl = l;
+  d.add = C; d.add_b = 2L * l * N; d.add_p = (long)l * N; d.add_mask = 3; d.shifts = nullptr;
+  drop_last_limb(c, B, d, tmpP);
+  c.free(tmp); c.free(D); c.free(acc); c.free(C); c.free(tmpP);
 }
 
 void eval_square(Context& c, const CtBatch& a, CtBatch& out) {

@@ -90,24 +90,23 @@ void ConvLayer::run(Context& c, const CtBatch& taps, CtBatch& maps) {
 
 // ----------------------------------------------------------------- merge ----
 void merge_maps(Context& c, const CtBatch& maps, int nmaps, int64_t w, CtBatch& out) {
-  const int B = out.count, l = maps.level, S = c.S();
+  const int S = c.S();
   const size_t st = maps.stride();
-  CK(cudaMemcpy2DAsync(out.d, st * 8, maps.d, (size_t)nmaps * st * 8, st * 8, B, cudaMemcpyDeviceToDevice,
-                       c.stream));
   out.scale = maps.scale;
-  if (nmaps == 1) return;
-  CtBatch rot{&c, B, l, maps.scale, c.alloc((size_t)B * st)};
+  if (nmaps == 1) {
+    CK(cudaMemcpyAsync(out.d, maps.d, (size_t)out.count * st * 8, cudaMemcpyDeviceToDevice, c.stream));
+    return;
+  }
+  if (nmaps - 1 > HEGPU_MAX_BATCH_PERIOD) fail(HEGPU_ERR_CAPACITY, "merge_maps: too many maps");
+  // all c-1 rotations in one batched key switch with a single ModDown
+  KeyRowMap km{};
+  km.period = nmaps - 1;
   for (int j = 1; j < nmaps; ++j) {
     const int shift = (int)((S - ((int64_t)j * w) % S) % S);
-    if (shift == 0) continue;
-    KeyRowMap km{};
-    km.period = 1;
-    km.shift[0] = shift;
-    km.key[0] = c.rot_key(shift).data;
-    eval_rotate(c, maps.d + (size_t)j * st, (long)((size_t)nmaps * st), B, l, km, rot.d, (long)st);
-    launch_add(c, out.d, rot.d, out.d, B, l);
+    km.shift[j - 1] = shift;
+    km.key[j - 1] = c.rot_key(shift).data;
   }
-  c.free(rot.d);
+  eval_merge(c, maps, nmaps, km, out);
 }
 
 // ---------------------------------------------------------------- square ----

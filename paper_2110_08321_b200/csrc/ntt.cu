@@ -305,7 +305,8 @@ __global__ void NTT_BOUNDS k_ks_intt(TwArgs ta, PrimeTable pt, const u64d* __res
   constexpr int N = 1 << LOGN, S = N >> 1;
   const int r = blockIdx.x, b = r / l, j = r % l;
   const int s = use_shift ? km.shift[b % km.period] : 0;
-  const u64d* in = src + b * src_stride + (size_t)j * N;
+  const u64d* in = src + (km.grp ? (b / km.grp) * km.grp_stride + (b % km.grp) * src_stride : b * src_stride) +
+                   (size_t)j * N;
   u64d* own = D + (((size_t)b * l + j) * (l + 1) + j) * N;
   for (int p = threadIdx.x; p < N; p += blockDim.x) {
     const u64d v = in[s ? shifted(p, s, S) : p];
