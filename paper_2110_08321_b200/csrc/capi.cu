@@ -2,6 +2,7 @@
 // translation, host<->device conversion and the evaluator / layer entry
 // points.  No CPU fallback exists: every evaluator call runs CUDA kernels
 // and fails with HEGPU_ERR_CUDA when no device is present.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -341,15 +342,27 @@ extern "C" int hegpu_gen_rotation_keys(hegpu_ctx* h, const int64_t* rots, int n)
   return guarded(&c, [&] {
     need_gpu(c);
     const int S = c.S();
-    std::vector<u64> wire(c.client->key_words());
+    std::vector<int> todo;
     for (int i = 0; i < n; ++i) {
       need(rots[i] >= 0 && rots[i] < S, HEGPU_ERR_RANGE, "rotation amount outside [0, S)");
       const int shift = (int)((S - rots[i] % S) % S);
       if (shift == 0 || c.rot_keys.count(shift)) continue;
-      c.client->gen_galois_key(c.P->galois_left(shift), wire.data());
-      DeviceKey& k = c.rot_keys[shift];
-      k.shift = shift;
-      upload_key(c, wire, k);
+      if (std::find(todo.begin(), todo.end(), shift) == todo.end()) todo.push_back(shift);
+    }
+    // host key generation is independent per Galois element: batches of keys
+    // are generated on all host cores, then uploaded in order
+    const size_t kw = c.client->key_words();
+    const int batch = 32;
+    std::vector<std::vector<u64>> wires(batch, std::vector<u64>(kw));
+    for (size_t b0 = 0; b0 < todo.size(); b0 += batch) {
+      const int nb = (int)std::min<size_t>(batch, todo.size() - b0);
+#pragma omp parallel for schedule(dynamic)
+      for (int i = 0; i < nb; ++i) c.client->gen_galois_key(c.P->galois_left(todo[b0 + i]), wires[i].data());
+      for (int i = 0; i < nb; ++i) {
+        DeviceKey& k = c.rot_keys[todo[b0 + i]];
+        k.shift = todo[b0 + i];
+        upload_key(c, wires[i], k);
+      }
     }
   });
 }

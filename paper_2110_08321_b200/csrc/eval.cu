@@ -263,10 +263,16 @@ __global__ void __launch_bounds__(kTpb) k_conv_mac(PrimeTable pt, const u64d* __
 // every diagonal of the chunk reads it from there.
 constexpr int kHsKB = 128;  // output positions per CTA
 constexpr int kHsCW = 128;  // max r span of a chunk
-constexpr int kHsBT = 4;    // images per thread
+#ifndef HEGPU_HS_BT
+#define HEGPU_HS_BT 4
+#endif
+#ifndef HEGPU_HS_MINB
+#define HEGPU_HS_MINB 4
+#endif
+constexpr int kHsBT = HEGPU_HS_BT;  // images per thread
 
 template <int LV>
-__global__ void __launch_bounds__(kHsKB, 4) k_hs_diag(PrimeTable pt, const u64d* __restrict__ v,
+__global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt, const u64d* __restrict__ v,
                                                    const u64d* __restrict__ D, int B, int L, int N,
                                                    HsDiagTable tab, u64d* __restrict__ acc,
                                                    u64d* __restrict__ cacc) {

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhegpu.so")
+LIB_PATH = os.environ.get("HEGPU_LIB") or os.path.join(_HERE, "libhegpu.so")
 
 OK, ERR_CAPACITY, ERR_SHAPE, ERR_LAYOUT, ERR_RANGE, ERR_IO, ERR_CUDA, ERR_NCCL, ERR_ARG, ERR_KEY = range(10)
 CLIENT_ONLY = -1

@@ -290,6 +290,48 @@ def test_cfg0_run_host_compact_pipeline(cfg0, chunk):
     assert np.array_equal(host_out, out.download())
 
 
+def test_cfg3_net_logits_and_hops():
+    """Config 3 (CIFAR-shaped, N=16384): conv 5x5/2 3->32 (75 taps), merge 32
+    maps (6272 slots), HS 6272->256, HS 256->10; logits vs ref_forward and
+    the golden per-inference HOPs (34/2673/2666/2/305)."""
+    from paper_2110_08321_b200.workloads import CFG3
+    cfg = CFG3
+    ctx = H.Context(cfg.log_n, list(cfg.qbits), cfg.pbits, seed=303)
+    w = net_weights(cfg, 3)
+    net = H.Net(ctx, cfg, w)
+    B = 2
+    imgs = [net_image(cfg, 100 + s) for s in range(B)]
+    taps = np.concatenate([net.encrypt_image(im, nonce=s) for s, im in enumerate(imgs)])
+    out = ctx.ct(B, net.out_level)
+    ctx.reset_meter()
+    net.run(ctx.ct(B * net.ntaps, net.top, taps, DELTA), out)
+    got = out.download().reshape(B, -1)
+    spec = HS.CnnSpec(cfg.in_c, cfg.in_d, cfg.k, cfg.s, cfg.c_out, cfg.dense, cfg.n_slots)
+    golden = HS.golden_stage_tallies(spec)
+    assert dict(ctx.stages()) == {k: tuple(B * x for x in v) for k, v in golden.items()}
+    assert tuple(np.sum(list(golden.values()), axis=0)) == (34, 2673, 2666, 2, 305)
+    for b in range(B):
+        ref = HS.ref_forward(spec, w, imgs[b])
+        assert np.abs(net.decrypt_logits(got[b]) - ref).max() < 1e-3
+
+
+def test_cfg3_shaped_hs_bit_exact():
+    """HS 6272 -> 256 at N=16384 (config 3's dense layer, plain branch with 5
+    folds) against the oracle, on a 3-prime chain to bound key memory."""
+    ctx = H.Context(14, [60, 40, 40], 60, seed=33)
+    ck = Ckks(14, [60, 40, 40], 60, seed=33)
+    A = np.random.default_rng(0).normal(0, 0.02, (256, 6272))
+    x = np.random.default_rng(1).uniform(0, 1, 6272)
+    v = ck.encrypt(ck.encode(x, DELTA, 3), 3, 9)
+    plan = ctx.hs_plan(A, 3)
+    assert (plan.m_eff, plan.folds, plan.kept) == (256, 5, 256)
+    ctx.gen_rotation_keys(plan.rotations())
+    out = ctx.ct(1, 2)
+    got = ctx.hs_matvec(plan, ctx.ct(1, 3, v, DELTA), out).download()
+    assert np.array_equal(got, P.hs_matvec(ck, v, 3, A))
+    assert np.abs(ck.decrypt_decode(got, 2, DELTA)[:256] - A @ x).max() < 1e-4
+
+
 def test_cfg1_point_hs(cfg0):
     """Config 1 shape at reduced ring (full sizes run in bench): m=64, n=256."""
     ctx = H.Context(12, [60, 40], 60, seed=3)
