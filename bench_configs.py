@@ -1,0 +1,153 @@
+"""bench_configs.py -- the other BASELINE.json configs on one B200 (bench.py
+measures the headline config 2).  One JSON line per measured point.
+
+  python bench_configs.py --config 1   # HS matvec sweep, N=16384, one rescale
+  python bench_configs.py --config 3   # CIFAR-shaped net, N=16384, 5 rescales
+  python bench_configs.py --config 4   # conv-pack layer sweep, N=16384
+
+Device time with CUDA events on the engine's stream after warm-up; inputs are
+fresh seeded encryptions (synthetic, BASELINE.json shapes/distributions).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DELTA = 2.0 ** 40
+
+
+def timed(ctx, fn, steps, warmup):
+    import torch
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr())
+    for _ in range(warmup):
+        fn()
+    ctx.sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def config1(args):
+    """BASELINE configs[1]: m x n in {64,256,1024,4096}^2, A ~ N(0,.05^2),
+    v ~ U[-1,1]^n, N=16384, Q={60,40}, one rescale.  Reports rotations/s
+    (key-switched, HS metering) and the fused-HS kernel's achieved GB/s."""
+    from paper_2110_08321_b200 import hegpu as H
+    from paper_2110_08321_b200.workloads import hs_sweep_case
+    ctx = H.Context(14, [60, 40], 60, seed=1)
+    dims = [64, 256, 1024, 4096]
+    for m in dims:
+        for n in dims:
+            A, x = hs_sweep_case(m, n)
+            t0 = time.perf_counter()
+            plan = ctx.hs_plan(A, 2)
+            ctx.gen_rotation_keys(plan.rotations())
+            setup_s = time.perf_counter() - t0
+            for B in (1, args.batch):
+                pt = ctx.encode(x, DELTA, 2)
+                v = ctx.ct(B, 2, np.concatenate([ctx.encrypt(pt, 2, 7 + i) for i in range(B)]), DELTA)
+                out = ctx.ct(B, 1)
+                ctx.hs_matvec(plan, v, out)  # first run fuses keys x masks (offline)
+                ctx.reset_meter()
+                ctx.hs_matvec(plan, v, out)
+                tally = ctx.total()
+                ms = timed(ctx, lambda: ctx.hs_matvec(plan, v, out), args.steps, args.warmup)
+                ctx.kernel_timer("k_hs_diag")
+                ctx.hs_matvec(plan, v, out)
+                kms, _, kbytes = ctx.kernel_timer_read()
+                ctx.kernel_timer(None)
+                rot = tally[4]
+                print(json.dumps({
+                    "config": 1, "m": m, "n": n, "batch": B, "ms_per_matvec_batch": ms,
+                    "matvecs_per_s": B / (ms / 1e3), "rotations_per_s": rot / (ms / 1e3),
+                    "rotations_per_matvec": rot // B, "mul_pc_per_matvec": tally[2] // B,
+                    "m_eff": plan.m_eff, "folds": plan.folds,
+                    "hs_diag_ms": kms, "hs_diag_gbs": kbytes / (kms / 1e3) / 1e9 if kms else None,
+                    "setup_s": setup_s}), flush=True)
+            del plan
+
+
+def config3(args):
+    """BASELINE configs[3]: CIFAR-shaped net (3x32x32 U[0,1], conv 5x5/2
+    3->32, square, HS 6272->256, square, HS 256->10), N=16384, 5 rescales."""
+    from paper_2110_08321_b200 import hegpu as H
+    from paper_2110_08321_b200.workloads import CFG3, net_image, net_weights
+    cfg = CFG3
+    ctx = H.Context(cfg.log_n, list(cfg.qbits), cfg.pbits, seed=3)
+    t0 = time.perf_counter()
+    net = H.Net(ctx, cfg, net_weights(cfg, 3))
+    setup_s = time.perf_counter() - t0
+    B = args.batch
+    taps = np.concatenate([net.encrypt_image(net_image(cfg, i), nonce=i) for i in range(B)])
+    dt = ctx.ct(B * net.ntaps, net.top, taps, DELTA)
+    out = ctx.ct(B, net.out_level)
+    net.run(dt, out)
+    ctx.reset_meter()
+    g = ctx.capture(lambda: net.run(dt, out))
+    tally = ctx.total()
+    ms = timed(ctx, g, args.steps, args.warmup)
+    print(json.dumps({
+        "config": 3, "batch": B, "ms_per_step": ms, "inferences_per_s": B / (ms / 1e3),
+        "rotations_per_s": tally[4] / (ms / 1e3), "hops_per_inference": [t / B for t in tally],
+        "setup_s": setup_s}), flush=True)
+
+
+def config4(args):
+    """BASELINE configs[4]: conv-pack layer sweep, c_in in {1,3,16,32}, 32x32
+    U[0,1] inputs, k in {3,5} (stride 1), c_out in {5,32,64}, N=16384.
+    Reports layers/s and the closed-form HOPs (convlower.cpp:39-74)."""
+    from paper_2110_08321_b200 import hegpu as H
+    from oracle import hesim_oracle as HS  # only for ref_conv in the spot check
+    ctx = H.Context(14, [60, 40], 60, seed=4)
+    rng = np.random.default_rng(4)
+    for c_in in (1, 3, 16, 32):
+        img = rng.uniform(0, 1, (c_in, 32, 32))
+        for k in (3, 5):
+            d_out = 32 - k + 1
+            ntaps = k * k * c_in
+            shape = HS.ConvShape(32, c_in, k, 1, 1)
+            taps = HS.conv_pack(img, shape, ctx.S)
+            cts = np.concatenate([ctx.encrypt(ctx.encode(t.slots[: d_out * d_out], DELTA, 2), 2, i)
+                                  for i, t in enumerate(taps)])
+            dt = ctx.ct(ntaps, 2, cts, DELTA)
+            for c_out in (5, 32, 64):
+                W = rng.normal(0, 0.05, (c_out, c_in, k, k))
+                b = rng.normal(0, 0.01, c_out)
+                out = ctx.ct(c_out, 1)
+                plan = ctx.conv_plan(ntaps, W.reshape(c_out, -1), b, d_out * d_out, 2, DELTA)  # offline
+                ctx.reset_meter()
+                ctx.conv_plan_run(plan, dt, out)
+                tally = ctx.total()
+                ms = timed(ctx, lambda: ctx.conv_plan_run(plan, dt, out), args.steps, args.warmup)
+                # spot check: decrypt map 0 against the FP64 reference conv
+                want = HS.ref_conv(img, W[:1], b[:1], 1)[0].ravel()
+                got = ctx.decode(ctx.decrypt(out.download()[: 2 * ctx.N], 1), 1, DELTA)[: d_out * d_out]
+                print(json.dumps({
+                    "config": 4, "c_in": c_in, "k": k, "c_out": c_out, "ms_per_layer": ms,
+                    "layers_per_s": 1e3 / ms, "hops": dict(zip(H.TALLY_FIELDS, tally)),
+                    "max_abs_err_vs_ref_conv": float(np.abs(got - want).max())}), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, required=True, choices=[1, 3, 4])
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--batch", type=int, default=16)
+    args = ap.parse_args()
+    {1: config1, 3: config3, 4: config4}[args.config](args)
+
+
+if __name__ == "__main__":
+    main()

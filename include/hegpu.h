@@ -171,6 +171,13 @@ int hegpu_square(hegpu_ctx* ctx, const hegpu_ct* a, hegpu_ct* out);
  * maps_out: count B*c_out ordered [b][co], level l-1. */
 int hegpu_conv_packed_forward(hegpu_ctx* ctx, const hegpu_ct* taps, int ntaps, const double* weights,
                               int c_out, const double* bias, int w_used, hegpu_ct* maps_out);
+/* the same layer with its plaintexts (scalar weights, bias encodings)
+ * prepared once: plan at tap level `level`, tap scale `tap_scale` */
+typedef struct hegpu_conv_plan hegpu_conv_plan;
+int hegpu_conv_plan_create(hegpu_ctx* ctx, int ntaps, const double* weights, int c_out, const double* bias,
+                           int w_used, int level, double tap_scale, hegpu_conv_plan** out);
+void hegpu_conv_plan_destroy(hegpu_conv_plan* plan);
+int hegpu_conv_plan_run(hegpu_ctx* ctx, const hegpu_conv_plan* plan, const hegpu_ct* taps, hegpu_ct* maps_out);
 /* merge_maps (convlower.cpp:145-160): maps count B*c ordered [b][j];
  * out count B; CapacityError if c*w > S */
 int hegpu_merge_maps(hegpu_ctx* ctx, const hegpu_ct* maps, int c, int64_t w, hegpu_ct* out);

@@ -645,6 +645,50 @@ extern "C" int hegpu_conv_packed_forward(hegpu_ctx* h, const hegpu_ct* taps, int
   });
 }
 
+struct hegpu_conv_plan {
+  std::unique_ptr<ConvLayer> layer;
+  int ntaps, c_out;
+};
+
+extern "C" int hegpu_conv_plan_create(hegpu_ctx* h, int ntaps, const double* weights, int c_out, const double* bias,
+                                      int w_used, int level, double tap_scale, hegpu_conv_plan** out) {
+  if (!h || !weights || !out) return HEGPU_ERR_ARG;
+  Context& c = h->c;
+  return guarded(&c, [&] {
+    need_gpu(c);
+    need(ntaps >= 1 && c_out >= 1, HEGPU_ERR_SHAPE, "conv_plan: bad shape");
+    need(level >= 2 && level <= c.L(), HEGPU_ERR_CAPACITY, "conv_plan: level must leave a prime to rescale");
+    need(w_used >= 0 && w_used <= c.S(), HEGPU_ERR_CAPACITY, "conv_plan: w exceeds slots");
+    auto* p = new hegpu_conv_plan{nullptr, ntaps, c_out};
+    try {
+      p->layer = std::make_unique<ConvLayer>(c, ntaps, c_out, weights, bias, w_used, level, tap_scale);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
+extern "C" void hegpu_conv_plan_destroy(hegpu_conv_plan* p) { delete p; }
+
+extern "C" int hegpu_conv_plan_run(hegpu_ctx* h, const hegpu_conv_plan* p, const hegpu_ct* taps, hegpu_ct* maps) {
+  if (!h || !p || !taps || !maps) return HEGPU_ERR_ARG;
+  Context& c = h->c;
+  return guarded(&c, [&] {
+    const int ntaps = p->ntaps, c_out = p->c_out;
+    need(taps->b.level == p->layer->level && taps->b.count % ntaps == 0, HEGPU_ERR_SHAPE,
+         "conv_plan_run: taps must be B*ntaps at the plan level");
+    const int B = taps->b.count / ntaps;
+    need(maps->b.count == B * c_out && maps->b.level == taps->b.level - 1, HEGPU_ERR_SHAPE,
+         "conv_plan_run: maps must be B*c_out at level - 1");
+    p->layer->run(c, taps->b, maps->b);
+    c.meter.bump(HEGPU_MUL_PC, (int64_t)B * ntaps * c_out);
+    c.meter.bump(HEGPU_ADD_CC, (int64_t)B * (ntaps - 1) * c_out);
+    c.meter.bump(HEGPU_ADD_PC, (int64_t)B * c_out);
+  });
+}
+
 extern "C" int hegpu_merge_maps(hegpu_ctx* h, const hegpu_ct* maps, int nmaps, int64_t w, hegpu_ct* out) {
   if (!h || !maps || !out) return HEGPU_ERR_ARG;
   Context& c = h->c;

@@ -7,6 +7,8 @@
 // conv_packed_forward (:39-74), hs_matvec (proj/src/matvec.cpp:82-105).  The
 // CKKS math (hybrid key switch, alpha = 1, one special prime) is fixed in
 // DESIGN.md §3 and restated by oracle/ckks_oracle.c.
+#include <algorithm>
+
 #include "engine.hpp"
 
 namespace hegpu {
@@ -275,11 +277,18 @@ template <int LV>
 __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt, const u64d* __restrict__ v,
                                                    const u64d* __restrict__ D, int B, int L, int N,
                                                    HsDiagTable tab, u64d* __restrict__ acc,
-                                                   u64d* __restrict__ cacc) {
+                                                   u64d* __restrict__ cacc, int gsplit, size_t part_acc,
+                                                   size_t part_cacc) {
   extern __shared__ u64d win[];  // [BT][LV + 1][kHsW], split-31 words
   constexpr int kW = kHsKB + kHsCW;  // window row stride (compile-time -> immediate LDS offsets)
   const int S = N >> 1;
-  const int kb = blockIdx.y, t = blockIdx.z >> 1, p = blockIdx.z & 1, b0 = blockIdx.x * kHsBT;
+  // blockIdx.x = image tile * gsplit + diagonal group: with few images the
+  // diagonal chunks are split over gsplit CTAs writing partial sums
+  const int g = blockIdx.x % gsplit;
+  const int kb = blockIdx.y, t = blockIdx.z >> 1, p = blockIdx.z & 1, b0 = (blockIdx.x / gsplit) * kHsBT;
+  acc += (size_t)g * part_acc;
+  cacc += (size_t)g * part_cacc;
+  const int ch_lo = (int)((long)tab.nchunk * g / gsplit), ch_hi = (int)((long)tab.nchunk * (g + 1) / gsplit);
   const int k0 = kb * kHsKB, k = k0 + threadIdx.x;
   const int half = k0 >= S ? S : 0;
   const int pi = t == LV ? L : t;
@@ -294,7 +303,7 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
   for (int bb = 0; bb < kHsBT; ++bb) a[bb].zero(), c[bb].zero();
 
   const u64d* mrow = tab.masks + (size_t)t * N + k;
-  for (int ch = 0; ch < tab.nchunk; ++ch) {
+  for (int ch = ch_lo; ch < ch_hi; ++ch) {
     const int i0 = __ldg(tab.chunk + ch), i1 = __ldg(tab.chunk + ch + 1);
     const int r_lo = __ldg(tab.r + i0), r_hi = __ldg(tab.r + i1 - 1);
     const int W = kHsKB + r_hi - r_lo;
@@ -363,7 +372,7 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
   }
   // r == 0 diagonal (if kept) is the only contributor to the c1 part
   u64d m0 = 0;
-  const bool c1_term = has_c && p == 1 && tab.ndiag > 0 && __ldg(tab.r) == 0;
+  const bool c1_term = has_c && p == 1 && g == 0 && tab.ndiag > 0 && __ldg(tab.r) == 0;
   if (c1_term) m0 = unsplit31(__ldg(tab.masks + (size_t)t * N + k));
 #pragma unroll
   for (int bb = 0; bb < kHsBT; ++bb) {
@@ -392,6 +401,18 @@ __global__ void k_fuse_key(PrimeTable pt, const u64d* __restrict__ key, const u6
   fk[((size_t)jp * (l + 1) + t) * N + k] = split31(mont_mul(kv, mv, pr.q, pr.qneg_inv));
 }
 
+// out[i] = sum_g part[g][i] mod q(limb of i); rows of nl limbs, limb p_limb -> P
+__global__ void k_sum_parts(PrimeTable pt, const u64d* __restrict__ part, u64d* __restrict__ out, size_t n,
+                            int gs, int nl, int p_limb, int L, int N) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int limb = (int)((i / N) % nl);
+    const u64d q = pt.p[limb == p_limb ? L : limb].q;
+    u64d s = part[i];
+    for (int g = 1; g < gs; ++g) s = add_mod_d(s, part[(size_t)g * n + i], q);
+    out[i] = s;
+  }
+}
+
 // in-place split-31 re-packing of Montgomery multiplier tables
 __global__ void k_split31(u64d* __restrict__ p, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
@@ -418,7 +439,28 @@ void launch_hs_lv(Context& c, const u64d* v, int B, const u64d* D, const HsDiagT
   const double NB = 8.0 * N;
   const double bytes = NB * (t.keyed * LV * 2.0 * (LV + 1) + t.ndiag * LV + B * (LV * (LV + 1.0) + 2.0 * LV) +
                              B * (2.0 * (LV + 1) + 2.0 * LV));
-  LAUNCH_B(c, "k_hs_diag", bytes, k_hs_diag<LV><<<grid, kHsKB, sm, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc));
+  // small batches: split the diagonal chunks over more CTAs (partial sums)
+  const int base = (int)(grid.x * grid.y * grid.z), target = 148 * 32;
+  int gsplit = 1;
+  if (base < target && t.nchunk > 1) gsplit = std::min(t.nchunk, (target + base - 1) / base);
+  if (gsplit == 1) {
+    LAUNCH_B(c, "k_hs_diag", bytes,
+             k_hs_diag<LV><<<grid, kHsKB, sm, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc, 1, 0, 0));
+    return;
+  }
+  const size_t acc_w = (size_t)B * 2 * (LV + 1) * N, cacc_w = (size_t)B * 2 * LV * N;
+  u64d* pa = c.alloc(gsplit * acc_w);
+  u64d* pc = c.alloc(gsplit * cacc_w);
+  grid.x *= gsplit;
+  LAUNCH_B(c, "k_hs_diag", bytes,
+           k_hs_diag<LV><<<grid, kHsKB, sm, c.stream>>>(c.primes, v, D, B, c.L(), N, t, pa, pc, gsplit, acc_w,
+                                                         cacc_w));
+  LAUNCH_B(c, "k_sum_parts", 8.0 * (gsplit + 1) * acc_w,
+           k_sum_parts<<<grid_for(acc_w), kTpb, 0, c.stream>>>(c.primes, pa, acc, acc_w, gsplit, LV + 1, LV, c.L(), N));
+  LAUNCH_B(c, "k_sum_parts", 8.0 * (gsplit + 1) * cacc_w,
+           k_sum_parts<<<grid_for(cacc_w), kTpb, 0, c.stream>>>(c.primes, pc, cacc, cacc_w, gsplit, LV, -1, c.L(), N));
+  c.free(pa);
+  c.free(pc);
 }
 
 }  // namespace

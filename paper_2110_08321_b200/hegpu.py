@@ -115,6 +115,9 @@ def lib():
             "hegpu_square": (i, [vp, vp, vp]),
             "hegpu_conv_packed_forward": (i, [vp, vp, i, f64p, i, vp, i, vp]),
             "hegpu_merge_maps": (i, [vp, vp, i, C.c_int64, vp]),
+            "hegpu_conv_plan_create": (i, [vp, i, f64p, i, vp, i, i, d, pp]),
+            "hegpu_conv_plan_destroy": (None, [vp]),
+            "hegpu_conv_plan_run": (i, [vp, vp, vp, vp]),
             "hegpu_hs_plan_create": (i, [vp, f64p, i, i, i, i, pp]),
             "hegpu_hs_plan_destroy": (None, [vp]),
             "hegpu_hs_plan_rotations": (i, [vp, vp, i]),
@@ -332,6 +335,13 @@ class Context:
                                                    None if b is None else b.ctypes.data, w_used, out.h))
         return out
 
+    def conv_plan(self, ntaps, weights, bias, w_used, level, tap_scale):
+        return ConvPlan(self, ntaps, weights, bias, w_used, level, tap_scale)
+
+    def conv_plan_run(self, plan, taps, out):
+        self.check(lib().hegpu_conv_plan_run(self.h, plan.h, taps.h, out.h))
+        return out
+
     def merge_maps(self, maps, c, w, out):
         self.check(lib().hegpu_merge_maps(self.h, maps.h, c, w, out.h))
         return out
@@ -430,6 +440,26 @@ class Plaintext:
         try:
             if self.h:
                 lib().hegpu_pt_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+class ConvPlan:
+    def __init__(self, ctx, ntaps, weights, bias, w_used, level, tap_scale):
+        w = np.ascontiguousarray(weights, dtype=np.float64).ravel()
+        self.c_out = len(w) // ntaps
+        self._b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float64)
+        h = C.c_void_p()
+        ctx.check(lib().hegpu_conv_plan_create(ctx.h, ntaps, w, self.c_out,
+                                               None if self._b is None else self._b.ctypes.data,
+                                               w_used, level, tap_scale, C.byref(h)))
+        self.ctx, self.h = ctx, h
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().hegpu_conv_plan_destroy(self.h)
                 self.h = None
         except Exception:
             pass

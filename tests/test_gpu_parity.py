@@ -168,6 +168,9 @@ def test_conv_packed_forward(pair):
     want = P.conv_layer(ck, taps, 9, L, W.reshape(4, 9), bias, 100, DELTA)
     assert np.array_equal(got, want)
     assert ctx.total() == (4, 32, 36, 0, 0)   # (c_out, (k^2-1) c_out, k^2 c_out, 0, 0)
+    plan = ctx.conv_plan(9, W.reshape(4, 9), bias, 100, L, DELTA)  # prepared once, same result
+    out2 = ctx.ct(4, L - 1)
+    assert np.array_equal(ctx.conv_plan_run(plan, dt, out2).download(), want)
     ref = HS.ref_conv(img, W, bias, 1)
     per = 2 * (L - 1) * ck.N
     for co in range(4):
@@ -199,7 +202,8 @@ def test_merge_maps(pair):
 
 
 @pytest.mark.parametrize("m,n,skip", [(2, 2, True), (10, 100, True), (32, 300, True), (3, 4, False),
-                                      (7, 500, True), (4, 4, True)])
+                                      (7, 500, True), (4, 4, True),
+                                      (300, 200, True)])  # padding branch, 4 diagonal chunks, split CTAs
 def test_hs_matvec(pair, m, n, skip):
     ctx, ck = pair
     rng = np.random.default_rng(m * 1000 + n)
