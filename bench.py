@@ -47,6 +47,32 @@ def peaks():
         return 6650.0, "fallback"
 
 
+# IMAD.WIDE.U32 issue rate measured on B200 (tools/ubench_int.cu,
+# profiles/r01_int_ubench.txt); one split-30/31 64x64 multiply-accumulate
+# term is 4 IMAD.WIDE.U32
+IMAD_WIDE_PER_CLK_SM = 59.0
+N_SM = 148
+
+
+def int_pipe_roofline(kd, clk_mhz):
+    if not kd.get("modmuls"):
+        return None
+    peak = N_SM * IMAD_WIDE_PER_CLK_SM * clk_mhz * 1e6 / 4 / 1e9
+    return {"achieved": kd["gmodmul_s"], "peak": peak, "unit": "Gmodmul/s", "frac": kd["gmodmul_s"] / peak,
+            "peak_basis": f"{N_SM} SMs x {IMAD_WIDE_PER_CLK_SM} IMAD.WIDE.U32/clk/SM x {clk_mhz:.0f} MHz / 4"}
+
+
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the committed ncu --set full captures (profiles/), or None"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            t = json.load(f)
+        return float(t[kernel]["per_launch_bytes"])
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """SM clocks and throttle reasons sampled (NVML, every 10 ms) during the
     timed region; falls back to one nvidia-smi query if NVML is missing."""
@@ -238,20 +264,28 @@ def run_gpu(args):
     for name in KERNELS:
         ctx.kernel_timer(name)
         net.run(dtaps, out)  # direct launches (the timer brackets each one)
-        kms, kn, kbytes = ctx.kernel_timer_read()
+        kms, kn, kbytes, kops = ctx.kernel_timer_read_ops()
         if kn:
             kernels[name] = {"ms_per_step": kms, "launches": kn, "alg_bytes": kbytes,
                              "gbs": kbytes / (kms / 1e3) / 1e9 if kms > 0 else None,
+                             "modmuls": kops, "gmodmul_s": kops / (kms / 1e3) / 1e9 if kms > 0 else None,
                              "share": kms / ms_max}
     ctx.kernel_timer(None)
     dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
     hbm, which = peaks()
     kd = kernels[dom]
+    traffic = ncu_traffic(dom)
+    clk_mhz = clk.summary()["sm_mhz"] or 1965.0
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kd["gbs"], "peak": hbm, "unit": "GB/s",
-                "frac": kd["gbs"] / hbm, "traffic": None, "peak_source": which,
+                "frac": kd["gbs"] / hbm, "traffic": traffic, "peak_source": which,
+                "alg_bytes_per_launch": kd["alg_bytes"] / kd["launches"],
                 "avg_launch_ms": kd["ms_per_step"] / kd["launches"], "launches_per_step": kd["launches"],
                 "share_of_step": kd["share"],
-                "note": "integer-pipe bound (64-bit modmul); alg bytes per DESIGN.md §5"}
+                # the kernel is bound by the 64-bit multiply-accumulate issue
+                # rate, not HBM: its integer-pipe roofline
+                "int_pipe": int_pipe_roofline(kd, clk_mhz),
+                "note": "alg bytes / modmuls per launch per DESIGN.md §5; traffic = ncu dram bytes per launch "
+                        "(profiles/r01_ncu_traffic.json)"}
 
     # ---- correctness spot check (outside timing): decrypt one output
     host_out = out.download()

@@ -89,6 +89,10 @@ int64_t hegpu_kernel_launches(const hegpu_ctx* ctx);
  * re-arms it. */
 int hegpu_kernel_timer(hegpu_ctx* ctx, const char* name);
 int hegpu_kernel_timer_read(hegpu_ctx* ctx, double* total_ms, int64_t* launches, double* alg_bytes);
+/* as hegpu_kernel_timer_read, plus the launches' algorithmic modular
+ * multiplies (multiply-accumulate terms, NTT butterflies) */
+int hegpu_kernel_timer_read_ops(hegpu_ctx* ctx, double* total_ms, int64_t* launches, double* alg_bytes,
+                                double* modmuls);
 /* CUDA-graph capture of everything the context enqueues between begin and
  * end (e.g. one hegpu_net_run); replay with hegpu_graph_launch.  Metering
  * and launch counters advance only while capturing. */

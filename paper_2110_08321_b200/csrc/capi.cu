@@ -231,10 +231,16 @@ extern "C" int hegpu_kernel_timer(hegpu_ctx* h, const char* name) {
   h->c.ktimer_name = name ? name : "";
   h->c.ktimer_used = 0;
   h->c.ktimer_bytes = 0;
+  h->c.ktimer_ops = 0;
   return HEGPU_OK;
 }
 
 extern "C" int hegpu_kernel_timer_read(hegpu_ctx* h, double* total_ms, int64_t* launches, double* bytes) {
+  return hegpu_kernel_timer_read_ops(h, total_ms, launches, bytes, nullptr);
+}
+
+extern "C" int hegpu_kernel_timer_read_ops(hegpu_ctx* h, double* total_ms, int64_t* launches, double* bytes,
+                                           double* modmuls) {
   if (!h) return HEGPU_ERR_ARG;
   Context& c = h->c;
   return guarded(&c, [&] {
@@ -249,8 +255,10 @@ extern "C" int hegpu_kernel_timer_read(hegpu_ctx* h, double* total_ms, int64_t* 
     if (total_ms) *total_ms = tot;
     if (launches) *launches = (int64_t)c.ktimer_used;
     if (bytes) *bytes = c.ktimer_bytes;
+    if (modmuls) *modmuls = c.ktimer_ops;
     c.ktimer_used = 0;
     c.ktimer_bytes = 0;
+    c.ktimer_ops = 0;
   });
 }
 

@@ -71,6 +71,7 @@ struct Context {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ktimer_events;
   size_t ktimer_used = 0;
   double ktimer_bytes = 0;
+  double ktimer_ops = 0;  // algorithmic modular multiply(-accumulate)s
 
   int N() const { return P->n; }
   int S() const { return P->slots; }
@@ -110,11 +111,13 @@ struct Launch {
   Context& c;
   cudaEvent_t stop = nullptr;
   // bytes: the launch's ALGORITHMIC HBM bytes (each operand read or written
-  // once), accumulated for the timed kernel -> roofline achieved GB/s
-  Launch(Context& cc, const char* name, double bytes = 0.0) : c(cc) {
+  // once), accumulated for the timed kernel -> roofline achieved GB/s;
+  // ops: its algorithmic modular multiplies (MAC terms / butterflies)
+  Launch(Context& cc, const char* name, double bytes = 0.0, double ops = 0.0) : c(cc) {
     ++c.launches;
     if (!c.ktimer_name.empty() && c.ktimer_name == name) {
       c.ktimer_bytes += bytes;
+      c.ktimer_ops += ops;
       if (c.ktimer_used == c.ktimer_events.size()) {
         cudaEvent_t a, b;
         CK(cudaEventCreate(&a));
@@ -139,6 +142,13 @@ struct Launch {
     _launch.end();                               \
   } while (0)
 #define LAUNCH(ctx, name, ...) LAUNCH_B(ctx, name, 0.0, __VA_ARGS__)
+// LAUNCH_BO: as LAUNCH_B plus the launch's algorithmic modular-multiply count
+#define LAUNCH_BO(ctx, name, bytes, ops, ...)             \
+  do {                                                    \
+    ::hegpu::Launch _launch(ctx, name, (bytes), (ops));   \
+    __VA_ARGS__;                                          \
+    _launch.end();                                        \
+  } while (0)
 
 // compact fresh ciphertexts (io.cu): bytes per ct, device expansion
 size_t compact_ct_bytes(Context& c, int level);

@@ -439,12 +439,14 @@ void launch_hs_lv(Context& c, const u64d* v, int B, const u64d* D, const HsDiagT
   const double NB = 8.0 * N;
   const double bytes = NB * (t.keyed * LV * 2.0 * (LV + 1) + t.ndiag * LV + B * (LV * (LV + 1.0) + 2.0 * LV) +
                              B * (2.0 * (LV + 1) + 2.0 * LV));
+  // multiply-accumulates: keyed diagonals x digits x ext limbs x 2, plus c0 x mask
+  const double ops = (double)N * B * (t.keyed * LV * (LV + 1) * 2.0 + t.ndiag * LV);
   // small batches: split the diagonal chunks over more CTAs (partial sums)
   const int base = (int)(grid.x * grid.y * grid.z), target = 148 * 32;
   int gsplit = 1;
   if (base < target && t.nchunk > 1) gsplit = std::min(t.nchunk, (target + base - 1) / base);
   if (gsplit == 1) {
-    LAUNCH_B(c, "k_hs_diag", bytes,
+    LAUNCH_BO(c, "k_hs_diag", bytes, ops,
              k_hs_diag<LV><<<grid, kHsKB, sm, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc, 1, 0, 0));
     return;
   }
@@ -452,7 +454,7 @@ void launch_hs_lv(Context& c, const u64d* v, int B, const u64d* D, const HsDiagT
   u64d* pa = c.alloc(gsplit * acc_w);
   u64d* pc = c.alloc(gsplit * cacc_w);
   grid.x *= gsplit;
-  LAUNCH_B(c, "k_hs_diag", bytes,
+  LAUNCH_BO(c, "k_hs_diag", bytes, ops,
            k_hs_diag<LV><<<grid, kHsKB, sm, c.stream>>>(c.primes, v, D, B, c.L(), N, t, pa, pc, gsplit, acc_w,
                                                          cacc_w));
   LAUNCH_B(c, "k_sum_parts", 8.0 * (gsplit + 1) * acc_w,
@@ -496,7 +498,7 @@ void ks_inner(Context& c, const u64d* D, int B, int l, const KeyRowMap& keys, u6
   dim3 grid((c.N() + kTpb - 1) / kTpb, l + 1, per * tiles);
   double kb = 0;  // distinct keys read once each
   for (int i = 0; i < per && i < B; ++i) kb += 8.0 * l * 2 * (l + 1) * c.N();
-  LAUNCH_B(c, "k_ks_inner", 8.0 * B * (l + 2) * (l + 1) * c.N() + kb,
+  LAUNCH_BO(c, "k_ks_inner", 8.0 * B * (l + 2) * (l + 1) * c.N() + kb, 2.0 * B * l * (l + 1) * c.N(),
            k_ks_inner<<<grid, kTpb, 0, c.stream>>>(c.primes, D, B, l, c.L(), c.N(), keys, acc));
 }
 
@@ -515,7 +517,7 @@ void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, cons
       CK(cudaFuncSetAttribute(k_conv_mac<CO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));      \
       done = sm;                                                                                           \
     }                                                                                                      \
-    LAUNCH_B(c, "k_conv_mac", bytes,                                                                       \
+    LAUNCH_BO(c, "k_conv_mac", bytes, 2.0 * c.N() * l * B * ntaps * c_out,                                 \
              k_conv_mac<CO><<<grid, kTpb, sm, c.stream>>>(c.primes, taps, ntaps, l, c.N(), w, c_out, bias, out)); \
     break;                                                                                                 \
   }
@@ -597,7 +599,8 @@ void eval_merge(Context& c, const CtBatch& maps, int nmaps, const KeyRowMap& km,
   kg.grp_stride = (long)(nmaps * st);
   ks_modup(c, maps.d + st + (size_t)l * N, (long)st, B * G, l, &kg, tmp, D);
   dim3 gi((N + kTpb - 1) / kTpb, l + 1, (B + kKsKT - 1) / kKsKT);
-  LAUNCH_B(c, "k_ks_inner", 8.0 * N * ((double)B * G * l * (l + 1) + 2.0 * G * l * (l + 1) + 2.0 * B * (l + 1)),
+  LAUNCH_BO(c, "k_ks_inner", 8.0 * N * ((double)B * G * l * (l + 1) + 2.0 * G * l * (l + 1) + 2.0 * B * (l + 1)),
+            2.0 * N * B * G * l * (l + 1),
            k_ks_inner_sum<<<gi, kTpb, 0, c.stream>>>(c.primes, D, B, G, l, c.L(), N, km, acc));
   dim3 gc((N + kTpb - 1) / kTpb, 2 * l, B);
   LAUNCH_B(c, "k_merge_c", 8.0 * N * ((double)B * (nmaps + 1) * l + 2.0 * B * l),

@@ -421,7 +421,8 @@ void prep_kernel(K kernel, size_t bytes) {
     static bool prepared = false;                                                                   \
     const size_t smb = ntt_smem(1 << LG);                                                           \
     if (!prepared) { prep_kernel(KERNEL<LG>, smb); prepared = true; }                                \
-    LAUNCH_B(c, #KERNEL, _ntt_bytes, KERNEL<LG><<<(GRID), (1 << LG) >> lr_of(LG), smb, c.stream>>>(__VA_ARGS__)); \
+    LAUNCH_BO(c, #KERNEL, _ntt_bytes, (double)(GRID) * (LG << (LG - 1)),                           \
+              KERNEL<LG><<<(GRID), (1 << LG) >> lr_of(LG), smb, c.stream>>>(__VA_ARGS__));          \
   } while (0)
 
 }  // namespace

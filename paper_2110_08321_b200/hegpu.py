@@ -83,6 +83,7 @@ def lib():
             "hegpu_graph_destroy": (None, [vp]),
             "hegpu_kernel_timer": (i, [vp, C.c_char_p]),
             "hegpu_kernel_timer_read": (i, [vp, C.POINTER(d), C.POINTER(C.c_int64), C.POINTER(d)]),
+            "hegpu_kernel_timer_read_ops": (i, [vp, C.POINTER(d), C.POINTER(C.c_int64), C.POINTER(d), C.POINTER(d)]),
             "hegpu_ct_export_device": (i, [vp, vp, sz]),
             "hegpu_begin_stage": (i, [vp, C.c_char_p]),
             "hegpu_num_stages": (i, [vp]),
@@ -294,6 +295,13 @@ class Context:
         ms, n, b = C.c_double(), C.c_int64(), C.c_double()
         self.check(lib().hegpu_kernel_timer_read(self.h, C.byref(ms), C.byref(n), C.byref(b)))
         return ms.value, n.value, b.value
+
+    def kernel_timer_read_ops(self):
+        """(total device ms, launches, algorithmic bytes, algorithmic modular
+        multiplies) since arming"""
+        ms, n, b, o = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+        self.check(lib().hegpu_kernel_timer_read_ops(self.h, C.byref(ms), C.byref(n), C.byref(b), C.byref(o)))
+        return ms.value, n.value, b.value, o.value
 
     def sync(self):
         self.check(lib().hegpu_sync(self.h))
