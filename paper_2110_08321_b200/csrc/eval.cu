@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kTpb) k_conv_mac(PrimeTable pt, const u64d* __
   const DevPrime pr = pt.p[t];
   const size_t ct_words = (size_t)2 * l * N;
   const u64d* tp = taps + (size_t)b * ntaps * ct_words + (size_t)poly * l * N + (size_t)t * N + k;
-  Acc3 acc[CO];
+  AccC acc[CO];
 #pragma unroll
   for (int c = 0; c < CO; ++c) acc[c].zero();
   int s = 0;
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
   const int nrow = do_c0 ? LV + 1 : LV;  // D digits (+ c0)
   const int ln = LV * N, kp = (LV + 1) * N;
 
-  Acc3 a[kHsBT], c[kHsBT];
+  AccC a[kHsBT], c[kHsBT];
 #pragma unroll
   for (int bb = 0; bb < kHsBT; ++bb) a[bb].zero(), c[bb].zero();
 

@@ -146,4 +146,59 @@ struct Acc3 {  // s0 + s1 2^31 + s2 2^62 (partial), folded into lo:hi:top
   }
 };
 
+struct AccC {  // as Acc3; s0 + s1 2^31 + s2 2^62 kept as 32-bit halves
+  // the PTX carry chains below (mad.lo.cc + madc.hi per product) become one
+  // accumulating IMAD.WIDE.U32 per product, where Acc3's 64-bit mad.wide
+  // chains are re-associated by ptxas into products plus IADD3 trees (14.3 ->
+  // 10.6 SASS per MAC in the HS loop).  Costs registers: used by the HS and
+  // conv kernels; the key-switch inner products keep Acc3 (profiles/r01_notes.md)
+  uint32_t a0l, a0h, a1l, a1h, a2l, a2h;
+  u64d lo, hi;
+  uint32_t top;
+  __device__ __forceinline__ void zero() {
+    a0l = a0h = a1l = a1h = a2l = a2h = 0;
+    lo = hi = 0;
+    top = 0;
+  }
+  __device__ __forceinline__ void mad(u64d xs, u64d ys) {
+    const uint32_t x0 = (uint32_t)xs, x1 = (uint32_t)(xs >> 32);
+    const uint32_t y0 = (uint32_t)ys, y1 = (uint32_t)(ys >> 32);
+    asm("mad.lo.cc.u32 %0, %6, %8, %0;\n\t"
+        "madc.hi.u32 %1, %6, %8, %1;\n\t"
+        "mad.lo.cc.u32 %2, %6, %9, %2;\n\t"
+        "madc.hi.u32 %3, %6, %9, %3;\n\t"
+        "mad.lo.cc.u32 %2, %7, %8, %2;\n\t"
+        "madc.hi.u32 %3, %7, %8, %3;\n\t"
+        "mad.lo.cc.u32 %4, %7, %9, %4;\n\t"
+        "madc.hi.u32 %5, %7, %9, %5;\n\t"
+        : "+r"(a0l), "+r"(a0h), "+r"(a1l), "+r"(a1h), "+r"(a2l), "+r"(a2h)
+        : "r"(x0), "r"(x1), "r"(y0), "r"(y1));
+  }
+  __device__ __forceinline__ void fold() {
+    // (an __int128 formulation measured 9% slower on the HS kernel)
+    const u64d s0 = ((u64d)a0h << 32) | a0l, s1 = ((u64d)a1h << 32) | a1l, s2 = ((u64d)a2h << 32) | a2l;
+    const u64d l1 = s1 << 31, h1 = s1 >> 33, l2 = s2 << 62, h2 = s2 >> 2;
+    asm("add.cc.u64 %0, %0, %3;\n\t"
+        "addc.cc.u64 %1, %1, 0;\n\t"
+        "addc.u32 %2, %2, 0;\n\t"
+        "add.cc.u64 %0, %0, %4;\n\t"
+        "addc.cc.u64 %1, %1, %5;\n\t"
+        "addc.u32 %2, %2, 0;\n\t"
+        "add.cc.u64 %0, %0, %6;\n\t"
+        "addc.cc.u64 %1, %1, %7;\n\t"
+        "addc.u32 %2, %2, 0;\n\t"
+        : "+l"(lo), "+l"(hi), "+r"(top)
+        : "l"(s0), "l"(l1), "l"(h1), "l"(l2), "l"(h2));
+    a0l = a0h = a1l = a1h = a2l = a2h = 0;
+  }
+  // (top:hi:lo) * 2^-64 mod q  (products of standard x Montgomery operands)
+  __device__ __forceinline__ u64d reduce(const DevPrime& pr) {
+    fold();
+    u64d x = mont_reduce128(hi, (u64d)top, pr.q, pr.qneg_inv);
+    x = mont_mul(x, pr.r2_mod, pr.q, pr.qneg_inv);
+    const u64d y = mont_reduce128(lo, 0ull, pr.q, pr.qneg_inv);
+    return add_mod_d(x, y, pr.q);
+  }
+};
+
 }  // namespace hegpu
