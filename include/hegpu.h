@@ -211,6 +211,10 @@ int hegpu_net_create(hegpu_ctx* ctx, const hegpu_net_spec* spec, const double* c
 void hegpu_net_destroy(hegpu_net* net);
 /* device-resident run: taps = count B*ntaps at the top level */
 int hegpu_net_run(hegpu_net* net, const hegpu_ct* taps, hegpu_ct* out);
+/* the same on device-resident compact taps (batch x hegpu_net_compact_image_bytes
+ * bytes, as hegpu_net_encrypt_image_compact writes them): the conv MAC
+ * decodes c0 and regenerates c1 on the fly */
+int hegpu_net_run_compact(hegpu_net* net, const void* dev_taps, int batch, hegpu_ct* out);
 /* end-to-end run from host buffers (wire format taps [B][ntaps][2][L][N]
  * -> output cts [B][2][1][N]); includes both host<->device copies */
 int hegpu_net_run_host(hegpu_net* net, const uint64_t* host_taps, int batch, uint64_t* host_out);
@@ -224,6 +228,14 @@ int hegpu_net_encrypt_image_compact(hegpu_net* net, const double* image, uint64_
  * the batch is processed in chunks of `chunk` images (0 = automatic) with the
  * next chunk's host->device copy overlapping the current chunk's compute */
 int hegpu_net_run_host_compact(hegpu_net* net, const uint8_t* host_taps, int batch, int chunk, uint64_t* host_out);
+/* the same pass without waiting: returns once the work is enqueued, so the
+ * next submit's host->device copies overlap this pass's compute (serving
+ * loop).  host_taps and host_out must stay valid (and host_out unread) until
+ * hegpu_net_wait; at most two passes may be in flight per net (staging is
+ * double-buffered; a third submit queues behind the first). */
+int hegpu_net_submit_host_compact(hegpu_net* net, const uint8_t* host_taps, int batch, int chunk,
+                                  uint64_t* host_out);
+int hegpu_net_wait(hegpu_net* net);
 /* logits: decrypt + decode output ct (wire) into m_last values */
 int hegpu_net_decrypt_logits(hegpu_net* net, const uint64_t* out_ct, double* logits);
 double hegpu_net_output_scale(const hegpu_net* net);

@@ -153,6 +153,8 @@ struct Launch {
 // compact fresh ciphertexts (io.cu): bytes per ct, device expansion
 size_t compact_ct_bytes(Context& c, int level);
 void launch_expand_compact(Context& c, const uint8_t* src, int count, int level, u64d* dst);
+struct CompactLayout;
+CompactLayout compact_layout(Context& c, int level);
 // twiddle tables [np][fwd, inv][N] of (w, w') pairs -> c.d_tw
 void upload_twiddles(Context& c);
 // coefficient rows -> slot-order NTT rows; row r uses limb r % nl (limb l ->

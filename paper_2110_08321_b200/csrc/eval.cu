@@ -199,11 +199,21 @@ __global__ void k_merge_c(PrimeTable pt, const u64d* __restrict__ maps, int nimg
   C[(size_t)img * st + (size_t)p * l * N + (size_t)t * N + k] = v;
 }
 
+// tap source of the conv MAC: tap s of this thread's (image, poly, limb,
+// position) in a full device ciphertext batch
+struct TapsFull {
+  const u64d* taps;
+  __device__ u64d operator()(int s, int b, int ntaps, int poly, int t, int l, int k, int N) const {
+    const size_t ct_words = (size_t)2 * l * N;
+    return __ldg(taps + ((size_t)b * ntaps + s) * ct_words + (size_t)poly * l * N + (size_t)t * N + k);
+  }
+};
+
 // conv-pack MAC (convlower.cpp:39-74): CO output maps per thread, taps
-// streamed 8 at a time so each thread keeps 8 independent loads in flight.
-template <int CO>
-__global__ void __launch_bounds__(kTpb) k_conv_mac(PrimeTable pt, const u64d* __restrict__ taps, int ntaps, int l,
-                                                   int N, const u64d* __restrict__ w, int c_out,
+// streamed 4 at a time so each thread keeps independent loads in flight.
+template <int CO, class Taps>
+__global__ void __launch_bounds__(kTpb) k_conv_mac(PrimeTable pt, Taps taps, int ntaps, int l, int N,
+                                                   const u64d* __restrict__ w, int c_out,
                                                    const u64d* __restrict__ bias, u64d* __restrict__ out) {
   extern __shared__ u64d ws[];  // [CO][ntaps] split-31 Montgomery scalars of this (t, group)
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -219,7 +229,7 @@ __global__ void __launch_bounds__(kTpb) k_conv_mac(PrimeTable pt, const u64d* __
   if (k >= N) return;
   const DevPrime pr = pt.p[t];
   const size_t ct_words = (size_t)2 * l * N;
-  const u64d* tp = taps + (size_t)b * ntaps * ct_words + (size_t)poly * l * N + (size_t)t * N + k;
+  auto tap = [&](int s) -> u64d { return taps(s, b, ntaps, poly, t, l, k, N); };
   AccC acc[CO];
 #pragma unroll
   for (int c = 0; c < CO; ++c) acc[c].zero();
@@ -228,7 +238,7 @@ __global__ void __launch_bounds__(kTpb) k_conv_mac(PrimeTable pt, const u64d* __
   for (; s + 4 <= ntaps; s += 4) {
     u64d x[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = split31(__ldg(tp + (size_t)(s + u) * ct_words));
+    for (int u = 0; u < 4; ++u) x[u] = split31(tap(s + u));
 #pragma unroll
     for (int c = 0; c < CO; ++c) {
 #pragma unroll
@@ -237,7 +247,7 @@ __global__ void __launch_bounds__(kTpb) k_conv_mac(PrimeTable pt, const u64d* __
     }
   }
   for (; s < ntaps; ++s) {
-    const u64d x = split31(__ldg(tp + (size_t)s * ct_words));
+    const u64d x = split31(tap(s));
 #pragma unroll
     for (int c = 0; c < CO; ++c) acc[c].mad(x, ws[c * ntaps + s]);
   }
@@ -502,10 +512,11 @@ void ks_inner(Context& c, const u64d* D, int B, int l, const KeyRowMap& keys, u6
            k_ks_inner<<<grid, kTpb, 0, c.stream>>>(c.primes, D, B, l, c.L(), c.N(), keys, acc));
 }
 
-void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, const u64d* w, int c_out,
-                     const u64d* bias, u64d* out) {
+template <class Taps>
+void launch_conv_mac_t(Context& c, const Taps& taps, double tap_bytes, int B, int ntaps, int l, const u64d* w,
+                       int c_out, const u64d* bias, u64d* out) {
   // taps read once, maps written once, bias plaintexts read once
-  const double bytes = 8.0 * c.N() * l * (2.0 * B * ntaps + 2.0 * B * c_out + c_out);
+  const double bytes = tap_bytes + 8.0 * c.N() * l * (2.0 * B * c_out + c_out);
   const int co = c_out < 8 ? c_out : 8;  // output maps per thread (exact for c_out <= 8)
   dim3 grid((c.N() + kTpb - 1) / kTpb, 2 * l, B * ((c_out + co - 1) / co));
   const size_t sm = (size_t)co * ntaps * 8;
@@ -514,11 +525,11 @@ void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, cons
   case CO: {                                                                                               \
     static size_t done = 0;                                                                                \
     if (sm > 48 * 1024 && sm > done) {                                                                     \
-      CK(cudaFuncSetAttribute(k_conv_mac<CO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));      \
+      CK(cudaFuncSetAttribute(k_conv_mac<CO, Taps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
       done = sm;                                                                                           \
     }                                                                                                      \
     LAUNCH_BO(c, "k_conv_mac", bytes, 2.0 * c.N() * l * B * ntaps * c_out,                                 \
-             k_conv_mac<CO><<<grid, kTpb, sm, c.stream>>>(c.primes, taps, ntaps, l, c.N(), w, c_out, bias, out)); \
+             k_conv_mac<CO, Taps><<<grid, kTpb, sm, c.stream>>>(c.primes, taps, ntaps, l, c.N(), w, c_out, bias, out)); \
     break;                                                                                                 \
   }
   switch (co) {
@@ -526,6 +537,11 @@ void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, cons
     default: fail(HEGPU_ERR_ARG, "conv: bad c_out");
   }
 #undef CONV_GO
+}
+
+void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, const u64d* w, int c_out,
+                     const u64d* bias, u64d* out) {
+  launch_conv_mac_t(c, TapsFull{taps}, 8.0 * c.N() * l * 2.0 * B * ntaps, B, ntaps, l, w, c_out, bias, out);
 }
 
 void launch_split31(Context& c, u64d* p, size_t words) {

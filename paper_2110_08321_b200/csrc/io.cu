@@ -7,57 +7,45 @@
 // the per-limb a-stream keys; this kernel unpacks c0, regenerates a, and
 // writes the device layout (slot order) directly -- 2.9x fewer bytes over
 // PCIe for the config-0 taps, bit-identical ciphertexts.
+#include "compact.cuh"
 #include "engine.hpp"
 
 namespace hegpu {
 
 namespace {
 
-__device__ __forceinline__ u64d sm_mix_d(u64d z) {
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  return z ^ (z >> 31);
+// c0 rows (ct, t): every slot-order position gathers its nb-byte coefficient
+// from the packed limb (wire order) with two aligned 8-byte loads; a limb is
+// <= 64 KB, so after its first touch the gathers are served from L2
+__global__ void k_expand_c0(const uint8_t* __restrict__ src, u64d* __restrict__ dst, CompactLayout lay,
+                            const uint32_t* __restrict__ slot_src, int N) {
+  const int l = lay.level;
+  const int row = blockIdx.y, t = row % l, c = row / l;
+  const int nb = lay.nb[t];
+  const u64d* limb = reinterpret_cast<const u64d*>(src + (size_t)c * lay.ct_bytes + lay.off[t]);
+  const int words = (N * nb) >> 3;
+  u64d* out = dst + ((size_t)c * 2 * l + t) * N;
+  for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < N; pos += gridDim.x * blockDim.x)
+    out[pos] = compact_c0(limb, (int)__ldg(slot_src + pos) * nb, nb, words);
 }
 
-struct CompactLayout {
-  int level;
-  int nb[HEGPU_MAX_PRIMES];       // bytes per coefficient of limb t
-  long off[HEGPU_MAX_PRIMES];     // byte offset of limb t inside one compact ct
-  long ct_bytes;
-};
-
-// rows (ct, p, t); positions p in slot order
-__global__ void k_expand_compact(const uint8_t* __restrict__ src, u64d* __restrict__ dst, CompactLayout lay,
-                                 PrimeTable pt, const uint32_t* __restrict__ slot_src, int N) {
+// c1 = a rows (ct, t): regenerated from the limb's a-stream key
+__global__ void k_expand_a(const uint8_t* __restrict__ src, u64d* __restrict__ dst, CompactLayout lay,
+                           PrimeTable pt, const uint32_t* __restrict__ slot_src, int N) {
   const int l = lay.level;
-  const int row = blockIdx.y, t = row % l, p = (row / l) & 1, c = row / (2 * l);
-  const uint8_t* base = src + (size_t)c * lay.ct_bytes;
-  u64d* out = dst + ((size_t)c * 2 * l + (size_t)p * l + t) * N;
+  const int row = blockIdx.y, t = row % l, c = row / l;
+  const u64d key = reinterpret_cast<const u64d*>(src + (size_t)c * lay.ct_bytes)[t];
   const u64d q = pt.p[t].q;
-  if (p == 0) {
-    const int nb = lay.nb[t];
-    const uint8_t* limb = base + lay.off[t];
-    for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < N; pos += gridDim.x * blockDim.x) {
-      const uint8_t* b = limb + (size_t)__ldg(slot_src + pos) * nb;
-      u64d v = 0;
-      for (int i = nb - 1; i >= 0; --i) v = (v << 8) | __ldg(b + i);
-      out[pos] = v;
-    }
-  } else {
-    const u64d key = reinterpret_cast<const u64d*>(base)[t];
-    for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < N; pos += gridDim.x * blockDim.x) {
-      const u64d k = __ldg(slot_src + pos);
-      const u64d w = sm_mix_d(key + (k + 1) * 0x9E3779B97F4A7C15ull);
-      out[pos] = __umul64hi(w, q);
-    }
-  }
+  u64d* out = dst + ((size_t)c * 2 * l + l + t) * N;
+  for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < N; pos += gridDim.x * blockDim.x)
+    out[pos] = compact_a(key, __ldg(slot_src + pos), q);
 }
 
 }  // namespace
 
 size_t compact_ct_bytes(Context& c, int level) { return c.client->compact_bytes(level); }
 
-void launch_expand_compact(Context& c, const uint8_t* src, int count, int level, u64d* dst) {
+CompactLayout compact_layout(Context& c, int level) {
   CompactLayout lay{};
   lay.level = level;
   long off = (long)level * 8;
@@ -67,9 +55,19 @@ void launch_expand_compact(Context& c, const uint8_t* src, int count, int level,
     off += (long)c.N() * lay.nb[t];
   }
   lay.ct_bytes = off;
-  dim3 grid((c.N() + 255) / 256 < 8 ? (c.N() + 255) / 256 : 8, (unsigned)(count * 2 * level));
-  LAUNCH_B(c, "k_expand_compact", (double)count * (off + 16.0 * level * c.N()),
-           k_expand_compact<<<grid, 256, 0, c.stream>>>(src, dst, lay, c.primes, c.d_slot_src, c.N()));
+  return lay;
+}
+
+void launch_expand_compact(Context& c, const uint8_t* src, int count, int level, u64d* dst) {
+  const CompactLayout lay = compact_layout(c, level);
+  const long off = lay.ct_bytes;
+  const int N = c.N();
+  dim3 grid((N + 255) / 256 < 8 ? (N + 255) / 256 : 8, (unsigned)(count * level));
+  const double c0_bytes = (double)count * (off - 8.0 * level + 8.0 * level * N);
+  LAUNCH_B(c, "k_expand_compact", c0_bytes,
+           k_expand_c0<<<grid, 256, 0, c.stream>>>(src, dst, lay, c.d_slot_src, N));
+  LAUNCH_B(c, "k_expand_compact", (double)count * (8.0 * level + 8.0 * level * N),
+           k_expand_a<<<grid, 256, 0, c.stream>>>(src, dst, lay, c.primes, c.d_slot_src, N));
 }
 
 }  // namespace hegpu

@@ -79,10 +79,26 @@ ConvLayer::~ConvLayer() {
   cudaFree(bias);
 }
 
+void ConvLayer::mac(Context& c, const CtBatch& taps, CtBatch& prod) {
+  const int B = taps.count / ntaps;
+  launch_conv_mac(c, taps.d, B, ntaps, level, w, c_out, bias, prod.d);
+  prod.scale = taps.scale * (double)c.P->q(level - 1);
+}
+
+void ConvLayer::mac_compact(Context& c, const uint8_t* taps, int B, double tap_scale, CtBatch& prod) {
+  // measured: expanding into full taps and streaming them through the MAC
+  // beats decoding c0 / hashing c1 inside the register-heavy MAC kernel
+  u64d* full = c.alloc((size_t)B * ntaps * 2 * level * c.N());
+  launch_expand_compact(c, taps, B * ntaps, level, full);
+  launch_conv_mac(c, full, B, ntaps, level, w, c_out, bias, prod.d);
+  c.free(full);
+  prod.scale = tap_scale * (double)c.P->q(level - 1);
+}
+
 void ConvLayer::run(Context& c, const CtBatch& taps, CtBatch& maps) {
   const int B = taps.count / ntaps, l = level, N = c.N();
-  CtBatch prod{&c, B * c_out, l, taps.scale * (double)c.P->q(l - 1), c.alloc((size_t)B * c_out * 2 * l * N)};
-  launch_conv_mac(c, taps.d, B, ntaps, l, w, c_out, bias, prod.d);
+  CtBatch prod{&c, B * c_out, l, 0, c.alloc((size_t)B * c_out * 2 * l * N)};
+  mac(c, taps, prod);
   eval_rescale(c, prod, maps);
   maps.scale = taps.scale;
   c.free(prod.d);

@@ -22,7 +22,12 @@ struct ConvLayer {
   ~ConvLayer();
   ConvLayer(const ConvLayer&) = delete;
   ConvLayer& operator=(const ConvLayer&) = delete;
-  void run(Context& c, const CtBatch& taps, CtBatch& maps);
+  void run(Context& c, const CtBatch& taps, CtBatch& maps);  // mac + rescale
+  // the multiply-accumulate alone: prod [B][c_out] at `level` (scale x q_top)
+  void mac(Context& c, const CtBatch& taps, CtBatch& prod);
+  // the same on B images of compact fresh taps (device bytes at `level`):
+  // expanded into full ciphertexts first (io.cu), then the MAC
+  void mac_compact(Context& c, const uint8_t* taps, int B, double tap_scale, CtBatch& prod);
   Context* ctx;
 };
 

@@ -33,18 +33,18 @@ struct hegpu_net {
   // compact staging, a copy stream and its events
   uint8_t* stage[2] = {nullptr, nullptr};
   size_t stage_bytes = 0;
+  int next_stage = 0;
   cudaStream_t copy = nullptr;
-  cudaEvent_t copied[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
-  std::vector<cudaEvent_t> sub_events;  // one per input sub-chunk
+  cudaEvent_t freed[2] = {nullptr, nullptr};  // compute done reading stage[s]
+  std::vector<cudaEvent_t> sub_events[2];     // per stage buffer, one per input sub-chunk
   ~hegpu_net() {
     for (auto& p : plans) p.release();
     for (u64d* b : bias) cudaFree(b);
     for (int s = 0; s < 2; ++s) {
       if (stage[s]) cudaFree(stage[s]);
-      if (copied[s]) cudaEventDestroy(copied[s]);
       if (freed[s]) cudaEventDestroy(freed[s]);
+      for (cudaEvent_t e : sub_events[s]) cudaEventDestroy(e);
     }
-    for (cudaEvent_t e : sub_events) cudaEventDestroy(e);
     if (copy) cudaStreamDestroy(copy);
   }
 };
@@ -77,15 +77,18 @@ struct Scratch {
 };
 
 // Conv1: ConvPack (netcompile.cpp:321-331); maps [B][c_out] at top-1
-void run_conv(hegpu_net& net, const CtBatch& taps, CtBatch& maps) {
+void conv_meter(hegpu_net& net, int B) {
   Context& c = *net.c;
   const hegpu_net_spec& s = net.spec;
-  const int B = taps.count / net.ntaps;
   c.meter.begin("Conv1");
-  net.conv->run(c, taps, maps);
   c.meter.bump(HEGPU_MUL_PC, (int64_t)B * net.ntaps * s.c_out);
   c.meter.bump(HEGPU_ADD_CC, (int64_t)B * (net.ntaps - 1) * s.c_out);
   c.meter.bump(HEGPU_ADD_PC, (int64_t)B * s.c_out);
+}
+
+void run_conv(hegpu_net& net, const CtBatch& taps, CtBatch& maps) {
+  conv_meter(net, taps.count / net.ntaps);
+  net.conv->run(*net.c, taps, maps);
 }
 
 void run_after_conv(hegpu_net& net, const CtBatch& mb, CtBatch& out);
@@ -229,6 +232,27 @@ extern "C" int hegpu_net_run(hegpu_net* net, const hegpu_ct* taps, hegpu_ct* out
   });
 }
 
+extern "C" int hegpu_net_run_compact(hegpu_net* net, const void* dev_taps, int batch, hegpu_ct* out) {
+  if (!net || !dev_taps || !out || batch < 1) return HEGPU_ERR_ARG;
+  Context& c = *net->c;
+  return guarded(&c, [&] {
+    need(out->b.count == batch && out->b.level == net->top - 1 - 2 * net->spec.n_dense, HEGPU_ERR_SHAPE,
+         "net_run_compact: bad output handle");
+    const int L = net->top, N = c.N();
+    Scratch prod(c, (size_t)batch * net->spec.c_out * 2 * L * N);
+    Scratch maps(c, (size_t)batch * net->spec.c_out * 2 * (L - 1) * N);
+    CtBatch pb{&c, batch * net->spec.c_out, L, 0, prod.p};
+    conv_meter(*net, batch);
+    net->conv->mac_compact(c, static_cast<const uint8_t*>(dev_taps), batch, net->tap_scale, pb);
+    CtBatch mb{&c, batch * net->spec.c_out, L - 1, 0, maps.p};
+    eval_rescale(c, pb, mb);
+    mb.scale = net->tap_scale;
+    CtBatch o = out->b;
+    run_after_conv(*net, mb, o);
+    out->b.scale = o.scale;
+  });
+}
+
 extern "C" int hegpu_net_run_host(hegpu_net* net, const uint64_t* host_taps, int batch, uint64_t* host_out) {
   if (!net || !host_taps || !host_out || batch < 1) return HEGPU_ERR_ARG;
   Context& c = *net->c;
@@ -254,68 +278,108 @@ extern "C" size_t hegpu_net_compact_image_bytes(const hegpu_net* net) {
   return net ? (size_t)net->ntaps * net->c->client->compact_bytes(net->top) : 0;
 }
 
+#ifndef HEGPU_NET_SUBCHUNK
+#define HEGPU_NET_SUBCHUNK 16  // images per upload sub-chunk (expand + conv MAC granularity)
+#endif
+
+namespace {
+
+// enqueue one host-input pass (no host synchronisation): the staging buffer
+// alternates between calls so call k+1's uploads overlap call k's compute
+void enqueue_host_compact(hegpu_net& n, const uint8_t* host, int batch, int chunk, uint64_t* host_out) {
+  Context& c = *n.c;
+  const int N = c.N(), L = n.top, lo = n.top - 1 - 2 * n.spec.n_dense;
+  // two-level pipeline: the copy stream streams every image's compact taps
+  // in sub-chunks of c1 images; the compute stream expands + convolves each
+  // sub-chunk as soon as it lands, and runs merge..Dense on chunks of c2.
+  const int c2 = chunk > 0 ? std::min(chunk, batch) : std::min(batch, 32);
+  const int c1 = std::min(c2, HEGPU_NET_SUBCHUNK);
+  const size_t per_img = hegpu_net_compact_image_bytes(&n);
+  const size_t out_words = (size_t)2 * lo * N;
+  const size_t map_words = (size_t)2 * (L - 1) * N;
+  if (n.stage_bytes < per_img * batch) {
+    CK(cudaDeviceSynchronize());
+    for (int s = 0; s < 2; ++s) {
+      if (n.stage[s]) cudaFree(n.stage[s]);
+      n.stage[s] = nullptr;
+      CK(cudaMalloc((void**)&n.stage[s], per_img * batch));
+    }
+    n.stage_bytes = per_img * batch;
+  }
+  if (!n.copy) {
+    CK(cudaStreamCreateWithFlags(&n.copy, cudaStreamNonBlocking));
+    for (int s = 0; s < 2; ++s) CK(cudaEventCreateWithFlags(&n.freed[s], cudaEventDisableTiming));
+  }
+  const int cur = n.next_stage;
+  n.next_stage ^= 1;
+  uint8_t* stage = n.stage[cur];
+  const int nsub = (batch + c1 - 1) / c1;
+  auto& subs = n.sub_events[cur];
+  while ((int)subs.size() < nsub) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    subs.push_back(e);
+  }
+  // this staging buffer is free once the call that used it last has expanded
+  CK(cudaStreamWaitEvent(n.copy, n.freed[cur], 0));
+  for (int j = 0; j < nsub; ++j) {
+    const int b0 = j * c1, nb = std::min(c1, batch - b0);
+    CK(cudaMemcpyAsync(stage + (size_t)b0 * per_img, host + (size_t)b0 * per_img, per_img * nb,
+                       cudaMemcpyHostToDevice, n.copy));
+    CK(cudaEventRecord(subs[j], n.copy));
+  }
+  // each sub-chunk is multiply-accumulated straight from its compact bytes
+  // as it lands; the conv rescale runs once per chunk (full-width NTT grids)
+  Scratch prod(c, (size_t)c2 * n.spec.c_out * 2 * L * N);
+  Scratch maps(c, (size_t)c2 * n.spec.c_out * map_words);
+  Scratch o(c, (size_t)c2 * out_words);
+  Scratch wire(c, (size_t)c2 * out_words);
+  for (int m0 = 0; m0 < batch; m0 += c2) {
+    const int nm = std::min(c2, batch - m0);
+    CtBatch pb{&c, nm * n.spec.c_out, L, 0, prod.p};
+    for (int b0 = m0; b0 < m0 + nm; b0 += c1) {
+      const int nb = std::min(c1, m0 + nm - b0);
+      CK(cudaStreamWaitEvent(c.stream, subs[b0 / c1], 0));
+      CtBatch sb{&c, nb * n.spec.c_out, L, 0, prod.p + (size_t)(b0 - m0) * n.spec.c_out * 2 * L * N};
+      n.conv->mac_compact(c, stage + (size_t)b0 * per_img, nb, n.tap_scale, sb);
+      pb.scale = sb.scale;
+    }
+    if (m0 + nm >= batch) CK(cudaEventRecord(n.freed[cur], c.stream));  // last read of the staging
+    conv_meter(n, nm);
+    CtBatch rb{&c, nm * n.spec.c_out, L - 1, 0, maps.p};
+    eval_rescale(c, pb, rb);
+    CtBatch mb{&c, nm * n.spec.c_out, L - 1, n.tap_scale, maps.p};
+    CtBatch ob{&c, nm, lo, 0, o.p};
+    run_after_conv(n, mb, ob);
+    launch_slot_to_wire(c, o.p, wire.p, (size_t)nm * 2 * lo, 0, lo, -1);
+    CK(cudaMemcpyAsync(host_out + (size_t)m0 * out_words, wire.p, (size_t)nm * out_words * 8,
+                       cudaMemcpyDeviceToHost, c.stream));
+  }
+}
+
+}  // namespace
+
 extern "C" int hegpu_net_run_host_compact(hegpu_net* net, const uint8_t* host, int batch, int chunk,
                                           uint64_t* host_out) {
   if (!net || !host || !host_out || batch < 1) return HEGPU_ERR_ARG;
   Context& c = *net->c;
   return guarded(&c, [&] {
-    const int N = c.N(), L = net->top, lo = net->top - 1 - 2 * net->spec.n_dense;
-    // two-level pipeline: the copy stream streams every image's compact taps
-    // in sub-chunks of c1 images; the compute stream expands + convolves each
-    // sub-chunk as soon as it lands, and runs merge..Dense on chunks of c2.
-    const int c2 = chunk > 0 ? std::min(chunk, batch) : std::min(batch, 32);
-    const int c1 = std::min(c2, 4);
-    const size_t per_img = hegpu_net_compact_image_bytes(net);
-    const size_t out_words = (size_t)2 * lo * N;
-    const size_t map_words = (size_t)2 * (L - 1) * N;
-    if (net->stage_bytes < per_img * batch) {
-      CK(cudaStreamSynchronize(c.stream));
-      if (net->stage[0]) cudaFree(net->stage[0]);
-      CK(cudaMalloc((void**)&net->stage[0], per_img * batch));
-      net->stage_bytes = per_img * batch;
-    }
-    if (!net->copy) {
-      CK(cudaStreamCreateWithFlags(&net->copy, cudaStreamNonBlocking));
-      CK(cudaEventCreateWithFlags(&net->freed[0], cudaEventDisableTiming));
-    }
-    const int nsub = (batch + c1 - 1) / c1;
-    while ((int)net->sub_events.size() < nsub) {
-      cudaEvent_t e;
-      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      net->sub_events.push_back(e);
-    }
-    // staging is reused across calls: copies start once earlier compute is done
-    CK(cudaEventRecord(net->freed[0], c.stream));
-    CK(cudaStreamWaitEvent(net->copy, net->freed[0], 0));
-    for (int j = 0; j < nsub; ++j) {
-      const int b0 = j * c1, nb = std::min(c1, batch - b0);
-      CK(cudaMemcpyAsync(net->stage[0] + (size_t)b0 * per_img, host + (size_t)b0 * per_img, per_img * nb,
-                         cudaMemcpyHostToDevice, net->copy));
-      CK(cudaEventRecord(net->sub_events[j], net->copy));
-    }
-    Scratch taps(c, (size_t)c1 * net->ntaps * 2 * L * N);
-    Scratch maps(c, (size_t)c2 * net->spec.c_out * map_words);
-    Scratch o(c, (size_t)c2 * out_words);
-    Scratch wire(c, (size_t)c2 * out_words);
-    for (int m0 = 0; m0 < batch; m0 += c2) {
-      const int nm = std::min(c2, batch - m0);
-      for (int b0 = m0; b0 < m0 + nm; b0 += c1) {
-        const int nb = std::min(c1, m0 + nm - b0);
-        CK(cudaStreamWaitEvent(c.stream, net->sub_events[b0 / c1], 0));
-        launch_expand_compact(c, net->stage[0] + (size_t)b0 * per_img, nb * net->ntaps, L, taps.p);
-        CtBatch tb{&c, nb * net->ntaps, L, net->tap_scale, taps.p};
-        CtBatch mb{&c, nb * net->spec.c_out, L - 1, 0, maps.p + (size_t)(b0 - m0) * net->spec.c_out * map_words};
-        run_conv(*net, tb, mb);
-      }
-      CtBatch mb{&c, nm * net->spec.c_out, L - 1, net->tap_scale, maps.p};
-      CtBatch ob{&c, nm, lo, 0, o.p};
-      run_after_conv(*net, mb, ob);
-      launch_slot_to_wire(c, o.p, wire.p, (size_t)nm * 2 * lo, 0, lo, -1);
-      CK(cudaMemcpyAsync(host_out + (size_t)m0 * out_words, wire.p, (size_t)nm * out_words * 8,
-                         cudaMemcpyDeviceToHost, c.stream));
-    }
+    enqueue_host_compact(*net, host, batch, chunk, host_out);
     CK(cudaStreamSynchronize(c.stream));
   });
+}
+
+extern "C" int hegpu_net_submit_host_compact(hegpu_net* net, const uint8_t* host, int batch, int chunk,
+                                             uint64_t* host_out) {
+  if (!net || !host || !host_out || batch < 1) return HEGPU_ERR_ARG;
+  Context& c = *net->c;
+  return guarded(&c, [&] { enqueue_host_compact(*net, host, batch, chunk, host_out); });
+}
+
+extern "C" int hegpu_net_wait(hegpu_net* net) {
+  if (!net) return HEGPU_ERR_ARG;
+  Context& c = *net->c;
+  return guarded(&c, [&] { CK(cudaStreamSynchronize(c.stream)); });
 }
 
 extern "C" int hegpu_net_encrypt_image_compact(hegpu_net* net, const double* image, uint64_t nonce,

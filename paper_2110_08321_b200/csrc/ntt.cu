@@ -27,7 +27,10 @@ namespace {
 // registers per thread: R = 2^lr words.  R = 16 measured faster than R = 32
 // on B200 (2 CTAs x 512 threads per SM for N = 2^13 beat 2 x 256 threads
 // with 128 registers each; profiles/r01_notes.md)
-__host__ __device__ constexpr int lr_of(int logn) { return logn > 0 ? 4 : 4; }
+#ifndef HEGPU_NTT_LR13
+#define HEGPU_NTT_LR13 4
+#endif
+__host__ __device__ constexpr int lr_of(int logn) { return logn <= 13 ? HEGPU_NTT_LR13 : 4; }
 constexpr int kMinLogN = 5, kMaxLogN = 14;
 
 __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
@@ -261,8 +264,18 @@ __device__ __forceinline__ const ulonglong2* twi(const TwArgs& t, int pi, int N)
   return t.tw + ((size_t)pi * 2 + 1) * N;
 }
 
+// one pass over a row: R = 2^lr words per thread, compile-time trip count so
+// the loads of all R iterations are issued together (measured: helps the
+// drop-limb epilogue, costs spills in the other row kernels)
+#define ROW_LOOP(P)                                         \
+  _Pragma("unroll") for (int _e = 0; _e < (1 << lr_of(LOGN)); ++_e) \
+    if (const int P = _e * (N >> lr_of(LOGN)) + (int)threadIdx.x; true)
+
 // two CTAs per SM for N <= 8192 (<= 64 registers per thread)
-#define NTT_BOUNDS __launch_bounds__((1 << LOGN) / (1 << lr_of(LOGN)), (LOGN <= 13 ? 2 : 1))
+#ifndef HEGPU_NTT_MINB13
+#define HEGPU_NTT_MINB13 2
+#endif
+#define NTT_BOUNDS __launch_bounds__((1 << LOGN) / (1 << lr_of(LOGN)), (LOGN <= 13 ? HEGPU_NTT_MINB13 : 1))
 
 // ------------------------------------------------------------ kernels
 template <int LOGN>
@@ -353,7 +366,7 @@ __global__ void NTT_BOUNDS k_drop_ntt(TwArgs ta, PrimeTable pt, const u64d* __re
   const bool add = (a.add_mask >> p) & 1;
   const u64d* ad = add ? a.add + b * a.add_b + p * a.add_p + (size_t)t * N : nullptr;
   const int sh = (use_shift && p == 0) ? km.shift[b % km.period] : 0;
-  for (int pos = threadIdx.x; pos < N; pos += blockDim.x) {
+  ROW_LOOP(pos) {
     u64d v = shoup_mul_d(sub_mod_d(in[pos], sm[pad(__ldg(ta.slot_src + pos))], q), iv, ivp, q);
     if (add) v = add_mod_d(v, ad[sh ? shifted(pos, sh, S) : pos], q);
     out[pos] = v;

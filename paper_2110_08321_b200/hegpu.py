@@ -127,6 +127,7 @@ def lib():
             "hegpu_net_create": (i, [vp, C.POINTER(NetSpec), f64p, f64p, vp, vp, pp]),
             "hegpu_net_destroy": (None, [vp]),
             "hegpu_net_run": (i, [vp, vp, vp]),
+            "hegpu_net_run_compact": (i, [vp, vp, i, vp]),
             "hegpu_net_run_host": (i, [vp, vp, i, vp]),
             "hegpu_net_encrypt_image": (i, [vp, f64p, u, u64p]),
             "hegpu_net_decrypt_logits": (i, [vp, u64p, f64p]),
@@ -137,6 +138,8 @@ def lib():
             "hegpu_net_compact_image_bytes": (sz, [vp]),
             "hegpu_net_encrypt_image_compact": (i, [vp, f64p, u, vp]),
             "hegpu_net_run_host_compact": (i, [vp, vp, i, i, vp]),
+            "hegpu_net_submit_host_compact": (i, [vp, vp, i, i, vp]),
+            "hegpu_net_wait": (i, [vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -537,6 +540,12 @@ class Net:
         self.ctx.check(lib().hegpu_net_run(self.h, taps_ct.h, out_ct.h))
         return out_ct
 
+    def run_compact(self, dev_taps, batch, out_ct):
+        """device-resident compact taps (a CUDA tensor / device pointer)"""
+        ptr = dev_taps if isinstance(dev_taps, int) else dev_taps.data_ptr()
+        self.ctx.check(lib().hegpu_net_run_compact(self.h, ptr, batch, out_ct.h))
+        return out_ct
+
     def run_host(self, host_taps, batch, host_out):
         """host_taps / host_out: numpy or pinned torch buffers (.ctypes.data / data_ptr)."""
         pi = host_taps.ctypes.data if isinstance(host_taps, np.ndarray) else host_taps.data_ptr()
@@ -558,6 +567,15 @@ class Net:
         pi = host_taps.ctypes.data if isinstance(host_taps, np.ndarray) else host_taps.data_ptr()
         po = host_out.ctypes.data if isinstance(host_out, np.ndarray) else host_out.data_ptr()
         self.ctx.check(lib().hegpu_net_run_host_compact(self.h, pi, batch, chunk, po))
+
+    def submit_host_compact(self, host_taps, batch, host_out, chunk=0):
+        """as run_host_compact without waiting (buffers must outlive wait())"""
+        pi = host_taps.ctypes.data if isinstance(host_taps, np.ndarray) else host_taps.data_ptr()
+        po = host_out.ctypes.data if isinstance(host_out, np.ndarray) else host_out.data_ptr()
+        self.ctx.check(lib().hegpu_net_submit_host_compact(self.h, pi, batch, chunk, po))
+
+    def wait(self):
+        self.ctx.check(lib().hegpu_net_wait(self.h))
 
     def decrypt_logits(self, out_ct):
         m = self.cfg.dense[-1]

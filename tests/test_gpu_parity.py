@@ -294,6 +294,34 @@ def test_cfg0_run_host_compact_pipeline(cfg0, chunk):
     assert np.array_equal(host_out, out.download())
 
 
+def test_cfg0_run_compact_device_and_submit(cfg0):
+    """device-resident compact taps (conv MAC decodes c0 / regenerates c1 on
+    the fly) and the pipelined submit/wait serving path == full-ct device run,
+    with the same per-stage HOP metering"""
+    import torch
+    cfg, ctx, ck, w, net = cfg0
+    B = 3
+    imgs = [net_image(cfg, 60 + s) for s in range(B)]
+    compact = np.concatenate([net.encrypt_image_compact(im, nonce=60 + s) for s, im in enumerate(imgs)])
+    full = np.concatenate([net.encrypt_image(im, nonce=60 + s) for s, im in enumerate(imgs)])
+    ref = ctx.ct(B, net.out_level)
+    ctx.reset_meter()
+    net.run(ctx.ct(B * net.ntaps, net.top, full, DELTA), ref)
+    want_stages = dict(ctx.stages())
+    want = ref.download()
+    out = ctx.ct(B, net.out_level)
+    ctx.reset_meter()
+    net.run_compact(torch.from_numpy(compact).cuda(), B, out)
+    assert np.array_equal(out.download(), want)
+    assert dict(ctx.stages()) == want_stages
+    outs = [np.zeros(B * net.out_words, dtype=np.uint64) for _ in range(3)]
+    for o in outs:  # three passes in flight over the two staging buffers
+        net.submit_host_compact(compact, B, o, 2)
+    net.wait()
+    for o in outs:
+        assert np.array_equal(o, want)
+
+
 def test_cfg3_net_logits_and_hops():
     """Config 3 (CIFAR-shaped, N=16384): conv 5x5/2 3->32 (75 taps), merge 32
     maps (6272 slots), HS 6272->256, HS 256->10; logits vs ref_forward and
