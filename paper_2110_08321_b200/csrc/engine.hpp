@@ -203,7 +203,11 @@ struct HsDiagTable {
   int ndiag;
   int keyed;                 // diagonals with r > 0 (carry a fused key)
   const int* r;              // [ndiag] device: right rotation r_i, ascending
-  const u64d* const* fkeys;  // [ndiag] device: key_i * mask_i, [l][2][l+1][N] (null for r = 0)
+  // fused keys key_i * mask_i of the keyed diagonals, contiguous:
+  // diagonal i (>= first_keyed) at fk + (i - first_keyed) * fk_words, [l][2][l+1][N]
+  const u64d* fk;
+  size_t fk_words;
+  int first_keyed;           // 1 when diagonal 0 has r = 0 (no key), else 0
   const u64d* masks;         // [ndiag][l+1][N] mont, slot order
   int nchunk;
   const int* chunk;          // [nchunk + 1] diagonal ranges with r span < hs_chunk_span()

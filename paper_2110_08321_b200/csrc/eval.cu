@@ -98,7 +98,16 @@ __global__ void k_tensor_square(PrimeTable pt, const u64d* __restrict__ a, u64d*
 // key-switch inner product: acc[b][p][t] = sum_j D[b][j][t] * key_b[j][p][pi(t)].
 // Rows sharing a key (b = (u*KT + bb) * period + jkey) are tiled KT per
 // thread so every key word is loaded once for KT ciphertexts.
-constexpr int kKsKT = 4;
+// rows per thread / accumulator of the key-switch inner products: measured
+// on cfg2 (profiles/r01_notes.md) KT=1 with the carry-chain AccC 0.735 ms,
+// KT=1 Acc3 0.789, KT=2 Acc3 0.797, KT=4 Acc3 1.07, KT=4 AccC 1.48, KT=8 1.84
+#ifndef HEGPU_KS_KT
+#define HEGPU_KS_KT 1
+#endif
+#ifndef HEGPU_KS_ACC
+#define HEGPU_KS_ACC AccC
+#endif
+constexpr int kKsKT = HEGPU_KS_KT;
 __global__ void __launch_bounds__(kTpb) k_ks_inner(PrimeTable pt, const u64d* __restrict__ D, int B, int l, int L,
                                                    int N, KeyRowMap km, u64d* __restrict__ acc) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -110,7 +119,7 @@ __global__ void __launch_bounds__(kTpb) k_ks_inner(PrimeTable pt, const u64d* __
   const u64d* key = km.key[jkey] + (size_t)pi * N + k;  // split-31 Montgomery words
   const size_t kp = (size_t)(L + 1) * N;                // one key poly over all primes
   int rows[kKsKT];
-  Acc3 a0[kKsKT], a1[kKsKT];
+  HEGPU_KS_ACC a0[kKsKT], a1[kKsKT];
 #pragma unroll
   for (int bb = 0; bb < kKsKT; ++bb) {
     rows[bb] = (u * kKsKT + bb) * km.period + jkey;
@@ -151,7 +160,7 @@ __global__ void __launch_bounds__(kTpb) k_ks_inner_sum(PrimeTable pt, const u64d
   const int pi = t == l ? L : t;
   const DevPrime pr = pt.p[pi];
   const size_t kp = (size_t)(L + 1) * N;
-  Acc3 a0[kKsKT], a1[kKsKT];
+  HEGPU_KS_ACC a0[kKsKT], a1[kKsKT];
 #pragma unroll
   for (int bb = 0; bb < kKsKT; ++bb) a0[bb].zero(), a1[bb].zero();
   int cnt = 0;
@@ -198,6 +207,10 @@ __global__ void k_merge_c(PrimeTable pt, const u64d* __restrict__ maps, int nimg
     for (int j = 1; j < c; ++j) v = add_mod_d(v, m[(size_t)j * st + shifted_pos(k, km.shift[j - 1], S)], q);
   C[(size_t)img * st + (size_t)p * l * N + (size_t)t * N + k] = v;
 }
+
+#ifndef HEGPU_CONV_CO
+#define HEGPU_CONV_CO 8
+#endif
 
 // tap source of the conv MAC: tap s of this thread's (image, poly, limb,
 // position) in a full device ciphertext batch
@@ -334,13 +347,15 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
     __syncthreads();
     const u64d* wb = win + threadIdx.x + r_hi;
     // software pipeline: the fused-key words and mask of diagonal i + 1 are
-    // in flight while diagonal i is accumulated
+    // in flight while diagonal i is accumulated (addresses are arithmetic:
+    // no load feeds another load's address)
+    const u64d* fkb = tab.fk + p * kp + t * N + k;
     u64d kn[LV], mn = 0;
     int rn = __ldg(tab.r + i0);
     {
-      const u64d* fk = rn ? tab.fkeys[i0] + p * kp + t * N + k : nullptr;
+      const u64d* fk = fkb + (size_t)(i0 - tab.first_keyed) * tab.fk_words;
 #pragma unroll
-      for (int j = 0; j < LV; ++j) kn[j] = fk ? __ldg(fk + j * 2 * kp) : 0ull;
+      for (int j = 0; j < LV; ++j) kn[j] = i0 >= tab.first_keyed ? __ldg(fk + j * 2 * kp) : 0ull;
       if (do_c0) mn = __ldg(mrow + (size_t)i0 * kp);
     }
     for (int i = i0; i < i1; ++i) {
@@ -351,9 +366,9 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
       const u64d m = mn;
       if (i + 1 < i1) {
         rn = __ldg(tab.r + i + 1);
-        const u64d* fk = rn ? tab.fkeys[i + 1] + p * kp + t * N + k : nullptr;
+        const u64d* fk = fkb + (size_t)(i + 1 - tab.first_keyed) * tab.fk_words;
 #pragma unroll
-        for (int j = 0; j < LV; ++j) kn[j] = fk ? __ldg(fk + j * 2 * kp) : 0ull;
+        for (int j = 0; j < LV; ++j) kn[j] = __ldg(fk + j * 2 * kp);  // i + 1 >= 1 >= first_keyed
         if (do_c0) mn = __ldg(mrow + (size_t)(i + 1) * kp);
       }
       const u64d* wp = wb - r;  // + (bb * (LV + 1) + row) * kW, compile-time below
@@ -517,7 +532,7 @@ void launch_conv_mac_t(Context& c, const Taps& taps, double tap_bytes, int B, in
                        int c_out, const u64d* bias, u64d* out) {
   // taps read once, maps written once, bias plaintexts read once
   const double bytes = tap_bytes + 8.0 * c.N() * l * (2.0 * B * c_out + c_out);
-  const int co = c_out < 8 ? c_out : 8;  // output maps per thread (exact for c_out <= 8)
+  const int co = c_out < HEGPU_CONV_CO ? c_out : HEGPU_CONV_CO;  // output maps per thread
   dim3 grid((c.N() + kTpb - 1) / kTpb, 2 * l, B * ((c_out + co - 1) / co));
   const size_t sm = (size_t)co * ntaps * 8;
   if (sm > 200 * 1024) fail(HEGPU_ERR_CAPACITY, "conv_packed_forward: too many taps");

@@ -193,7 +193,6 @@ void HsPlan::build(Context& c, const double* A, int m_, int n_, int lvl, bool sk
   if (!r.empty()) CK(cudaMemcpy(d_r, r.data(), r.size() * sizeof(int), cudaMemcpyHostToDevice));
   CK(cudaMalloc((void**)&d_chunk, chunk.size() * sizeof(int)));
   CK(cudaMemcpy(d_chunk, chunk.data(), chunk.size() * sizeof(int), cudaMemcpyHostToDevice));
-  CK(cudaMalloc((void**)&d_fkeys, (diag.size() + 1) * sizeof(u64d*)));
 }
 
 void HsPlan::release() {
@@ -202,11 +201,9 @@ void HsPlan::release() {
   cudaFree(d_r);
   cudaFree(d_chunk);
   cudaFree(fkeys);
-  cudaFree(d_fkeys);
   masks = nullptr;
   d_r = d_chunk = nullptr;
   fkeys = nullptr;
-  d_fkeys = nullptr;
 }
 
 std::vector<int64_t> HsPlan::right_rotations() const {
@@ -228,15 +225,12 @@ void HsPlan::run(Context& c, const CtBatch& v, CtBatch& out) {
     size_t nkeyed = 0;
     for (const HsDiag& d : diag) nkeyed += d.shift != 0;
     if (nkeyed) CK(cudaMalloc((void**)&fkeys, nkeyed * fk_words * 8));
-    std::vector<const u64d*> kp(diag.size(), nullptr);
-    size_t slot = 0;
+    size_t slot = 0;  // only diagonal 0 can be unkeyed (r ascending)
     for (size_t i = 0; i < diag.size(); ++i) {
       if (!diag[i].shift) continue;
-      u64d* dst = fkeys + slot++ * fk_words;
-      launch_fuse_key(c, c.rot_key(diag[i].shift).data, masks + i * (size_t)(l + 1) * N, l, dst);
-      kp[i] = dst;
+      launch_fuse_key(c, c.rot_key(diag[i].shift).data, masks + i * (size_t)(l + 1) * N, l,
+                      fkeys + slot++ * fk_words);
     }
-    if (!kp.empty()) CK(cudaMemcpy(d_fkeys, kp.data(), kp.size() * sizeof(u64d*), cudaMemcpyHostToDevice));
     CK(cudaStreamSynchronize(c.stream));
     keys_resolved = true;
   }
@@ -251,7 +245,9 @@ void HsPlan::run(Context& c, const CtBatch& v, CtBatch& out) {
   // (2) diagonal accumulation in the extended basis
   int keyed = 0;
   for (const HsDiag& dd : diag) keyed += dd.shift != 0;
-  HsDiagTable tab{(int)diag.size(), keyed, d_r, d_fkeys, masks, nchunk, d_chunk};
+  const int first_keyed = !diag.empty() && diag[0].shift == 0 ? 1 : 0;
+  HsDiagTable tab{(int)diag.size(), keyed, d_r, fkeys, (size_t)l * 2 * (l + 1) * N, first_keyed, masks, nchunk,
+                  d_chunk};
   launch_hs_diag(c, v.d, B, l, D, tab, acc, cacc);
   // (3) one ModDown of the sum (+ the Q-basis c-part)
   DropArgs d{};

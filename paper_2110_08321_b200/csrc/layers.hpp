@@ -47,8 +47,7 @@ struct HsPlan {
   int* d_r = nullptr;         // [kept] right rotations
   int* d_chunk = nullptr;     // chunk boundaries
   int nchunk = 0;
-  u64d* fkeys = nullptr;      // [kept][level][2][level+1][N] key_i * mask_i (first run)
-  const u64d** d_fkeys = nullptr;  // [kept]
+  u64d* fkeys = nullptr;      // [keyed][level][2][level+1][N] key_i * mask_i (first run)
   bool keys_resolved = false;
   void build(Context& c, const double* A, int m, int n, int level, bool skip_zero);
   void release();
