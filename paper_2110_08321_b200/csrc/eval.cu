@@ -252,12 +252,13 @@ __global__ void __launch_bounds__(kTpb) k_conv_mac(PrimeTable pt, Taps taps, int
     u64d x[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) x[u] = split31(tap(s + u));
+    // tap-major: the CO accumulators advance in turn (independent chains)
 #pragma unroll
-    for (int c = 0; c < CO; ++c) {
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[c].mad(x[u], ws[c * ntaps + s + u]);
-      acc[c].fold();
-    }
+      for (int c = 0; c < CO; ++c) acc[c].mad(x[u], ws[c * ntaps + s + u]);
+#pragma unroll
+    for (int c = 0; c < CO; ++c) acc[c].fold();
   }
   for (; s < ntaps; ++s) {
     const u64d x = split31(tap(s));
@@ -377,14 +378,19 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
         for (int bb = 0; bb < kHsBT; ++bb) c[bb].mad(wp[(bb * (LV + 1) + LV) * kW], m);
       }
       if (r != 0) {
+        // digit-major: the BT accumulators advance in turn (independent
+        // chains; image-major measured 6% slower)
 #pragma unroll
-        for (int bb = 0; bb < kHsBT; ++bb) {
+        for (int j = 0; j < LV; ++j) {
 #pragma unroll
-          for (int j = 0; j < LV; ++j) {
+          for (int bb = 0; bb < kHsBT; ++bb) {
             a[bb].mad(wp[(bb * (LV + 1) + j) * kW], kv[j]);
             if ((j & 3) == 3) a[bb].fold();
           }
-          if (LV & 3) a[bb].fold();
+        }
+        if (LV & 3) {
+#pragma unroll
+          for (int bb = 0; bb < kHsBT; ++bb) a[bb].fold();
         }
       }
       if (do_c0 && ((i - i0) & 3) == 3) {
