@@ -16,11 +16,17 @@ os.makedirs(os.path.join(ROOT, "tools", "bin"), exist_ok=True)
 for spec in sys.argv[1:]:
     name, _, flags = spec.partition(":")
     flags = [f for f in flags.split(",") if f]
-    src = sys.argv[0] and os.environ.get("VARIANT_SRC", "eval.cu")
-    obj = f"/tmp/var/{src}_{name}.o"
-    subprocess.run([B.NVCC, *B.ARCH, *B.COMMON, *flags, "-c", os.path.join(B.CSRC, src), "-o", obj], check=True)
+    srcs = os.environ.get("VARIANT_SRC", "eval.cu").split(",")
+    vobjs = []
+    for src in srcs:
+        obj = f"/tmp/var/{src}_{name}.o"
+        cmd = [B.NVCC, *B.ARCH, *B.COMMON, *flags, "-c", os.path.join(B.CSRC, src), "-o", obj]
+        if src.endswith(".cpp"):
+            cmd = [B.NVCC, *B.COMMON, *flags, "-x", "c++", "-c", os.path.join(B.CSRC, src), "-o", obj]
+        subprocess.run(cmd, check=True)
+        vobjs.append(obj)
     lib = os.path.join(ROOT, "tools", "bin", f"libhegpu_{name}.so")
-    link = [o for o in objs if not o.endswith(src + ".o")] + [obj]
+    link = [o for o in objs if not any(o.endswith(src + ".o") for src in srcs)] + vobjs
     subprocess.run([B.NVCC, *B.ARCH, "-shared", "-o", lib, *link, "-Xcompiler", "-fopenmp", "-lgomp", "-lcudart"],
                    check=True)
     print(lib)
