@@ -216,11 +216,25 @@ __global__ void k_merge_c(PrimeTable pt, const u64d* __restrict__ maps, int nimg
 // position) in a full device ciphertext batch
 struct TapsFull {
   const u64d* taps;
-  __device__ u64d operator()(int s, int b, int ntaps, int poly, int t, int l, int k, int N) const {
+  __device__ const u64d* addr(int s, int b, int ntaps, int poly, int t, int l, int k, int N) const {
     const size_t ct_words = (size_t)2 * l * N;
-    return __ldg(taps + ((size_t)b * ntaps + s) * ct_words + (size_t)poly * l * N + (size_t)t * N + k);
+    return taps + ((size_t)b * ntaps + s) * ct_words + (size_t)poly * l * N + (size_t)t * N + k;
+  }
+  __device__ u64d operator()(int s, int b, int ntaps, int poly, int t, int l, int k, int N) const {
+    return __ldg(addr(s, b, ntaps, poly, t, l, k, N));
   }
 };
+
+__device__ __forceinline__ void cp_async8(u64d* dst, const u64d* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+#ifndef HEGPU_CONV_STAGE
+#define HEGPU_CONV_STAGE 32  // taps per cp.async batch staged per thread in shared memory (0: direct loads)
+#endif
 
 // conv-pack MAC (convlower.cpp:39-74): CO output maps per thread, taps
 // streamed 4 at a time so each thread keeps independent loads in flight.
@@ -247,6 +261,36 @@ __global__ void __launch_bounds__(kTpb) k_conv_mac(PrimeTable pt, Taps taps, int
 #pragma unroll
   for (int c = 0; c < CO; ++c) acc[c].zero();
   int s = 0;
+#if HEGPU_CONV_STAGE
+  // every tap word of this thread is fetched with cp.async into its own
+  // shared-memory slots (no register cost, all loads in flight at once)
+  u64d* stg = ws + CO * ntaps + threadIdx.x;
+  for (int s0 = 0; s0 < ntaps; s0 += HEGPU_CONV_STAGE) {
+    const int s1 = min(ntaps, s0 + HEGPU_CONV_STAGE);
+    for (int q = s0; q < s1; ++q)
+      cp_async8(stg + (q - s0) * blockDim.x, taps.addr(q, b, ntaps, poly, t, l, k, N));
+    cp_async_wait_all();
+    for (s = s0; s + 4 <= s1; s += 4) {
+      u64d x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = split31(stg[(s + u - s0) * blockDim.x]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < CO; ++c) acc[c].mad(x[u], ws[c * ntaps + s + u]);
+#pragma unroll
+      for (int c = 0; c < CO; ++c) acc[c].fold();
+    }
+    for (; s < s1; ++s) {
+      const u64d x = split31(stg[(s - s0) * blockDim.x]);
+#pragma unroll
+      for (int c = 0; c < CO; ++c) acc[c].mad(x, ws[c * ntaps + s]);
+#pragma unroll
+      for (int c = 0; c < CO; ++c) acc[c].fold();
+    }
+  }
+  s = ntaps;
+#endif
   // 4 taps in flight per thread; fold every 4 products
   for (; s + 4 <= ntaps; s += 4) {
     u64d x[4];
@@ -540,7 +584,7 @@ void launch_conv_mac_t(Context& c, const Taps& taps, double tap_bytes, int B, in
   const double bytes = tap_bytes + 8.0 * c.N() * l * (2.0 * B * c_out + c_out);
   const int co = c_out < HEGPU_CONV_CO ? c_out : HEGPU_CONV_CO;  // output maps per thread
   dim3 grid((c.N() + kTpb - 1) / kTpb, 2 * l, B * ((c_out + co - 1) / co));
-  const size_t sm = (size_t)co * ntaps * 8;
+  const size_t sm = (size_t)co * ntaps * 8 + (size_t)HEGPU_CONV_STAGE * kTpb * 8;
   if (sm > 200 * 1024) fail(HEGPU_ERR_CAPACITY, "conv_packed_forward: too many taps");
 #define CONV_GO(CO)                                                                                        \
   case CO: {                                                                                               \

@@ -25,6 +25,7 @@ __global__ void k_expand_c0(const uint8_t* __restrict__ src, u64d* __restrict__ 
   const u64d* limb = reinterpret_cast<const u64d*>(src + (size_t)c * lay.ct_bytes + lay.off[t]);
   const int words = (N * nb) >> 3;
   u64d* out = dst + ((size_t)c * 2 * l + t) * N;
+#pragma unroll 4
   for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < N; pos += gridDim.x * blockDim.x)
     out[pos] = compact_c0(limb, (int)__ldg(slot_src + pos) * nb, nb, words);
 }
@@ -37,6 +38,7 @@ __global__ void k_expand_a(const uint8_t* __restrict__ src, u64d* __restrict__ d
   const u64d key = reinterpret_cast<const u64d*>(src + (size_t)c * lay.ct_bytes)[t];
   const u64d q = pt.p[t].q;
   u64d* out = dst + ((size_t)c * 2 * l + l + t) * N;
+#pragma unroll 4
   for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < N; pos += gridDim.x * blockDim.x)
     out[pos] = compact_a(key, __ldg(slot_src + pos), q);
 }
