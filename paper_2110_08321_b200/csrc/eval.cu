@@ -107,7 +107,17 @@ __global__ void k_tensor_square(PrimeTable pt, const u64d* __restrict__ a, u64d*
 #ifndef HEGPU_KS_ACC
 #define HEGPU_KS_ACC AccC
 #endif
+__device__ __forceinline__ void cp_async8(u64d* dst, const u64d* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 constexpr int kKsKT = HEGPU_KS_KT;
+#ifndef HEGPU_KS_STAGE
+#define HEGPU_KS_STAGE 0  // 1: KT = 1 stages the key and digit words with cp.async (measured 0.757 vs 0.735 ms)
+#endif
 __global__ void __launch_bounds__(kTpb) k_ks_inner(PrimeTable pt, const u64d* __restrict__ D, int B, int l, int L,
                                                    int N, KeyRowMap km, u64d* __restrict__ acc) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -126,6 +136,32 @@ __global__ void __launch_bounds__(kTpb) k_ks_inner(PrimeTable pt, const u64d* __
     a0[bb].zero();
     a1[bb].zero();
   }
+#if HEGPU_KS_STAGE
+  if constexpr (kKsKT == 1) {
+    // all 3l words of this thread in flight at once, into its own smem slots
+    extern __shared__ u64d stg[];
+    u64d* my = stg + threadIdx.x;
+    const int row = rows[0];
+    if (row < B) {
+      for (int j = 0; j < l; ++j) {
+        cp_async8(my + (3 * j) * blockDim.x, key + (size_t)j * 2 * kp);
+        cp_async8(my + (3 * j + 1) * blockDim.x, key + (size_t)j * 2 * kp + kp);
+        cp_async8(my + (3 * j + 2) * blockDim.x, D + (((size_t)row * l + j) * (l + 1) + t) * N + k);
+      }
+      cp_async_wait_all();
+      for (int j = 0; j < l; ++j) {
+        const u64d d = split31(my[(3 * j + 2) * blockDim.x]);
+        a0[0].mad(d, my[(3 * j) * blockDim.x]);
+        a1[0].mad(d, my[(3 * j + 1) * blockDim.x]);
+        if ((j & 3) == 3) a0[0].fold(), a1[0].fold();
+      }
+      u64d* o = acc + ((size_t)row * 2 * (l + 1) + t) * N + k;
+      o[0] = a0[0].reduce(pr);
+      o[(size_t)(l + 1) * N] = a1[0].reduce(pr);
+    }
+    return;
+  }
+#endif
   for (int j = 0; j < l; ++j) {
     const u64d k0 = __ldg(key + (size_t)j * 2 * kp), k1 = __ldg(key + (size_t)j * 2 * kp + kp);
 #pragma unroll
@@ -224,13 +260,6 @@ struct TapsFull {
     return __ldg(addr(s, b, ntaps, poly, t, l, k, N));
   }
 };
-
-__device__ __forceinline__ void cp_async8(u64d* dst, const u64d* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 #ifndef HEGPU_CONV_STAGE
 #define HEGPU_CONV_STAGE 32  // taps per cp.async batch staged per thread in shared memory (0: direct loads)
@@ -573,8 +602,14 @@ void ks_inner(Context& c, const u64d* D, int B, int l, const KeyRowMap& keys, u6
   dim3 grid((c.N() + kTpb - 1) / kTpb, l + 1, per * tiles);
   double kb = 0;  // distinct keys read once each
   for (int i = 0; i < per && i < B; ++i) kb += 8.0 * l * 2 * (l + 1) * c.N();
+  const size_t sm = (HEGPU_KS_STAGE && kKsKT == 1) ? (size_t)3 * l * kTpb * 8 : 0;
+  static size_t done = 0;
+  if (sm > 48 * 1024 && sm > done) {
+    CK(cudaFuncSetAttribute(k_ks_inner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    done = sm;
+  }
   LAUNCH_BO(c, "k_ks_inner", 8.0 * B * (l + 2) * (l + 1) * c.N() + kb, 2.0 * B * l * (l + 1) * c.N(),
-           k_ks_inner<<<grid, kTpb, 0, c.stream>>>(c.primes, D, B, l, c.L(), c.N(), keys, acc));
+           k_ks_inner<<<grid, kTpb, sm, c.stream>>>(c.primes, D, B, l, c.L(), c.N(), keys, acc));
 }
 
 template <class Taps>
