@@ -24,6 +24,10 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-I", os.path.join(ROOT, "include"),
           "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off,-fno-fast-math", "-Xptxas", "-O3"]
 
 
+# translation units that #include another .cu (rebuild when it changes)
+INCLUDED_SOURCES = {"ntt_r8.cu": ["ntt.cu"]}
+
+
 def sources():
     return sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
 
@@ -37,8 +41,9 @@ def headers_mtime():
 def _compile(src, force):
     obj = os.path.join(OBJ, src + ".o")
     path = os.path.join(CSRC, src)
+    deps = [path] + [os.path.join(CSRC, d) for d in INCLUDED_SOURCES.get(src, [])]
     if (not force and os.path.exists(obj)
-            and os.path.getmtime(obj) >= max(os.path.getmtime(path), headers_mtime())):
+            and os.path.getmtime(obj) >= max(max(os.path.getmtime(d) for d in deps), headers_mtime())):
         return obj
     cmd = [NVCC, *ARCH, *COMMON, "-c", path, "-o", obj]
     if src.endswith(".cpp"):

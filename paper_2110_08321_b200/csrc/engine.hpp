@@ -191,6 +191,19 @@ struct DropArgs {
   const KeyRowMap* shifts;  // shift for add reads of poly 0 (may be null)
 };
 void drop_last_limb(Context& c, int B, const DropArgs& a, u64d* tmpP);
+// the two NTT builds (ntt.cu: 16 words/thread, ntt_r8.cu: 8 for N <= 2^13)
+void launch_ntt_rows_r8(Context& c, const u64d* src, u64d* dst, int rows, int nl, int p_limb);
+void launch_ntt_rows_r16(Context& c, const u64d* src, u64d* dst, int rows, int nl, int p_limb);
+void launch_intt_rows_r8(Context& c, const u64d* src, u64d* dst, int n_outer, int n_inner, long so, long si,
+                         long dox, long di, const int* prime_of_inner);
+void launch_intt_rows_r16(Context& c, const u64d* src, u64d* dst, int n_outer, int n_inner, long so, long si,
+                          long dox, long di, const int* prime_of_inner);
+void ks_modup_r8(Context& c, const u64d* src, long src_stride, int B, int l, const KeyRowMap* shifts, u64d* tmp,
+                 u64d* D);
+void ks_modup_r16(Context& c, const u64d* src, long src_stride, int B, int l, const KeyRowMap* shifts, u64d* tmp,
+                  u64d* D);
+void drop_last_limb_r8(Context& c, int B, const DropArgs& a, u64d* tmpP);
+void drop_last_limb_r16(Context& c, int B, const DropArgs& a, u64d* tmpP);
 
 // pointwise (eval.cu)
 void launch_add(Context& c, const u64d* a, const u64d* b, u64d* out, int count, int l);

@@ -440,6 +440,17 @@ void prep_kernel(K kernel, size_t bytes) {
 
 }  // namespace
 
+// ntt_r8.cu re-includes this file with 8 words per thread for N <= 2^13
+// (1024-thread CTAs, no register spills): measured faster for the row
+// INTTs and the drop-limb NTTs, slower for ModUp (profiles/r01_notes.md),
+// so those two entry points dispatch to the _r8 build.
+#ifdef HEGPU_NTT_R8_VARIANT
+#define NTT_PUB(x) x##_r8
+#else
+#define NTT_PUB(x) x##_r16
+#endif
+
+#ifndef HEGPU_NTT_R8_VARIANT
 void upload_twiddles(Context& c) {
   const Params& P = *c.P;
   const int np = P.np(), N = P.n;
@@ -458,14 +469,16 @@ void upload_twiddles(Context& c) {
   CK(cudaMemcpy(c.d_tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice));
 }
 
-void launch_ntt_rows(Context& c, const u64d* src, u64d* dst, int rows, int nl, int p_limb) {
+#endif  // !HEGPU_NTT_R8_VARIANT
+
+void NTT_PUB(launch_ntt_rows)(Context& c, const u64d* src, u64d* dst, int rows, int nl, int p_limb) {
   if (rows <= 0) return;
   const double _ntt_bytes = 16.0 * c.N() * rows;  // read + write one limb per row
   NTT_DISPATCH(c.P->log_n, k_ntt_rows, rows, tw_args(c), c.primes, src, dst, nl, p_limb, c.L());
 }
 
-void launch_intt_rows(Context& c, const u64d* src, u64d* dst, int n_outer, int n_inner, long so, long si,
-                      long dox, long di, const int* prime_of_inner) {
+void NTT_PUB(launch_intt_rows)(Context& c, const u64d* src, u64d* dst, int n_outer, int n_inner, long so, long si,
+                               long dox, long di, const int* prime_of_inner) {
   if (n_outer * n_inner <= 0) return;
   if (n_inner > HEGPU_MAX_PRIMES) fail(HEGPU_ERR_ARG, "intt_rows: too many limbs");
   PMap pm{};
@@ -475,6 +488,7 @@ void launch_intt_rows(Context& c, const u64d* src, u64d* dst, int n_outer, int n
                di, pm);
 }
 
+#ifndef HEGPU_NTT_R8_VARIANT
 void launch_wire_to_slot(Context& c, const u64d* src, u64d* dst, size_t rows, int to_mont, int nl, int p_limb) {
   if (!rows) return;
   dim3 grid((c.N() + 255) / 256 < 8 ? (c.N() + 255) / 256 : 8, (unsigned)rows);
@@ -491,8 +505,10 @@ void launch_slot_to_wire(Context& c, const u64d* src, u64d* dst, size_t rows, in
                                                     c.L()));
 }
 
-void ks_modup(Context& c, const u64d* src, long src_stride, int B, int l, const KeyRowMap* shifts, u64d* tmp,
-              u64d* D) {
+#endif  // !HEGPU_NTT_R8_VARIANT
+
+void NTT_PUB(ks_modup)(Context& c, const u64d* src, long src_stride, int B, int l, const KeyRowMap* shifts,
+                       u64d* tmp, u64d* D) {
   KeyRowMap dummy{};
   dummy.period = 1;
   double _ntt_bytes = 24.0 * c.N() * B * l;  // read digit, write coefficients + own-prime copy
@@ -502,10 +518,10 @@ void ks_modup(Context& c, const u64d* src, long src_stride, int B, int l, const 
   if (B * l * l > 0) NTT_DISPATCH(c.P->log_n, k_ks_modup, B * l * l, tw_args(c), c.primes, tmp, l, c.L(), D);
 }
 
-void drop_last_limb(Context& c, int B, const DropArgs& a, u64d* tmpP) {
+void NTT_PUB(drop_last_limb)(Context& c, int B, const DropArgs& a, u64d* tmpP) {
   const int N = c.N();
   const int pmap[2] = {a.pd, a.pd};
-  launch_intt_rows(c, a.src + (size_t)(a.src_limbs - 1) * N, tmpP, B, 2, a.src_b, a.src_p, 2L * N, N, pmap);
+  NTT_PUB(launch_intt_rows)(c, a.src + (size_t)(a.src_limbs - 1) * N, tmpP, B, 2, a.src_b, a.src_p, 2L * N, N, pmap);
   if (a.nl <= 0) return;
   KeyRowMap dummy{};
   dummy.period = 1;
@@ -514,5 +530,21 @@ void drop_last_limb(Context& c, int B, const DropArgs& a, u64d* tmpP) {
   NTT_DISPATCH(c.P->log_n, k_drop_ntt, B * 2 * a.nl, tw_args(c), c.primes, c.qinv_tab(), c.P->np(), a, tmpP,
                a.shifts ? *a.shifts : dummy, a.shifts != nullptr);
 }
+
+#ifndef HEGPU_NTT_R8_VARIANT
+// per-entry-point choice of the thread granularity (see NTT_PUB above)
+void launch_ntt_rows(Context& c, const u64d* src, u64d* dst, int rows, int nl, int p_limb) {
+  launch_ntt_rows_r16(c, src, dst, rows, nl, p_limb);
+}
+void launch_intt_rows(Context& c, const u64d* src, u64d* dst, int n_outer, int n_inner, long so, long si, long dox,
+                      long di, const int* prime_of_inner) {
+  launch_intt_rows_r8(c, src, dst, n_outer, n_inner, so, si, dox, di, prime_of_inner);
+}
+void ks_modup(Context& c, const u64d* src, long src_stride, int B, int l, const KeyRowMap* shifts, u64d* tmp,
+              u64d* D) {
+  ks_modup_r16(c, src, src_stride, B, l, shifts, tmp, D);
+}
+void drop_last_limb(Context& c, int B, const DropArgs& a, u64d* tmpP) { drop_last_limb_r8(c, B, a, tmpP); }
+#endif
 
 }  // namespace hegpu
