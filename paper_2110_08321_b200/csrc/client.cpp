@@ -193,12 +193,16 @@ void Client::encrypt_compact(const u64* pt, int level, u64 nonce, uint8_t* out) 
   encrypt(pt, level, nonce, ct.data());
   u64* keys = reinterpret_cast<u64*>(out);
   for (int t = 0; t < level; ++t) keys[t] = Stream(P_.seed, tag_enc(nonce, 0, (u64)t)).key;
+  // c0 in the DEVICE SLOT ORDER (position p = wire index slot_src[p]), so the
+  // device expansion is a linear unpack
   uint8_t* o = out + (size_t)level * 8;
   for (int t = 0; t < level; ++t) {
     const int nb = limb_bytes(t);
     const u64* c0 = ct.data() + (size_t)t * N;
-    for (int k = 0; k < N; ++k)
-      for (int b = 0; b < nb; ++b) *o++ = (uint8_t)(c0[k] >> (8 * b));
+    for (int p = 0; p < N; ++p) {
+      const u64 v = c0[P_.slot_src[p]];
+      for (int b = 0; b < nb; ++b) *o++ = (uint8_t)(v >> (8 * b));
+    }
   }
 }
 

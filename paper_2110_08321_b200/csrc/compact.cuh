@@ -1,8 +1,9 @@
 // compact.cuh -- device decoding of compact fresh ciphertexts.
 //
 // One compact ct at level l is [l a-stream keys (u64)] then, per limb t,
-// N coefficients of c0 byte-packed in wire (bit-reversed) order with
-// nb[t] = ceil(bits(q_t)/8) bytes each.  c1 = a is regenerated:
+// N coefficients of c0 byte-packed in device slot order (position p holds
+// wire index slot_src[p]) with nb[t] = ceil(bits(q_t)/8) bytes each.  c1 = a
+// is regenerated:
 //   a_t[k] = umulhi(sm_mix(key_t + (k + 1) * gamma), q_t)   (client.cpp)
 // Used by the expansion kernel (io.cu) and fused into the conv MAC (eval.cu)
 // so fresh taps never have to be materialised in HBM.
@@ -29,7 +30,7 @@ __device__ __forceinline__ u64d compact_a(u64d key, u64d k, u64d q) {
   return __umul64hi(sm_mix_d(key + (k + 1) * 0x9E3779B97F4A7C15ull), q);
 }
 
-// c0 coefficient at byte offset boff (= wire index * nb) of a packed limb
+// c0 coefficient at byte offset boff (= position * nb) of a packed limb
 // of `words` 8-byte words: two aligned loads (the limb is 8-byte aligned)
 __device__ __forceinline__ u64d compact_c0(const u64d* __restrict__ limb, int boff, int nb, int words) {
   const int w = boff >> 3, sh = (boff & 7) * 8;

@@ -14,9 +14,8 @@ namespace hegpu {
 
 namespace {
 
-// c0 rows (ct, t): every slot-order position gathers its nb-byte coefficient
-// from the packed limb (wire order) with two aligned 8-byte loads; a limb is
-// <= 64 KB, so after its first touch the gathers are served from L2
+// c0 rows (ct, t): the packed limb is already in slot order, so position
+// pos reads bytes [pos * nb, pos * nb + nb) -- a linear, coalesced unpack
 __global__ void k_expand_c0(const uint8_t* __restrict__ src, u64d* __restrict__ dst, CompactLayout lay,
                             const uint32_t* __restrict__ slot_src, int N) {
   const int l = lay.level;
@@ -27,7 +26,7 @@ __global__ void k_expand_c0(const uint8_t* __restrict__ src, u64d* __restrict__ 
   u64d* out = dst + ((size_t)c * 2 * l + t) * N;
 #pragma unroll 4
   for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < N; pos += gridDim.x * blockDim.x)
-    out[pos] = compact_c0(limb, (int)__ldg(slot_src + pos) * nb, nb, words);
+    out[pos] = compact_c0(limb, pos * nb, nb, words);
 }
 
 // c1 = a rows (ct, t): regenerated from the limb's a-stream key

@@ -69,14 +69,33 @@ def test_encode_encrypt_bit_exact(log_n, qbits, pbits):
     assert np.abs(d1 - d2).max() < 1e-9
 
 
+def slot_src(log_n):
+    """device slot order: position p < S holds psi^(5^p), p >= S psi^(-5^(p-S));
+    wire index brv((e - 1) / 2)"""
+    n, s, m2n = 1 << log_n, 1 << (log_n - 1), 2 << log_n
+    out = np.empty(n, dtype=np.int64)
+    g = 1
+    for p in range(s):
+        for e, q in ((g, p), (m2n - g, p + s)):
+            k = (e - 1) // 2
+            out[q] = int(format(k, f"0{log_n}b")[::-1], 2)
+        g = g * 5 % m2n
+    return out
+
+
 def unpack_compact(ctx, blob, level):
-    """host-side reference unpacking of the compact format (c0 only)"""
+    """host-side reference unpacking of the compact format (c0 only, back to
+    wire order)"""
     off = 8 * level
+    perm = slot_src(int(ctx.N).bit_length() - 1)
     c0 = []
     for t in range(level):
         nb = (int(ctx.primes[t]).bit_length() + 7) // 8
         raw = blob[off:off + nb * ctx.N].reshape(ctx.N, nb).astype(np.uint64)
-        c0.append(sum(raw[:, b] << np.uint64(8 * b) for b in range(nb)))
+        slot = sum(raw[:, b] << np.uint64(8 * b) for b in range(nb))
+        wire = np.empty_like(slot)
+        wire[perm] = slot
+        c0.append(wire)
         off += nb * ctx.N
     assert off == len(blob)
     return np.concatenate(c0)
