@@ -11,6 +11,7 @@
 // beyond n (matvec.cpp:57-61) and logits are read from slots 0..m-1.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -37,6 +38,21 @@ struct hegpu_net {
   cudaStream_t copy = nullptr;
   cudaEvent_t freed[2] = {nullptr, nullptr};  // compute done reading stage[s]
   std::vector<cudaEvent_t> sub_events[2];     // per stage buffer, one per input sub-chunk
+  // the compute side of a serving pass as a CUDA graph, per (buffers, shape,
+  // staging buffer): one stream entry instead of ~900 launches, so the host
+  // never blocks on a full launch queue and the next pass's uploads are
+  // enqueued while this pass computes.  Replays re-apply the captured
+  // metering.
+  struct ServeGraph {
+    const uint8_t* host;
+    const uint64_t* out;
+    int batch, chunk, cur, uses = 0;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<std::pair<std::string, std::array<int64_t, 5>>> meter;
+    int64_t launches = 0;
+  };
+  std::vector<ServeGraph> serve_graphs;
   ~hegpu_net() {
     for (auto& p : plans) p.release();
     for (u64d* b : bias) cudaFree(b);
@@ -44,6 +60,10 @@ struct hegpu_net {
       if (stage[s]) cudaFree(stage[s]);
       if (freed[s]) cudaEventDestroy(freed[s]);
       for (cudaEvent_t e : sub_events[s]) cudaEventDestroy(e);
+    }
+    for (auto& g : serve_graphs) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      if (g.g) cudaGraphDestroy(g.g);
     }
     if (copy) cudaStreamDestroy(copy);
   }
@@ -284,6 +304,8 @@ extern "C" size_t hegpu_net_compact_image_bytes(const hegpu_net* net) {
 
 namespace {
 
+void serve_compute(hegpu_net& n, const uint8_t* stage, int cur, int batch, int chunk, uint64_t* host_out);
+
 // enqueue one host-input pass (no host synchronisation): the staging buffer
 // alternates between calls so call k+1's uploads overlap call k's compute
 void enqueue_host_compact(hegpu_net& n, const uint8_t* host, int batch, int chunk, uint64_t* host_out) {
@@ -324,10 +346,27 @@ void enqueue_host_compact(hegpu_net& n, const uint8_t* host, int batch, int chun
   CK(cudaStreamWaitEvent(n.copy, n.freed[cur], 0));
   for (int j = 0; j < nsub; ++j) {
     const int b0 = j * c1, nb = std::min(c1, batch - b0);
+#ifndef HEGPU_DIAG_NO_H2D  // diagnostics build only: compute path without the uploads
     CK(cudaMemcpyAsync(stage + (size_t)b0 * per_img, host + (size_t)b0 * per_img, per_img * nb,
                        cudaMemcpyHostToDevice, n.copy));
+#endif
     CK(cudaEventRecord(subs[j], n.copy));
   }
+  serve_compute(n, stage, cur, batch, chunk, host_out);
+}
+
+// compute side of one serving pass on the engine stream (captured into a
+// CUDA graph from the second use of the same buffers on)
+void compute_pass(hegpu_net& n, const uint8_t* stage, int cur, int batch, int chunk, uint64_t* host_out,
+                  bool captured) {
+  Context& c = *n.c;
+  const int N = c.N(), L = n.top, lo = n.top - 1 - 2 * n.spec.n_dense;
+  const int c2 = chunk > 0 ? std::min(chunk, batch) : std::min(batch, 32);
+  const int c1 = std::min(c2, HEGPU_NET_SUBCHUNK);
+  const size_t per_img = hegpu_net_compact_image_bytes(&n);
+  const size_t out_words = (size_t)2 * lo * N;
+  const size_t map_words = (size_t)2 * (L - 1) * N;
+  const auto& subs = n.sub_events[cur];
   // each sub-chunk is multiply-accumulated straight from its compact bytes
   // as it lands; the conv rescale runs once per chunk (full-width NTT grids)
   Scratch prod(c, (size_t)c2 * n.spec.c_out * 2 * L * N);
@@ -339,12 +378,15 @@ void enqueue_host_compact(hegpu_net& n, const uint8_t* host, int batch, int chun
     CtBatch pb{&c, nm * n.spec.c_out, L, 0, prod.p};
     for (int b0 = m0; b0 < m0 + nm; b0 += c1) {
       const int nb = std::min(c1, m0 + nm - b0);
-      CK(cudaStreamWaitEvent(c.stream, subs[b0 / c1], 0));
+      CK(cudaStreamWaitEvent(c.stream, subs[b0 / c1], captured ? cudaEventWaitExternal : 0));
       CtBatch sb{&c, nb * n.spec.c_out, L, 0, prod.p + (size_t)(b0 - m0) * n.spec.c_out * 2 * L * N};
       n.conv->mac_compact(c, stage + (size_t)b0 * per_img, nb, n.tap_scale, sb);
       pb.scale = sb.scale;
     }
-    if (m0 + nm >= batch) CK(cudaEventRecord(n.freed[cur], c.stream));  // last read of the staging
+    if (m0 + nm >= batch) {  // last read of the staging buffer
+      if (captured) CK(cudaEventRecordWithFlags(n.freed[cur], c.stream, cudaEventRecordExternal));
+      else CK(cudaEventRecord(n.freed[cur], c.stream));
+    }
     conv_meter(n, nm);
     CtBatch rb{&c, nm * n.spec.c_out, L - 1, 0, maps.p};
     eval_rescale(c, pb, rb);
@@ -355,6 +397,61 @@ void enqueue_host_compact(hegpu_net& n, const uint8_t* host, int batch, int chun
     CK(cudaMemcpyAsync(host_out + (size_t)m0 * out_words, wire.p, (size_t)nm * out_words * 8,
                        cudaMemcpyDeviceToHost, c.stream));
   }
+}
+
+void serve_compute(hegpu_net& n, const uint8_t* stage, int cur, int batch, int chunk, uint64_t* host_out) {
+  Context& c = *n.c;
+  static const bool graphs = [] {
+    const char* e = std::getenv("HEGPU_SERVE_GRAPHS");
+    return !(e && e[0] == '0');
+  }();
+  if (!graphs) return compute_pass(n, stage, cur, batch, chunk, host_out, false);
+  hegpu_net::ServeGraph* sg = nullptr;
+  for (auto& g : n.serve_graphs)
+    if (g.host == stage && g.out == host_out && g.batch == batch && g.chunk == chunk && g.cur == cur) sg = &g;
+  if (!sg) {
+    if (n.serve_graphs.size() >= 16) {  // bounded cache: drop the oldest
+      auto& old = n.serve_graphs.front();
+      CK(cudaStreamSynchronize(c.stream));
+      if (old.exec) cudaGraphExecDestroy(old.exec);
+      if (old.g) cudaGraphDestroy(old.g);
+      n.serve_graphs.erase(n.serve_graphs.begin());
+    }
+    n.serve_graphs.push_back({stage, host_out, batch, chunk, cur});
+    sg = &n.serve_graphs.back();
+  }
+  if (sg->exec) {
+    for (const auto& st : sg->meter) {
+      c.meter.begin(st.first);
+      for (int f = 0; f < 5; ++f) c.meter.bump(f, st.second[f]);
+    }
+    c.launches += sg->launches;
+    CK(cudaGraphLaunch(sg->exec, c.stream));
+    return;
+  }
+  if (sg->uses++ == 0) return compute_pass(n, stage, cur, batch, chunk, host_out, false);  // warm-up pass
+  const auto before = c.meter.stages;
+  const int64_t l0 = c.launches;
+  CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    compute_pass(n, stage, cur, batch, chunk, host_out, true);
+  } catch (...) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(c.stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  CK(cudaStreamEndCapture(c.stream, &sg->g));
+  CK(cudaGraphInstantiate(&sg->exec, sg->g, 0));
+  for (const auto& st : c.meter.stages) {
+    std::array<int64_t, 5> d = st.second;
+    for (const auto& b : before)
+      if (b.first == st.first)
+        for (int f = 0; f < 5; ++f) d[f] -= b.second[f];
+    sg->meter.emplace_back(st.first, d);
+  }
+  sg->launches = c.launches - l0;
+  CK(cudaGraphLaunch(sg->exec, c.stream));
 }
 
 }  // namespace
