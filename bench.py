@@ -32,7 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "encrypted inferences/sec + key-switched rotations/sec, % of HBM roofline"
-KERNELS = ["k_hs_diag", "k_drop_ntt", "k_ks_modup", "k_conv_mac", "k_intt_rows", "k_ks_intt", "k_ks_inner",
+KERNELS = ["k_hs_diag", "k_drop_ntt", "k_ks_modup", "k_conv_mac", "k_intt_rows", "k_ks_intt", "k_ks_inner", "k_ntt_rows",
            "k_wire_to_slot", "k_add", "k_tensor_square", "k_add_plain"]
 UNIT = "inferences/s"
 SEED = 2110
@@ -283,6 +283,9 @@ def run_gpu(args):
                              "share": kms / ms_max}
     ctx.kernel_timer(None)
     dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
+    ntt_rows = sum(kernels[k]["modmuls"] for k in ("k_drop_ntt", "k_ks_modup", "k_intt_rows", "k_ks_intt",
+                                                  "k_ntt_rows") if k in kernels) / (
+        (1 << (cfg.log_n - 1)) * cfg.log_n)
     hbm, which = peaks()
     kd = kernels[dom]
     traffic = ncu_traffic(dom)
@@ -351,6 +354,10 @@ def run_gpu(args):
                    "input": args.input,
                    "l2": ("inputs 0.43 GB (compact) / 1.26 GB (full) per step > L2, no flush")},
         "rotations_per_s": per_step_rot * world / (ms_max / 1e3),
+        # limb transforms per second: every NTT-family launch's butterflies
+        # / (N/2 log2 N) (one transform = one limb of one polynomial)
+        "ntts_per_s": ntt_rows * world / (ms_max / 1e3),
+        "ntts_per_step": ntt_rows,
         "keyswitches_per_s": per_step_ks * world / (ms_max / 1e3),
         "hops_per_inference": {k: v / B for k, v in zip(H.TALLY_FIELDS, tally)},
         "cuda_graph": bool(args.graph),
