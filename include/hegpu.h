@@ -196,6 +196,18 @@ int hegpu_hs_plan_rotations(const hegpu_hs_plan* plan, int64_t* rots, int cap);
 int hegpu_hs_plan_info(const hegpu_hs_plan* plan, int* m_eff, int* folds, int* kept);
 /* hs_matvec (matvec.cpp:82-105): out level = level-1 (one rescale) */
 int hegpu_hs_matvec(hegpu_ctx* ctx, const hegpu_hs_plan* plan, const hegpu_ct* v, hegpu_ct* out);
+/* hs_matvec split over nparts GPUs (config 3: "partial sums reduced across
+ * GPUs"): part p accumulates the kept diagonals of the p-th of nparts equal
+ * ranges in the extended basis into a device buffer of hegpu_hs_acc_words
+ * uint64 words; the buffers are summed element-wise (e.g. NCCL all-reduce,
+ * int64 sum -- entries stay < nparts * 2^60); _finish reduces the sum and
+ * runs the single ModDown, the rescale and the folds.  Bit-identical to
+ * hegpu_hs_matvec; metering splits the same totals over the parts. */
+size_t hegpu_hs_acc_words(const hegpu_hs_plan* plan, int batch);
+int hegpu_hs_matvec_partial(hegpu_ctx* ctx, const hegpu_hs_plan* plan, const hegpu_ct* v, int part, int nparts,
+                            void* dev_acc);
+int hegpu_hs_matvec_finish(hegpu_ctx* ctx, const hegpu_hs_plan* plan, const hegpu_ct* v, void* dev_acc,
+                           int nparts, hegpu_ct* out);
 
 /* ---- stage driver: execute (proj/src/netcompile.cpp:291-446) ------------ */
 typedef struct {

@@ -757,6 +757,48 @@ extern "C" int hegpu_hs_plan_info(const hegpu_hs_plan* p, int* m_eff, int* folds
   return HEGPU_OK;
 }
 
+extern "C" size_t hegpu_hs_acc_words(const hegpu_hs_plan* p, int batch) {
+  return p && p->p.ctx ? p->p.acc_words(batch, p->p.ctx->N()) : 0;
+}
+
+extern "C" int hegpu_hs_matvec_partial(hegpu_ctx* h, const hegpu_hs_plan* p, const hegpu_ct* v, int part, int nparts,
+                                       void* dev_acc) {
+  if (!h || !p || !v || !dev_acc) return HEGPU_ERR_ARG;
+  Context& c = h->c;
+  return guarded(&c, [&] {
+    HsPlan& pl = const_cast<HsPlan&>(p->p);
+    need(v->b.level == pl.level, HEGPU_ERR_LAYOUT, "hs_matvec_partial: input level does not match the plan");
+    need(nparts >= 1 && part >= 0 && part < nparts, HEGPU_ERR_RANGE, "hs_matvec_partial: bad part");
+    need(nparts <= 8, HEGPU_ERR_CAPACITY, "hs_matvec_partial: at most 8 parts (sums must stay < 2^64)");
+    const int kept = (int)pl.diag.size(), B = v->b.count;
+    const int i_lo = (int)((int64_t)kept * part / nparts), i_hi = (int)((int64_t)kept * (part + 1) / nparts);
+    u64d* acc = static_cast<u64d*>(dev_acc);
+    pl.accumulate(c, v->b, i_lo, i_hi, acc, acc + (size_t)B * 2 * (pl.level + 1) * c.N());
+    int64_t rots = 0;
+    for (int i = i_lo; i < i_hi; ++i) rots += pl.diag[i].right != 0;
+    c.meter.bump(HEGPU_MUL_PC, (int64_t)B * (i_hi - i_lo));
+    c.meter.bump(HEGPU_ROT, (int64_t)B * rots);
+    c.meter.bump(HEGPU_ADD_CC, (int64_t)B * (i_hi - i_lo - (i_lo == 0 && i_hi > 0 ? 1 : 0)));
+  });
+}
+
+extern "C" int hegpu_hs_matvec_finish(hegpu_ctx* h, const hegpu_hs_plan* p, const hegpu_ct* v, void* dev_acc,
+                                      int nparts, hegpu_ct* out) {
+  if (!h || !p || !v || !dev_acc || !out) return HEGPU_ERR_ARG;
+  Context& c = h->c;
+  return guarded(&c, [&] {
+    HsPlan& pl = const_cast<HsPlan&>(p->p);
+    need(out->b.count == v->b.count && out->b.level == v->b.level - 1, HEGPU_ERR_SHAPE,
+         "hs_matvec_finish: output must have level - 1");
+    need(nparts >= 1 && nparts <= 8, HEGPU_ERR_RANGE, "hs_matvec_finish: 1..8 parts");
+    const int B = v->b.count;
+    u64d* acc = static_cast<u64d*>(dev_acc);
+    pl.finish(c, B, v->b.scale, acc, acc + (size_t)B * 2 * (pl.level + 1) * c.N(), nparts, out->b);
+    c.meter.bump(HEGPU_ROT, (int64_t)B * pl.folds);
+    c.meter.bump(HEGPU_ADD_CC, (int64_t)B * pl.folds);
+  });
+}
+
 extern "C" int hegpu_hs_matvec(hegpu_ctx* h, const hegpu_hs_plan* p, const hegpu_ct* v, hegpu_ct* out) {
   if (!h || !p || !v || !out) return HEGPU_ERR_ARG;
   Context& c = h->c;

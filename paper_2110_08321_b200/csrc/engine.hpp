@@ -221,6 +221,7 @@ struct HsDiagTable {
   const u64d* fk;
   size_t fk_words;
   int first_keyed;           // 1 when diagonal 0 has r = 0 (no key), else 0
+  int own_c1;                // this run carries diagonal 0's c1 * mask term (the range starts at 0)
   const u64d* masks;         // [ndiag][l+1][N] mont, slot order
   int nchunk;
   const int* chunk;          // [nchunk + 1] diagonal ranges with r span < hs_chunk_span()
@@ -231,6 +232,9 @@ void launch_hs_diag(Context& c, const u64d* v, int B, int l, const u64d* D, cons
 void launch_fuse_key(Context& c, const u64d* key, const u64d* mask, int l, u64d* fk);
 // re-pack Montgomery multiplier words x -> (x mod 2^31) | (x >> 31) << 32
 void launch_split31(Context& c, u64d* p, size_t words);
+// x -> x mod q(limb) for rows of nl limbs (limb p_limb is the special prime P);
+// x < 2^64 (e.g. a sum of partial accumulators from several GPUs)
+void launch_reduce_rows(Context& c, u64d* p, size_t words, int nl, int p_limb);
 
 // high-level evaluator (eval.cu)
 void eval_rescale(Context& c, const CtBatch& a, CtBatch& out);

@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
   }
   // r == 0 diagonal (if kept) is the only contributor to the c1 part
   u64d m0 = 0;
-  const bool c1_term = has_c && p == 1 && g == 0 && tab.ndiag > 0 && __ldg(tab.r) == 0;
+  const bool c1_term = has_c && p == 1 && g == 0 && tab.own_c1 && tab.ndiag > 0 && __ldg(tab.r) == 0;
   if (c1_term) m0 = unsplit31(__ldg(tab.masks + (size_t)t * N + k));
 #pragma unroll
   for (int bb = 0; bb < kHsBT; ++bb) {
@@ -514,6 +514,18 @@ __global__ void k_sum_parts(PrimeTable pt, const u64d* __restrict__ part, u64d* 
     u64d s = part[i];
     for (int g = 1; g < gs; ++g) s = add_mod_d(s, part[(size_t)g * n + i], q);
     out[i] = s;
+  }
+}
+
+// exact x mod q per word; rows of nl limbs, limb p_limb -> P
+__global__ void k_reduce_rows(PrimeTable pt, u64d* __restrict__ p, size_t n, int nl, int p_limb, int L, int N) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int limb = (int)((i / N) % nl);
+    const DevPrime pr = pt.p[limb == p_limb ? L : limb];
+    u64d v = reduce_lazy4(p[i], pr);
+    if (v >= 2 * pr.q) v -= 2 * pr.q;
+    if (v >= pr.q) v -= pr.q;
+    p[i] = v;
   }
 }
 
@@ -642,6 +654,12 @@ void launch_conv_mac_t(Context& c, const Taps& taps, double tap_bytes, int B, in
 void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, const u64d* w, int c_out,
                      const u64d* bias, u64d* out) {
   launch_conv_mac_t(c, TapsFull{taps}, 8.0 * c.N() * l * 2.0 * B * ntaps, B, ntaps, l, w, c_out, bias, out);
+}
+
+void launch_reduce_rows(Context& c, u64d* p, size_t words, int nl, int p_limb) {
+  if (!words) return;
+  LAUNCH_B(c, "k_reduce_rows", 16.0 * words,
+           k_reduce_rows<<<grid_for(words), kTpb, 0, c.stream>>>(c.primes, p, words, nl, p_limb, c.L(), c.N()));
 }
 
 void launch_split31(Context& c, u64d* p, size_t words) {

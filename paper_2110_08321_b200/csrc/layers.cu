@@ -193,6 +193,7 @@ void HsPlan::build(Context& c, const double* A, int m_, int n_, int lvl, bool sk
   if (!r.empty()) CK(cudaMemcpy(d_r, r.data(), r.size() * sizeof(int), cudaMemcpyHostToDevice));
   CK(cudaMalloc((void**)&d_chunk, chunk.size() * sizeof(int)));
   CK(cudaMemcpy(d_chunk, chunk.data(), chunk.size() * sizeof(int), cudaMemcpyHostToDevice));
+  h_chunk = chunk;
 }
 
 void HsPlan::release() {
@@ -200,6 +201,8 @@ void HsPlan::release() {
   cudaFree(masks);
   cudaFree(d_r);
   cudaFree(d_chunk);
+  for (auto& e : sub_chunks) cudaFree(e.second.first);
+  sub_chunks.clear();
   cudaFree(fkeys);
   masks = nullptr;
   d_r = d_chunk = nullptr;
@@ -215,40 +218,76 @@ std::vector<int64_t> HsPlan::right_rotations() const {
   return r;
 }
 
-void HsPlan::run(Context& c, const CtBatch& v, CtBatch& out) {
-  const int B = v.count, l = level, N = c.N(), S = c.S();
-  if (!keys_resolved) {
-    // fuse each diagonal's Galois key with its mask once (offline work):
-    // fk_i[j][p][t] = key_i[j][p][t] * mask'_i[t] over the level-l ext basis
-    for (int t = folds - 1; t >= 0; --t) c.rot_key((int)(((int64_t)m_eff << t) % S));
-    const size_t fk_words = (size_t)l * 2 * (l + 1) * N;
-    size_t nkeyed = 0;
-    for (const HsDiag& d : diag) nkeyed += d.shift != 0;
-    if (nkeyed) CK(cudaMalloc((void**)&fkeys, nkeyed * fk_words * 8));
-    size_t slot = 0;  // only diagonal 0 can be unkeyed (r ascending)
-    for (size_t i = 0; i < diag.size(); ++i) {
-      if (!diag[i].shift) continue;
-      launch_fuse_key(c, c.rot_key(diag[i].shift).data, masks + i * (size_t)(l + 1) * N, l,
-                      fkeys + slot++ * fk_words);
+void HsPlan::ensure_keys(Context& c) {
+  if (keys_resolved) return;
+  const int l = level, N = c.N(), S = c.S();
+  // fuse each diagonal's Galois key with its mask once (offline work):
+  // fk_i[j][p][t] = key_i[j][p][t] * mask'_i[t] over the level-l ext basis
+  for (int t = folds - 1; t >= 0; --t) c.rot_key((int)(((int64_t)m_eff << t) % S));
+  const size_t fk_words = (size_t)l * 2 * (l + 1) * N;
+  size_t nkeyed = 0;
+  for (const HsDiag& d : diag) nkeyed += d.shift != 0;
+  if (nkeyed) CK(cudaMalloc((void**)&fkeys, nkeyed * fk_words * 8));
+  size_t slot = 0;  // only diagonal 0 can be unkeyed (r ascending)
+  for (size_t i = 0; i < diag.size(); ++i) {
+    if (!diag[i].shift) continue;
+    launch_fuse_key(c, c.rot_key(diag[i].shift).data, masks + i * (size_t)(l + 1) * N, l,
+                    fkeys + slot++ * fk_words);
+  }
+  CK(cudaStreamSynchronize(c.stream));
+  keys_resolved = true;
+}
+
+void HsPlan::accumulate(Context& c, const CtBatch& v, int i_lo, int i_hi, u64d* acc, u64d* cacc) {
+  const int B = v.count, l = level, N = c.N();
+  ensure_keys(c);
+  // the plan's chunks clipped to [i_lo, i_hi) (cached per range)
+  const int* chunks = d_chunk;
+  int nch = nchunk;
+  if (i_lo != 0 || i_hi != (int)diag.size()) {
+    auto key = std::make_pair(i_lo, i_hi);
+    auto it = sub_chunks.find(key);
+    if (it == sub_chunks.end()) {
+      std::vector<int> sc{i_lo};
+      for (int b : h_chunk)
+        if (b > i_lo && b < i_hi) sc.push_back(b);
+      if (i_hi > i_lo) sc.push_back(i_hi);
+      int* d = nullptr;
+      CK(cudaMalloc((void**)&d, sc.size() * sizeof(int)));
+      CK(cudaMemcpy(d, sc.data(), sc.size() * sizeof(int), cudaMemcpyHostToDevice));
+      it = sub_chunks.emplace(key, std::make_pair(d, (int)sc.size() - 1)).first;
     }
-    CK(cudaStreamSynchronize(c.stream));
-    keys_resolved = true;
+    chunks = it->second.first;
+    nch = it->second.second;
   }
   u64d* tmp = c.alloc((size_t)B * l * N);
   u64d* D = c.alloc((size_t)B * l * (l + 1) * N);
-  u64d* acc = c.alloc((size_t)B * 2 * (l + 1) * N);
-  u64d* cacc = c.alloc((size_t)B * 2 * l * N);
-  u64d* tmpP = c.alloc((size_t)B * 2 * N);
-  CtBatch u{&c, B, l, v.scale * (double)c.P->q(l - 1), c.alloc((size_t)B * 2 * l * N)};
   // (1) one ModUp of v.c1 for all diagonals (hoisting)
   ks_modup(c, v.d + (size_t)l * N, (long)v.stride(), B, l, nullptr, tmp, D);
   // (2) diagonal accumulation in the extended basis
   int keyed = 0;
-  for (const HsDiag& dd : diag) keyed += dd.shift != 0;
+  for (int i = i_lo; i < i_hi; ++i) keyed += diag[i].shift != 0;
   const int first_keyed = !diag.empty() && diag[0].shift == 0 ? 1 : 0;
-  HsDiagTable tab{(int)diag.size(), keyed, d_r, fkeys, (size_t)l * 2 * (l + 1) * N, first_keyed, masks, nchunk,
-                  d_chunk};
-  launch_hs_diag(c, v.d, B, l, D, tab, acc, cacc);
+  if (nch > 0 && i_hi > i_lo) {
+    HsDiagTable tab{i_hi - i_lo, keyed, d_r, fkeys, (size_t)l * 2 * (l + 1) * N, first_keyed, i_lo == 0 ? 1 : 0,
+                    masks, nch, chunks};
+    launch_hs_diag(c, v.d, B, l, D, tab, acc, cacc);
+  } else {
+    CK(cudaMemsetAsync(acc, 0, (size_t)B * 2 * (l + 1) * N * 8, c.stream));
+    CK(cudaMemsetAsync(cacc, 0, (size_t)B * 2 * l * N * 8, c.stream));
+  }
+  c.free(tmp);
+  c.free(D);
+}
+
+void HsPlan::finish(Context& c, int B, double v_scale, u64d* acc, u64d* cacc, int nparts, CtBatch& out) {
+  const int l = level, N = c.N(), S = c.S();
+  if (nparts > 1) {  // sums of nparts reduced residues
+    launch_reduce_rows(c, acc, (size_t)B * 2 * (l + 1) * N, l + 1, l);
+    launch_reduce_rows(c, cacc, (size_t)B * 2 * l * N, l, -1);
+  }
+  u64d* tmpP = c.alloc((size_t)B * 2 * N);
+  CtBatch u{&c, B, l, v_scale * (double)c.P->q(l - 1), c.alloc((size_t)B * 2 * l * N)};
   // (3) one ModDown of the sum (+ the Q-basis c-part)
   DropArgs d{};
   d.src = acc; d.src_b = 2L * (l + 1) * N; d.src_p = (long)(l + 1) * N; d.src_limbs = l + 1;
@@ -258,7 +297,7 @@ void HsPlan::run(Context& c, const CtBatch& v, CtBatch& out) {
   drop_last_limb(c, B, d, tmpP);
   // (4) rescale by q_{l-1}: the masks were encoded at exactly that scale
   eval_rescale(c, u, out);
-  out.scale = v.scale;
+  out.scale = v_scale;
   // (5) log-depth fold, matvec.cpp:101-103: s += rot_left(s, m_eff * 2^t)
   if (folds > 0) {
     CtBatch r{&c, B, l - 1, out.scale, c.alloc((size_t)B * 2 * (l - 1) * N)};
@@ -273,7 +312,18 @@ void HsPlan::run(Context& c, const CtBatch& v, CtBatch& out) {
     }
     c.free(r.d);
   }
-  c.free(tmp); c.free(D); c.free(acc); c.free(cacc); c.free(tmpP); c.free(u.d);
+  c.free(tmpP);
+  c.free(u.d);
+}
+
+void HsPlan::run(Context& c, const CtBatch& v, CtBatch& out) {
+  const int B = v.count, l = level, N = c.N();
+  u64d* acc = c.alloc((size_t)B * 2 * (l + 1) * N);
+  u64d* cacc = c.alloc((size_t)B * 2 * l * N);
+  accumulate(c, v, 0, (int)diag.size(), acc, cacc);
+  finish(c, B, v.scale, acc, cacc, 1, out);
+  c.free(acc);
+  c.free(cacc);
 }
 
 }  // namespace hegpu

@@ -4,6 +4,7 @@
 //   square_layer square_layer        proj/src/convlower.cpp:141-143
 //   HsPlan      extract_diagonals + hs_matvec  proj/src/matvec.cpp:45-105
 #pragma once
+#include <map>
 
 #include "engine.hpp"
 
@@ -47,12 +48,22 @@ struct HsPlan {
   int* d_r = nullptr;         // [kept] right rotations
   int* d_chunk = nullptr;     // chunk boundaries
   int nchunk = 0;
+  std::vector<int> h_chunk;   // chunk boundaries (host copy)
+  std::map<std::pair<int, int>, std::pair<int*, int>> sub_chunks;  // diagonal range -> (device chunks, count)
   u64d* fkeys = nullptr;      // [keyed][level][2][level+1][N] key_i * mask_i (first run)
   bool keys_resolved = false;
   void build(Context& c, const double* A, int m, int n, int level, bool skip_zero);
   void release();
   std::vector<int64_t> right_rotations() const;  // diagonals, then folds
   void run(Context& c, const CtBatch& v, CtBatch& out);
+  // distributed HS (config 3): the extended-basis accumulators of the kept
+  // diagonals [i_lo, i_hi) -- acc [B][2][l+1][N], cacc [B][2][l][N] -- and the
+  // finish (ModDown, rescale, folds) on accumulators summed over nparts
+  // such ranges (entries < nparts * q, reduced here)
+  void ensure_keys(Context& c);
+  void accumulate(Context& c, const CtBatch& v, int i_lo, int i_hi, u64d* acc, u64d* cacc);
+  void finish(Context& c, int B, double v_scale, u64d* acc, u64d* cacc, int nparts, CtBatch& out);
+  size_t acc_words(int B, int N) const { return (size_t)B * (2 * (level + 1) + 2 * level) * N; }
   Context* ctx = nullptr;
 };
 

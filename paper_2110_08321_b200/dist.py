@@ -26,6 +26,16 @@ def gather_outputs(local, world: int, out=None):
     return out
 
 
+def reduce_partials(acc, world: int):
+    """element-wise sum of the per-rank HS partial accumulators (int64 view
+    of uint64 residues < 2^60: the sum of <= 8 stays < 2^63, so the int64
+    all-reduce is exact); the library's finish reduces mod q.  In place."""
+    import torch.distributed as dist
+    if world > 1:
+        dist.all_reduce(acc, op=dist.ReduceOp.SUM)
+    return acc
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """the step time every rank reports is the max over ranks"""
     import torch

@@ -124,6 +124,9 @@ def lib():
             "hegpu_hs_plan_rotations": (i, [vp, vp, i]),
             "hegpu_hs_plan_info": (i, [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i)]),
             "hegpu_hs_matvec": (i, [vp, vp, vp, vp]),
+            "hegpu_hs_acc_words": (C.c_size_t, [vp, i]),
+            "hegpu_hs_matvec_partial": (i, [vp, vp, vp, i, i, vp]),
+            "hegpu_hs_matvec_finish": (i, [vp, vp, vp, vp, i, vp]),
             "hegpu_net_create": (i, [vp, C.POINTER(NetSpec), f64p, f64p, vp, vp, pp]),
             "hegpu_net_destroy": (None, [vp]),
             "hegpu_net_run": (i, [vp, vp, vp]),
@@ -362,6 +365,20 @@ class Context:
 
     def hs_matvec(self, plan, v, out):
         self.check(lib().hegpu_hs_matvec(self.h, plan.h, v.h, out.h))
+        return out
+
+    def hs_acc_words(self, plan, batch):
+        return int(lib().hegpu_hs_acc_words(plan.h, batch))
+
+    def hs_matvec_partial(self, plan, v, part, nparts, acc):
+        """extended-basis partial accumulator of diagonal range `part` of
+        `nparts` into `acc` (a CUDA int64 tensor of hs_acc_words words)"""
+        self.check(lib().hegpu_hs_matvec_partial(self.h, plan.h, v.h, part, nparts, acc.data_ptr()))
+        return acc
+
+    def hs_matvec_finish(self, plan, v, acc, nparts, out):
+        """ModDown + rescale + folds from the element-wise sum of nparts partials"""
+        self.check(lib().hegpu_hs_matvec_finish(self.h, plan.h, v.h, acc.data_ptr(), nparts, out.h))
         return out
 
 

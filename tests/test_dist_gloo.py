@@ -49,6 +49,38 @@ def test_shard_and_gather_two_ranks():
     assert t == 1.5  # max over ranks
 
 
+def _reduce_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(rank)
+    # residues below a 60-bit prime, as the HS partial accumulators hold
+    part = rng.integers(0, (1 << 60) - 93, 64, dtype=np.uint64)
+    acc = torch.from_numpy(part.view(np.int64).copy())
+    D.reduce_partials(acc, world)
+    q.put((rank, part, acc.numpy().view(np.uint64).copy()))
+    dist.destroy_process_group()
+
+
+def test_reduce_partials_two_ranks():
+    """the config-3 HS partial-sum reduction: an int64 SUM all-reduce of
+    uint64 residues is the exact element-wise sum (< 2^63 for <= 8 parts)"""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_reduce_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    parts = {r: part for r, part, _ in res}
+    want = [int(a) + int(b) for a, b in zip(parts[0], parts[1])]
+    for _, _, got in res:
+        assert [int(x) for x in got] == want
+
+
 def test_image_ranges_partition_the_batch():
     seen = [i for r in range(4) for i in D.image_range(r, 64)]
     assert seen == list(range(256))

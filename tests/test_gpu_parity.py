@@ -227,6 +227,38 @@ def test_hs_matvec(pair, m, n, skip):
     assert ctx.total() == mc.tally.as_tuple()
 
 
+@pytest.mark.parametrize("m,n,nparts", [(300, 200, 3), (32, 300, 2), (10, 100, 8), (4, 4, 5)])
+def test_hs_matvec_split_partial_sums(pair, m, n, nparts):
+    """config-3 style distributed HS: per-part extended-basis accumulators
+    over diagonal ranges, summed element-wise (what the NCCL all-reduce
+    does), then one finish == the single-GPU hs_matvec bit for bit, with the
+    same total metering"""
+    import torch
+    ctx, ck = pair
+    rng = np.random.default_rng(7 * m + n)
+    l = 3
+    A = np.eye(4) if (m, n) == (4, 4) else rng.normal(0, 0.05, (m, n))
+    z, v = fresh(ck, rng, l, 300 + m, n=n)
+    plan = ctx.hs_plan(A, l, True)
+    ctx.gen_rotation_keys(plan.rotations())
+    dv = ctx.ct(1, l, v, DELTA)
+    want = ctx.hs_matvec(plan, dv, ctx.ct(1, l - 1)).download()
+    ctx.reset_meter()
+    words = ctx.hs_acc_words(plan, 1)
+    total = torch.zeros(words, dtype=torch.int64, device="cuda")
+    for p in range(nparts):
+        part = torch.empty(words, dtype=torch.int64, device="cuda")
+        ctx.hs_matvec_partial(plan, dv, p, nparts, part)
+        ctx.sync()
+        total += part
+    out = ctx.ct(1, l - 1)
+    ctx.hs_matvec_finish(plan, dv, total, nparts, out)
+    assert np.array_equal(out.download(), want)
+    mc = HS.MeterContext()
+    HS.hs_matvec(A, HS.pack(z, ck.S, HS.CIPHERTEXT), mc, skip_zero_diagonals=True)
+    assert ctx.total() == mc.tally.as_tuple()
+
+
 def test_hs_capacity(pair):
     ctx, ck = pair
     with pytest.raises(H.CapacityError):
