@@ -80,27 +80,59 @@ def config1(args):
 
 def config3(args):
     """BASELINE configs[3]: CIFAR-shaped net (3x32x32 U[0,1], conv 5x5/2
-    3->32, square, HS 6272->256, square, HS 256->10), N=16384, 5 rescales."""
+    3->32, square, HS 6272->256, square, HS 256->10), N=16384, 5 rescales.
+    Under torchrun: --split-hs splits HS1's diagonals across the ranks (same
+    images on every rank, partial extended-basis sums all-reduced over NCCL,
+    strong scaling); otherwise images are sharded (weak scaling)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2110_08321_b200 import dist as D
     from paper_2110_08321_b200 import hegpu as H
     from paper_2110_08321_b200.workloads import CFG3, net_image, net_weights
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
     cfg = CFG3
-    ctx = H.Context(cfg.log_n, list(cfg.qbits), cfg.pbits, seed=3)
+    ctx = H.Context(cfg.log_n, list(cfg.qbits), cfg.pbits, seed=3, device=local)
     t0 = time.perf_counter()
     net = H.Net(ctx, cfg, net_weights(cfg, 3))
     setup_s = time.perf_counter() - t0
     B = args.batch
-    taps = np.concatenate([net.encrypt_image(net_image(cfg, i), nonce=i) for i in range(B)])
+    first = 0 if args.split_hs else rank * B
+    taps = np.concatenate([net.encrypt_image(net_image(cfg, first + i), nonce=first + i) for i in range(B)])
     dt = ctx.ct(B * net.ntaps, net.top, taps, DELTA)
     out = ctx.ct(B, net.out_level)
-    net.run(dt, out)
-    ctx.reset_meter()
-    g = ctx.capture(lambda: net.run(dt, out))
+    if args.split_hs and world > 1:
+        def run():
+            net.run_split(dt, out, 0, rank, world, lambda t: D.reduce_partials(t, world))
+        run()
+        ref = ctx.ct(B, net.out_level)
+        net.run(dt, ref)
+        assert np.array_equal(out.download(), ref.download()), "split HS differs from the single-GPU run"
+        fn = run
+        ctx.reset_meter()
+        fn()
+    else:
+        net.run(dt, out)
+        ctx.reset_meter()  # the capture meters one step (graph replays do not)
+        fn = ctx.capture(lambda: net.run(dt, out))
     tally = ctx.total()
-    ms = timed(ctx, g, args.steps, args.warmup)
-    print(json.dumps({
-        "config": 3, "batch": B, "ms_per_step": ms, "inferences_per_s": B / (ms / 1e3),
-        "rotations_per_s": tally[4] / (ms / 1e3), "hops_per_inference": [t / B for t in tally],
-        "setup_s": setup_s}), flush=True)
+    if world > 1:
+        dist.barrier()
+    ms = timed(ctx, fn, args.steps, args.warmup)
+    ms = D.max_over_ranks(ms, device=f"cuda:{local}")
+    imgs = B if args.split_hs else B * world
+    if rank == 0:
+        print(json.dumps({
+            "config": 3, "batch": B, "n_gpus": world, "mode": "split-hs" if args.split_hs else "image-shard",
+            "ms_per_step": ms, "inferences_per_s": imgs / (ms / 1e3),
+            "rotations_per_s": tally[4] * (1 if args.split_hs else world) / (ms / 1e3),
+            "hops_per_inference": [t / B for t in tally], "setup_s": setup_s}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def config4(args):
@@ -145,6 +177,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--split-hs", action="store_true", help="config 3 under torchrun: split HS1 across ranks")
     args = ap.parse_args()
     {1: config1, 3: config3, 4: config4}[args.config](args)
 

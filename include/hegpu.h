@@ -223,6 +223,16 @@ int hegpu_net_create(hegpu_ctx* ctx, const hegpu_net_spec* spec, const double* c
 void hegpu_net_destroy(hegpu_net* net);
 /* device-resident run: taps = count B*ntaps at the top level */
 int hegpu_net_run(hegpu_net* net, const hegpu_ct* taps, hegpu_ct* out);
+/* config 3 across GPUs ("partial sums reduced across GPUs"): the same run,
+ * but dense layer `layer`'s HS accumulates only diagonal range `part` of
+ * `nparts` (hegpu_hs_matvec_partial); `reduce(dev_words, words, user)` is
+ * then called with the engine stream synchronised and must replace the
+ * device accumulator by the element-wise int64 sum over all parts (an NCCL
+ * all-reduce; return 0 on success); every rank then finishes the layer and
+ * the rest of the net identically.  Bit-identical to hegpu_net_run. */
+typedef int (*hegpu_reduce_fn)(void* dev_words, size_t words, void* user);
+int hegpu_net_run_split(hegpu_net* net, const hegpu_ct* taps, hegpu_ct* out, int layer, int part, int nparts,
+                        hegpu_reduce_fn reduce, void* user);
 /* the same on device-resident compact taps (batch x hegpu_net_compact_image_bytes
  * bytes, as hegpu_net_encrypt_image_compact writes them): the conv MAC
  * decodes c0 and regenerates c1 on the fly */

@@ -53,6 +53,13 @@ struct hegpu_net {
     int64_t launches = 0;
   };
   std::vector<ServeGraph> serve_graphs;
+  // hegpu_net_run_split: dense layer `layer`'s HS accumulated over part
+  // `part` of `nparts` diagonal ranges, partials combined by `reduce`
+  struct Split {
+    int layer = -1, part = 0, nparts = 1;
+    hegpu_reduce_fn reduce = nullptr;
+    void* user = nullptr;
+  } split;
   ~hegpu_net() {
     for (auto& p : plans) p.release();
     for (u64d* b : bias) cudaFree(b);
@@ -148,13 +155,29 @@ void run_after_conv(hegpu_net& net, const CtBatch& mb, CtBatch& out) {
     HsPlan& pl = net.plans[i];
     const bool last = i + 1 == s.n_dense;
     CtBatch z{&c, B, l - 1, 0, last ? out.d : cur.p};
-    pl.run(c, y, z);
     const int64_t kept = (int64_t)pl.diag.size();
+    int i_lo = 0, i_hi = (int)kept;
+    if (net.split.layer == i) {
+      // this rank's diagonal range; partial sums combined by the caller's
+      // reduction (NCCL all-reduce), then one ModDown / rescale / folds
+      const auto& sp = net.split;
+      i_lo = (int)(kept * sp.part / sp.nparts);
+      i_hi = (int)(kept * (sp.part + 1) / sp.nparts);
+      const size_t words = pl.acc_words(B, N);
+      Scratch acc(c, words);
+      u64d* cacc = acc.p + (size_t)B * 2 * (l + 1) * N;
+      pl.accumulate(c, y, i_lo, i_hi, acc.p, cacc);
+      CK(cudaStreamSynchronize(c.stream));
+      need(sp.reduce(acc.p, words, sp.user) == 0, HEGPU_ERR_CUDA, "net_run_split: the partial-sum reduction failed");
+      pl.finish(c, B, y.scale, acc.p, cacc, sp.nparts, z);
+    } else {
+      pl.run(c, y, z);
+    }
     int64_t rots = 0;
-    for (const auto& d : pl.diag) rots += d.right != 0;
-    c.meter.bump(HEGPU_MUL_PC, B * kept);
+    for (int d = i_lo; d < i_hi; ++d) rots += pl.diag[d].right != 0;
+    c.meter.bump(HEGPU_MUL_PC, B * (i_hi - i_lo));
     c.meter.bump(HEGPU_ROT, B * (rots + pl.folds));
-    c.meter.bump(HEGPU_ADD_CC, B * ((kept > 0 ? kept - 1 : 0) + pl.folds));
+    c.meter.bump(HEGPU_ADD_CC, B * ((i_lo == 0 && i_hi > 0 ? i_hi - i_lo - 1 : i_hi - i_lo) + pl.folds));
     // bias add(out, pack(b)) (netcompile.cpp:423)
     launch_add_plain(c, z.d, net.bias[i], 0, z.d, B, l - 1);
     c.meter.bump(HEGPU_ADD_PC, B);
@@ -248,6 +271,31 @@ extern "C" int hegpu_net_run(hegpu_net* net, const hegpu_ct* taps, hegpu_ct* out
          "net_run: bad output handle");
     CtBatch o = out->b;
     run_net(*net, taps->b, o);
+    out->b.scale = o.scale;
+  });
+}
+
+extern "C" int hegpu_net_run_split(hegpu_net* net, const hegpu_ct* taps, hegpu_ct* out, int layer, int part,
+                                   int nparts, hegpu_reduce_fn reduce, void* user) {
+  if (!net || !taps || !out || !reduce) return HEGPU_ERR_ARG;
+  Context& c = *net->c;
+  return guarded(&c, [&] {
+    need(layer >= 0 && layer < net->spec.n_dense, HEGPU_ERR_RANGE, "net_run_split: no such dense layer");
+    need(nparts >= 1 && nparts <= 8 && part >= 0 && part < nparts, HEGPU_ERR_RANGE, "net_run_split: bad part");
+    need(taps->b.level == net->top && taps->b.count % net->ntaps == 0, HEGPU_ERR_SHAPE,
+         "net_run_split: taps must be B*ntaps ciphertexts at the top level");
+    const int B = taps->b.count / net->ntaps;
+    need(out->b.count == B && out->b.level == net->top - 1 - 2 * net->spec.n_dense, HEGPU_ERR_SHAPE,
+         "net_run_split: bad output handle");
+    net->split = {layer, part, nparts, reduce, user};
+    CtBatch o = out->b;
+    try {
+      run_net(*net, taps->b, o);
+    } catch (...) {
+      net->split = {};
+      throw;
+    }
+    net->split = {};
     out->b.scale = o.scale;
   });
 }

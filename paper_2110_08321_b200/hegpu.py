@@ -131,6 +131,7 @@ def lib():
             "hegpu_net_destroy": (None, [vp]),
             "hegpu_net_run": (i, [vp, vp, vp]),
             "hegpu_net_run_compact": (i, [vp, vp, i, vp]),
+            "hegpu_net_run_split": (i, [vp, vp, vp, i, i, i, REDUCE_FN, vp]),
             "hegpu_net_run_host": (i, [vp, vp, i, vp]),
             "hegpu_net_encrypt_image": (i, [vp, f64p, u, u64p]),
             "hegpu_net_decrypt_logits": (i, [vp, u64p, f64p]),
@@ -150,6 +151,18 @@ def lib():
             f.argtypes = args
         _lib = L
     return _lib
+
+
+# int (*hegpu_reduce_fn)(void* dev_words, size_t words, void* user)
+REDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
+class _DevWords:
+    """zero-copy view of a library device buffer for torch (CUDA array interface)"""
+
+    def __init__(self, ptr, words):
+        self.__cuda_array_interface__ = {"shape": (words,), "typestr": "<i8", "data": (ptr, False),
+                                         "version": 3, "strides": None}
 
 
 def declared_symbols():
@@ -555,6 +568,25 @@ class Net:
 
     def run(self, taps_ct, out_ct):
         self.ctx.check(lib().hegpu_net_run(self.h, taps_ct.h, out_ct.h))
+        return out_ct
+
+    def run_split(self, taps_ct, out_ct, layer, part, nparts, reduce):
+        """hegpu_net_run_split: dense layer `layer`'s HS over diagonal range
+        `part` of `nparts`; reduce(t) receives the partial accumulator as a
+        CUDA int64 tensor view and must sum it over all parts in place"""
+        import torch
+
+        def cb(ptr, words, _user):
+            try:
+                t = torch.as_tensor(_DevWords(ptr, words), device="cuda")
+                reduce(t)
+                torch.cuda.synchronize()
+                return 0
+            except Exception:  # reported as a failed reduction by the library
+                return 1
+
+        fn = REDUCE_FN(cb)
+        self.ctx.check(lib().hegpu_net_run_split(self.h, taps_ct.h, out_ct.h, layer, part, nparts, fn, None))
         return out_ct
 
     def run_compact(self, dev_taps, batch, out_ct):

@@ -359,6 +359,41 @@ def test_cfg0_run_compact_device_and_submit(cfg0):
     assert dict(ctx.stages()) == {k: tuple(6 * x for x in v) for k, v in want_stages.items()}
 
 
+def test_cfg0_net_run_split_dense1(cfg0):
+    """the multi-GPU config-3 scheme on one GPU: each "rank" runs the net with
+    HS1 restricted to its diagonal range, the partial accumulators are summed
+    (here: rank 0's partial is stashed and added by rank 1's reduction), and
+    the finished output equals the single-GPU run bit for bit, with the HOP
+    tallies of the two parts adding up to one run's"""
+    import torch
+    cfg, ctx, ck, w, net = cfg0
+    B = 2
+    imgs = [net_image(cfg, 80 + s) for s in range(B)]
+    taps = ctx.ct(B * net.ntaps, net.top,
+                  np.concatenate([net.encrypt_image(im, nonce=80 + s) for s, im in enumerate(imgs)]), DELTA)
+    ref = ctx.ct(B, net.out_level)
+    ctx.reset_meter()
+    net.run(taps, ref)
+    one_run = dict(ctx.stages())
+    want = ref.download()
+    # nparts = 1: plumbing only
+    out = ctx.ct(B, net.out_level)
+    net.run_split(taps, out, 0, 0, 1, lambda t: None)
+    assert np.array_equal(out.download(), want)
+    # nparts = 2: rank 0's partial sum is kept for rank 1's reduction
+    stash = {}
+    ctx.reset_meter()
+    net.run_split(taps, ctx.ct(B, net.out_level), 0, 0, 2, lambda t: stash.setdefault("p0", t.clone()))
+    net.run_split(taps, out, 0, 1, 2, lambda t: t.add_(stash["p0"]))
+    assert np.array_equal(out.download(), want)
+    # HS1's MulPC is split over the two parts; every other stage ran twice
+    two = dict(ctx.stages())
+    assert two["Dense1"][2] == one_run["Dense1"][2]
+    for st in one_run:
+        if st != "Dense1":
+            assert two[st] == tuple(2 * x for x in one_run[st])
+
+
 def test_cfg3_net_logits_and_hops():
     """Config 3 (CIFAR-shaped, N=16384): conv 5x5/2 3->32 (75 taps), merge 32
     maps (6272 slots), HS 6272->256, HS 256->10; logits vs ref_forward and
