@@ -46,7 +46,7 @@ def config1(args):
     from paper_2110_08321_b200 import hegpu as H
     from paper_2110_08321_b200.workloads import hs_sweep_case
     ctx = H.Context(14, [60, 40], 60, seed=1)
-    dims = [64, 256, 1024, 4096]
+    dims = [int(x) for x in args.dims.split(",")]
     for m in dims:
         for n in dims:
             A, x = hs_sweep_case(m, n)
@@ -54,7 +54,7 @@ def config1(args):
             plan = ctx.hs_plan(A, 2)
             ctx.gen_rotation_keys(plan.rotations())
             setup_s = time.perf_counter() - t0
-            for B in (1, args.batch):
+            for B in sorted({1, args.batch}):
                 pt = ctx.encode(x, DELTA, 2)
                 v = ctx.ct(B, 2, np.concatenate([ctx.encrypt(pt, 2, 7 + i) for i in range(B)]), DELTA)
                 out = ctx.ct(B, 1)
@@ -177,6 +177,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--dims", default="64,256,1024,4096", help="config 1 matrix dims (m and n)")
     ap.add_argument("--split-hs", action="store_true", help="config 3 under torchrun: split HS1 across ranks")
     args = ap.parse_args()
     {1: config1, 3: config3, 4: config4}[args.config](args)

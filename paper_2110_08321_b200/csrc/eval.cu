@@ -113,6 +113,11 @@ __device__ __forceinline__ void cp_async8(u64d* dst, const u64d* src) {
                : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 constexpr int kKsKT = HEGPU_KS_KT;
 #ifndef HEGPU_KS_STAGE
@@ -368,9 +373,18 @@ constexpr int kHsCW = 128;  // max r span of a chunk
 #ifndef HEGPU_HS_MINB
 #define HEGPU_HS_MINB 4
 #endif
-constexpr int kHsBT = HEGPU_HS_BT;  // images per thread
+#ifndef HEGPU_HS_PD1
+#define HEGPU_HS_PD1 4  // cp.async prefetch depth (diagonals) at 1 image per thread (measured 4 > 8 > 16 > 0)
+#endif
+#ifndef HEGPU_HS_PD2
+#define HEGPU_HS_PD2 8  // ... at 2 images per thread (measured 8 = 16 > 4 > 0)
+#endif
+constexpr int kHsBTMax = HEGPU_HS_BT;  // images per thread (smaller batches use 2 or 1)
 
-template <int LV>
+// PD > 0 (small batches, where the fused keys stream from HBM once per use):
+// each thread keeps the fused-key words of the next PD - 1 diagonals in
+// flight with cp.async into its own shared-memory ring slots
+template <int LV, int kHsBT, int PD>
 __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt, const u64d* __restrict__ v,
                                                    const u64d* __restrict__ D, int B, int L, int N,
                                                    HsDiagTable tab, u64d* __restrict__ acc,
@@ -424,26 +438,56 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
     // in flight while diagonal i is accumulated (addresses are arithmetic:
     // no load feeds another load's address)
     const u64d* fkb = tab.fk + p * kp + t * N + k;
+    u64d* ring = win + kHsBT * (LV + 1) * kW + threadIdx.x;  // [PD][LV + 1][KB]
+    auto issue = [&](int i) {
+      u64d* slot = ring + (i % (PD > 0 ? PD : 1)) * (LV + 1) * kHsKB;
+      if (i >= tab.first_keyed) {
+        const u64d* fk = fkb + (size_t)(i - tab.first_keyed) * tab.fk_words;
+#pragma unroll
+        for (int j = 0; j < LV; ++j) cp_async8(slot + j * kHsKB, fk + j * 2 * kp);
+      }
+      if (do_c0) cp_async8(slot + LV * kHsKB, mrow + (size_t)i * kp);
+    };
+    if constexpr (PD > 0) {
+#pragma unroll
+      for (int d = 0; d < PD - 1; ++d) {
+        if (i0 + d < i1) issue(i0 + d);
+        cp_async_commit();
+      }
+    }
     u64d kn[LV], mn = 0;
     int rn = __ldg(tab.r + i0);
-    {
+    if constexpr (PD == 0) {
       const u64d* fk = fkb + (size_t)(i0 - tab.first_keyed) * tab.fk_words;
 #pragma unroll
       for (int j = 0; j < LV; ++j) kn[j] = i0 >= tab.first_keyed ? __ldg(fk + j * 2 * kp) : 0ull;
       if (do_c0) mn = __ldg(mrow + (size_t)i0 * kp);
     }
     for (int i = i0; i < i1; ++i) {
-      const int r = rn;
       u64d kv[LV];
+      u64d m;
+      int r;
+      if constexpr (PD > 0) {
+        if (i + PD - 1 < i1) issue(i + PD - 1);
+        cp_async_commit();
+        cp_async_wait<(PD > 0 ? PD - 1 : 0)>();
+        const u64d* slot = ring + (i % (PD > 0 ? PD : 1)) * (LV + 1) * kHsKB;
+#pragma unroll
+        for (int j = 0; j < LV; ++j) kv[j] = slot[j * kHsKB];
+        m = do_c0 ? slot[LV * kHsKB] : 0ull;
+        r = __ldg(tab.r + i);
+      } else {
+      r = rn;
 #pragma unroll
       for (int j = 0; j < LV; ++j) kv[j] = kn[j];
-      const u64d m = mn;
+      m = mn;
       if (i + 1 < i1) {
         rn = __ldg(tab.r + i + 1);
         const u64d* fk = fkb + (size_t)(i + 1 - tab.first_keyed) * tab.fk_words;
 #pragma unroll
         for (int j = 0; j < LV; ++j) kn[j] = __ldg(fk + j * 2 * kp);  // i + 1 >= 1 >= first_keyed
         if (do_c0) mn = __ldg(mrow + (size_t)(i + 1) * kp);
+      }
       }
       const u64d* wp = wb - r;  // + (bb * (LV + 1) + row) * kW, compile-time below
       if (do_c0) {
@@ -540,15 +584,15 @@ unsigned grid_for(size_t total) {
   return (unsigned)(g < 148 * 16 ? (g ? g : 1) : 148 * 16);
 }
 
-template <int LV>
-void launch_hs_lv(Context& c, const u64d* v, int B, const u64d* D, const HsDiagTable& t, u64d* acc, u64d* cacc) {
+template <int LV, int kHsBT, int PD>
+void launch_hs_lvbt(Context& c, const u64d* v, int B, const u64d* D, const HsDiagTable& t, u64d* acc, u64d* cacc) {
   const int N = c.N(), S = N / 2;
   if (S < kHsKB) fail(HEGPU_ERR_ARG, "hs_matvec on the device needs N >= 256");
   dim3 grid((B + kHsBT - 1) / kHsBT, N / kHsKB, 2 * (LV + 1));
-  const size_t sm = (size_t)kHsBT * (LV + 1) * (kHsKB + kHsCW) * 8;
+  const size_t sm = ((size_t)kHsBT * (LV + 1) * (kHsKB + kHsCW) + (size_t)PD * (LV + 1) * kHsKB) * 8;
   static size_t done = 0;
   if (sm > 48 * 1024 && sm > done) {
-    CK(cudaFuncSetAttribute(k_hs_diag<LV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(k_hs_diag<LV, kHsBT, PD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     done = sm;
   }
   // fused keys + masks (c-part limbs) once; v, D read once; acc, cacc written once
@@ -563,7 +607,7 @@ void launch_hs_lv(Context& c, const u64d* v, int B, const u64d* D, const HsDiagT
   if (base < target && t.nchunk > 1) gsplit = std::min(t.nchunk, (target + base - 1) / base);
   if (gsplit == 1) {
     LAUNCH_BO(c, "k_hs_diag", bytes, ops,
-             k_hs_diag<LV><<<grid, kHsKB, sm, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc, 1, 0, 0));
+             k_hs_diag<LV, kHsBT, PD><<<grid, kHsKB, sm, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc, 1, 0, 0));
     return;
   }
   const size_t acc_w = (size_t)B * 2 * (LV + 1) * N, cacc_w = (size_t)B * 2 * LV * N;
@@ -571,7 +615,7 @@ void launch_hs_lv(Context& c, const u64d* v, int B, const u64d* D, const HsDiagT
   u64d* pc = c.alloc(gsplit * cacc_w);
   grid.x *= gsplit;
   LAUNCH_BO(c, "k_hs_diag", bytes, ops,
-           k_hs_diag<LV><<<grid, kHsKB, sm, c.stream>>>(c.primes, v, D, B, c.L(), N, t, pa, pc, gsplit, acc_w,
+           k_hs_diag<LV, kHsBT, PD><<<grid, kHsKB, sm, c.stream>>>(c.primes, v, D, B, c.L(), N, t, pa, pc, gsplit, acc_w,
                                                          cacc_w));
   LAUNCH_B(c, "k_sum_parts", 8.0 * (gsplit + 1) * acc_w,
            k_sum_parts<<<grid_for(acc_w), kTpb, 0, c.stream>>>(c.primes, pa, acc, acc_w, gsplit, LV + 1, LV, c.L(), N));
@@ -579,6 +623,15 @@ void launch_hs_lv(Context& c, const u64d* v, int B, const u64d* D, const HsDiagT
            k_sum_parts<<<grid_for(cacc_w), kTpb, 0, c.stream>>>(c.primes, pc, cacc, cacc_w, gsplit, LV, -1, c.L(), N));
   c.free(pa);
   c.free(pc);
+}
+
+// images per thread: 4 for batches >= 4 (fused keys reused 4x), else the
+// batch itself (B = 1 would otherwise compute 3 zero images per thread)
+template <int LV>
+void launch_hs_lv(Context& c, const u64d* v, int B, const u64d* D, const HsDiagTable& t, u64d* acc, u64d* cacc) {
+  if (B >= kHsBTMax) launch_hs_lvbt<LV, kHsBTMax, 0>(c, v, B, D, t, acc, cacc);
+  else if (B >= 2) launch_hs_lvbt<LV, 2, HEGPU_HS_PD2>(c, v, B, D, t, acc, cacc);
+  else launch_hs_lvbt<LV, 1, HEGPU_HS_PD1>(c, v, B, D, t, acc, cacc);
 }
 
 }  // namespace

@@ -77,7 +77,11 @@ __device__ __forceinline__ void fwd_pass(u64d (&x)[1 << lr_of(LOGN)], const ulon
         const ulonglong2 W = __ldg(tw + (1 << (S0 + u)) + (hi << u) + (j >> (RR - u)));
         // values in [0, 8q) (q < 2^60): one conditional subtraction per butterfly
         u64d a = x[g * J + j];
+#ifdef HEGPU_CSUB_LOP3
+        a = csub64(a, q4);
+#else
         if (a >= q4) a -= q4;
+#endif
         const u64d t = shoup_mul_lazy4(x[g * J + j + half], W.x, W.y, q);  // [0, 4q)
         x[g * J + j] = a + t;
         x[g * J + j + half] = a - t + q4;
@@ -168,7 +172,11 @@ __device__ __forceinline__ void inv_pass(u64d (&x)[1 << lr_of(LOGN)], const ulon
         // values in [0, 4q): one conditional subtraction per butterfly
         const u64d a = x[g * J + j], b = x[g * J + j + dist];
         u64d s = a + b;
+#ifdef HEGPU_CSUB_LOP3
+        s = csub64(s, q4);
+#else
         if (s >= q4) s -= q4;
+#endif
         x[g * J + j] = s;
         x[g * J + j + dist] = shoup_mul_lazy4(a - b + q4, W.x, W.y, q);  // [0, 4q)
       }
