@@ -1,6 +1,7 @@
 """bench_configs.py -- the other BASELINE.json configs on one B200 (bench.py
 measures the headline config 2).  One JSON line per measured point.
 
+  python bench_configs.py --config 0   # cfg-0 net, batch 1 (one inference's latency)
   python bench_configs.py --config 1   # HS matvec sweep, N=16384, one rescale
   python bench_configs.py --config 3   # CIFAR-shaped net, N=16384, 5 rescales
   python bench_configs.py --config 4   # conv-pack layer sweep, N=16384
@@ -78,7 +79,14 @@ def config1(args):
             del plan
 
 
-def config3(args):
+def config0(args):
+    """BASELINE configs[0]: the cfg-0 MNIST-sized net at batch 1 (latency of
+    one encrypted inference, device-resident taps, one CUDA graph)."""
+    args.batch = 1
+    return config3(args, which=0)
+
+
+def config3(args, which=3):
     """BASELINE configs[3]: CIFAR-shaped net (3x32x32 U[0,1], conv 5x5/2
     3->32, square, HS 6272->256, square, HS 256->10), N=16384, 5 rescales.
     Under torchrun: --split-hs splits HS1's diagonals across the ranks (same
@@ -88,17 +96,17 @@ def config3(args):
     import torch.distributed as dist
     from paper_2110_08321_b200 import dist as D
     from paper_2110_08321_b200 import hegpu as H
-    from paper_2110_08321_b200.workloads import CFG3, net_image, net_weights
+    from paper_2110_08321_b200.workloads import CFG0, CFG3, net_image, net_weights
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
-    cfg = CFG3
-    ctx = H.Context(cfg.log_n, list(cfg.qbits), cfg.pbits, seed=3, device=local)
+    cfg = CFG3 if which == 3 else CFG0
+    ctx = H.Context(cfg.log_n, list(cfg.qbits), cfg.pbits, seed=which, device=local)
     t0 = time.perf_counter()
-    net = H.Net(ctx, cfg, net_weights(cfg, 3))
+    net = H.Net(ctx, cfg, net_weights(cfg, which))
     setup_s = time.perf_counter() - t0
     B = args.batch
     first = 0 if args.split_hs else rank * B
@@ -127,7 +135,7 @@ def config3(args):
     imgs = B if args.split_hs else B * world
     if rank == 0:
         print(json.dumps({
-            "config": 3, "batch": B, "n_gpus": world, "mode": "split-hs" if args.split_hs else "image-shard",
+            "config": which, "batch": B, "n_gpus": world, "mode": "split-hs" if args.split_hs else "image-shard",
             "ms_per_step": ms, "inferences_per_s": imgs / (ms / 1e3),
             "rotations_per_s": tally[4] * (1 if args.split_hs else world) / (ms / 1e3),
             "hops_per_inference": [t / B for t in tally], "setup_s": setup_s}), flush=True)
@@ -173,14 +181,14 @@ def config4(args):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", type=int, required=True, choices=[1, 3, 4])
+    ap.add_argument("--config", type=int, required=True, choices=[0, 1, 3, 4])
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--dims", default="64,256,1024,4096", help="config 1 matrix dims (m and n)")
     ap.add_argument("--split-hs", action="store_true", help="config 3 under torchrun: split HS1 across ranks")
     args = ap.parse_args()
-    {1: config1, 3: config3, 4: config4}[args.config](args)
+    {0: config0, 1: config1, 3: config3, 4: config4}[args.config](args)
 
 
 if __name__ == "__main__":
