@@ -258,6 +258,37 @@ int hegpu_net_run_host_compact(hegpu_net* net, const uint8_t* host_taps, int bat
 int hegpu_net_submit_host_compact(hegpu_net* net, const uint8_t* host_taps, int batch, int chunk,
                                   uint64_t* host_out);
 int hegpu_net_wait(hegpu_net* net);
+/* ---- model / weights / input files (proj/src/modelio.cpp:106-248) ----------
+ * model JSON {"name", "input": [c, d, d], "n_slots", "layers": [{"kind",
+ * "k", "s", "out_channels" | "units", "groups", "policy", "label"}]} with
+ * unknown keys rejected; weights a little-endian float32 stream in layer
+ * order (conv [c_out][c_in][k][k] then [c_out]; dense [m][n] then [m]);
+ * inputs [c][d][d] float32.  Errors: HEGPU_ERR_IO (hesim::IoError). */
+typedef struct hegpu_model hegpu_model;
+enum {
+  HEGPU_LAYER_CONV = 0, HEGPU_LAYER_SUBCONV = 1, HEGPU_LAYER_AVGPOOL = 2,
+  HEGPU_LAYER_SQUARE = 3, HEGPU_LAYER_FLATTEN = 4, HEGPU_LAYER_DENSE = 5
+};
+enum {
+  HEGPU_POLICY_CONVPACK = 0, HEGPU_POLICY_HS = 1, HEGPU_POLICY_LOLA_DENSE = 2, HEGPU_POLICY_LOLA_STACKED = 3
+};
+int hegpu_model_parse(const char* json_text, hegpu_model** out);       /* parse_model_json */
+int hegpu_model_load(const char* name_or_path, hegpu_model** out);      /* resolve_model ($HECNN_MODEL_DIR) */
+const char* hegpu_model_last_error(const hegpu_model* model);          /* NULL: last parse/load failure */
+void hegpu_model_destroy(hegpu_model* model);
+int hegpu_model_info(const hegpu_model* model, int* in_c, int* in_d, int* n_slots, int* n_layers,
+                     size_t* weight_floats);
+/* policy = -1 when the layer names none */
+int hegpu_model_layer(const hegpu_model* model, int i, int* kind, int* k, int* s, int* out, int* groups,
+                      int* policy);
+int hegpu_model_load_weights(hegpu_model* model, const char* path, double* out, size_t count); /* load_weights */
+int hegpu_model_save_weights(hegpu_model* model, const char* path, const double* w, size_t count);
+int hegpu_model_load_input(hegpu_model* model, const char* path, double* out);   /* load_input */
+int hegpu_model_save_input(hegpu_model* model, const char* path, const double* x);
+/* the net spec of a model in the GPU path's family conv, square, [flatten],
+ * dense, (square, dense)*; HEGPU_ERR_SHAPE otherwise */
+int hegpu_model_net_spec(const hegpu_model* model, hegpu_net_spec* spec);
+int hegpu_net_create_from_model(hegpu_ctx* ctx, hegpu_model* model, const char* weights_path, hegpu_net** out);
 /* logits: decrypt + decode output ct (wire) into m_last values */
 int hegpu_net_decrypt_logits(hegpu_net* net, const uint64_t* out_ct, double* logits);
 double hegpu_net_output_scale(const hegpu_net* net);

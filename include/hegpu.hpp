@@ -288,4 +288,51 @@ inline Ciphertext hs_matvec(const HsPlan& plan, const Ciphertext& v, Context& ct
   return out;
 }
 
+// ---- model / weights / input files (proj/include/hesim/modelio.hpp) --------
+class ModelSpec {
+ public:
+  explicit ModelSpec(hegpu_model* h) : h_(h) {}
+  ~ModelSpec() { hegpu_model_destroy(h_); }
+  ModelSpec(const ModelSpec&) = delete;
+  ModelSpec& operator=(const ModelSpec&) = delete;
+  ModelSpec(ModelSpec&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  hegpu_model* get() const { return h_; }
+  size_t weight_floats() const {
+    size_t n = 0;
+    hegpu_model_info(h_, nullptr, nullptr, nullptr, nullptr, &n);
+    return n;
+  }
+  void check(int rc) const { throw_status(rc, hegpu_model_last_error(h_)); }
+
+ private:
+  hegpu_model* h_;
+};
+
+inline ModelSpec parse_model_json(const std::string& text) {
+  hegpu_model* h = nullptr;
+  throw_status(hegpu_model_parse(text.c_str(), &h), hegpu_model_last_error(nullptr));
+  return ModelSpec(h);
+}
+inline ModelSpec resolve_model(const std::string& name_or_path) {
+  hegpu_model* h = nullptr;
+  throw_status(hegpu_model_load(name_or_path.c_str(), &h), hegpu_model_last_error(nullptr));
+  return ModelSpec(h);
+}
+// flat float32-rounded weights in layer order (conv bank + bias, dense W + b)
+inline std::vector<double> load_weights(const ModelSpec& m, const std::string& path) {
+  std::vector<double> w(m.weight_floats());
+  m.check(hegpu_model_load_weights(m.get(), path.c_str(), w.data(), w.size()));
+  return w;
+}
+inline void save_weights(const ModelSpec& m, const std::vector<double>& w, const std::string& path) {
+  m.check(hegpu_model_save_weights(m.get(), path.c_str(), w.data(), w.size()));
+}
+inline std::vector<double> load_input(const ModelSpec& m, const std::string& path) {
+  int c = 0, d = 0;
+  hegpu_model_info(m.get(), &c, &d, nullptr, nullptr, nullptr);
+  std::vector<double> x((size_t)c * d * d);
+  m.check(hegpu_model_load_input(m.get(), path.c_str(), x.data()));
+  return x;
+}
+
 }  // namespace hegpu

@@ -41,7 +41,12 @@ class RangeError(HegpuError, IndexError):
     """std::out_of_range (proj/src/slotvec.cpp:45-48)"""
 
 
-_ERR = {ERR_CAPACITY: CapacityError, ERR_SHAPE: ShapeError, ERR_LAYOUT: LayoutError, ERR_RANGE: RangeError}
+class IoError(HegpuError):
+    """hesim::IoError (model / weights / input files)"""
+
+
+_ERR = {ERR_CAPACITY: CapacityError, ERR_SHAPE: ShapeError, ERR_LAYOUT: LayoutError, ERR_RANGE: RangeError,
+        ERR_IO: IoError}
 
 
 class Params(C.Structure):
@@ -131,6 +136,19 @@ def lib():
             "hegpu_net_destroy": (None, [vp]),
             "hegpu_net_run": (i, [vp, vp, vp]),
             "hegpu_net_run_compact": (i, [vp, vp, i, vp]),
+            "hegpu_model_parse": (i, [C.c_char_p, pp]),
+            "hegpu_model_load": (i, [C.c_char_p, pp]),
+            "hegpu_model_last_error": (C.c_char_p, [vp]),
+            "hegpu_model_destroy": (None, [vp]),
+            "hegpu_model_info": (i, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                     C.POINTER(C.c_int), C.POINTER(C.c_size_t)]),
+            "hegpu_model_layer": (i, [vp, i] + [C.POINTER(C.c_int)] * 6),
+            "hegpu_model_load_weights": (i, [vp, C.c_char_p, f64p, C.c_size_t]),
+            "hegpu_model_save_weights": (i, [vp, C.c_char_p, f64p, C.c_size_t]),
+            "hegpu_model_load_input": (i, [vp, C.c_char_p, f64p]),
+            "hegpu_model_save_input": (i, [vp, C.c_char_p, f64p]),
+            "hegpu_model_net_spec": (i, [vp, C.POINTER(NetSpec)]),
+            "hegpu_net_create_from_model": (i, [vp, vp, C.c_char_p, pp]),
             "hegpu_net_run_split": (i, [vp, vp, vp, i, i, i, REDUCE_FN, vp]),
             "hegpu_net_run_host": (i, [vp, vp, i, vp]),
             "hegpu_net_encrypt_image": (i, [vp, f64p, u, u64p]),
@@ -533,6 +551,86 @@ class HsPlan:
             pass
 
 
+LAYER_KINDS = ("conv", "subconv", "avgpool", "square", "flatten", "dense")
+POLICIES = ("convpack", "hs", "lola-dense", "lola-stacked")
+
+
+class _SpecCfg:
+    """the NetConfig fields a Net needs, from a hegpu_net_spec"""
+
+    def __init__(self, spec):
+        self.in_c, self.in_d, self.k, self.s, self.c_out = spec.in_c, spec.in_d, spec.k, spec.stride, spec.c_out
+        self.dense = tuple(spec.dense_out[i] for i in range(spec.n_dense))
+
+
+class Model:
+    """A model description (parse_model_json / resolve_model,
+    proj/src/modelio.cpp:106-167) with its weights and input file formats."""
+
+    def __init__(self, h):
+        self.h = h
+        ic, d, ns, nl, nw = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_size_t()
+        self._check(lib().hegpu_model_info(h, C.byref(ic), C.byref(d), C.byref(ns), C.byref(nl), C.byref(nw)))
+        self.in_c, self.in_d, self.n_slots, self.weight_floats = ic.value, d.value, ns.value, nw.value
+        self.layers = []
+        for k in range(nl.value):
+            v = [C.c_int() for _ in range(6)]
+            self._check(lib().hegpu_model_layer(h, k, *[C.byref(x) for x in v]))
+            kind, kk, s, out, groups, pol = (x.value for x in v)
+            self.layers.append({"kind": LAYER_KINDS[kind], "k": kk, "s": s, "out": out, "groups": groups,
+                                "policy": POLICIES[pol] if pol >= 0 else None})
+
+    @staticmethod
+    def _status(rc, h=None):
+        if rc:
+            msg = lib().hegpu_model_last_error(h)
+            raise _ERR.get(rc, HegpuError)(rc, msg.decode() if msg else "")
+
+    def _check(self, rc):
+        Model._status(rc, self.h)
+
+    @classmethod
+    def parse(cls, text):
+        h = C.c_void_p()
+        cls._status(lib().hegpu_model_parse(text.encode(), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def load(cls, name_or_path):
+        h = C.c_void_p()
+        cls._status(lib().hegpu_model_load(str(name_or_path).encode(), C.byref(h)))
+        return cls(h)
+
+    def __del__(self):
+        try:
+            lib().hegpu_model_destroy(self.h)
+        except Exception:
+            pass
+
+    def load_weights(self, path):
+        out = np.empty(self.weight_floats, dtype=np.float64)
+        self._check(lib().hegpu_model_load_weights(self.h, str(path).encode(), out, out.size))
+        return out
+
+    def save_weights(self, path, flat):
+        flat = np.ascontiguousarray(flat, dtype=np.float64)
+        self._check(lib().hegpu_model_save_weights(self.h, str(path).encode(), flat, flat.size))
+
+    def load_input(self, path):
+        out = np.empty(self.in_c * self.in_d * self.in_d, dtype=np.float64)
+        self._check(lib().hegpu_model_load_input(self.h, str(path).encode(), out))
+        return out.reshape(self.in_c, self.in_d, self.in_d)
+
+    def save_input(self, path, x):
+        x = np.ascontiguousarray(x, dtype=np.float64).ravel()
+        self._check(lib().hegpu_model_save_input(self.h, str(path).encode(), x))
+
+    def net_spec(self):
+        spec = NetSpec()
+        self._status(lib().hegpu_model_net_spec(self.h, C.byref(spec)), None)
+        return spec
+
+
 class Net:
     """Stage driver (execute, proj/src/netcompile.cpp:291-446) for the
     Conv -> (Square -> Dense)* family on a batch of images."""
@@ -559,6 +657,24 @@ class Net:
         self.out_level = ctx.L - 1 - 2 * len(cfg.dense)
         self.tap_words = 2 * self.top * ctx.N
         self.out_words = 2 * self.out_level * ctx.N
+
+    @classmethod
+    def from_model(cls, ctx, model, weights_path):
+        """hegpu_net_create_from_model: the model's conv / square / dense
+        stack with its float32 weights file"""
+        spec = model.net_spec()
+        h = C.c_void_p()
+        ctx.check(lib().hegpu_net_create_from_model(ctx.h, model.h, str(weights_path).encode(), C.byref(h)))
+        self = cls.__new__(cls)
+        self.ctx = ctx
+        self.cfg = _SpecCfg(spec)
+        self.h = h
+        self.ntaps = spec.k * spec.k * spec.in_c
+        self.top = ctx.L
+        self.out_level = ctx.L - 1 - 2 * spec.n_dense
+        self.tap_words = 2 * self.top * ctx.N
+        self.out_words = 2 * self.out_level * ctx.N
+        return self
 
     def encrypt_image(self, image, nonce):
         out = np.empty(self.ntaps * self.tap_words, dtype=np.uint64)

@@ -134,6 +134,20 @@ int main() {
   // test_matvec.cpp:298-304 capacity violations throw
   CHECK_THROWS_AS(HsPlan(std::vector<double>(4 * (S + 1), 1.0), 4, S + 1, L, ctx), CapacityError);
 
+  // test_netcompile.cpp "model json round trip and validation" (modelio)
+  {
+    const ModelSpec m = parse_model_json(R"({"name": "tiny", "input": [1, 4, 4], "n_slots": 32, "layers": [
+      {"kind": "conv", "k": 3, "s": 1, "out_channels": 2, "label": "Conv1"}, {"kind": "square"},
+      {"kind": "flatten"}, {"kind": "dense", "units": 3, "label": "Dense1"}]})");
+    CHECK(m.weight_floats() == 2 * 9 + 2 + 3 * 8 + 3);
+    CHECK_THROWS_AS(parse_model_json(R"({"name":"x"})"), IoError);
+    CHECK_THROWS_AS(parse_model_json(R"({"name":"x","input":[1,2,2],"n_slots":8,"layers":[],"extra":1})"), IoError);
+    CHECK_THROWS_AS(parse_model_json(R"({"name":"x","input":[1,2,2],"n_slots":8,
+                                         "layers":[{"kind":"dense","units":1,"typo_field":2}]})"),
+                    IoError);
+    CHECK_THROWS_AS(load_weights(m, "/nonexistent/w.bin"), IoError);
+  }
+
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }

@@ -394,6 +394,30 @@ def test_cfg0_net_run_split_dense1(cfg0):
             assert two[st] == tuple(2 * x for x in one_run[st])
 
 
+def test_cfg0_net_from_model_files(cfg0, tmp_path):
+    """hegpu_net_create_from_model: the cfg-0 net described as a model JSON +
+    float32 weights file + float32 input file (the reference's formats)
+    computes bit-identical ciphertexts to the net built from arrays"""
+    from test_modelio import CFG0_JSON, flat_weights
+    cfg, ctx, ck, w, net = cfg0
+    model = H.Model.parse(CFG0_JSON)
+    model.save_weights(tmp_path / "w.bin", flat_weights(w))
+    img = net_image(cfg, 90)
+    model.save_input(tmp_path / "x.bin", img)
+    x = model.load_input(tmp_path / "x.bin")
+    assert np.array_equal(x, img)  # inputs are float32 values already
+    net2 = H.Net.from_model(ctx, model, tmp_path / "w.bin")
+    t1 = net.encrypt_image(img, nonce=90)
+    t2 = net2.encrypt_image(x, nonce=90)
+    assert np.array_equal(t1, t2)
+    o1, o2 = ctx.ct(1, net.out_level), ctx.ct(1, net2.out_level)
+    net.run(ctx.ct(net.ntaps, net.top, t1, DELTA), o1)
+    net2.run(ctx.ct(net2.ntaps, net2.top, t2, DELTA), o2)
+    assert np.array_equal(o1.download(), o2.download())
+    spec = HS.CnnSpec(cfg.in_c, cfg.in_d, cfg.k, cfg.s, cfg.c_out, cfg.dense, cfg.n_slots)
+    assert np.abs(net2.decrypt_logits(o2.download()) - HS.ref_forward(spec, w, img)).max() < 1e-3
+
+
 def test_cfg3_net_logits_and_hops():
     """Config 3 (CIFAR-shaped, N=16384): conv 5x5/2 3->32 (75 taps), merge 32
     maps (6272 slots), HS 6272->256, HS 256->10; logits vs ref_forward and

@@ -1,0 +1,98 @@
+"""Model / weights / input files (the reference's
+proj/src/modelio.cpp:106-248 behaviour; cases restated from
+proj/tests/test_netcompile.cpp "model json round trip and validation" and
+"weights and input files round trip").  Host-only: runs without a GPU."""
+import numpy as np
+import pytest
+
+from paper_2110_08321_b200 import hegpu as H
+from paper_2110_08321_b200.workloads import CFG0, net_weights
+
+TINY = """{
+  "name": "tiny",
+  "input": [1, 4, 4],
+  "n_slots": 32,
+  "layers": [
+    {"kind": "conv", "k": 3, "s": 1, "out_channels": 2, "label": "Conv1"},
+    {"kind": "square"},
+    {"kind": "flatten"},
+    {"kind": "dense", "units": 3, "label": "Dense1"}
+  ]
+}"""
+
+CFG0_JSON = """{"name": "cfg0-mnist", "input": [1, 29, 29], "n_slots": 4096, "layers": [
+  {"kind": "conv", "k": 5, "s": 2, "out_channels": 5, "policy": "convpack", "label": "Conv1"},
+  {"kind": "square"}, {"kind": "flatten"},
+  {"kind": "dense", "units": 100, "policy": "hs", "label": "Dense1"},
+  {"kind": "square"},
+  {"kind": "dense", "units": 10, "label": "Dense2"}]}"""
+
+
+def test_parse_tiny_model():
+    m = H.Model.parse(TINY)
+    assert (m.in_c, m.in_d, m.n_slots) == (1, 4, 4 * 8)
+    assert [l["kind"] for l in m.layers] == ["conv", "square", "flatten", "dense"]
+    assert m.layers[3]["out"] == 3 and m.layers[0]["k"] == 3
+    # conv 2x1x3x3 + 2, dense 3 x (2*2*2) + 3
+    assert m.weight_floats == 2 * 9 + 2 + 3 * 8 + 3
+    spec = m.net_spec()
+    assert (spec.k, spec.stride, spec.c_out, spec.n_dense, spec.dense_out[0]) == (3, 1, 2, 1, 3)
+
+
+@pytest.mark.parametrize("text", [
+    '{"name":"x"}',                                                          # missing fields
+    '{"name":"x","input":[1,2,2],"n_slots":8,"layers":[],"extra":1}',         # unknown top-level key
+    '{"name":"x","input":[1,2,2],"n_slots":8,"layers":[{"kind":"dense","units":1,"typo_field":2}]}',
+    '{"name":"x","input":[1,2,3],"n_slots":8,"layers":[]}',                  # non-square input
+    '{"name":"x","input":[1,2,2],"n_slots":8,"layers":[{"kind":"maxpool"}]}',  # unknown kind
+    '{"name":"x","input":[1,2,2],"n_slots":8,"layers":[{"kind":"dense","policy":"fft"}]}',
+    '{"name":"x","input":[1,2,2],"n_slots":8,"layers":[',                     # truncated JSON
+])
+def test_model_validation_rejects(text):
+    with pytest.raises(H.IoError):
+        H.Model.parse(text)
+
+
+def test_model_outside_gpu_family():
+    m = H.Model.parse('{"name":"p","input":[1,8,8],"n_slots":64,"layers":['
+                      '{"kind":"conv","k":3,"out_channels":2},{"kind":"square"},'
+                      '{"kind":"avgpool","k":2,"s":2},{"kind":"dense","units":3}]}')
+    with pytest.raises(H.ShapeError):
+        m.net_spec()
+
+
+def test_load_resolves_model_dir(tmp_path, monkeypatch):
+    (tmp_path / "cfg0.json").write_text(CFG0_JSON)
+    monkeypatch.setenv("HECNN_MODEL_DIR", str(tmp_path))
+    m = H.Model.load("cfg0")
+    assert [l["out"] for l in m.layers if l["kind"] == "dense"] == [100, 10]
+    assert m.layers[0]["policy"] == "convpack" and m.layers[5]["policy"] is None
+    with pytest.raises(H.IoError):
+        H.Model.load("no-such-model")
+
+
+def flat_weights(w):
+    parts = [np.ravel(w["conv_w"]), np.ravel(w["conv_b"])]
+    for W, b in w["dense"]:
+        parts += [np.ravel(W), np.ravel(b)]
+    return np.concatenate(parts)
+
+
+def test_weights_and_input_round_trip(tmp_path):
+    m = H.Model.parse(CFG0_JSON)
+    w = flat_weights(net_weights(CFG0, 11))
+    assert w.size == m.weight_floats
+    m.save_weights(tmp_path / "w.bin", w)
+    back = m.load_weights(tmp_path / "w.bin")
+    assert np.array_equal(back, w.astype(np.float32).astype(np.float64))  # float32 serialisation
+    x = np.random.default_rng(11).uniform(0, 1, (1, 29, 29))
+    m.save_input(tmp_path / "i.bin", x)
+    assert np.array_equal(m.load_input(tmp_path / "i.bin"), x.astype(np.float32).astype(np.float64))
+    (tmp_path / "t.bin").write_bytes(b"xy")                 # truncated
+    with pytest.raises(H.IoError):
+        m.load_weights(tmp_path / "t.bin")
+    (tmp_path / "x.bin").write_bytes((tmp_path / "i.bin").read_bytes() + b"\0")  # trailing bytes
+    with pytest.raises(H.IoError):
+        m.load_input(tmp_path / "x.bin")
+    with pytest.raises(H.IoError):
+        m.load_weights(tmp_path / "missing.bin")
