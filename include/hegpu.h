@@ -285,9 +285,17 @@ int hegpu_model_load_weights(hegpu_model* model, const char* path, double* out, 
 int hegpu_model_save_weights(hegpu_model* model, const char* path, const double* w, size_t count);
 int hegpu_model_load_input(hegpu_model* model, const char* path, double* out);   /* load_input */
 int hegpu_model_save_input(hegpu_model* model, const char* path, const double* x);
-/* the net spec of a model in the GPU path's family conv, square, [flatten],
- * dense, (square, dense)*; HEGPU_ERR_SHAPE otherwise */
+/* lower() for model files (proj/src/netcompile.cpp:106-278): a first
+ * conv-pack conv, then Square stages alternating with maximal linear runs
+ * (conv / avgpool / flatten / dense), each run's affine map composed on the
+ * host (conv_to_matrix, pool_to_matrix, dense; FP64) into one HS layer
+ * labelled by its joined layer labels.  HEGPU_ERR_SHAPE outside this family
+ * (SubConv groups, RepackConv, LoLa policies).  _net_spec gives the shapes;
+ * _compose the composed M (rows x cols, row-major; may be NULL to query the
+ * size) and bias b of linear stage `stage` from a flat weights stream. */
 int hegpu_model_net_spec(const hegpu_model* model, hegpu_net_spec* spec);
+int hegpu_model_compose(hegpu_model* model, const double* weights, size_t count, int stage, double* M, double* b,
+                        int* rows, int* cols);
 int hegpu_net_create_from_model(hegpu_ctx* ctx, hegpu_model* model, const char* weights_path, hegpu_net** out);
 /* logits: decrypt + decode output ct (wire) into m_last values */
 int hegpu_net_decrypt_logits(hegpu_net* net, const uint64_t* out_ct, double* logits);

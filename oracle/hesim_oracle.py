@@ -347,6 +347,20 @@ def conv_bias_vector(shape, bias):
     return np.repeat(np.asarray(bias, dtype=np.float64), w)
 
 
+def pool_to_matrix(c, d_in, k, stride):
+    """proj/src/convlower.cpp:115-139 (dense form)"""
+    d_out = (d_in - k) // stride + 1
+    A = np.zeros((d_out * d_out * c, d_in * d_in * c))
+    for ci in range(c):
+        for oy in range(d_out):
+            for ox in range(d_out):
+                r = (ci * d_out + oy) * d_out + ox
+                for ky in range(k):
+                    for kx in range(k):
+                        A[r, (ci * d_in + oy * stride + ky) * d_in + ox * stride + kx] += 1.0 / (k * k)
+    return A
+
+
 def square_layer(v, ctx):
     """proj/src/convlower.cpp:141-143"""
     return mul(v, v, ctx)
@@ -387,6 +401,21 @@ def ref_conv(x, weights, bias, stride):
                         for kx in range(k):
                             acc += weights[co, ci, ky, kx] * x[ci, oy * stride + ky, ox * stride + kx]
                 out[co, oy, ox] = acc
+    return out
+
+
+def ref_avgpool(x, k, stride):
+    """proj/src/refmodel.cpp:48-66"""
+    x = np.asarray(x, dtype=np.float64)
+    c, d = x.shape[0], x.shape[1]
+    if k > d:
+        raise ShapeError("window larger than input")
+    d_out = (d - k) // stride + 1
+    out = np.zeros((c, d_out, d_out))
+    for oy in range(d_out):
+        for ox in range(d_out):
+            out[:, oy, ox] = x[:, oy * stride:oy * stride + k, ox * stride:ox * stride + k].sum(axis=(1, 2)) * (
+                1.0 / (k * k))
     return out
 
 
@@ -462,6 +491,74 @@ def ref_forward(spec, weights, image):
             flat = ref_square(flat)
         flat = ref_dense(flat, W, b)
     return flat
+
+
+# ------------------------------------------ model files (layer lists) ---
+def split_weights(layers, in_c, in_d, flat):
+    """the float32 weights stream of proj/src/modelio.cpp:169-202 -> per-layer
+    (W, b); layers: dicts with kind, k, s, out"""
+    out, o, c, d = [], 0, in_c, in_d
+    for l in layers:
+        if l["kind"] == "conv":
+            n = l["out"] * c * l["k"] ** 2
+            out.append((flat[o:o + n].reshape(l["out"], c, l["k"], l["k"]), flat[o + n:o + n + l["out"]]))
+            o += n + l["out"]
+            c, d = l["out"], (d - l["k"]) // l["s"] + 1
+        elif l["kind"] == "dense":
+            n = l["out"] * c * d * d
+            out.append((flat[o:o + n].reshape(l["out"], c * d * d), flat[o + n:o + n + l["out"]]))
+            o += n + l["out"]
+            c, d = l["out"], 1
+        else:
+            out.append(None)
+            if l["kind"] == "avgpool":
+                d = (d - l["k"]) // l["s"] + 1
+    assert o == len(flat)
+    return out
+
+
+def compose_run(layers, weights, c, d):
+    """proj/src/netcompile.cpp:225-278 (dense): the affine map (M, b) of one
+    linear run of conv / avgpool / flatten / dense layers on a (c, d, d) input"""
+    M, b = None, None
+
+    def fold(A, bias):
+        nonlocal M, b
+        if M is None:
+            M, b = A, bias
+        else:
+            M, b = A @ M, A @ b + bias
+
+    for l, w in zip(layers, weights):
+        if l["kind"] == "conv":
+            shape = ConvShape(d, c, l["k"], l["s"], l["out"])
+            fold(conv_to_matrix(shape, w[0]), conv_bias_vector(shape, w[1]))
+            c, d = l["out"], shape.d_out()
+        elif l["kind"] == "avgpool":
+            d_out = (d - l["k"]) // l["s"] + 1
+            fold(pool_to_matrix(c, d, l["k"], l["s"]), np.zeros(c * d_out * d_out))
+            d = d_out
+        elif l["kind"] == "dense":
+            fold(np.asarray(w[0], dtype=np.float64), np.asarray(w[1], dtype=np.float64))
+            c, d = l["out"], 1
+    return M, b
+
+
+def ref_forward_layers(layers, weights, image):
+    """proj/src/netcompile.cpp:448-503 over a general layer list"""
+    t = np.asarray(image, dtype=np.float64)
+    for l, w in zip(layers, weights):
+        if l["kind"] == "conv":
+            t = ref_conv(t, w[0], w[1], l["s"])
+        elif l["kind"] == "avgpool":
+            t = ref_avgpool(t, l["k"], l["s"])
+        elif l["kind"] == "square":
+            t = ref_square(t)
+        elif l["kind"] == "flatten":
+            t = t.ravel()
+        elif l["kind"] == "dense":
+            t = ref_dense(np.ravel(t), w[0], w[1])
+    return np.ravel(t)
 
 
 def golden_stage_tallies(spec):

@@ -22,6 +22,7 @@
 
 #include "core.hpp"
 #include "hegpu.h"
+#include "lower.hpp"
 
 using namespace hegpu;
 
@@ -155,12 +156,6 @@ struct JParser {
   }
 };
 
-// -------------------------------------------------------------- the model
-struct Layer {
-  int kind = 0, k = 0, s = 1, out = 0, groups = 1, policy = -1;
-  std::string label;
-};
-
 [[noreturn]] void io(const std::string& msg) { fail(HEGPU_ERR_IO, msg); }
 
 void reject_unknown(const JVal& o, std::initializer_list<const char*> allowed, const std::string& where) {
@@ -220,45 +215,8 @@ bool exists(const std::string& p) {
 
 }  // namespace
 
-struct hegpu_model {
-  std::string name;
-  int in_c = 0, in_d = 0, n_slots = 0;
-  std::vector<Layer> layers;
+struct hegpu_model : ModelDesc {
   std::string last_error;
-
-  // (channels, side) entering layer idx (proj/src/modelio.cpp shape walk)
-  std::pair<int, int> shape_before(size_t idx) const {
-    int c = in_c, d = in_d;
-    for (size_t i = 0; i < idx; ++i) {
-      const Layer& l = layers[i];
-      if (l.kind == HEGPU_LAYER_CONV || l.kind == HEGPU_LAYER_SUBCONV) {
-        c = l.out;
-        d = (d - l.k) / l.s + 1;
-      } else if (l.kind == HEGPU_LAYER_AVGPOOL) {
-        d = (d - l.k) / l.s + 1;
-      } else if (l.kind == HEGPU_LAYER_DENSE) {
-        c = l.out;
-        d = 1;
-      }
-    }
-    return {c, d};
-  }
-  // float32 count of the weights stream
-  size_t weight_count() const {
-    size_t n = 0;
-    for (size_t i = 0; i < layers.size(); ++i) {
-      const Layer& l = layers[i];
-      const auto s = shape_before(i);
-      if (l.kind == HEGPU_LAYER_CONV) {
-        n += (size_t)l.out * s.first * l.k * l.k + l.out;
-      } else if (l.kind == HEGPU_LAYER_SUBCONV) {
-        n += (size_t)l.groups * ((size_t)(l.out / l.groups) * (s.first / l.groups) * l.k * l.k + l.out / l.groups);
-      } else if (l.kind == HEGPU_LAYER_DENSE) {
-        n += (size_t)l.out * s.first * s.second * s.second + l.out;
-      }
-    }
-    return n;
-  }
 };
 
 namespace {
@@ -283,7 +241,7 @@ std::unique_ptr<hegpu_model> parse_model(const std::string& text) {
   for (const JVal& jl : layers.arr) {
     if (jl.kind != JVal::Obj) io("model JSON: a layer must be an object");
     reject_unknown(jl, {"kind", "k", "s", "out_channels", "units", "groups", "policy", "label"}, "layer");
-    Layer l;
+    ModelLayer l;
     l.kind = parse_kind(as_str(at(jl, "kind"), "kind"));
     if (const JVal* v = jl.get("k")) l.k = as_int(*v, "k");
     if (const JVal* v = jl.get("s")) l.s = as_int(*v, "s");
@@ -382,7 +340,7 @@ extern "C" int hegpu_model_info(const hegpu_model* m, int* in_c, int* in_d, int*
 extern "C" int hegpu_model_layer(const hegpu_model* m, int i, int* kind, int* k, int* s, int* out, int* groups,
                                  int* policy) {
   if (!m || i < 0 || i >= (int)m->layers.size()) return HEGPU_ERR_RANGE;
-  const Layer& l = m->layers[i];
+  const ModelLayer& l = m->layers[i];
   if (kind) *kind = l.kind;
   if (k) *k = l.k;
   if (s) *s = l.s;
@@ -441,38 +399,26 @@ extern "C" int hegpu_model_save_input(hegpu_model* m, const char* path, const do
   });
 }
 
+namespace {
+
+hegpu_net_spec spec_of(const Lowered& lw) {
+  hegpu_net_spec s{};
+  s.in_c = lw.in_c;
+  s.in_d = lw.in_d;
+  s.k = lw.k;
+  s.stride = lw.stride;
+  s.c_out = lw.c_out;
+  s.n_dense = (int)lw.dense.size();
+  for (int i = 0; i < s.n_dense; ++i) s.dense_out[i] = lw.dense[i].rows;
+  return s;
+}
+
+}  // namespace
+
 extern "C" int hegpu_model_net_spec(const hegpu_model* m, hegpu_net_spec* spec) {
   if (!m || !spec) return HEGPU_ERR_ARG;
   try {
-    // the GPU path's family: conv, square, [flatten], dense, (square, dense)*
-    const auto& L = m->layers;
-    size_t i = 0;
-    auto shape_err = [&](const std::string& why) {
-      fail(HEGPU_ERR_SHAPE, "model \"" + m->name + "\" is outside the GPU path (" + why +
-                                "; AvgPool / SubConv / LoLa policies are SURVEY.md §8f next #2-#3)");
-    };
-    if (L.empty() || L[0].kind != HEGPU_LAYER_CONV) shape_err("the first layer must be a conv");
-    if (L[0].groups != 1 || (L[0].policy != -1 && L[0].policy != HEGPU_POLICY_CONVPACK))
-      shape_err("the conv must be a plain conv-pack layer");
-    hegpu_net_spec s{};
-    s.in_c = m->in_c;
-    s.in_d = m->in_d;
-    s.k = L[0].k;
-    s.stride = L[0].s;
-    s.c_out = L[0].out;
-    i = 1;
-    while (i < L.size()) {
-      if (L[i].kind != HEGPU_LAYER_SQUARE) shape_err("layer " + std::to_string(i) + " must be a square");
-      ++i;
-      if (i < L.size() && L[i].kind == HEGPU_LAYER_FLATTEN) ++i;
-      if (i >= L.size() || L[i].kind != HEGPU_LAYER_DENSE) shape_err("a square must be followed by a dense layer");
-      if (L[i].policy != -1 && L[i].policy != HEGPU_POLICY_HS) shape_err("dense layers use the HS policy");
-      if (s.n_dense >= 4) shape_err("at most 4 dense layers");
-      s.dense_out[s.n_dense++] = L[i].out;
-      ++i;
-    }
-    if (s.n_dense == 0) shape_err("no dense layer");
-    *spec = s;
+    *spec = spec_of(lower_model(*m, nullptr, 0));
     return HEGPU_OK;
   } catch (const Error& e) {
     g_model_error = e.what();
@@ -480,34 +426,39 @@ extern "C" int hegpu_model_net_spec(const hegpu_model* m, hegpu_net_spec* spec) 
   }
 }
 
+extern "C" int hegpu_model_compose(hegpu_model* m, const double* weights, size_t count, int stage, double* M,
+                                   double* b, int* rows, int* cols) {
+  if (!m || !weights) return HEGPU_ERR_ARG;
+  return guarded_model(m, [&] {
+    const Lowered lw = lower_model(*m, weights, count);
+    if (stage < 0 || stage >= (int)lw.dense.size()) fail(HEGPU_ERR_RANGE, "model_compose: no such linear stage");
+    const LoweredDense& d = lw.dense[stage];
+    if (rows) *rows = d.rows;
+    if (cols) *cols = d.cols;
+    if (M) std::copy(d.M.begin(), d.M.end(), M);
+    if (b) std::copy(d.b.begin(), d.b.end(), b);
+  });
+}
+
 extern "C" int hegpu_net_create_from_model(hegpu_ctx* ctx, hegpu_model* m, const char* weights_path,
                                            hegpu_net** out) {
   if (!ctx || !m || !weights_path || !out) return HEGPU_ERR_ARG;
-  hegpu_net_spec s{};
-  int rc = hegpu_model_net_spec(m, &s);
-  if (rc) {
-    m->last_error = g_model_error;
-    return rc;
-  }
   std::vector<double> w(m->weight_count());
-  rc = hegpu_model_load_weights(m, weights_path, w.data(), w.size());
+  int rc = hegpu_model_load_weights(m, weights_path, w.data(), w.size());
   if (rc) return rc;
-  // split the layer-ordered stream: conv bank + bias, then each dense W, b
-  const double* p = w.data();
-  const size_t conv_n = (size_t)s.c_out * s.in_c * s.k * s.k;
-  const double* conv_w = p;
-  const double* conv_b = p + conv_n;
-  p += conv_n + s.c_out;
+  Lowered lw;
+  rc = guarded_model(m, [&] { lw = lower_model(*m, w.data(), w.size()); });
+  if (rc) return rc;
+  const hegpu_net_spec s = spec_of(lw);
   const double* dw[4] = {nullptr, nullptr, nullptr, nullptr};
   const double* db[4] = {nullptr, nullptr, nullptr, nullptr};
-  const int d_out = (s.in_d - s.k) / s.stride + 1;
-  size_t n = (size_t)s.c_out * d_out * d_out;
+  std::vector<std::string> labels;
   for (int i = 0; i < s.n_dense; ++i) {
-    dw[i] = p;
-    p += (size_t)s.dense_out[i] * n;
-    db[i] = p;
-    p += s.dense_out[i];
-    n = s.dense_out[i];
+    dw[i] = lw.dense[i].M.data();
+    db[i] = lw.dense[i].b.data();
+    labels.push_back(lw.dense[i].label);
   }
-  return hegpu_net_create(ctx, &s, conv_w, conv_b, dw, db, out);
+  rc = hegpu_net_create(ctx, &s, lw.conv_w.data(), lw.conv_b.data(), dw, db, out);
+  if (rc == HEGPU_OK) net_set_labels(*out, lw.conv_label, labels);
+  return rc;
 }

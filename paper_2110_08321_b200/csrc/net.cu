@@ -17,6 +17,7 @@
 
 #include "handles.hpp"
 #include "layers.hpp"
+#include "lower.hpp"
 
 using namespace hegpu;
 
@@ -30,6 +31,10 @@ struct hegpu_net {
   std::vector<HsPlan> plans;
   std::vector<u64d*> bias;   // per dense layer, [level][N] Montgomery
   std::vector<double> bias_scale;
+  // meter stage labels (execute's labels: ConvPack, Flat<i>, Square<i>, and
+  // the linear runs' joined layer labels for nets built from model files)
+  std::string conv_label = "Conv1";
+  std::vector<std::string> dense_labels;
   // host-input pipeline (hegpu_net_run_host_compact): double-buffered
   // compact staging, a copy stream and its events
   uint8_t* stage[2] = {nullptr, nullptr};
@@ -107,7 +112,7 @@ struct Scratch {
 void conv_meter(hegpu_net& net, int B) {
   Context& c = *net.c;
   const hegpu_net_spec& s = net.spec;
-  c.meter.begin("Conv1");
+  c.meter.begin(net.conv_label);
   c.meter.bump(HEGPU_MUL_PC, (int64_t)B * net.ntaps * s.c_out);
   c.meter.bump(HEGPU_ADD_CC, (int64_t)B * (net.ntaps - 1) * s.c_out);
   c.meter.bump(HEGPU_ADD_PC, (int64_t)B * s.c_out);
@@ -151,7 +156,7 @@ void run_after_conv(hegpu_net& net, const CtBatch& mb, CtBatch& out) {
     c.meter.bump(HEGPU_MUL_CC, B);
     --l;
     // Dense<i>: Linear / HS (netcompile.cpp:380-434)
-    c.meter.begin("Dense" + std::to_string(i + 1));
+    c.meter.begin(i < (int)net.dense_labels.size() ? net.dense_labels[i] : "Dense" + std::to_string(i + 1));
     HsPlan& pl = net.plans[i];
     const bool last = i + 1 == s.n_dense;
     CtBatch z{&c, B, l - 1, 0, last ? out.d : cur.p};
@@ -188,6 +193,13 @@ void run_after_conv(hegpu_net& net, const CtBatch& mb, CtBatch& out) {
 }
 
 }  // namespace
+
+namespace hegpu {
+void net_set_labels(hegpu_net* net, const std::string& conv, const std::vector<std::string>& dense) {
+  net->conv_label = conv;
+  net->dense_labels = dense;
+}
+}  // namespace hegpu
 
 extern "C" int hegpu_net_create(hegpu_ctx* h, const hegpu_net_spec* spec, const double* conv_w,
                                 const double* conv_b, const double* const* dense_w, const double* const* dense_b,

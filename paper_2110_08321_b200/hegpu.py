@@ -148,6 +148,7 @@ def lib():
             "hegpu_model_load_input": (i, [vp, C.c_char_p, f64p]),
             "hegpu_model_save_input": (i, [vp, C.c_char_p, f64p]),
             "hegpu_model_net_spec": (i, [vp, C.POINTER(NetSpec)]),
+            "hegpu_model_compose": (i, [vp, f64p, C.c_size_t, i, vp, vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
             "hegpu_net_create_from_model": (i, [vp, vp, C.c_char_p, pp]),
             "hegpu_net_run_split": (i, [vp, vp, vp, i, i, i, REDUCE_FN, vp]),
             "hegpu_net_run_host": (i, [vp, vp, i, vp]),
@@ -624,6 +625,16 @@ class Model:
     def save_input(self, path, x):
         x = np.ascontiguousarray(x, dtype=np.float64).ravel()
         self._check(lib().hegpu_model_save_input(self.h, str(path).encode(), x))
+
+    def compose(self, weights, stage):
+        """lower()'s composed affine map (M, b) of linear stage `stage`"""
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        r, c = C.c_int(), C.c_int()
+        self._check(lib().hegpu_model_compose(self.h, w, w.size, stage, None, None, C.byref(r), C.byref(c)))
+        M = np.empty((r.value, c.value))
+        b = np.empty(r.value)
+        self._check(lib().hegpu_model_compose(self.h, w, w.size, stage, M.ctypes.data, b.ctypes.data, None, None))
+        return M, b
 
     def net_spec(self):
         spec = NetSpec()

@@ -418,6 +418,30 @@ def test_cfg0_net_from_model_files(cfg0, tmp_path):
     assert np.abs(net2.decrypt_logits(o2.download()) - HS.ref_forward(spec, w, img)).max() < 1e-3
 
 
+def test_cryptonets_model_lowered_on_gpu(tmp_path):
+    """the reference's builtin cryptonets-hs layer list (conv, square,
+    avgpool, conv, avgpool, flatten, dense, square, dense) from a model file:
+    lower() fuses the linear run into one HS layer; decrypted logits match
+    the FP64 forward pass of the layer list; stage labels follow lower()"""
+    from test_modelio import cryptonets_weights
+    m, w = cryptonets_weights(7)
+    m.save_weights(tmp_path / "w.bin", w)
+    ctx = H.Context(13, [60, 40, 40, 40, 40, 40], 60, seed=77)
+    net = H.Net.from_model(ctx, m, tmp_path / "w.bin")
+    per_layer = HS.split_weights(m.layers, m.in_c, m.in_d, w)
+    rng = np.random.default_rng(3)
+    for s in range(2):
+        img = np.zeros((1, 29, 29))
+        img[0, :28, :28] = rng.uniform(0, 1, (28, 28)).astype(np.float32)
+        out = ctx.ct(1, net.out_level)
+        ctx.reset_meter()
+        net.run(ctx.ct(net.ntaps, net.top, net.encrypt_image(img, nonce=s), DELTA), out)
+        logits = net.decrypt_logits(out.download())
+        want = HS.ref_forward_layers(m.layers, per_layer, img)
+        assert np.abs(logits - want).max() < 1e-3
+    assert [k for k, _ in ctx.stages()] == ["Conv1", "Flat1", "Square1", "Conv2-Dense1", "Square2", "Dense2"]
+
+
 def test_cfg3_net_logits_and_hops():
     """Config 3 (CIFAR-shaped, N=16384): conv 5x5/2 3->32 (75 taps), merge 32
     maps (6272 slots), HS 6272->256, HS 256->10; logits vs ref_forward and

@@ -5,6 +5,7 @@ proj/tests/test_netcompile.cpp "model json round trip and validation" and
 import numpy as np
 import pytest
 
+from oracle import hesim_oracle as HS
 from paper_2110_08321_b200 import hegpu as H
 from paper_2110_08321_b200.workloads import CFG0, net_weights
 
@@ -53,12 +54,17 @@ def test_model_validation_rejects(text):
         H.Model.parse(text)
 
 
-def test_model_outside_gpu_family():
+def test_pool_inside_a_linear_run_is_lowered():
     m = H.Model.parse('{"name":"p","input":[1,8,8],"n_slots":64,"layers":['
                       '{"kind":"conv","k":3,"out_channels":2},{"kind":"square"},'
                       '{"kind":"avgpool","k":2,"s":2},{"kind":"dense","units":3}]}')
+    spec = m.net_spec()   # conv -> square -> [avgpool, dense] fused into one HS layer
+    assert (spec.n_dense, spec.dense_out[0]) == (1, 3)
+    # a square must follow the conv
+    bad = H.Model.parse('{"name":"q","input":[1,8,8],"n_slots":64,"layers":['
+                        '{"kind":"conv","k":3,"out_channels":2},{"kind":"dense","units":3}]}')
     with pytest.raises(H.ShapeError):
-        m.net_spec()
+        bad.net_spec()
 
 
 def test_load_resolves_model_dir(tmp_path, monkeypatch):
@@ -96,3 +102,56 @@ def test_weights_and_input_round_trip(tmp_path):
         m.load_input(tmp_path / "x.bin")
     with pytest.raises(H.IoError):
         m.load_weights(tmp_path / "missing.bin")
+
+
+# the reference's builtin cryptonets-hs layer list (netcompile.cpp:567-585) as
+# a model file, with slot count sized for the N = 8192 ring
+CRYPTONETS_JSON = """{"name": "cryptonets-hs", "input": [1, 29, 29], "n_slots": 4096, "layers": [
+  {"kind": "conv", "k": 5, "s": 2, "out_channels": 5, "label": "Conv1"},
+  {"kind": "square"},
+  {"kind": "avgpool", "k": 2, "s": 2},
+  {"kind": "conv", "k": 5, "s": 1, "out_channels": 50, "label": "Conv2"},
+  {"kind": "avgpool", "k": 2, "s": 2},
+  {"kind": "flatten"},
+  {"kind": "dense", "units": 100, "label": "Dense1"},
+  {"kind": "square"},
+  {"kind": "dense", "units": 10, "label": "Dense2"}]}"""
+
+
+def cryptonets_weights(seed=5):
+    m = H.Model.parse(CRYPTONETS_JSON)
+    rng = np.random.default_rng(seed)
+    return m, rng.normal(0, 0.05, m.weight_floats).astype(np.float32).astype(np.float64)
+
+
+def test_lower_composes_linear_runs():
+    """lower(): the avgpool-conv-avgpool-flatten-dense run is one affine map,
+    equal to the oracle's compose_run (netcompile.cpp:225-278)"""
+    m, w = cryptonets_weights()
+    spec = m.net_spec()
+    assert (spec.c_out, spec.n_dense, spec.dense_out[0], spec.dense_out[1]) == (5, 2, 100, 10)
+    per_layer = HS.split_weights(m.layers, m.in_c, m.in_d, w)
+    M, b = m.compose(w, 0)
+    Mo, bo = HS.compose_run(m.layers[2:7], per_layer[2:7], 5, 13)
+    assert M.shape == (100, 845)
+    assert np.abs(M - Mo).max() < 1e-12 and np.abs(b - bo).max() < 1e-12
+    M2, b2 = m.compose(w, 1)
+    assert np.array_equal(M2, per_layer[8][0]) and np.array_equal(b2, per_layer[8][1])
+    # the lowered net computes the reference forward pass in cleartext
+    x = np.random.default_rng(1).uniform(0, 1, (1, 29, 29))
+    t = HS.ref_square(HS.ref_conv(x, *per_layer[0], 2)).ravel()
+    y = M2 @ HS.ref_square(M @ t + b) + b2
+    assert np.abs(y - HS.ref_forward_layers(m.layers, per_layer, x)).max() < 1e-10
+
+
+def test_lower_rejects_outside_family():
+    sub = H.Model.parse('{"name":"g","input":[2,8,8],"n_slots":64,"layers":['
+                        '{"kind":"conv","k":3,"out_channels":4},{"kind":"square"},'
+                        '{"kind":"subconv","k":3,"out_channels":4,"groups":2},{"kind":"dense","units":3}]}')
+    with pytest.raises(H.ShapeError):
+        sub.net_spec()
+    lola = H.Model.parse('{"name":"l","input":[1,8,8],"n_slots":64,"layers":['
+                         '{"kind":"conv","k":3,"out_channels":2},{"kind":"square"},'
+                         '{"kind":"dense","units":3,"policy":"lola-dense"}]}')
+    with pytest.raises(H.ShapeError):
+        lola.net_spec()
