@@ -64,9 +64,27 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    build_cli(force)
     if verbose:
         print(LIB)
     return LIB
+
+
+CLI_SRC = os.path.join(ROOT, "tools", "hegpu_cli.cpp")
+CLI = os.path.join(HERE, "hegpu_cli")
+
+
+def build_cli(force: bool = False) -> str:
+    """the hesim-style command-line front end (tools/hegpu_cli.cpp) over libhegpu.so"""
+    if (not force and os.path.exists(CLI)
+            and os.path.getmtime(CLI) >= max(os.path.getmtime(CLI_SRC), os.path.getmtime(LIB))):
+        return CLI
+    cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), CLI_SRC, "-o", CLI, "-L", HERE,
+           "-lhegpu", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"hegpu_cli build failed:\n{r.stdout}\n{r.stderr}")
+    return CLI
 
 
 if __name__ == "__main__":

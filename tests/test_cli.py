@@ -1,0 +1,69 @@
+"""hegpu_cli: the reference CLI's commands, exit
+codes (0 ok, 1 I/O, 2 capacity/shape, 3 verification) and CSV formats
+(proj/tools/hesim.cpp) over the encrypted path."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import hesim_oracle as HS
+from paper_2110_08321_b200 import build as B
+from paper_2110_08321_b200 import hegpu as H
+
+CLI = B.CLI
+
+
+def cli(*args, **kw):
+    return subprocess.run([CLI, *args], capture_output=True, text=True, timeout=kw.get("timeout", 600))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    B.build()
+
+
+def test_sweep_matches_predict_hs():
+    r = cli("sweep", "--n-min", "16", "--n-max", "1024", "--m-min", "4", "--m-max", "256", "--n-slots", "4096,16384")
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.strip().splitlines()
+    assert lines[0] == "method,n,m,N,rotations,multiplications"
+    rows = [l.split(",") for l in lines[1:]]
+    assert len(rows) == 7 * 7 * 2
+    for method, n, m, N, rot, mul in rows:
+        assert method == "hs"
+        want = HS.predict_hs(int(m), int(n), int(N))
+        assert (int(rot), int(mul)) == (want[0], want[1])
+
+
+def test_exit_codes_without_gpu():
+    assert cli("run", "--model", "/no/such/model.json").returncode == 1   # IoError
+    assert cli("count", "--model", "ce").returncode == 2                  # SubConv: outside the path
+    assert cli("frobnicate").returncode == 2
+    assert cli("sweep", "--methods", "lola-dense").returncode == 2
+
+
+@pytest.mark.gpu
+def test_run_count_verify_on_gpu(tmp_path):
+    from test_modelio import CRYPTONETS_JSON, cryptonets_weights
+    (tmp_path / "m.json").write_text(CRYPTONETS_JSON)
+    m, w = cryptonets_weights(9)
+    m.save_weights(tmp_path / "w.bin", w)
+    x = np.random.default_rng(9).uniform(0, 1, (1, 29, 29))
+    m.save_input(tmp_path / "x.bin", x)
+    r = cli("run", "--model", str(tmp_path / "m.json"), "--weights", str(tmp_path / "w.bin"),
+            "--input", str(tmp_path / "x.bin"), "--report", str(tmp_path / "r.csv"))
+    assert r.returncode == 0, r.stderr
+    logits = np.array([float(l.split(",")[2]) for l in r.stdout.splitlines() if l.startswith("logit,")])
+    want = HS.ref_forward_layers(m.layers, HS.split_weights(m.layers, 1, 29, w), m.load_input(tmp_path / "x.bin"))
+    assert np.abs(logits - want).max() < 1e-3
+    rep = (tmp_path / "r.csv").read_text().splitlines()
+    assert rep[0] == "layer,total,add_pc,add_cc,mul_pc,mul_cc,rot"
+    assert [l.split(",")[0] for l in rep[1:]] == ["Conv1", "Flat1", "Square1", "Conv2-Dense1", "Square2", "Dense2",
+                                                  "Total"]
+    c = cli("count", "--model", "cryptonets-hs", "--seed", "3")
+    assert c.returncode == 0, c.stderr
+    assert "Conv2-Dense1" in c.stdout and c.stdout.strip().splitlines()[-1].startswith("Total")
+    v = cli("verify", "--cases", "3", timeout=1200)
+    assert v.returncode == 0, v.stdout + v.stderr
+    assert "verify: PASS" in v.stdout
