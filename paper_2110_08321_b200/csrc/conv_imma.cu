@@ -1,0 +1,184 @@
+// conv_imma.cu -- the conv-pack multiply-accumulate on the int8 tensor cores.
+//
+// out[co][k] = sum_s W[co][s] * tap_s[k] mod q (per image, poly, limb) is a
+// GEMM: the weights are shared by every slot position.  It runs exactly on
+// IMMA.16832 (mma.sync m16n8k32 u8 x u8 -> s32, measured 1.1 POPS on this
+// B200, tools/ubench_mma.cu) through a byte decomposition:
+//   tap x = sum_i x_i 2^(8i)             (x_i = byte i, i < 8: the B operand
+//                                         is just the two 32-bit halves of x)
+//   w_{co,s,i} = W[co][s] 2^(8i) R mod q (precomputed per limb; R = 2^64
+//                                         Montgomery form, so the single
+//                                         reduction below lands in standard form)
+//   w_{co,s,i} = sum_e w_e 2^(8e)        (e < 8: the A operand)
+//   T_e[co][k] = sum_{s,i} w_e[co,s,i] x_i[s][k]        <- the GEMM, K = 8 ntaps
+//   out = (sum_e T_e 2^(8e) + bias R) R^-1 mod q   (T_e < 2^29: < 2^86
+//                                         total, one Montgomery reduction)
+// so the result is the same residue as the IMAD path, bit for bit.
+// Tile: a warp owns 4 x 8 slot positions (n8 tiles) and 4 output-map pairs
+// (m16 = 2 maps x 8 byte planes e) with k32 = 4 taps x 8 bytes per step.
+#include <cstdint>
+
+#include "engine.hpp"
+
+namespace hegpu {
+
+namespace {
+
+constexpr int kImmaWarps = 8;                   // warps per CTA
+constexpr int kImmaNT = 4;                      // n8 position tiles per warp (A fragment reuse)
+constexpr int kImmaCPG = 4;                     // map pairs per warp pass (B fragment reuse)
+constexpr int kImmaPos = 8 * kImmaNT * kImmaWarps;  // slot positions per CTA
+constexpr int kImmaDepth = 3;                   // cp.async pipeline stages (k32 steps; 48 KB static smem)
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void mma_u8(int (&c)[4], const uint4& a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+
+// a warp: kImmaNT tiles of 8 positions x kImmaCPG map pairs; per k32 step
+// the B fragments of the NT tiles are loaded once and reused by CPG map
+// pairs, each A fragment by NT tiles
+__global__ void __launch_bounds__(32 * kImmaWarps) k_conv_imma(PrimeTable pt, const u64d* __restrict__ taps,
+                                                              int ntaps, int l, int N,
+                                                              const uint4* __restrict__ wa, int cps, int kbn,
+                                                              int c_out, const u64d* __restrict__ bias,
+                                                              u64d* __restrict__ out) {
+  __shared__ int scratch[kImmaWarps][2][16][9];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.y % l, poly = blockIdx.y / l;
+  // the map-pair group varies fastest, so the CTAs reading the same taps
+  // run together and the taps come from L2 after the first group
+  const int groups = (cps + kImmaCPG - 1) / kImmaCPG;
+  const int b = blockIdx.z, cp0 = (blockIdx.x % groups) * kImmaCPG;
+  const int kw = (blockIdx.x / groups) * kImmaPos + warp * 8 * kImmaNT;  // first position of the warp
+  const size_t ct_words = (size_t)2 * l * N;
+  // B operand source: the half (lane & 1) of tap word x[s][kw + 8 nt + lane/4]
+  const uint32_t* tp = reinterpret_cast<const uint32_t*>(taps + (size_t)b * ntaps * ct_words + (size_t)poly * l * N +
+                                                         (size_t)t * N + kw + (lane >> 2)) +
+                       (lane & 1);
+  const int sub = (lane & 3) >> 1;  // tap offset within the 4-tap k32 block
+  int c[kImmaCPG][kImmaNT][4];
+#pragma unroll
+  for (int j = 0; j < kImmaCPG; ++j)
+#pragma unroll
+    for (int n = 0; n < kImmaNT; ++n) c[j][n][0] = c[j][n][1] = c[j][n][2] = c[j][n][3] = 0;
+  const uint4* wt = wa + (size_t)t * cps * kbn * 32;
+  // kImmaDepth-stage cp.async pipeline: A fragments of the CTA's map pairs
+  // (shared by its warps) and each lane's own B words
+  __shared__ uint4 a_s[kImmaDepth][kImmaCPG][32];
+  __shared__ uint32_t b_s[kImmaDepth][2 * kImmaNT][32 * kImmaWarps];
+  auto issue = [&](int kb) {
+    const int st = kb % kImmaDepth;
+    if (threadIdx.x < kImmaCPG * 32) {
+      const int j = threadIdx.x >> 5;
+      if (cp0 + j < cps) cp_async16(&a_s[st][j][lane], wt + ((size_t)(cp0 + j) * kbn + kb) * 32 + lane);
+    }
+    const int s0 = 4 * kb + sub, s1 = s0 + 2;
+#pragma unroll
+    for (int n = 0; n < kImmaNT; ++n) {
+      if (s0 < ntaps) cp_async4(&b_s[st][2 * n][threadIdx.x], tp + 2 * ((size_t)s0 * ct_words + 8 * n));
+      else b_s[st][2 * n][threadIdx.x] = 0u;
+      if (s1 < ntaps) cp_async4(&b_s[st][2 * n + 1][threadIdx.x], tp + 2 * ((size_t)s1 * ct_words + 8 * n));
+      else b_s[st][2 * n + 1][threadIdx.x] = 0u;
+    }
+  };
+#pragma unroll
+  for (int d = 0; d < kImmaDepth - 1; ++d) {
+    if (d < kbn) issue(d);
+    cp_async_commit();
+  }
+  for (int kb = 0; kb < kbn; ++kb) {
+    if (kb + kImmaDepth - 1 < kbn) issue(kb + kImmaDepth - 1);
+    cp_async_commit();
+    cp_async_wait<kImmaDepth - 1>();
+    __syncthreads();  // every thread's copies of stage kb are visible
+    const int st = kb % kImmaDepth;
+    uint32_t b0[kImmaNT], b1[kImmaNT];
+#pragma unroll
+    for (int n = 0; n < kImmaNT; ++n) {
+      b0[n] = b_s[st][2 * n][threadIdx.x];
+      b1[n] = b_s[st][2 * n + 1][threadIdx.x];
+    }
+#pragma unroll
+    for (int j = 0; j < kImmaCPG; ++j) {
+      if (cp0 + j < cps) {
+        const uint4 a = a_s[st][j][lane];
+#pragma unroll
+        for (int n = 0; n < kImmaNT; ++n) mma_u8(c[j][n], a, b0[n], b1[n]);
+      }
+    }
+    __syncthreads();  // stage kb may be refilled
+  }
+  // epilogue: fragments go through shared memory two at a time; each lane
+  // combines the 8 byte planes of one (map, position) of one fragment
+  const int row = lane >> 2, col = 2 * (lane & 3);
+  const DevPrime pr = pt.p[t];
+  const int half = (lane >> 3) & 1, pc = lane & 7, fsel = lane >> 4;
+#pragma unroll
+  for (int f0 = 0; f0 < kImmaCPG * kImmaNT; f0 += 2) {
+    const int j = f0 / kImmaNT;  // fragments f0, f0 + 1 share j (NT even)
+    if (cp0 + j >= cps) break;
+    __syncwarp();
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      const int n = (f0 + f) % kImmaNT;
+      scratch[warp][f][row][col] = c[j][n][0];
+      scratch[warp][f][row][col + 1] = c[j][n][1];
+      scratch[warp][f][row + 8][col] = c[j][n][2];
+      scratch[warp][f][row + 8][col + 1] = c[j][n][3];
+    }
+    __syncwarp();
+    const int co = 2 * (cp0 + j) + half;
+    if (co < c_out) {
+      const int k = kw + 8 * ((f0 + fsel) % kImmaNT) + pc;
+      // + bias R (the stored Montgomery bias) before the reduction
+      u64d lo = (poly == 0 && bias) ? bias[((size_t)co * l + t) * N + k] : 0ull, hi = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const u64d v = (u64d)(uint32_t)scratch[warp][fsel][half * 8 + e][pc];
+        const u64d l_add = v << (8 * e), h_add = e ? v >> (64 - 8 * e) : 0ull;
+        asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(l_add), "l"(h_add));
+      }
+      // (hi:lo) < 2^87 < q 2^64: one Montgomery reduction -> standard form
+      out[((size_t)b * c_out + co) * ct_words + (size_t)poly * l * N + (size_t)t * N + k] =
+          mont_reduce128(lo, hi, pr.q, pr.qneg_inv);
+    }
+  }
+}
+
+}  // namespace
+
+bool conv_imma_supported(Context& c) { return c.N() % kImmaPos == 0; }
+
+void launch_conv_imma(Context& c, const u64d* taps, int B, int ntaps, int l, const uint32_t* wa, int cps, int kbn,
+                      int c_out, const u64d* bias, u64d* out) {
+  const int N = c.N();
+  const double bytes = 8.0 * N * l * (2.0 * B * ntaps + 2.0 * B * c_out + c_out);
+  const double ops = 2.0 * N * l * B * ntaps * c_out;  // modular MAC terms (as the IMAD path)
+  const uint4* w4 = reinterpret_cast<const uint4*>(wa);
+const int groups = (cps + kImmaCPG - 1) / kImmaCPG;
+  dim3 grid(N / kImmaPos * groups, 2 * l, B);
+  LAUNCH_BO(c, "k_conv_mac", bytes, ops,
+            k_conv_imma<<<grid, 32 * kImmaWarps, 0, c.stream>>>(c.primes, taps, ntaps, l, N, w4, cps, kbn, c_out,
+                                                                bias, out));
+}
+
+}  // namespace hegpu

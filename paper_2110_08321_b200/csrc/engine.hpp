@@ -210,6 +210,12 @@ void launch_add(Context& c, const u64d* a, const u64d* b, u64d* out, int count, 
 void launch_add_plain(Context& c, const u64d* a, const u64d* p, long p_stride, u64d* out, int count, int l);
 void launch_mul_plain(Context& c, const u64d* a, const u64d* p, long p_stride, u64d* out, int count, int l);
 void launch_tensor_square(Context& c, const u64d* a, u64d* d01, u64d* d2, int count, int l);
+// the same MAC on the int8 tensor cores (conv_imma.cu); wa: per limb, map
+// pair, 4-tap block and lane the A fragment (uint4) of the byte planes of
+// W * 2^(8i) mod q
+bool conv_imma_supported(Context& c);
+void launch_conv_imma(Context& c, const u64d* taps, int B, int ntaps, int l, const uint32_t* wa, int cps, int kbn,
+                      int c_out, const u64d* bias, u64d* out);
 void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, const u64d* wmont /*[c_out][ntaps][l]*/,
                      int c_out, const u64d* bias /*[c_out][l][N] mont*/, u64d* out);
 struct HsDiagTable {

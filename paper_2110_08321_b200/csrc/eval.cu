@@ -373,6 +373,9 @@ constexpr int kHsCW = 128;  // max r span of a chunk
 #ifndef HEGPU_HS_MINB
 #define HEGPU_HS_MINB 4
 #endif
+#ifndef HEGPU_HS_ACC
+#define HEGPU_HS_ACC AccC  // accumulator of the HS kernel (AccW: no in-loop folds)
+#endif
 #ifndef HEGPU_HS_PD1
 #define HEGPU_HS_PD1 4  // cp.async prefetch depth (diagonals) at 1 image per thread (measured 4 > 8 > 16 > 0)
 #endif
@@ -409,7 +412,7 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
   const int nrow = do_c0 ? LV + 1 : LV;  // D digits (+ c0)
   const int ln = LV * N, kp = (LV + 1) * N;
 
-  AccC a[kHsBT], c[kHsBT];
+  HEGPU_HS_ACC a[kHsBT], c[kHsBT];
 #pragma unroll
   for (int bb = 0; bb < kHsBT; ++bb) a[bb].zero(), c[bb].zero();
 

@@ -61,6 +61,48 @@ ConvLayer::ConvLayer(Context& c, int nt, int co_n, const double* weights, const 
     }
   CK(cudaMalloc((void**)&this->w, w.size() * 8));
   CK(cudaMemcpy(this->w, w.data(), w.size() * 8, cudaMemcpyHostToDevice));
+  // tensor-core operand: per limb, map pair cp, 4-tap block kb and lane, the
+  // m16n8k32 A fragment whose (row, col) = (map 2cp + row / 8, byte plane
+  // e = row % 8; tap 4kb + col / 8, tap byte i = col % 8) holds byte e of
+  // W[co][s] * 2^(8i) mod q (standard form)
+  cps = (c_out + 1) / 2;
+  kbn = (ntaps + 3) / 4;
+  {
+    std::vector<u64> ws((size_t)level * c_out * ntaps * 8);  // [li][co][s][i]
+    for (int li = 0; li < level; ++li) {
+      const u64 q = P.q(li);
+      for (int co = 0; co < c_out; ++co)
+        for (int s = 0; s < ntaps; ++s) {
+          // Montgomery form: the kernel's single reduction divides by R
+          u64 v = mul_mod(residue_of_double(std::rint(weights[(size_t)co * ntaps + s] * (double)qlast), q),
+                          P.primes[li].r_mod, q);
+          for (int i = 0; i < 8; ++i) {
+            ws[(((size_t)li * c_out + co) * ntaps + s) * 8 + i] = v;
+            v = mul_mod(v, 256 % q, q);
+          }
+        }
+    }
+    auto byte_at = [&](int li, int row, int col, int cp, int kb) -> uint32_t {
+      const int co = 2 * cp + row / 8, e = row % 8, s = 4 * kb + col / 8, i = col % 8;
+      if (co >= c_out || s >= ntaps) return 0u;
+      return (uint32_t)((ws[(((size_t)li * c_out + co) * ntaps + s) * 8 + i] >> (8 * e)) & 0xFF);
+    };
+    std::vector<uint32_t> wa_h((size_t)level * cps * kbn * 32 * 4);
+    for (int li = 0; li < level; ++li)
+      for (int cp = 0; cp < cps; ++cp)
+        for (int kb = 0; kb < kbn; ++kb)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int r = lane / 4, c0 = 4 * (lane % 4);
+            uint32_t reg[4] = {0, 0, 0, 0};
+            const int rows[4] = {r, r + 8, r, r + 8}, cols[4] = {c0, c0, 16 + c0, 16 + c0};
+            for (int q4 = 0; q4 < 4; ++q4)
+              for (int bb = 0; bb < 4; ++bb) reg[q4] |= byte_at(li, rows[q4], cols[q4] + bb, cp, kb) << (8 * bb);
+            uint32_t* dst = wa_h.data() + ((((size_t)li * cps + cp) * kbn + kb) * 32 + lane) * 4;
+            for (int q4 = 0; q4 < 4; ++q4) dst[q4] = reg[q4];
+          }
+    CK(cudaMalloc((void**)&wa, wa_h.size() * 4));
+    CK(cudaMemcpy(wa, wa_h.data(), wa_h.size() * 4, cudaMemcpyHostToDevice));
+  }
   // bias[co] on the first w_used slots (convlower.cpp:68-71), at the product scale
   const int N = P.n;
   std::vector<u64> wire((size_t)c_out * level * N);
@@ -77,11 +119,19 @@ ConvLayer::~ConvLayer() {
   cudaStreamSynchronize(ctx->stream);
   cudaFree(w);
   cudaFree(bias);
+  cudaFree(wa);
 }
+
+#ifndef HEGPU_CONV_IMMA
+#define HEGPU_CONV_IMMA 1  // conv MAC on the int8 tensor cores (conv_imma.cu)
+#endif
 
 void ConvLayer::mac(Context& c, const CtBatch& taps, CtBatch& prod) {
   const int B = taps.count / ntaps;
-  launch_conv_mac(c, taps.d, B, ntaps, level, w, c_out, bias, prod.d);
+  if (HEGPU_CONV_IMMA && conv_imma_supported(c))
+    launch_conv_imma(c, taps.d, B, ntaps, level, wa, cps, kbn, c_out, bias, prod.d);
+  else
+    launch_conv_mac(c, taps.d, B, ntaps, level, w, c_out, bias, prod.d);
   prod.scale = taps.scale * (double)c.P->q(level - 1);
 }
 
@@ -90,7 +140,10 @@ void ConvLayer::mac_compact(Context& c, const uint8_t* taps, int B, double tap_s
   // beats decoding c0 / hashing c1 inside the register-heavy MAC kernel
   u64d* full = c.alloc((size_t)B * ntaps * 2 * level * c.N());
   launch_expand_compact(c, taps, B * ntaps, level, full);
-  launch_conv_mac(c, full, B, ntaps, level, w, c_out, bias, prod.d);
+  if (HEGPU_CONV_IMMA && conv_imma_supported(c))
+    launch_conv_imma(c, full, B, ntaps, level, wa, cps, kbn, c_out, bias, prod.d);
+  else
+    launch_conv_mac(c, full, B, ntaps, level, w, c_out, bias, prod.d);
   c.free(full);
   prod.scale = tap_scale * (double)c.P->q(level - 1);
 }

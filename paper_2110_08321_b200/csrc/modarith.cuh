@@ -238,4 +238,59 @@ struct AccC {  // as Acc3; s0 + s1 2^31 + s2 2^62 kept as 32-bit halves
   }
 };
 
+// Wide-limb accumulator: each partial sum (s0, s1, s2 as in Acc3) is kept in
+// three 32-bit words and every product's carry is propagated at once
+// (mad.lo.cc / madc.hi.cc / addc), so nothing is folded inside the loop
+// (capacity 2^34 products); the 192-bit total is formed once in reduce().
+struct AccW {
+  uint32_t a[3], b[3], c[3];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) a[i] = b[i] = c[i] = 0;
+  }
+  __device__ __forceinline__ void mad(u64d xs, u64d ys) {
+    const uint32_t x0 = (uint32_t)xs, x1 = (uint32_t)(xs >> 32);
+    const uint32_t y0 = (uint32_t)ys, y1 = (uint32_t)(ys >> 32);
+    asm("mad.lo.cc.u32 %0, %9, %11, %0;\n\t"
+        "madc.hi.cc.u32 %1, %9, %11, %1;\n\t"
+        "addc.u32 %2, %2, 0;\n\t"
+        "mad.lo.cc.u32 %3, %9, %12, %3;\n\t"
+        "madc.hi.cc.u32 %4, %9, %12, %4;\n\t"
+        "addc.u32 %5, %5, 0;\n\t"
+        "mad.lo.cc.u32 %3, %10, %11, %3;\n\t"
+        "madc.hi.cc.u32 %4, %10, %11, %4;\n\t"
+        "addc.u32 %5, %5, 0;\n\t"
+        "mad.lo.cc.u32 %6, %10, %12, %6;\n\t"
+        "madc.hi.cc.u32 %7, %10, %12, %7;\n\t"
+        "addc.u32 %8, %8, 0;\n\t"
+        : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(c[0]), "+r"(c[1]),
+          "+r"(c[2])
+        : "r"(x0), "r"(x1), "r"(y0), "r"(y1));
+  }
+  __device__ __forceinline__ void fold() {}  // nothing to fold
+  // s0 + s1 2^31 + s2 2^62 (each < 2^96) -> lo:hi:top, then as Acc3::reduce
+  __device__ __forceinline__ u64d reduce(const DevPrime& pr) {
+    u64d lo = 0, hi = 0;
+    uint32_t top = 0;
+    auto add_shifted = [&](const uint32_t (&v)[3], int sh) {
+      const u64d v0 = ((u64d)v[1] << 32) | v[0], v1 = v[2];
+      const u64d l = sh ? v0 << sh : v0;
+      const u64d m = sh ? (v0 >> (64 - sh)) | (v1 << sh) : v1;
+      const uint32_t t = sh ? (uint32_t)(v1 >> (64 - sh)) : 0u;
+      asm("add.cc.u64 %0, %0, %3;\n\t"
+          "addc.cc.u64 %1, %1, %4;\n\t"
+          "addc.u32 %2, %2, %5;\n\t"
+          : "+l"(lo), "+l"(hi), "+r"(top)
+          : "l"(l), "l"(m), "r"(t));
+    };
+    add_shifted(a, 0);
+    add_shifted(b, 31);
+    add_shifted(c, 62);
+    u64d x = mont_reduce128(hi, (u64d)top, pr.q, pr.qneg_inv);
+    x = mont_mul(x, pr.r2_mod, pr.q, pr.qneg_inv);
+    const u64d y = mont_reduce128(lo, 0ull, pr.q, pr.qneg_inv);
+    return add_mod_d(x, y, pr.q);
+  }
+};
+
 }  // namespace hegpu
