@@ -28,7 +28,10 @@ constexpr int kImmaWarps = 8;                   // warps per CTA
 constexpr int kImmaNT = 4;                      // n8 position tiles per warp (A fragment reuse)
 constexpr int kImmaCPG = 4;                     // map pairs per warp pass (B fragment reuse)
 constexpr int kImmaPos = 8 * kImmaNT * kImmaWarps;  // slot positions per CTA
-constexpr int kImmaDepth = 3;                   // cp.async pipeline stages (k32 steps; 48 KB static smem)
+#ifndef HEGPU_IMMA_DEPTH
+#define HEGPU_IMMA_DEPTH 8  // measured: 3: -, 4: 3.77, 6: 3.49, 8: 3.22, 10: 3.49, 12+: 4.8 ms (cfg3 conv)
+#endif
+constexpr int kImmaDepth = HEGPU_IMMA_DEPTH;    // cp.async pipeline stages (k32 steps)
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
@@ -61,7 +64,12 @@ __global__ void __launch_bounds__(32 * kImmaWarps) k_conv_imma(PrimeTable pt, co
                                                               const uint4* __restrict__ wa, int cps, int kbn,
                                                               int c_out, const u64d* __restrict__ bias,
                                                               u64d* __restrict__ out) {
-  __shared__ int scratch[kImmaWarps][2][16][9];
+  extern __shared__ __align__(16) uint4 dyn_smem[];
+  // [kImmaDepth][kImmaCPG][32] A fragments, then [kImmaDepth][2 NT][threads] B words
+  auto a_s = reinterpret_cast<uint4 (*)[kImmaCPG][32]>(dyn_smem);
+  auto b_s = reinterpret_cast<uint32_t (*)[2 * kImmaNT][32 * kImmaWarps]>(dyn_smem + kImmaDepth * kImmaCPG * 32);
+  // epilogue transpose scratch reuses the pipeline buffers
+  auto scratch = reinterpret_cast<int (*)[2][16][9]>(dyn_smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.y % l, poly = blockIdx.y / l;
   // the map-pair group varies fastest, so the CTAs reading the same taps
@@ -83,8 +91,6 @@ __global__ void __launch_bounds__(32 * kImmaWarps) k_conv_imma(PrimeTable pt, co
   const uint4* wt = wa + (size_t)t * cps * kbn * 32;
   // kImmaDepth-stage cp.async pipeline: A fragments of the CTA's map pairs
   // (shared by its warps) and each lane's own B words
-  __shared__ uint4 a_s[kImmaDepth][kImmaCPG][32];
-  __shared__ uint32_t b_s[kImmaDepth][2 * kImmaNT][32 * kImmaWarps];
   auto issue = [&](int kb) {
     const int st = kb % kImmaDepth;
     if (threadIdx.x < kImmaCPG * 32) {
@@ -176,8 +182,14 @@ void launch_conv_imma(Context& c, const u64d* taps, int B, int ntaps, int l, con
   const uint4* w4 = reinterpret_cast<const uint4*>(wa);
 const int groups = (cps + kImmaCPG - 1) / kImmaCPG;
   dim3 grid(N / kImmaPos * groups, 2 * l, B);
+  const size_t sm = (size_t)kImmaDepth * (kImmaCPG * 32 * 16 + 2 * kImmaNT * 32 * kImmaWarps * 4);
+  static bool prepared = false;
+  if (!prepared && sm > 48 * 1024) {
+    CK(cudaFuncSetAttribute(k_conv_imma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    prepared = true;
+  }
   LAUNCH_BO(c, "k_conv_mac", bytes, ops,
-            k_conv_imma<<<grid, 32 * kImmaWarps, 0, c.stream>>>(c.primes, taps, ntaps, l, N, w4, cps, kbn, c_out,
+            k_conv_imma<<<grid, 32 * kImmaWarps, sm, c.stream>>>(c.primes, taps, ntaps, l, N, w4, cps, kbn, c_out,
                                                                 bias, out));
 }
 
