@@ -32,6 +32,7 @@ constexpr int kImmaPos = 8 * kImmaNT * kImmaWarps;  // slot positions per CTA
 #define HEGPU_IMMA_DEPTH 8  // measured: 3: -, 4: 3.77, 6: 3.49, 8: 3.22, 10: 3.49, 12+: 4.8 ms (cfg3 conv)
 #endif
 constexpr int kImmaDepth = HEGPU_IMMA_DEPTH;    // cp.async pipeline stages (k32 steps)
+constexpr int kBRow = 2 * kImmaPos + 16;        // u32 words per staged tap row (+16: bank offset)
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
@@ -65,9 +66,10 @@ __global__ void __launch_bounds__(32 * kImmaWarps) k_conv_imma(PrimeTable pt, co
                                                               int c_out, const u64d* __restrict__ bias,
                                                               u64d* __restrict__ out) {
   extern __shared__ __align__(16) uint4 dyn_smem[];
-  // [kImmaDepth][kImmaCPG][32] A fragments, then [kImmaDepth][2 NT][threads] B words
+  // [kImmaDepth][kImmaCPG][32] A fragments, then [kImmaDepth][4 taps][kBRow]
+  // tap words of the CTA's positions (rows padded: conflict-free reads)
   auto a_s = reinterpret_cast<uint4 (*)[kImmaCPG][32]>(dyn_smem);
-  auto b_s = reinterpret_cast<uint32_t (*)[2 * kImmaNT][32 * kImmaWarps]>(dyn_smem + kImmaDepth * kImmaCPG * 32);
+  auto b_s = reinterpret_cast<uint32_t (*)[4][kBRow]>(dyn_smem + kImmaDepth * kImmaCPG * 32);
   // epilogue transpose scratch reuses the pipeline buffers
   auto scratch = reinterpret_cast<int (*)[2][16][9]>(dyn_smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -76,13 +78,13 @@ __global__ void __launch_bounds__(32 * kImmaWarps) k_conv_imma(PrimeTable pt, co
   // run together and the taps come from L2 after the first group
   const int groups = (cps + kImmaCPG - 1) / kImmaCPG;
   const int b = blockIdx.z, cp0 = (blockIdx.x % groups) * kImmaCPG;
-  const int kw = (blockIdx.x / groups) * kImmaPos + warp * 8 * kImmaNT;  // first position of the warp
+  const int kc = (blockIdx.x / groups) * kImmaPos;      // first position of the CTA
+  const int kw = kc + warp * 8 * kImmaNT;               // ... of the warp
   const size_t ct_words = (size_t)2 * l * N;
-  // B operand source: the half (lane & 1) of tap word x[s][kw + 8 nt + lane/4]
-  const uint32_t* tp = reinterpret_cast<const uint32_t*>(taps + (size_t)b * ntaps * ct_words + (size_t)poly * l * N +
-                                                         (size_t)t * N + kw + (lane >> 2)) +
-                       (lane & 1);
-  const int sub = (lane & 3) >> 1;  // tap offset within the 4-tap k32 block
+  const u64d* tap0 = taps + (size_t)b * ntaps * ct_words + (size_t)poly * l * N + (size_t)t * N + kc;
+  // B operand: the half (lane & 1) of tap word x[4 kb + sub (+2)][kw + 8 nt + lane/4]
+  const int sub = (lane & 3) >> 1;
+  const int boff = sub * kBRow + 2 * (warp * 8 * kImmaNT + (lane >> 2)) + (lane & 1);
   int c[kImmaCPG][kImmaNT][4];
 #pragma unroll
   for (int j = 0; j < kImmaCPG; ++j)
@@ -97,13 +99,13 @@ __global__ void __launch_bounds__(32 * kImmaWarps) k_conv_imma(PrimeTable pt, co
       const int j = threadIdx.x >> 5;
       if (cp0 + j < cps) cp_async16(&a_s[st][j][lane], wt + ((size_t)(cp0 + j) * kbn + kb) * 32 + lane);
     }
-    const int s0 = 4 * kb + sub, s1 = s0 + 2;
+    // 4 taps x kImmaPos words in 16-byte copies, 2 per thread
 #pragma unroll
-    for (int n = 0; n < kImmaNT; ++n) {
-      if (s0 < ntaps) cp_async4(&b_s[st][2 * n][threadIdx.x], tp + 2 * ((size_t)s0 * ct_words + 8 * n));
-      else b_s[st][2 * n][threadIdx.x] = 0u;
-      if (s1 < ntaps) cp_async4(&b_s[st][2 * n + 1][threadIdx.x], tp + 2 * ((size_t)s1 * ct_words + 8 * n));
-      else b_s[st][2 * n + 1][threadIdx.x] = 0u;
+    for (int r = 0; r < 4 * kImmaPos / 2 / (32 * kImmaWarps); ++r) {
+      const int idx = threadIdx.x + r * 32 * kImmaWarps, q = idx / (kImmaPos / 2), ch = idx % (kImmaPos / 2);
+      uint32_t* dst = &b_s[st][q][4 * ch];
+      if (4 * kb + q < ntaps) cp_async16(dst, tap0 + (size_t)(4 * kb + q) * ct_words + 2 * ch);
+      else *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
     }
   };
 #pragma unroll
@@ -118,10 +120,11 @@ __global__ void __launch_bounds__(32 * kImmaWarps) k_conv_imma(PrimeTable pt, co
     __syncthreads();  // every thread's copies of stage kb are visible
     const int st = kb % kImmaDepth;
     uint32_t b0[kImmaNT], b1[kImmaNT];
+    const uint32_t* bs = &b_s[st][0][0] + boff;
 #pragma unroll
     for (int n = 0; n < kImmaNT; ++n) {
-      b0[n] = b_s[st][2 * n][threadIdx.x];
-      b1[n] = b_s[st][2 * n + 1][threadIdx.x];
+      b0[n] = bs[16 * n];
+      b1[n] = bs[2 * kBRow + 16 * n];
     }
 #pragma unroll
     for (int j = 0; j < kImmaCPG; ++j) {
@@ -182,7 +185,7 @@ void launch_conv_imma(Context& c, const u64d* taps, int B, int ntaps, int l, con
   const uint4* w4 = reinterpret_cast<const uint4*>(wa);
 const int groups = (cps + kImmaCPG - 1) / kImmaCPG;
   dim3 grid(N / kImmaPos * groups, 2 * l, B);
-  const size_t sm = (size_t)kImmaDepth * (kImmaCPG * 32 * 16 + 2 * kImmaNT * 32 * kImmaWarps * 4);
+  const size_t sm = (size_t)kImmaDepth * (kImmaCPG * 32 * 16 + 4 * kBRow * 4);
   static bool prepared = false;
   if (!prepared && sm > 48 * 1024) {
     CK(cudaFuncSetAttribute(k_conv_imma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
