@@ -32,7 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "encrypted inferences/sec + key-switched rotations/sec, % of HBM roofline"
-KERNELS = ["k_hs_diag", "k_drop_ntt", "k_ks_modup", "k_conv_mac", "k_intt_rows", "k_ks_intt", "k_ks_inner", "k_ntt_rows",
+KERNELS = ["k_hs_diag", "k_hs_imma", "k_drop_ntt", "k_ks_modup", "k_conv_mac", "k_intt_rows", "k_ks_intt", "k_ks_inner", "k_ntt_rows",
            "k_wire_to_slot", "k_add", "k_tensor_square", "k_add_plain"]
 UNIT = "inferences/s"
 SEED = 2110

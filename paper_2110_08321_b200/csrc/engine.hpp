@@ -236,6 +236,25 @@ int hs_chunk_span();
 void launch_hs_diag(Context& c, const u64d* v, int B, int l, const u64d* D, const HsDiagTable& t,
                     u64d* acc, u64d* cacc);
 void launch_fuse_key(Context& c, const u64d* key, const u64d* mask, int l, u64d* fk);
+// the same accumulation on the int8 tensor cores (hs_imma.cu): one chunk of
+// kept diagonals with r in [r_lo, r_hi], its A fragments wt ([l+1][N][ns][32]
+// uint4: byte planes of the fused keys and P * masks per position)
+struct HsImmaChunk {
+  int r_lo, r_hi, ns;
+  int keyed, ndiag;  // kept diagonals in the chunk (with a key / all)
+  u64d* wt;
+};
+int hs_imma_chunk_span(int l);
+bool hs_imma_supported(Context& c, int l);
+size_t hs_imma_tile_words(Context& c, int l, const HsImmaChunk& ch);
+// rdiag[r] = kept diagonal index of right rotation r (or -1); pmod[t] = P mod q_t
+void launch_hs_imma_tiles(Context& c, int l, const HsDiagTable& t, const u64d* pmod, const int* rdiag,
+                          const HsImmaChunk& ch, u64d* wt);
+// acc (= or += when accumulate) for one chunk; ec: [np][2][4][2] epilogue constants
+void launch_hs_imma(Context& c, const u64d* v, int B, int l, const u64d* D, const HsImmaChunk& ch,
+                    const u64d* ec, int accumulate, u64d* acc);
+// cacc of the tensor-core path: 0, or diagonal 0's c1 * m0 in part 1
+void launch_hs_cacc(Context& c, const u64d* v, const u64d* m0, int B, int l, int c1_term, u64d* cacc);
 // re-pack Montgomery multiplier words x -> (x mod 2^31) | (x >> 31) << 32
 void launch_split31(Context& c, u64d* p, size_t words);
 // x -> x mod q(limb) for rows of nl limbs (limb p_limb is the special prime P);

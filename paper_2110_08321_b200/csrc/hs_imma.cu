@@ -1,0 +1,412 @@
+// hs_imma.cu -- the Halevi-Shoup diagonal accumulation on the int8 tensor
+// cores.
+//
+// Per output position k (slot order, inside one half), ext limb t, image b
+// and key part p the hoisted HS layer accumulates
+//   acc[b][p][t][k] = sum_{r kept} ( sum_{j<l} D_j[b][t][k - r] fk_{r,j,p}[t][k]
+//                                    + [p == 0] c0[b][t][k - r] P m_r[t][k] )
+// (the c0 * mask term is folded into the extended-basis accumulator as
+// P * c0 * m: the ModDown divides it back out exactly, so the result is the
+// same residue as ModDown(acc) + c0 * m).  Indexing the sum by the window
+// position pos = k - r instead of r turns it into a BANDED GEMM over
+// kappa = pos * J + j (J = l + 1 "digits": the l ModUp digits and c0):
+//   A[(k, p, e)][kappa] = byte e of the weight (fk or P m) -- per position,
+//                         precomputed once per plan in mma fragment order
+//   B[kappa][(b, d)]    = byte d of the window element x_kappa of image b
+//   C[(k,p,e)][(b,d)]   = sum_kappa A B   (exact: < 2^32 for kappa < 66k)
+//   value(k, b, p)      = sum_{e,d} C 2^(8(e+d)) = sum_kappa w x  (exact)
+// on mma.sync m16n8k32 u8 (rows = (p, e) of one position, columns = the 8
+// byte planes of one image).  Consecutive positions share the B fragments
+// (the window slides by J bytes per position), so a warp owns 4 positions x
+// 4 images and a CTA streams a strip of 16-position blocks through a ring
+// buffer of window bytes (each element staged once per strip).
+#include <cstdint>
+#include <vector>
+
+#include "engine.hpp"
+
+namespace hegpu {
+
+namespace {
+
+constexpr int kHiWarps = 16;              // 4 position groups x 4 image groups
+constexpr int kHiKB = 16;                 // output positions per block
+constexpr int kHiBc = 16;                 // images per CTA
+constexpr int kHiCols = kHiBc * 8;        // window columns (image, byte plane)
+constexpr int kHiRS = 32;                 // ring size in 32-byte k-steps
+constexpr int kHiRK = kHiRS * 32;         // ring bytes per column (power of 2)
+constexpr int kHiRKP = kHiRK + 16;        // padded column stride (== 16 mod 128: conflict-free ldmatrix)
+constexpr int kHiDepth = 4;               // A-fragment pipeline stages (cp.async)
+constexpr int kHiStage = 4 * 4 * 32;      // uint4 per stage: 4 position groups x 4 positions x 32 lanes
+constexpr int kHiERow = 68;               // epilogue scratch row (u32): 64 values + pad
+constexpr size_t kHiSmem =
+    (size_t)kHiCols * kHiRKP + (size_t)kHiDepth * kHiStage * 16 + (size_t)kHiWarps * 8 * kHiERow * 4;
+
+__device__ __forceinline__ int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+__device__ __forceinline__ void mma_u8(int (&c)[4], const uint4& a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory");
+}
+
+// byte d of four words -> one u32 (word i in byte i)
+__device__ __forceinline__ uint32_t gather_byte(const u64d (&w)[4], int d) {
+  const int sh = 8 * (d & 3);
+  uint32_t x[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) x[i] = (uint32_t)(d < 4 ? w[i] : (w[i] >> 32)) >> sh;
+  return (x[0] & 0xFF) | ((x[1] & 0xFF) << 8) | ((x[2] & 0xFF) << 16) | (x[3] << 24);
+}
+
+struct HiArgs {
+  PrimeTable pt;
+  const u64d* D;      // [B][l][l+1][N] ModUp digits, slot order, canonical
+  const u64d* v;      // [B][2][l][N] input ciphertexts (c0 = poly 0)
+  const uint4* wt;    // [l+1][N/16][NSG][4][4][32] A fragments of this chunk
+  const u64d* ec;     // [np][4][3][2] (2^(24 g + 16 q) mod q, Shoup companion)
+  u64d* acc;          // [B][2][l+1][N]
+  int B, L, N, NSG, r_hi, nig, strips, accumulate;
+};
+
+// k-step (32 kappa bytes) holding the first kappa of position kh's band
+template <int J>
+__device__ __forceinline__ int sfirst(int kh, int r_hi) {
+  return floor_div((kh - r_hi) * J, 32);
+}
+
+template <int J>
+__global__ void __launch_bounds__(32 * kHiWarps, 1) k_hs_imma(HiArgs a) {
+  constexpr int LV = J - 1;
+  extern __shared__ __align__(16) uint8_t hi_smem[];
+  uint8_t* ring = hi_smem;  // [kHiCols][kHiRKP]
+  uint4* astage = reinterpret_cast<uint4*>(hi_smem + (size_t)kHiCols * kHiRKP);  // [kHiDepth][kHiStage]
+  uint32_t* epi = reinterpret_cast<uint32_t*>(astage + kHiDepth * kHiStage);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mg = warp >> 2, ng = warp & 3;
+  const int N = a.N, S = N >> 1, bps = S / kHiKB, NSG = a.NSG;
+  const int ig = blockIdx.x % a.nig, strip = blockIdx.x / a.nig;
+  const long T = (long)(LV + 1) * 2 * bps;
+  const long blk0 = T * strip / a.strips, blk1 = T * (strip + 1) / a.strips;
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  const uint32_t astage_s = (uint32_t)__cvta_generic_to_shared(astage);
+  uint32_t* E = epi + warp * 8 * kHiERow;
+  // ldmatrix row address of this lane (before the k-step offset): matrix
+  // lane/8 = (n-tile pair member, kappa half), row lane%8 = byte plane
+  const int lm = lane >> 3, lrow = lane & 7;
+  const uint32_t lbase0 = ring_s + (uint32_t)((4 * ng + (lm >> 1)) * 8 + lrow) * kHiRKP + 16 * (lm & 1);
+  const uint32_t lbase1 = lbase0 + 2 * 8 * kHiRKP;  // n-tiles 2, 3
+  int cur_seg = -1, st_hi = 0;
+  for (long blk = blk0; blk < blk1; ++blk) {
+    const int seg = (int)(blk / bps), kb = (int)(blk % bps);
+    const int t = seg >> 1, half = seg & 1, kh0 = kb * kHiKB;
+    const int lo_s = sfirst<J>(kh0, a.r_hi), hi_s = sfirst<J>(kh0 + kHiKB - 4, a.r_hi) + NSG;
+    __syncthreads();  // all warps are done with the previous block's ring and stages
+    if (seg != cur_seg) {
+      cur_seg = seg;
+      st_hi = lo_s;
+    }
+    // ---- A-fragment pipeline prologue: stages 0 .. kHiDepth-2
+    const uint4* wsrc = a.wt + ((size_t)t * (N / kHiKB) + (size_t)half * bps + kb) * NSG * kHiStage + threadIdx.x;
+#pragma unroll
+    for (int d = 0; d < kHiDepth - 1; ++d) {
+      if (d < NSG) cp_async16(astage_s + (uint32_t)(d * kHiStage + threadIdx.x) * 16, wsrc + (size_t)d * kHiStage);
+      cp_commit();
+    }
+    // ---- stage window steps [st_hi, hi_s): items = (image, 4 kappa bytes)
+    {
+      const int nk4 = 8 * (hi_s - st_hi), items = nk4 * kHiBc;
+      const u64d* Dt = a.D + (size_t)t * N + (size_t)half * S;
+      const u64d* ct = a.v + (size_t)t * N + (size_t)half * S;
+      for (int it = threadIdx.x; it < items; it += 32 * kHiWarps) {
+        const int img = it / nk4, k4 = 8 * st_hi + it % nk4, b = ig * kHiBc + img;
+        u64d w[4];
+        int pos = floor_div(4 * k4, J), j = 4 * k4 - pos * J;
+        const u64d* Db = Dt + (size_t)b * LV * (LV + 1) * N;
+        const u64d* cb = ct + (size_t)b * 2 * LV * N;
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const int pm = pos & (S - 1);  // S is a power of two
+          u64d val = 0;
+          if (b < a.B) {
+            if (j < LV) val = __ldg(Db + (size_t)j * (LV + 1) * N + pm);
+            else if (t < LV) val = __ldg(cb + pm);
+          }
+          w[x] = val;
+          if (++j == J) j = 0, ++pos;
+        }
+        const int off = (4 * k4) & (kHiRK - 1);
+#pragma unroll
+        for (int d = 0; d < 8; ++d)
+          *reinterpret_cast<uint32_t*>(ring + (size_t)(img * 8 + d) * kHiRKP + off) = gather_byte(w, d);
+      }
+      st_hi = hi_s;
+    }
+    // ---- warp: positions kh0 + 4 mg + u, images ig*16 + 4 ng + n; all
+    // warps walk the same NSG local steps (the group's own first step + ls)
+    const int kw = kh0 + 4 * mg;
+    const int s0 = sfirst<J>(kw, a.r_hi);
+    int c[4][4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int n = 0; n < 4; ++n) c[u][n][0] = c[u][n][1] = c[u][n][2] = c[u][n][3] = 0;
+    const uint4* arow = astage + mg * 4 * 32 + lane;
+    for (int ls = 0; ls < NSG; ++ls) {
+      cp_wait<kHiDepth - 2>();
+      __syncthreads();  // stage ls is visible to all; stage ls-1 is free
+      if (ls + kHiDepth - 1 < NSG)
+        cp_async16(astage_s + (uint32_t)(((ls + kHiDepth - 1) % kHiDepth) * kHiStage + threadIdx.x) * 16,
+                   wsrc + (size_t)(ls + kHiDepth - 1) * kHiStage);
+      cp_commit();
+      const uint4* as = arow + (ls % kHiDepth) * kHiStage;
+      uint4 ac[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) ac[u] = as[u * 32];
+      const uint32_t off = (uint32_t)((32 * (s0 + ls)) & (kHiRK - 1));
+      uint32_t b0[4], b1[4];
+      ldsm_x4(lbase0 + off, b0[0], b1[0], b0[1], b1[1]);
+      ldsm_x4(lbase1 + off, b0[2], b1[2], b0[3], b1[3]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) mma_u8(c[u][n], ac[u], b0[n], b1[n]);
+    }
+    // ---- epilogue: four rounds (one position each) of 4 images x 2 parts
+    // = 8 outputs through the warp's scratch; lane (o, qq) combines byte
+    // planes e in {2 qq, 2 qq + 1}, d < 8 of output o
+    const int pi = t == LV ? a.L : t;
+    const DevPrime pr = a.pt.p[pi];
+    const int o = lane & 7, qq = lane >> 3;
+    const u64d* ecp = a.ec + ((size_t)pi * 4 + qq) * 6;
+    const u64d e0 = __ldg(ecp), e0p = __ldg(ecp + 1), e1 = __ldg(ecp + 2), e1p = __ldg(ecp + 3),
+               e2 = __ldg(ecp + 4), e2p = __ldg(ecp + 5);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      __syncwarp();
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        const int col = (lane >> 2) * 8 + 2 * (lane & 3);
+        *reinterpret_cast<uint2*>(E + (2 * n) * kHiERow + col) = make_uint2((uint32_t)c[u][n][0], (uint32_t)c[u][n][1]);
+        *reinterpret_cast<uint2*>(E + (2 * n + 1) * kHiERow + col) =
+            make_uint2((uint32_t)c[u][n][2], (uint32_t)c[u][n][3]);
+      }
+      __syncwarp();
+      u64d A[3] = {0, 0, 0};
+#pragma unroll
+      for (int ee = 0; ee < 2; ++ee)
+#pragma unroll
+        for (int dq = 0; dq < 2; ++dq) {
+          const uint4 q4 = *reinterpret_cast<const uint4*>(E + o * kHiERow + (2 * qq + ee) * 8 + 4 * dq);
+          const uint32_t cv[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+          for (int dd = 0; dd < 4; ++dd) {
+            const int sp = ee + 4 * dq + dd;  // + 2 qq (applied through the constants)
+            A[sp / 3] += (u64d)cv[dd] << (8 * (sp % 3));
+          }
+        }
+      // < 6q, then the four quarters' sums mod q
+      u64d sum = shoup_mul_lazy(A[0], e0, e0p, pr.q) + shoup_mul_lazy(A[1], e1, e1p, pr.q) +
+                 shoup_mul_lazy(A[2], e2, e2p, pr.q);
+      sum = shoup_mul_d(sum, 1ull, pr.one_sh, pr.q);
+      sum = add_mod_d(sum, __shfl_xor_sync(0xffffffffu, sum, 8), pr.q);
+      sum = add_mod_d(sum, __shfl_xor_sync(0xffffffffu, sum, 16), pr.q);
+      if (qq == 0) {
+        const int n = o >> 1, p = o & 1;
+        const int b = ig * kHiBc + 4 * ng + n, k = half * S + kw + u;
+        if (b < a.B) {
+          u64d* dst = a.acc + ((size_t)b * 2 + p) * (LV + 1) * N + (size_t)t * N + k;
+          *dst = a.accumulate ? add_mod_d(sum, *dst, pr.q) : sum;
+        }
+      }
+    }
+  }
+  cp_wait<0>();
+}
+
+// A fragments of one chunk: thread = (t, block, local step, group, position, lane)
+template <int J>
+__global__ void k_hs_imma_tiles(PrimeTable pt, const u64d* __restrict__ fk, size_t fk_words, int first_keyed,
+                                const u64d* __restrict__ masks, const int* __restrict__ rdiag, const u64d* pmod,
+                                int L, int N, int NSG, int r_lo, int r_hi, uint4* __restrict__ wt) {
+  constexpr int LV = J - 1;
+  const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = (int)(gid & 31), u = (int)((gid >> 5) & 3), g4 = (int)((gid >> 7) & 3);
+  const size_t item = gid >> 9;  // (t, kb, ls)
+  const int nkb = N / kHiKB;
+  const size_t total = (size_t)(LV + 1) * nkb * NSG;
+  if (item >= total) return;
+  const int ls = (int)(item % NSG), kb = (int)((item / NSG) % nkb), t = (int)(item / ((size_t)NSG * nkb));
+  const int S = N >> 1, k = kb * kHiKB + 4 * g4 + u, kh = k & (S - 1);
+  const int pi = t == LV ? L : t;
+  const DevPrime pr = pt.p[pi];
+  const int s = floor_div((kh - u - r_hi) * J, 32) + ls, e = lane >> 2;
+  uint32_t reg[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int p = i & 1, kk = (i >> 1) * 16 + 4 * (lane & 3);
+    uint32_t word = 0;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int kap = 32 * s + kk + x, pos = floor_div(kap, J), j = kap - pos * J, r = kh - pos;
+      if (r < r_lo || r > r_hi) continue;
+      const int di = rdiag[r];
+      if (di < 0) continue;
+      u64d w = 0;
+      if (j < LV) {
+        if (r != 0) {
+          const u64d f = fk[(size_t)(di - first_keyed) * fk_words + ((size_t)(j * 2 + p) * (LV + 1) + t) * N + k];
+          w = mont_mul(unsplit31(f), 1ull, pr.q, pr.qneg_inv);
+        }
+      } else if (p == 0 && t < LV) {
+        const u64d m = masks[((size_t)di * (LV + 1) + t) * N + k];
+        w = mont_mul(unsplit31(m), pmod[t], pr.q, pr.qneg_inv);
+      }
+      word |= (uint32_t)((w >> (8 * e)) & 0xFF) << (8 * x);
+    }
+    reg[i] = word;
+  }
+  wt[gid] = make_uint4(reg[0], reg[1], reg[2], reg[3]);
+}
+
+// cacc for the IMMA path: the c0 * mask term lives in acc (P-scaled), so
+// cacc holds only diagonal 0's c1 * mask term (part 1)
+__global__ void k_hs_cacc(const u64d* __restrict__ v, const u64d* __restrict__ m0, PrimeTable pt, int B, int l,
+                          int N, int c1_term, u64d* __restrict__ cacc) {
+  const size_t total = (size_t)B * 2 * l * N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % N), t = (int)((i / N) % l), p = (int)((i / ((size_t)l * N)) % 2);
+    const size_t b = i / ((size_t)2 * l * N);
+    u64d r = 0;
+    if (p == 1 && c1_term) {
+      const DevPrime pr = pt.p[t];
+      r = mont_mul(v[(b * 2 + 1) * l * N + (size_t)t * N + k], unsplit31(m0[(size_t)t * N + k]), pr.q, pr.qneg_inv);
+    }
+    cacc[i] = r;
+  }
+}
+
+template <int J>
+void hs_imma_go(Context& c, const HiArgs& a, int grid, double bytes, double ops) {
+  static bool prepared = false;
+  if (!prepared) {
+    CK(cudaFuncSetAttribute(k_hs_imma<J>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHiSmem));
+    prepared = true;
+  }
+  LAUNCH_BO(c, "k_hs_imma", bytes, ops, k_hs_imma<J><<<grid, 32 * kHiWarps, kHiSmem, c.stream>>>(a));
+}
+
+template <int J>
+void hs_tiles_go(Context& c, const HsDiagTable& t, const u64d* pmod, const int* rdiag, const HsImmaChunk& ch,
+                 uint4* wt) {
+  const size_t threads = (size_t)J * c.N() * ch.ns * 32;  // (t, position, local step, lane)
+  LAUNCH(c, "k_hs_imma_tiles",
+         k_hs_imma_tiles<J><<<(unsigned)((threads + 255) / 256), 256, 0, c.stream>>>(
+             c.primes, t.fk, t.fk_words, t.first_keyed, t.masks, rdiag, pmod, c.L(), c.N(), ch.ns, ch.r_lo,
+             ch.r_hi, wt));
+}
+
+}  // namespace
+
+int hs_imma_chunk_span(int l) {
+  const int J = l + 1;
+  // ring: NSG + ceil(12 J / 32) + 1 <= kHiRS, NSG = ceil((span J + 31) / 32) + 1
+  const int span = ((kHiRS - 3 - (12 * J + 31) / 32) * 32 - 31) / J;
+  return span < 128 ? span : 128;
+}
+
+bool hs_imma_supported(Context& c, int l) { return l >= 1 && l <= 6 && c.S() % kHiKB == 0 && c.S() >= 64; }
+
+size_t hs_imma_tile_words(Context& c, int l, const HsImmaChunk& ch) {
+  return (size_t)(l + 1) * c.N() * ch.ns * 32 * 2;  // uint4 = 2 words; ns = NSG (group steps)
+}
+
+void launch_hs_imma_tiles(Context& c, int l, const HsDiagTable& t, const u64d* pmod, const int* rdiag,
+                          const HsImmaChunk& ch, u64d* wt) {
+  uint4* w4 = reinterpret_cast<uint4*>(wt);
+  switch (l + 1) {
+    case 2: hs_tiles_go<2>(c, t, pmod, rdiag, ch, w4); break;
+    case 3: hs_tiles_go<3>(c, t, pmod, rdiag, ch, w4); break;
+    case 4: hs_tiles_go<4>(c, t, pmod, rdiag, ch, w4); break;
+    case 5: hs_tiles_go<5>(c, t, pmod, rdiag, ch, w4); break;
+    case 6: hs_tiles_go<6>(c, t, pmod, rdiag, ch, w4); break;
+    case 7: hs_tiles_go<7>(c, t, pmod, rdiag, ch, w4); break;
+    default: fail(HEGPU_ERR_ARG, "hs_imma: level out of range");
+  }
+}
+
+void launch_hs_imma(Context& c, const u64d* v, int B, int l, const u64d* D, const HsImmaChunk& ch,
+                    const u64d* ec, int accumulate, u64d* acc) {
+  const int keyed = ch.keyed, ndiag = ch.ndiag;
+  const int N = c.N(), S = N / 2, J = l + 1;
+  HiArgs a{};
+  a.pt = c.primes;
+  a.D = D;
+  a.v = v;
+  a.wt = reinterpret_cast<const uint4*>(ch.wt);
+  a.ec = ec;
+  a.acc = acc;
+  a.B = B;
+  a.L = c.L();
+  a.N = N;
+  a.NSG = ch.ns;
+  a.r_hi = ch.r_hi;
+  a.nig = (B + kHiBc - 1) / kHiBc;
+  const long T = (long)J * 2 * (S / kHiKB);
+  int sms = 148;
+  {
+    static int dev_sms = 0;
+    if (!dev_sms) {
+      int d = 0;
+      CK(cudaGetDevice(&d));
+      CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, d));
+    }
+    sms = dev_sms;
+  }
+  long strips = sms / a.nig;
+  if (strips < 1) strips = 1;
+  if (strips > T) strips = T;
+  a.strips = (int)strips;
+  a.accumulate = accumulate;
+  // the chunk's A fragments once, D/c0 windows once per strip (~once), acc
+  // written (and read back when accumulating)
+  const double NB = 8.0 * N;
+  const double bytes = 16.0 * ch.ns * 32 * J * N + NB * B * (l * J + l) + NB * B * 2 * J * (accumulate ? 2 : 1);
+  const double ops = (double)N * B * (keyed * l * J * 2.0 + ndiag * l);  // modular MAC terms (as the IMAD path)
+  const int grid = (int)(a.nig * strips);
+  switch (J) {
+    case 2: hs_imma_go<2>(c, a, grid, bytes, ops); break;
+    case 3: hs_imma_go<3>(c, a, grid, bytes, ops); break;
+    case 4: hs_imma_go<4>(c, a, grid, bytes, ops); break;
+    case 5: hs_imma_go<5>(c, a, grid, bytes, ops); break;
+    case 6: hs_imma_go<6>(c, a, grid, bytes, ops); break;
+    case 7: hs_imma_go<7>(c, a, grid, bytes, ops); break;
+    default: fail(HEGPU_ERR_ARG, "hs_imma: level out of range");
+  }
+}
+
+void launch_hs_cacc(Context& c, const u64d* v, const u64d* m0, int B, int l, int c1_term, u64d* cacc) {
+  const size_t total = (size_t)B * 2 * l * c.N();
+  unsigned g = (unsigned)((total + 255) / 256);
+  if (g > 148 * 16) g = 148 * 16;
+  LAUNCH_B(c, "k_hs_cacc", 8.0 * total * (c1_term ? 1.5 : 1.0),
+           k_hs_cacc<<<g, 256, 0, c.stream>>>(v, m0, c.primes, B, l, c.N(), c1_term, cacc));
+}
+
+}  // namespace hegpu

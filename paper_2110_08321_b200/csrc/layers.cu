@@ -257,6 +257,14 @@ void HsPlan::release() {
   for (auto& e : sub_chunks) cudaFree(e.second.first);
   sub_chunks.clear();
   cudaFree(fkeys);
+  for (HsImmaChunk& ch : imma) cudaFree(ch.wt);
+  imma.clear();
+  cudaFree(imma_ec);
+  cudaFree(imma_pmod);
+  cudaFree(d_rdiag);
+  imma_ec = imma_pmod = nullptr;
+  d_rdiag = nullptr;
+  imma_built = false;
   masks = nullptr;
   d_r = d_chunk = nullptr;
   fkeys = nullptr;
@@ -291,9 +299,87 @@ void HsPlan::ensure_keys(Context& c) {
   keys_resolved = true;
 }
 
+// HEGPU_HS_IMMA=0 keeps the integer-pipe kernel for every batch
+static int hs_imma_min_batch() {
+  static int mb = -1;
+  if (mb < 0) {
+    const char* e = getenv("HEGPU_HS_IMMA");
+    mb = e && atoi(e) == 0 ? 1 << 30 : 8;
+    if (e && atoi(e) > 1) mb = atoi(e);  // HEGPU_HS_IMMA=<min batch>
+  }
+  return mb;
+}
+
+bool HsPlan::use_imma(Context& c, int B, int i_lo, int i_hi) const {
+  return B >= hs_imma_min_batch() && i_lo == 0 && i_hi == (int)diag.size() && !diag.empty() &&
+         hs_imma_supported(c, level);
+}
+
+void HsPlan::ensure_imma(Context& c) {
+  if (imma_built) return;
+  ensure_keys(c);
+  const int l = level, N = c.N(), S = c.S(), np = c.P->np(), J = l + 1;
+  // epilogue constants 2^(24 g + 32 h) mod q with Shoup companions
+  std::vector<u64> ec((size_t)np * 24);
+  for (int pi = 0; pi < np; ++pi) {
+    const u64 q = c.P->q(pi);
+    for (int h = 0; h < 4; ++h)
+      for (int g = 0; g < 3; ++g) {
+        u128 w = 1;
+        for (int e = 0; e < 24 * g + 16 * h; ++e) w = (w * 2) % q;
+        ec[((size_t)pi * 4 + h) * 6 + 2 * g] = (u64)w;
+        ec[((size_t)pi * 4 + h) * 6 + 2 * g + 1] = (u64)((w << 64) / q);
+      }
+  }
+  std::vector<u64> pm(l);
+  for (int t = 0; t < l; ++t) pm[t] = c.P->q(c.L()) % c.P->q(t);
+  std::vector<int> rd(S, -1);
+  for (size_t i = 0; i < diag.size(); ++i) rd[diag[i].right] = (int)i;
+  CK(cudaMalloc((void**)&imma_ec, ec.size() * 8));
+  CK(cudaMemcpy(imma_ec, ec.data(), ec.size() * 8, cudaMemcpyHostToDevice));
+  CK(cudaMalloc((void**)&imma_pmod, pm.size() * 8));
+  CK(cudaMemcpy(imma_pmod, pm.data(), pm.size() * 8, cudaMemcpyHostToDevice));
+  CK(cudaMalloc((void**)&d_rdiag, rd.size() * sizeof(int)));
+  CK(cudaMemcpy(d_rdiag, rd.data(), rd.size() * sizeof(int), cudaMemcpyHostToDevice));
+  // chunks of kept diagonals whose r span fits the kernel's window ring
+  const int span = hs_imma_chunk_span(l);
+  const int first_keyed = diag[0].shift == 0 ? 1 : 0;
+  HsDiagTable tab{(int)diag.size(), 0, d_r, fkeys, (size_t)l * 2 * (l + 1) * N, first_keyed, 1, masks, 0, nullptr};
+  size_t i = 0;
+  while (i < diag.size()) {
+    HsImmaChunk ch{};
+    ch.r_lo = (int)diag[i].right;
+    ch.r_hi = ch.r_lo;
+    while (i < diag.size() && diag[i].right - ch.r_lo < span) {
+      ch.r_hi = (int)diag[i].right;
+      ch.keyed += diag[i].shift != 0;
+      ++ch.ndiag;
+      ++i;
+    }
+    // steps per 4-position group: ceil((span J + 31) / 32) + 1 (hs_imma.cu)
+    ch.ns = ((ch.r_hi - ch.r_lo + 1) * J + 62) / 32 + 1;
+    CK(cudaMalloc((void**)&ch.wt, hs_imma_tile_words(c, l, ch) * 8));
+    launch_hs_imma_tiles(c, l, tab, imma_pmod, d_rdiag, ch, ch.wt);
+    imma.push_back(ch);
+  }
+  CK(cudaStreamSynchronize(c.stream));
+  imma_built = true;
+}
+
 void HsPlan::accumulate(Context& c, const CtBatch& v, int i_lo, int i_hi, u64d* acc, u64d* cacc) {
   const int B = v.count, l = level, N = c.N();
   ensure_keys(c);
+  if (use_imma(c, B, i_lo, i_hi)) {
+    ensure_imma(c);
+    u64d* tmp = c.alloc((size_t)B * l * N);
+    u64d* D = c.alloc((size_t)B * l * (l + 1) * N);
+    ks_modup(c, v.d + (size_t)l * N, (long)v.stride(), B, l, nullptr, tmp, D);
+    for (size_t ci = 0; ci < imma.size(); ++ci) launch_hs_imma(c, v.d, B, l, D, imma[ci], imma_ec, ci > 0, acc);
+    launch_hs_cacc(c, v.d, masks, B, l, diag[0].right == 0 ? 1 : 0, cacc);
+    c.free(tmp);
+    c.free(D);
+    return;
+  }
   // the plan's chunks clipped to [i_lo, i_hi) (cached per range)
   const int* chunks = d_chunk;
   int nch = nchunk;

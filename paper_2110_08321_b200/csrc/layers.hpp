@@ -54,6 +54,15 @@ struct HsPlan {
   std::map<std::pair<int, int>, std::pair<int*, int>> sub_chunks;  // diagonal range -> (device chunks, count)
   u64d* fkeys = nullptr;      // [keyed][level][2][level+1][N] key_i * mask_i (first run)
   bool keys_resolved = false;
+  // tensor-core path (hs_imma.cu): chunks with their A fragments, built on
+  // the first run with a batch of >= hs_imma_min_batch() images
+  std::vector<HsImmaChunk> imma;
+  u64d* imma_ec = nullptr;    // [np][2][4][2] epilogue constants
+  u64d* imma_pmod = nullptr;  // [level] P mod q_t
+  int* d_rdiag = nullptr;     // [S] right rotation -> kept diagonal (or -1)
+  bool imma_built = false;
+  void ensure_imma(Context& c);
+  bool use_imma(Context& c, int B, int i_lo, int i_hi) const;
   void build(Context& c, const double* A, int m, int n, int level, bool skip_zero);
   void release();
   std::vector<int64_t> right_rotations() const;  // diagonals, then folds

@@ -227,6 +227,31 @@ def test_hs_matvec(pair, m, n, skip):
     assert ctx.total() == mc.tally.as_tuple()
 
 
+@pytest.mark.parametrize("m,n,l,B", [(10, 100, 3, 8), (32, 300, 3, 17), (300, 200, 3, 16), (4, 4, 3, 8),
+                                     (2, 2, 2, 9), (7, 500, 4, 16), (100, 400, 4, 33), (64, 256, 2, 8), (64, 400, 4, 16),
+                                     (50, 60, 5, 8)])
+def test_hs_matvec_batched_tensor_core(pair, m, n, l, B):
+    """batches of >= 8 ciphertexts take the int8 tensor-core HS kernel
+    (hs_imma.cu): every image's limbs == the single-ciphertext (integer
+    pipe) run and the CPU oracle"""
+    ctx, ck = pair
+    rng = np.random.default_rng(11 * m + n + B)
+    A = np.eye(4) if (m, n) == (4, 4) else rng.normal(0, 0.05, (m, n))
+    cts = [fresh(ck, rng, l, 500 + i, n=n) for i in range(B)]
+    plan = ctx.hs_plan(A, l, True)
+    ctx.gen_rotation_keys(plan.rotations())
+    batch = np.concatenate([c for _, c in cts])
+    out = ctx.ct(B, l - 1)
+    got = ctx.hs_matvec(plan, ctx.ct(B, l, batch, DELTA), out).download().reshape(B, -1)
+    for i in (0, B - 1):
+        one = ctx.hs_matvec(plan, ctx.ct(1, l, cts[i][1], DELTA), ctx.ct(1, l - 1)).download()
+        assert np.array_equal(got[i], one), i
+    assert np.array_equal(got[B // 2], P.hs_matvec(ck, cts[B // 2][1], l, A, True))
+    for i in range(B):
+        dec = ck.decrypt_decode(got[i], l - 1, DELTA)
+        assert np.abs(dec[:m] - A @ cts[i][0]).max() < 1e-4
+
+
 @pytest.mark.parametrize("m,n,nparts", [(300, 200, 3), (32, 300, 2), (10, 100, 8), (4, 4, 5)])
 def test_hs_matvec_split_partial_sums(pair, m, n, nparts):
     """config-3 style distributed HS: per-part extended-basis accumulators
@@ -298,6 +323,23 @@ def test_cfg0_net_bit_exact_and_logits(cfg0):
         logits = net.decrypt_logits(got[b])
         ref = HS.ref_forward(spec, w, imgs[b])
         assert np.abs(logits - ref).max() < 1e-3
+
+
+def test_cfg0_net_batch_tensor_core_hs(cfg0):
+    """a batch of 9 images: both HS layers run on the tensor-core kernel;
+    image 0's limbs == the oracle pipeline, all logits within 1e-3"""
+    cfg, ctx, ck, w, net = cfg0
+    B = 9
+    imgs = [net_image(cfg, 40 + s) for s in range(B)]
+    taps = np.concatenate([net.encrypt_image(im, nonce=40 + s) for s, im in enumerate(imgs)])
+    out = ctx.ct(B, net.out_level)
+    net.run(ctx.ct(B * net.ntaps, net.top, taps, DELTA), out)
+    got = out.download().reshape(B, -1)
+    want, _ = P.run_net(ck, cfg, w, imgs[0], nonce=40)
+    assert np.array_equal(got[0], want)
+    spec = HS.CnnSpec(cfg.in_c, cfg.in_d, cfg.k, cfg.s, cfg.c_out, cfg.dense, cfg.n_slots)
+    for b in range(B):
+        assert np.abs(net.decrypt_logits(got[b]) - HS.ref_forward(spec, w, imgs[b])).max() < 1e-3
 
 
 def test_cfg0_run_host_matches_device_run(cfg0):
