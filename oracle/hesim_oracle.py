@@ -253,6 +253,77 @@ def hs_matvec(A, v, ctx, skip_zero_diagonals=True):
     return s
 
 
+def lola_dense_matvec(A, v, ctx):
+    """proj/src/matvec.cpp:107-123: one ciphertext per row i, slot 0 = A[i] . x
+    (product with the packed row, rotate-and-sum over next_pow2(n) slots,
+    the fold residue cleared at the value level)"""
+    A = np.asarray(A, dtype=np.float64)
+    m, n = A.shape
+    N = v.n_slots
+    _check_dims(m, n, N)
+    delta = next_power_of_two(n)
+    out = []
+    for i in range(m):
+        row = pack(A[i], N, PLAINTEXT)
+        p = rotate_and_sum(mul(row, v, ctx), delta, 1, ctx)
+        out.append(p.masked_prefix(1))
+    return out
+
+
+def lola_stacked_matvec(A, v, ctx):
+    """proj/src/matvec.cpp:125-166: k = N / next_pow2(n) rows per batch; the
+    input is re-stacked k times per batch (k-1 rotations + additions), one
+    product, rotate-and-sum, segment starts kept (free), batches combined by
+    right rotations by the batch index.  Returns (ct, slot_of_row)."""
+    A = np.asarray(A, dtype=np.float64)
+    m, n = A.shape
+    N = v.n_slots
+    _check_dims(m, n, N)
+    delta = next_power_of_two(n)
+    if delta > N:
+        raise CapacityError(f"stacked: padded width {delta} exceeds {N} slots")
+    k = N // delta
+    batches = _ceil_div(m, k)
+    vd = v.masked_prefix(n)
+    res = zeros(N, CIPHERTEXT)
+    slot_of_row = [0] * m
+    for b in range(batches):
+        stacked = vd
+        for j in range(1, k):
+            stacked = add(stacked, rotate_right(vd, j * delta, ctx), ctx)
+        rows_pt = np.zeros(N)
+        for j in range(k):
+            if b * k + j < m:
+                rows_pt[j * delta: j * delta + n] = A[b * k + j]
+        p = mul(SlotVector(rows_pt, PLAINTEXT), stacked, ctx)
+        p = rotate_and_sum(p, delta, 1, ctx)
+        clean = np.zeros(N)
+        for j in range(k):
+            if b * k + j < m:
+                clean[j * delta] = p[j * delta]
+                slot_of_row[b * k + j] = j * delta + b
+        batch = SlotVector(clean, CIPHERTEXT)
+        res = batch if b == 0 else add(res, rotate_right(batch, b, ctx), ctx)
+    return res, slot_of_row
+
+
+def predict_lola_dense(m, n):
+    """proj/src/matvec.cpp:189-195 -> (rotations, multiplications, additions)"""
+    lg = _ceil_log2(n)
+    return m * lg, m, m * lg
+
+
+def predict_lola_stacked(m, n, n_slots):
+    """proj/src/matvec.cpp:197-211 -> (rotations, multiplications, additions)"""
+    delta = next_power_of_two(n)
+    if delta > n_slots:
+        raise CapacityError("stacked: padded width exceeds slot count")
+    k = n_slots // delta
+    batches = _ceil_div(m, k)
+    r = batches * (k + _ceil_log2(n) - 1) + batches - 1
+    return r, batches, r
+
+
 def predict_hs(m, n, n_slots):
     """proj/src/matvec.cpp:168-187 -> (rotations, multiplications, additions)"""
     _check_dims(m, n, n_slots)

@@ -33,14 +33,14 @@ constexpr int kHiWarps = 16;              // 4 position groups x 4 image groups
 constexpr int kHiKB = 16;                 // output positions per block
 constexpr int kHiBc = 16;                 // images per CTA
 constexpr int kHiCols = kHiBc * 8;        // window columns (image, byte plane)
-constexpr int kHiRS = 32;                 // ring size in 32-byte k-steps
-constexpr int kHiRK = kHiRS * 32;         // ring bytes per column (power of 2)
-constexpr int kHiRKP = kHiRK + 16;        // padded column stride (== 16 mod 128: conflict-free ldmatrix)
-constexpr int kHiDepth = 4;               // A-fragment pipeline stages (cp.async)
+constexpr int kHiRSMax = 24;              // max ring size in 32-byte k-steps (runtime RS <= this)
+constexpr int kHiMaxDepth = 8;            // A-fragment pipeline stages (runtime D <= this)
 constexpr int kHiStage = 4 * 4 * 32;      // uint4 per stage: 4 position groups x 4 positions x 32 lanes
 constexpr int kHiERow = 68;               // epilogue scratch row (u32): 64 values + pad
-constexpr size_t kHiSmem =
-    (size_t)kHiCols * kHiRKP + (size_t)kHiDepth * kHiStage * 16 + (size_t)kHiWarps * 8 * kHiERow * 4;
+constexpr size_t kHiEpiBytes = (size_t)kHiWarps * 16 * kHiERow * 4;
+constexpr size_t kHiSmemMax = 226 * 1024;  // dynamic (227 KB less the static barriers)
+// padded column stride of an RS-step ring (== 16 mod 128: conflict-free ldmatrix)
+__host__ __device__ constexpr int hi_rkp(int rs) { return (32 * rs + 127) / 128 * 128 + 16; }
 
 __device__ __forceinline__ int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
@@ -55,6 +55,31 @@ __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                : "r"(addr));
+}
+
+// mbarrier / bulk-copy (TMA) pipeline primitives
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
@@ -80,9 +105,10 @@ struct HiArgs {
   const u64d* D;      // [B][l][l+1][N] ModUp digits, slot order, canonical
   const u64d* v;      // [B][2][l][N] input ciphertexts (c0 = poly 0)
   const uint4* wt;    // [l+1][N/16][NSG][4][4][32] A fragments of this chunk
-  const u64d* ec;     // [np][4][3][2] (2^(24 g + 16 q) mod q, Shoup companion)
+  const u64d* ec;     // [np][2][4][2] (2^(24 g + 32 h) mod q, Shoup companion)
   u64d* acc;          // [B][2][l+1][N]
   int B, L, N, NSG, r_hi, nig, strips, accumulate;
+  int RS, RKP, depth;  // ring steps, ring column stride (bytes), pipeline stages
 };
 
 // k-step (32 kappa bytes) holding the first kappa of position kh's band
@@ -95,9 +121,11 @@ template <int J>
 __global__ void __launch_bounds__(32 * kHiWarps, 1) k_hs_imma(HiArgs a) {
   constexpr int LV = J - 1;
   extern __shared__ __align__(16) uint8_t hi_smem[];
-  uint8_t* ring = hi_smem;  // [kHiCols][kHiRKP]
-  uint4* astage = reinterpret_cast<uint4*>(hi_smem + (size_t)kHiCols * kHiRKP);  // [kHiDepth][kHiStage]
-  uint32_t* epi = reinterpret_cast<uint32_t*>(astage + kHiDepth * kHiStage);
+  __shared__ __align__(8) uint64_t bars[2 * kHiMaxDepth];  // full[d], empty[d]
+  const int RS = a.RS, RK = 32 * a.RS, RKP = a.RKP, DEP = a.depth;
+  uint8_t* ring = hi_smem;  // [kHiCols][RKP]
+  uint4* astage = reinterpret_cast<uint4*>(hi_smem + (size_t)kHiCols * RKP);  // [DEP][kHiStage]
+  uint32_t* epi = reinterpret_cast<uint32_t*>(astage + DEP * kHiStage);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mg = warp >> 2, ng = warp & 3;
   const int N = a.N, S = N >> 1, bps = S / kHiKB, NSG = a.NSG;
@@ -106,29 +134,43 @@ __global__ void __launch_bounds__(32 * kHiWarps, 1) k_hs_imma(HiArgs a) {
   const long blk0 = T * strip / a.strips, blk1 = T * (strip + 1) / a.strips;
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
   const uint32_t astage_s = (uint32_t)__cvta_generic_to_shared(astage);
-  uint32_t* E = epi + warp * 8 * kHiERow;
+  uint32_t* E = epi + warp * 16 * kHiERow;
   // ldmatrix row address of this lane (before the k-step offset): matrix
   // lane/8 = (n-tile pair member, kappa half), row lane%8 = byte plane
   const int lm = lane >> 3, lrow = lane & 7;
-  const uint32_t lbase0 = ring_s + (uint32_t)((4 * ng + (lm >> 1)) * 8 + lrow) * kHiRKP + 16 * (lm & 1);
-  const uint32_t lbase1 = lbase0 + 2 * 8 * kHiRKP;  // n-tiles 2, 3
+  const uint32_t lbase0 = ring_s + (uint32_t)((4 * ng + (lm >> 1)) * 8 + lrow) * RKP + 16 * (lm & 1);
+  const uint32_t lbase1 = lbase0 + 2 * 8 * RKP;  // n-tiles 2, 3
+  const uint32_t full_s = (uint32_t)__cvta_generic_to_shared(bars), empty_s = full_s + 8 * kHiMaxDepth;
+  if (threadIdx.x == 0) {
+    for (int d = 0; d < DEP; ++d) {
+      mbar_init(full_s + 8 * d, 1);
+      mbar_init(empty_s + 8 * d, kHiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // A-fragment stages: one bulk copy (8 KB) per k-step, issued by thread 0
+  // into stage pst (phase pph); consumers read stage cst (phase cph)
+  uint32_t pst = 0, pph = 0, cst = 0, cph = 0;
+  auto produce = [&](const uint4* src) {
+    mbar_wait(empty_s + 8 * pst, pph ^ 1);  // passes at once on a fresh barrier
+    mbar_expect_tx(full_s + 8 * pst, kHiStage * 16);
+    bulk_g2s(astage_s + pst * kHiStage * 16, src, kHiStage * 16, full_s + 8 * pst);
+    if (++pst == (uint32_t)DEP) pst = 0, pph ^= 1;
+  };
   int cur_seg = -1, st_hi = 0;
   for (long blk = blk0; blk < blk1; ++blk) {
     const int seg = (int)(blk / bps), kb = (int)(blk % bps);
     const int t = seg >> 1, half = seg & 1, kh0 = kb * kHiKB;
     const int lo_s = sfirst<J>(kh0, a.r_hi), hi_s = sfirst<J>(kh0 + kHiKB - 4, a.r_hi) + NSG;
-    __syncthreads();  // all warps are done with the previous block's ring and stages
+    __syncthreads();  // all warps are done with the previous block's ring
     if (seg != cur_seg) {
       cur_seg = seg;
       st_hi = lo_s;
     }
-    // ---- A-fragment pipeline prologue: stages 0 .. kHiDepth-2
-    const uint4* wsrc = a.wt + ((size_t)t * (N / kHiKB) + (size_t)half * bps + kb) * NSG * kHiStage + threadIdx.x;
-#pragma unroll
-    for (int d = 0; d < kHiDepth - 1; ++d) {
-      if (d < NSG) cp_async16(astage_s + (uint32_t)(d * kHiStage + threadIdx.x) * 16, wsrc + (size_t)d * kHiStage);
-      cp_commit();
-    }
+    // ---- A-fragment pipeline prologue: steps 0 .. D-2
+    const uint4* wsrc = a.wt + ((size_t)t * (N / kHiKB) + (size_t)half * bps + kb) * NSG * kHiStage;
+    if (threadIdx.x == 0)
+      for (int d = 0; d < DEP - 1 && d < NSG; ++d) produce(wsrc + (size_t)d * kHiStage);
     // ---- stage window steps [st_hi, hi_s): items = (image, 4 kappa bytes)
     {
       const int nk4 = 8 * (hi_s - st_hi), items = nk4 * kHiBc;
@@ -151,13 +193,15 @@ __global__ void __launch_bounds__(32 * kHiWarps, 1) k_hs_imma(HiArgs a) {
           w[x] = val;
           if (++j == J) j = 0, ++pos;
         }
-        const int off = (4 * k4) & (kHiRK - 1);
+        int off = (4 * k4) % RK;
+        if (off < 0) off += RK;
 #pragma unroll
         for (int d = 0; d < 8; ++d)
-          *reinterpret_cast<uint32_t*>(ring + (size_t)(img * 8 + d) * kHiRKP + off) = gather_byte(w, d);
+          *reinterpret_cast<uint32_t*>(ring + (size_t)(img * 8 + d) * RKP + off) = gather_byte(w, d);
       }
       st_hi = hi_s;
     }
+    __syncthreads();  // the window is staged
     // ---- warp: positions kh0 + 4 mg + u, images ig*16 + 4 ng + n; all
     // warps walk the same NSG local steps (the group's own first step + ls)
     const int kw = kh0 + 4 * mg;
@@ -168,68 +212,69 @@ __global__ void __launch_bounds__(32 * kHiWarps, 1) k_hs_imma(HiArgs a) {
 #pragma unroll
       for (int n = 0; n < 4; ++n) c[u][n][0] = c[u][n][1] = c[u][n][2] = c[u][n][3] = 0;
     const uint4* arow = astage + mg * 4 * 32 + lane;
+    int off = (32 * s0) % RK;
+    if (off < 0) off += RK;
     for (int ls = 0; ls < NSG; ++ls) {
-      cp_wait<kHiDepth - 2>();
-      __syncthreads();  // stage ls is visible to all; stage ls-1 is free
-      if (ls + kHiDepth - 1 < NSG)
-        cp_async16(astage_s + (uint32_t)(((ls + kHiDepth - 1) % kHiDepth) * kHiStage + threadIdx.x) * 16,
-                   wsrc + (size_t)(ls + kHiDepth - 1) * kHiStage);
-      cp_commit();
-      const uint4* as = arow + (ls % kHiDepth) * kHiStage;
+      const uint32_t st = cst;
+      mbar_wait(full_s + 8 * st, cph);
+      if (++cst == (uint32_t)DEP) cst = 0, cph ^= 1;
+      const uint4* as = arow + st * kHiStage;
       uint4 ac[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) ac[u] = as[u * 32];
-      const uint32_t off = (uint32_t)((32 * (s0 + ls)) & (kHiRK - 1));
       uint32_t b0[4], b1[4];
       ldsm_x4(lbase0 + off, b0[0], b1[0], b0[1], b1[1]);
       ldsm_x4(lbase1 + off, b0[2], b1[2], b0[3], b1[3]);
+      off += 32;
+      if (off == RK) off = 0;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_s + 8 * st);  // this warp is done with the stage
+      if (threadIdx.x == 0 && ls + DEP - 1 < NSG) produce(wsrc + (size_t)(ls + DEP - 1) * kHiStage);
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int n = 0; n < 4; ++n) mma_u8(c[u][n], ac[u], b0[n], b1[n]);
     }
-    // ---- epilogue: four rounds (one position each) of 4 images x 2 parts
-    // = 8 outputs through the warp's scratch; lane (o, qq) combines byte
-    // planes e in {2 qq, 2 qq + 1}, d < 8 of output o
+    // ---- epilogue: two rounds of 2 positions x 4 images x 2 parts = 16
+    // outputs through the warp's scratch; lane (o, dh) combines the byte
+    // planes e < 8, d in [4 dh, 4 dh + 4) of output o
     const int pi = t == LV ? a.L : t;
     const DevPrime pr = a.pt.p[pi];
-    const int o = lane & 7, qq = lane >> 3;
-    const u64d* ecp = a.ec + ((size_t)pi * 4 + qq) * 6;
-    const u64d e0 = __ldg(ecp), e0p = __ldg(ecp + 1), e1 = __ldg(ecp + 2), e1p = __ldg(ecp + 3),
-               e2 = __ldg(ecp + 4), e2p = __ldg(ecp + 5);
+    const int o = lane & 15, dh = lane >> 4;
+    const u64d* ecp = a.ec + ((size_t)pi * 2 + dh) * 8;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int h = 0; h < 2; ++h) {
       __syncwarp();
 #pragma unroll
-      for (int n = 0; n < 4; ++n) {
-        const int col = (lane >> 2) * 8 + 2 * (lane & 3);
-        *reinterpret_cast<uint2*>(E + (2 * n) * kHiERow + col) = make_uint2((uint32_t)c[u][n][0], (uint32_t)c[u][n][1]);
-        *reinterpret_cast<uint2*>(E + (2 * n + 1) * kHiERow + col) =
-            make_uint2((uint32_t)c[u][n][2], (uint32_t)c[u][n][3]);
-      }
-      __syncwarp();
-      u64d A[3] = {0, 0, 0};
+      for (int uu = 0; uu < 2; ++uu)
 #pragma unroll
-      for (int ee = 0; ee < 2; ++ee)
-#pragma unroll
-        for (int dq = 0; dq < 2; ++dq) {
-          const uint4 q4 = *reinterpret_cast<const uint4*>(E + o * kHiERow + (2 * qq + ee) * 8 + 4 * dq);
-          const uint32_t cv[4] = {q4.x, q4.y, q4.z, q4.w};
-#pragma unroll
-          for (int dd = 0; dd < 4; ++dd) {
-            const int sp = ee + 4 * dq + dd;  // + 2 qq (applied through the constants)
-            A[sp / 3] += (u64d)cv[dd] << (8 * (sp % 3));
-          }
+        for (int n = 0; n < 4; ++n) {
+          const int o0 = (uu * 4 + n) * 2, col = (lane >> 2) * 8 + 2 * (lane & 3);
+          *reinterpret_cast<uint2*>(E + o0 * kHiERow + col) =
+              make_uint2((uint32_t)c[2 * h + uu][n][0], (uint32_t)c[2 * h + uu][n][1]);
+          *reinterpret_cast<uint2*>(E + (o0 + 1) * kHiERow + col) =
+              make_uint2((uint32_t)c[2 * h + uu][n][2], (uint32_t)c[2 * h + uu][n][3]);
         }
-      // < 6q, then the four quarters' sums mod q
-      u64d sum = shoup_mul_lazy(A[0], e0, e0p, pr.q) + shoup_mul_lazy(A[1], e1, e1p, pr.q) +
-                 shoup_mul_lazy(A[2], e2, e2p, pr.q);
+      __syncwarp();
+      u64d A[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint4 q4 = *reinterpret_cast<const uint4*>(E + o * kHiERow + e * 8 + 4 * dh);
+        const uint32_t cv[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+        for (int dd = 0; dd < 4; ++dd) {
+          const int sp = e + dd;  // + 4 dh (applied through the constants)
+          A[sp / 3] += (u64d)cv[dd] << (8 * (sp % 3));
+        }
+      }
+      u64d sum = 0;  // < 8q
+#pragma unroll
+      for (int g = 0; g < 4; ++g) sum += shoup_mul_lazy(A[g], __ldg(ecp + 2 * g), __ldg(ecp + 2 * g + 1), pr.q);
       sum = shoup_mul_d(sum, 1ull, pr.one_sh, pr.q);
-      sum = add_mod_d(sum, __shfl_xor_sync(0xffffffffu, sum, 8), pr.q);
       sum = add_mod_d(sum, __shfl_xor_sync(0xffffffffu, sum, 16), pr.q);
-      if (qq == 0) {
-        const int n = o >> 1, p = o & 1;
-        const int b = ig * kHiBc + 4 * ng + n, k = half * S + kw + u;
+      if (dh == 0) {
+        const int uu = o >> 3, n = (o >> 1) & 3, p = o & 1;
+        const int b = ig * kHiBc + 4 * ng + n, k = half * S + kw + 2 * h + uu;
         if (b < a.B) {
           u64d* dst = a.acc + ((size_t)b * 2 + p) * (LV + 1) * N + (size_t)t * N + k;
           *dst = a.accumulate ? add_mod_d(sum, *dst, pr.q) : sum;
@@ -237,7 +282,6 @@ __global__ void __launch_bounds__(32 * kHiWarps, 1) k_hs_imma(HiArgs a) {
       }
     }
   }
-  cp_wait<0>();
 }
 
 // A fragments of one chunk: thread = (t, block, local step, group, position, lane)
@@ -303,13 +347,13 @@ __global__ void k_hs_cacc(const u64d* __restrict__ v, const u64d* __restrict__ m
 }
 
 template <int J>
-void hs_imma_go(Context& c, const HiArgs& a, int grid, double bytes, double ops) {
+void hs_imma_go(Context& c, const HiArgs& a, size_t smem, int grid, double bytes, double ops) {
   static bool prepared = false;
   if (!prepared) {
-    CK(cudaFuncSetAttribute(k_hs_imma<J>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHiSmem));
+    CK(cudaFuncSetAttribute(k_hs_imma<J>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHiSmemMax));
     prepared = true;
   }
-  LAUNCH_BO(c, "k_hs_imma", bytes, ops, k_hs_imma<J><<<grid, 32 * kHiWarps, kHiSmem, c.stream>>>(a));
+  LAUNCH_BO(c, "k_hs_imma", bytes, ops, k_hs_imma<J><<<grid, 32 * kHiWarps, smem, c.stream>>>(a));
 }
 
 template <int J>
@@ -326,8 +370,8 @@ void hs_tiles_go(Context& c, const HsDiagTable& t, const u64d* pmod, const int* 
 
 int hs_imma_chunk_span(int l) {
   const int J = l + 1;
-  // ring: NSG + ceil(12 J / 32) + 1 <= kHiRS, NSG = ceil((span J + 31) / 32) + 1
-  const int span = ((kHiRS - 3 - (12 * J + 31) / 32) * 32 - 31) / J;
+  // ring: NSG + ceil(12 J / 32) + 1 <= kHiRSMax, NSG = floor((span J + 62) / 32) + 1
+  const int span = ((kHiRSMax - 2 - (12 * J + 31) / 32) * 32 - 31) / J;
   return span < 128 ? span : 128;
 }
 
@@ -384,6 +428,17 @@ void launch_hs_imma(Context& c, const u64d* v, int B, int l, const u64d* D, cons
   if (strips > T) strips = T;
   a.strips = (int)strips;
   a.accumulate = accumulate;
+  // ring: the block's steps [sfirst(kh0), sfirst(kh0 + 12) + NSG); the rest
+  // of shared memory goes to A-fragment stages
+  a.RS = ch.ns + (12 * J + 31) / 32 + 1;
+  if (a.RS > kHiRSMax) fail(HEGPU_ERR_ARG, "hs_imma: chunk span exceeds the window ring");
+  a.RKP = hi_rkp(a.RS);
+  const size_t fixed = (size_t)kHiCols * a.RKP + kHiEpiBytes;
+  int depth = (int)((kHiSmemMax - 64 - fixed) / (kHiStage * 16));
+  if (depth > kHiMaxDepth) depth = kHiMaxDepth;
+  if (depth < 2) fail(HEGPU_ERR_ARG, "hs_imma: shared memory too small");
+  a.depth = depth;
+  const size_t smem = fixed + (size_t)depth * kHiStage * 16;
   // the chunk's A fragments once, D/c0 windows once per strip (~once), acc
   // written (and read back when accumulating)
   const double NB = 8.0 * N;
@@ -391,12 +446,12 @@ void launch_hs_imma(Context& c, const u64d* v, int B, int l, const u64d* D, cons
   const double ops = (double)N * B * (keyed * l * J * 2.0 + ndiag * l);  // modular MAC terms (as the IMAD path)
   const int grid = (int)(a.nig * strips);
   switch (J) {
-    case 2: hs_imma_go<2>(c, a, grid, bytes, ops); break;
-    case 3: hs_imma_go<3>(c, a, grid, bytes, ops); break;
-    case 4: hs_imma_go<4>(c, a, grid, bytes, ops); break;
-    case 5: hs_imma_go<5>(c, a, grid, bytes, ops); break;
-    case 6: hs_imma_go<6>(c, a, grid, bytes, ops); break;
-    case 7: hs_imma_go<7>(c, a, grid, bytes, ops); break;
+    case 2: hs_imma_go<2>(c, a, smem, grid, bytes, ops); break;
+    case 3: hs_imma_go<3>(c, a, smem, grid, bytes, ops); break;
+    case 4: hs_imma_go<4>(c, a, smem, grid, bytes, ops); break;
+    case 5: hs_imma_go<5>(c, a, smem, grid, bytes, ops); break;
+    case 6: hs_imma_go<6>(c, a, smem, grid, bytes, ops); break;
+    case 7: hs_imma_go<7>(c, a, smem, grid, bytes, ops); break;
     default: fail(HEGPU_ERR_ARG, "hs_imma: level out of range");
   }
 }

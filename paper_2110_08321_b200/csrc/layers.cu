@@ -320,15 +320,15 @@ void HsPlan::ensure_imma(Context& c) {
   ensure_keys(c);
   const int l = level, N = c.N(), S = c.S(), np = c.P->np(), J = l + 1;
   // epilogue constants 2^(24 g + 32 h) mod q with Shoup companions
-  std::vector<u64> ec((size_t)np * 24);
+  std::vector<u64> ec((size_t)np * 16);
   for (int pi = 0; pi < np; ++pi) {
     const u64 q = c.P->q(pi);
-    for (int h = 0; h < 4; ++h)
-      for (int g = 0; g < 3; ++g) {
+    for (int h = 0; h < 2; ++h)
+      for (int g = 0; g < 4; ++g) {
         u128 w = 1;
-        for (int e = 0; e < 24 * g + 16 * h; ++e) w = (w * 2) % q;
-        ec[((size_t)pi * 4 + h) * 6 + 2 * g] = (u64)w;
-        ec[((size_t)pi * 4 + h) * 6 + 2 * g + 1] = (u64)((w << 64) / q);
+        for (int e = 0; e < 24 * g + 32 * h; ++e) w = (w * 2) % q;
+        ec[((size_t)pi * 2 + h) * 8 + 2 * g] = (u64)w;
+        ec[((size_t)pi * 2 + h) * 8 + 2 * g + 1] = (u64)((w << 64) / q);
       }
   }
   std::vector<u64> pm(l);
@@ -342,7 +342,9 @@ void HsPlan::ensure_imma(Context& c) {
   CK(cudaMalloc((void**)&d_rdiag, rd.size() * sizeof(int)));
   CK(cudaMemcpy(d_rdiag, rd.data(), rd.size() * sizeof(int), cudaMemcpyHostToDevice));
   // chunks of kept diagonals whose r span fits the kernel's window ring
-  const int span = hs_imma_chunk_span(l);
+  // balanced: nchunk = ceil(r span / max span) chunks of about equal r span
+  const int smax = hs_imma_chunk_span(l), rtot = (int)(diag.back().right - diag[0].right) + 1;
+  const int nch = (rtot + smax - 1) / smax, span = (rtot + nch - 1) / nch;
   const int first_keyed = diag[0].shift == 0 ? 1 : 0;
   HsDiagTable tab{(int)diag.size(), 0, d_r, fkeys, (size_t)l * 2 * (l + 1) * N, first_keyed, 1, masks, 0, nullptr};
   size_t i = 0;

@@ -340,3 +340,99 @@ def test_cfg3_golden_totals():  # 5680 HOPs, 305 Rot
     spec = H.CnnSpec(in_c=3, in_d=32, k=5, s=2, c_out=32, dense=(256, 10), n_slots=8192)
     tot = np.sum(list(H.golden_stage_tallies(spec).values()), axis=0)
     assert tuple(tot) == (34, 2673, 2666, 2, 305) and tot.sum() == 5680
+
+
+# ---- LoLa comparators (proj/src/matvec.cpp:107-211) -------------------------
+def test_lola_dense_examples():  # test_matvec.cpp:133-155
+    ctx = H.MeterContext()
+    out = H.lola_dense_matvec(np.array([[3.0]]), ct([7], 4), ctx)
+    assert len(out) == 1 and out[0][0] == 21
+    assert ctx.tally.rot == 0
+    rng = np.random.default_rng(9)
+    B = rng.uniform(-1, 1, (5, 8))
+    y = rng.uniform(-1, 1, 8)
+    ctx2 = H.MeterContext()
+    rows = H.lola_dense_matvec(B, H.pack(y, 16, H.CIPHERTEXT), ctx2)
+    want = B @ y
+    for i in range(5):
+        assert abs(rows[i][0] - want[i]) < 1e-9 * max(1, abs(want[i]))
+        assert not np.any(rows[i].slots[1:])  # masked_prefix(1)
+    assert ctx2.tally.rot == 5 * 3 and ctx2.tally.mul_pc == 5
+
+
+def test_predict_lola_dense():  # test_matvec.cpp:157-161
+    assert H.predict_lola_dense(64, 4096)[:2] == (768, 64)
+    assert H.predict_lola_dense(1, 2)[0] == 1
+
+
+def test_lola_stacked_4x3_in_8_slots():  # test_matvec.cpp:163-176
+    rng = np.random.default_rng(17)
+    A = rng.uniform(-1, 1, (4, 3))
+    x = rng.uniform(-1, 1, 3)
+    ctx = H.MeterContext()
+    res, slot_of_row = H.lola_stacked_matvec(A, H.pack(x, 8, H.CIPHERTEXT), ctx)
+    want = A @ x
+    for i in range(4):
+        assert abs(res[slot_of_row[i]] - want[i]) < 1e-9 * max(1, abs(want[i]))
+    assert slot_of_row == [0, 4, 1, 5]
+    assert ctx.tally.rot == 7 and ctx.tally.mul_pc == 2  # 2*(2+2-1)+1
+
+
+def test_predict_lola_stacked():  # test_matvec.cpp:178-185
+    assert H.predict_lola_stacked(64, 4096, 16384)[:2] == (255, 16)
+    assert H.predict_lola_stacked(4, 3, 8)[0] == 7
+    assert H.predict_lola_stacked(4, 16, 64)[0] == 4 + 4 - 1
+    with pytest.raises(H.CapacityError):
+        H.predict_lola_stacked(4, 9, 8)
+
+
+def test_worked_example_formula_figures():  # test_matvec.cpp:187-196 (formula half)
+    assert H.predict_hs(64, 4096, 16384)[:2] == (70, 64)
+    assert H.predict_lola_dense(64, 4096)[0] == 768
+    assert H.predict_lola_stacked(64, 4096, 16384)[:2] == (255, 16)
+
+
+def test_all_kernels_match_naive_on_random_triples():  # test_matvec.cpp:198-220
+    rng = np.random.default_rng(23)
+    for _ in range(150):
+        m = 1 + int(rng.integers(24))
+        n = 1 + int(rng.integers(100))
+        N = H.next_power_of_two(max(m + n - 1, 2))
+        if rng.integers(2):
+            N *= 2
+        A = rng.uniform(-1, 1, (m, n))
+        x = rng.uniform(-1, 1, n)
+        want = A @ x
+        v = H.pack(x, N, H.CIPHERTEXT)
+        ctx = H.MeterContext()
+        hs = H.hs_matvec(A, v, ctx)
+        dn = H.lola_dense_matvec(A, v, ctx)
+        st, sor = H.lola_stacked_matvec(A, v, ctx)
+        for i in range(m):
+            tol = 1e-9 * max(1, abs(want[i]))
+            assert abs(hs[i] - want[i]) < tol
+            assert abs(dn[i][0] - want[i]) < tol
+            assert abs(st[sor[i]] - want[i]) < tol
+
+
+def test_lola_metering_equals_prediction():  # test_matvec.cpp:249-283 (LoLa part, reduced grid)
+    rng = np.random.default_rng(31)
+    for N in (4096, 16384):
+        for n in (16, 64, 256, 1024):
+            for m in (4, 16, 64):
+                A = rng.uniform(-1, 1, (m, n)) + 2.0
+                v = H.pack(rng.uniform(-1, 1, n), N, H.CIPHERTEXT)
+                dn = H.MeterContext()
+                H.lola_dense_matvec(A, v, dn)
+                assert (dn.tally.rot, dn.tally.mul_pc) == H.predict_lola_dense(m, n)[:2]
+                st = H.MeterContext()
+                H.lola_stacked_matvec(A, v, st)
+                assert (st.tally.rot, st.tally.mul_pc) == H.predict_lola_stacked(m, n, N)[:2]
+
+
+def test_figure2_regime_hs_dominates():  # test_matvec.cpp:285-296
+    for N in (4096, 16384):
+        for n in (256, 512, 1024, 2048, 4096):
+            for m in (64, 128, 256, 512):
+                hs = H.predict_hs(m, n, N)[0]
+                assert hs < min(H.predict_lola_dense(m, n)[0], H.predict_lola_stacked(m, n, N)[0])
