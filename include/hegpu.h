@@ -57,6 +57,7 @@ typedef struct hegpu_ctx hegpu_ctx;
 typedef struct hegpu_ct hegpu_ct;
 typedef struct hegpu_pt hegpu_pt;
 typedef struct hegpu_hs_plan hegpu_hs_plan;
+typedef struct hegpu_lola_plan hegpu_lola_plan;
 typedef struct hegpu_net hegpu_net;
 
 #define HEGPU_MAX_Q 15
@@ -208,6 +209,26 @@ int hegpu_hs_matvec_partial(hegpu_ctx* ctx, const hegpu_hs_plan* plan, const heg
                             void* dev_acc);
 int hegpu_hs_matvec_finish(hegpu_ctx* ctx, const hegpu_hs_plan* plan, const hegpu_ct* v, void* dev_acc,
                            int nparts, hegpu_ct* out);
+
+/* ---- LoLa comparators (proj/src/matvec.cpp:107-211) ---------------------- */
+#define HEGPU_LOLA_DENSE 0   /* lola_dense_matvec   (matvec.cpp:107-123) */
+#define HEGPU_LOLA_STACKED 1 /* lola_stacked_matvec (matvec.cpp:125-166) */
+/* row plaintexts + clearing masks encoded once per matrix; input at `level`
+ * (>= 3), outputs at level - 2 (product rescale + the value-level clearing,
+ * done as a 0/1 mask multiply that is not metered, as in the reference);
+ * CapacityError if m or n > S, or (stacked) next_pow2(n) > S */
+int hegpu_lola_plan_create(hegpu_ctx* ctx, int kind, const double* A, int m, int n, int level,
+                           hegpu_lola_plan** out);
+void hegpu_lola_plan_destroy(hegpu_lola_plan* plan);
+int hegpu_lola_plan_rotations(const hegpu_lola_plan* plan, int64_t* rots, int cap);
+/* delta = next_pow2(n), k rows per batch (stacked), batches, folds =
+ * log2(delta), outputs per input ciphertext (dense: m, stacked: 1) */
+int hegpu_lola_plan_info(const hegpu_lola_plan* plan, int* delta, int* k, int* batches, int* folds, int* per_input);
+/* InterleavedResult::slot_of_row (matvec.hpp:32-36); dense rows are slot 0 */
+int64_t hegpu_lola_slot_of_row(const hegpu_lola_plan* plan, int row);
+/* dense: out count = B * m (image-major); stacked: out count = B.  Metering
+ * per input = predict_lola_dense / predict_lola_stacked (matvec.cpp:189-211) */
+int hegpu_lola_matvec(hegpu_ctx* ctx, const hegpu_lola_plan* plan, const hegpu_ct* v, hegpu_ct* out);
 
 /* ---- stage driver: execute (proj/src/netcompile.cpp:291-446) ------------ */
 typedef struct {

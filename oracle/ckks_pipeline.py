@@ -155,3 +155,78 @@ def run_net(ck, cfg, weights, image, nonce=0, keys=None):
     prep = PreparedNet(ck, cfg, weights)
     taps = conv_pack_taps(ck, cfg, image, nonce, prep.tap_scale)
     return prep.eval(taps), prep.out_scale
+
+
+def _key(ck, keys, g):
+    if g not in keys:
+        keys[g] = ck.galois_key(g)
+    return keys[g]
+
+
+def _rotate_and_sum(ck, u, l, delta, keys):
+    """rotate_and_sum(v, delta, 1) (proj/src/matvec.cpp:67-80) at level l"""
+    for t in range(HS._ceil_log2(delta) - 1, -1, -1):
+        g = ck.galois_left(1 << t)
+        u = ck.add(u, ck.rotate(u, l, g, _key(ck, keys, g)), l)
+    return u
+
+
+def lola_dense(ck, v, level, A, keys=None):
+    """lola_dense_matvec (proj/src/matvec.cpp:107-123) on one ciphertext:
+    per row, product with the packed row (scale q_{level-1}) + rescale,
+    rotate_and_sum, then masked_prefix(1) as a mask multiply (scale
+    q_{level-2}) + rescale.  Returns the m output ciphertexts at level-2."""
+    keys = keys if keys is not None else {}
+    A = np.asarray(A, dtype=np.float64)
+    m, n = A.shape
+    S = ck.S
+    delta = HS.next_power_of_two(n)
+    e0 = np.zeros(S)
+    e0[0] = 1.0
+    mask = ck.encode(e0, float(ck.primes[level - 2]), level - 1)
+    outs = []
+    for i in range(m):
+        row = np.zeros(S)
+        row[:n] = A[i]
+        u = ck.rescale(ck.mul_pc(v, ck.encode(row, float(ck.primes[level - 1]), level), level), level)
+        u = _rotate_and_sum(ck, u, level - 1, delta, keys)
+        outs.append(ck.rescale(ck.mul_pc(u, mask, level - 1), level - 1))
+    return np.concatenate(outs)
+
+
+def lola_stacked(ck, v, level, A, keys=None):
+    """lola_stacked_matvec (proj/src/matvec.cpp:125-166) on one ciphertext
+    whose slots >= n are zero (the masked_prefix(n) of the input): stacked =
+    v + sum_j rot_right(v, j delta); per batch the product with the stacked
+    rows + rescale, rotate_and_sum, the segment starts kept by a mask
+    multiply + rescale; res = batch_0 + sum_b rot_right(batch_b, b).
+    Returns (ct at level-2, slot_of_row)."""
+    keys = keys if keys is not None else {}
+    A = np.asarray(A, dtype=np.float64)
+    m, n = A.shape
+    S = ck.S
+    delta = HS.next_power_of_two(n)
+    k = S // delta
+    batches = -(-m // k)
+    stacked = v
+    for j in range(1, k):
+        g = ck.galois_right(j * delta)
+        stacked = ck.add(stacked, ck.rotate(v, level, g, _key(ck, keys, g)), level)
+    res, slot_of_row = None, [0] * m
+    l2 = level - 2
+    for b in range(batches):
+        rows, clean = np.zeros(S), np.zeros(S)
+        for j in range(k):
+            if b * k + j < m:
+                rows[j * delta: j * delta + n] = A[b * k + j]
+                clean[j * delta] = 1.0
+                slot_of_row[b * k + j] = j * delta + b
+        u = ck.rescale(ck.mul_pc(stacked, ck.encode(rows, float(ck.primes[level - 1]), level), level), level)
+        u = _rotate_and_sum(ck, u, level - 1, delta, keys)
+        u = ck.rescale(ck.mul_pc(u, ck.encode(clean, float(ck.primes[level - 2]), level - 1), level - 1), level - 1)
+        if b == 0:
+            res = u
+        else:
+            g = ck.galois_right(b)
+            res = ck.add(res, ck.rotate(u, l2, g, _key(ck, keys, g)), l2)
+    return res, slot_of_row

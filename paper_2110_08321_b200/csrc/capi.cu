@@ -817,3 +817,79 @@ extern "C" int hegpu_hs_matvec(hegpu_ctx* h, const hegpu_hs_plan* p, const hegpu
     c.meter.bump(HEGPU_ADD_CC, B * ((kept > 0 ? kept - 1 : 0) + pl.folds));
   });
 }
+
+// ---- LoLa comparators (proj/src/matvec.cpp:107-211) -------------------------
+struct hegpu_lola_plan {
+  LolaPlan p;
+};
+
+extern "C" int hegpu_lola_plan_create(hegpu_ctx* h, int kind, const double* A, int m, int n, int level,
+                                      hegpu_lola_plan** out) {
+  if (!h || !A || !out) return HEGPU_ERR_ARG;
+  Context& c = h->c;
+  return guarded(&c, [&] {
+    need_gpu(c);
+    need(kind == HEGPU_LOLA_DENSE || kind == HEGPU_LOLA_STACKED, HEGPU_ERR_ARG, "lola: unknown kind");
+    auto* pl = new hegpu_lola_plan();
+    try {
+      pl->p.build(c, kind, A, m, n, level);
+    } catch (...) {
+      delete pl;
+      throw;
+    }
+    *out = pl;
+  });
+}
+
+extern "C" void hegpu_lola_plan_destroy(hegpu_lola_plan* p) {
+  if (!p) return;
+  p->p.release();
+  delete p;
+}
+
+extern "C" int hegpu_lola_plan_rotations(const hegpu_lola_plan* p, int64_t* rots, int cap) {
+  if (!p) return -1;
+  const std::vector<int64_t> r = p->p.right_rotations();
+  for (int i = 0; rots && i < cap && i < (int)r.size(); ++i) rots[i] = r[i];
+  return (int)r.size();
+}
+
+extern "C" int hegpu_lola_plan_info(const hegpu_lola_plan* p, int* delta, int* k, int* batches, int* folds,
+                                    int* per_input) {
+  if (!p) return HEGPU_ERR_ARG;
+  if (delta) *delta = p->p.delta;
+  if (k) *k = p->p.k;
+  if (batches) *batches = p->p.batches;
+  if (folds) *folds = p->p.folds;
+  if (per_input) *per_input = p->p.out_count(1);
+  return HEGPU_OK;
+}
+
+extern "C" int64_t hegpu_lola_slot_of_row(const hegpu_lola_plan* p, int row) {
+  if (!p || row < 0 || row >= p->p.m) return -1;
+  return p->p.slot_of_row(row);
+}
+
+extern "C" int hegpu_lola_matvec(hegpu_ctx* h, const hegpu_lola_plan* p, const hegpu_ct* v, hegpu_ct* out) {
+  if (!h || !p || !v || !out) return HEGPU_ERR_ARG;
+  Context& c = h->c;
+  return guarded(&c, [&] {
+    const LolaPlan& pl = p->p;
+    need(v->b.level == pl.level, HEGPU_ERR_LAYOUT, "lola_matvec: input level does not match the plan");
+    need(out->b.count == pl.out_count(v->b.count) && out->b.level == v->b.level - 2, HEGPU_ERR_SHAPE,
+         "lola_matvec: output must hold out_count ciphertexts at level - 2");
+    need(v != out, HEGPU_ERR_ARG, "lola_matvec: output must not alias the input");
+    const_cast<LolaPlan&>(pl).run(c, v->b, out->b);
+    const int64_t B = v->b.count;
+    if (pl.kind == HEGPU_LOLA_DENSE) {  // predict_lola_dense (matvec.cpp:189-195)
+      c.meter.bump(HEGPU_MUL_PC, B * pl.m);
+      c.meter.bump(HEGPU_ROT, B * pl.m * pl.folds);
+      c.meter.bump(HEGPU_ADD_CC, B * pl.m * pl.folds);
+    } else {  // predict_lola_stacked (matvec.cpp:197-211): the input is re-stacked per batch
+      const int64_t r = (int64_t)pl.batches * (pl.k + pl.folds - 1) + pl.batches - 1;
+      c.meter.bump(HEGPU_MUL_PC, B * pl.batches);
+      c.meter.bump(HEGPU_ROT, B * r);
+      c.meter.bump(HEGPU_ADD_CC, B * r);
+    }
+  });
+}

@@ -78,4 +78,21 @@ struct HsPlan {
   Context* ctx = nullptr;
 };
 
+// LoLa comparators (lola.cu): kind 0 = lola_dense_matvec, 1 = lola_stacked_matvec
+// (proj/src/matvec.cpp:107-166).  Input at `level`, outputs at level - 2:
+// dense -> B * m ciphertexts (image-major, A[i] . x in slot 0), stacked ->
+// B ciphertexts (row i in slot slot_of_row(i)).
+struct LolaPlan {
+  int kind = 0, m = 0, n = 0, level = 0, delta = 1, folds = 0, k = 1, batches = 0;
+  u64d* rows = nullptr;   // [batches][level][N] product plaintexts (scale q_{level-1})
+  u64d* masks = nullptr;  // [1 or batches][level-1][N] clearing masks (scale q_{level-2})
+  void build(Context& c, int kind, const double* A, int m, int n, int level);
+  void release();
+  std::vector<int64_t> right_rotations() const;
+  int out_count(int B) const;
+  int64_t slot_of_row(int i) const;
+  void run(Context& c, const CtBatch& v, CtBatch& out);
+  Context* ctx = nullptr;
+};
+
 }  // namespace hegpu

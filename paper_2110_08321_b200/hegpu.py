@@ -129,6 +129,12 @@ def lib():
             "hegpu_hs_plan_rotations": (i, [vp, vp, i]),
             "hegpu_hs_plan_info": (i, [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i)]),
             "hegpu_hs_matvec": (i, [vp, vp, vp, vp]),
+            "hegpu_lola_plan_create": (i, [vp, i, f64p, i, i, i, pp]),
+            "hegpu_lola_plan_destroy": (None, [vp]),
+            "hegpu_lola_plan_rotations": (i, [vp, vp, i]),
+            "hegpu_lola_plan_info": (i, [vp] + [C.POINTER(i)] * 5),
+            "hegpu_lola_slot_of_row": (C.c_int64, [vp, i]),
+            "hegpu_lola_matvec": (i, [vp, vp, vp, vp]),
             "hegpu_hs_acc_words": (C.c_size_t, [vp, i]),
             "hegpu_hs_matvec_partial": (i, [vp, vp, vp, i, i, vp]),
             "hegpu_hs_matvec_finish": (i, [vp, vp, vp, vp, i, vp]),
@@ -399,6 +405,14 @@ class Context:
         self.check(lib().hegpu_hs_matvec(self.h, plan.h, v.h, out.h))
         return out
 
+    def lola_plan(self, kind, A, level):
+        """kind: "dense" (lola_dense_matvec) or "stacked" (lola_stacked_matvec)"""
+        return LolaPlan(self, kind, A, level)
+
+    def lola_matvec(self, plan, v, out):
+        self.check(lib().hegpu_lola_matvec(self.h, plan.h, v.h, out.h))
+        return out
+
     def hs_acc_words(self, plan, batch):
         return int(lib().hegpu_hs_acc_words(plan.h, batch))
 
@@ -547,6 +561,38 @@ class HsPlan:
         try:
             if self.h:
                 lib().hegpu_hs_plan_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+class LolaPlan:
+    KINDS = {"dense": 0, "stacked": 1}
+
+    def __init__(self, ctx, kind, A, level):
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        self.ctx, self.kind, self.m, self.n, self.level = ctx, kind, A.shape[0], A.shape[1], level
+        h = C.c_void_p()
+        ctx.check(lib().hegpu_lola_plan_create(ctx.h, self.KINDS[kind], A.ravel(), self.m, self.n, level,
+                                               C.byref(h)))
+        self.h = h
+        v = [C.c_int() for _ in range(5)]
+        lib().hegpu_lola_plan_info(h, *[C.byref(x) for x in v])
+        self.delta, self.k, self.batches, self.folds, self.per_input = (x.value for x in v)
+
+    def rotations(self):
+        n = lib().hegpu_lola_plan_rotations(self.h, None, 0)
+        r = np.zeros(max(n, 1), dtype=np.int64)
+        lib().hegpu_lola_plan_rotations(self.h, r.ctypes.data, n)
+        return [int(x) for x in r[:n]]
+
+    def slot_of_row(self):
+        return [int(lib().hegpu_lola_slot_of_row(self.h, i)) for i in range(self.m)]
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().hegpu_lola_plan_destroy(self.h)
                 self.h = None
         except Exception:
             pass

@@ -139,3 +139,27 @@ def test_cfg0_galois_key_bit_exact():
     ctx = H.Context(13, [60, 40, 40, 40, 40, 40], 60, seed=9, device=H.CLIENT_ONLY)
     ck = Ckks(13, [60, 40, 40, 40, 40, 40], 60, seed=9)
     assert np.array_equal(ctx.export_rotation_key(169), ck.galois_key(ck.galois_right(169)))
+
+
+def test_oracle_lola_pipelines_decrypt_to_reference_slots():
+    """the CPU-oracle LoLa compositions (checkers of the GPU LoLa path)
+    decrypt to the reference's slot vectors (proj/src/matvec.cpp:107-166)"""
+    import numpy as np
+    from oracle import ckks_pipeline as P
+    from oracle import hesim_oracle as HS
+    from oracle.ckks import Ckks
+    ck = Ckks(9, [60, 40, 40, 40], 60, seed=5)
+    rng = np.random.default_rng(3)
+    for m, n in ((3, 5), (6, 20)):
+        A = rng.normal(0, 0.3, (m, n))
+        x = rng.uniform(-1, 1, n)
+        v = ck.encrypt(ck.encode(x, 2.0 ** 40, 4), 4, 1)
+        outs = P.lola_dense(ck, v, 4, A).reshape(m, -1)
+        for i in range(m):
+            dec = ck.decrypt_decode(outs[i], 2, 2.0 ** 40)
+            assert abs(dec[0] - A[i] @ x) < 1e-5 and np.abs(dec[1:]).max() < 1e-5
+        res, sor = P.lola_stacked(ck, v, 4, A)
+        ctx = HS.MeterContext()
+        want, sor_ref = HS.lola_stacked_matvec(A, HS.pack(x, ck.S, HS.CIPHERTEXT), ctx)
+        assert sor == sor_ref
+        assert np.abs(ck.decrypt_decode(res, 2, 2.0 ** 40) - want.slots).max() < 1e-5

@@ -252,6 +252,57 @@ def test_hs_matvec_batched_tensor_core(pair, m, n, l, B):
         assert np.abs(dec[:m] - A @ cts[i][0]).max() < 1e-4
 
 
+@pytest.mark.parametrize("kind,m,n,B", [("dense", 1, 1, 1), ("dense", 5, 8, 2), ("dense", 3, 100, 1),
+                                         ("stacked", 4, 3, 1), ("stacked", 12, 100, 2), ("stacked", 3, 200, 1),
+                                         ("stacked", 300, 2, 1)])
+def test_lola_matvec(pair, kind, m, n, B):
+    """lola_dense / lola_stacked (proj/src/matvec.cpp:107-166) on the GPU:
+    limbs == the CPU oracle composition, decrypted slots == the reference's
+    slot vector (A x in slot 0 / at slot_of_row, zeros elsewhere), metering
+    == predict_lola_* per input"""
+    ctx, ck = pair
+    rng = np.random.default_rng(13 * m + n)
+    l = 4
+    A = rng.normal(0, 0.3, (m, n))
+    cts = [fresh(ck, rng, l, 900 + i, n=n) for i in range(B)]
+    plan = ctx.lola_plan(kind, A, l)
+    ctx.gen_rotation_keys(plan.rotations())
+    out = ctx.ct(B * plan.per_input, l - 2)
+    ctx.reset_meter()
+    got = ctx.lola_matvec(plan, ctx.ct(B, l, np.concatenate([c for _, c in cts]), DELTA), out).download()
+    per = plan.per_input
+    got = got.reshape(B, per, -1)
+    N = ck.N
+    if kind == "dense":
+        want = P.lola_dense(ck, cts[-1][1], l, A).reshape(per, -1)
+        assert np.array_equal(got[-1], want)
+        pred = HS.predict_lola_dense(m, n)
+        for b in range(B):
+            for i in range(m):
+                dec = ck.decrypt_decode(got[b][i], l - 2, DELTA)
+                assert abs(dec[0] - A[i] @ cts[b][0]) < 1e-4
+                assert np.abs(dec[1:]).max() < 1e-4
+    else:
+        want, sor = P.lola_stacked(ck, cts[-1][1], l, A)
+        assert np.array_equal(got[-1][0], want)
+        assert plan.slot_of_row() == sor
+        pred = HS.predict_lola_stacked(m, n, ck.S)
+        for b in range(B):
+            dec = ck.decrypt_decode(got[b][0], l - 2, DELTA)
+            ref = np.zeros(ck.S)
+            ref[sor] = A @ cts[b][0]
+            assert np.abs(dec - ref).max() < 1e-4
+    assert ctx.total()[2] == B * pred[1] and ctx.total()[4] == B * pred[0] and ctx.total()[1] == B * pred[2]
+
+
+def test_lola_capacity(pair):
+    ctx, ck = pair
+    with pytest.raises(H.CapacityError):
+        ctx.lola_plan("dense", np.ones((2, ck.S + 1)), 4)
+    with pytest.raises(H.CapacityError):
+        ctx.lola_plan("stacked", np.ones((ck.S + 1, 2)), 4)
+
+
 @pytest.mark.parametrize("m,n,nparts", [(300, 200, 3), (32, 300, 2), (10, 100, 8), (4, 4, 5)])
 def test_hs_matvec_split_partial_sums(pair, m, n, nparts):
     """config-3 style distributed HS: per-part extended-basis accumulators
