@@ -23,16 +23,19 @@ def built():
     B.build()
 
 
-def test_sweep_matches_predict_hs():
+def test_sweep_matches_predictions():
+    """cmd_sweep (hesim.cpp:142-208): all three methods by default"""
     r = cli("sweep", "--n-min", "16", "--n-max", "1024", "--m-min", "4", "--m-max", "256", "--n-slots", "4096,16384")
     assert r.returncode == 0, r.stderr
     lines = r.stdout.strip().splitlines()
     assert lines[0] == "method,n,m,N,rotations,multiplications"
     rows = [l.split(",") for l in lines[1:]]
-    assert len(rows) == 7 * 7 * 2
+    assert len(rows) == 3 * 7 * 7 * 2
+    pred = {"hs": lambda m, n, N: HS.predict_hs(m, n, N), "lola-dense": lambda m, n, N: HS.predict_lola_dense(m, n),
+            "lola-stacked": lambda m, n, N: HS.predict_lola_stacked(m, n, N)}
+    assert [r[0] for r in rows[::98]] == ["hs", "lola-dense", "lola-stacked"]
     for method, n, m, N, rot, mul in rows:
-        assert method == "hs"
-        want = HS.predict_hs(int(m), int(n), int(N))
+        want = pred[method](int(m), int(n), int(N))
         assert (int(rot), int(mul)) == (want[0], want[1])
 
 
@@ -40,7 +43,7 @@ def test_exit_codes_without_gpu():
     assert cli("run", "--model", "/no/such/model.json").returncode == 1   # IoError
     assert cli("count", "--model", "ce").returncode == 2                  # SubConv: outside the path
     assert cli("frobnicate").returncode == 2
-    assert cli("sweep", "--methods", "lola-dense").returncode == 2
+    assert cli("sweep", "--methods", "lola-sparse").returncode == 2
 
 
 @pytest.mark.gpu
@@ -67,3 +70,17 @@ def test_run_count_verify_on_gpu(tmp_path):
     v = cli("verify", "--cases", "3", timeout=1200)
     assert v.returncode == 0, v.stdout + v.stderr
     assert "verify: PASS" in v.stdout
+
+
+@pytest.mark.gpu
+def test_sweep_measure_on_gpu():
+    """sweep --measure (hesim.cpp:119-140): every method runs on the GPU and
+    its metered rotations / multiplications equal the prediction for dense
+    matrices (test_matvec.cpp:249-283)"""
+    r = cli("sweep", "--n-min", "16", "--n-max", "64", "--m-min", "4", "--m-max", "16", "--n-slots", "4096",
+            "--measure")
+    assert r.returncode == 0, r.stderr
+    rows = [l.split(",") for l in r.stdout.strip().splitlines()[1:]]
+    assert len(rows) == 3 * 3 * 3
+    for method, n, m, N, rot, mul, mrot, mmul in rows:
+        assert (mrot, mmul) == (rot, mul), (method, n, m, N)

@@ -220,7 +220,7 @@ std::vector<double> ref_forward(const Model& m, const std::vector<double>& w, co
 }
 
 struct Args {
-  std::string cmd, model, weights, input, report, out, methods = "hs";
+  std::string cmd, model, weights, input, report, out, methods = "hs,lola-dense,lola-stacked";
   uint64_t seed = 0;
   bool seed_set = false, measure = false;
   int cases = 20, n_min = 16, n_max = 4096, m_min = 4, m_max = 512;
@@ -424,53 +424,94 @@ std::pair<int64_t, int64_t> predict_hs(int64_t m, int64_t n, int64_t N) {
   return {me - 1 + folds, me};
 }
 
+// predict_lola_dense / predict_lola_stacked (proj/src/matvec.cpp:189-211)
+std::pair<int64_t, int64_t> predict_lola(bool stacked, int64_t m, int64_t n, int64_t N) {
+  int lg = 0;
+  while ((int64_t{1} << lg) < n) ++lg;
+  if (!stacked) return {m * lg, m};
+  const int64_t delta = int64_t{1} << lg;
+  if (delta > N) throw Fail{kExitCapacity, "stacked: padded width exceeds slot count"};
+  const int64_t k = N / delta, batches = (m + k - 1) / k;
+  return {batches * (k + lg - 1) + batches - 1, batches};
+}
+
+// one kernel call on the GPU with a dense matrix of U[0.5, 1.5] entries
+// (hesim.cpp:119-140): the context's metered rotations / multiplications
+std::pair<int64_t, int64_t> measure_gpu(const std::string& method, int m, int n, int N, uint64_t seed) {
+  const bool hs = method == "hs";
+  const int level = hs ? 2 : 3;
+  Ctx ctx(log2i(2 * N), level, seed + 7);
+  std::mt19937_64 rng(seed ^ ((uint64_t)m << 32) ^ (uint64_t)n ^ ((uint64_t)N << 16));
+  std::uniform_real_distribution<double> dist(0.5, 1.5);
+  std::vector<double> A((size_t)m * n), xv(n);
+  for (auto& v : A) v = dist(rng);
+  for (auto& v : xv) v = dist(rng);
+  hegpu_hs_plan* hp = nullptr;
+  hegpu_lola_plan* lp = nullptr;
+  std::vector<int64_t> rots(4 * (size_t)N + 64);
+  int nr = 0, outs = 1;
+  if (hs) {
+    ctx.ok(hegpu_hs_plan_create(ctx.h, A.data(), m, n, level, 1, &hp));
+    nr = hegpu_hs_plan_rotations(hp, rots.data(), (int)rots.size());
+  } else {
+    ctx.ok(hegpu_lola_plan_create(ctx.h, method == "lola-dense" ? HEGPU_LOLA_DENSE : HEGPU_LOLA_STACKED, A.data(), m,
+                                  n, level, &lp));
+    nr = hegpu_lola_plan_rotations(lp, rots.data(), (int)rots.size());
+    ctx.ok(hegpu_lola_plan_info(lp, nullptr, nullptr, nullptr, nullptr, &outs));
+  }
+  ctx.ok(hegpu_gen_rotation_keys(ctx.h, rots.data(), nr));
+  int nn, slots, L;
+  hegpu_ctx_info(ctx.h, &nn, &slots, &L, nullptr);
+  std::vector<uint64_t> pt((size_t)level * nn), ct((size_t)2 * level * nn);
+  ctx.ok(hegpu_encode(ctx.h, xv.data(), n, std::ldexp(1.0, 40), level, 0, pt.data()));
+  ctx.ok(hegpu_encrypt(ctx.h, pt.data(), level, 1, ct.data()));
+  hegpu_ct *v = nullptr, *o = nullptr;
+  ctx.ok(hegpu_ct_create(ctx.h, 1, level, &v));
+  ctx.ok(hegpu_ct_upload(v, ct.data(), ct.size(), std::ldexp(1.0, 40)));
+  ctx.ok(hegpu_ct_create(ctx.h, outs, hs ? level - 1 : level - 2, &o));
+  ctx.ok(hegpu_reset_meter(ctx.h));
+  if (hs) ctx.ok(hegpu_hs_matvec(ctx.h, hp, v, o));
+  else ctx.ok(hegpu_lola_matvec(ctx.h, lp, v, o));
+  int64_t t[5];
+  ctx.ok(hegpu_total_tally(ctx.h, t));
+  hegpu_ct_destroy(v);
+  hegpu_ct_destroy(o);
+  if (hp) hegpu_hs_plan_destroy(hp);
+  if (lp) hegpu_lola_plan_destroy(lp);
+  return {t[4], t[2]};
+}
+
+// cmd_sweep (proj/tools/hesim.cpp:142-208): predicted (and with --measure,
+// GPU-metered) rotations / multiplications per method, n, m, N
 int cmd_sweep(const Args& a) {
+  std::vector<std::string> methods;
+  {
+    std::stringstream ss(a.methods);
+    std::string m;
+    while (std::getline(ss, m, ','))
+      if (!m.empty()) methods.push_back(m);
+  }
+  for (const auto& m : methods)
+    if (m != "hs" && m != "lola-dense" && m != "lola-stacked") throw Fail{kExitCapacity, "--methods: unknown method " + m};
   std::ostringstream os;
   os << "method,n,m,N,rotations,multiplications";
   if (a.measure) os << ",measured_rotations,measured_multiplications";
   os << "\n";
-  if (a.methods != "hs") throw Fail{kExitCapacity, "--methods: the GPU path implements hs (LoLa is next #3)"};
-  for (int n = a.n_min; n <= a.n_max; n *= 2)
-    for (int m = a.m_min; m <= a.m_max; m *= 2)
-      for (int N : a.slots) {
-        if (n > N || m > N) continue;
-        const auto p = predict_hs(m, n, N);
-        os << "hs," << n << "," << m << "," << N << "," << p.first << "," << p.second;
-        if (a.measure && log2i(2 * N) > 14) {
-          os << ",,";  // ring degree 2N above the device NTT's 2^14
-        } else if (a.measure) {
-          // measured on the GPU: dense matrix (no zero diagonals), one HS
-          Ctx ctx(log2i(2 * N), 2, a.seed + 7);
-          std::mt19937_64 rng(a.seed ^ ((uint64_t)m << 32) ^ (uint64_t)n ^ ((uint64_t)N << 16));
-          std::uniform_real_distribution<double> dist(0.5, 1.5);
-          std::vector<double> A((size_t)m * n), xv(n);
-          for (auto& v : A) v = dist(rng);
-          for (auto& v : xv) v = dist(rng);
-          hegpu_hs_plan* plan = nullptr;
-          ctx.ok(hegpu_hs_plan_create(ctx.h, A.data(), m, n, 2, 1, &plan));
-          std::vector<int64_t> rots(N + 64);
-          const int nr = hegpu_hs_plan_rotations(plan, rots.data(), (int)rots.size());
-          ctx.ok(hegpu_gen_rotation_keys(ctx.h, rots.data(), nr));
-          int nn, slots, L;
-          hegpu_ctx_info(ctx.h, &nn, &slots, &L, nullptr);
-          std::vector<uint64_t> pt((size_t)2 * nn), ct((size_t)4 * nn);
-          ctx.ok(hegpu_encode(ctx.h, xv.data(), n, std::ldexp(1.0, 40), 2, 0, pt.data()));
-          ctx.ok(hegpu_encrypt(ctx.h, pt.data(), 2, 1, ct.data()));
-          hegpu_ct *v = nullptr, *o = nullptr;
-          ctx.ok(hegpu_ct_create(ctx.h, 1, 2, &v));
-          ctx.ok(hegpu_ct_upload(v, ct.data(), ct.size(), std::ldexp(1.0, 40)));
-          ctx.ok(hegpu_ct_create(ctx.h, 1, 1, &o));
-          ctx.ok(hegpu_reset_meter(ctx.h));
-          ctx.ok(hegpu_hs_matvec(ctx.h, plan, v, o));
-          int64_t t[5];
-          ctx.ok(hegpu_total_tally(ctx.h, t));
-          os << "," << t[4] << "," << t[2];
-          hegpu_ct_destroy(v);
-          hegpu_ct_destroy(o);
-          hegpu_hs_plan_destroy(plan);
+  for (const std::string& method : methods)
+    for (int n = a.n_min; n <= a.n_max; n *= 2)
+      for (int m = a.m_min; m <= a.m_max; m *= 2)
+        for (int N : a.slots) {
+          if (n > N || m > N) continue;
+          const auto p = method == "hs" ? predict_hs(m, n, N) : predict_lola(method == "lola-stacked", m, n, N);
+          os << method << "," << n << "," << m << "," << N << "," << p.first << "," << p.second;
+          if (a.measure && log2i(2 * N) > 14) {
+            os << ",,";  // ring degree 2N above the device NTT's 2^14
+          } else if (a.measure) {
+            const auto g = measure_gpu(method, m, n, N, a.seed);
+            os << "," << g.first << "," << g.second;
+          }
+          os << "\n";
         }
-        os << "\n";
-      }
   emit(a.out, os.str());
   return kExitOk;
 }
