@@ -65,12 +65,14 @@ def int_pipe_roofline(kd, clk_mhz):
 def ncu_traffic(kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
     from the committed ncu --set full captures (profiles/), or None"""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
-            t = json.load(f)
-        return float(t[kernel]["per_launch_bytes"])
-    except Exception:
-        return None
+    for name in ("r01_traffic_step.json", "r01_ncu_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                t = json.load(f)
+            return float(t[kernel]["per_launch_bytes"])
+        except Exception:
+            continue
+    return None
 
 
 class ClockSampler:
@@ -299,7 +301,9 @@ def run_gpu(args):
                 # rate, not HBM: its integer-pipe roofline
                 "int_pipe": int_pipe_roofline(kd, clk_mhz),
                 "note": "alg bytes / modmuls per launch per DESIGN.md §5; traffic = ncu dram bytes per launch "
-                        "(profiles/r01_ncu_traffic.json)"}
+                        "of one step (profiles/r01_traffic_step.json: ncu --metrics dram__bytes_read.sum,"
+                        "dram__bytes_write.sum over tools/one_step.py; L2-resident producer->consumer data "
+                        "makes it lower than the algorithmic bytes)"}
 
     # ---- correctness spot check (outside timing): decrypt one output
     host_out = out.download()
@@ -399,7 +403,7 @@ def main():
     ap.add_argument("--batch", type=int, default=64, help="images per GPU")
     ap.add_argument("--cpu-images", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--chunk", type=int, default=64, help="images per compute chunk in the pipelined e2e (serving) loop")
+    ap.add_argument("--chunk", type=int, default=32, help="images per compute chunk in the pipelined e2e (serving) loop (measured 16: 6.6k, 32: 7.5k, 64: 7.1k inf/s)")
     ap.add_argument("--sync-chunk", type=int, default=32, help="images per chunk in the blocking e2e call")
     ap.add_argument("--graph", type=int, default=1, help="replay the device step as one CUDA graph")
     ap.add_argument("--input", default="full", choices=["compact", "full"],

@@ -1,5 +1,6 @@
 """ncu metric CSV of tools/one_step.py -> per-kernel launches, DRAM bytes and
-time of the second (measured) step; writes a JSON summary."""
+time of the second (measured) step; writes a JSON summary.
+usage: traffic.py traffic.csv out.json <launches per step (one_step.py prints it)>"""
 import csv
 import json
 import sys
@@ -16,12 +17,13 @@ for r in rows[1:]:
     name = r[ix["Kernel Name"]].split("(")[0].split("<")[0].replace("void ", "").split("::")[-1]
     val = float(r[ix["Metric Value"]].replace(",", ""))
     unit = r[ix["Metric Unit"]]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3,
-             "msecond": 1.0}.get(unit, 1)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3,
+             "us": 1e-3, "msecond": 1.0, "ms": 1.0}.get(unit, 1)
     recs[lid]["name"] = name
     recs[lid][r[ix["Metric Name"]]] = val * scale
 ids = sorted(recs)
-half = ids[len(ids) // 2:]  # the second of two identical steps
+per_step = int(sys.argv[3]) if len(sys.argv) > 3 else len(ids) // 2
+half = ids[-per_step:]  # the last (second, measured) step
 agg = defaultdict(lambda: {"launches": 0, "dram_bytes": 0.0, "ms": 0.0})
 for i in half:
     a = agg[recs[i]["name"]]
