@@ -199,6 +199,14 @@ def declared_symbols():
                                  text, re.M)))
 
 
+def _ctx_alive(obj):
+    """a handle tied to a context is destroyed only while that context lives
+    (at interpreter shutdown the GC may finalize the context first: the
+    context's teardown already released the device memory)"""
+    ctx = getattr(obj, "ctx", None)
+    return ctx is None or getattr(ctx, "h", None) is not None
+
+
 class Context:
     def __init__(self, log_n, qbits, pbits, seed=1, device=0):
         p = Params()
@@ -437,7 +445,7 @@ class Graph:
 
     def __del__(self):
         try:
-            if self.h:
+            if self.h and _ctx_alive(self):
                 lib().hegpu_graph_destroy(self.h)
                 self.h = None
         except Exception:
@@ -481,7 +489,7 @@ class Ciphertext:
 
     def __del__(self):
         try:
-            if self.h:
+            if self.h and _ctx_alive(self):
                 lib().hegpu_ct_destroy(self.h)
                 self.h = None
         except Exception:
@@ -512,7 +520,7 @@ class Plaintext:
 
     def __del__(self):
         try:
-            if self.h:
+            if self.h and _ctx_alive(self):
                 lib().hegpu_pt_destroy(self.h)
                 self.h = None
         except Exception:
@@ -532,7 +540,7 @@ class ConvPlan:
 
     def __del__(self):
         try:
-            if self.h:
+            if self.h and _ctx_alive(self):
                 lib().hegpu_conv_plan_destroy(self.h)
                 self.h = None
         except Exception:
@@ -559,7 +567,7 @@ class HsPlan:
 
     def __del__(self):
         try:
-            if self.h:
+            if self.h and _ctx_alive(self):
                 lib().hegpu_hs_plan_destroy(self.h)
                 self.h = None
         except Exception:
@@ -591,7 +599,7 @@ class LolaPlan:
 
     def __del__(self):
         try:
-            if self.h:
+            if self.h and _ctx_alive(self):
                 lib().hegpu_lola_plan_destroy(self.h)
                 self.h = None
         except Exception:
@@ -807,7 +815,7 @@ class Net:
 
     def __del__(self):
         try:
-            if self.h:
+            if self.h and _ctx_alive(self):
                 lib().hegpu_net_destroy(self.h)
                 self.h = None
         except Exception:
