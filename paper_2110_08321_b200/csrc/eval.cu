@@ -190,6 +190,44 @@ __global__ void __launch_bounds__(kTpb) k_ks_inner(PrimeTable pt, const u64d* __
   }
 }
 
+// the same with the digit count a template parameter: every load of the
+// thread (LV digit words, 2 LV key words) is issued before the first
+// multiply-accumulate and all addressing is compile-time strided (the
+// runtime-l loop above executed ~680 SASS per output pair at l = 5)
+template <int LV>
+__global__ void __launch_bounds__(kTpb) k_ks_inner_t(PrimeTable pt, const u64d* __restrict__ D, int B, int L, int N,
+                                                     KeyRowMap km, u64d* __restrict__ acc) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.y;
+  const int jkey = blockIdx.z % km.period, row = (blockIdx.z / km.period) * km.period + jkey;
+  if (k >= N || row >= B) return;
+  const int pi = t == LV ? L : t;
+  const DevPrime pr = pt.p[pi];
+  const u64d* key = km.key[jkey] + (size_t)pi * N + k;  // split-31 Montgomery words
+  const size_t kp = (size_t)(L + 1) * N;
+  const u64d* d = D + ((size_t)row * LV * (LV + 1) + t) * N + k;
+  u64d dv[LV], k0[LV], k1[LV];
+#pragma unroll
+  for (int j = 0; j < LV; ++j) {
+    dv[j] = d[(size_t)j * (LV + 1) * N];
+    k0[j] = __ldg(key + (size_t)j * 2 * kp);
+    k1[j] = __ldg(key + (size_t)j * 2 * kp + kp);
+  }
+  HEGPU_KS_ACC a0, a1;
+  a0.zero();
+  a1.zero();
+#pragma unroll
+  for (int j = 0; j < LV; ++j) {
+    const u64d x = split31(dv[j]);
+    a0.mad(x, k0[j]);
+    a1.mad(x, k1[j]);
+    if ((j & 3) == 3 && j + 1 < LV) a0.fold(), a1.fold();
+  }
+  u64d* o = acc + ((size_t)row * 2 * (LV + 1) + t) * N + k;
+  o[0] = a0.reduce(pr);
+  o[(size_t)(LV + 1) * N] = a1.reduce(pr);
+}
+
 // merge inner product, summed over the G rotated maps of each image:
 //   acc[img][p][t] = sum_j sum_d D[img*G + j][d][t] * key_j[d][p][pi(t)]
 __global__ void __launch_bounds__(kTpb) k_ks_inner_sum(PrimeTable pt, const u64d* __restrict__ D, int nimg, int G,
@@ -676,7 +714,18 @@ void ks_inner(Context& c, const u64d* D, int B, int l, const KeyRowMap& keys, u6
     CK(cudaFuncSetAttribute(k_ks_inner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     done = sm;
   }
-  LAUNCH_BO(c, "k_ks_inner", 8.0 * B * (l + 2) * (l + 1) * c.N() + kb, 2.0 * B * l * (l + 1) * c.N(),
+  const double kbytes = 8.0 * B * (l + 2) * (l + 1) * c.N() + kb, kops = 2.0 * B * l * (l + 1) * c.N();
+  if (kKsKT == 1 && !HEGPU_KS_STAGE && l <= 8) {
+#define KSI_GO(LV) \
+  case LV: \
+    LAUNCH_BO(c, "k_ks_inner", kbytes, kops, \
+              k_ks_inner_t<LV><<<grid, kTpb, 0, c.stream>>>(c.primes, D, B, c.L(), c.N(), keys, acc)); \
+    break;
+    switch (l) { KSI_GO(1) KSI_GO(2) KSI_GO(3) KSI_GO(4) KSI_GO(5) KSI_GO(6) KSI_GO(7) KSI_GO(8) }
+#undef KSI_GO
+    return;
+  }
+  LAUNCH_BO(c, "k_ks_inner", kbytes, kops,
            k_ks_inner<<<grid, kTpb, sm, c.stream>>>(c.primes, D, B, l, c.L(), c.N(), keys, acc));
 }
 
