@@ -143,6 +143,16 @@ __device__ __forceinline__ u64d reduce_lazy4(u64d x, const DevPrime& p) {
 __device__ __forceinline__ u64d split31(u64d x) { return (x & 0x7FFFFFFFull) | ((x >> 31) << 32); }
 __device__ __forceinline__ u64d unsplit31(u64d s) { return (s & 0xFFFFFFFFull) + ((s >> 32) << 31); }
 
+// (top:hi:lo) * 2^-64 mod q: h = (top 2^64 + hi) mod q, then one Montgomery
+// reduction of (h:lo).  top is 0 unless a sum of > 8 products of 61-bit
+// operands carried past 2^128 (the rare path).
+__device__ __forceinline__ u64d reduce192(u64d lo, u64d hi, uint32_t top, const DevPrime& pr) {
+  u64d h;
+  if (top) h = mont_mul(mont_reduce128(hi, (u64d)top, pr.q, pr.qneg_inv), pr.r2_mod, pr.q, pr.qneg_inv);
+  else h = shoup_mul_d(hi, 1ull, pr.one_sh, pr.q);
+  return mont_reduce128(lo, h, pr.q, pr.qneg_inv);
+}
+
 struct Acc3 {  // s0 + s1 2^31 + s2 2^62 (partial), folded into lo:hi:top
   u64d s0, s1, s2, lo, hi;
   uint32_t top;
@@ -176,10 +186,7 @@ struct Acc3 {  // s0 + s1 2^31 + s2 2^62 (partial), folded into lo:hi:top
   // (top:hi:lo) * 2^-64 mod q  (products of standard x Montgomery operands)
   __device__ __forceinline__ u64d reduce(const DevPrime& pr) {
     fold();
-    u64d x = mont_reduce128(hi, (u64d)top, pr.q, pr.qneg_inv);
-    x = mont_mul(x, pr.r2_mod, pr.q, pr.qneg_inv);
-    const u64d y = mont_reduce128(lo, 0ull, pr.q, pr.qneg_inv);
-    return add_mod_d(x, y, pr.q);
+    return reduce192(lo, hi, top, pr);
   }
 };
 
@@ -231,10 +238,7 @@ struct AccC {  // as Acc3; s0 + s1 2^31 + s2 2^62 kept as 32-bit halves
   // (top:hi:lo) * 2^-64 mod q  (products of standard x Montgomery operands)
   __device__ __forceinline__ u64d reduce(const DevPrime& pr) {
     fold();
-    u64d x = mont_reduce128(hi, (u64d)top, pr.q, pr.qneg_inv);
-    x = mont_mul(x, pr.r2_mod, pr.q, pr.qneg_inv);
-    const u64d y = mont_reduce128(lo, 0ull, pr.q, pr.qneg_inv);
-    return add_mod_d(x, y, pr.q);
+    return reduce192(lo, hi, top, pr);
   }
 };
 
