@@ -356,7 +356,23 @@ __global__ void NTT_BOUNDS k_ks_modup(TwArgs ta, PrimeTable pt, const u64d* __re
   for (int p = threadIdx.x; p < N; p += blockDim.x) d[p] = sm[pad(__ldg(ta.slot_src + p))];
 }
 
-// drop-limb NTT: rows (b, p, t < nl)
+__device__ __forceinline__ void cp_async16_g2s(u64d* dst, const u64d* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+
+// shared words of the drop-limb kernel: the NTT buffer, then the source limb
+// and the add term of the epilogue (prefetched during the transform)
+// (N <= 2^13: the prefetch buffers fit next to the transform buffer)
+__host__ __device__ constexpr bool drop_prefetch(int N) { return N <= 8192; }
+__host__ __device__ constexpr size_t drop_smem_words(int N) {
+  return ((size_t)(N + (N >> 4) + 1 + 1) & ~(size_t)1) + (drop_prefetch(N) ? 2 * (size_t)N : 0);
+}
+
+// drop-limb NTT: rows (b, p, t < nl).  The epilogue's operands (the source
+// limb and the add term) are copied into shared memory with cp.async while
+// the transform runs, so the epilogue does not wait on HBM.
 template <int LOGN>
 __global__ void NTT_BOUNDS k_drop_ntt(TwArgs ta, PrimeTable pt, const u64d* __restrict__ qinv, int np_all,
                                       DropArgs a, const u64d* __restrict__ tmpP, KeyRowMap km, int use_shift) {
@@ -367,16 +383,34 @@ __global__ void NTT_BOUNDS k_drop_ntt(TwArgs ta, PrimeTable pt, const u64d* __re
   const DevPrime pr = pt.p[t];
   const u64d q = pr.q;
   const u64d qd = pt.p[a.pd].q;
-  fwd_transform<LOGN>(sm, LdLift{tmpP + ((size_t)b * 2 + p) * N, pr, qd, (qd >> 1) >= q}, twf(ta, t, N), q);
-  const u64d iv = qinv[((size_t)t * np_all + a.pd) * 2], ivp = qinv[((size_t)t * np_all + a.pd) * 2 + 1];
   const u64d* in = a.src + b * a.src_b + p * a.src_p + (size_t)t * N;
   u64d* out = a.dst + b * a.dst_b + p * a.dst_p + (size_t)t * N;
   const bool add = (a.add_mask >> p) & 1;
   const u64d* ad = add ? a.add + b * a.add_b + p * a.add_p + (size_t)t * N : nullptr;
+  constexpr bool kPre = drop_prefetch(N);
+  const u64d* in_s = in;
+  const u64d* ad_s = ad;
+  if constexpr (kPre) {
+    u64d* is = sm + (((size_t)N + (N >> 4) + 1 + 1) & ~(size_t)1);
+    u64d* as = is + N;
+    for (int i = threadIdx.x; i < N / 2; i += blockDim.x) {
+      cp_async16_g2s(is + 2 * i, in + 2 * i);
+      if (add) cp_async16_g2s(as + 2 * i, ad + 2 * i);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    in_s = is;
+    ad_s = as;
+  }
+  fwd_transform<LOGN>(sm, LdLift{tmpP + ((size_t)b * 2 + p) * N, pr, qd, (qd >> 1) >= q}, twf(ta, t, N), q);
+  const u64d iv = qinv[((size_t)t * np_all + a.pd) * 2], ivp = qinv[((size_t)t * np_all + a.pd) * 2 + 1];
   const int sh = (use_shift && p == 0) ? km.shift[b % km.period] : 0;
+  if constexpr (kPre) {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+  }
   ROW_LOOP(pos) {
-    u64d v = shoup_mul_d(sub_mod_d(in[pos], sm[pad(__ldg(ta.slot_src + pos))], q), iv, ivp, q);
-    if (add) v = add_mod_d(v, ad[sh ? shifted(pos, sh, S) : pos], q);
+    u64d v = shoup_mul_d(sub_mod_d(in_s[pos], sm[pad(__ldg(ta.slot_src + pos))], q), iv, ivp, q);
+    if (add) v = add_mod_d(v, ad_s[sh ? shifted(pos, sh, S) : pos], q);
     out[pos] = v;
   }
 }
@@ -535,8 +569,26 @@ void NTT_PUB(drop_last_limb)(Context& c, int B, const DropArgs& a, u64d* tmpP) {
   dummy.period = 1;
   // read lifted residue + source limb (+ add term), write the output limb
   const double _ntt_bytes = (24.0 + (a.add ? 8.0 : 0.0)) * N * B * 2 * a.nl;
+#undef NTT_GO
+#define NTT_GO(LG, KERNEL, GRID, ...)                                                               \
+  do {                                                                                              \
+    static bool prepared = false;                                                                   \
+    const size_t smb = drop_smem_words(1 << LG) * 8;                                                \
+    if (!prepared) { prep_kernel(KERNEL<LG>, smb); prepared = true; }                                \
+    LAUNCH_BO(c, #KERNEL, _ntt_bytes, (double)(GRID) * (LG << (LG - 1)),                           \
+              KERNEL<LG><<<(GRID), (1 << LG) >> lr_of(LG), smb, c.stream>>>(__VA_ARGS__));          \
+  } while (0)
   NTT_DISPATCH(c.P->log_n, k_drop_ntt, B * 2 * a.nl, tw_args(c), c.primes, c.qinv_tab(), c.P->np(), a, tmpP,
                a.shifts ? *a.shifts : dummy, a.shifts != nullptr);
+#undef NTT_GO
+#define NTT_GO(LG, KERNEL, GRID, ...)                                                               \
+  do {                                                                                              \
+    static bool prepared = false;                                                                   \
+    const size_t smb = ntt_smem(1 << LG);                                                           \
+    if (!prepared) { prep_kernel(KERNEL<LG>, smb); prepared = true; }                                \
+    LAUNCH_BO(c, #KERNEL, _ntt_bytes, (double)(GRID) * (LG << (LG - 1)),                           \
+              KERNEL<LG><<<(GRID), (1 << LG) >> lr_of(LG), smb, c.stream>>>(__VA_ARGS__));          \
+  } while (0)
 }
 
 #ifndef HEGPU_NTT_R8_VARIANT
