@@ -310,9 +310,21 @@ static int hs_imma_min_batch() {
   return mb;
 }
 
+// narrow diagonal bands (e.g. a 10-row output layer) stay on the integer
+// kernel: the MMA band is too short to amortise the window staging and the
+// byte-plane epilogue (HEGPU_HS_IMMA_MINSPAN, default 32 rotations)
+static int hs_imma_min_span() {
+  static int ms = -1;
+  if (ms < 0) {
+    const char* e = getenv("HEGPU_HS_IMMA_MINSPAN");
+    ms = e ? atoi(e) : 32;
+  }
+  return ms;
+}
+
 bool HsPlan::use_imma(Context& c, int B, int i_lo, int i_hi) const {
   return B >= hs_imma_min_batch() && i_lo == 0 && i_hi == (int)diag.size() && !diag.empty() &&
-         hs_imma_supported(c, level);
+         diag.back().right - diag.front().right + 1 >= hs_imma_min_span() && hs_imma_supported(c, level);
 }
 
 void HsPlan::ensure_imma(Context& c) {
