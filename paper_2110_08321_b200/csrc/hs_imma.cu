@@ -32,12 +32,14 @@ namespace {
 constexpr int kHiWarps = 16;              // 4 position groups x 4 image groups
 constexpr int kHiKB = 16;                 // output positions per block
 constexpr int kHiBc = 16;                 // images per CTA
-constexpr int kHiCols = kHiBc * 8;        // window columns (image, byte plane)
 constexpr int kHiRSMax = 24;              // max ring size in 32-byte k-steps (runtime RS <= this)
 constexpr int kHiMaxDepth = 8;            // A-fragment pipeline stages (runtime D <= this)
 constexpr int kHiStage = 4 * 4 * 32;      // uint4 per stage: 4 position groups x 4 positions x 32 lanes
 constexpr int kHiERow = 68;               // epilogue scratch row (u32): 64 values + pad
+constexpr int kHiE5Row = 44;              // 5-plane epilogue row (u32): 40 columns + pad
+constexpr int kHiE5Rows = 20;             // (position, part, plane e < 5)
 constexpr size_t kHiEpiBytes = (size_t)kHiWarps * 16 * kHiERow * 4;
+constexpr size_t kHiEpi5Bytes = (size_t)kHiWarps * kHiE5Rows * kHiE5Row * 4;
 constexpr size_t kHiSmemMax = 226 * 1024;  // dynamic (227 KB less the static barriers)
 // padded column stride of an RS-step ring (== 16 mod 128: conflict-free ldmatrix)
 __host__ __device__ constexpr int hi_rkp(int rs) { return (32 * rs + 127) / 128 * 128 + 16; }
@@ -49,6 +51,10 @@ __device__ __forceinline__ void mma_u8(int (&c)[4], const uint4& a, uint32_t b0,
       "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
       : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
       : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];\n" : "=r"(r0), "=r"(r1) : "r"(addr));
 }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
@@ -109,6 +115,7 @@ struct HiArgs {
   u64d* acc;          // [B][2][l+1][N]
   int B, L, N, NSG, r_hi, nig, strips, accumulate;
   int RS, RKP, depth;  // ring steps, ring column stride (bytes), pipeline stages
+  int ntl, tl[8];      // the ext-basis limbs this launch covers (one byte-plane class)
 };
 
 // k-step (32 kappa bytes) holding the first kappa of position kh's band
@@ -117,29 +124,39 @@ __device__ __forceinline__ int sfirst(int kh, int r_hi) {
   return floor_div((kh - r_hi) * J, 32);
 }
 
-template <int J>
+// PL = byte planes of the window elements (8; 5 for limbs of primes < 2^40,
+// whose residues have 5 bytes): PL = 8 warps own 4 positions x 4 images
+// (n-tile = one image's 8 planes), PL = 5 warps own 2 positions x 8 images
+// (5 n-tiles of 8 (image, plane) columns)
+template <int J, int PL>
 __global__ void __launch_bounds__(32 * kHiWarps, 1) k_hs_imma(HiArgs a) {
   constexpr int LV = J - 1;
+  constexpr int COLS = kHiBc * PL;
   extern __shared__ __align__(16) uint8_t hi_smem[];
   __shared__ __align__(8) uint64_t bars[2 * kHiMaxDepth];  // full[d], empty[d]
   const int RS = a.RS, RK = 32 * a.RS, RKP = a.RKP, DEP = a.depth;
-  uint8_t* ring = hi_smem;  // [kHiCols][RKP]
-  uint4* astage = reinterpret_cast<uint4*>(hi_smem + (size_t)kHiCols * RKP);  // [DEP][kHiStage]
+  uint8_t* ring = hi_smem;  // [COLS][RKP]
+  uint4* astage = reinterpret_cast<uint4*>(hi_smem + (size_t)COLS * RKP);  // [DEP][kHiStage]
   uint32_t* epi = reinterpret_cast<uint32_t*>(astage + DEP * kHiStage);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mg = warp >> 2, ng = warp & 3;
+  // PL = 8: position group mg (4 positions), images 4 ng ..; PL = 5:
+  // position pair mg (2 positions), images 8 ng ..
+  const int mg = PL == 8 ? warp >> 2 : warp >> 1, ng = PL == 8 ? warp & 3 : warp & 1;
   const int N = a.N, S = N >> 1, bps = S / kHiKB, NSG = a.NSG;
   const int ig = blockIdx.x % a.nig, strip = blockIdx.x / a.nig;
-  const long T = (long)(LV + 1) * 2 * bps;
+  const long T = (long)a.ntl * 2 * bps;
   const long blk0 = T * strip / a.strips, blk1 = T * (strip + 1) / a.strips;
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
   const uint32_t astage_s = (uint32_t)__cvta_generic_to_shared(astage);
-  uint32_t* E = epi + warp * 16 * kHiERow;
+  uint32_t* E = epi + warp * (PL == 8 ? 16 * kHiERow : kHiE5Rows * kHiE5Row);
   // ldmatrix row address of this lane (before the k-step offset): matrix
   // lane/8 = (n-tile pair member, kappa half), row lane%8 = byte plane
   const int lm = lane >> 3, lrow = lane & 7;
-  const uint32_t lbase0 = ring_s + (uint32_t)((4 * ng + (lm >> 1)) * 8 + lrow) * RKP + 16 * (lm & 1);
-  const uint32_t lbase1 = lbase0 + 2 * 8 * RKP;  // n-tiles 2, 3
+  constexpr int NT = PL == 8 ? 4 : 5;  // n-tiles per warp
+  const int nt0 = ng * NT;              // first n-tile of the warp
+  const uint32_t lbase0 = ring_s + (uint32_t)((nt0 + (lm >> 1)) * 8 + lrow) * RKP + 16 * (lm & 1);
+  const uint32_t lbase1 = lbase0 + 2 * 8 * RKP;  // n-tiles +2, +3
+  const uint32_t lbase2 = ring_s + (uint32_t)((nt0 + 4) * 8 + lrow) * RKP + 16 * ((lane >> 3) & 1);  // n-tile +4 (x2)
   const uint32_t full_s = (uint32_t)__cvta_generic_to_shared(bars), empty_s = full_s + 8 * kHiMaxDepth;
   if (threadIdx.x == 0) {
     for (int d = 0; d < DEP; ++d) {
@@ -160,7 +177,7 @@ __global__ void __launch_bounds__(32 * kHiWarps, 1) k_hs_imma(HiArgs a) {
   int cur_seg = -1, st_hi = 0;
   for (long blk = blk0; blk < blk1; ++blk) {
     const int seg = (int)(blk / bps), kb = (int)(blk % bps);
-    const int t = seg >> 1, half = seg & 1, kh0 = kb * kHiKB;
+    const int t = a.tl[seg >> 1], half = seg & 1, kh0 = kb * kHiKB;
     const int lo_s = sfirst<J>(kh0, a.r_hi), hi_s = sfirst<J>(kh0 + kHiKB - 4, a.r_hi) + NSG;
     __syncthreads();  // all warps are done with the previous block's ring
     if (seg != cur_seg) {
@@ -196,22 +213,24 @@ __global__ void __launch_bounds__(32 * kHiWarps, 1) k_hs_imma(HiArgs a) {
         int off = (4 * k4) % RK;
         if (off < 0) off += RK;
 #pragma unroll
-        for (int d = 0; d < 8; ++d)
-          *reinterpret_cast<uint32_t*>(ring + (size_t)(img * 8 + d) * RKP + off) = gather_byte(w, d);
+        for (int d = 0; d < PL; ++d)
+          *reinterpret_cast<uint32_t*>(ring + (size_t)(img * PL + d) * RKP + off) = gather_byte(w, d);
       }
       st_hi = hi_s;
     }
     __syncthreads();  // the window is staged
-    // ---- warp: positions kh0 + 4 mg + u, images ig*16 + 4 ng + n; all
-    // warps walk the same NSG local steps (the group's own first step + ls)
-    const int kw = kh0 + 4 * mg;
-    const int s0 = sfirst<J>(kw, a.r_hi);
-    int c[4][4][4];
+    // ---- warp: PL = 8: positions kh0 + 4 mg + u (u < 4), images ig*16 +
+    // 4 ng + n; PL = 5: positions kh0 + 2 mg + u (u < 2), images ig*16 + 8 ng
+    // + ...; every warp walks the same NSG local steps of its 4-position group
+    constexpr int MT = PL == 8 ? 4 : 2;
+    const int kw = kh0 + MT * mg, grp = PL == 8 ? mg : mg >> 1, u0 = PL == 8 ? 0 : 2 * (mg & 1);
+    const int s0 = sfirst<J>(kh0 + 4 * grp, a.r_hi);
+    int c[MT][NT][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < MT; ++u)
 #pragma unroll
-      for (int n = 0; n < 4; ++n) c[u][n][0] = c[u][n][1] = c[u][n][2] = c[u][n][3] = 0;
-    const uint4* arow = astage + mg * 4 * 32 + lane;
+      for (int n = 0; n < NT; ++n) c[u][n][0] = c[u][n][1] = c[u][n][2] = c[u][n][3] = 0;
+    const uint4* arow = astage + (grp * 4 + u0) * 32 + lane;
     int off = (32 * s0) % RK;
     if (off < 0) off += RK;
     for (int ls = 0; ls < NSG; ++ls) {
@@ -219,66 +238,107 @@ __global__ void __launch_bounds__(32 * kHiWarps, 1) k_hs_imma(HiArgs a) {
       mbar_wait(full_s + 8 * st, cph);
       if (++cst == (uint32_t)DEP) cst = 0, cph ^= 1;
       const uint4* as = arow + st * kHiStage;
-      uint4 ac[4];
+      uint4 ac[MT];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) ac[u] = as[u * 32];
-      uint32_t b0[4], b1[4];
+      for (int u = 0; u < MT; ++u) ac[u] = as[u * 32];
+      uint32_t b0[NT], b1[NT];
       ldsm_x4(lbase0 + off, b0[0], b1[0], b0[1], b1[1]);
       ldsm_x4(lbase1 + off, b0[2], b1[2], b0[3], b1[3]);
+      if constexpr (NT == 5) ldsm_x2(lbase2 + off, b0[4], b1[4]);
       off += 32;
       if (off == RK) off = 0;
       __syncwarp();
       if (lane == 0) mbar_arrive(empty_s + 8 * st);  // this warp is done with the stage
       if (threadIdx.x == 0 && ls + DEP - 1 < NSG) produce(wsrc + (size_t)(ls + DEP - 1) * kHiStage);
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < MT; ++u)
 #pragma unroll
-        for (int n = 0; n < 4; ++n) mma_u8(c[u][n], ac[u], b0[n], b1[n]);
+        for (int n = 0; n < NT; ++n) mma_u8(c[u][n], ac[u], b0[n], b1[n]);
     }
-    // ---- epilogue: two rounds of 2 positions x 4 images x 2 parts = 16
-    // outputs through the warp's scratch; lane (o, dh) combines the byte
-    // planes e < 8, d in [4 dh, 4 dh + 4) of output o
     const int pi = t == LV ? a.L : t;
     const DevPrime pr = a.pt.p[pi];
-    const int o = lane & 15, dh = lane >> 4;
-    const u64d* ecp = a.ec + ((size_t)pi * 2 + dh) * 8;
+    if constexpr (PL == 8) {
+      // ---- epilogue: two rounds of 2 positions x 4 images x 2 parts = 16
+      // outputs through the warp's scratch; lane (o, dh) combines the byte
+      // planes e < 8, d in [4 dh, 4 dh + 4) of output o
+      const int o = lane & 15, dh = lane >> 4;
+      const u64d* ecp = a.ec + ((size_t)pi * 2 + dh) * 8;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      __syncwarp();
+      for (int h = 0; h < 2; ++h) {
+        __syncwarp();
 #pragma unroll
-      for (int uu = 0; uu < 2; ++uu)
+        for (int uu = 0; uu < 2; ++uu)
 #pragma unroll
-        for (int n = 0; n < 4; ++n) {
-          const int o0 = (uu * 4 + n) * 2, col = (lane >> 2) * 8 + 2 * (lane & 3);
-          *reinterpret_cast<uint2*>(E + o0 * kHiERow + col) =
-              make_uint2((uint32_t)c[2 * h + uu][n][0], (uint32_t)c[2 * h + uu][n][1]);
-          *reinterpret_cast<uint2*>(E + (o0 + 1) * kHiERow + col) =
-              make_uint2((uint32_t)c[2 * h + uu][n][2], (uint32_t)c[2 * h + uu][n][3]);
+          for (int n = 0; n < 4; ++n) {
+            const int o0 = (uu * 4 + n) * 2, col = (lane >> 2) * 8 + 2 * (lane & 3);
+            *reinterpret_cast<uint2*>(E + o0 * kHiERow + col) =
+                make_uint2((uint32_t)c[2 * h + uu][n][0], (uint32_t)c[2 * h + uu][n][1]);
+            *reinterpret_cast<uint2*>(E + (o0 + 1) * kHiERow + col) =
+                make_uint2((uint32_t)c[2 * h + uu][n][2], (uint32_t)c[2 * h + uu][n][3]);
+          }
+        __syncwarp();
+        u64d A[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint4 q4 = *reinterpret_cast<const uint4*>(E + o * kHiERow + e * 8 + 4 * dh);
+          const uint32_t cv[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+          for (int dd = 0; dd < 4; ++dd) {
+            const int sp = e + dd;  // + 4 dh (applied through the constants)
+            A[sp / 3] += (u64d)cv[dd] << (8 * (sp % 3));
+          }
         }
-      __syncwarp();
-      u64d A[4] = {0, 0, 0, 0};
+        u64d sum = 0;  // < 8q
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const uint4 q4 = *reinterpret_cast<const uint4*>(E + o * kHiERow + e * 8 + 4 * dh);
-        const uint32_t cv[4] = {q4.x, q4.y, q4.z, q4.w};
-#pragma unroll
-        for (int dd = 0; dd < 4; ++dd) {
-          const int sp = e + dd;  // + 4 dh (applied through the constants)
-          A[sp / 3] += (u64d)cv[dd] << (8 * (sp % 3));
+        for (int g = 0; g < 4; ++g) sum += shoup_mul_lazy(A[g], __ldg(ecp + 2 * g), __ldg(ecp + 2 * g + 1), pr.q);
+        sum = shoup_mul_d(sum, 1ull, pr.one_sh, pr.q);
+        sum = add_mod_d(sum, __shfl_xor_sync(0xffffffffu, sum, 16), pr.q);
+        if (dh == 0) {
+          const int uu = o >> 3, n = (o >> 1) & 3, p = o & 1;
+          const int b = ig * kHiBc + 4 * ng + n, k = half * S + kw + 2 * h + uu;
+          if (b < a.B) {
+            u64d* dst = a.acc + ((size_t)b * 2 + p) * (LV + 1) * N + (size_t)t * N + k;
+            *dst = a.accumulate ? add_mod_d(sum, *dst, pr.q) : sum;
+          }
         }
       }
-      u64d sum = 0;  // < 8q
+    } else {
+      // ---- epilogue (5 planes): the warp's 2 positions x 8 images x 2 parts
+      // = 32 outputs, one per lane; weight planes e >= 5 are zero (q < 2^40)
+      // so only rows e < 5 are kept: scratch [(u, p, e)][40 columns]
+      const int e = lane >> 2;
+      __syncwarp();
+      if (e < 5) {
 #pragma unroll
-      for (int g = 0; g < 4; ++g) sum += shoup_mul_lazy(A[g], __ldg(ecp + 2 * g), __ldg(ecp + 2 * g + 1), pr.q);
-      sum = shoup_mul_d(sum, 1ull, pr.one_sh, pr.q);
-      sum = add_mod_d(sum, __shfl_xor_sync(0xffffffffu, sum, 16), pr.q);
-      if (dh == 0) {
-        const int uu = o >> 3, n = (o >> 1) & 3, p = o & 1;
-        const int b = ig * kHiBc + 4 * ng + n, k = half * S + kw + 2 * h + uu;
-        if (b < a.B) {
-          u64d* dst = a.acc + ((size_t)b * 2 + p) * (LV + 1) * N + (size_t)t * N + k;
-          *dst = a.accumulate ? add_mod_d(sum, *dst, pr.q) : sum;
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int n = 0; n < 5; ++n) {
+            const int col = n * 8 + 2 * (lane & 3);
+            *reinterpret_cast<uint2*>(E + ((u * 2 + 0) * 5 + e) * kHiE5Row + col) =
+                make_uint2((uint32_t)c[u][n][0], (uint32_t)c[u][n][1]);
+            *reinterpret_cast<uint2*>(E + ((u * 2 + 1) * 5 + e) * kHiE5Row + col) =
+                make_uint2((uint32_t)c[u][n][2], (uint32_t)c[u][n][3]);
+          }
+      }
+      __syncwarp();
+      const int u = lane >> 4, img = (lane >> 1) & 7, p = lane & 1;
+      u64d A[3] = {0, 0, 0};
+#pragma unroll
+      for (int ee = 0; ee < 5; ++ee)
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+          const int sp = ee + d;
+          A[sp / 3] += (u64d)E[((u * 2 + p) * 5 + ee) * kHiE5Row + img * 5 + d] << (8 * (sp % 3));
         }
+      const u64d* ecp = a.ec + (size_t)pi * 2 * 8;  // 2^(24 g), g < 3
+      u64d sum = 0;  // < 6q
+#pragma unroll
+      for (int g = 0; g < 3; ++g) sum += shoup_mul_lazy(A[g], __ldg(ecp + 2 * g), __ldg(ecp + 2 * g + 1), pr.q);
+      sum = shoup_mul_d(sum, 1ull, pr.one_sh, pr.q);
+      const int b = ig * kHiBc + 8 * ng + img, k = half * S + kw + u;
+      if (b < a.B) {
+        u64d* dst = a.acc + ((size_t)b * 2 + p) * (LV + 1) * N + (size_t)t * N + k;
+        *dst = a.accumulate ? add_mod_d(sum, *dst, pr.q) : sum;
       }
     }
   }
@@ -346,14 +406,14 @@ __global__ void k_hs_cacc(const u64d* __restrict__ v, const u64d* __restrict__ m
   }
 }
 
-template <int J>
+template <int J, int PL>
 void hs_imma_go(Context& c, const HiArgs& a, size_t smem, int grid, double bytes, double ops) {
   static bool prepared = false;
   if (!prepared) {
-    CK(cudaFuncSetAttribute(k_hs_imma<J>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHiSmemMax));
+    CK(cudaFuncSetAttribute(k_hs_imma<J, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHiSmemMax));
     prepared = true;
   }
-  LAUNCH_BO(c, "k_hs_imma", bytes, ops, k_hs_imma<J><<<grid, 32 * kHiWarps, smem, c.stream>>>(a));
+  LAUNCH_BO(c, "k_hs_imma", bytes, ops, (k_hs_imma<J, PL><<<grid, 32 * kHiWarps, smem, c.stream>>>(a)));
 }
 
 template <int J>
@@ -412,47 +472,57 @@ void launch_hs_imma(Context& c, const u64d* v, int B, int l, const u64d* D, cons
   a.NSG = ch.ns;
   a.r_hi = ch.r_hi;
   a.nig = (B + kHiBc - 1) / kHiBc;
-  const long T = (long)J * 2 * (S / kHiKB);
-  int sms = 148;
-  {
-    static int dev_sms = 0;
-    if (!dev_sms) {
-      int d = 0;
-      CK(cudaGetDevice(&d));
-      CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, d));
-    }
-    sms = dev_sms;
-  }
-  long strips = sms / a.nig;
-  if (strips < 1) strips = 1;
-  if (strips > T) strips = T;
-  a.strips = (int)strips;
   a.accumulate = accumulate;
-  // ring: the block's steps [sfirst(kh0), sfirst(kh0 + 12) + NSG); the rest
-  // of shared memory goes to A-fragment stages
+  static int sms = 0;
+  if (!sms) {
+    int d = 0;
+    CK(cudaGetDevice(&d));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d));
+  }
+  // ring: the block's steps [sfirst(kh0), sfirst(kh0 + 12) + NSG)
   a.RS = ch.ns + (12 * J + 31) / 32 + 1;
   if (a.RS > kHiRSMax) fail(HEGPU_ERR_ARG, "hs_imma: chunk span exceeds the window ring");
   a.RKP = hi_rkp(a.RS);
-  const size_t fixed = (size_t)kHiCols * a.RKP + kHiEpiBytes;
-  int depth = (int)((kHiSmemMax - 64 - fixed) / (kHiStage * 16));
-  if (depth > kHiMaxDepth) depth = kHiMaxDepth;
-  if (depth < 2) fail(HEGPU_ERR_ARG, "hs_imma: shared memory too small");
-  a.depth = depth;
-  const size_t smem = fixed + (size_t)depth * kHiStage * 16;
-  // the chunk's A fragments once, D/c0 windows once per strip (~once), acc
-  // written (and read back when accumulating)
-  const double NB = 8.0 * N;
-  const double bytes = 16.0 * ch.ns * 32 * J * N + NB * B * (l * J + l) + NB * B * 2 * J * (accumulate ? 2 : 1);
-  const double ops = (double)N * B * (keyed * l * J * 2.0 + ndiag * l);  // modular MAC terms (as the IMAD path)
-  const int grid = (int)(a.nig * strips);
-  switch (J) {
-    case 2: hs_imma_go<2>(c, a, smem, grid, bytes, ops); break;
-    case 3: hs_imma_go<3>(c, a, smem, grid, bytes, ops); break;
-    case 4: hs_imma_go<4>(c, a, smem, grid, bytes, ops); break;
-    case 5: hs_imma_go<5>(c, a, smem, grid, bytes, ops); break;
-    case 6: hs_imma_go<6>(c, a, smem, grid, bytes, ops); break;
-    case 7: hs_imma_go<7>(c, a, smem, grid, bytes, ops); break;
-    default: fail(HEGPU_ERR_ARG, "hs_imma: level out of range");
+  // limbs by byte-plane class: residues of primes < 2^40 have 5 bytes
+  std::vector<int> cls[2];  // [0]: 8 planes, [1]: 5 planes
+  for (int t = 0; t <= l; ++t) {
+    const u64 q = c.P->q(t == l ? c.L() : t);
+    cls[q < (1ull << 40) ? 1 : 0].push_back(t);
+  }
+  for (int ci = 0; ci < 2; ++ci) {
+    if (cls[ci].empty()) continue;
+    const int PL = ci ? 5 : 8;
+    a.ntl = (int)cls[ci].size();
+    for (int i = 0; i < a.ntl; ++i) a.tl[i] = cls[ci][i];
+    const long T = (long)a.ntl * 2 * (S / kHiKB);
+    long strips = sms / a.nig;
+    if (strips < 1) strips = 1;
+    if (strips > T) strips = T;
+    a.strips = (int)strips;
+    // the rest of shared memory goes to A-fragment stages
+    const size_t fixed = (size_t)kHiBc * PL * a.RKP + (PL == 8 ? kHiEpiBytes : kHiEpi5Bytes);
+    int depth = (int)((kHiSmemMax - 64 - fixed) / (kHiStage * 16));
+    if (depth > kHiMaxDepth) depth = kHiMaxDepth;
+    if (depth < 2) fail(HEGPU_ERR_ARG, "hs_imma: shared memory too small");
+    a.depth = depth;
+    const size_t smem = fixed + (size_t)depth * kHiStage * 16;
+    // the chunk's A fragments once, D/c0 windows once per strip (~once), acc
+    // written (and read back when accumulating) -- for this launch's limbs
+    const double NB = 8.0 * N, fr = (double)a.ntl / J;
+    const double bytes =
+        fr * (16.0 * ch.ns * 32 * J * N + NB * B * (l * J + l) + NB * B * 2 * J * (accumulate ? 2 : 1));
+    const double ops = fr * (double)N * B * (keyed * l * J * 2.0 + ndiag * l);  // modular MAC terms
+    const int grid = (int)(a.nig * strips);
+#define HI_GO(JJ)                                                               \
+  case JJ:                                                                      \
+    if (PL == 8) hs_imma_go<JJ, 8>(c, a, smem, grid, bytes, ops);               \
+    else hs_imma_go<JJ, 5>(c, a, smem, grid, bytes, ops);                       \
+    break;
+    switch (J) {
+      HI_GO(2) HI_GO(3) HI_GO(4) HI_GO(5) HI_GO(6) HI_GO(7)
+      default: fail(HEGPU_ERR_ARG, "hs_imma: level out of range");
+    }
+#undef HI_GO
   }
 }
 
