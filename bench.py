@@ -54,12 +54,30 @@ IMAD_WIDE_PER_CLK_SM = 59.0
 N_SM = 148
 
 
-def int_pipe_roofline(kd, clk_mhz):
+# integer-pipe cost of one algorithmic op per kernel: a split-31 modular
+# multiply-accumulate term is 4 IMAD.WIDE.U32; an NTT
+# butterfly's Shoup product is 6 multiply instructions (modarith.cuh
+# shoup_mul_lazy4) -- the ceiling if nothing but the multiplies issued
+INT_OPS_IMAD = {"k_hs_diag": 4, "k_ks_inner": 4, "k_drop_ntt": 6, "k_ks_modup": 6, "k_intt_rows": 6,
+                "k_ks_intt": 6, "k_ntt_rows": 6}
+# kernels whose MACs run on IMMA.16832.U8 as 64 byte-plane products each
+TENSOR_KERNELS = ("k_hs_imma", "k_conv_mac")
+IMMA_POPS = 1.1  # measured legacy mma.sync u8 rate on this B200 (tools/ubench_mma.cu)
+
+
+def int_pipe_roofline(name, kd, clk_mhz):
     if not kd.get("modmuls"):
         return None
-    peak = N_SM * IMAD_WIDE_PER_CLK_SM * clk_mhz * 1e6 / 4 / 1e9
-    return {"achieved": kd["gmodmul_s"], "peak": peak, "unit": "Gmodmul/s", "frac": kd["gmodmul_s"] / peak,
-            "peak_basis": f"{N_SM} SMs x {IMAD_WIDE_PER_CLK_SM} IMAD.WIDE.U32/clk/SM x {clk_mhz:.0f} MHz / 4"}
+    if name in TENSOR_KERNELS:
+        ops = kd["modmuls"] * 64 * 2 / (kd["ms_per_step"] / 1e3) / 1e12
+        return {"pipe": "tensor (IMMA u8)", "achieved": ops, "peak": IMMA_POPS * 1e3, "unit": "TOPS (byte-plane)",
+                "frac": ops / (IMMA_POPS * 1e3),
+                "peak_basis": "measured mma.sync m16n8k32 u8 throughput, 64 byte-plane MACs per modular MAC"}
+    per = INT_OPS_IMAD.get(name, 4)
+    peak = N_SM * IMAD_WIDE_PER_CLK_SM * clk_mhz * 1e6 / per / 1e9
+    return {"pipe": "int (IMAD)", "achieved": kd["gmodmul_s"], "peak": peak,
+            "unit": "Gmodmul/s" if per == 4 else "G butterflies/s", "frac": kd["gmodmul_s"] / peak,
+            "peak_basis": f"{N_SM} SMs x {IMAD_WIDE_PER_CLK_SM} IMAD.WIDE.U32/clk/SM x {clk_mhz:.0f} MHz / {per}"}
 
 
 def ncu_traffic(kernel):
@@ -283,6 +301,9 @@ def run_gpu(args):
                              "gbs": kbytes / (kms / 1e3) / 1e9 if kms > 0 else None,
                              "modmuls": kops, "gmodmul_s": kops / (kms / 1e3) / 1e9 if kms > 0 else None,
                              "share": kms / ms_max}
+    clk_mhz = clk.summary()["sm_mhz"] or 1965.0
+    for name, kd in kernels.items():
+        kd["compute_roofline"] = int_pipe_roofline(name, kd, clk_mhz)
     ctx.kernel_timer(None)
     dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
     ntt_rows = sum(kernels[k]["modmuls"] for k in ("k_drop_ntt", "k_ks_modup", "k_intt_rows", "k_ks_intt",
@@ -291,7 +312,6 @@ def run_gpu(args):
     hbm, which = peaks()
     kd = kernels[dom]
     traffic = ncu_traffic(dom)
-    clk_mhz = clk.summary()["sm_mhz"] or 1965.0
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kd["gbs"], "peak": hbm, "unit": "GB/s",
                 "frac": kd["gbs"] / hbm, "traffic": traffic, "peak_source": which,
                 "alg_bytes_per_launch": kd["alg_bytes"] / kd["launches"],
@@ -299,7 +319,7 @@ def run_gpu(args):
                 "share_of_step": kd["share"],
                 # the kernel is bound by the 64-bit multiply-accumulate issue
                 # rate, not HBM: its integer-pipe roofline
-                "int_pipe": int_pipe_roofline(kd, clk_mhz),
+                "int_pipe": int_pipe_roofline(dom, kd, clk_mhz),
                 "note": "alg bytes / modmuls per launch per DESIGN.md §5; traffic = ncu dram bytes per launch "
                         "of one step (profiles/r01_traffic_step.json: ncu --metrics dram__bytes_read.sum,"
                         "dram__bytes_write.sum over tools/one_step.py; L2-resident producer->consumer data "

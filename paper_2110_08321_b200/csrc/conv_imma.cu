@@ -57,14 +57,23 @@ __device__ __forceinline__ void mma_u8(int (&c)[4], const uint4& a, uint32_t b0,
       : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
 }
 
-// a warp: kImmaNT tiles of 8 positions x kImmaCPG map pairs; per k32 step
+// a warp: kImmaNT tiles of 8 positions x kImmaCPG map groups; per k32 step
 // the B fragments of the NT tiles are loaded once and reused by CPG map
-// pairs, each A fragment by NT tiles
+// groups, each A fragment by NT tiles.  MPT = maps per MMA row tile: 2 (rows
+// = map x 8 byte planes e) or, for limbs of primes < 2^40 whose weight
+// digits have 5 bytes, 3 (rows = map x 5 planes, row 15 unused).
+struct ConvLimbs {
+  int n;
+  unsigned long long t;  // the limbs, 4 bits each (a register, not a local array)
+  int stride;            // map groups per limb in the fragment table (the pair count)
+};
+template <int MPT>
 __global__ void __launch_bounds__(32 * kImmaWarps) k_conv_imma(PrimeTable pt, const u64d* __restrict__ taps,
                                                               int ntaps, int l, int N,
                                                               const uint4* __restrict__ wa, int cps, int kbn,
                                                               int c_out, const u64d* __restrict__ bias,
-                                                              u64d* __restrict__ out) {
+                                                              u64d* __restrict__ out, ConvLimbs lim) {
+  constexpr int EP = MPT == 2 ? 8 : 5;  // byte planes per map row block
   extern __shared__ __align__(16) uint4 dyn_smem[];
   // [kImmaDepth][kImmaCPG][32] A fragments, then [kImmaDepth][4 taps][kBRow]
   // tap words of the CTA's positions (rows padded: conflict-free reads)
@@ -73,7 +82,7 @@ __global__ void __launch_bounds__(32 * kImmaWarps) k_conv_imma(PrimeTable pt, co
   // epilogue transpose scratch reuses the pipeline buffers
   auto scratch = reinterpret_cast<int (*)[2][16][9]>(dyn_smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = blockIdx.y % l, poly = blockIdx.y / l;
+  const int t = (int)((lim.t >> (4 * (blockIdx.y % lim.n))) & 15), poly = blockIdx.y / lim.n;
   // the map-pair group varies fastest, so the CTAs reading the same taps
   // run together and the taps come from L2 after the first group
   const int groups = (cps + kImmaCPG - 1) / kImmaCPG;
@@ -90,7 +99,7 @@ __global__ void __launch_bounds__(32 * kImmaWarps) k_conv_imma(PrimeTable pt, co
   for (int j = 0; j < kImmaCPG; ++j)
 #pragma unroll
     for (int n = 0; n < kImmaNT; ++n) c[j][n][0] = c[j][n][1] = c[j][n][2] = c[j][n][3] = 0;
-  const uint4* wt = wa + (size_t)t * cps * kbn * 32;
+  const uint4* wt = wa + (size_t)t * lim.stride * kbn * 32;
   // kImmaDepth-stage cp.async pipeline: A fragments of the CTA's map pairs
   // (shared by its warps) and each lane's own B words
   auto issue = [&](int kb) {
@@ -136,39 +145,69 @@ __global__ void __launch_bounds__(32 * kImmaWarps) k_conv_imma(PrimeTable pt, co
     }
     __syncthreads();  // stage kb may be refilled
   }
-  // epilogue: fragments go through shared memory two at a time; each lane
-  // combines the 8 byte planes of one (map, position) of one fragment
-  const int row = lane >> 2, col = 2 * (lane & 3);
   const DevPrime pr = pt.p[t];
-  const int half = (lane >> 3) & 1, pc = lane & 7, fsel = lane >> 4;
+  const int row = lane >> 2, col = 2 * (lane & 3);
+  if constexpr (MPT == 2) {
+    // epilogue: fragments go through shared memory two at a time; each lane
+    // combines the 8 byte planes of one (map, position) of one fragment
+    const int half = (lane >> 3) & 1, pc = lane & 7, fsel = lane >> 4;
 #pragma unroll
-  for (int f0 = 0; f0 < kImmaCPG * kImmaNT; f0 += 2) {
-    const int j = f0 / kImmaNT;  // fragments f0, f0 + 1 share j (NT even)
-    if (cp0 + j >= cps) break;
-    __syncwarp();
+    for (int f0 = 0; f0 < kImmaCPG * kImmaNT; f0 += 2) {
+      const int j = f0 / kImmaNT;  // fragments f0, f0 + 1 share j (NT even)
+      if (cp0 + j >= cps) break;
+      __syncwarp();
 #pragma unroll
-    for (int f = 0; f < 2; ++f) {
-      const int n = (f0 + f) % kImmaNT;
-      scratch[warp][f][row][col] = c[j][n][0];
-      scratch[warp][f][row][col + 1] = c[j][n][1];
-      scratch[warp][f][row + 8][col] = c[j][n][2];
-      scratch[warp][f][row + 8][col + 1] = c[j][n][3];
-    }
-    __syncwarp();
-    const int co = 2 * (cp0 + j) + half;
-    if (co < c_out) {
-      const int k = kw + 8 * ((f0 + fsel) % kImmaNT) + pc;
-      // + bias R (the stored Montgomery bias) before the reduction
-      u64d lo = (poly == 0 && bias) ? bias[((size_t)co * l + t) * N + k] : 0ull, hi = 0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const u64d v = (u64d)(uint32_t)scratch[warp][fsel][half * 8 + e][pc];
-        const u64d l_add = v << (8 * e), h_add = e ? v >> (64 - 8 * e) : 0ull;
-        asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(l_add), "l"(h_add));
+      for (int f = 0; f < 2; ++f) {
+        const int n = (f0 + f) % kImmaNT;
+        scratch[warp][f][row][col] = c[j][n][0];
+        scratch[warp][f][row][col + 1] = c[j][n][1];
+        scratch[warp][f][row + 8][col] = c[j][n][2];
+        scratch[warp][f][row + 8][col + 1] = c[j][n][3];
       }
-      // (hi:lo) < 2^87 < q 2^64: one Montgomery reduction -> standard form
-      out[((size_t)b * c_out + co) * ct_words + (size_t)poly * l * N + (size_t)t * N + k] =
-          mont_reduce128(lo, hi, pr.q, pr.qneg_inv);
+      __syncwarp();
+      const int co = 2 * (cp0 + j) + half;
+      if (co < c_out) {
+        const int k = kw + 8 * ((f0 + fsel) % kImmaNT) + pc;
+        // + bias R (the stored Montgomery bias) before the reduction
+        u64d lo = (poly == 0 && bias) ? bias[((size_t)co * l + t) * N + k] : 0ull, hi = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const u64d v = (u64d)(uint32_t)scratch[warp][fsel][half * 8 + e][pc];
+          const u64d l_add = v << (8 * e), h_add = e ? v >> (64 - 8 * e) : 0ull;
+          asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(l_add), "l"(h_add));
+        }
+        // (hi:lo) < 2^87 < q 2^64: one Montgomery reduction -> standard form
+        out[((size_t)b * c_out + co) * ct_words + (size_t)poly * l * N + (size_t)t * N + k] =
+            mont_reduce128(lo, hi, pr.q, pr.qneg_inv);
+      }
+    }
+  } else {
+    // epilogue (3 maps x 5 planes): one fragment per round; lanes < 24
+    // combine planes e < 5 of (map lane / 8, position lane % 8)
+    const int m = lane >> 3, pc = lane & 7;
+#pragma unroll
+    for (int f = 0; f < kImmaCPG * kImmaNT; ++f) {
+      const int j = f / kImmaNT, n = f % kImmaNT;
+      if (cp0 + j >= cps) break;
+      __syncwarp();
+      scratch[warp][0][row][col] = c[j][n][0];
+      scratch[warp][0][row][col + 1] = c[j][n][1];
+      scratch[warp][0][row + 8][col] = c[j][n][2];
+      scratch[warp][0][row + 8][col + 1] = c[j][n][3];
+      __syncwarp();
+      const int co = 3 * (cp0 + j) + m;
+      if (m < 3 && co < c_out) {
+        const int k = kw + 8 * n + pc;
+        u64d lo = (poly == 0 && bias) ? bias[((size_t)co * l + t) * N + k] : 0ull, hi = 0;
+#pragma unroll
+        for (int e = 0; e < EP; ++e) {
+          const u64d v = (u64d)(uint32_t)scratch[warp][0][m * 5 + e][pc];
+          const u64d l_add = v << (8 * e), h_add = e ? v >> (64 - 8 * e) : 0ull;
+          asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(l_add), "l"(h_add));
+        }
+        out[((size_t)b * c_out + co) * ct_words + (size_t)poly * l * N + (size_t)t * N + k] =
+            mont_reduce128(lo, hi, pr.q, pr.qneg_inv);
+      }
     }
   }
 }
@@ -177,23 +216,47 @@ __global__ void __launch_bounds__(32 * kImmaWarps) k_conv_imma(PrimeTable pt, co
 
 bool conv_imma_supported(Context& c) { return c.N() % kImmaPos == 0; }
 
-void launch_conv_imma(Context& c, const u64d* taps, int B, int ntaps, int l, const uint32_t* wa, int cps, int kbn,
-                      int c_out, const u64d* bias, u64d* out) {
-  const int N = c.N();
-  const double bytes = 8.0 * N * l * (2.0 * B * ntaps + 2.0 * B * c_out + c_out);
-  const double ops = 2.0 * N * l * B * ntaps * c_out;  // modular MAC terms (as the IMAD path)
-  const uint4* w4 = reinterpret_cast<const uint4*>(wa);
-const int groups = (cps + kImmaCPG - 1) / kImmaCPG;
-  dim3 grid(N / kImmaPos * groups, 2 * l, B);
-  const size_t sm = (size_t)kImmaDepth * (kImmaCPG * 32 * 16 + 4 * kBRow * 4);
+template <int MPT>
+void conv_imma_go(Context& c, dim3 grid, size_t sm, double bytes, double ops, const u64d* taps, int ntaps, int l,
+                  const uint4* w4, int groups_n, int kbn, int c_out, const u64d* bias, u64d* out, const ConvLimbs& lim) {
   static bool prepared = false;
   if (!prepared && sm > 48 * 1024) {
-    CK(cudaFuncSetAttribute(k_conv_imma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(k_conv_imma<MPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     prepared = true;
   }
   LAUNCH_BO(c, "k_conv_mac", bytes, ops,
-            k_conv_imma<<<grid, 32 * kImmaWarps, sm, c.stream>>>(c.primes, taps, ntaps, l, N, w4, cps, kbn, c_out,
-                                                                bias, out));
+            k_conv_imma<MPT><<<grid, 32 * kImmaWarps, sm, c.stream>>>(c.primes, taps, ntaps, l, c.N(), w4, groups_n,
+                                                                     kbn, c_out, bias, out, lim));
 }
+
+void launch_conv_imma(Context& c, const u64d* taps, int B, int ntaps, int l, const uint32_t* wa, int cps, int kbn,
+                      int c_out, const u64d* bias, u64d* out) {
+  const int N = c.N();
+  const uint4* w4 = reinterpret_cast<const uint4*>(wa);
+  const size_t sm = (size_t)kImmaDepth * (kImmaCPG * 32 * 16 + 4 * kBRow * 4);
+  // limbs by weight-digit width: primes < 2^40 pack 3 maps per row tile
+  ConvLimbs lim[2]{};
+  for (int t = 0; t < l; ++t) {
+    ConvLimbs& L = lim[conv_imma_triples(c, t, c_out) ? 1 : 0];
+    L.t |= (unsigned long long)t << (4 * L.n++);
+    L.stride = cps;
+  }
+  for (int k = 0; k < 2; ++k) {
+    if (!lim[k].n) continue;
+    const int groups_n = k ? (c_out + 2) / 3 : cps;
+    const int groups = (groups_n + kImmaCPG - 1) / kImmaCPG;
+    dim3 grid(N / kImmaPos * groups, 2 * lim[k].n, B);
+    const double fr = (double)lim[k].n / l;
+    const double bytes = fr * 8.0 * N * l * (2.0 * B * ntaps + 2.0 * B * c_out + c_out);
+    const double ops = fr * 2.0 * N * l * B * ntaps * c_out;  // modular MAC terms (as the IMAD path)
+    if (k) conv_imma_go<3>(c, grid, sm, bytes, ops, taps, ntaps, l, w4, groups_n, kbn, c_out, bias, out, lim[k]);
+    else conv_imma_go<2>(c, grid, sm, bytes, ops, taps, ntaps, l, w4, groups_n, kbn, c_out, bias, out, lim[k]);
+  }
+}
+
+// (few maps -- cfg 0's 5 -- leave the MAC bound by the tap stream, where the
+// extra epilogue rounds of the triple layout cost more than the MMAs saved:
+// measured 0.552 vs 0.568 ms at 5 maps, 3 % faster cfg 3 at 32 maps)
+bool conv_imma_triples(Context& c, int t, int c_out) { return c_out > 6 && c.P->q(t) < (1ull << 40); }
 
 }  // namespace hegpu

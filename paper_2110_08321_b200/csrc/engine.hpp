@@ -214,6 +214,8 @@ void launch_tensor_square(Context& c, const u64d* a, u64d* d01, u64d* d2, int co
 // pair, 4-tap block and lane the A fragment (uint4) of the byte planes of
 // W * 2^(8i) mod q
 bool conv_imma_supported(Context& c);
+// limb t packs 3 maps x 5 weight-byte planes per MMA row tile (q_t < 2^40)
+bool conv_imma_triples(Context& c, int t, int c_out);
 void launch_conv_imma(Context& c, const u64d* taps, int B, int ntaps, int l, const uint32_t* wa, int cps, int kbn,
                       int c_out, const u64d* bias, u64d* out);
 void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, const u64d* wmont /*[c_out][ntaps][l]*/,

@@ -82,8 +82,13 @@ ConvLayer::ConvLayer(Context& c, int nt, int co_n, const double* weights, const 
           }
         }
     }
+    // limbs of primes < 2^40 (5-byte weight digits) pack rows as 3 maps x 5
+    // planes (row 15 unused; conv_imma.cu MPT = 3), the others 2 maps x 8
     auto byte_at = [&](int li, int row, int col, int cp, int kb) -> uint32_t {
-      const int co = 2 * cp + row / 8, e = row % 8, s = 4 * kb + col / 8, i = col % 8;
+      const bool tri = conv_imma_triples(c, li, c_out);
+      if (tri && row >= 15) return 0u;
+      const int co = tri ? 3 * cp + row / 5 : 2 * cp + row / 8, e = tri ? row % 5 : row % 8;
+      const int s = 4 * kb + col / 8, i = col % 8;
       if (co >= c_out || s >= ntaps) return 0u;
       return (uint32_t)((ws[(((size_t)li * c_out + co) * ntaps + s) * 8 + i] >> (8 * e)) & 0xFF);
     };

@@ -151,29 +151,30 @@ def test_batched_ops_match_per_ciphertext(pair):
         assert np.array_equal(got[i], ck.rescale(ck.square(cts[i], l, rlk), l))
 
 
-def test_conv_packed_forward(pair):
+@pytest.mark.parametrize("c_out", [4, 7, 11])  # 7, 11: the 3-maps-per-tile layout on the 40-bit limbs
+def test_conv_packed_forward(pair, c_out):
     ctx, ck = pair
-    rng = np.random.default_rng(8)
-    # a 1x12x12 image, 3x3 kernel, stride 1 -> d_out 10 (w = 100 slots), 4 maps
-    cfg = type("C", (), dict(in_c=1, in_d=12, k=3, s=1, c_out=4))
+    rng = np.random.default_rng(8 + c_out)
+    # a 1x12x12 image, 3x3 kernel, stride 1 -> d_out 10 (w = 100 slots)
+    cfg = type("C", (), dict(in_c=1, in_d=12, k=3, s=1, c_out=c_out))
     img = rng.uniform(0, 1, (1, 12, 12))
-    W = rng.normal(0, 0.05, (4, 1, 3, 3))
-    bias = rng.normal(0, 0.01, 4)
+    W = rng.normal(0, 0.05, (c_out, 1, 3, 3))
+    bias = rng.normal(0, 0.01, c_out)
     L = ck.L
     taps = P.conv_pack_taps(ck, cfg, img, 3, DELTA)
     dt = ctx.ct(9, L, taps, DELTA)
-    out = ctx.ct(4, L - 1)
+    out = ctx.ct(c_out, L - 1)
     ctx.reset_meter()
-    got = ctx.conv_packed_forward(dt, 9, W.reshape(4, 9), bias, 100, out).download()
-    want = P.conv_layer(ck, taps, 9, L, W.reshape(4, 9), bias, 100, DELTA)
+    got = ctx.conv_packed_forward(dt, 9, W.reshape(c_out, 9), bias, 100, out).download()
+    want = P.conv_layer(ck, taps, 9, L, W.reshape(c_out, 9), bias, 100, DELTA)
     assert np.array_equal(got, want)
-    assert ctx.total() == (4, 32, 36, 0, 0)   # (c_out, (k^2-1) c_out, k^2 c_out, 0, 0)
-    plan = ctx.conv_plan(9, W.reshape(4, 9), bias, 100, L, DELTA)  # prepared once, same result
-    out2 = ctx.ct(4, L - 1)
+    assert ctx.total() == (c_out, 8 * c_out, 9 * c_out, 0, 0)   # (c_out, (k^2-1) c_out, k^2 c_out, 0, 0)
+    plan = ctx.conv_plan(9, W.reshape(c_out, 9), bias, 100, L, DELTA)  # prepared once, same result
+    out2 = ctx.ct(c_out, L - 1)
     assert np.array_equal(ctx.conv_plan_run(plan, dt, out2).download(), want)
     ref = HS.ref_conv(img, W, bias, 1)
     per = 2 * (L - 1) * ck.N
-    for co in range(4):
+    for co in range(c_out):
         dec = ck.decrypt_decode(got[co * per:(co + 1) * per], L - 1, DELTA)
         assert np.abs(dec[:100] - ref[co].ravel()).max() < 1e-6
 
