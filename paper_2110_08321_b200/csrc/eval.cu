@@ -8,6 +8,7 @@
 // CKKS math (hybrid key switch, alpha = 1, one special prime) is fixed in
 // DESIGN.md §3 and restated by oracle/ckks_oracle.c.
 #include <algorithm>
+#include <cstdlib>
 
 #include "engine.hpp"
 
@@ -576,6 +577,61 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
   }
 }
 
+// narrow diagonal bands (a few rotations, e.g. the 10-row output layer):
+// one thread per (image, limb, position) for both key parts, every operand
+// read straight from L1/L2 (consecutive positions -> coalesced; a warp of 32
+// positions x 8 images per CTA shares each fused-key word), no window
+// staging -- the windowed kernel exposed its staging latency at 16 warps/SM
+template <int LV>
+__global__ void __launch_bounds__(256) k_hs_narrow(PrimeTable pt, const u64d* __restrict__ v,
+                                                   const u64d* __restrict__ D, int B, int L, int N, HsDiagTable tab,
+                                                   u64d* __restrict__ acc, u64d* __restrict__ cacc) {
+  const int k = blockIdx.x * 32 + (threadIdx.x & 31), b = blockIdx.y * 8 + (threadIdx.x >> 5), t = blockIdx.z;
+  if (k >= N || b >= B) return;
+  const int S = N >> 1, half = k >= S ? S : 0, kh = k - half;
+  const int pi = t == LV ? L : t;
+  const DevPrime pr = pt.p[pi];
+  const bool has_c = t < LV;
+  const size_t kp = (size_t)(LV + 1) * N;
+  const u64d* Db = D + ((size_t)b * LV * (LV + 1) + t) * N + half;
+  const u64d* c0 = v + (size_t)b * 2 * LV * N + (size_t)t * N + half;
+  AccC a0, a1, cc;
+  a0.zero();
+  a1.zero();
+  cc.zero();
+  int na = 0, nc = 0;
+  const int i0 = __ldg(tab.chunk), i1 = __ldg(tab.chunk + 1);  // absolute diagonal range (one chunk)
+  for (int i = i0; i < i1; ++i) {
+    const int r = __ldg(tab.r + i), pos = (kh - r) & (S - 1);
+    if (r != 0) {
+      const u64d* fk = tab.fk + (size_t)(i - tab.first_keyed) * tab.fk_words + (size_t)t * N + k;
+#pragma unroll
+      for (int j = 0; j < LV; ++j) {
+        const u64d d = split31(Db[(size_t)j * kp + pos]);
+        a0.mad(d, __ldg(fk + (size_t)(j * 2) * kp));
+        a1.mad(d, __ldg(fk + (size_t)(j * 2 + 1) * kp));
+        if (++na == 4) a0.fold(), a1.fold(), na = 0;
+      }
+    }
+    if (has_c) {
+      cc.mad(split31(c0[pos]), __ldg(tab.masks + ((size_t)i * (LV + 1) + t) * N + k));
+      if (++nc == 4) cc.fold(), nc = 0;
+    }
+  }
+  u64d* o = acc + (size_t)b * 2 * kp + (size_t)t * N + k;
+  o[0] = a0.reduce(pr);
+  o[kp] = a1.reduce(pr);
+  if (has_c) {
+    const size_t ln = (size_t)LV * N;
+    u64d* cb = cacc + (size_t)b * 2 * ln + (size_t)t * N + k;
+    cb[0] = cc.reduce(pr);
+    const bool c1_term = tab.own_c1 && tab.ndiag > 0 && __ldg(tab.r) == 0;
+    cb[ln] = c1_term ? mont_mul(v[(size_t)b * 2 * ln + ln + (size_t)t * N + k],
+                                unsplit31(__ldg(tab.masks + (size_t)t * N + k)), pr.q, pr.qneg_inv)
+                     : 0ull;
+  }
+}
+
 // fused key: fk[j][p][t] = key[j][p][pi(t)] * m[t]   (t over the ext basis);
 // key, mask and result are split-31 Montgomery words
 __global__ void k_fuse_key(PrimeTable pt, const u64d* __restrict__ key, const u64d* __restrict__ m, int l, int L,
@@ -779,6 +835,25 @@ void launch_fuse_key(Context& c, const u64d* key, const u64d* mask, int l, u64d*
 
 void launch_hs_diag(Context& c, const u64d* v, int B, int l, const u64d* D, const HsDiagTable& t, u64d* acc,
                     u64d* cacc) {
+  static const int narrow_max = [] {
+    const char* e = getenv("HEGPU_HS_NARROW");
+    return e ? atoi(e) : 16;
+  }();
+  if (t.ndiag <= narrow_max && t.nchunk == 1 && l <= 8) {
+    const int N = c.N();
+    dim3 grid((N + 31) / 32, (B + 7) / 8, l + 1);
+    const double NB = 8.0 * N;
+    const double bytes = NB * (t.keyed * l * 2.0 * (l + 1) + t.ndiag * l + B * (l * (l + 1.0) + 2.0 * l) +
+                               B * (2.0 * (l + 1) + 2.0 * l));
+    const double ops = (double)N * B * (t.keyed * l * (l + 1) * 2.0 + t.ndiag * l);
+#define NARROW_GO(LV)                                                                                        \
+  case LV:                                                                                                   \
+    LAUNCH_BO(c, "k_hs_diag", bytes, ops,                                                                    \
+              k_hs_narrow<LV><<<grid, 256, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc));      \
+    return;
+    switch (l) { NARROW_GO(1) NARROW_GO(2) NARROW_GO(3) NARROW_GO(4) NARROW_GO(5) NARROW_GO(6) NARROW_GO(7) NARROW_GO(8) }
+#undef NARROW_GO
+  }
   switch (l) {
     case 1: launch_hs_lv<1>(c, v, B, D, t, acc, cacc); break;
     case 2: launch_hs_lv<2>(c, v, B, D, t, acc, cacc); break;
