@@ -4,7 +4,7 @@ measures the headline config 2).  One JSON line per measured point.
   python bench_configs.py --config 0   # cfg-0 net, batch 1 (one inference's latency)
   python bench_configs.py --config 1   # HS matvec sweep, N=16384, one rescale
   python bench_configs.py --config 3   # CIFAR-shaped net, N=16384, 5 rescales
-  python bench_configs.py --config 4   # conv-pack layer sweep, N=16384
+  python bench_configs.py --config 4 [--hs]  # conv layer sweep, N=16384 (torchrun: shard by output channel)
 
 Device time with CUDA events on the engine's stream after warm-up; inputs are
 fresh seeded encryptions (synthetic, BASELINE.json shapes/distributions).
@@ -143,40 +143,135 @@ def config3(args, which=3):
         dist.destroy_process_group()
 
 
+def _dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def _ref_conv_map(img, w, b):
+    """FP64 direct convolution of one output map (stride 1), the spot check"""
+    c_in, d_in, _ = img.shape
+    k = w.shape[-1]
+    d_out = d_in - k + 1
+    out = np.full((d_out, d_out), float(b))
+    for ci in range(c_in):
+        for ky in range(k):
+            for kx in range(k):
+                out += w[ci, ky, kx] * img[ci, ky: ky + d_out, kx: kx + d_out]
+    return out.ravel()
+
+
 def config4(args):
-    """BASELINE configs[4]: conv-pack layer sweep, c_in in {1,3,16,32}, 32x32
-    U[0,1] inputs, k in {3,5} (stride 1), c_out in {5,32,64}, N=16384.
-    Reports layers/s and the closed-form HOPs (convlower.cpp:39-74)."""
+    """BASELINE configs[4]: conv-layer sweep, c_in in {1,3,16,32}, 32x32
+    U[0,1] inputs, k in {3,5} (stride 1), c_out in {5,32,64}, N=16384,
+    weights N(0,.05^2).  Conv-pack (convlower.cpp:39-74) sharded by output
+    channel over the ranks of a torchrun job (no collective on the data
+    path; the step time is the max over ranks), HOPs summed over ranks; and
+    the Halevi-Shoup formulation of the same layer (conv_to_matrix +
+    hs_matvec, convlower.cpp:76-102 / matvec.cpp:82-105) where it fits one
+    ciphertext (the reference throws CapacityError elsewhere), its
+    diagonals split over the ranks with an all-reduce of the partial sums."""
+    import torch
+    import torch.distributed as dist
     from paper_2110_08321_b200 import hegpu as H
-    from oracle import hesim_oracle as HS  # only for ref_conv in the spot check
-    ctx = H.Context(14, [60, 40], 60, seed=4)
+    from paper_2110_08321_b200 import dist as Dm
+    from paper_2110_08321_b200.workloads import conv_as_matrix, conv_pack_image
+    rank, world, local = _dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    ctx = H.Context(14, [60, 40], 60, seed=4, device=local)
     rng = np.random.default_rng(4)
+
+    def tmax(ms):
+        return Dm.max_over_ranks(ms, device=f"cuda:{local}")
+
     for c_in in (1, 3, 16, 32):
         img = rng.uniform(0, 1, (c_in, 32, 32))
         for k in (3, 5):
             d_out = 32 - k + 1
             ntaps = k * k * c_in
-            shape = HS.ConvShape(32, c_in, k, 1, 1)
-            taps = HS.conv_pack(img, shape, ctx.S)
-            cts = np.concatenate([ctx.encrypt(ctx.encode(t.slots[: d_out * d_out], DELTA, 2), 2, i)
-                                  for i, t in enumerate(taps)])
+            taps = conv_pack_image(img, k)
+            cts = np.concatenate([ctx.encrypt(ctx.encode(t, DELTA, 2), 2, i) for i, t in enumerate(taps)])
             dt = ctx.ct(ntaps, 2, cts, DELTA)
             for c_out in (5, 32, 64):
                 W = rng.normal(0, 0.05, (c_out, c_in, k, k))
                 b = rng.normal(0, 0.01, c_out)
-                out = ctx.ct(c_out, 1)
-                plan = ctx.conv_plan(ntaps, W.reshape(c_out, -1), b, d_out * d_out, 2, DELTA)  # offline
-                ctx.reset_meter()
-                ctx.conv_plan_run(plan, dt, out)
-                tally = ctx.total()
-                ms = timed(ctx, lambda: ctx.conv_plan_run(plan, dt, out), args.steps, args.warmup)
-                # spot check: decrypt map 0 against the FP64 reference conv
-                want = HS.ref_conv(img, W[:1], b[:1], 1)[0].ravel()
-                got = ctx.decode(ctx.decrypt(out.download()[: 2 * ctx.N], 1), 1, DELTA)[: d_out * d_out]
-                print(json.dumps({
-                    "config": 4, "c_in": c_in, "k": k, "c_out": c_out, "ms_per_layer": ms,
-                    "layers_per_s": 1e3 / ms, "hops": dict(zip(H.TALLY_FIELDS, tally)),
-                    "max_abs_err_vs_ref_conv": float(np.abs(got - want).max())}), flush=True)
+                lo, hi = c_out * rank // world, c_out * (rank + 1) // world  # this rank's output channels
+                line = {"config": 4, "c_in": c_in, "k": k, "c_out": c_out, "n_gpus": world,
+                        "sharding": "output channels"}
+                if hi > lo:
+                    out = ctx.ct(hi - lo, 1)
+                    plan = ctx.conv_plan(ntaps, W[lo:hi].reshape(hi - lo, -1), b[lo:hi], d_out * d_out, 2, DELTA)
+                    ctx.reset_meter()
+                    ctx.conv_plan_run(plan, dt, out)
+                    tally = np.array(ctx.total(), dtype=np.int64)
+                    ms = timed(ctx, lambda: ctx.conv_plan_run(plan, dt, out), args.steps, args.warmup)
+                    err = 0.0
+                    if rank == 0:  # spot check: map 0 against the FP64 direct conv
+                        got = ctx.decode(ctx.decrypt(out.download()[: 2 * ctx.N], 1), 1, DELTA)[: d_out * d_out]
+                        err = float(np.abs(got - _ref_conv_map(img, W[0], b[0])).max())
+                else:
+                    tally, ms, err = np.zeros(5, dtype=np.int64), 0.0, 0.0
+                ms = tmax(ms)
+                if world > 1:
+                    tt = torch.tensor(tally, device=f"cuda:{local}")
+                    dist.all_reduce(tt)
+                    tally = tt.cpu().numpy()
+                line.update({"ms_per_layer": ms, "layers_per_s": 1e3 / ms,
+                             "hops": dict(zip(H.TALLY_FIELDS, [int(x) for x in tally])),
+                             "max_abs_err_vs_ref_conv": err})
+                if args.hs and c_in * 32 * 32 <= ctx.S:
+                    line["hs"] = hs_formulation(ctx, W, b, img, world, rank, local, args)
+                if rank == 0:
+                    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def hs_formulation(ctx, W, b, img, world, rank, local, args):
+    """the conv layer as one HS matvec (conv_to_matrix), if it fits"""
+    import torch
+    from paper_2110_08321_b200 import hegpu as H
+    from paper_2110_08321_b200 import dist as Dm
+    from paper_2110_08321_b200.workloads import conv_as_matrix
+    A = conv_as_matrix(W, 32)
+    try:
+        t0 = time.perf_counter()
+        plan = ctx.hs_plan(A, 2)
+    except H.CapacityError as e:
+        return {"capacity_error": str(e)}
+    ctx.gen_rotation_keys(plan.rotations())
+    setup_s = time.perf_counter() - t0
+    x = img.ravel()
+    v = ctx.ct(1, 2, ctx.encrypt(ctx.encode(x, DELTA, 2), 2, 99), DELTA)
+    out = ctx.ct(1, 1)
+    if world > 1:
+        words = ctx.hs_acc_words(plan, 1)
+        part = torch.empty(words, dtype=torch.int64, device=f"cuda:{local}")
+
+        def run():
+            ctx.hs_matvec_partial(plan, v, rank, world, part)
+            ctx.sync()
+            Dm.reduce_partials(part, world)
+            ctx.hs_matvec_finish(plan, v, part, world, out)
+    else:
+        def run():
+            ctx.hs_matvec(plan, v, out)
+    ctx.reset_meter()
+    run()
+    tally = ctx.total()
+    ms = Dm.max_over_ranks(timed(ctx, run, args.steps, args.warmup), device=f"cuda:{local}")
+    rot = tally[4] if world == 1 else None
+    res = {"m": A.shape[0], "n": A.shape[1], "m_eff": plan.m_eff, "kept_diagonals": plan.kept,
+           "folds": plan.folds, "ms": ms, "setup_s": setup_s}
+    if world == 1:
+        res.update({"rotations": int(tally[4]), "mul_pc": int(tally[2]), "rotations_per_s": tally[4] / (ms / 1e3)})
+        if rank == 0:
+            want = A @ x + 0.0
+            got = ctx.decode(ctx.decrypt(out.download(), 1), 1, DELTA)[: A.shape[0]]
+            res["max_abs_err_vs_ref"] = float(np.abs(got - want).max())
+    return res
 
 
 def main():
@@ -187,6 +282,8 @@ def main():
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--dims", default="64,256,1024,4096", help="config 1 matrix dims (m and n)")
     ap.add_argument("--split-hs", action="store_true", help="config 3 under torchrun: split HS1 across ranks")
+    ap.add_argument("--hs", action="store_true",
+                    help="config 4: also run the Halevi-Shoup formulation where it fits one ciphertext")
     args = ap.parse_args()
     {0: config0, 1: config1, 3: config3, 4: config4}[args.config](args)
 

@@ -328,8 +328,12 @@ static int hs_imma_min_span() {
 }
 
 bool HsPlan::use_imma(Context& c, int B, int i_lo, int i_hi) const {
-  return B >= hs_imma_min_batch() && i_lo == 0 && i_hi == (int)diag.size() && !diag.empty() &&
-         diag.back().right - diag.front().right + 1 >= hs_imma_min_span() && hs_imma_supported(c, level);
+  if (diag.empty()) return false;
+  const int64_t span = diag.back().right - diag.front().right + 1;
+  // dense bands only: the fragments cover the whole rotation span (a sparse
+  // band -- e.g. a convolution's matrix -- would store mostly zero tiles)
+  return B >= hs_imma_min_batch() && i_lo == 0 && i_hi == (int)diag.size() && span >= hs_imma_min_span() &&
+         4 * (int64_t)diag.size() >= span && hs_imma_supported(c, level);
 }
 
 void HsPlan::ensure_imma(Context& c) {

@@ -90,3 +90,36 @@ def hs_sweep_case(m: int, n: int, seed: int = 0):
     """BASELINE.json configs[1]: A ~ N(0, 0.05^2) (m x n), v ~ U[-1, 1]^n."""
     rng = np.random.default_rng(np.random.SeedSequence([seed, m, n]))
     return f32(rng.normal(0.0, 0.05, (m, n))), f32(rng.uniform(-1.0, 1.0, n))
+
+
+# ---- client-side cleartext packing for the conv sweep (config 4) ----------
+def conv_pack_image(image, k, s=1):
+    """conv_pack (proj/src/convlower.cpp:9-37) on the client: tap t = (ci k +
+    ky) k + kx holds img[ci, oy s + ky, ox s + kx] at slot oy d_out + ox"""
+    image = np.asarray(image, dtype=np.float64)
+    c_in, d_in = image.shape[0], image.shape[1]
+    d_out = (d_in - k) // s + 1
+    taps = []
+    for ci in range(c_in):
+        for ky in range(k):
+            for kx in range(k):
+                taps.append(image[ci, ky: ky + s * (d_out - 1) + 1: s, kx: kx + s * (d_out - 1) + 1: s].ravel())
+    return taps
+
+
+def conv_as_matrix(weights, d_in, s=1):
+    """conv_to_matrix (proj/src/convlower.cpp:76-102): the conv as a
+    (d_out^2 c_out) x (d_in^2 c_in) matrix for the HS formulation"""
+    weights = np.asarray(weights, dtype=np.float64)
+    c_out, c_in, k, _ = weights.shape
+    d_out = (d_in - k) // s + 1
+    A = np.zeros((d_out * d_out * c_out, d_in * d_in * c_in))
+    oy, ox = np.meshgrid(np.arange(d_out), np.arange(d_out), indexing="ij")
+    for co in range(c_out):
+        rows = (co * d_out + oy) * d_out + ox
+        for ci in range(c_in):
+            for ky in range(k):
+                for kx in range(k):
+                    cols = (ci * d_in + oy * s + ky) * d_in + ox * s + kx
+                    A[rows.ravel(), cols.ravel()] += weights[co, ci, ky, kx]
+    return A

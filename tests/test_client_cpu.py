@@ -163,3 +163,21 @@ def test_oracle_lola_pipelines_decrypt_to_reference_slots():
         want, sor_ref = HS.lola_stacked_matvec(A, HS.pack(x, ck.S, HS.CIPHERTEXT), ctx)
         assert sor == sor_ref
         assert np.abs(ck.decrypt_decode(res, 2, 2.0 ** 40) - want.slots).max() < 1e-5
+
+
+def test_workload_conv_helpers_match_the_oracle():
+    """the client-side packing helpers used by bench_configs (config 4)
+    equal the oracle's conv_pack / conv_to_matrix restatements"""
+    import numpy as np
+    from oracle import hesim_oracle as HS
+    from paper_2110_08321_b200.workloads import conv_as_matrix, conv_pack_image
+    rng = np.random.default_rng(2)
+    img = rng.uniform(0, 1, (3, 9, 9))
+    W = rng.normal(0, 1, (4, 3, 3, 3))
+    for s in (1, 2):
+        shape = HS.ConvShape(9, 3, 3, s, 4)
+        taps = HS.conv_pack(img, shape, 64)
+        mine = conv_pack_image(img, 3, s)
+        w = shape.d_out() ** 2
+        assert all(np.array_equal(t.slots[:w], m) for t, m in zip(taps, mine))
+        assert np.array_equal(HS.conv_to_matrix(shape, W), conv_as_matrix(W, 9, s))
