@@ -43,10 +43,21 @@ def timed(ctx, fn, steps, warmup):
 def config1(args):
     """BASELINE configs[1]: m x n in {64,256,1024,4096}^2, A ~ N(0,.05^2),
     v ~ U[-1,1]^n, N=16384, Q={60,40}, one rescale.  Reports rotations/s
-    (key-switched, HS metering) and the fused-HS kernel's achieved GB/s."""
+    (key-switched, HS metering) and the HS kernel's achieved GB/s.  Under
+    torchrun with --split-hs the kept diagonals are split over the ranks
+    (per-rank extended-basis partial sums, one NCCL
+    all-reduce, ModDown/rescale/folds on every rank; strong scaling)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2110_08321_b200 import dist as Dm
     from paper_2110_08321_b200 import hegpu as H
     from paper_2110_08321_b200.workloads import hs_sweep_case
-    ctx = H.Context(14, [60, 40], 60, seed=1)
+    rank, world, local = _dist_env()
+    split = args.split_hs and world > 1
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    ctx = H.Context(14, [60, 40], 60, seed=1, device=local)
     dims = [int(x) for x in args.dims.split(",")]
     for m in dims:
         for n in dims:
@@ -59,24 +70,49 @@ def config1(args):
                 pt = ctx.encode(x, DELTA, 2)
                 v = ctx.ct(B, 2, np.concatenate([ctx.encrypt(pt, 2, 7 + i) for i in range(B)]), DELTA)
                 out = ctx.ct(B, 1)
-                ctx.hs_matvec(plan, v, out)  # first run fuses keys x masks (offline)
+                if split:
+                    part = torch.empty(ctx.hs_acc_words(plan, B), dtype=torch.int64, device=f"cuda:{local}")
+
+                    def run():
+                        ctx.hs_matvec_partial(plan, v, rank, world, part)
+                        ctx.sync()
+                        Dm.reduce_partials(part, world)
+                        ctx.hs_matvec_finish(plan, v, part, world, out)
+                else:
+                    def run():
+                        ctx.hs_matvec(plan, v, out)
+                run()  # first run fuses keys x masks (offline)
                 ctx.reset_meter()
-                ctx.hs_matvec(plan, v, out)
-                tally = ctx.total()
-                ms = timed(ctx, lambda: ctx.hs_matvec(plan, v, out), args.steps, args.warmup)
-                ctx.kernel_timer("k_hs_diag")
-                ctx.hs_matvec(plan, v, out)
-                kms, _, kbytes = ctx.kernel_timer_read()
+                run()
+                tally = np.array(ctx.total(), dtype=np.int64)
+                ms = Dm.max_over_ranks(timed(ctx, run, args.steps, args.warmup), device=f"cuda:{local}")
+                if split:
+                    tt = torch.tensor(tally, device=f"cuda:{local}")
+                    dist.all_reduce(tt)
+                    tally = tt.cpu().numpy()
+                    tally[1] -= (world - 1) * B * plan.folds  # the folds run on every rank,
+                    tally[4] -= (world - 1) * B * plan.folds  # the reference meters them once
+                kms = kbytes = 0.0
+                for kern in ("k_hs_diag", "k_hs_imma"):
+                    ctx.kernel_timer(kern)
+                    run()
+                    a, _, b_ = ctx.kernel_timer_read()
+                    kms, kbytes = kms + a, kbytes + b_
                 ctx.kernel_timer(None)
-                rot = tally[4]
-                print(json.dumps({
-                    "config": 1, "m": m, "n": n, "batch": B, "ms_per_matvec_batch": ms,
-                    "matvecs_per_s": B / (ms / 1e3), "rotations_per_s": rot / (ms / 1e3),
-                    "rotations_per_matvec": rot // B, "mul_pc_per_matvec": tally[2] // B,
-                    "m_eff": plan.m_eff, "folds": plan.folds,
-                    "hs_diag_ms": kms, "hs_diag_gbs": kbytes / (kms / 1e3) / 1e9 if kms else None,
-                    "setup_s": setup_s}), flush=True)
+                rot = int(tally[4])
+                if rank == 0:
+                    print(json.dumps({
+                        "config": 1, "m": m, "n": n, "batch": B, "n_gpus": world,
+                        "mode": "split-diagonals" if split else "single",
+                        "ms_per_matvec_batch": ms,
+                        "matvecs_per_s": B / (ms / 1e3), "rotations_per_s": rot / (ms / 1e3),
+                        "rotations_per_matvec": rot // B, "mul_pc_per_matvec": int(tally[2]) // B,
+                        "m_eff": plan.m_eff, "folds": plan.folds,
+                        "hs_kernel_ms": kms, "hs_kernel_gbs": kbytes / (kms / 1e3) / 1e9 if kms else None,
+                        "setup_s": setup_s}), flush=True)
             del plan
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def config0(args):
@@ -281,7 +317,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--dims", default="64,256,1024,4096", help="config 1 matrix dims (m and n)")
-    ap.add_argument("--split-hs", action="store_true", help="config 3 under torchrun: split HS1 across ranks")
+    ap.add_argument("--split-hs", action="store_true",
+                    help="configs 1 / 3 under torchrun: split the (first) HS layer's diagonals across ranks")
     ap.add_argument("--hs", action="store_true",
                     help="config 4: also run the Halevi-Shoup formulation where it fits one ciphertext")
     args = ap.parse_args()
