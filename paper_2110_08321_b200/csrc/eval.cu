@@ -272,6 +272,44 @@ __global__ void __launch_bounds__(kTpb) k_ks_inner_sum(PrimeTable pt, const u64d
   }
 }
 
+// the merge inner sum with the digit count a template parameter (loads of
+// one rotation issued together, compile-time strides)
+template <int LV>
+__global__ void __launch_bounds__(kTpb) k_ks_inner_sum_t(PrimeTable pt, const u64d* __restrict__ D, int nimg, int G,
+                                                         int L, int N, KeyRowMap km, u64d* __restrict__ acc) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.y, img = blockIdx.z;
+  if (k >= N || img >= nimg) return;
+  const int pi = t == LV ? L : t;
+  const DevPrime pr = pt.p[pi];
+  const size_t kp = (size_t)(L + 1) * N;
+  HEGPU_KS_ACC a0, a1;
+  a0.zero();
+  a1.zero();
+  int cnt = 0;
+  for (int j = 0; j < G; ++j) {
+    const u64d* key = km.key[j] + (size_t)pi * N + k;
+    const u64d* d = D + (((size_t)img * G + j) * LV * (LV + 1) + t) * N + k;
+    u64d dv[LV], k0[LV], k1[LV];
+#pragma unroll
+    for (int q = 0; q < LV; ++q) {
+      dv[q] = d[(size_t)q * (LV + 1) * N];
+      k0[q] = __ldg(key + (size_t)q * 2 * kp);
+      k1[q] = __ldg(key + (size_t)q * 2 * kp + kp);
+    }
+#pragma unroll
+    for (int q = 0; q < LV; ++q) {
+      const u64d x = split31(dv[q]);
+      a0.mad(x, k0[q]);
+      a1.mad(x, k1[q]);
+      if (++cnt == 4) a0.fold(), a1.fold(), cnt = 0;
+    }
+  }
+  u64d* o = acc + ((size_t)img * 2 * (LV + 1) + t) * N + k;
+  o[0] = a0.reduce(pr);
+  o[(size_t)(LV + 1) * N] = a1.reduce(pr);
+}
+
 // merge Q-basis part: C0 = map_0.c0 + sum_j sigma_j(map_j.c0), C1 = map_0.c1
 __global__ void k_merge_c(PrimeTable pt, const u64d* __restrict__ maps, int nimg, int c, int l, int N,
                           KeyRowMap km, u64d* __restrict__ C) {
@@ -913,9 +951,21 @@ void eval_merge(Context& c, const CtBatch& maps, int nmaps, const KeyRowMap& km,
   kg.grp_stride = (long)(nmaps * st);
   ks_modup(c, maps.d + st + (size_t)l * N, (long)st, B * G, l, &kg, tmp, D);
   dim3 gi((N + kTpb - 1) / kTpb, l + 1, (B + kKsKT - 1) / kKsKT);
-  LAUNCH_BO(c, "k_ks_inner", 8.0 * N * ((double)B * G * l * (l + 1) + 2.0 * G * l * (l + 1) + 2.0 * B * (l + 1)),
-            2.0 * N * B * G * l * (l + 1),
-           k_ks_inner_sum<<<gi, kTpb, 0, c.stream>>>(c.primes, D, B, G, l, c.L(), N, km, acc));
+  const double sbytes = 8.0 * N * ((double)B * G * l * (l + 1) + 2.0 * G * l * (l + 1) + 2.0 * B * (l + 1));
+  const double sops = 2.0 * N * B * G * l * (l + 1);
+  if (kKsKT == 1 && l <= 8) {
+    dim3 gt((N + kTpb - 1) / kTpb, l + 1, B);
+#define KSS_GO(LV) \
+  case LV: \
+    LAUNCH_BO(c, "k_ks_inner", sbytes, sops, \
+              k_ks_inner_sum_t<LV><<<gt, kTpb, 0, c.stream>>>(c.primes, D, B, G, c.L(), N, km, acc)); \
+    break;
+    switch (l) { KSS_GO(1) KSS_GO(2) KSS_GO(3) KSS_GO(4) KSS_GO(5) KSS_GO(6) KSS_GO(7) KSS_GO(8) }
+#undef KSS_GO
+  } else {
+    LAUNCH_BO(c, "k_ks_inner", sbytes, sops,
+              k_ks_inner_sum<<<gi, kTpb, 0, c.stream>>>(c.primes, D, B, G, l, c.L(), N, km, acc));
+  }
   dim3 gc((N + kTpb - 1) / kTpb, 2 * l, B);
   LAUNCH_B(c, "k_merge_c", 8.0 * N * ((double)B * (nmaps + 1) * l + 2.0 * B * l),
            k_merge_c<<<gc, kTpb, 0, c.stream>>>(c.primes, maps.d, B, nmaps, l, N, km, C));
