@@ -3,6 +3,7 @@ measures the headline config 2).  One JSON line per measured point.
 
   python bench_configs.py --config 0   # cfg-0 net, batch 1 (one inference's latency)
   python bench_configs.py --config 1   # HS matvec sweep, N=16384, one rescale
+  python bench_configs.py --config 1 --method lola   # the LoLa comparators on the same grid
   python bench_configs.py --config 3   # CIFAR-shaped net, N=16384, 5 rescales
   python bench_configs.py --config 4 [--hs]  # conv layer sweep, N=16384 (torchrun: shard by output channel)
 
@@ -113,6 +114,47 @@ def config1(args):
             del plan
     if world > 1:
         dist.destroy_process_group()
+
+
+def config1_lola(args):
+    """The LoLa comparators of Fig. 2 on config 1's grid (measured, not
+    predicted): lola_dense / lola_stacked (matvec.cpp:107-166) on one
+    ciphertext (and a batch), N=16384, Q={60,40,40} (two rescales: product
+    + the value-level clearing).  Reports rotations/s next to the metered
+    counts, which equal predict_lola_* (matvec.cpp:189-211)."""
+    from paper_2110_08321_b200 import hegpu as H
+    from paper_2110_08321_b200.workloads import hs_sweep_case
+    ctx = H.Context(14, [60, 40, 40], 60, seed=1)
+    dims = [int(x) for x in args.dims.split(",")]
+    for kind in ("dense", "stacked"):
+        for m in dims:
+            for n in dims:
+                A, x = hs_sweep_case(m, n)
+                try:
+                    t0 = time.perf_counter()
+                    plan = ctx.lola_plan(kind, A, 3)
+                    ctx.gen_rotation_keys(plan.rotations())
+                    setup_s = time.perf_counter() - t0
+                except H.CapacityError as e:
+                    print(json.dumps({"config": 1, "method": "lola-" + kind, "m": m, "n": n,
+                                      "capacity_error": str(e)}), flush=True)
+                    continue
+                for B in sorted({1, args.batch}):
+                    if B * plan.batches > 8192:  # products in flight (dense: m per input) at ~0.8 MB each
+                        continue
+                    pt = ctx.encode(x, DELTA, 3)
+                    v = ctx.ct(B, 3, np.concatenate([ctx.encrypt(pt, 3, 7 + i) for i in range(B)]), DELTA)
+                    out = ctx.ct(B * plan.per_input, 1)
+                    ctx.reset_meter()
+                    ctx.lola_matvec(plan, v, out)
+                    tally = ctx.total()
+                    ms = timed(ctx, lambda: ctx.lola_matvec(plan, v, out), args.steps, args.warmup)
+                    print(json.dumps({
+                        "config": 1, "method": "lola-" + kind, "m": m, "n": n, "batch": B,
+                        "ms_per_matvec_batch": ms, "matvecs_per_s": B / (ms / 1e3),
+                        "rotations_per_s": tally[4] / (ms / 1e3), "rotations_per_matvec": tally[4] // B,
+                        "mul_pc_per_matvec": tally[2] // B, "setup_s": setup_s}), flush=True)
+                del plan
 
 
 def config0(args):
@@ -313,6 +355,8 @@ def hs_formulation(ctx, W, b, img, world, rank, local, args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, required=True, choices=[0, 1, 3, 4])
+    ap.add_argument("--method", default="hs", choices=["hs", "lola"],
+                    help="config 1: the HS matvec (default) or the two LoLa comparators")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--batch", type=int, default=16)
@@ -322,6 +366,8 @@ def main():
     ap.add_argument("--hs", action="store_true",
                     help="config 4: also run the Halevi-Shoup formulation where it fits one ciphertext")
     args = ap.parse_args()
+    if args.config == 1 and args.method == "lola":
+        return config1_lola(args)
     {0: config0, 1: config1, 3: config3, 4: config4}[args.config](args)
 
 
