@@ -25,9 +25,30 @@ def hs_masks(ck, A, level, skip_zero=True):
     return m_eff, folds, rots, (np.concatenate(enc) if enc else np.zeros(0, dtype=np.uint64))
 
 
+def fold_rotations(S, m_eff, folds):
+    """the log-depth fold s += rot_left(s, m_eff 2^t), t = folds-1 .. 0
+    (proj/src/matvec.cpp:101-103) sums rot_left(s, m_eff u) over u <
+    2^folds; as right rotations, ascending (0 first)"""
+    return sorted({(S - (m_eff * u) % S) % S for u in range(1 << folds)})
+
+
+def fold_sum(ck, u, l, m_eff, folds, key):
+    """the fold as ONE hoisted rotation sum: one ModUp of u.c1, 2^folds - 1
+    key-switch inner products on the rotated digits, one ModDown (the HS
+    machinery with unit masks) -- the same slots as the serial folds,
+    metered as the reference's `folds` rotations"""
+    if folds == 0:
+        return u
+    rots = fold_rotations(ck.S, m_eff, folds)
+    ones = np.ones(len(rots) * (l + 1) * ck.N, dtype=np.uint64)
+    kl = [key(ck.galois_right(r)) for r in rots if r != 0]
+    return ck.hs_hoisted(u, l, np.array(rots, dtype=np.int64), ones, np.concatenate(kl))
+
+
 def hs_matvec(ck, v, level, A, skip_zero=True, keys=None):
     """Oracle HS layer: hoisted diagonal sum, rescale, log-depth fold
-    (proj/src/matvec.cpp:82-105).  Returns ct at level-1."""
+    (proj/src/matvec.cpp:82-105) as one hoisted rotation sum.  Returns ct at
+    level-1."""
     m_eff, folds, rots, masks = hs_masks(ck, A, level, skip_zero)
     keys = keys if keys is not None else {}
 
@@ -40,11 +61,7 @@ def hs_matvec(ck, v, level, A, skip_zero=True, keys=None):
     kbuf = np.concatenate(kl) if kl else np.zeros(1, dtype=np.uint64)
     u = ck.hs_hoisted(v, level, np.array(rots, dtype=np.int64), masks, kbuf)
     u = ck.rescale(u, level)
-    l = level - 1
-    for t in range(folds - 1, -1, -1):
-        g = ck.galois_left(m_eff << t)
-        u = ck.add(u, ck.rotate(u, l, g, key(g)), l)
-    return u
+    return fold_sum(ck, u, level - 1, m_eff, folds, key)
 
 
 def conv_layer(ck, taps, ntaps, level, weights, bias, w_used, tap_scale):
@@ -123,11 +140,13 @@ class PreparedNet:
             m_eff, folds, rots, masks = hs_masks(ck, np.asarray(W), l, True)
             kl = [key(ck.galois_right(r)) for r in rots if r != 0]
             kbuf = np.concatenate(kl) if kl else np.zeros(1, dtype=np.uint64)
-            fold_keys = [(ck.galois_left(m_eff << t), key(ck.galois_left(m_eff << t)))
-                         for t in range(folds - 1, -1, -1)]
+            frots = fold_rotations(ck.S, m_eff, folds) if folds else [0]
+            fkl = [key(ck.galois_right(r)) for r in frots if r != 0]
+            fold = (np.array(frots, dtype=np.int64), np.ones(len(frots) * l * ck.N, dtype=np.uint64),
+                    np.concatenate(fkl) if fkl else None)
             l -= 1
             bias = ck.encode(np.asarray(b), scale, l)
-            self.layers.append((l + 1, np.array(rots, dtype=np.int64), masks, kbuf, fold_keys, bias))
+            self.layers.append((l + 1, np.array(rots, dtype=np.int64), masks, kbuf, fold, bias))
         self.out_scale = scale
 
     def eval(self, taps):
@@ -138,13 +157,13 @@ class PreparedNet:
         maps = np.concatenate([ck.rescale(maps[co * per:(co + 1) * per], L) for co in range(cfg.c_out)])
         l = L - 1
         x = ck.merge(maps, cfg.c_out, l, self.w_used, self.merge_keys)
-        for lv, rots, masks, kbuf, fold_keys, bias in self.layers:
+        for lv, rots, masks, kbuf, fold, bias in self.layers:
             x = ck.rescale(ck.square(x, l, self.rlk), l)
             l = lv
             u = ck.rescale(ck.hs_hoisted(x, l, rots, masks, kbuf), l)
             l -= 1
-            for g, k in fold_keys:
-                u = ck.add(u, ck.rotate(u, l, g, k), l)
+            if fold[2] is not None:  # the folds as one hoisted rotation sum
+                u = ck.hs_hoisted(u, l, fold[0], fold[1], fold[2])
             x = ck.add_pc(u, bias, l)
         return x
 

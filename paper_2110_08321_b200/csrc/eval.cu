@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(256) k_hs_narrow(PrimeTable pt, const u64d* __
   a1.zero();
   cc.zero();
   int na = 0, nc = 0;
-  const int i0 = __ldg(tab.chunk), i1 = __ldg(tab.chunk + 1);  // absolute diagonal range (one chunk)
+  const int i0 = __ldg(tab.chunk), i1 = __ldg(tab.chunk + tab.nchunk);  // absolute diagonal range
   for (int i = i0; i < i1; ++i) {
     const int r = __ldg(tab.r + i), pos = (kh - r) & (S - 1);
     if (r != 0) {
@@ -875,9 +875,9 @@ void launch_hs_diag(Context& c, const u64d* v, int B, int l, const u64d* D, cons
                     u64d* cacc) {
   static const int narrow_max = [] {
     const char* e = getenv("HEGPU_HS_NARROW");
-    return e ? atoi(e) : 16;
+    return e ? atoi(e) : 32;
   }();
-  if (t.ndiag <= narrow_max && t.nchunk == 1 && l <= 8) {
+  if (t.ndiag <= narrow_max && l <= 8) {
     const int N = c.N();
     dim3 grid((N + 31) / 32, (B + 7) / 8, l + 1);
     const double NB = 8.0 * N;

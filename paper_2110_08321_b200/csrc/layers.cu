@@ -1,6 +1,7 @@
 // layers.cu -- conv-pack, merge, square and Halevi-Shoup layers on the
 // CKKS engine (reference semantics: proj/src/convlower.cpp:39-74,141-160,
 // proj/src/matvec.cpp:45-105).
+#include <algorithm>
 #include <cmath>
 #include <string>
 
@@ -256,6 +257,8 @@ void HsPlan::build(Context& c, const double* A, int m_, int n_, int lvl, bool sk
 
 void HsPlan::release() {
   if (ctx) cudaStreamSynchronize(ctx->stream);
+  if (fold) fold->release();
+  fold.reset();
   cudaFree(masks);
   cudaFree(d_r);
   cudaFree(d_chunk);
@@ -275,13 +278,55 @@ void HsPlan::release() {
   fkeys = nullptr;
 }
 
+std::vector<int64_t> HsPlan::fold_rights() const {
+  // s += rot_left(s, m_eff 2^t) for t = folds-1..0 sums rot_left(s, m_eff u)
+  // over u < 2^folds (distinct: m_eff 2^folds <= S in both branches)
+  const int64_t S = ctx->S();
+  std::vector<int64_t> r;
+  if (folds > 0)
+    for (int64_t u = 0; u < (int64_t{1} << folds); ++u) r.push_back((S - (m_eff * u) % S) % S);
+  std::sort(r.begin(), r.end());
+  return r;
+}
+
 std::vector<int64_t> HsPlan::right_rotations() const {
   std::vector<int64_t> r;
   for (const HsDiag& d : diag)
     if (d.right) r.push_back(d.right);
-  const int S = ctx->S();
-  for (int t = folds - 1; t >= 0; --t) r.push_back((S - (((int64_t)m_eff << t) % S)) % S);
+  for (int64_t f : fold_rights())
+    if (f) r.push_back(f);  // the fold's hoisted rotations
   return r;
+}
+
+void HsPlan::build_rotsum(Context& c, const std::vector<int64_t>& rights, int lvl) {
+  ctx = &c;
+  level = lvl;
+  m = n = m_eff = 0;
+  folds = 0;
+  const int S = c.S(), N = c.N(), nl = level + 1;
+  for (int64_t r : rights) diag.push_back(HsDiag{(int)diag.size(), r, (int)((S - r) % S)});
+  // unit masks: Montgomery 1 = 2^64 mod q per limb (limb `level` is P), split-31
+  std::vector<u64> mk(diag.size() * (size_t)nl * N);
+  for (int t = 0; t < nl; ++t) {
+    const u64 q = c.P->q(t == level ? c.L() : t);
+    const u64 one = (u64)(((u128)1 << 64) % q);
+    const u64 sp = (one & 0x7FFFFFFFull) | ((one >> 31) << 32);
+    for (size_t i = 0; i < diag.size(); ++i) std::fill_n(mk.data() + (i * nl + t) * N, N, sp);
+  }
+  CK(cudaMalloc((void**)&masks, mk.size() * 8));
+  CK(cudaMemcpy(masks, mk.data(), mk.size() * 8, cudaMemcpyHostToDevice));
+  std::vector<int> r(diag.size()), chunk{0};
+  for (size_t i = 0; i < diag.size(); ++i) {
+    r[i] = (int)diag[i].right;
+    if (i > 0 && r[i] - r[chunk.back()] >= hs_chunk_span()) chunk.push_back((int)i);
+  }
+  chunk.push_back((int)diag.size());
+  nchunk = (int)chunk.size() - 1;
+  CK(cudaMalloc((void**)&d_r, (r.size() + 1) * sizeof(int)));
+  CK(cudaMemcpy(d_r, r.data(), r.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMalloc((void**)&d_chunk, chunk.size() * sizeof(int)));
+  CK(cudaMemcpy(d_chunk, chunk.data(), chunk.size() * sizeof(int), cudaMemcpyHostToDevice));
+  h_chunk = chunk;
 }
 
 void HsPlan::ensure_keys(Context& c) {
@@ -461,17 +506,29 @@ void HsPlan::finish(Context& c, int B, double v_scale, u64d* acc, u64d* cacc, in
   eval_rescale(c, u, out);
   out.scale = v_scale;
   // (5) log-depth fold, matvec.cpp:101-103: s += rot_left(s, m_eff * 2^t)
+  // for t = folds-1..0 = sum of rot_left(s, m_eff u) over u < 2^folds, run
+  // as ONE hoisted rotation sum (one ModUp of s.c1, the 2^folds - 1 key
+  // inner products on the rotated digits, one ModDown) instead of `folds`
+  // serial key switches; metered as the reference's folds (capi.cu)
   if (folds > 0) {
-    CtBatch r{&c, B, l - 1, out.scale, c.alloc((size_t)B * 2 * (l - 1) * N)};
-    for (int t = folds - 1; t >= 0; --t) {
-      const int shift = (int)(((int64_t)m_eff << t) % S);
-      KeyRowMap km{};
-      km.period = 1;
-      km.shift[0] = shift;
-      km.key[0] = c.rot_key(shift).data;
-      eval_rotate(c, out.d, (long)out.stride(), B, l - 1, km, r.d, (long)r.stride());
-      launch_add(c, out.d, r.d, out.d, B, l - 1);
+    const int lf = l - 1;
+    if (!fold) {
+      fold = std::make_unique<HsPlan>();
+      fold->build_rotsum(c, fold_rights(), lf);
     }
+    u64d* facc = c.alloc((size_t)B * 2 * (lf + 1) * N);
+    u64d* fcacc = c.alloc((size_t)B * 2 * lf * N);
+    fold->accumulate(c, out, 0, (int)fold->diag.size(), facc, fcacc);
+    CtBatch r{&c, B, lf, out.scale, c.alloc((size_t)B * 2 * lf * N)};
+    DropArgs f{};
+    f.src = facc; f.src_b = 2L * (lf + 1) * N; f.src_p = (long)(lf + 1) * N; f.src_limbs = lf + 1;
+    f.dst = r.d; f.dst_b = (long)r.stride(); f.dst_p = (long)lf * N;
+    f.pd = c.L(); f.nl = lf;
+    f.add = fcacc; f.add_b = 2L * lf * N; f.add_p = (long)lf * N; f.add_mask = 3; f.shifts = nullptr;
+    drop_last_limb(c, B, f, tmpP);
+    CK(cudaMemcpyAsync(out.d, r.d, out.words() * 8, cudaMemcpyDeviceToDevice, c.stream));
+    c.free(facc);
+    c.free(fcacc);
     c.free(r.d);
   }
   c.free(tmpP);

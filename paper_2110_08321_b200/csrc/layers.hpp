@@ -5,6 +5,7 @@
 //   HsPlan      extract_diagonals + hs_matvec  proj/src/matvec.cpp:45-105
 #pragma once
 #include <map>
+#include <memory>
 
 #include "engine.hpp"
 
@@ -63,6 +64,11 @@ struct HsPlan {
   bool imma_built = false;
   void ensure_imma(Context& c);
   bool use_imma(Context& c, int B, int i_lo, int i_hi) const;
+  // the log-depth fold (matvec.cpp:101-103) as one hoisted rotation sum:
+  // a unit-mask plan over rot_left(., m_eff u), u < 2^folds, at level - 1
+  std::unique_ptr<HsPlan> fold;
+  std::vector<int64_t> fold_rights() const;  // ascending, 0 first
+  void build_rotsum(Context& c, const std::vector<int64_t>& rights, int level);
   void build(Context& c, const double* A, int m, int n, int level, bool skip_zero);
   void release();
   std::vector<int64_t> right_rotations() const;  // diagonals, then folds
