@@ -233,6 +233,7 @@ struct HsDiagTable {
   const u64d* masks;         // [ndiag][l+1][N] mont, slot order
   int nchunk;
   const int* chunk;          // [nchunk + 1] diagonal ranges with r span < hs_chunk_span()
+  int unit_masks = 0;        // every mask is 1 (the fold's hoisted rotation sum)
 };
 int hs_chunk_span();
 void launch_hs_diag(Context& c, const u64d* v, int B, int l, const u64d* D, const HsDiagTable& t,

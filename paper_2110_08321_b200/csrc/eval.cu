@@ -620,53 +620,92 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
 // read straight from L1/L2 (consecutive positions -> coalesced; a warp of 32
 // positions x 8 images per CTA shares each fused-key word), no window
 // staging -- the windowed kernel exposed its staging latency at 16 warps/SM
-template <int LV>
+template <int LV, int IPT, bool UNIT>
 __global__ void __launch_bounds__(256) k_hs_narrow(PrimeTable pt, const u64d* __restrict__ v,
                                                    const u64d* __restrict__ D, int B, int L, int N, HsDiagTable tab,
                                                    u64d* __restrict__ acc, u64d* __restrict__ cacc) {
-  const int k = blockIdx.x * 32 + (threadIdx.x & 31), b = blockIdx.y * 8 + (threadIdx.x >> 5), t = blockIdx.z;
-  if (k >= N || b >= B) return;
+  // IPT images per thread share every fused-key word (register reuse);
+  // UNIT: all masks are 1 (the fold's rotation sum) -> the c0 part is a sum
+  const int k = blockIdx.x * 32 + (threadIdx.x & 31), b0 = (blockIdx.y * 8 + (threadIdx.x >> 5)) * IPT;
+  const int t = blockIdx.z;
+  if (k >= N || b0 >= B) return;
   const int S = N >> 1, half = k >= S ? S : 0, kh = k - half;
   const int pi = t == LV ? L : t;
   const DevPrime pr = pt.p[pi];
   const bool has_c = t < LV;
-  const size_t kp = (size_t)(LV + 1) * N;
-  const u64d* Db = D + ((size_t)b * LV * (LV + 1) + t) * N + half;
-  const u64d* c0 = v + (size_t)b * 2 * LV * N + (size_t)t * N + half;
-  AccC a0, a1, cc;
-  a0.zero();
-  a1.zero();
-  cc.zero();
+  const size_t kp = (size_t)(LV + 1) * N, ln = (size_t)LV * N;
+  const u64d* Db[IPT];
+  const u64d* c0[IPT];
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    const int b = b0 + q < B ? b0 + q : B - 1;  // (extra lanes recompute the last image, not stored)
+    Db[q] = D + ((size_t)b * LV * (LV + 1) + t) * N + half;
+    c0[q] = v + (size_t)b * 2 * ln + (size_t)t * N + half;
+  }
+  AccC a0[IPT], a1[IPT], cc[IPT];
+  u64d cs[IPT];
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) a0[q].zero(), a1[q].zero(), cc[q].zero(), cs[q] = 0;
   int na = 0, nc = 0;
   const int i0 = __ldg(tab.chunk), i1 = __ldg(tab.chunk + tab.nchunk);  // absolute diagonal range
   for (int i = i0; i < i1; ++i) {
     const int r = __ldg(tab.r + i), pos = (kh - r) & (S - 1);
     if (r != 0) {
       const u64d* fk = tab.fk + (size_t)(i - tab.first_keyed) * tab.fk_words + (size_t)t * N + k;
+      u64d k0[LV], k1[LV], d[IPT][LV];
 #pragma unroll
       for (int j = 0; j < LV; ++j) {
-        const u64d d = split31(Db[(size_t)j * kp + pos]);
-        a0.mad(d, __ldg(fk + (size_t)(j * 2) * kp));
-        a1.mad(d, __ldg(fk + (size_t)(j * 2 + 1) * kp));
-        if (++na == 4) a0.fold(), a1.fold(), na = 0;
+        k0[j] = __ldg(fk + (size_t)(j * 2) * kp);
+        k1[j] = __ldg(fk + (size_t)(j * 2 + 1) * kp);
+#pragma unroll
+        for (int q = 0; q < IPT; ++q) d[q][j] = Db[q][(size_t)j * kp + pos];
+      }
+#pragma unroll
+      for (int j = 0; j < LV; ++j) {
+#pragma unroll
+        for (int q = 0; q < IPT; ++q) {
+          const u64d x = split31(d[q][j]);
+          a0[q].mad(x, k0[j]);
+          a1[q].mad(x, k1[j]);
+        }
+        if (++na == 4) {
+#pragma unroll
+          for (int q = 0; q < IPT; ++q) a0[q].fold(), a1[q].fold();
+          na = 0;
+        }
       }
     }
     if (has_c) {
-      cc.mad(split31(c0[pos]), __ldg(tab.masks + ((size_t)i * (LV + 1) + t) * N + k));
-      if (++nc == 4) cc.fold(), nc = 0;
+      if constexpr (UNIT) {
+#pragma unroll
+        for (int q = 0; q < IPT; ++q) cs[q] = add_mod_d(cs[q], c0[q][pos], pr.q);
+      } else {
+        const u64d m = __ldg(tab.masks + ((size_t)i * (LV + 1) + t) * N + k);
+#pragma unroll
+        for (int q = 0; q < IPT; ++q) cc[q].mad(split31(c0[q][pos]), m);
+        if (++nc == 4) {
+#pragma unroll
+          for (int q = 0; q < IPT; ++q) cc[q].fold();
+          nc = 0;
+        }
+      }
     }
   }
-  u64d* o = acc + (size_t)b * 2 * kp + (size_t)t * N + k;
-  o[0] = a0.reduce(pr);
-  o[kp] = a1.reduce(pr);
-  if (has_c) {
-    const size_t ln = (size_t)LV * N;
-    u64d* cb = cacc + (size_t)b * 2 * ln + (size_t)t * N + k;
-    cb[0] = cc.reduce(pr);
-    const bool c1_term = tab.own_c1 && tab.ndiag > 0 && __ldg(tab.r) == 0;
-    cb[ln] = c1_term ? mont_mul(v[(size_t)b * 2 * ln + ln + (size_t)t * N + k],
-                                unsplit31(__ldg(tab.masks + (size_t)t * N + k)), pr.q, pr.qneg_inv)
-                     : 0ull;
+  const bool c1_term = has_c && tab.own_c1 && tab.ndiag > 0 && __ldg(tab.r) == 0;
+  const u64d m0 = c1_term && !UNIT ? unsplit31(__ldg(tab.masks + (size_t)t * N + k)) : 0ull;
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    const int b = b0 + q;
+    if (b >= B) break;
+    u64d* o = acc + (size_t)b * 2 * kp + (size_t)t * N + k;
+    o[0] = a0[q].reduce(pr);
+    o[kp] = a1[q].reduce(pr);
+    if (has_c) {
+      u64d* cb = cacc + (size_t)b * 2 * ln + (size_t)t * N + k;
+      cb[0] = UNIT ? cs[q] : cc[q].reduce(pr);
+      const u64d c1 = v[(size_t)b * 2 * ln + ln + (size_t)t * N + k];
+      cb[ln] = !c1_term ? 0ull : UNIT ? c1 : mont_mul(c1, m0, pr.q, pr.qneg_inv);
+    }
   }
 }
 
@@ -879,15 +918,20 @@ void launch_hs_diag(Context& c, const u64d* v, int B, int l, const u64d* D, cons
   }();
   if (t.ndiag <= narrow_max && l <= 8) {
     const int N = c.N();
-    dim3 grid((N + 31) / 32, (B + 7) / 8, l + 1);
+    constexpr int IPT = 1;
+    dim3 grid((N + 31) / 32, (B + 8 * IPT - 1) / (8 * IPT), l + 1);
     const double NB = 8.0 * N;
     const double bytes = NB * (t.keyed * l * 2.0 * (l + 1) + t.ndiag * l + B * (l * (l + 1.0) + 2.0 * l) +
                                B * (2.0 * (l + 1) + 2.0 * l));
     const double ops = (double)N * B * (t.keyed * l * (l + 1) * 2.0 + t.ndiag * l);
 #define NARROW_GO(LV)                                                                                        \
   case LV:                                                                                                   \
-    LAUNCH_BO(c, "k_hs_diag", bytes, ops,                                                                    \
-              k_hs_narrow<LV><<<grid, 256, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc));      \
+    if (t.unit_masks)                                                                                        \
+      LAUNCH_BO(c, "k_hs_diag", bytes, ops,                                                                  \
+                (k_hs_narrow<LV, IPT, true><<<grid, 256, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc))); \
+    else                                                                                                     \
+      LAUNCH_BO(c, "k_hs_diag", bytes, ops,                                                                  \
+                (k_hs_narrow<LV, IPT, false><<<grid, 256, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc))); \
     return;
     switch (l) { NARROW_GO(1) NARROW_GO(2) NARROW_GO(3) NARROW_GO(4) NARROW_GO(5) NARROW_GO(6) NARROW_GO(7) NARROW_GO(8) }
 #undef NARROW_GO

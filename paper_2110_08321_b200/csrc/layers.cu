@@ -303,6 +303,7 @@ void HsPlan::build_rotsum(Context& c, const std::vector<int64_t>& rights, int lv
   level = lvl;
   m = n = m_eff = 0;
   folds = 0;
+  unit_masks = true;
   const int S = c.S(), N = c.N(), nl = level + 1;
   for (int64_t r : rights) diag.push_back(HsDiag{(int)diag.size(), r, (int)((S - r) % S)});
   // unit masks: Montgomery 1 = 2^64 mod q per limb (limb `level` is P), split-31
@@ -477,7 +478,7 @@ void HsPlan::accumulate(Context& c, const CtBatch& v, int i_lo, int i_hi, u64d* 
   const int first_keyed = !diag.empty() && diag[0].shift == 0 ? 1 : 0;
   if (nch > 0 && i_hi > i_lo) {
     HsDiagTable tab{i_hi - i_lo, keyed, d_r, fkeys, (size_t)l * 2 * (l + 1) * N, first_keyed, i_lo == 0 ? 1 : 0,
-                    masks, nch, chunks};
+                    masks, nch, chunks, unit_masks ? 1 : 0};
     launch_hs_diag(c, v.d, B, l, D, tab, acc, cacc);
   } else {
     CK(cudaMemsetAsync(acc, 0, (size_t)B * 2 * (l + 1) * N * 8, c.stream));

@@ -67,6 +67,7 @@ struct HsPlan {
   // the log-depth fold (matvec.cpp:101-103) as one hoisted rotation sum:
   // a unit-mask plan over rot_left(., m_eff u), u < 2^folds, at level - 1
   std::unique_ptr<HsPlan> fold;
+  bool unit_masks = false;  // a rotation-sum plan (build_rotsum)
   std::vector<int64_t> fold_rights() const;  // ascending, 0 first
   void build_rotsum(Context& c, const std::vector<int64_t>& rights, int level);
   void build(Context& c, const double* A, int m, int n, int level, bool skip_zero);
