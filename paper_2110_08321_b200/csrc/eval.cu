@@ -621,12 +621,15 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
 // positions x 8 images per CTA shares each fused-key word), no window
 // staging -- the windowed kernel exposed its staging latency at 16 warps/SM
 template <int LV, int IPT, bool UNIT>
-__global__ void __launch_bounds__(256) k_hs_narrow(PrimeTable pt, const u64d* __restrict__ v,
+#ifndef HEGPU_NARROW_WARPS
+#define HEGPU_NARROW_WARPS 4  // image warps per CTA (measured 1: 0.459, 2: 0.451, 4: 0.454, 8: 0.490, 16: 0.621 ms)
+#endif
+__global__ void __launch_bounds__(32 * HEGPU_NARROW_WARPS) k_hs_narrow(PrimeTable pt, const u64d* __restrict__ v,
                                                    const u64d* __restrict__ D, int B, int L, int N, HsDiagTable tab,
                                                    u64d* __restrict__ acc, u64d* __restrict__ cacc) {
   // IPT images per thread share every fused-key word (register reuse);
   // UNIT: all masks are 1 (the fold's rotation sum) -> the c0 part is a sum
-  const int k = blockIdx.x * 32 + (threadIdx.x & 31), b0 = (blockIdx.y * 8 + (threadIdx.x >> 5)) * IPT;
+  const int k = blockIdx.x * 32 + (threadIdx.x & 31), b0 = (blockIdx.y * HEGPU_NARROW_WARPS + (threadIdx.x >> 5)) * IPT;
   const int t = blockIdx.z;
   if (k >= N || b0 >= B) return;
   const int S = N >> 1, half = k >= S ? S : 0, kh = k - half;
@@ -919,7 +922,8 @@ void launch_hs_diag(Context& c, const u64d* v, int B, int l, const u64d* D, cons
   if (t.ndiag <= narrow_max && l <= 8) {
     const int N = c.N();
     constexpr int IPT = 1;
-    dim3 grid((N + 31) / 32, (B + 8 * IPT - 1) / (8 * IPT), l + 1);
+    constexpr int NW = HEGPU_NARROW_WARPS;
+    dim3 grid((N + 31) / 32, (B + NW * IPT - 1) / (NW * IPT), l + 1);
     const double NB = 8.0 * N;
     const double bytes = NB * (t.keyed * l * 2.0 * (l + 1) + t.ndiag * l + B * (l * (l + 1.0) + 2.0 * l) +
                                B * (2.0 * (l + 1) + 2.0 * l));
@@ -928,10 +932,10 @@ void launch_hs_diag(Context& c, const u64d* v, int B, int l, const u64d* D, cons
   case LV:                                                                                                   \
     if (t.unit_masks)                                                                                        \
       LAUNCH_BO(c, "k_hs_diag", bytes, ops,                                                                  \
-                (k_hs_narrow<LV, IPT, true><<<grid, 256, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc))); \
+                (k_hs_narrow<LV, IPT, true><<<grid, 32 * NW, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc))); \
     else                                                                                                     \
       LAUNCH_BO(c, "k_hs_diag", bytes, ops,                                                                  \
-                (k_hs_narrow<LV, IPT, false><<<grid, 256, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc))); \
+                (k_hs_narrow<LV, IPT, false><<<grid, 32 * NW, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc))); \
     return;
     switch (l) { NARROW_GO(1) NARROW_GO(2) NARROW_GO(3) NARROW_GO(4) NARROW_GO(5) NARROW_GO(6) NARROW_GO(7) NARROW_GO(8) }
 #undef NARROW_GO
