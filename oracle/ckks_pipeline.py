@@ -93,16 +93,40 @@ def square(ck, v, level, rlk):
     return ck.rescale(ck.square(v, level, rlk), level)
 
 
-def conv_pack_taps(ck, cfg, image, nonce, tap_scale):
+def conv_pack_taps(ck, cfg, image, nonce, tap_scale, merged=True):
     """Client side: conv_pack (proj/src/convlower.cpp:9-37) + encode + encrypt,
-    nonces nonce*ntaps + t (same convention as hegpu_net_encrypt_image)."""
+    nonces nonce*ntaps + t (same convention as hegpu_net_encrypt_image).
+    merged: the stage driver's fused Conv1 + Flat1 -- each tap's window is
+    packed at every map offset co * d_out^2 (hegpu_net_encrypt_image)."""
     shape = HS.ConvShape(cfg.in_d, cfg.in_c, cfg.k, cfg.s, cfg.c_out)
     taps = HS.conv_pack(image, shape, ck.S)
     L = ck.L
     ntaps = len(taps)
     w_used = shape.d_out() ** 2
-    cts = [ck.encrypt(ck.encode(t.slots[:w_used], tap_scale, L), L, nonce * ntaps + i) for i, t in enumerate(taps)]
+    reps = cfg.c_out if merged else 1
+    cts = [ck.encrypt(ck.encode(np.tile(t.slots[:w_used], reps), tap_scale, L), L, nonce * ntaps + i)
+           for i, t in enumerate(taps)]
     return np.concatenate(cts)
+
+
+def merged_conv(ck, taps, ntaps, level, weights, bias, w_used, tap_scale):
+    """the fused Conv1 + Flat1 of the stage driver on replicated taps:
+    sum_s tap_s * P_s + bias_pt with P_s = W[co][s] on map block co (scale
+    q_{level-1}) and the block bias at the product scale, then one rescale:
+    the merged ciphertext (maps at offsets co * w_used) -- the same slots as
+    conv_packed_forward + merge_maps (convlower.cpp:39-74, 145-160)"""
+    W = np.asarray(weights, dtype=np.float64).reshape(-1, ntaps)
+    c_out = W.shape[0]
+    qlast = float(ck.primes[level - 1])
+    per = 2 * level * ck.N
+    acc = None
+    for s_ in range(ntaps):
+        p = ck.encode(np.repeat(W[:, s_], w_used), qlast, level)
+        term = ck.mul_pc(taps[s_ * per:(s_ + 1) * per], p, level)
+        acc = term if acc is None else ck.add(acc, term, level)
+    b = np.repeat(np.asarray(bias, dtype=np.float64) if bias is not None else np.zeros(c_out), w_used)
+    acc = ck.add_pc(acc, ck.encode(b, tap_scale * qlast, level), level)
+    return ck.rescale(acc, level)
 
 
 class PreparedNet:
@@ -117,10 +141,7 @@ class PreparedNet:
         d_out = (cfg.in_d - cfg.k) // cfg.s + 1
         self.w_used = d_out * d_out
         self.conv_w = np.asarray(weights["conv_w"], dtype=np.float64).reshape(cfg.c_out, -1)
-        qlast = float(ck.primes[L - 1])
-        self.conv_bias = np.concatenate([
-            ck.encode(np.full(self.w_used, weights["conv_b"][co]), self.tap_scale * qlast, L)
-            for co in range(cfg.c_out)])
+        self.conv_b = np.asarray(weights["conv_b"], dtype=np.float64)
         keys = {}
 
         def key(g):
@@ -129,8 +150,6 @@ class PreparedNet:
             return keys[g]
 
         l = L - 1
-        self.merge_keys = np.concatenate([key(ck.galois_right(j * self.w_used)) for j in range(1, cfg.c_out)]) \
-            if cfg.c_out > 1 else np.zeros(1, dtype=np.uint64)
         self.rlk = ck.relin_key()
         scale = self.tap_scale
         self.layers = []
@@ -152,11 +171,9 @@ class PreparedNet:
     def eval(self, taps):
         ck, cfg = self.ck, self.cfg
         L = ck.L
-        maps = ck.conv_mac(taps, self.ntaps, L, self.conv_w, cfg.c_out, float(ck.primes[L - 1]), self.conv_bias)
-        per = 2 * L * ck.N
-        maps = np.concatenate([ck.rescale(maps[co * per:(co + 1) * per], L) for co in range(cfg.c_out)])
+        # Conv1 + Flat1 fused on the replicated taps (the stage driver's form)
+        x = merged_conv(ck, taps, self.ntaps, L, self.conv_w, self.conv_b, self.w_used, self.tap_scale)
         l = L - 1
-        x = ck.merge(maps, cfg.c_out, l, self.w_used, self.merge_keys)
         for lv, rots, masks, kbuf, fold, bias in self.layers:
             x = ck.rescale(ck.square(x, l, self.rlk), l)
             l = lv

@@ -121,8 +121,40 @@ ConvLayer::ConvLayer(Context& c, int nt, int co_n, const double* weights, const 
   upload_mont(c, wire, bias, (size_t)c_out * level, level, -1);
 }
 
+void ConvLayer::make_merged(Context& c, const double* weights, const double* bias_vals, int w_used,
+                            double tap_scale) {
+  const int N = c.N(), S = c.S();
+  need((int64_t)c_out * w_used <= S, HEGPU_ERR_CAPACITY, "merged conv: c_out * d_out^2 exceeds the slots");
+  const double qlast = (double)c.P->q(level - 1);
+  std::vector<u64> wire((size_t)ntaps * level * N);
+#pragma omp parallel for schedule(dynamic)
+  for (int t = 0; t < ntaps; ++t) {
+    std::vector<double> z((size_t)c_out * w_used);
+    for (int co = 0; co < c_out; ++co)
+      std::fill_n(z.data() + (size_t)co * w_used, w_used, weights[(size_t)co * ntaps + t]);
+    c.client->encode(z.data(), (int)z.size(), qlast, level, false, wire.data() + (size_t)t * level * N);
+  }
+  CK(cudaMalloc((void**)&pw, wire.size() * 8));
+  upload_mont(c, wire, pw, (size_t)ntaps * level, level, -1);
+  launch_split31(c, pw, wire.size());
+  std::vector<double> zb((size_t)c_out * w_used);
+  for (int co = 0; co < c_out; ++co)
+    std::fill_n(zb.data() + (size_t)co * w_used, w_used, bias_vals ? bias_vals[co] : 0.0);
+  std::vector<u64> bw((size_t)level * N);
+  c.client->encode(zb.data(), (int)zb.size(), tap_scale * qlast, level, false, bw.data());
+  CK(cudaMalloc((void**)&pbias, bw.size() * 8));
+  u64d* stage = c.alloc(bw.size());
+  CK(cudaMemcpyAsync(stage, bw.data(), bw.size() * 8, cudaMemcpyHostToDevice, c.stream));
+  launch_wire_to_slot(c, stage, pbias, (size_t)level, 0, level, -1);  // standard form
+  c.free(stage);
+  CK(cudaStreamSynchronize(c.stream));
+  merged = true;
+}
+
 ConvLayer::~ConvLayer() {
   cudaStreamSynchronize(ctx->stream);
+  cudaFree(pw);
+  cudaFree(pbias);
   cudaFree(w);
   cudaFree(bias);
   cudaFree(wa);
@@ -134,7 +166,8 @@ ConvLayer::~ConvLayer() {
 
 void ConvLayer::mac(Context& c, const CtBatch& taps, CtBatch& prod) {
   const int B = taps.count / ntaps;
-  if (HEGPU_CONV_IMMA && conv_imma_supported(c))
+  if (merged) launch_conv_pt(c, taps.d, B, ntaps, level, pw, pbias, prod.d);
+  else if (HEGPU_CONV_IMMA && conv_imma_supported(c))
     launch_conv_imma(c, taps.d, B, ntaps, level, wa, cps, kbn, c_out, bias, prod.d);
   else
     launch_conv_mac(c, taps.d, B, ntaps, level, w, c_out, bias, prod.d);
@@ -146,7 +179,8 @@ void ConvLayer::mac_compact(Context& c, const uint8_t* taps, int B, double tap_s
   // beats decoding c0 / hashing c1 inside the register-heavy MAC kernel
   u64d* full = c.alloc((size_t)B * ntaps * 2 * level * c.N());
   launch_expand_compact(c, taps, B * ntaps, level, full);
-  if (HEGPU_CONV_IMMA && conv_imma_supported(c))
+  if (merged) launch_conv_pt(c, full, B, ntaps, level, pw, pbias, prod.d);
+  else if (HEGPU_CONV_IMMA && conv_imma_supported(c))
     launch_conv_imma(c, full, B, ntaps, level, wa, cps, kbn, c_out, bias, prod.d);
   else
     launch_conv_mac(c, full, B, ntaps, level, w, c_out, bias, prod.d);
@@ -155,8 +189,8 @@ void ConvLayer::mac_compact(Context& c, const uint8_t* taps, int B, double tap_s
 }
 
 void ConvLayer::run(Context& c, const CtBatch& taps, CtBatch& maps) {
-  const int B = taps.count / ntaps, l = level, N = c.N();
-  CtBatch prod{&c, B * c_out, l, 0, c.alloc((size_t)B * c_out * 2 * l * N)};
+  const int B = taps.count / ntaps, l = level, N = c.N(), mo = out_per_image();
+  CtBatch prod{&c, B * mo, l, 0, c.alloc((size_t)B * mo * 2 * l * N)};
   mac(c, taps, prod);
   eval_rescale(c, prod, maps);
   maps.scale = taps.scale;

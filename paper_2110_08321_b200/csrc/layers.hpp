@@ -32,6 +32,16 @@ struct ConvLayer {
   // the same on B images of compact fresh taps (device bytes at `level`):
   // expanded into full ciphertexts first (io.cu), then the MAC
   void mac_compact(Context& c, const uint8_t* taps, int B, double tap_scale, CtBatch& prod);
+  // merged mode (the stage driver's Conv1 + Flat1): the
+  // client packs every tap replicated at the c_out map offsets co * w_used,
+  // the weights become block plaintexts P_s (W[co][s] on block co, scale
+  // q_{level-1}) and the bias one block plaintext, so the MAC lands each map
+  // at its merged slots: ONE ciphertext per image, no merge rotations
+  void make_merged(Context& c, const double* weights, const double* bias_vals, int w_used, double tap_scale);
+  bool merged = false;
+  u64d* pw = nullptr;     // [ntaps][level][N] split-31 Montgomery block plaintexts
+  u64d* pbias = nullptr;  // [level][N] standard-form block bias (product scale)
+  int out_per_image() const { return merged ? 1 : c_out; }
   Context* ctx;
 };
 

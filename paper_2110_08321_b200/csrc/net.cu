@@ -128,8 +128,9 @@ void run_after_conv(hegpu_net& net, const CtBatch& mb, CtBatch& out);
 void run_net(hegpu_net& net, const CtBatch& taps, CtBatch& out) {
   Context& c = *net.c;
   const int B = taps.count / net.ntaps;
-  Scratch maps(c, (size_t)B * net.spec.c_out * 2 * (net.top - 1) * c.N());
-  CtBatch mb{&c, B * net.spec.c_out, net.top - 1, 0, maps.p};
+  const int mo = net.conv->out_per_image();
+  Scratch maps(c, (size_t)B * mo * 2 * (net.top - 1) * c.N());
+  CtBatch mb{&c, B * mo, net.top - 1, 0, maps.p};
   run_conv(net, taps, mb);
   run_after_conv(net, mb, out);
 }
@@ -138,13 +139,16 @@ void run_net(hegpu_net& net, const CtBatch& taps, CtBatch& out) {
 void run_after_conv(hegpu_net& net, const CtBatch& mb, CtBatch& out) {
   Context& c = *net.c;
   const hegpu_net_spec& s = net.spec;
-  const int B = mb.count / s.c_out, N = c.N();
+  const int mo = net.conv->out_per_image(), B = mb.count / mo, N = c.N();
   int l = mb.level;
-  // Flat1: Merge (netcompile.cpp:332-347)
+  // Flat1: Merge (netcompile.cpp:332-347).  With the merged first layer the
+  // maps already sit at their merged offsets (one ciphertext per image): the
+  // stage's HOPs are the reference's (c_out - 1 rotations + additions), no
+  // key switch runs
   c.meter.begin("Flat1");
   Scratch cur(c, (size_t)B * 2 * l * N);
   CtBatch x{&c, B, l, 0, cur.p};
-  merge_maps(c, mb, s.c_out, net.w_used, x);
+  merge_maps(c, mb, mo, net.w_used, x);
   c.meter.bump(HEGPU_ROT, (int64_t)B * (s.c_out - 1));
   c.meter.bump(HEGPU_ADD_CC, (int64_t)B * (s.c_out - 1));
   Scratch nxt(c, (size_t)B * 2 * l * N);
@@ -228,8 +232,8 @@ extern "C" int hegpu_net_create(hegpu_ctx* h, const hegpu_net_spec* spec, const 
     net->tap_scale = std::ldexp(1.0, 40);
     net->conv = std::make_unique<ConvLayer>(c, net->ntaps, s.c_out, conv_w, conv_b, net->w_used, net->top,
                                             net->tap_scale);
+    net->conv->make_merged(c, conv_w, conv_b, net->w_used, net->tap_scale);  // Conv1 + Flat1 fused
     std::vector<int64_t> rots;
-    for (int j = 1; j < s.c_out; ++j) rots.push_back((int64_t)j * net->w_used);
     double scale = net->tap_scale;  // after conv + rescale
     int l = net->top - 1;
     int n = s.c_out * net->w_used;
@@ -319,12 +323,13 @@ extern "C" int hegpu_net_run_compact(hegpu_net* net, const void* dev_taps, int b
     need(out->b.count == batch && out->b.level == net->top - 1 - 2 * net->spec.n_dense, HEGPU_ERR_SHAPE,
          "net_run_compact: bad output handle");
     const int L = net->top, N = c.N();
-    Scratch prod(c, (size_t)batch * net->spec.c_out * 2 * L * N);
-    Scratch maps(c, (size_t)batch * net->spec.c_out * 2 * (L - 1) * N);
-    CtBatch pb{&c, batch * net->spec.c_out, L, 0, prod.p};
+    const int mo = net->conv->out_per_image();
+    Scratch prod(c, (size_t)batch * mo * 2 * L * N);
+    Scratch maps(c, (size_t)batch * mo * 2 * (L - 1) * N);
+    CtBatch pb{&c, batch * mo, L, 0, prod.p};
     conv_meter(*net, batch);
     net->conv->mac_compact(c, static_cast<const uint8_t*>(dev_taps), batch, net->tap_scale, pb);
-    CtBatch mb{&c, batch * net->spec.c_out, L - 1, 0, maps.p};
+    CtBatch mb{&c, batch * mo, L - 1, 0, maps.p};
     eval_rescale(c, pb, mb);
     mb.scale = net->tap_scale;
     CtBatch o = out->b;
@@ -429,17 +434,18 @@ void compute_pass(hegpu_net& n, const uint8_t* stage, int cur, int batch, int ch
   const auto& subs = n.sub_events[cur];
   // each sub-chunk is multiply-accumulated straight from its compact bytes
   // as it lands; the conv rescale runs once per chunk (full-width NTT grids)
-  Scratch prod(c, (size_t)c2 * n.spec.c_out * 2 * L * N);
-  Scratch maps(c, (size_t)c2 * n.spec.c_out * map_words);
+  const int mo = n.conv->out_per_image();
+  Scratch prod(c, (size_t)c2 * mo * 2 * L * N);
+  Scratch maps(c, (size_t)c2 * mo * map_words);
   Scratch o(c, (size_t)c2 * out_words);
   Scratch wire(c, (size_t)c2 * out_words);
   for (int m0 = 0; m0 < batch; m0 += c2) {
     const int nm = std::min(c2, batch - m0);
-    CtBatch pb{&c, nm * n.spec.c_out, L, 0, prod.p};
+    CtBatch pb{&c, nm * mo, L, 0, prod.p};
     for (int b0 = m0; b0 < m0 + nm; b0 += c1) {
       const int nb = std::min(c1, m0 + nm - b0);
       CK(cudaStreamWaitEvent(c.stream, subs[b0 / c1], captured ? cudaEventWaitExternal : 0));
-      CtBatch sb{&c, nb * n.spec.c_out, L, 0, prod.p + (size_t)(b0 - m0) * n.spec.c_out * 2 * L * N};
+      CtBatch sb{&c, nb * mo, L, 0, prod.p + (size_t)(b0 - m0) * mo * 2 * L * N};
       n.conv->mac_compact(c, stage + (size_t)b0 * per_img, nb, n.tap_scale, sb);
       pb.scale = sb.scale;
     }
@@ -448,9 +454,9 @@ void compute_pass(hegpu_net& n, const uint8_t* stage, int cur, int batch, int ch
       else CK(cudaEventRecord(n.freed[cur], c.stream));
     }
     conv_meter(n, nm);
-    CtBatch rb{&c, nm * n.spec.c_out, L - 1, 0, maps.p};
+    CtBatch rb{&c, nm * mo, L - 1, 0, maps.p};
     eval_rescale(c, pb, rb);
-    CtBatch mb{&c, nm * n.spec.c_out, L - 1, n.tap_scale, maps.p};
+    CtBatch mb{&c, nm * mo, L - 1, n.tap_scale, maps.p};
     CtBatch ob{&c, nm, lo, 0, o.p};
     run_after_conv(n, mb, ob);
     launch_slot_to_wire(c, o.p, wire.p, (size_t)nm * 2 * lo, 0, lo, -1);
@@ -548,7 +554,8 @@ extern "C" int hegpu_net_encrypt_image_compact(hegpu_net* net, const double* ima
     const size_t per = c.client->compact_bytes(L);
     // same conv_pack + encode as hegpu_net_encrypt_image, same nonces: the
     // compact taps expand to exactly those ciphertexts
-    std::vector<double> z(net->w_used);
+    const int reps = net->conv->merged ? net->spec.c_out : 1;
+    std::vector<double> z((size_t)reps * net->w_used);
     std::vector<u64> pt((size_t)L * c.N());
     const hegpu_net_spec& s = net->spec;
     const int d = net->d_out;
@@ -559,7 +566,9 @@ extern "C" int hegpu_net_encrypt_image_compact(hegpu_net* net, const double* ima
           for (int oy = 0; oy < d; ++oy)
             for (int ox = 0; ox < d; ++ox)
               z[oy * d + ox] = image[((size_t)ci * s.in_d + oy * s.stride + ky) * s.in_d + ox * s.stride + kx];
-          c.client->encode(z.data(), net->w_used, net->tap_scale, L, false, pt.data());
+          for (int co = 1; co < reps; ++co)  // merged first layer: the window at every map offset
+            std::copy_n(z.data(), net->w_used, z.data() + (size_t)co * net->w_used);
+          c.client->encode(z.data(), reps * net->w_used, net->tap_scale, L, false, pt.data());
           c.client->encrypt_compact(pt.data(), L, nonce * (uint64_t)net->ntaps + (uint64_t)t,
                                     taps_out + (size_t)t * per);
         }
@@ -572,7 +581,8 @@ extern "C" int hegpu_net_encrypt_image(hegpu_net* net, const double* image, uint
   return guarded(&c, [&] {
     const hegpu_net_spec& s = net->spec;
     const int N = c.N(), L = net->top, d = net->d_out;
-    std::vector<double> z(net->w_used);
+    const int reps = net->conv->merged ? net->spec.c_out : 1;
+    std::vector<double> z((size_t)reps * net->w_used);
     std::vector<u64> pt((size_t)L * N);
     // conv_pack (convlower.cpp:9-37): tap t = (ci*k+ky)*k+kx, slot oy*d_out+ox
     for (int ci = 0; ci < s.in_c; ++ci)
@@ -582,7 +592,9 @@ extern "C" int hegpu_net_encrypt_image(hegpu_net* net, const double* image, uint
           for (int oy = 0; oy < d; ++oy)
             for (int ox = 0; ox < d; ++ox)
               z[oy * d + ox] = image[((size_t)ci * s.in_d + oy * s.stride + ky) * s.in_d + ox * s.stride + kx];
-          c.client->encode(z.data(), net->w_used, net->tap_scale, L, false, pt.data());
+          for (int co = 1; co < reps; ++co)  // merged first layer: the window at every map offset
+            std::copy_n(z.data(), net->w_used, z.data() + (size_t)co * net->w_used);
+          c.client->encode(z.data(), reps * net->w_used, net->tap_scale, L, false, pt.data());
           c.client->encrypt(pt.data(), L, nonce * (uint64_t)net->ntaps + (uint64_t)t,
                             taps_out + (size_t)t * 2 * L * N);
         }

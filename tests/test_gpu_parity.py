@@ -161,7 +161,7 @@ def test_conv_packed_forward(pair, c_out):
     W = rng.normal(0, 0.05, (c_out, 1, 3, 3))
     bias = rng.normal(0, 0.01, c_out)
     L = ck.L
-    taps = P.conv_pack_taps(ck, cfg, img, 3, DELTA)
+    taps = P.conv_pack_taps(ck, cfg, img, 3, DELTA, merged=False)  # the standalone per-map conv API
     dt = ctx.ct(9, L, taps, DELTA)
     out = ctx.ct(c_out, L - 1)
     ctx.reset_meter()
