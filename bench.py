@@ -378,6 +378,9 @@ def run_gpu(args):
                    "input": args.input,
                    "l2": ("inputs 0.43 GB (compact) / 1.26 GB (full) per step > L2, no flush")},
         "rotations_per_s": per_step_rot * world / (ms_max / 1e3),
+        "rotation_metering": ("reference HOP semantics (hesim's per-stage tally: 120 rotations per cfg-0 "
+                              "inference); the engine runs fewer key switches than that -- HS diagonals and "
+                              "folds hoisted, Conv1 + Flat1 fused (DESIGN.md §4)"),
         # limb transforms per second: every NTT-family launch's butterflies
         # / (N/2 log2 N) (one transform = one limb of one polynomial)
         "ntts_per_s": ntt_rows * world / (ms_max / 1e3),
