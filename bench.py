@@ -154,8 +154,11 @@ def _cpu_worker(args):
     from paper_2110_08321_b200.workloads import CFG0, net_image, net_weights
     cfg = CFG0
     ck = Ckks(cfg.log_n, list(cfg.qbits), cfg.pbits, seed=SEED)
-    prep = P.PreparedNet(ck, cfg, net_weights(cfg, SEED))
-    taps = [P.conv_pack_taps(ck, cfg, net_image(cfg, seed + i), seed + i, prep.tap_scale) for i in range(n_images)]
+    # the reference's algorithm (per-map conv + merge; the GPU's fused first
+    # layer is not the reference's, so the baseline does not get it)
+    prep = P.PreparedNet(ck, cfg, net_weights(cfg, SEED), merged=False)
+    taps = [P.conv_pack_taps(ck, cfg, net_image(cfg, seed + i), seed + i, prep.tap_scale, merged=False)
+            for i in range(n_images)]
     t0 = time.perf_counter()
     for t in taps:
         prep.eval(t)

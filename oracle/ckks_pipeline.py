@@ -133,8 +133,11 @@ class PreparedNet:
     """Server-side offline state for one model (keys, encoded HS masks,
     bias plaintexts) so that eval() times only the homomorphic evaluation."""
 
-    def __init__(self, ck, cfg, weights):
-        self.ck, self.cfg = ck, cfg
+    def __init__(self, ck, cfg, weights, merged=True):
+        """merged: Conv1 + Flat1 fused as the GPU stage driver runs them
+        (replicated taps); False: the reference's per-map conv + merge
+        (proj/src/netcompile.cpp:321-347) -- the CPU baseline's algorithm."""
+        self.ck, self.cfg, self.merged = ck, cfg, merged
         self.tap_scale = 2.0 ** 40
         L = ck.L
         self.ntaps = cfg.k * cfg.k * cfg.in_c
@@ -142,6 +145,11 @@ class PreparedNet:
         self.w_used = d_out * d_out
         self.conv_w = np.asarray(weights["conv_w"], dtype=np.float64).reshape(cfg.c_out, -1)
         self.conv_b = np.asarray(weights["conv_b"], dtype=np.float64)
+        if not merged:
+            qlast = float(ck.primes[L - 1])
+            self.conv_bias = np.concatenate([
+                ck.encode(np.full(self.w_used, self.conv_b[co]), self.tap_scale * qlast, L)
+                for co in range(cfg.c_out)])
         keys = {}
 
         def key(g):
@@ -150,6 +158,9 @@ class PreparedNet:
             return keys[g]
 
         l = L - 1
+        if not merged:
+            self.merge_keys = np.concatenate([key(ck.galois_right(j * self.w_used)) for j in range(1, cfg.c_out)]) \
+                if cfg.c_out > 1 else np.zeros(1, dtype=np.uint64)
         self.rlk = ck.relin_key()
         scale = self.tap_scale
         self.layers = []
@@ -171,8 +182,13 @@ class PreparedNet:
     def eval(self, taps):
         ck, cfg = self.ck, self.cfg
         L = ck.L
-        # Conv1 + Flat1 fused on the replicated taps (the stage driver's form)
-        x = merged_conv(ck, taps, self.ntaps, L, self.conv_w, self.conv_b, self.w_used, self.tap_scale)
+        if self.merged:  # Conv1 + Flat1 fused on the replicated taps (the stage driver's form)
+            x = merged_conv(ck, taps, self.ntaps, L, self.conv_w, self.conv_b, self.w_used, self.tap_scale)
+        else:  # the reference's per-map conv, rescale, merge
+            maps = ck.conv_mac(taps, self.ntaps, L, self.conv_w, cfg.c_out, float(ck.primes[L - 1]), self.conv_bias)
+            per = 2 * L * ck.N
+            maps = np.concatenate([ck.rescale(maps[co * per:(co + 1) * per], L) for co in range(cfg.c_out)])
+            x = ck.merge(maps, cfg.c_out, L - 1, self.w_used, self.merge_keys)
         l = L - 1
         for lv, rots, masks, kbuf, fold, bias in self.layers:
             x = ck.rescale(ck.square(x, l, self.rlk), l)
