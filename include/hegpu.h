@@ -264,6 +264,9 @@ int hegpu_net_run_host(hegpu_net* net, const uint64_t* host_taps, int batch, uin
 /* client helper: conv_pack (convlower.cpp:9-37) + encode + encrypt of one
  * image [in_c][in_d][in_d] -> ntaps wire ciphertexts at the top level */
 int hegpu_net_encrypt_image(hegpu_net* net, const double* image, uint64_t nonce, uint64_t* taps_out);
+/* tap ciphertexts per image: ceil(k^2 c_in / R), R = taps packed per
+ * ciphertext by the fused first layer */
+int hegpu_net_tap_cts(const hegpu_net* net);
 /* the same taps in compact form (hegpu_net_compact_image_bytes per image) */
 size_t hegpu_net_compact_image_bytes(const hegpu_net* net);
 int hegpu_net_encrypt_image_compact(hegpu_net* net, const double* image, uint64_t nonce, uint8_t* taps_out);

@@ -103,13 +103,29 @@ def conv_pack_taps(ck, cfg, image, nonce, tap_scale, merged=True):
     L = ck.L
     ntaps = len(taps)
     w_used = shape.d_out() ** 2
-    reps = cfg.c_out if merged else 1
-    cts = [ck.encrypt(ck.encode(np.tile(t.slots[:w_used], reps), tap_scale, L), L, nonce * ntaps + i)
-           for i, t in enumerate(taps)]
+    if not merged:
+        return np.concatenate([ck.encrypt(ck.encode(t.slots[:w_used], tap_scale, L), L, nonce * ntaps + i)
+                               for i, t in enumerate(taps)])
+    # fused first layer: R taps per ciphertext, tap s's window replicated
+    # over the c_out map blocks of region s % R (hegpu_net_encrypt_image)
+    R = tap_regions(ck, cfg)
+    F = cfg.c_out * w_used
+    G = -(-ntaps // R)
+    cts = []
+    for g in range(G):
+        used = min(R, ntaps - g * R)
+        z = np.concatenate([np.tile(taps[g * R + r].slots[:w_used], cfg.c_out) for r in range(used)])
+        cts.append(ck.encrypt(ck.encode(z, tap_scale, L), L, nonce * G + g))
     return np.concatenate(cts)
 
 
-def merged_conv(ck, taps, ntaps, level, weights, bias, w_used, tap_scale):
+def tap_regions(ck, cfg):
+    """taps packed per input ciphertext by the fused first layer"""
+    d_out = (cfg.in_d - cfg.k) // cfg.s + 1
+    return max(1, min(cfg.k * cfg.k * cfg.in_c, ck.S // (cfg.c_out * d_out * d_out)))
+
+
+def merged_conv(ck, taps, ntaps, level, weights, bias, w_used, tap_scale, regions=1, keys=None):
     """the fused Conv1 + Flat1 of the stage driver on replicated taps:
     sum_s tap_s * P_s + bias_pt with P_s = W[co][s] on map block co (scale
     q_{level-1}) and the block bias at the product scale, then one rescale:
@@ -117,16 +133,31 @@ def merged_conv(ck, taps, ntaps, level, weights, bias, w_used, tap_scale):
     conv_packed_forward + merge_maps (convlower.cpp:39-74, 145-160)"""
     W = np.asarray(weights, dtype=np.float64).reshape(-1, ntaps)
     c_out = W.shape[0]
+    F = c_out * w_used
     qlast = float(ck.primes[level - 1])
     per = 2 * level * ck.N
     acc = None
     for s_ in range(ntaps):
-        p = ck.encode(np.repeat(W[:, s_], w_used), qlast, level)
-        term = ck.mul_pc(taps[s_ * per:(s_ + 1) * per], p, level)
+        r, g = s_ % regions, s_ // regions
+        p = ck.encode(np.concatenate([np.zeros(r * F), np.repeat(W[:, s_], w_used)]), qlast, level)
+        term = ck.mul_pc(taps[g * per:(g + 1) * per], p, level)
         acc = term if acc is None else ck.add(acc, term, level)
     b = np.repeat(np.asarray(bias, dtype=np.float64) if bias is not None else np.zeros(c_out), w_used)
     acc = ck.add_pc(acc, ck.encode(b, tap_scale * qlast, level), level)
-    return ck.rescale(acc, level)
+    x = ck.rescale(acc, level)
+    if regions > 1:  # regions onto region 0: one hoisted rotation sum (unit masks)
+        rots = sorted({(ck.S - (r * F) % ck.S) % ck.S for r in range(regions)})
+        keys = keys if keys is not None else {}
+        kl = []
+        for rr in rots:
+            if rr:
+                gk = ck.galois_right(rr)
+                if gk not in keys:
+                    keys[gk] = ck.galois_key(gk)
+                kl.append(keys[gk])
+        x = ck.hs_hoisted(x, level - 1, np.array(rots, dtype=np.int64),
+                          np.ones(len(rots) * level * ck.N, dtype=np.uint64), np.concatenate(kl))
+    return x
 
 
 class PreparedNet:
@@ -151,6 +182,7 @@ class PreparedNet:
                 ck.encode(np.full(self.w_used, self.conv_b[co]), self.tap_scale * qlast, L)
                 for co in range(cfg.c_out)])
         keys = {}
+        self.keys = keys
 
         def key(g):
             if g not in keys:
@@ -182,8 +214,9 @@ class PreparedNet:
     def eval(self, taps):
         ck, cfg = self.ck, self.cfg
         L = ck.L
-        if self.merged:  # Conv1 + Flat1 fused on the replicated taps (the stage driver's form)
-            x = merged_conv(ck, taps, self.ntaps, L, self.conv_w, self.conv_b, self.w_used, self.tap_scale)
+        if self.merged:  # Conv1 + Flat1 fused on the region-packed replicated taps (the stage driver's form)
+            x = merged_conv(ck, taps, self.ntaps, L, self.conv_w, self.conv_b, self.w_used, self.tap_scale,
+                            tap_regions(ck, cfg), self.keys)
         else:  # the reference's per-map conv, rescale, merge
             maps = ck.conv_mac(taps, self.ntaps, L, self.conv_w, cfg.c_out, float(ck.primes[L - 1]), self.conv_bias)
             per = 2 * L * ck.N

@@ -220,8 +220,8 @@ void launch_conv_imma(Context& c, const u64d* taps, int B, int ntaps, int l, con
                       int c_out, const u64d* bias, u64d* out);
 // out[b] = sum_s taps[b][s] * pw[s] + pbias (poly 0): per-position plaintext
 // weights (the merged first layer), pw split-31 Montgomery, pbias standard
-void launch_conv_pt(Context& c, const u64d* taps, int B, int ntaps, int l, const u64d* pw, const u64d* pbias,
-                    u64d* out);
+void launch_conv_pt(Context& c, const u64d* taps, int B, int ntaps, int regions, int l, const u64d* pw,
+                    const u64d* pbias, u64d* out);
 void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, const u64d* wmont /*[c_out][ntaps][l]*/,
                      int c_out, const u64d* bias /*[c_out][l][N] mont*/, u64d* out);
 struct HsDiagTable {

@@ -232,15 +232,18 @@ __global__ void __launch_bounds__(kTpb) k_ks_inner_t(PrimeTable pt, const u64d* 
 // merged first layer: out[b][p][t][k] = sum_s tap_s[b][p][t][k] * P_s[t][k]
 // (+ the block bias on part 0), one thread per output word, taps streamed
 // from HBM once (each weight word is shared by all images through L1/L2)
-__global__ void __launch_bounds__(kTpb) k_conv_pt(PrimeTable pt, const u64d* __restrict__ taps, int ntaps, int l,
-                                                  int N, const u64d* __restrict__ pw,
+__global__ void __launch_bounds__(kTpb) k_conv_pt(PrimeTable pt, const u64d* __restrict__ taps, int ntaps,
+                                                  int regions, int l, int N, const u64d* __restrict__ pw,
                                                   const u64d* __restrict__ pbias, u64d* __restrict__ out) {
+  // tap s lives in input ciphertext s / regions (its own slot region; P_s
+  // is zero outside that region)
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = blockIdx.y % l, p = blockIdx.y / l, b = blockIdx.z;
   if (k >= N) return;
   const DevPrime pr = pt.p[t];
   const size_t ct = (size_t)2 * l * N;
-  const u64d* x = taps + (size_t)b * ntaps * ct + (size_t)p * l * N + (size_t)t * N + k;
+  const int G = (ntaps + regions - 1) / regions;
+  const u64d* x = taps + (size_t)b * G * ct + (size_t)p * l * N + (size_t)t * N + k;
   const u64d* w = pw + (size_t)t * N + k;
   AccC a;
   a.zero();
@@ -249,14 +252,14 @@ __global__ void __launch_bounds__(kTpb) k_conv_pt(PrimeTable pt, const u64d* __r
     u64d xv[4], wv[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      xv[u] = x[(size_t)(s + u) * ct];
+      xv[u] = x[(size_t)((s + u) / regions) * ct];
       wv[u] = __ldg(w + (size_t)(s + u) * l * N);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) a.mad(split31(xv[u]), wv[u]);
     a.fold();
   }
-  for (int u = 0; s < ntaps; ++s, ++u) a.mad(split31(x[(size_t)s * ct]), __ldg(w + (size_t)s * l * N));
+  for (; s < ntaps; ++s) a.mad(split31(x[(size_t)(s / regions) * ct]), __ldg(w + (size_t)s * l * N));
   u64d v = a.reduce(pr);
   if (p == 0) v = add_mod_d(v, __ldg(pbias + (size_t)t * N + k), pr.q);
   out[(size_t)b * ct + (size_t)p * l * N + (size_t)t * N + k] = v;
@@ -925,14 +928,14 @@ void launch_conv_mac_t(Context& c, const Taps& taps, double tap_bytes, int B, in
 #undef CONV_GO
 }
 
-void launch_conv_pt(Context& c, const u64d* taps, int B, int ntaps, int l, const u64d* pw, const u64d* pbias,
-                    u64d* out) {
-  const int N = c.N();
+void launch_conv_pt(Context& c, const u64d* taps, int B, int ntaps, int regions, int l, const u64d* pw,
+                    const u64d* pbias, u64d* out) {
+  const int N = c.N(), G = (ntaps + regions - 1) / regions;
   dim3 grid((N + kTpb - 1) / kTpb, 2 * l, B);
-  // taps once, weights + bias once, outputs once
-  const double bytes = 8.0 * N * l * (2.0 * B * ntaps + ntaps + 1 + 2.0 * B);
+  // tap ciphertexts once, weights + bias once, outputs once
+  const double bytes = 8.0 * N * l * (2.0 * B * G + ntaps + 1 + 2.0 * B);
   LAUNCH_BO(c, "k_conv_mac", bytes, 2.0 * N * l * B * ntaps,
-            k_conv_pt<<<grid, kTpb, 0, c.stream>>>(c.primes, taps, ntaps, l, N, pw, pbias, out));
+            k_conv_pt<<<grid, kTpb, 0, c.stream>>>(c.primes, taps, ntaps, regions, l, N, pw, pbias, out));
 }
 
 void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, const u64d* w, int c_out,

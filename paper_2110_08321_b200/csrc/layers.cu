@@ -122,16 +122,20 @@ ConvLayer::ConvLayer(Context& c, int nt, int co_n, const double* weights, const 
 }
 
 void ConvLayer::make_merged(Context& c, const double* weights, const double* bias_vals, int w_used,
-                            double tap_scale) {
+                            double tap_scale, int regs) {
   const int N = c.N(), S = c.S();
-  need((int64_t)c_out * w_used <= S, HEGPU_ERR_CAPACITY, "merged conv: c_out * d_out^2 exceeds the slots");
+  const size_t F = (size_t)c_out * w_used;
+  need((int64_t)regs * F <= S, HEGPU_ERR_CAPACITY, "merged conv: regions * c_out * d_out^2 exceeds the slots");
+  regions = regs;
   const double qlast = (double)c.P->q(level - 1);
   std::vector<u64> wire((size_t)ntaps * level * N);
 #pragma omp parallel for schedule(dynamic)
   for (int t = 0; t < ntaps; ++t) {
-    std::vector<double> z((size_t)c_out * w_used);
+    // P_t: W[co][t] on block co of tap t's region
+    const size_t off = (size_t)(t % regions) * F;
+    std::vector<double> z(off + F, 0.0);
     for (int co = 0; co < c_out; ++co)
-      std::fill_n(z.data() + (size_t)co * w_used, w_used, weights[(size_t)co * ntaps + t]);
+      std::fill_n(z.data() + off + (size_t)co * w_used, w_used, weights[(size_t)co * ntaps + t]);
     c.client->encode(z.data(), (int)z.size(), qlast, level, false, wire.data() + (size_t)t * level * N);
   }
   CK(cudaMalloc((void**)&pw, wire.size() * 8));
@@ -166,7 +170,7 @@ ConvLayer::~ConvLayer() {
 
 void ConvLayer::mac(Context& c, const CtBatch& taps, CtBatch& prod) {
   const int B = taps.count / ntaps;
-  if (merged) launch_conv_pt(c, taps.d, B, ntaps, level, pw, pbias, prod.d);
+  if (merged) launch_conv_pt(c, taps.d, taps.count / cts_per_image(), ntaps, regions, level, pw, pbias, prod.d);
   else if (HEGPU_CONV_IMMA && conv_imma_supported(c))
     launch_conv_imma(c, taps.d, B, ntaps, level, wa, cps, kbn, c_out, bias, prod.d);
   else
@@ -177,9 +181,9 @@ void ConvLayer::mac(Context& c, const CtBatch& taps, CtBatch& prod) {
 void ConvLayer::mac_compact(Context& c, const uint8_t* taps, int B, double tap_scale, CtBatch& prod) {
   // measured: expanding into full taps and streaming them through the MAC
   // beats decoding c0 / hashing c1 inside the register-heavy MAC kernel
-  u64d* full = c.alloc((size_t)B * ntaps * 2 * level * c.N());
-  launch_expand_compact(c, taps, B * ntaps, level, full);
-  if (merged) launch_conv_pt(c, full, B, ntaps, level, pw, pbias, prod.d);
+  u64d* full = c.alloc((size_t)B * cts_per_image() * 2 * level * c.N());
+  launch_expand_compact(c, taps, B * cts_per_image(), level, full);
+  if (merged) launch_conv_pt(c, full, B, ntaps, regions, level, pw, pbias, prod.d);
   else if (HEGPU_CONV_IMMA && conv_imma_supported(c))
     launch_conv_imma(c, full, B, ntaps, level, wa, cps, kbn, c_out, bias, prod.d);
   else
@@ -189,7 +193,7 @@ void ConvLayer::mac_compact(Context& c, const uint8_t* taps, int B, double tap_s
 }
 
 void ConvLayer::run(Context& c, const CtBatch& taps, CtBatch& maps) {
-  const int B = taps.count / ntaps, l = level, N = c.N(), mo = out_per_image();
+  const int B = taps.count / cts_per_image(), l = level, N = c.N(), mo = out_per_image();
   CtBatch prod{&c, B * mo, l, 0, c.alloc((size_t)B * mo * 2 * l * N)};
   mac(c, taps, prod);
   eval_rescale(c, prod, maps);

@@ -37,8 +37,11 @@ struct ConvLayer {
   // the weights become block plaintexts P_s (W[co][s] on block co, scale
   // q_{level-1}) and the bias one block plaintext, so the MAC lands each map
   // at its merged slots: ONE ciphertext per image, no merge rotations
-  void make_merged(Context& c, const double* weights, const double* bias_vals, int w_used, double tap_scale);
+  void make_merged(Context& c, const double* weights, const double* bias_vals, int w_used, double tap_scale,
+                   int regions = 1);
   bool merged = false;
+  int regions = 1;  // merged: taps per input ciphertext (tap s in region s % regions, offset region * c_out * w)
+  int cts_per_image() const { return merged ? (ntaps + regions - 1) / regions : ntaps; }
   u64d* pw = nullptr;     // [ntaps][level][N] split-31 Montgomery block plaintexts
   u64d* pbias = nullptr;  // [level][N] standard-form block bias (product scale)
   int out_per_image() const { return merged ? 1 : c_out; }

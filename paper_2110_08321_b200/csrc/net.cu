@@ -26,6 +26,12 @@ struct hegpu_net {
   Context* c = nullptr;
   hegpu_net_spec spec{};
   int d_out = 0, w_used = 0, ntaps = 0, top = 0;
+  // region packing of the fused first layer: `regions` taps share one tap
+  // ciphertext (tap s in region s % regions of ciphertext s / regions), so
+  // an image ships tap_cts = ceil(ntaps / regions) ciphertexts; after the
+  // conv one hoisted rotation sum folds the regions onto region 0
+  int regions = 1, tap_cts = 0;
+  std::unique_ptr<HsPlan> region_sum;
   double tap_scale = 0, out_scale = 0;
   std::unique_ptr<ConvLayer> conv;
   std::vector<HsPlan> plans;
@@ -118,16 +124,42 @@ void conv_meter(hegpu_net& net, int B) {
   c.meter.bump(HEGPU_ADD_PC, (int64_t)B * s.c_out);
 }
 
+// out = sum_{r < regions} rot_left(x, r F): one ModUp, regions - 1 key inner
+// products on the rotated digits, one ModDown (unit-mask HS plan)
+void region_fold(hegpu_net& net, CtBatch& x) {
+  if (net.regions <= 1) return;
+  Context& c = *net.c;
+  const int B = x.count, l = x.level, N = c.N();
+  HsPlan& pl = *net.region_sum;
+  u64d* acc = c.alloc((size_t)B * 2 * (l + 1) * N);
+  u64d* cacc = c.alloc((size_t)B * 2 * l * N);
+  u64d* tmpP = c.alloc((size_t)B * 2 * N);
+  pl.accumulate(c, x, 0, (int)pl.diag.size(), acc, cacc);
+  u64d* r = c.alloc((size_t)B * 2 * l * N);
+  DropArgs f{};
+  f.src = acc; f.src_b = 2L * (l + 1) * N; f.src_p = (long)(l + 1) * N; f.src_limbs = l + 1;
+  f.dst = r; f.dst_b = 2L * l * N; f.dst_p = (long)l * N;
+  f.pd = c.L(); f.nl = l;
+  f.add = cacc; f.add_b = 2L * l * N; f.add_p = (long)l * N; f.add_mask = 3; f.shifts = nullptr;
+  drop_last_limb(c, B, f, tmpP);
+  CK(cudaMemcpyAsync(x.d, r, x.words() * 8, cudaMemcpyDeviceToDevice, c.stream));
+  c.free(acc);
+  c.free(cacc);
+  c.free(tmpP);
+  c.free(r);
+}
+
 void run_conv(hegpu_net& net, const CtBatch& taps, CtBatch& maps) {
-  conv_meter(net, taps.count / net.ntaps);
+  conv_meter(net, taps.count / net.tap_cts);
   net.conv->run(*net.c, taps, maps);
+  region_fold(net, maps);
 }
 
 void run_after_conv(hegpu_net& net, const CtBatch& mb, CtBatch& out);
 
 void run_net(hegpu_net& net, const CtBatch& taps, CtBatch& out) {
   Context& c = *net.c;
-  const int B = taps.count / net.ntaps;
+  const int B = taps.count / net.tap_cts;
   const int mo = net.conv->out_per_image();
   Scratch maps(c, (size_t)B * mo * 2 * (net.top - 1) * c.N());
   CtBatch mb{&c, B * mo, net.top - 1, 0, maps.p};
@@ -232,8 +264,21 @@ extern "C" int hegpu_net_create(hegpu_ctx* h, const hegpu_net_spec* spec, const 
     net->tap_scale = std::ldexp(1.0, 40);
     net->conv = std::make_unique<ConvLayer>(c, net->ntaps, s.c_out, conv_w, conv_b, net->w_used, net->top,
                                             net->tap_scale);
-    net->conv->make_merged(c, conv_w, conv_b, net->w_used, net->tap_scale);  // Conv1 + Flat1 fused
+    // Conv1 + Flat1 fused, taps packed `regions` per ciphertext
+    const int F = s.c_out * net->w_used;
+    net->regions = std::max(1, std::min(net->ntaps, S / F));
+    net->tap_cts = (net->ntaps + net->regions - 1) / net->regions;
+    net->conv->make_merged(c, conv_w, conv_b, net->w_used, net->tap_scale, net->regions);
     std::vector<int64_t> rots;
+    if (net->regions > 1) {
+      std::vector<int64_t> rr{0};
+      for (int r = 1; r < net->regions; ++r) rr.push_back((S - (int64_t)r * F % S) % S);
+      std::sort(rr.begin(), rr.end());
+      net->region_sum = std::make_unique<HsPlan>();
+      net->region_sum->build_rotsum(c, rr, net->top - 1);
+      for (int64_t r : rr)
+        if (r) rots.push_back(r);
+    }
     double scale = net->tap_scale;  // after conv + rescale
     int l = net->top - 1;
     int n = s.c_out * net->w_used;
@@ -280,9 +325,9 @@ extern "C" int hegpu_net_run(hegpu_net* net, const hegpu_ct* taps, hegpu_ct* out
   if (!net || !taps || !out) return HEGPU_ERR_ARG;
   Context& c = *net->c;
   return guarded(&c, [&] {
-    need(taps->b.level == net->top && taps->b.count % net->ntaps == 0, HEGPU_ERR_SHAPE,
-         "net_run: taps must be B*ntaps ciphertexts at the top level");
-    const int B = taps->b.count / net->ntaps;
+    need(taps->b.level == net->top && taps->b.count % net->tap_cts == 0, HEGPU_ERR_SHAPE,
+         "net_run: taps must be B * tap_cts ciphertexts at the top level");
+    const int B = taps->b.count / net->tap_cts;
     need(out->b.count == B && out->b.level == net->top - 1 - 2 * net->spec.n_dense, HEGPU_ERR_SHAPE,
          "net_run: bad output handle");
     CtBatch o = out->b;
@@ -298,9 +343,9 @@ extern "C" int hegpu_net_run_split(hegpu_net* net, const hegpu_ct* taps, hegpu_c
   return guarded(&c, [&] {
     need(layer >= 0 && layer < net->spec.n_dense, HEGPU_ERR_RANGE, "net_run_split: no such dense layer");
     need(nparts >= 1 && nparts <= 8 && part >= 0 && part < nparts, HEGPU_ERR_RANGE, "net_run_split: bad part");
-    need(taps->b.level == net->top && taps->b.count % net->ntaps == 0, HEGPU_ERR_SHAPE,
-         "net_run_split: taps must be B*ntaps ciphertexts at the top level");
-    const int B = taps->b.count / net->ntaps;
+    need(taps->b.level == net->top && taps->b.count % net->tap_cts == 0, HEGPU_ERR_SHAPE,
+         "net_run_split: taps must be B * tap_cts ciphertexts at the top level");
+    const int B = taps->b.count / net->tap_cts;
     need(out->b.count == B && out->b.level == net->top - 1 - 2 * net->spec.n_dense, HEGPU_ERR_SHAPE,
          "net_run_split: bad output handle");
     net->split = {layer, part, nparts, reduce, user};
@@ -332,6 +377,7 @@ extern "C" int hegpu_net_run_compact(hegpu_net* net, const void* dev_taps, int b
     CtBatch mb{&c, batch * mo, L - 1, 0, maps.p};
     eval_rescale(c, pb, mb);
     mb.scale = net->tap_scale;
+    region_fold(*net, mb);
     CtBatch o = out->b;
     run_after_conv(*net, mb, o);
     out->b.scale = o.scale;
@@ -343,13 +389,13 @@ extern "C" int hegpu_net_run_host(hegpu_net* net, const uint64_t* host_taps, int
   Context& c = *net->c;
   return guarded(&c, [&] {
     const int N = c.N(), L = net->top, lo = net->top - 1 - 2 * net->spec.n_dense;
-    const size_t in_words = (size_t)batch * net->ntaps * 2 * L * N;
+    const size_t in_words = (size_t)batch * net->tap_cts * 2 * L * N;
     const size_t out_words = (size_t)batch * 2 * lo * N;
     Scratch stage(c, in_words);
     Scratch taps(c, in_words);
     CK(cudaMemcpyAsync(stage.p, host_taps, in_words * 8, cudaMemcpyHostToDevice, c.stream));
-    launch_wire_to_slot(c, stage.p, taps.p, (size_t)batch * net->ntaps * 2 * L, 0, L, -1);
-    CtBatch tb{&c, batch * net->ntaps, L, net->tap_scale, taps.p};
+    launch_wire_to_slot(c, stage.p, taps.p, (size_t)batch * net->tap_cts * 2 * L, 0, L, -1);
+    CtBatch tb{&c, batch * net->tap_cts, L, net->tap_scale, taps.p};
     Scratch o(c, out_words);
     CtBatch ob{&c, batch, lo, 0, o.p};
     run_net(*net, tb, ob);
@@ -360,7 +406,7 @@ extern "C" int hegpu_net_run_host(hegpu_net* net, const uint64_t* host_taps, int
 }
 
 extern "C" size_t hegpu_net_compact_image_bytes(const hegpu_net* net) {
-  return net ? (size_t)net->ntaps * net->c->client->compact_bytes(net->top) : 0;
+  return net ? (size_t)net->tap_cts * net->c->client->compact_bytes(net->top) : 0;
 }
 
 #ifndef HEGPU_NET_SUBCHUNK
@@ -456,6 +502,8 @@ void compute_pass(hegpu_net& n, const uint8_t* stage, int cur, int batch, int ch
     conv_meter(n, nm);
     CtBatch rb{&c, nm * mo, L - 1, 0, maps.p};
     eval_rescale(c, pb, rb);
+    rb.scale = n.tap_scale;
+    region_fold(n, rb);
     CtBatch mb{&c, nm * mo, L - 1, n.tap_scale, maps.p};
     CtBatch ob{&c, nm, lo, 0, o.p};
     run_after_conv(n, mb, ob);
@@ -545,6 +593,42 @@ extern "C" int hegpu_net_wait(hegpu_net* net) {
   return guarded(&c, [&] { CK(cudaStreamSynchronize(c.stream)); });
 }
 
+namespace {
+// the client's input packing (conv_pack, convlower.cpp:9-37, tap t =
+// (ci*k+ky)*k+kx, slot oy*d_out+ox) in the fused first layer's form: tap
+// ciphertext g holds taps g*R .. g*R+R-1, tap s's window replicated at the
+// c_out map offsets of its region s % R (R = net.regions)
+template <class Emit>
+void pack_image_taps(hegpu_net& net, const double* image, Emit&& emit) {
+  Context& c = *net.c;
+  const hegpu_net_spec& s = net.spec;
+  const int d = net.d_out, w = net.w_used, L = net.top, R = net.regions;
+  const int reps = net.conv->merged ? s.c_out : 1;
+  const size_t F = (size_t)reps * w;
+  std::vector<double> win((size_t)net.ntaps * w);
+  for (int ci = 0; ci < s.in_c; ++ci)
+    for (int ky = 0; ky < s.k; ++ky)
+      for (int kx = 0; kx < s.k; ++kx) {
+        const int t = (ci * s.k + ky) * s.k + kx;
+        for (int oy = 0; oy < d; ++oy)
+          for (int ox = 0; ox < d; ++ox)
+            win[(size_t)t * w + oy * d + ox] =
+                image[((size_t)ci * s.in_d + oy * s.stride + ky) * s.in_d + ox * s.stride + kx];
+      }
+  std::vector<double> z((size_t)R * F);
+  std::vector<u64> pt((size_t)L * c.N());
+  for (int g = 0; g < net.tap_cts; ++g) {
+    std::fill(z.begin(), z.end(), 0.0);
+    int used = 0;
+    for (int r = 0; r < R && g * R + r < net.ntaps; ++r, ++used)
+      for (int co = 0; co < reps; ++co)
+        std::copy_n(win.data() + (size_t)(g * R + r) * w, w, z.data() + (size_t)r * F + (size_t)co * w);
+    c.client->encode(z.data(), (int)((size_t)used * F), net.tap_scale, L, false, pt.data());
+    emit(g, pt.data());
+  }
+}
+}  // namespace
+
 extern "C" int hegpu_net_encrypt_image_compact(hegpu_net* net, const double* image, uint64_t nonce,
                                                uint8_t* taps_out) {
   if (!net || !image || !taps_out) return HEGPU_ERR_ARG;
@@ -552,26 +636,11 @@ extern "C" int hegpu_net_encrypt_image_compact(hegpu_net* net, const double* ima
   return guarded(&c, [&] {
     const int L = net->top;
     const size_t per = c.client->compact_bytes(L);
-    // same conv_pack + encode as hegpu_net_encrypt_image, same nonces: the
+    // same packing + encode as hegpu_net_encrypt_image, same nonces: the
     // compact taps expand to exactly those ciphertexts
-    const int reps = net->conv->merged ? net->spec.c_out : 1;
-    std::vector<double> z((size_t)reps * net->w_used);
-    std::vector<u64> pt((size_t)L * c.N());
-    const hegpu_net_spec& s = net->spec;
-    const int d = net->d_out;
-    for (int ci = 0; ci < s.in_c; ++ci)
-      for (int ky = 0; ky < s.k; ++ky)
-        for (int kx = 0; kx < s.k; ++kx) {
-          const int t = (ci * s.k + ky) * s.k + kx;
-          for (int oy = 0; oy < d; ++oy)
-            for (int ox = 0; ox < d; ++ox)
-              z[oy * d + ox] = image[((size_t)ci * s.in_d + oy * s.stride + ky) * s.in_d + ox * s.stride + kx];
-          for (int co = 1; co < reps; ++co)  // merged first layer: the window at every map offset
-            std::copy_n(z.data(), net->w_used, z.data() + (size_t)co * net->w_used);
-          c.client->encode(z.data(), reps * net->w_used, net->tap_scale, L, false, pt.data());
-          c.client->encrypt_compact(pt.data(), L, nonce * (uint64_t)net->ntaps + (uint64_t)t,
-                                    taps_out + (size_t)t * per);
-        }
+    pack_image_taps(*net, image, [&](int g, const u64* pt) {
+      c.client->encrypt_compact(pt, L, nonce * (uint64_t)net->tap_cts + (uint64_t)g, taps_out + (size_t)g * per);
+    });
   });
 }
 
@@ -579,27 +648,14 @@ extern "C" int hegpu_net_encrypt_image(hegpu_net* net, const double* image, uint
   if (!net || !image || !taps_out) return HEGPU_ERR_ARG;
   Context& c = *net->c;
   return guarded(&c, [&] {
-    const hegpu_net_spec& s = net->spec;
-    const int N = c.N(), L = net->top, d = net->d_out;
-    const int reps = net->conv->merged ? net->spec.c_out : 1;
-    std::vector<double> z((size_t)reps * net->w_used);
-    std::vector<u64> pt((size_t)L * N);
-    // conv_pack (convlower.cpp:9-37): tap t = (ci*k+ky)*k+kx, slot oy*d_out+ox
-    for (int ci = 0; ci < s.in_c; ++ci)
-      for (int ky = 0; ky < s.k; ++ky)
-        for (int kx = 0; kx < s.k; ++kx) {
-          const int t = (ci * s.k + ky) * s.k + kx;
-          for (int oy = 0; oy < d; ++oy)
-            for (int ox = 0; ox < d; ++ox)
-              z[oy * d + ox] = image[((size_t)ci * s.in_d + oy * s.stride + ky) * s.in_d + ox * s.stride + kx];
-          for (int co = 1; co < reps; ++co)  // merged first layer: the window at every map offset
-            std::copy_n(z.data(), net->w_used, z.data() + (size_t)co * net->w_used);
-          c.client->encode(z.data(), reps * net->w_used, net->tap_scale, L, false, pt.data());
-          c.client->encrypt(pt.data(), L, nonce * (uint64_t)net->ntaps + (uint64_t)t,
-                            taps_out + (size_t)t * 2 * L * N);
-        }
+    const int N = c.N(), L = net->top;
+    pack_image_taps(*net, image, [&](int g, const u64* pt) {
+      c.client->encrypt(pt, L, nonce * (uint64_t)net->tap_cts + (uint64_t)g, taps_out + (size_t)g * 2 * L * N);
+    });
   });
 }
+
+extern "C" int hegpu_net_tap_cts(const hegpu_net* net) { return net ? net->tap_cts : -1; }
 
 extern "C" int hegpu_net_decrypt_logits(hegpu_net* net, const uint64_t* out_ct, double* logits) {
   if (!net || !out_ct || !logits) return HEGPU_ERR_ARG;

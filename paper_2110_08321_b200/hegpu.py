@@ -168,6 +168,7 @@ def lib():
             "hegpu_net_encrypt_image_compact": (i, [vp, f64p, u, vp]),
             "hegpu_net_run_host_compact": (i, [vp, vp, i, i, vp]),
             "hegpu_net_submit_host_compact": (i, [vp, vp, i, i, vp]),
+            "hegpu_net_tap_cts": (i, [vp]),
             "hegpu_net_wait": (i, [vp]),
         }
         for name, (res, args) in sig.items():
@@ -717,7 +718,7 @@ class Net:
         ctx.check(lib().hegpu_net_create(ctx.h, C.byref(spec), cw, cb, C.cast(wp, C.c_void_p),
                                          C.cast(bp, C.c_void_p), C.byref(h)))
         self.h = h
-        self.ntaps = cfg.k * cfg.k * cfg.in_c
+        self.ntaps = int(lib().hegpu_net_tap_cts(h))  # tap ciphertexts per image (region-packed)
         self.top = ctx.L
         self.out_level = ctx.L - 1 - 2 * len(cfg.dense)
         self.tap_words = 2 * self.top * ctx.N
@@ -734,7 +735,7 @@ class Net:
         self.ctx = ctx
         self.cfg = _SpecCfg(spec)
         self.h = h
-        self.ntaps = spec.k * spec.k * spec.in_c
+        self.ntaps = int(lib().hegpu_net_tap_cts(h))
         self.top = ctx.L
         self.out_level = ctx.L - 1 - 2 * spec.n_dense
         self.tap_words = 2 * self.top * ctx.N

@@ -325,7 +325,7 @@ RunResult run_model(const Model& m, const std::vector<double>& w, const std::vec
     throw Fail{rc == HEGPU_ERR_IO ? kExitIo : kExitCapacity,
                (e && *e) ? e : hegpu_last_error(ctx.h)};
   }
-  const int ntaps = spec.k * spec.k * spec.in_c;
+  const int ntaps = hegpu_net_tap_cts(net);  // tap ciphertexts per image (region-packed)
   int n, slots, L;
   hegpu_ctx_info(ctx.h, &n, &slots, &L, nullptr);
   const int out_level = L - 1 - 2 * spec.n_dense;
