@@ -1,3 +1,4 @@
+#include <type_traits>
 // eval.cu -- pointwise RNS kernels, the key-switch inner product, the
 // conv-pack MAC, the Halevi-Shoup diagonal accumulation, and the evaluator
 // compositions (rescale, Galois rotation, square + relinearise).
@@ -656,21 +657,11 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
 // read straight from L1/L2 (consecutive positions -> coalesced; a warp of 32
 // positions x 8 images per CTA shares each fused-key word), no window
 // staging -- the windowed kernel exposed its staging latency at 16 warps/SM
-template <int LV, int IPT, bool UNIT>
-#ifndef HEGPU_NARROW_WARPS
-#define HEGPU_NARROW_WARPS 4  // image warps per CTA (measured 1: 0.459, 2: 0.451, 4: 0.454, 8: 0.490, 16: 0.621 ms)
-#endif
-__global__ void __launch_bounds__(32 * HEGPU_NARROW_WARPS) k_hs_narrow(PrimeTable pt, const u64d* __restrict__ v,
-                                                   const u64d* __restrict__ D, int B, int L, int N, HsDiagTable tab,
-                                                   u64d* __restrict__ acc, u64d* __restrict__ cacc) {
-  // IPT images per thread share every fused-key word (register reuse);
-  // UNIT: all masks are 1 (the fold's rotation sum) -> the c0 part is a sum
-  const int k = blockIdx.x * 32 + (threadIdx.x & 31), b0 = (blockIdx.y * HEGPU_NARROW_WARPS + (threadIdx.x >> 5)) * IPT;
-  const int t = blockIdx.z;
-  if (k >= N || b0 >= B) return;
+template <int LV, int IPT, bool UNIT, class Acc>
+__device__ __forceinline__ void hs_narrow_body(const DevPrime& pr, const u64d* __restrict__ v,
+                                               const u64d* __restrict__ D, int B, int N, const HsDiagTable& tab,
+                                               u64d* __restrict__ acc, u64d* __restrict__ cacc, int k, int b0, int t) {
   const int S = N >> 1, half = k >= S ? S : 0, kh = k - half;
-  const int pi = t == LV ? L : t;
-  const DevPrime pr = pt.p[pi];
   const bool has_c = t < LV;
   const size_t kp = (size_t)(LV + 1) * N, ln = (size_t)LV * N;
   const u64d* Db[IPT];
@@ -681,7 +672,7 @@ __global__ void __launch_bounds__(32 * HEGPU_NARROW_WARPS) k_hs_narrow(PrimeTabl
     Db[q] = D + ((size_t)b * LV * (LV + 1) + t) * N + half;
     c0[q] = v + (size_t)b * 2 * ln + (size_t)t * N + half;
   }
-  AccC a0[IPT], a1[IPT], cc[IPT];
+  Acc a0[IPT], a1[IPT], cc[IPT];
   u64d cs[IPT];
 #pragma unroll
   for (int q = 0; q < IPT; ++q) a0[q].zero(), a1[q].zero(), cc[q].zero(), cs[q] = 0;
@@ -703,11 +694,10 @@ __global__ void __launch_bounds__(32 * HEGPU_NARROW_WARPS) k_hs_narrow(PrimeTabl
       for (int j = 0; j < LV; ++j) {
 #pragma unroll
         for (int q = 0; q < IPT; ++q) {
-          const u64d x = split31(d[q][j]);
-          a0[q].mad(x, k0[j]);
-          a1[q].mad(x, k1[j]);
+          a0[q].mac(d[q][j], k0[j]);
+          a1[q].mac(d[q][j], k1[j]);
         }
-        if (++na == 4) {
+        if (std::is_same<Acc, AccC>::value && ++na == 4) {
 #pragma unroll
           for (int q = 0; q < IPT; ++q) a0[q].fold(), a1[q].fold();
           na = 0;
@@ -721,8 +711,8 @@ __global__ void __launch_bounds__(32 * HEGPU_NARROW_WARPS) k_hs_narrow(PrimeTabl
       } else {
         const u64d m = __ldg(tab.masks + ((size_t)i * (LV + 1) + t) * N + k);
 #pragma unroll
-        for (int q = 0; q < IPT; ++q) cc[q].mad(split31(c0[q][pos]), m);
-        if (++nc == 4) {
+        for (int q = 0; q < IPT; ++q) cc[q].mac(c0[q][pos], m);
+        if (std::is_same<Acc, AccC>::value && ++nc == 4) {
 #pragma unroll
           for (int q = 0; q < IPT; ++q) cc[q].fold();
           nc = 0;
@@ -746,6 +736,25 @@ __global__ void __launch_bounds__(32 * HEGPU_NARROW_WARPS) k_hs_narrow(PrimeTabl
       cb[ln] = !c1_term ? 0ull : UNIT ? c1 : mont_mul(c1, m0, pr.q, pr.qneg_inv);
     }
   }
+}
+
+template <int LV, int IPT, bool UNIT>
+#ifndef HEGPU_NARROW_WARPS
+#define HEGPU_NARROW_WARPS 4  // image warps per CTA (measured 1: 0.459, 2: 0.451, 4: 0.454, 8: 0.490, 16: 0.621 ms)
+#endif
+__global__ void __launch_bounds__(32 * HEGPU_NARROW_WARPS) k_hs_narrow(PrimeTable pt, const u64d* __restrict__ v,
+                                                   const u64d* __restrict__ D, int B, int L, int N, HsDiagTable tab,
+                                                   u64d* __restrict__ acc, u64d* __restrict__ cacc) {
+  // IPT images per thread share every fused-key word (register reuse);
+  // UNIT: all masks are 1 (the fold's rotation sum) -> the c0 part is a sum;
+  // limbs of a 40-bit prime accumulate fold-free in Acc20 (CTA-uniform branch)
+  const int k = blockIdx.x * 32 + (threadIdx.x & 31), b0 = (blockIdx.y * HEGPU_NARROW_WARPS + (threadIdx.x >> 5)) * IPT;
+  const int t = blockIdx.z;
+  if (k >= N || b0 >= B) return;
+  const int pi = t == LV ? L : t;
+  const DevPrime pr = pt.p[pi];
+  if (pr.q >> 40) hs_narrow_body<LV, IPT, UNIT, AccC>(pr, v, D, B, N, tab, acc, cacc, k, b0, t);
+  else hs_narrow_body<LV, IPT, UNIT, Acc20>(pr, v, D, B, N, tab, acc, cacc, k, b0, t);
 }
 
 // fused key: fk[j][p][t] = key[j][p][pi(t)] * m[t]   (t over the ext basis);

@@ -153,6 +153,29 @@ __device__ __forceinline__ u64d reduce192(u64d lo, u64d hi, uint32_t top, const 
   return mont_reduce128(lo, h, pr.q, pr.qneg_inv);
 }
 
+// 40-bit primes: operands split at 20 bits; every partial product is
+// < 2^41, so hundreds of them sum carry-free in three 64-bit words and no
+// fold is ever needed (AccC folds every 4 products).  Same integer total,
+// same reduce192 -> bit-identical to AccC.
+struct Acc20 {
+  u64d s0, s1, s2;
+  __device__ __forceinline__ void zero() { s0 = s1 = s2 = 0; }
+  // x plain (< 2^40), ys in split31 form (< 2^40)
+  __device__ __forceinline__ void mac(u64d x, u64d ys) {
+    const uint32_t x0 = (uint32_t)x & 0xFFFFFu, x1 = (uint32_t)(x >> 20);
+    const uint32_t yl = (uint32_t)ys, yh = (uint32_t)(ys >> 32);
+    const uint32_t y0 = yl & 0xFFFFFu, y1 = (yl >> 20) | (yh << 11);
+    s0 += (u64d)x0 * y0;
+    s1 += (u64d)x0 * y1 + (u64d)x1 * y0;
+    s2 += (u64d)x1 * y1;
+  }
+  __device__ __forceinline__ void fold() {}
+  __device__ __forceinline__ u64d reduce(const DevPrime& pr) {
+    const unsigned __int128 t = (unsigned __int128)s0 + ((unsigned __int128)s1 << 20) + ((unsigned __int128)s2 << 40);
+    return reduce192((u64d)t, (u64d)(t >> 64), 0u, pr);
+  }
+};
+
 struct Acc3 {  // s0 + s1 2^31 + s2 2^62 (partial), folded into lo:hi:top
   u64d s0, s1, s2, lo, hi;
   uint32_t top;
@@ -218,6 +241,7 @@ struct AccC {  // as Acc3; s0 + s1 2^31 + s2 2^62 kept as 32-bit halves
         : "+r"(a0l), "+r"(a0h), "+r"(a1l), "+r"(a1h), "+r"(a2l), "+r"(a2h)
         : "r"(x0), "r"(x1), "r"(y0), "r"(y1));
   }
+  __device__ __forceinline__ void mac(u64d x, u64d ys) { mad(split31(x), ys); }
   __device__ __forceinline__ void fold() {
     // (an __int128 formulation measured 9% slower on the HS kernel)
     const u64d s0 = ((u64d)a0h << 32) | a0l, s1 = ((u64d)a1h << 32) | a1l, s2 = ((u64d)a2h << 32) | a2l;
