@@ -233,35 +233,42 @@ __global__ void __launch_bounds__(kTpb) k_ks_inner_t(PrimeTable pt, const u64d* 
 // merged first layer: out[b][p][t][k] = sum_s tap_s[b][p][t][k] * P_s[t][k]
 // (+ the block bias on part 0), one thread per output word, taps streamed
 // from HBM once (each weight word is shared by all images through L1/L2)
-__global__ void __launch_bounds__(kTpb) k_conv_pt(PrimeTable pt, const u64d* __restrict__ taps, int ntaps,
-                                                  int regions, int l, int N, const u64d* __restrict__ pw,
+template <class Acc>
+__device__ __forceinline__ u64d conv_pt_mac(const u64d* __restrict__ x, const u64d* __restrict__ w, int G,
+                                            size_t ct, size_t wstride, const DevPrime& pr) {
+  Acc a;
+  a.zero();
+  int g = 0;
+  for (; g + 4 <= G; g += 4) {
+    u64d xv[4], wv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      xv[u] = x[(size_t)(g + u) * ct];
+      wv[u] = __ldg(w + (size_t)(g + u) * wstride);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a.mac(xv[u], wv[u]);
+    a.fold();
+  }
+  for (; g < G; ++g) a.mac(x[(size_t)g * ct], __ldg(w + (size_t)g * wstride));
+  return a.reduce(pr);
+}
+
+__global__ void __launch_bounds__(kTpb) k_conv_pt(PrimeTable pt, const u64d* __restrict__ taps, int G, int l,
+                                                  int N, const u64d* __restrict__ pw,
                                                   const u64d* __restrict__ pbias, u64d* __restrict__ out) {
-  // tap s lives in input ciphertext s / regions (its own slot region; P_s
-  // is zero outside that region)
+  // tap ciphertext g carries R taps in disjoint slot regions; pw row g is the
+  // sum of their block plaintexts (ConvLayer::make_merged), so one product
+  // per tap ciphertext; 40-bit limbs accumulate fold-free (Acc20)
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = blockIdx.y % l, p = blockIdx.y / l, b = blockIdx.z;
   if (k >= N) return;
   const DevPrime pr = pt.p[t];
   const size_t ct = (size_t)2 * l * N;
-  const int G = (ntaps + regions - 1) / regions;
   const u64d* x = taps + (size_t)b * G * ct + (size_t)p * l * N + (size_t)t * N + k;
   const u64d* w = pw + (size_t)t * N + k;
-  AccC a;
-  a.zero();
-  int s = 0;
-  for (; s + 4 <= ntaps; s += 4) {
-    u64d xv[4], wv[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      xv[u] = x[(size_t)((s + u) / regions) * ct];
-      wv[u] = __ldg(w + (size_t)(s + u) * l * N);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) a.mad(split31(xv[u]), wv[u]);
-    a.fold();
-  }
-  for (; s < ntaps; ++s) a.mad(split31(x[(size_t)(s / regions) * ct]), __ldg(w + (size_t)s * l * N));
-  u64d v = a.reduce(pr);
+  u64d v = pr.q >> 40 ? conv_pt_mac<AccC>(x, w, G, ct, (size_t)l * N, pr)
+                      : conv_pt_mac<Acc20>(x, w, G, ct, (size_t)l * N, pr);
   if (p == 0) v = add_mod_d(v, __ldg(pbias + (size_t)t * N + k), pr.q);
   out[(size_t)b * ct + (size_t)p * l * N + (size_t)t * N + k] = v;
 }
@@ -941,10 +948,10 @@ void launch_conv_pt(Context& c, const u64d* taps, int B, int ntaps, int regions,
                     const u64d* pbias, u64d* out) {
   const int N = c.N(), G = (ntaps + regions - 1) / regions;
   dim3 grid((N + kTpb - 1) / kTpb, 2 * l, B);
-  // tap ciphertexts once, weights + bias once, outputs once
-  const double bytes = 8.0 * N * l * (2.0 * B * G + ntaps + 1 + 2.0 * B);
-  LAUNCH_BO(c, "k_conv_mac", bytes, 2.0 * N * l * B * ntaps,
-            k_conv_pt<<<grid, kTpb, 0, c.stream>>>(c.primes, taps, ntaps, regions, l, N, pw, pbias, out));
+  // tap ciphertexts once, per-ciphertext weights + bias once, outputs once
+  const double bytes = 8.0 * N * l * (2.0 * B * G + G + 1 + 2.0 * B);
+  LAUNCH_BO(c, "k_conv_mac", bytes, 2.0 * N * l * B * G,
+            k_conv_pt<<<grid, kTpb, 0, c.stream>>>(c.primes, taps, G, l, N, pw, pbias, out));
 }
 
 void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, const u64d* w, int c_out,

@@ -138,9 +138,26 @@ void ConvLayer::make_merged(Context& c, const double* weights, const double* bia
       std::fill_n(z.data() + off + (size_t)co * w_used, w_used, weights[(size_t)co * ntaps + t]);
     c.client->encode(z.data(), (int)z.size(), qlast, level, false, wire.data() + (size_t)t * level * N);
   }
-  CK(cudaMalloc((void**)&pw, wire.size() * 8));
-  upload_mont(c, wire, pw, (size_t)ntaps * level, level, -1);
-  launch_split31(c, pw, wire.size());
+  // the R taps of one tap ciphertext meet the same input limb, so their
+  // plaintexts are summed once here (exact mod q; linear through the NTT):
+  // the MAC runs G = ceil(ntaps / R) products per slot instead of ntaps
+  const int G = (ntaps + regions - 1) / regions;
+  std::vector<u64> gw((size_t)G * level * N, 0);
+  for (int g = 0; g < G; ++g)
+    for (int t = 0; t < level; ++t) {
+      const u64 q = c.P->q(t);
+      u64* dst = gw.data() + ((size_t)g * level + t) * N;
+      for (int s = g * regions; s < std::min(ntaps, (g + 1) * regions); ++s) {
+        const u64* src = wire.data() + ((size_t)s * level + t) * N;
+        for (int k = 0; k < N; ++k) {
+          const u64 v = dst[k] + src[k] % q;
+          dst[k] = v >= q ? v - q : v;
+        }
+      }
+    }
+  CK(cudaMalloc((void**)&pw, gw.size() * 8));
+  upload_mont(c, gw, pw, (size_t)G * level, level, -1);
+  launch_split31(c, pw, gw.size());
   std::vector<double> zb((size_t)c_out * w_used);
   for (int co = 0; co < c_out; ++co)
     std::fill_n(zb.data() + (size_t)co * w_used, w_used, bias_vals ? bias_vals[co] : 0.0);
