@@ -508,13 +508,13 @@ constexpr int kHsBTMax = HEGPU_HS_BT;  // images per thread (smaller batches use
 // PD > 0 (small batches, where the fused keys stream from HBM once per use):
 // each thread keeps the fused-key words of the next PD - 1 diagonals in
 // flight with cp.async into its own shared-memory ring slots
-template <int LV, int kHsBT, int PD>
-__global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt, const u64d* __restrict__ v,
-                                                   const u64d* __restrict__ D, int B, int L, int N,
-                                                   HsDiagTable tab, u64d* __restrict__ acc,
-                                                   u64d* __restrict__ cacc, int gsplit, size_t part_acc,
-                                                   size_t part_cacc) {
-  extern __shared__ u64d win[];  // [BT][LV + 1][kHsW], split-31 words
+template <int LV, int kHsBT, int PD, class Acc>
+__device__ __forceinline__ void hs_diag_body(PrimeTable& pt, const u64d* __restrict__ v,
+                                             const u64d* __restrict__ D, int B, int L, int N,
+                                             const HsDiagTable& tab, u64d* __restrict__ acc,
+                                             u64d* __restrict__ cacc, int gsplit, size_t part_acc,
+                                             size_t part_cacc) {
+  extern __shared__ u64d win[];  // [BT][LV + 1][kHsW], Acc::prep words (split-31, or plain for Acc20)
   constexpr int kW = kHsKB + kHsCW;  // window row stride (compile-time -> immediate LDS offsets)
   const int S = N >> 1;
   // blockIdx.x = image tile * gsplit + diagonal group: with few images the
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
   const int nrow = do_c0 ? LV + 1 : LV;  // D digits (+ c0)
   const int ln = LV * N, kp = (LV + 1) * N;
 
-  HEGPU_HS_ACC a[kHsBT], c[kHsBT];
+  Acc a[kHsBT], c[kHsBT];
 #pragma unroll
   for (int bb = 0; bb < kHsBT; ++bb) a[bb].zero(), c[bb].zero();
 
@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
       for (int w = threadIdx.x; w < W; w += kHsKB) {
         int pos = k0 - half - r_hi + w;
         if (pos < 0) pos += S;
-        dst[w] = src ? split31(src[half + pos]) : 0ull;
+        dst[w] = src ? Acc::prep(src[half + pos]) : 0ull;
       }
     }
     __syncthreads();
@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
       const u64d* wp = wb - r;  // + (bb * (LV + 1) + row) * kW, compile-time below
       if (do_c0) {
 #pragma unroll
-        for (int bb = 0; bb < kHsBT; ++bb) c[bb].mad(wp[(bb * (LV + 1) + LV) * kW], m);
+        for (int bb = 0; bb < kHsBT; ++bb) c[bb].macw(wp[(bb * (LV + 1) + LV) * kW], m);
       }
       if (r != 0) {
         // digit-major: the BT accumulators advance in turn (independent
@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
         for (int j = 0; j < LV; ++j) {
 #pragma unroll
           for (int bb = 0; bb < kHsBT; ++bb) {
-            a[bb].mad(wp[(bb * (LV + 1) + j) * kW], kv[j]);
+            a[bb].macw(wp[(bb * (LV + 1) + j) * kW], kv[j]);
             if ((j & 3) == 3) a[bb].fold();
           }
         }
@@ -657,6 +657,20 @@ __global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt,
       else *cb = c1_term ? mont_mul(v[(size_t)b * 2 * ln + ln + (size_t)t * N + k], m0, pr.q, pr.qneg_inv) : 0ull;
     }
   }
+}
+
+template <int LV, int kHsBT, int PD>
+__global__ void __launch_bounds__(kHsKB, HEGPU_HS_MINB) k_hs_diag(PrimeTable pt, const u64d* __restrict__ v,
+                                                   const u64d* __restrict__ D, int B, int L, int N,
+                                                   HsDiagTable tab, u64d* __restrict__ acc,
+                                                   u64d* __restrict__ cacc, int gsplit, size_t part_acc,
+                                                   size_t part_cacc) {
+  // limbs of 40-bit primes accumulate fold-free in Acc20 (CTA-uniform)
+  const int t = blockIdx.z >> 1;
+  if (pt.p[t == LV ? L : t].q >> 40)
+    hs_diag_body<LV, kHsBT, PD, HEGPU_HS_ACC>(pt, v, D, B, L, N, tab, acc, cacc, gsplit, part_acc, part_cacc);
+  else
+    hs_diag_body<LV, kHsBT, PD, Acc20>(pt, v, D, B, L, N, tab, acc, cacc, gsplit, part_acc, part_cacc);
 }
 
 // narrow diagonal bands (a few rotations, e.g. the 10-row output layer):

@@ -169,6 +169,9 @@ struct Acc20 {
     s1 += (u64d)x0 * y1 + (u64d)x1 * y0;
     s2 += (u64d)x1 * y1;
   }
+  // window words: staged plain (prep), multiplied by split31 operands (macw)
+  __device__ __forceinline__ static u64d prep(u64d x) { return x; }
+  __device__ __forceinline__ void macw(u64d x, u64d ys) { mac(x, ys); }
   __device__ __forceinline__ void fold() {}
   __device__ __forceinline__ u64d reduce(const DevPrime& pr) {
     const unsigned __int128 t = (unsigned __int128)s0 + ((unsigned __int128)s1 << 20) + ((unsigned __int128)s2 << 40);
@@ -242,6 +245,8 @@ struct AccC {  // as Acc3; s0 + s1 2^31 + s2 2^62 kept as 32-bit halves
         : "r"(x0), "r"(x1), "r"(y0), "r"(y1));
   }
   __device__ __forceinline__ void mac(u64d x, u64d ys) { mad(split31(x), ys); }
+  __device__ __forceinline__ static u64d prep(u64d x) { return split31(x); }
+  __device__ __forceinline__ void macw(u64d xs, u64d ys) { mad(xs, ys); }
   __device__ __forceinline__ void fold() {
     // (an __int128 formulation measured 9% slower on the HS kernel)
     const u64d s0 = ((u64d)a0h << 32) | a0l, s1 = ((u64d)a1h << 32) | a1l, s2 = ((u64d)a2h << 32) | a2l;
@@ -295,6 +300,8 @@ struct AccW {
           "+r"(c[2])
         : "r"(x0), "r"(x1), "r"(y0), "r"(y1));
   }
+  __device__ __forceinline__ static u64d prep(u64d x) { return split31(x); }
+  __device__ __forceinline__ void macw(u64d xs, u64d ys) { mad(xs, ys); }
   __device__ __forceinline__ void fold() {}  // nothing to fold
   // s0 + s1 2^31 + s2 2^62 (each < 2^96) -> lo:hi:top, then as Acc3::reduce
   __device__ __forceinline__ u64d reduce(const DevPrime& pr) {
