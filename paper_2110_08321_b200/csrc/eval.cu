@@ -759,16 +759,19 @@ __device__ __forceinline__ void hs_narrow_body(const DevPrime& pr, const u64d* _
   }
 }
 
-template <int LV, int IPT, bool UNIT>
+template <int LV, int IPT, bool UNIT, int NC>
 #ifndef HEGPU_NARROW_WARPS
 #define HEGPU_NARROW_WARPS 4  // image warps per CTA (measured 1: 0.459, 2: 0.451, 4: 0.454, 8: 0.490, 16: 0.621 ms)
 #endif
 __global__ void __launch_bounds__(32 * HEGPU_NARROW_WARPS) k_hs_narrow(PrimeTable pt, const u64d* __restrict__ v,
-                                                   const u64d* __restrict__ D, int B, int L, int N, HsDiagTable tab,
+                                                   const u64d* __restrict__ D, int B, int L, int n_rt, HsDiagTable tab,
                                                    u64d* __restrict__ acc, u64d* __restrict__ cacc) {
   // IPT images per thread share every fused-key word (register reuse);
   // UNIT: all masks are 1 (the fold's rotation sum) -> the c0 part is a sum;
-  // limbs of a 40-bit prime accumulate fold-free in Acc20 (CTA-uniform branch)
+  // limbs of a 40-bit prime accumulate fold-free in Acc20 (CTA-uniform branch);
+  // NC: compile-time ring degree (0 = runtime) -> per-digit offsets fold
+  // into the loads' immediates
+  const int N = NC ? NC : n_rt;
   const int k = blockIdx.x * 32 + (threadIdx.x & 31), b0 = (blockIdx.y * HEGPU_NARROW_WARPS + (threadIdx.x >> 5)) * IPT;
   const int t = blockIdx.z;
   if (k >= N || b0 >= B) return;
@@ -1008,10 +1011,12 @@ void launch_hs_diag(Context& c, const u64d* v, int B, int l, const u64d* D, cons
   case LV:                                                                                                   \
     if (t.unit_masks)                                                                                        \
       LAUNCH_BO(c, "k_hs_diag", bytes, ops,                                                                  \
-                (k_hs_narrow<LV, IPT, true><<<grid, 32 * NW, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc))); \
+                (N == 8192 ? k_hs_narrow<LV, IPT, true, 8192><<<grid, 32 * NW, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc) \
+                           : k_hs_narrow<LV, IPT, true, 0><<<grid, 32 * NW, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc))); \
     else                                                                                                     \
       LAUNCH_BO(c, "k_hs_diag", bytes, ops,                                                                  \
-                (k_hs_narrow<LV, IPT, false><<<grid, 32 * NW, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc))); \
+                (N == 8192 ? k_hs_narrow<LV, IPT, false, 8192><<<grid, 32 * NW, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc) \
+                           : k_hs_narrow<LV, IPT, false, 0><<<grid, 32 * NW, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc))); \
     return;
     switch (l) { NARROW_GO(1) NARROW_GO(2) NARROW_GO(3) NARROW_GO(4) NARROW_GO(5) NARROW_GO(6) NARROW_GO(7) NARROW_GO(8) }
 #undef NARROW_GO
