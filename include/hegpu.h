@@ -262,7 +262,7 @@ int hegpu_net_run_compact(hegpu_net* net, const void* dev_taps, int batch, hegpu
  * -> output cts [B][2][1][N]); includes both host<->device copies */
 int hegpu_net_run_host(hegpu_net* net, const uint64_t* host_taps, int batch, uint64_t* host_out);
 /* client helper: conv_pack (convlower.cpp:9-37) + encode + encrypt of one
- * image [in_c][in_d][in_d] -> ntaps wire ciphertexts at the top level */
+ * image [in_c][in_d][in_d] -> hegpu_net_tap_cts(net) wire ciphertexts at the top level */
 int hegpu_net_encrypt_image(hegpu_net* net, const double* image, uint64_t nonce, uint64_t* taps_out);
 /* tap ciphertexts per image: ceil(k^2 c_in / R), R = taps packed per
  * ciphertext by the fused first layer */
