@@ -1012,10 +1012,12 @@ void launch_hs_diag(Context& c, const u64d* v, int B, int l, const u64d* D, cons
     if (t.unit_masks)                                                                                        \
       LAUNCH_BO(c, "k_hs_diag", bytes, ops,                                                                  \
                 (N == 8192 ? k_hs_narrow<LV, IPT, true, 8192><<<grid, 32 * NW, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc) \
+                 : N == 16384 ? k_hs_narrow<LV, IPT, true, 16384><<<grid, 32 * NW, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc) \
                            : k_hs_narrow<LV, IPT, true, 0><<<grid, 32 * NW, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc))); \
     else                                                                                                     \
       LAUNCH_BO(c, "k_hs_diag", bytes, ops,                                                                  \
                 (N == 8192 ? k_hs_narrow<LV, IPT, false, 8192><<<grid, 32 * NW, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc) \
+                 : N == 16384 ? k_hs_narrow<LV, IPT, false, 16384><<<grid, 32 * NW, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc) \
                            : k_hs_narrow<LV, IPT, false, 0><<<grid, 32 * NW, 0, c.stream>>>(c.primes, v, D, B, c.L(), N, t, acc, cacc))); \
     return;
     switch (l) { NARROW_GO(1) NARROW_GO(2) NARROW_GO(3) NARROW_GO(4) NARROW_GO(5) NARROW_GO(6) NARROW_GO(7) NARROW_GO(8) }
