@@ -1,19 +1,30 @@
 """bench.py -- encrypted-inference throughput of the B200 CKKS engine.
 
 Workload (BASELINE.json configs[2]): the config-0 MNIST-sized CryptoNets/
-LoLa-shaped net (conv 5x5/2 -> 5 maps via conv-packing, square, HS dense
-845->100, square, HS dense 100->10; CKKS N=8192, Delta=2^40, Q = 60+5x40
-bits, P = 60 bits) on 64 independent seeded images per GPU.  One "step" is
-one pass of the whole encrypted network over the 64-image batch.
+LoLa-shaped net on 64 independent seeded images per GPU, run with the
+reference's stages (proj/src/netcompile.cpp:321-447): conv_pack -> 25 tap
+ciphertexts per image -> conv_packed_forward + rescale (5 maps) -> merge_maps
+(4 key-switched rotations) -> square -> HS 845->100 -> square -> HS 100->10;
+CKKS N=8192, Delta=2^40, Q = 60+5x40 bits, P = 60 bits.  One "step" is one
+pass of the whole encrypted network over the 64-image batch.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Device-timed value: taps resident in HBM (1.26 GB per step > 126 MB L2, so
-no L2 flush is needed), CUDA events on the engine's own stream, max over
-ranks.  e2e: the same step through hegpu_net_run_host from pinned host
-buffers, both copies inside the timed region.  --impl reference times the
-CPU restatement (oracle/, plain C, one image per host core) -- the
-reference `hesim` itself is a plaintext simulator without CKKS and cannot
+--gpus N without a torchrun environment re-launches itself with N ranks
+(one process per GPU, NCCL; paper_2110_08321_b200.dist.launch_ranks).
+
+Device-timed `value`: the reference-layout taps resident in HBM (1.26 GB per
+step > 126 MB L2, so no L2 flush is needed), the step replayed as one CUDA
+graph, CUDA events on the engine's own stream, max over ranks.  `e2e`: the
+serving loop through the C-ABI (hegpu_net_submit_host_compact) from pinned
+host memory -- H2D of the step's compact taps (25 per image) and D2H of the
+output ciphertexts inside the timed region.  `fused` reports the same two
+numbers for the fused, region-packed first layer (HEGPU_FIRST_LAYER_FUSED,
+DESIGN.md §4.1c), which is not the reference's algorithm.
+
+--impl reference times the CPU restatement (oracle/, plain C, -O3
+-march=native) evaluating the same 64-image batch across all host cores --
+the reference `hesim` itself is a plaintext simulator without CKKS and cannot
 be built here.
 """
 from __future__ import annotations
@@ -32,10 +43,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "encrypted inferences/sec + key-switched rotations/sec, % of HBM roofline"
-KERNELS = ["k_hs_diag", "k_hs_imma", "k_drop_ntt", "k_ks_modup", "k_conv_mac", "k_intt_rows", "k_ks_intt", "k_ks_inner", "k_ntt_rows",
-           "k_wire_to_slot", "k_add", "k_tensor_square", "k_add_plain"]
+KERNELS = ["k_hs_diag", "k_hs_imma", "k_hs_narrow", "k_drop_ntt", "k_ks_modup", "k_conv_mac", "k_intt_rows",
+           "k_ks_intt", "k_ks_inner", "k_ntt_rows", "k_merge_c", "k_expand_c0", "k_expand_a", "k_wire_to_slot",
+           "k_add", "k_tensor_square", "k_add_plain"]
+NTT_KERNELS = ("k_drop_ntt", "k_ks_modup", "k_intt_rows", "k_ks_intt", "k_ntt_rows")
 UNIT = "inferences/s"
 SEED = 2110
+WORKLOAD = ("cfg2: 64 x cfg0 MNIST-sized net per GPU, reference stages (conv-pack 25 tap cts -> conv + rescale "
+            "-> merge 5 maps (4 key-switched rotations) -> square -> HS 845->100 -> square -> HS 100->10), "
+            "CKKS N=8192 L=6")
 
 
 def peaks():
@@ -53,13 +69,12 @@ def peaks():
 IMAD_WIDE_PER_CLK_SM = 59.0
 N_SM = 148
 
-
 # integer-pipe cost of one algorithmic op per kernel: a split-31 modular
 # multiply-accumulate term is 4 IMAD.WIDE.U32; an NTT
 # butterfly's Shoup product is 6 multiply instructions (modarith.cuh
 # shoup_mul_lazy4) -- the ceiling if nothing but the multiplies issued
-INT_OPS_IMAD = {"k_hs_diag": 4, "k_ks_inner": 4, "k_drop_ntt": 6, "k_ks_modup": 6, "k_intt_rows": 6,
-                "k_ks_intt": 6, "k_ntt_rows": 6}
+INT_OPS_IMAD = {"k_hs_diag": 4, "k_hs_narrow": 4, "k_ks_inner": 4, "k_drop_ntt": 6, "k_ks_modup": 6,
+                "k_intt_rows": 6, "k_ks_intt": 6, "k_ntt_rows": 6}
 # kernels whose MACs run on IMMA.16832.U8 as 64 byte-plane products each
 TENSOR_KERNELS = ("k_hs_imma", "k_conv_mac")
 IMMA_POPS = 1.1  # measured legacy mma.sync u8 rate on this B200 (tools/ubench_mma.cu)
@@ -82,15 +97,16 @@ def int_pipe_roofline(name, kd, clk_mhz):
 
 def ncu_traffic(kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
-    from the committed ncu --set full captures (profiles/), or None"""
-    for name in ("r01_traffic_step.json", "r01_ncu_traffic.json"):
+    from the newest committed ncu --set full capture of one step (profiles/),
+    or None"""
+    for name in ("r02_traffic_step.json", "r01_traffic_step.json"):
         try:
             with open(os.path.join(ROOT, "profiles", name)) as f:
                 t = json.load(f)
-            return float(t[kernel]["per_launch_bytes"])
+            return float(t[kernel]["per_launch_bytes"]), name
         except Exception:
             continue
-    return None
+    return None, None
 
 
 class ClockSampler:
@@ -146,40 +162,58 @@ def dist_env():
 
 
 # --------------------------------------------------------------------------- CPU
-def _cpu_worker(args):
-    """one image through the CPU restatement; returns seconds of evaluation"""
-    n_images, seed = args
+def _cpu_prepare(images):
+    """oracle state for the reference algorithm + the client's taps of `images`"""
     from oracle import ckks_pipeline as P
     from oracle.ckks import Ckks
     from paper_2110_08321_b200.workloads import CFG0, net_image, net_weights
     cfg = CFG0
     ck = Ckks(cfg.log_n, list(cfg.qbits), cfg.pbits, seed=SEED)
-    # the reference's algorithm (per-map conv + merge; the GPU's fused first
-    # layer is not the reference's, so the baseline does not get it)
+    # the reference's algorithm (per-map conv + rescale + merge), as the GPU arm
     prep = P.PreparedNet(ck, cfg, net_weights(cfg, SEED), merged=False)
-    taps = [P.conv_pack_taps(ck, cfg, net_image(cfg, seed + i), seed + i, prep.tap_scale, merged=False)
-            for i in range(n_images)]
-    t0 = time.perf_counter()
-    for t in taps:
-        prep.eval(t)
-    return time.perf_counter() - t0, n_images
+    taps = [P.conv_pack_taps(ck, cfg, net_image(cfg, i), i, prep.tap_scale, merged=False) for i in images]
+    return prep, taps
 
 
-def cpu_throughput(cores, images_per_core):
-    """inferences/s of the CPU port on `cores` processes (one image stream each)."""
+def _cpu_pool_worker(rank, nproc, n_images, steps, barrier, q):
+    prep, taps = _cpu_prepare([i for i in range(n_images) if i % nproc == rank])
+    for s in range(steps):
+        barrier.wait()
+        t0 = time.perf_counter()
+        for t in taps:
+            prep.eval(t)
+        q.put((s, rank, time.perf_counter() - t0))
+
+
+def cpu_batch_throughput(cores, n_images, steps):
+    """the CPU port evaluating an `n_images` batch on `cores` processes
+    (images dealt round-robin, keys / masks / taps prepared before the timed
+    region, every step starting at a barrier): per step, inferences/s =
+    n_images / the slowest process's evaluation time"""
     if cores == 1:
-        dt, n = _cpu_worker((images_per_core, 1000))
-        return n / dt, f"{n} cfg0 image(s) evaluated on 1 core ({dt:.1f} s), keys/masks/taps prepared offline"
+        prep, taps = _cpu_prepare(range(n_images))
+        vals = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            for t in taps:
+                prep.eval(t)
+            vals.append(n_images / (time.perf_counter() - t0))
+        return vals, f"{n_images} cfg0 image(s) evaluated on 1 core per step, keys/masks/taps prepared offline"
     import multiprocessing as mp
     ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
-        t0 = time.perf_counter()
-        res = pool.map(_cpu_worker, [(images_per_core, 1000 + 100 * i) for i in range(cores)])
-        wall = time.perf_counter() - t0
-    n = sum(r[1] for r in res)
-    per_core = [r[1] / r[0] for r in res]
-    return float(sum(per_core)), (f"{n} cfg0 images, {images_per_core} per process on {cores} processes "
-                                  f"(eval-only throughput summed over processes; wall {wall:.1f} s incl. setup)")
+    barrier, q = ctx.Barrier(cores), ctx.Queue()
+    procs = [ctx.Process(target=_cpu_pool_worker, args=(r, cores, n_images, steps, barrier, q)) for r in range(cores)]
+    for p in procs:
+        p.start()
+    res = [q.get() for _ in range(cores * steps)]
+    for p in procs:
+        p.join()
+    per_step = {}
+    for s, _, dt in res:
+        per_step[s] = max(per_step.get(s, 0.0), dt)
+    vals = [n_images / per_step[s] for s in sorted(per_step)]
+    return vals, (f"{n_images} cfg0 images per step dealt over {cores} processes (one per host core), "
+                  f"step time = slowest process; keys/masks/taps prepared before timing")
 
 
 def run_reference(args):
@@ -187,20 +221,16 @@ def run_reference(args):
     if rank != 0:
         return
     from oracle import ckks
-    ckks.build()
+    ckks.use_native()  # -march=native build of the port, compiled on this host
     cores = os.cpu_count() or 1
-    vals = []
-    for _ in range(args.warmup):
-        pass  # the CPU port has no warm-up state beyond key generation (excluded)
-    for _ in range(max(1, args.steps)):
-        v, sample = cpu_throughput(cores, 1)
-        vals.append(v)
+    steps = max(1, args.steps)
+    vals, sample = cpu_batch_throughput(cores, args.batch, steps + max(0, min(args.warmup, 1)))
+    vals = vals[-steps:]  # the first step warms page cache / allocator when warmup > 0
     v = float(np.median(vals))
-    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 64_000.0 / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": args.batch * 1e3 / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u64 (RNS mod q)", "data": "synthetic (seeded U[0,1] images, N(0,0.05^2) f32 weights)",
-            "config": {"workload": "cfg2: 64 x cfg0 MNIST-sized net, CKKS N=8192",
-                       "global_batch": 64, "parallelism": f"{cores} host processes"},
+            "config": {"workload": WORKLOAD, "global_batch": args.batch, "parallelism": f"{cores} host processes"},
             "impl": "reference",
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -214,207 +244,206 @@ def run_gpu(args):
 
     from paper_2110_08321_b200 import dist as D
     from paper_2110_08321_b200 import hegpu as H
-    from paper_2110_08321_b200.workloads import CFG0, net_image, net_weights
+    from paper_2110_08321_b200.workloads import CFG0, net_image, net_weights, plain_forward
 
     rank, world, local = dist_env()
     if world > 1:
         dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
     cfg = CFG0
     B = args.batch
+    weights = net_weights(cfg, SEED)
     ctx = H.Context(cfg.log_n, list(cfg.qbits), cfg.pbits, seed=SEED, device=local)
-    net = H.Net(ctx, cfg, net_weights(cfg, SEED))
-    # client side (outside the timed region): conv-pack + encrypt this rank's images
-    taps = np.concatenate([net.encrypt_image(net_image(cfg, i), nonce=i) for i in D.image_range(rank, B)])
-    # the same ciphertexts in the compact fresh form the client ships (seeded
-    # c1, byte-packed c0): the device step reads these straight from HBM
-    compact = np.concatenate([net.encrypt_image_compact(net_image(cfg, i), nonce=i)
-                              for i in D.image_range(rank, B)])
-    dtaps = ctx.ct(B * net.ntaps, net.top, taps, 2.0 ** 40)
-    dcompact = torch.from_numpy(compact).to(f"cuda:{local}")
-    out = ctx.ct(B, net.out_level)
-
-    def device_pass():
-        if args.input == "compact":
-            net.run_compact(dcompact, B, out)
-        else:
-            net.run(dtaps, out)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=local)
-    gather_buf = torch.empty(B * net.out_words, dtype=torch.int64, device=f"cuda:{local}")
-    gathered = torch.empty(world * B * net.out_words, dtype=torch.int64, device=f"cuda:{local}") if world > 1 else None
-
-    graph = None
-
-    def run_once():
-        if graph is not None:
-            graph()
-        else:
-            device_pass()
-
-    def step():
-        run_once()
-        if world > 1:  # NCCL all-gather of the output ciphertexts (config 2)
-            out.export_device(gather_buf.data_ptr())
-            with torch.cuda.stream(stream):
-                D.gather_outputs(gather_buf, world, gathered)
-
-    for _ in range(args.warmup):
-        step()
-    ctx.sync()
-    # one step's HOP tally and kernel launches (counted while issuing it)
-    ctx.reset_meter()
-    l0 = ctx.launches()
-    if args.graph:  # the whole step as one CUDA graph: no host launch gaps
-        graph = ctx.capture(device_pass)
-    else:
-        device_pass()
-    ctx.sync()
-    launches_per_step = ctx.launches() - l0
-    tally = ctx.total()
-    for _ in range(2):
-        step()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        ev1.synchronize()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    launches = launches_per_step * args.steps
-    ms_max = D.max_over_ranks(ev0.elapsed_time(ev1) / args.steps, device=f"cuda:{local}")
-    value = B * world / (ms_max / 1e3)
-    per_step_rot = tally[4]
-    per_step_ks = per_step_rot + tally[3]  # rotations + relinearisations
-
-    # ---- per-kernel device time (CUDA events around every launch of one
-    # kernel, one extra device-resident step per kernel) -> roofline
-    kernels = {}
-    for name in KERNELS:
-        ctx.kernel_timer(name)
-        device_pass()  # direct launches (the timer brackets each one)
-        kms, kn, kbytes, kops = ctx.kernel_timer_read_ops()
-        if kn:
-            kernels[name] = {"ms_per_step": kms, "launches": kn, "alg_bytes": kbytes,
-                             "gbs": kbytes / (kms / 1e3) / 1e9 if kms > 0 else None,
-                             "modmuls": kops, "gmodmul_s": kops / (kms / 1e3) / 1e9 if kms > 0 else None,
-                             "share": kms / ms_max}
-    clk_mhz = clk.summary()["sm_mhz"] or 1965.0
-    for name, kd in kernels.items():
-        kd["compute_roofline"] = int_pipe_roofline(name, kd, clk_mhz)
-    ctx.kernel_timer(None)
-    dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
-    ntt_rows = sum(kernels[k]["modmuls"] for k in ("k_drop_ntt", "k_ks_modup", "k_intt_rows", "k_ks_intt",
-                                                  "k_ntt_rows") if k in kernels) / (
-        (1 << (cfg.log_n - 1)) * cfg.log_n)
     hbm, which = peaks()
-    kd = kernels[dom]
-    traffic = ncu_traffic(dom)
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": kd["gbs"], "peak": hbm, "unit": "GB/s",
-                "frac": kd["gbs"] / hbm, "traffic": traffic, "peak_source": which,
-                "alg_bytes_per_launch": kd["alg_bytes"] / kd["launches"],
-                "avg_launch_ms": kd["ms_per_step"] / kd["launches"], "launches_per_step": kd["launches"],
-                "share_of_step": kd["share"],
-                # the kernel is bound by the 64-bit multiply-accumulate issue
-                # rate, not HBM: its integer-pipe roofline
-                "int_pipe": int_pipe_roofline(dom, kd, clk_mhz),
-                "note": "alg bytes / modmuls per launch per DESIGN.md §5; traffic = ncu dram bytes per launch "
-                        "of one step (profiles/r01_traffic_step.json: ncu --metrics dram__bytes_read.sum,"
-                        "dram__bytes_write.sum over tools/one_step.py; L2-resident producer->consumer data "
-                        "makes it lower than the algorithmic bytes)"}
+    images = {i: net_image(cfg, i) for i in D.image_range(rank, B)}
 
-    # ---- correctness spot check (outside timing): decrypt one output
-    host_out = out.download()
-    logits = net.decrypt_logits(host_out[: net.out_words])
-
-    # ---- e2e through the public C-ABI from pinned host buffers: the client's
-    # compact taps (c0 byte-packed + a-stream keys) go H2D chunk by chunk,
-    # overlapped with the previous chunk's compute; outputs come back D2H
-    pin_in = torch.from_numpy(compact).pin_memory()
-    pin_out = torch.empty(B * net.out_words, dtype=torch.int64).pin_memory()
-
-    def e2e_time(fn):
-        # >= 4 passes: each of the two staging buffers runs once direct and is
-        # then captured into a CUDA graph before the timed region
-        for _ in range(max(4, args.warmup)):
-            fn()
+    def timed(fn, steps):
+        """device time per call of fn over `steps` calls, max over ranks"""
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             fn()
         e1.record(stream)
         e1.synchronize()
-        return D.max_over_ranks(e0.elapsed_time(e1) / args.steps, device=f"cuda:{local}")
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        return D.max_over_ranks(e0.elapsed_time(e1) / steps, device=dev)
 
-    # serving loop: every step is one submit (H2D of that step's compact taps,
-    # compute, D2H of its outputs); step k+1's uploads overlap step k's
-    # compute.  The timed region ends when the last step's outputs are on
-    # the host.
-    def serve_step():
-        net.submit_host_compact(pin_in, B, pin_out, args.chunk)
+    def measure(first_layer, detail):
+        net = H.Net(ctx, cfg, weights, first_layer=first_layer)
+        # client side (outside the timed region): conv-pack + encrypt this rank's images
+        taps = np.concatenate([net.encrypt_image(images[i], nonce=i) for i in images])
+        compact = np.concatenate([net.encrypt_image_compact(images[i], nonce=i) for i in images])
+        dtaps = ctx.ct(B * net.tap_cts, net.top, taps, 2.0 ** 40)
+        out = ctx.ct(B, net.out_level)
+        gather_buf = torch.empty(B * net.out_words, dtype=torch.int64, device=dev)
+        gathered = torch.empty(world * B * net.out_words, dtype=torch.int64, device=dev) if world > 1 else None
+        for _ in range(args.warmup):
+            net.run(dtaps, out)
+        ctx.sync()
+        # one step's HOP tally, executed key-switch work and kernel launches
+        ctx.reset_meter()
+        l0 = ctx.launches()
+        graph = ctx.capture(lambda: net.run(dtaps, out)) if args.graph else None
+        if graph is None:
+            net.run(dtaps, out)
+        ctx.sync()
+        launches_per_step = ctx.launches() - l0
+        tally, ks = ctx.total(), ctx.ks_counters()
 
-    e2e_ms = e2e_time(serve_step)
-    net.wait()
-    assert np.array_equal(pin_out.numpy().view(np.uint64), host_out), "e2e output differs from device run"
-    # one synchronous call per step (no cross-step overlap)
-    sync_ms = e2e_time(lambda: net.run_host_compact(pin_in, B, pin_out, args.sync_chunk))
-    assert np.array_equal(pin_out.numpy().view(np.uint64), host_out), "sync e2e output differs from device run"
-    # the uncompressed full-ciphertext path, for reference
-    pin_full = torch.from_numpy(taps.view(np.int64)).pin_memory()
-    full_ms = e2e_time(lambda: net.run_host(pin_full, B, pin_out))
-    assert np.array_equal(pin_out.numpy().view(np.uint64), host_out), "full e2e output differs from device run"
+        def step():
+            if graph is not None:
+                graph()
+            else:
+                net.run(dtaps, out)
+            if world > 1:  # NCCL all-gather of the output ciphertexts (config 2)
+                out.export_device(gather_buf.data_ptr())
+                with torch.cuda.stream(stream):
+                    D.gather_outputs(gather_buf, world, gathered)
 
+        for _ in range(2):
+            step()
+        with ClockSampler(local) as clk:
+            ms = timed(step, args.steps)
+        host_out = out.download()
+        # sanity (outside timing): decrypted logits of this rank's first image
+        # against the cleartext network
+        i0 = next(iter(images))
+        logits = net.decrypt_logits(host_out[: net.out_words])
+        err = float(np.abs(logits - plain_forward(cfg, weights, images[i0])).max())
+        assert err < 1e-3, f"{first_layer}: decrypted logits off by {err}"
+
+        # e2e through the public C-ABI from pinned host buffers: the client's
+        # compact taps (c0 byte-packed + a-stream keys) go H2D in sub-chunks
+        # overlapped with compute; outputs come back D2H
+        pin_in = torch.from_numpy(compact).pin_memory()
+        pin_out = torch.empty(B * net.out_words, dtype=torch.int64).pin_memory()
+
+        def serve_step():  # step k+1's uploads overlap step k's compute
+            net.submit_host_compact(pin_in, B, pin_out, args.chunk)
+
+        for _ in range(max(4, args.warmup)):  # both staging buffers: direct, then captured
+            serve_step()
+        net.wait()
+        e2e_ms = timed(serve_step, args.steps)
+        net.wait()
+        assert np.array_equal(pin_out.numpy().view(np.uint64), host_out), "e2e output differs from device run"
+        res = {"ms": ms, "value": B * world / (ms / 1e3), "e2e_ms": e2e_ms,
+               "e2e_value": B * world / (e2e_ms / 1e3), "h2d": int(compact.nbytes), "d2h": int(host_out.nbytes),
+               "tally": tally, "ks": ks, "launches_per_step": launches_per_step, "clk": clk.summary(),
+               "logit_err": err, "tap_cts": net.tap_cts, "compact_bytes": int(compact.nbytes),
+               "full_bytes": int(taps.nbytes)}
+        if detail:
+            res["e2e_sync_ms"] = timed(lambda: net.run_host_compact(pin_in, B, pin_out, args.sync_chunk),
+                                       max(2, args.steps // 2))
+            # ---- per-kernel device time (CUDA events around every launch of
+            # one kernel, one extra direct-launch step per kernel) -> roofline
+            kernels = {}
+            for name in KERNELS:
+                ctx.kernel_timer(name)
+                net.run(dtaps, out)
+                kms, kn, kbytes, kops = ctx.kernel_timer_read_ops()
+                if kn:
+                    kernels[name] = {"ms_per_step": kms, "launches": kn, "alg_bytes": kbytes,
+                                     "gbs": kbytes / (kms / 1e3) / 1e9 if kms > 0 else None,
+                                     "modmuls": kops, "gmodmul_s": kops / (kms / 1e3) / 1e9 if kms > 0 else None,
+                                     "share": kms / ms}
+            ctx.kernel_timer(None)
+            res["kernels"] = kernels
+        del graph, dtaps, out, net
+        ctx.sync()
+        return res
+
+    ref = measure("reference", True)
+    fused = measure("fused", False) if not args.no_fused else None
+
+    kernels = ref["kernels"]
+    clk_mhz = ref["clk"]["sm_mhz"] or 1965.0
+    for name, kd in kernels.items():
+        kd["compute_roofline"] = int_pipe_roofline(name, kd, clk_mhz)
+    dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
+    kd = kernels[dom]
+    traffic, traffic_src = ncu_traffic(dom)
+    ms_max = ref["ms"]
+    sec = ms_max / 1e3
+    ntt_rows = sum(kernels[k]["modmuls"] for k in NTT_KERNELS if k in kernels) / ((1 << (cfg.log_n - 1)) * cfg.log_n)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": kd["gbs"], "peak": hbm, "unit": "GB/s",
+                "frac": kd["gbs"] / hbm, "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": which,
+                "alg_bytes_per_launch": kd["alg_bytes"] / kd["launches"],
+                "avg_launch_ms": kd["ms_per_step"] / kd["launches"], "launches_per_step": kd["launches"],
+                "share_of_step": kd["share"],
+                # the NTT-family kernels are bound by the 64-bit multiply issue
+                # rate more than HBM: their integer-pipe roofline (DESIGN.md §5)
+                "int_pipe": int_pipe_roofline(dom, kd, clk_mhz),
+                "note": "alg bytes / modmuls per launch per DESIGN.md §5 (LAUNCH_B byte models at each launch "
+                        "site); achieved = alg bytes / summed CUDA-event launch time on the engine stream; "
+                        "traffic = ncu dram bytes per launch of one step (profiles/)"}
+    tally, ks = ref["tally"], ref["ks"]
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": ref["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64 (RNS mod q, 60/40-bit primes)",
         "data": "synthetic (seeded U[0,1] 28x28 images padded to 29x29, N(0,0.05^2) f32 weights)",
-        "config": {"workload": "cfg2: 64 x cfg0 MNIST-sized net per GPU (conv-pack 25 cts -> merge -> "
-                               "square -> HS 845->100 -> square -> HS 100->10), CKKS N=8192 L=6",
-                   "global_batch": B * world, "images_per_gpu": B, "parallelism": f"dp{world} (image sharding)",
-                   "input": args.input,
-                   "l2": ("inputs 0.43 GB (compact) / 1.26 GB (full) per step > L2, no flush")},
-        "rotations_per_s": per_step_rot * world / (ms_max / 1e3),
-        "rotation_metering": ("reference HOP semantics (hesim's per-stage tally: 120 rotations per cfg-0 "
-                              "inference); the engine runs fewer key switches than that -- HS diagonals and "
-                              "folds hoisted, Conv1 + Flat1 fused (DESIGN.md §4)"),
+        "config": {"workload": WORKLOAD, "first_layer": "reference", "global_batch": B * world,
+                   "images_per_gpu": B, "parallelism": f"dp{world} (image sharding, NCCL all-gather of outputs)",
+                   "tap_cts_per_image": ref["tap_cts"],
+                   "l2": (f"device-resident inputs {ref['full_bytes'] / 1e9:.2f} GB of full tap ciphertexts per "
+                          f"step (> 126 MB L2): no flush needed; e2e H2D {ref['compact_bytes'] / 1e6:.0f} MB "
+                          f"compact taps per step")},
+        # reference HOP semantics: hesim's per-stage tally (120 rotations +
+        # 2 relinearisations per cfg-0 inference)
+        "rotations_per_s": tally[4] * world / sec,
+        "keyswitches_per_s": (tally[4] + tally[3]) * world / sec,
+        "rotation_metering": "reference HOP semantics (hesim per-stage OpTally); see `performed` for the "
+                             "key-switch work actually executed (hoisted HS diagonals share one ModUp)",
+        "performed": {"per_step": ks, "modups_per_s": ks["modups"] * world / sec,
+                      "key_inner_products_per_s": ks["key_inner_products"] * world / sec,
+                      "moddowns_per_s": ks["moddowns"] * world / sec,
+                      "rescales_per_s": ks["rescales"] * world / sec},
         # limb transforms per second: every NTT-family launch's butterflies
         # / (N/2 log2 N) (one transform = one limb of one polynomial)
-        "ntts_per_s": ntt_rows * world / (ms_max / 1e3),
-        "ntts_per_step": ntt_rows,
-        "keyswitches_per_s": per_step_ks * world / (ms_max / 1e3),
+        "ntts_per_s": ntt_rows * world / sec, "ntts_per_step": ntt_rows,
         "hops_per_inference": {k: v / B for k, v in zip(H.TALLY_FIELDS, tally)},
         "cuda_graph": bool(args.graph),
-        "gpu_launches": launches,
+        "gpu_launches": ref["launches_per_step"] * args.steps,
         "roofline": roofline,
         "kernels": kernels,
-        "clocks": clk.summary(),
-        "e2e": {"value": B * world / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(compact.nbytes),
-                "d2h_bytes_per_step": int(host_out.nbytes), "ms_per_step": e2e_ms,
-                "path": "hegpu_net_submit_host_compact per step (compact taps; step k+1 H2D overlaps step k "
-                        "compute), timed to the last step's outputs on the host",
+        "clocks": ref["clk"],
+        "e2e": {"value": ref["e2e_value"], "unit": UNIT, "h2d_bytes_per_step": ref["h2d"] * world,
+                "d2h_bytes_per_step": ref["d2h"] * world, "ms_per_step": ref["e2e_ms"],
+                "path": "hegpu_net_submit_host_compact per step (25 compact tap cts per image; step k+1 H2D "
+                        "overlaps step k compute), timed to the last step's outputs on the host",
                 "chunk": args.chunk},
-        "e2e_sync": {"value": B * world / (sync_ms / 1e3), "unit": UNIT, "ms_per_step": sync_ms,
-                     "path": "hegpu_net_run_host_compact (one blocking call per step, chunked H2D overlap)",
-                     "chunk": args.sync_chunk},
-        "e2e_uncompressed": {"value": B * world / (full_ms / 1e3), "unit": UNIT,
-                             "h2d_bytes_per_step": int(taps.nbytes), "ms_per_step": full_ms,
-                             "path": "hegpu_net_run_host (full wire ciphertexts)"},
-        "logits_sample": [float(x) for x in logits[:3]],
+        "e2e_sync": {"value": B * world / (ref["e2e_sync_ms"] / 1e3), "unit": UNIT, "ms_per_step": ref["e2e_sync_ms"],
+                     "path": "hegpu_net_run_host_compact (one blocking call per step)", "chunk": args.sync_chunk},
+        "logit_max_abs_err": ref["logit_err"],
         "peak_hbm_gbs": hbm, "peak_source": which,
     }
+    if fused is not None:
+        fsec = fused["ms"] / 1e3
+        line["fused"] = {
+            "note": "Conv1 + Flat1 fused by client-side replicated, region-packed taps (HEGPU_FIRST_LAYER_FUSED, "
+                    "DESIGN.md §4.1c) -- not the reference's first-layer algorithm; same HOP tally",
+            "value": fused["value"], "unit": UNIT, "ms_per_step": fused["ms"], "tap_cts_per_image": fused["tap_cts"],
+            "e2e": {"value": fused["e2e_value"], "unit": UNIT, "ms_per_step": fused["e2e_ms"],
+                    "h2d_bytes_per_step": fused["h2d"] * world, "d2h_bytes_per_step": fused["d2h"] * world},
+            "performed_per_step": fused["ks"], "gpu_launches_per_step": fused["launches_per_step"],
+            "rotations_per_s": fused["tally"][4] * world / fsec, "clocks": fused["clk"],
+            "logit_max_abs_err": fused["logit_err"]}
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, sample = cpu_throughput(1, args.cpu_images)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
+        from oracle import ckks
+        ckks.use_native()
+        vals, sample = cpu_batch_throughput(1, args.cpu_images, 1)
+        line["cpu_baseline"] = {"value": vals[0], "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    del net, dtaps, dcompact, out
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
@@ -427,14 +456,21 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="hegpu", choices=["hegpu", "reference"])
     ap.add_argument("--batch", type=int, default=64, help="images per GPU")
-    ap.add_argument("--cpu-images", type=int, default=8)
+    ap.add_argument("--cpu-images", type=int, default=24, help="images in the 1-core cpu_baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--chunk", type=int, default=64, help="images per compute chunk in the pipelined e2e (serving) loop (region-packed taps: 16: 10.9k, 32: 13.5k, 64: 14.8k inf/s)")
+    ap.add_argument("--no-fused", action="store_true", help="skip the fused-first-layer extra measurement")
+    ap.add_argument("--chunk", type=int, default=64, help="images per compute chunk in the pipelined e2e loop")
     ap.add_argument("--sync-chunk", type=int, default=32, help="images per chunk in the blocking e2e call")
     ap.add_argument("--graph", type=int, default=1, help="replay the device step as one CUDA graph")
-    ap.add_argument("--input", default="full", choices=["compact", "full"],
-                    help="device-resident input form: compact fresh taps (client wire form) or full ciphertexts")
     args = ap.parse_args()
+    rank, world, _ = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl != "reference":
+        # one process per GPU: re-launch under torch.distributed.run
+        from paper_2110_08321_b200.dist import launch_ranks
+        sys.exit(launch_ranks(args.gpus, os.path.abspath(__file__), sys.argv[1:]))
+    if "WORLD_SIZE" in os.environ and world != args.gpus and args.impl != "reference":
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
     else:

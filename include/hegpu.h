@@ -115,6 +115,14 @@ int hegpu_num_stages(const hegpu_ctx* ctx);
 int hegpu_stage_tally(const hegpu_ctx* ctx, int idx, char* label, int label_len, int64_t tally[5]);
 int hegpu_total_tally(const hegpu_ctx* ctx, int64_t tally[5]);
 int hegpu_reset_meter(hegpu_ctx* ctx);
+/* key-switch work the engine actually executed since the last
+ * hegpu_reset_meter (the OpTally above keeps the reference's HOP semantics,
+ * where a hoisted or fused rotation still counts as one Rot): out[0] ModUps
+ * (a polynomial decomposed and lifted to the extended basis), out[1] key
+ * inner products (one evaluation key applied to one ModUp'd polynomial),
+ * out[2] ModDowns (an extended-basis accumulator divided by P), out[3]
+ * rescales (a ciphertext batch entry dropping one prime) */
+int hegpu_ks_counters(const hegpu_ctx* ctx, int64_t out[4]);
 
 /* ---- client side (host CPU; the reference's pack/conv_pack are client-side,
  *      proj/include/hesim/convlower.hpp:20-23, proj/src/slotvec.cpp:26-40) --- */
@@ -231,10 +239,22 @@ int64_t hegpu_lola_slot_of_row(const hegpu_lola_plan* plan, int row);
 int hegpu_lola_matvec(hegpu_ctx* ctx, const hegpu_lola_plan* plan, const hegpu_ct* v, hegpu_ct* out);
 
 /* ---- stage driver: execute (proj/src/netcompile.cpp:291-446) ------------ */
+/* first-layer execution (hegpu_net_spec.first_layer):
+ *  REFERENCE (default, 0): the reference's stages as lower() emits them
+ *    (proj/src/netcompile.cpp:321-347): the client ships k^2 c_in conv_pack
+ *    tap ciphertexts (proj/src/convlower.cpp:9-37), the server runs
+ *    conv_packed_forward + rescale into c_out map ciphertexts, then
+ *    merge_maps with c_out - 1 key-switched rotations (convlower.cpp:145-160);
+ *  FUSED (1): Conv1 + Flat1 fused by client-side replicated, region-packed
+ *    taps: ceil(k^2 c_in / R) tap ciphertexts, no merge key
+ *    switches, R - 1 hoisted region-fold key switches.
+ * Both meter the reference's per-stage HOPs. */
+enum { HEGPU_FIRST_LAYER_REFERENCE = 0, HEGPU_FIRST_LAYER_FUSED = 1 };
 typedef struct {
   int in_c, in_d, k, stride, c_out;  /* first-layer conv (ConvPack stage) */
   int n_dense;                       /* Square+Dense pairs that follow */
   int dense_out[4];
+  int first_layer;                   /* HEGPU_FIRST_LAYER_* */
 } hegpu_net_spec;
 /* weights: conv_w [c_out][in_c][k][k], conv_b [c_out], then per dense layer
  * W (row-major m x n) and b [m]; all f64 */
@@ -242,7 +262,8 @@ int hegpu_net_create(hegpu_ctx* ctx, const hegpu_net_spec* spec, const double* c
                      const double* conv_b, const double* const* dense_w,
                      const double* const* dense_b, hegpu_net** out);
 void hegpu_net_destroy(hegpu_net* net);
-/* device-resident run: taps = count B*ntaps at the top level */
+/* device-resident run: taps = count B * hegpu_net_tap_cts(net) at the top
+ * level; out = count B at level L - 1 - 2 n_dense */
 int hegpu_net_run(hegpu_net* net, const hegpu_ct* taps, hegpu_ct* out);
 /* config 3 across GPUs ("partial sums reduced across GPUs"): the same run,
  * but dense layer `layer`'s HS accumulates only diagonal range `part` of
@@ -258,19 +279,22 @@ int hegpu_net_run_split(hegpu_net* net, const hegpu_ct* taps, hegpu_ct* out, int
  * bytes, as hegpu_net_encrypt_image_compact writes them): the conv MAC
  * decodes c0 and regenerates c1 on the fly */
 int hegpu_net_run_compact(hegpu_net* net, const void* dev_taps, int batch, hegpu_ct* out);
-/* end-to-end run from host buffers (wire format taps [B][ntaps][2][L][N]
- * -> output cts [B][2][1][N]); includes both host<->device copies */
+/* end-to-end run from host buffers (wire format taps [B][tap_cts][2][L][N]
+ * -> output cts [B][2][L-1-2 n_dense][N]); includes both host<->device copies */
 int hegpu_net_run_host(hegpu_net* net, const uint64_t* host_taps, int batch, uint64_t* host_out);
 /* client helper: conv_pack (convlower.cpp:9-37) + encode + encrypt of one
  * image [in_c][in_d][in_d] -> hegpu_net_tap_cts(net) wire ciphertexts at the top level */
 int hegpu_net_encrypt_image(hegpu_net* net, const double* image, uint64_t nonce, uint64_t* taps_out);
-/* tap ciphertexts per image: ceil(k^2 c_in / R), R = taps packed per
- * ciphertext by the fused first layer */
+/* tap ciphertexts per image: k^2 c_in for the reference first layer (tap t
+ * = (ci*k+ky)*k+kx carries the window on slots [0, d_out^2)), ceil(k^2 c_in / R)
+ * for the fused one (R taps packed per ciphertext) */
 int hegpu_net_tap_cts(const hegpu_net* net);
+/* HEGPU_FIRST_LAYER_* the net was built with */
+int hegpu_net_first_layer(const hegpu_net* net);
 /* the same taps in compact form (hegpu_net_compact_image_bytes per image) */
 size_t hegpu_net_compact_image_bytes(const hegpu_net* net);
 int hegpu_net_encrypt_image_compact(hegpu_net* net, const double* image, uint64_t nonce, uint8_t* taps_out);
-/* end-to-end run from compact host taps [batch][ntaps] -> output cts (wire);
+/* end-to-end run from compact host taps [batch][tap_cts] -> output cts (wire);
  * the batch is processed in chunks of `chunk` images (0 = automatic) with the
  * next chunk's host->device copy overlapping the current chunk's compute */
 int hegpu_net_run_host_compact(hegpu_net* net, const uint8_t* host_taps, int batch, int chunk, uint64_t* host_out);

@@ -31,6 +31,36 @@ def build() -> str:
     return _LIB_PATH
 
 
+def _cpu_fingerprint() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def use_native() -> str:
+    """switch this process to the -march=native build, compiled on the
+    machine that runs it (rebuilt when the host CPU model differs from the
+    one it was built for) -- the CPU baseline's build.
+    Must be called before the first lib()."""
+    global _LIB_PATH
+    src = os.path.join(_HERE, "ckks_oracle.c")
+    path = os.path.join(_HERE, "libckks_oracle_native.so")
+    stamp = path + ".cpu"
+    fp = _cpu_fingerprint()
+    have = open(stamp).read() if os.path.exists(stamp) else None
+    if (not os.path.exists(path) or have != fp or os.path.getmtime(path) < os.path.getmtime(src)):
+        subprocess.check_call(["make", "-s", "-C", _HERE, "native"])
+        with open(stamp, "w") as f:
+            f.write(fp)
+    _LIB_PATH = path
+    return path
+
+
 def lib():
     global _lib
     if _lib is None:

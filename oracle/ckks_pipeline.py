@@ -93,7 +93,7 @@ def square(ck, v, level, rlk):
     return ck.rescale(ck.square(v, level, rlk), level)
 
 
-def conv_pack_taps(ck, cfg, image, nonce, tap_scale, merged=True):
+def conv_pack_taps(ck, cfg, image, nonce, tap_scale, merged=False):
     """Client side: conv_pack (proj/src/convlower.cpp:9-37) + encode + encrypt,
     nonces nonce*ntaps + t (same convention as hegpu_net_encrypt_image).
     merged: the stage driver's fused Conv1 + Flat1 -- each tap's window is
@@ -164,7 +164,7 @@ class PreparedNet:
     """Server-side offline state for one model (keys, encoded HS masks,
     bias plaintexts) so that eval() times only the homomorphic evaluation."""
 
-    def __init__(self, ck, cfg, weights, merged=True):
+    def __init__(self, ck, cfg, weights, merged=False):
         """merged: Conv1 + Flat1 fused as the GPU stage driver runs them
         (replicated taps); False: the reference's per-map conv + merge
         (proj/src/netcompile.cpp:321-347) -- the CPU baseline's algorithm."""
@@ -234,11 +234,13 @@ class PreparedNet:
         return x
 
 
-def run_net(ck, cfg, weights, image, nonce=0, keys=None):
+def run_net(ck, cfg, weights, image, nonce=0, keys=None, merged=False):
     """Full oracle pipeline for one image (client encryption included);
-    returns (output ct at the last level, output scale)."""
-    prep = PreparedNet(ck, cfg, weights)
-    taps = conv_pack_taps(ck, cfg, image, nonce, prep.tap_scale)
+    returns (output ct at the last level, output scale).  merged=False: the
+    reference's first layer (conv_pack taps, per-map conv, merge), the GPU
+    net's default; True: the fused, region-packed first layer."""
+    prep = PreparedNet(ck, cfg, weights, merged=merged)
+    taps = conv_pack_taps(ck, cfg, image, nonce, prep.tap_scale, merged=merged)
     return prep.eval(taps), prep.out_scale
 
 

@@ -59,6 +59,7 @@ thread_local std::string g_create_error;
 template <typename F>
 int guarded(Context* c, F&& f) {
   try {
+    bind_device(c);
     f();
     return HEGPU_OK;
   } catch (const Error& e) {
@@ -151,6 +152,7 @@ extern "C" int hegpu_ctx_create(const hegpu_params* p, int device, hegpu_ctx** o
 extern "C" void hegpu_ctx_destroy(hegpu_ctx* h) {
   if (!h) return;
   Context& c = h->c;
+  try { bind_device(&c); } catch (...) {}
   if (c.stream) cudaStreamSynchronize(c.stream);
   for (auto& kv : c.rot_keys) cudaFree(kv.second.data);
   if (c.relin.data) cudaFree(c.relin.data);
@@ -220,6 +222,7 @@ extern "C" int hegpu_graph_launch(hegpu_graph* gr) {
 
 extern "C" void hegpu_graph_destroy(hegpu_graph* gr) {
   if (!gr) return;
+  try { bind_device(gr->c); } catch (...) {}
   cudaStreamSynchronize(gr->c->stream);
   cudaGraphExecDestroy(gr->exec);
   cudaGraphDestroy(gr->g);
@@ -297,6 +300,12 @@ extern "C" int hegpu_total_tally(const hegpu_ctx* h, int64_t t[5]) {
 extern "C" int hegpu_reset_meter(hegpu_ctx* h) {
   if (!h) return HEGPU_ERR_ARG;
   h->c.meter = Meter();
+  h->c.ks = {};
+  return HEGPU_OK;
+}
+extern "C" int hegpu_ks_counters(const hegpu_ctx* h, int64_t out[4]) {
+  if (!h || !out) return HEGPU_ERR_ARG;
+  for (int i = 0; i < 4; ++i) out[i] = h->c.ks[i];
   return HEGPU_OK;
 }
 
@@ -418,6 +427,7 @@ extern "C" int hegpu_ct_create(hegpu_ctx* h, int count, int level, hegpu_ct** ou
 
 extern "C" void hegpu_ct_destroy(hegpu_ct* t) {
   if (!t) return;
+  try { bind_device(t->b.ctx); } catch (...) {}
   cudaStreamSynchronize(t->b.ctx->stream);
   cudaFree(t->b.d);
   delete t;
@@ -488,6 +498,7 @@ extern "C" int hegpu_pt_create(hegpu_ctx* h, int count, int level, int with_p, h
 
 extern "C" void hegpu_pt_destroy(hegpu_pt* t) {
   if (!t) return;
+  try { bind_device(t->b.ctx); } catch (...) {}
   cudaStreamSynchronize(t->b.ctx->stream);
   cudaFree(t->b.d);
   delete t;
@@ -678,7 +689,11 @@ extern "C" int hegpu_conv_plan_create(hegpu_ctx* h, int ntaps, const double* wei
   });
 }
 
-extern "C" void hegpu_conv_plan_destroy(hegpu_conv_plan* p) { delete p; }
+extern "C" void hegpu_conv_plan_destroy(hegpu_conv_plan* p) {
+  if (!p) return;
+  try { bind_device(p->layer ? p->layer->ctx : nullptr); } catch (...) {}
+  delete p;
+}
 
 extern "C" int hegpu_conv_plan_run(hegpu_ctx* h, const hegpu_conv_plan* p, const hegpu_ct* taps, hegpu_ct* maps) {
   if (!h || !p || !taps || !maps) return HEGPU_ERR_ARG;
@@ -738,6 +753,7 @@ extern "C" int hegpu_hs_plan_create(hegpu_ctx* h, const double* A, int m, int n,
 
 extern "C" void hegpu_hs_plan_destroy(hegpu_hs_plan* p) {
   if (!p) return;
+  try { bind_device(p->p.ctx); } catch (...) {}
   p->p.release();
   delete p;
 }
@@ -843,6 +859,7 @@ extern "C" int hegpu_lola_plan_create(hegpu_ctx* h, int kind, const double* A, i
 
 extern "C" void hegpu_lola_plan_destroy(hegpu_lola_plan* p) {
   if (!p) return;
+  try { bind_device(p->p.ctx); } catch (...) {}
   p->p.release();
   delete p;
 }

@@ -219,11 +219,9 @@ bool conv_imma_supported(Context& c) { return c.N() % kImmaPos == 0; }
 template <int MPT>
 void conv_imma_go(Context& c, dim3 grid, size_t sm, double bytes, double ops, const u64d* taps, int ntaps, int l,
                   const uint4* w4, int groups_n, int kbn, int c_out, const u64d* bias, u64d* out, const ConvLimbs& lim) {
-  static bool prepared = false;
-  if (!prepared && sm > 48 * 1024) {
+  static PerDeviceOnce prepared;
+  if (sm > 48 * 1024 && prepared.first())
     CK(cudaFuncSetAttribute(k_conv_imma<MPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    prepared = true;
-  }
   LAUNCH_BO(c, "k_conv_mac", bytes, ops,
             k_conv_imma<MPT><<<grid, 32 * kImmaWarps, sm, c.stream>>>(c.primes, taps, ntaps, l, c.N(), w4, groups_n,
                                                                      kbn, c_out, bias, out, lim));

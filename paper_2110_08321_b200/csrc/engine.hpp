@@ -72,6 +72,9 @@ struct Context {
   size_t ktimer_used = 0;
   double ktimer_bytes = 0;
   double ktimer_ops = 0;  // algorithmic modular multiply(-accumulate)s
+  // key-switch work actually executed (hegpu_ks_counters): ModUps, key
+  // inner products, ModDowns, rescaled ciphertexts
+  std::array<int64_t, 4> ks{};
 
   int N() const { return P->n; }
   int S() const { return P->slots; }
@@ -104,6 +107,40 @@ struct PtBatch {
 // ---------------------------------------------------------------- launchers
 void check_cuda(cudaError_t e, const char* what);
 #define CK(x) ::hegpu::check_cuda((x), #x)
+
+enum { KS_MODUP = 0, KS_INNER = 1, KS_MODDOWN = 2, KS_RESCALE = 3 };
+
+// every C-ABI call binds the context's device first, so contexts on
+// different GPUs can be driven from one thread (single-process multi-GPU)
+inline void bind_device(const Context* c) {
+  if (c && c->device >= 0 && c->stream) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != c->device) check_cuda(cudaSetDevice(c->device), "cudaSetDevice");
+  }
+}
+inline int current_device() {
+  int d = 0;
+  check_cuda(cudaGetDevice(&d), "cudaGetDevice");
+  return d;
+}
+// one-time per-device setup (cudaFuncSetAttribute and device attributes are
+// per device): true the first time it is asked for the current device
+struct PerDeviceOnce {
+  unsigned long long mask = 0;
+  bool first() {
+    const unsigned long long bit = 1ull << (current_device() & 63);
+    if (mask & bit) return false;
+    mask |= bit;
+    return true;
+  }
+};
+// streaming multiprocessors of the current device (cached per device)
+inline int device_sms() {
+  static int sms[64] = {0};
+  const int d = current_device() & 63;
+  if (!sms[d]) check_cuda(cudaDeviceGetAttribute(&sms[d], cudaDevAttrMultiProcessorCount, d), "sm count");
+  return sms[d];
+}
 
 // Brackets one kernel launch: counts it and, when the context's kernel
 // timer names this kernel, records start/stop events around it.

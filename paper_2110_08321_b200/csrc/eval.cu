@@ -836,7 +836,7 @@ void launch_hs_lvbt(Context& c, const u64d* v, int B, const u64d* D, const HsDia
   if (S < kHsKB) fail(HEGPU_ERR_ARG, "hs_matvec on the device needs N >= 256");
   dim3 grid((B + kHsBT - 1) / kHsBT, N / kHsKB, 2 * (LV + 1));
   const size_t sm = ((size_t)kHsBT * (LV + 1) * (kHsKB + kHsCW) + (size_t)PD * (LV + 1) * kHsKB) * 8;
-  static size_t done = 0;
+  static size_t done_dev[64] = {0}; size_t& done = done_dev[current_device() & 63];
   if (sm > 48 * 1024 && sm > done) {
     CK(cudaFuncSetAttribute(k_hs_diag<LV, kHsBT, PD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     done = sm;
@@ -908,13 +908,14 @@ void launch_tensor_square(Context& c, const u64d* a, u64d* d01, u64d* d2, int co
 }
 
 void ks_inner(Context& c, const u64d* D, int B, int l, const KeyRowMap& keys, u64d* acc) {
+  c.ks[KS_INNER] += B;
   const int per = keys.period, rows_per_key = (B + per - 1) / per;
   const int tiles = (rows_per_key + kKsKT - 1) / kKsKT;
   dim3 grid((c.N() + kTpb - 1) / kTpb, l + 1, per * tiles);
   double kb = 0;  // distinct keys read once each
   for (int i = 0; i < per && i < B; ++i) kb += 8.0 * l * 2 * (l + 1) * c.N();
   const size_t sm = (HEGPU_KS_STAGE && kKsKT == 1) ? (size_t)3 * l * kTpb * 8 : 0;
-  static size_t done = 0;
+  static size_t done_dev[64] = {0}; size_t& done = done_dev[current_device() & 63];
   if (sm > 48 * 1024 && sm > done) {
     CK(cudaFuncSetAttribute(k_ks_inner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     done = sm;
@@ -945,7 +946,7 @@ void launch_conv_mac_t(Context& c, const Taps& taps, double tap_bytes, int B, in
   if (sm > 200 * 1024) fail(HEGPU_ERR_CAPACITY, "conv_packed_forward: too many taps");
 #define CONV_GO(CO)                                                                                        \
   case CO: {                                                                                               \
-    static size_t done = 0;                                                                                \
+    static size_t done_dev[64] = {0}; size_t& done = done_dev[current_device() & 63];                                                                                \
     if (sm > 48 * 1024 && sm > done) {                                                                     \
       CK(cudaFuncSetAttribute(k_conv_mac<CO, Taps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
       done = sm;                                                                                           \
@@ -1081,6 +1082,7 @@ void eval_merge(Context& c, const CtBatch& maps, int nmaps, const KeyRowMap& km,
   kg.grp = G;
   kg.grp_stride = (long)(nmaps * st);
   ks_modup(c, maps.d + st + (size_t)l * N, (long)st, B * G, l, &kg, tmp, D);
+  c.ks[KS_INNER] += (int64_t)B * G;
   dim3 gi((N + kTpb - 1) / kTpb, l + 1, (B + kKsKT - 1) / kKsKT);
   const double sbytes = 8.0 * N * ((double)B * G * l * (l + 1) + 2.0 * G * l * (l + 1) + 2.0 * B * (l + 1));
   const double sops = 2.0 * N * B * G * l * (l + 1);

@@ -408,11 +408,9 @@ __global__ void k_hs_cacc(const u64d* __restrict__ v, const u64d* __restrict__ m
 
 template <int J, int PL>
 void hs_imma_go(Context& c, const HiArgs& a, size_t smem, int grid, double bytes, double ops) {
-  static bool prepared = false;
-  if (!prepared) {
+  static PerDeviceOnce prepared;
+  if (prepared.first())
     CK(cudaFuncSetAttribute(k_hs_imma<J, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHiSmemMax));
-    prepared = true;
-  }
   LAUNCH_BO(c, "k_hs_imma", bytes, ops, (k_hs_imma<J, PL><<<grid, 32 * kHiWarps, smem, c.stream>>>(a)));
 }
 
@@ -473,12 +471,7 @@ void launch_hs_imma(Context& c, const u64d* v, int B, int l, const u64d* D, cons
   a.r_hi = ch.r_hi;
   a.nig = (B + kHiBc - 1) / kHiBc;
   a.accumulate = accumulate;
-  static int sms = 0;
-  if (!sms) {
-    int d = 0;
-    CK(cudaGetDevice(&d));
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d));
-  }
+  const int sms = device_sms();
   // ring: the block's steps [sfirst(kh0), sfirst(kh0 + 12) + NSG)
   a.RS = ch.ns + (12 * J + 31) / 32 + 1;
   if (a.RS > kHiRSMax) fail(HEGPU_ERR_ARG, "hs_imma: chunk span exceeds the window ring");

@@ -493,6 +493,7 @@ void HsPlan::ensure_imma(Context& c) {
 void HsPlan::accumulate(Context& c, const CtBatch& v, int i_lo, int i_hi, u64d* acc, u64d* cacc) {
   const int B = v.count, l = level, N = c.N();
   ensure_keys(c);
+  for (int i = i_lo; i < i_hi; ++i) c.ks[KS_INNER] += diag[i].shift != 0 ? B : 0;
   if (use_imma(c, B, i_lo, i_hi)) {
     ensure_imma(c);
     u64d* tmp = c.alloc((size_t)B * l * N);

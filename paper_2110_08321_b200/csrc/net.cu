@@ -61,6 +61,7 @@ struct hegpu_net {
     cudaGraph_t g = nullptr;
     cudaGraphExec_t exec = nullptr;
     std::vector<std::pair<std::string, std::array<int64_t, 5>>> meter;
+    std::array<int64_t, 4> ks{};
     int64_t launches = 0;
   };
   std::vector<ServeGraph> serve_graphs;
@@ -96,6 +97,7 @@ void need(bool ok, int code, const std::string& msg) {
 template <typename F>
 int guarded(Context* c, F&& f) {
   try {
+    bind_device(c);
     f();
     return HEGPU_OK;
   } catch (const Error& e) {
@@ -173,10 +175,11 @@ void run_after_conv(hegpu_net& net, const CtBatch& mb, CtBatch& out) {
   const hegpu_net_spec& s = net.spec;
   const int mo = net.conv->out_per_image(), B = mb.count / mo, N = c.N();
   int l = mb.level;
-  // Flat1: Merge (netcompile.cpp:332-347).  With the merged first layer the
-  // maps already sit at their merged offsets (one ciphertext per image): the
-  // stage's HOPs are the reference's (c_out - 1 rotations + additions), no
-  // key switch runs
+  // Flat1: Merge (netcompile.cpp:332-347): c_out - 1 key-switched
+  // rotations summed lazily with one ModDown per image (eval_merge).  With
+  // the fused first layer the maps already sit at their merged offsets (one
+  // ciphertext per image) and no key switch runs; the
+  // stage meters the reference's HOPs either way
   c.meter.begin("Flat1");
   Scratch cur(c, (size_t)B * 2 * l * N);
   CtBatch x{&c, B, l, 0, cur.p};
@@ -246,6 +249,8 @@ extern "C" int hegpu_net_create(hegpu_ctx* h, const hegpu_net_spec* spec, const 
     const hegpu_net_spec& s = *spec;
     need(c.device >= 0 && c.stream, HEGPU_ERR_CUDA, "client-only context: the evaluator needs a CUDA device");
     need(s.n_dense >= 1 && s.n_dense <= 4, HEGPU_ERR_SHAPE, "net: 1..4 dense layers supported");
+    need(s.first_layer == HEGPU_FIRST_LAYER_REFERENCE || s.first_layer == HEGPU_FIRST_LAYER_FUSED, HEGPU_ERR_ARG,
+         "net: unknown first_layer");
     need(s.k >= 1 && s.stride >= 1 && s.k <= s.in_d, HEGPU_ERR_SHAPE, "net: window larger than input");
     auto net = std::make_unique<hegpu_net>();
     net->c = &c;
@@ -264,12 +269,20 @@ extern "C" int hegpu_net_create(hegpu_ctx* h, const hegpu_net_spec* spec, const 
     net->tap_scale = std::ldexp(1.0, 40);
     net->conv = std::make_unique<ConvLayer>(c, net->ntaps, s.c_out, conv_w, conv_b, net->w_used, net->top,
                                             net->tap_scale);
-    // Conv1 + Flat1 fused, taps packed `regions` per ciphertext
-    const int F = s.c_out * net->w_used;
-    net->regions = std::max(1, std::min(net->ntaps, S / F));
-    net->tap_cts = (net->ntaps + net->regions - 1) / net->regions;
-    net->conv->make_merged(c, conv_w, conv_b, net->w_used, net->tap_scale, net->regions);
     std::vector<int64_t> rots;
+    const int F = s.c_out * net->w_used;
+    if (s.first_layer == HEGPU_FIRST_LAYER_FUSED) {
+      // Conv1 + Flat1 fused, taps packed `regions` per ciphertext
+      net->regions = std::max(1, std::min(net->ntaps, S / F));
+      net->conv->make_merged(c, conv_w, conv_b, net->w_used, net->tap_scale, net->regions);
+    } else {
+      // the reference's stages: conv_pack taps (one window per ciphertext),
+      // conv_packed_forward + rescale -> c_out maps, merge_maps with the
+      // right rotations j * d_out^2, j = 1 .. c_out - 1 (convlower.cpp:145-160)
+      net->regions = 1;
+      for (int j = 1; j < s.c_out; ++j) rots.push_back((int64_t)j * net->w_used % S);
+    }
+    net->tap_cts = (net->ntaps + net->regions - 1) / net->regions;
     if (net->regions > 1) {
       std::vector<int64_t> rr{0};
       for (int r = 1; r < net->regions; ++r) rr.push_back((S - (int64_t)r * F % S) % S);
@@ -317,6 +330,7 @@ extern "C" int hegpu_net_create(hegpu_ctx* h, const hegpu_net_spec* spec, const 
 
 extern "C" void hegpu_net_destroy(hegpu_net* net) {
   if (!net) return;
+  try { bind_device(net->c); } catch (...) {}
   cudaStreamSynchronize(net->c->stream);
   delete net;
 }
@@ -540,11 +554,13 @@ void serve_compute(hegpu_net& n, const uint8_t* stage, int cur, int batch, int c
       for (int f = 0; f < 5; ++f) c.meter.bump(f, st.second[f]);
     }
     c.launches += sg->launches;
+    for (int k = 0; k < 4; ++k) c.ks[k] += sg->ks[k];
     CK(cudaGraphLaunch(sg->exec, c.stream));
     return;
   }
   if (sg->uses++ == 0) return compute_pass(n, stage, cur, batch, chunk, host_out, false);  // warm-up pass
   const auto before = c.meter.stages;
+  const auto ks0 = c.ks;
   const int64_t l0 = c.launches;
   CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
   try {
@@ -565,6 +581,7 @@ void serve_compute(hegpu_net& n, const uint8_t* stage, int cur, int batch, int c
     sg->meter.emplace_back(st.first, d);
   }
   sg->launches = c.launches - l0;
+  for (int k = 0; k < 4; ++k) sg->ks[k] = c.ks[k] - ks0[k];
   CK(cudaGraphLaunch(sg->exec, c.stream));
 }
 
@@ -656,6 +673,7 @@ extern "C" int hegpu_net_encrypt_image(hegpu_net* net, const double* image, uint
 }
 
 extern "C" int hegpu_net_tap_cts(const hegpu_net* net) { return net ? net->tap_cts : -1; }
+extern "C" int hegpu_net_first_layer(const hegpu_net* net) { return net ? net->spec.first_layer : -1; }
 
 extern "C" int hegpu_net_decrypt_logits(hegpu_net* net, const uint64_t* out_ct, double* logits) {
   if (!net || !out_ct || !logits) return HEGPU_ERR_ARG;

@@ -473,9 +473,9 @@ void prep_kernel(K kernel, size_t bytes) {
 
 #define NTT_GO(LG, KERNEL, GRID, ...)                                                               \
   do {                                                                                              \
-    static bool prepared = false;                                                                   \
+    static PerDeviceOnce prepared;                                                                  \
     const size_t smb = ntt_smem(1 << LG);                                                           \
-    if (!prepared) { prep_kernel(KERNEL<LG>, smb); prepared = true; }                                \
+    if (prepared.first()) prep_kernel(KERNEL<LG>, smb);                                             \
     LAUNCH_BO(c, #KERNEL, _ntt_bytes, (double)(GRID) * (LG << (LG - 1)),                           \
               KERNEL<LG><<<(GRID), (1 << LG) >> lr_of(LG), smb, c.stream>>>(__VA_ARGS__));          \
   } while (0)
@@ -572,9 +572,9 @@ void NTT_PUB(drop_last_limb)(Context& c, int B, const DropArgs& a, u64d* tmpP) {
 #undef NTT_GO
 #define NTT_GO(LG, KERNEL, GRID, ...)                                                               \
   do {                                                                                              \
-    static bool prepared = false;                                                                   \
+    static PerDeviceOnce prepared;                                                                  \
     const size_t smb = drop_smem_words(1 << LG) * 8;                                                \
-    if (!prepared) { prep_kernel(KERNEL<LG>, smb); prepared = true; }                                \
+    if (prepared.first()) prep_kernel(KERNEL<LG>, smb);                                             \
     LAUNCH_BO(c, #KERNEL, _ntt_bytes, (double)(GRID) * (LG << (LG - 1)),                           \
               KERNEL<LG><<<(GRID), (1 << LG) >> lr_of(LG), smb, c.stream>>>(__VA_ARGS__));          \
   } while (0)
@@ -583,9 +583,9 @@ void NTT_PUB(drop_last_limb)(Context& c, int B, const DropArgs& a, u64d* tmpP) {
 #undef NTT_GO
 #define NTT_GO(LG, KERNEL, GRID, ...)                                                               \
   do {                                                                                              \
-    static bool prepared = false;                                                                   \
+    static PerDeviceOnce prepared;                                                                  \
     const size_t smb = ntt_smem(1 << LG);                                                           \
-    if (!prepared) { prep_kernel(KERNEL<LG>, smb); prepared = true; }                                \
+    if (prepared.first()) prep_kernel(KERNEL<LG>, smb);                                             \
     LAUNCH_BO(c, #KERNEL, _ntt_bytes, (double)(GRID) * (LG << (LG - 1)),                           \
               KERNEL<LG><<<(GRID), (1 << LG) >> lr_of(LG), smb, c.stream>>>(__VA_ARGS__));          \
   } while (0)
@@ -602,9 +602,13 @@ void launch_intt_rows(Context& c, const u64d* src, u64d* dst, int n_outer, int n
 }
 void ks_modup(Context& c, const u64d* src, long src_stride, int B, int l, const KeyRowMap* shifts, u64d* tmp,
               u64d* D) {
+  c.ks[KS_MODUP] += B;
   ks_modup_r16(c, src, src_stride, B, l, shifts, tmp, D);
 }
-void drop_last_limb(Context& c, int B, const DropArgs& a, u64d* tmpP) { drop_last_limb_r8(c, B, a, tmpP); }
+void drop_last_limb(Context& c, int B, const DropArgs& a, u64d* tmpP) {
+  c.ks[a.pd == c.L() ? KS_MODDOWN : KS_RESCALE] += B;
+  drop_last_limb_r8(c, B, a, tmpP);
+}
 #endif
 
 }  // namespace hegpu

@@ -45,3 +45,32 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(nproc: int, script: str, args, env=None, timeout=None) -> int:
+    """one process per GPU on this node: re-launch `script args` under
+    torch.distributed.run with `nproc` ranks (rendezvous on 127.0.0.1; the
+    ranks read RANK / LOCAL_RANK / WORLD_SIZE / MASTER_* from the
+    environment).  NCCL_DEBUG=INFO unless the caller set it, so the
+    communicator setup lines show up in the log.  Returns the exit code; the
+    ranks' stdout / stderr pass through."""
+    import os
+    import subprocess
+    import sys
+    e = dict(os.environ)
+    e.setdefault("NCCL_DEBUG", "INFO")
+    e.setdefault("OMP_NUM_THREADS", "4")
+    if env:
+        e.update(env)
+    for k in ("RANK", "LOCAL_RANK", "WORLD_SIZE", "LOCAL_WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT"):
+        e.pop(k, None)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", script, *map(str, args)]
+    return subprocess.run(cmd, env=e, timeout=timeout).returncode

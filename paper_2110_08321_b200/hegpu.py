@@ -56,7 +56,11 @@ class Params(C.Structure):
 
 class NetSpec(C.Structure):
     _fields_ = [("in_c", C.c_int), ("in_d", C.c_int), ("k", C.c_int), ("stride", C.c_int),
-                ("c_out", C.c_int), ("n_dense", C.c_int), ("dense_out", C.c_int * 4)]
+                ("c_out", C.c_int), ("n_dense", C.c_int), ("dense_out", C.c_int * 4),
+                ("first_layer", C.c_int)]
+
+
+FIRST_LAYERS = {"reference": 0, "fused": 1}  # HEGPU_FIRST_LAYER_*
 
 
 _lib = None
@@ -95,6 +99,7 @@ def lib():
             "hegpu_stage_tally": (i, [vp, i, C.c_char_p, i, i64p]),
             "hegpu_total_tally": (i, [vp, i64p]),
             "hegpu_reset_meter": (i, [vp]),
+            "hegpu_ks_counters": (i, [vp, i64p]),
             "hegpu_encode": (i, [vp, f64p, i, d, i, i, u64p]),
             "hegpu_decode": (i, [vp, u64p, i, d, f64p]),
             "hegpu_encrypt": (i, [vp, u64p, i, u, u64p]),
@@ -169,6 +174,7 @@ def lib():
             "hegpu_net_run_host_compact": (i, [vp, vp, i, i, vp]),
             "hegpu_net_submit_host_compact": (i, [vp, vp, i, i, vp]),
             "hegpu_net_tap_cts": (i, [vp]),
+            "hegpu_net_first_layer": (i, [vp]),
             "hegpu_net_wait": (i, [vp]),
         }
         for name, (res, args) in sig.items():
@@ -321,6 +327,14 @@ class Context:
 
     def reset_meter(self):
         self.check(lib().hegpu_reset_meter(self.h))
+
+    KS_FIELDS = ("modups", "key_inner_products", "moddowns", "rescales")
+
+    def ks_counters(self):
+        """key-switch work actually executed since reset_meter (hegpu_ks_counters)"""
+        t = np.zeros(4, dtype=np.int64)
+        self.check(lib().hegpu_ks_counters(self.h, t))
+        return dict(zip(self.KS_FIELDS, (int(x) for x in t)))
 
     def launches(self):
         return int(lib().hegpu_kernel_launches(self.h))
@@ -701,10 +715,14 @@ class Net:
     """Stage driver (execute, proj/src/netcompile.cpp:291-446) for the
     Conv -> (Square -> Dense)* family on a batch of images."""
 
-    def __init__(self, ctx, cfg, weights):
+    def __init__(self, ctx, cfg, weights, first_layer="reference"):
+        """first_layer: "reference" (k^2 c_in conv_pack taps, per-map conv +
+        rescale, merge_maps with c_out - 1 key switches; the reference's
+        stages) or "fused" (region-packed replicated taps)"""
         self.ctx, self.cfg = ctx, cfg
         spec = NetSpec()
         spec.in_c, spec.in_d, spec.k, spec.stride, spec.c_out = cfg.in_c, cfg.in_d, cfg.k, cfg.s, cfg.c_out
+        spec.first_layer = FIRST_LAYERS[first_layer]
         spec.n_dense = len(cfg.dense)
         for k, m in enumerate(cfg.dense):
             spec.dense_out[k] = m
@@ -718,9 +736,15 @@ class Net:
         ctx.check(lib().hegpu_net_create(ctx.h, C.byref(spec), cw, cb, C.cast(wp, C.c_void_p),
                                          C.cast(bp, C.c_void_p), C.byref(h)))
         self.h = h
-        self.ntaps = int(lib().hegpu_net_tap_cts(h))  # tap ciphertexts per image (region-packed)
+        self._post_init()
+
+    def _post_init(self):
+        h, ctx = self.h, self.ctx
+        self.tap_cts = int(lib().hegpu_net_tap_cts(h))  # tap ciphertexts per image
+        self.ntaps = self.tap_cts  # (round-1 name)
+        self.first_layer = {v: k for k, v in FIRST_LAYERS.items()}[int(lib().hegpu_net_first_layer(h))]
         self.top = ctx.L
-        self.out_level = ctx.L - 1 - 2 * len(cfg.dense)
+        self.out_level = ctx.L - 1 - 2 * len(self.cfg.dense)
         self.tap_words = 2 * self.top * ctx.N
         self.out_words = 2 * self.out_level * ctx.N
 
@@ -735,11 +759,7 @@ class Net:
         self.ctx = ctx
         self.cfg = _SpecCfg(spec)
         self.h = h
-        self.ntaps = int(lib().hegpu_net_tap_cts(h))
-        self.top = ctx.L
-        self.out_level = ctx.L - 1 - 2 * spec.n_dense
-        self.tap_words = 2 * self.top * ctx.N
-        self.out_words = 2 * self.out_level * ctx.N
+        self._post_init()
         return self
 
     def encrypt_image(self, image, nonce):

@@ -123,3 +123,17 @@ def conv_as_matrix(weights, d_in, s=1):
                     cols = (ci * d_in + oy * s + ky) * d_in + ox * s + kx
                     A[rows.ravel(), cols.ravel()] += weights[co, ci, ky, kx]
     return A
+
+
+def plain_forward(cfg: NetConfig, weights, image):
+    """the cleartext network (conv -> square -> dense -> square -> dense ...)
+    in vectorised FP64 -- bench.py's sanity check on decrypted logits (the
+    reference-order oracle ref_forward lives under oracle/ and is for tests)"""
+    x = np.asarray(image, dtype=np.float64)
+    W, b = np.asarray(weights["conv_w"]), np.asarray(weights["conv_b"])
+    taps = conv_pack_image(x, cfg.k, cfg.s)  # [k^2 c_in] windows of d_out^2
+    t = np.einsum("ot,tp->op", W.reshape(cfg.c_out, -1), np.stack(taps)) + b[:, None]
+    flat = t.ravel()
+    for Wd, bd in weights["dense"]:
+        flat = np.asarray(Wd) @ (flat * flat) + np.asarray(bd)
+    return flat

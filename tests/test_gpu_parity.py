@@ -360,7 +360,7 @@ def test_cfg0_net_bit_exact_and_logits(cfg0):
     B = 2
     imgs = [net_image(cfg, s) for s in range(B)]
     taps = np.concatenate([net.encrypt_image(im, nonce=s) for s, im in enumerate(imgs)])
-    dt = ctx.ct(B * net.ntaps, net.top, taps, DELTA)
+    dt = ctx.ct(B * net.tap_cts, net.top, taps, DELTA)
     out = ctx.ct(B, net.out_level)
     ctx.reset_meter()
     net.run(dt, out)
@@ -377,6 +377,54 @@ def test_cfg0_net_bit_exact_and_logits(cfg0):
         assert np.abs(logits - ref).max() < 1e-3
 
 
+def test_cfg0_performed_keyswitch_counters(cfg0):
+    """hegpu_ks_counters: the key-switch work the engine executes for one
+    cfg-0 inference with the reference first layer, next to the reference's
+    metered 120 rotations + 2 relinearisations.  Per image: merge 4 ModUps /
+    4 inner products / 1 ModDown (lazy sum); each square 1/1/1; HS1 one
+    hoisted ModUp, 99 keyed diagonals, 1 ModDown, then its fold as one hoisted
+    sum of 2^4 - 1 = 15 rotations (1/15/1); HS2 1/9/1 and fold 1/15/1;
+    rescales: 5 conv maps, 2 squares, 2 HS layers."""
+    cfg, ctx, ck, w, net = cfg0
+    B = 2
+    taps = np.concatenate([net.encrypt_image(net_image(cfg, 70 + s), nonce=70 + s) for s in range(B)])
+    out = ctx.ct(B, net.out_level)
+    dt = ctx.ct(B * net.tap_cts, net.top, taps, DELTA)
+    ctx.reset_meter()
+    net.run(dt, out)
+    got = ctx.ks_counters()
+    assert got == {"modups": 10 * B, "key_inner_products": 144 * B, "moddowns": 7 * B, "rescales": 9 * B}, got
+    assert ctx.total()[4] == 120 * B  # the reference's metered rotations are unchanged
+
+
+def test_cfg0_fused_first_layer_bit_exact(cfg0):
+    """the fused, region-packed first layer (HEGPU_FIRST_LAYER_FUSED,
+    DESIGN.md §4.1c): 7 tap ciphertexts per image instead of 25, limbs ==
+    the oracle's fused pipeline, logits within 1e-3 of ref_forward, the same
+    per-stage HOPs as the reference layout"""
+    cfg, ctx, ck, w, net = cfg0
+    fused = H.Net(ctx, cfg, w, first_layer="fused")
+    assert (net.tap_cts, fused.tap_cts) == (25, 7)
+    assert (net.first_layer, fused.first_layer) == ("reference", "fused")
+    B = 2
+    imgs = [net_image(cfg, 50 + s) for s in range(B)]
+    taps = np.concatenate([fused.encrypt_image(im, nonce=50 + s) for s, im in enumerate(imgs)])
+    out = ctx.ct(B, fused.out_level)
+    ctx.reset_meter()
+    fused.run(ctx.ct(B * fused.tap_cts, fused.top, taps, DELTA), out)
+    spec = HS.CnnSpec(cfg.in_c, cfg.in_d, cfg.k, cfg.s, cfg.c_out, cfg.dense, cfg.n_slots)
+    golden = HS.golden_stage_tallies(spec)
+    assert dict(ctx.stages()) == {k: tuple(B * x for x in v) for k, v in golden.items()}
+    # region fold 1/3/1 replaces the merge's 4/4/1; one conv rescale per image
+    assert ctx.ks_counters() == {"modups": 7 * B, "key_inner_products": 143 * B, "moddowns": 7 * B,
+                                 "rescales": 5 * B}
+    got = out.download().reshape(B, -1)
+    want, _ = P.run_net(ck, cfg, w, imgs[0], nonce=50, merged=True)
+    assert np.array_equal(got[0], want)
+    for b in range(B):
+        assert np.abs(fused.decrypt_logits(got[b]) - HS.ref_forward(spec, w, imgs[b])).max() < 1e-3
+
+
 def test_cfg0_net_batch_tensor_core_hs(cfg0):
     """a batch of 9 images: both HS layers run on the tensor-core kernel;
     image 0's limbs == the oracle pipeline, all logits within 1e-3"""
@@ -385,7 +433,7 @@ def test_cfg0_net_batch_tensor_core_hs(cfg0):
     imgs = [net_image(cfg, 40 + s) for s in range(B)]
     taps = np.concatenate([net.encrypt_image(im, nonce=40 + s) for s, im in enumerate(imgs)])
     out = ctx.ct(B, net.out_level)
-    net.run(ctx.ct(B * net.ntaps, net.top, taps, DELTA), out)
+    net.run(ctx.ct(B * net.tap_cts, net.top, taps, DELTA), out)
     got = out.download().reshape(B, -1)
     want, _ = P.run_net(ck, cfg, w, imgs[0], nonce=40)
     assert np.array_equal(got[0], want)
@@ -401,7 +449,7 @@ def test_cfg0_run_host_matches_device_run(cfg0):
     host_out = np.zeros(B * net.out_words, dtype=np.uint64)
     net.run_host(taps, B, host_out)
     out = ctx.ct(B, net.out_level)
-    net.run(ctx.ct(B * net.ntaps, net.top, taps, DELTA), out)
+    net.run(ctx.ct(B * net.tap_cts, net.top, taps, DELTA), out)
     assert np.array_equal(host_out, out.download())
 
 
@@ -416,7 +464,7 @@ def test_cfg0_run_host_compact_pipeline(cfg0, chunk):
     host_out = np.zeros(B * net.out_words, dtype=np.uint64)
     net.run_host_compact(compact, B, host_out, chunk)
     out = ctx.ct(B, net.out_level)
-    net.run(ctx.ct(B * net.ntaps, net.top, full, DELTA), out)
+    net.run(ctx.ct(B * net.tap_cts, net.top, full, DELTA), out)
     assert np.array_equal(host_out, out.download())
 
 
@@ -432,7 +480,7 @@ def test_cfg0_run_compact_device_and_submit(cfg0):
     full = np.concatenate([net.encrypt_image(im, nonce=60 + s) for s, im in enumerate(imgs)])
     ref = ctx.ct(B, net.out_level)
     ctx.reset_meter()
-    net.run(ctx.ct(B * net.ntaps, net.top, full, DELTA), ref)
+    net.run(ctx.ct(B * net.tap_cts, net.top, full, DELTA), ref)
     want_stages = dict(ctx.stages())
     want = ref.download()
     out = ctx.ct(B, net.out_level)
@@ -463,7 +511,7 @@ def test_cfg0_net_run_split_dense1(cfg0):
     cfg, ctx, ck, w, net = cfg0
     B = 2
     imgs = [net_image(cfg, 80 + s) for s in range(B)]
-    taps = ctx.ct(B * net.ntaps, net.top,
+    taps = ctx.ct(B * net.tap_cts, net.top,
                   np.concatenate([net.encrypt_image(im, nonce=80 + s) for s, im in enumerate(imgs)]), DELTA)
     ref = ctx.ct(B, net.out_level)
     ctx.reset_meter()
@@ -505,8 +553,8 @@ def test_cfg0_net_from_model_files(cfg0, tmp_path):
     t2 = net2.encrypt_image(x, nonce=90)
     assert np.array_equal(t1, t2)
     o1, o2 = ctx.ct(1, net.out_level), ctx.ct(1, net2.out_level)
-    net.run(ctx.ct(net.ntaps, net.top, t1, DELTA), o1)
-    net2.run(ctx.ct(net2.ntaps, net2.top, t2, DELTA), o2)
+    net.run(ctx.ct(net.tap_cts, net.top, t1, DELTA), o1)
+    net2.run(ctx.ct(net2.tap_cts, net2.top, t2, DELTA), o2)
     assert np.array_equal(o1.download(), o2.download())
     spec = HS.CnnSpec(cfg.in_c, cfg.in_d, cfg.k, cfg.s, cfg.c_out, cfg.dense, cfg.n_slots)
     assert np.abs(net2.decrypt_logits(o2.download()) - HS.ref_forward(spec, w, img)).max() < 1e-3
@@ -529,7 +577,7 @@ def test_cryptonets_model_lowered_on_gpu(tmp_path):
         img[0, :28, :28] = rng.uniform(0, 1, (28, 28)).astype(np.float32)
         out = ctx.ct(1, net.out_level)
         ctx.reset_meter()
-        net.run(ctx.ct(net.ntaps, net.top, net.encrypt_image(img, nonce=s), DELTA), out)
+        net.run(ctx.ct(net.tap_cts, net.top, net.encrypt_image(img, nonce=s), DELTA), out)
         logits = net.decrypt_logits(out.download())
         want = HS.ref_forward_layers(m.layers, per_layer, img)
         assert np.abs(logits - want).max() < 1e-3
@@ -550,7 +598,7 @@ def test_cfg3_net_logits_and_hops():
     taps = np.concatenate([net.encrypt_image(im, nonce=s) for s, im in enumerate(imgs)])
     out = ctx.ct(B, net.out_level)
     ctx.reset_meter()
-    net.run(ctx.ct(B * net.ntaps, net.top, taps, DELTA), out)
+    net.run(ctx.ct(B * net.tap_cts, net.top, taps, DELTA), out)
     got = out.download().reshape(B, -1)
     spec = HS.CnnSpec(cfg.in_c, cfg.in_d, cfg.k, cfg.s, cfg.c_out, cfg.dense, cfg.n_slots)
     golden = HS.golden_stage_tallies(spec)
