@@ -73,6 +73,16 @@ def test_run_count_verify_on_gpu(tmp_path):
 
 
 @pytest.mark.gpu
+def test_verify_negative_control_exits_3():
+    """--corrupt-kernel perturbs the expected A x, so verify must report FAIL
+    and exit 3 (proj/tools/hesim.cpp:212,237,334-337;
+    proj/tests/acceptance.cpp:232-238)"""
+    v = cli("verify", "--cases", "2", "--corrupt-kernel", timeout=1200)
+    assert v.returncode == 3, v.stdout + v.stderr
+    assert "verify: FAIL" in v.stdout
+
+
+@pytest.mark.gpu
 def test_sweep_measure_on_gpu():
     """sweep --measure (hesim.cpp:119-140): every method runs on the GPU and
     its metered rotations / multiplications equal the prediction for dense

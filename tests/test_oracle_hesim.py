@@ -307,6 +307,47 @@ def test_refmodel_hand_values():  # test_refmodel.cpp (dense + square)
     assert out[0].tolist() == [[9.0, 13.0], [21.0, 25.0]]
 
 
+def test_refmodel_conv_ones_2x2():  # test_refmodel.cpp:26-33
+    out = H.ref_conv(np.array([[[1.0, 2.0], [3.0, 4.0]]]), np.ones((1, 1, 2, 2)), np.zeros(1), 1)
+    assert out.shape == (1, 1, 1) and out[0, 0, 0] == pytest.approx(10.0)
+
+
+def test_refmodel_delta_filter_crops_shifted_window():  # test_refmodel.cpp:35-47
+    img = np.random.default_rng(3).uniform(-1, 1, (1, 5, 5))
+    W = np.zeros((1, 1, 3, 3))
+    W[0, 0, 1, 2] = 1.0  # tap (ky=1, kx=2)
+    out = H.ref_conv(img, W, np.zeros(1), 1)
+    assert out.shape == (1, 3, 3)
+    for oy in range(3):
+        for ox in range(3):
+            assert out[0, oy, ox] == pytest.approx(img[0, oy + 1, ox + 2])
+
+
+def test_refmodel_bias_per_output_channel():  # test_refmodel.cpp:49-57
+    out = H.ref_conv(np.ones((1, 2, 2)), np.ones((2, 1, 2, 2)), np.array([0.5, -1.0]), 1)
+    assert out[0, 0, 0] == pytest.approx(4.5) and out[1, 0, 0] == pytest.approx(3.0)
+
+
+def test_refmodel_avgpool():  # test_refmodel.cpp:59-76
+    out = H.ref_avgpool(np.array([[[1.0, 2.0], [3.0, 4.0]]]), 2, 2)
+    assert out.shape[1] == 1 and out.ravel()[0] == pytest.approx(2.5)
+    img = np.random.default_rng(5).uniform(-1, 1, (2, 6, 6))
+    out = H.ref_avgpool(img, 3, 2)
+    assert out.shape == (2, 2, 2)
+    assert out[1, 1, 1] == pytest.approx(img[1, 2:5, 2:5].sum() / 9.0)
+
+
+def test_refmodel_square():  # test_refmodel.cpp:78-86
+    out = H.ref_square(np.array([[[2.0, -3.0, 0.0]]]))
+    assert out.ravel().tolist() == [4.0, 9.0, 0.0]
+    assert not H.ref_square(np.zeros((2, 3, 3))).any()
+
+
+def test_refmodel_dense_identity():  # test_refmodel.cpp:88-95
+    v = np.random.default_rng(7).uniform(-1, 1, 5)
+    assert np.abs(H.ref_dense(v, np.eye(5), np.zeros(5)) - v).max() < 1e-15
+
+
 def cfg0_spec():
     return H.CnnSpec(in_c=1, in_d=29, k=5, s=2, c_out=5, dense=(100, 10), n_slots=4096)
 

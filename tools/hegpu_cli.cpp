@@ -5,7 +5,7 @@
 //   hegpu_cli run   --model M [--weights W] [--input X] [--report R] [--seed S]
 //   hegpu_cli count --model M [...]
 //   hegpu_cli sweep [--n-min 16 --n-max 4096 --m-min 4 --m-max 512 --n-slots 4096,16384] [--measure]
-//   hegpu_cli verify [--seed 1] [--cases 20]
+//   hegpu_cli verify [--seed 1] [--cases 20] [--corrupt-kernel]
 //
 // M is a model JSON (path or name under $HECNN_MODEL_DIR) or a builtin name
 // (cryptonets-hs, me, ce).  CKKS parameters follow the model: N = 2 n_slots,
@@ -223,6 +223,7 @@ struct Args {
   std::string cmd, model, weights, input, report, out, methods = "hs,lola-dense,lola-stacked";
   uint64_t seed = 0;
   bool seed_set = false, measure = false;
+  bool corrupt_kernel = false;  // verify's negative control (hesim.cpp:212,237,334-337)
   int cases = 20, n_min = 16, n_max = 4096, m_min = 4, m_max = 512;
   std::vector<int> slots = {4096, 16384};
 };
@@ -250,6 +251,7 @@ Args parse(int argc, char** argv) {
     else if (k == "--m-max") a.m_max = std::stoi(val());
     else if (k == "--methods") a.methods = val();
     else if (k == "--measure") a.measure = true;
+    else if (k == "--corrupt-kernel") a.corrupt_kernel = true;
     else if (k == "--n-slots") {
       a.slots.clear();
       std::stringstream ss(val());
@@ -552,6 +554,7 @@ int cmd_verify(const Args& a) {
       for (int r = 0; r < m; ++r) {
         double want = 0.0;
         for (int j = 0; j < n; ++j) want += A[(size_t)r * n + j] * xv[j];
+        if (a.corrupt_kernel && r == 0) want += 1e-3;  // negative control: perturbed expectation
         max_err = std::max(max_err, std::fabs(y[r] - want) / std::max(1.0, std::fabs(want)));
       }
       hegpu_ct_destroy(v);
