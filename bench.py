@@ -43,10 +43,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "encrypted inferences/sec + key-switched rotations/sec, % of HBM roofline"
-KERNELS = ["k_hs_diag", "k_hs_imma", "k_hs_narrow", "k_drop_ntt", "k_ks_modup", "k_conv_mac", "k_intt_rows",
+KERNELS = ["k_hs_diag", "k_hs_imma", "k_hs_narrow", "k_drop_ntt", "k_md_ntt", "k_md_intt", "k_ks_modup", "k_conv_mac", "k_intt_rows",
            "k_ks_intt", "k_ks_inner", "k_ntt_rows", "k_merge_c", "k_expand_c0", "k_expand_a", "k_wire_to_slot",
            "k_add", "k_tensor_square", "k_add_plain"]
-NTT_KERNELS = ("k_drop_ntt", "k_ks_modup", "k_intt_rows", "k_ks_intt", "k_ntt_rows")
+NTT_KERNELS = ("k_drop_ntt", "k_md_ntt", "k_md_intt", "k_ks_modup", "k_intt_rows", "k_ks_intt", "k_ntt_rows")
 UNIT = "inferences/s"
 SEED = 2110
 WORKLOAD = ("cfg2: 64 x cfg0 MNIST-sized net per GPU, reference stages (conv-pack 25 tap cts -> conv + rescale "
@@ -73,7 +73,8 @@ N_SM = 148
 # multiply-accumulate term is 4 IMAD.WIDE.U32; an NTT
 # butterfly's Shoup product is 6 multiply instructions (modarith.cuh
 # shoup_mul_lazy4) -- the ceiling if nothing but the multiplies issued
-INT_OPS_IMAD = {"k_hs_diag": 4, "k_hs_narrow": 4, "k_ks_inner": 4, "k_drop_ntt": 6, "k_ks_modup": 6,
+INT_OPS_IMAD = {"k_hs_diag": 4, "k_hs_narrow": 4, "k_ks_inner": 4, "k_drop_ntt": 6, "k_md_ntt": 6, "k_md_intt": 6,
+                "k_ks_modup": 6,
                 "k_intt_rows": 6, "k_ks_intt": 6, "k_ntt_rows": 6}
 # kernels whose MACs run on IMMA.16832.U8 as 64 byte-plane products each
 TENSOR_KERNELS = ("k_hs_imma", "k_conv_mac")

@@ -226,6 +226,9 @@ struct DropArgs {
   int nl;          // output limbs (primes 0..nl-1)
   const u64d* add; long add_b, add_p; int add_mask;  // add term per poly (bit p)
   const KeyRowMap* shifts;  // shift for add reads of poly 0 (may be null)
+  // ModDown (pd = P) followed by the rescale that drops q_{l-1}, fused
+  // (ntt.cu k_md_intt / k_md_ntt): dst gets nl = l - 1 limbs; add unshifted
+  int fuse_rescale;
 };
 void drop_last_limb(Context& c, int B, const DropArgs& a, u64d* tmpP);
 // the two NTT builds (ntt.cu: 16 words/thread, ntt_r8.cu: 8 for N <= 2^13)
@@ -311,6 +314,7 @@ void eval_rescale(Context& c, const CtBatch& a, CtBatch& out);
 void eval_rotate(Context& c, const u64d* a, long a_stride, int B, int l, const KeyRowMap& km, u64d* out,
                  long out_stride);
 void eval_square(Context& c, const CtBatch& a, CtBatch& out);  // tensor + relin, no rescale
+void eval_square_rescale(Context& c, const CtBatch& a, CtBatch& out);  // tensor + relin + rescale (fused)
 void eval_merge(Context& c, const CtBatch& maps, int nmaps, const KeyRowMap& km, CtBatch& out);
 
 }  // namespace hegpu

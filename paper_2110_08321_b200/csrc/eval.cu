@@ -1111,9 +1111,18 @@ void eval_merge(Context& c, const CtBatch& maps, int nmaps, const KeyRowMap& km,
   c.free(tmp); c.free(D); c.free(acc); c.free(C); c.free(tmpP);
 }
 
-void eval_square(Context& c, const CtBatch& a, CtBatch& out) {
+void eval_square_impl(Context& c, const CtBatch& a, CtBatch& out, bool rescale);
+
+void eval_square(Context& c, const CtBatch& a, CtBatch& out) { eval_square_impl(c, a, out, false); }
+
+// square + relinearise + rescale with the ModDown and the rescale fused
+// (drop_last_limb fuse_rescale, ntt.cu §4.8): out at level l - 1
+void eval_square_rescale(Context& c, const CtBatch& a, CtBatch& out) { eval_square_impl(c, a, out, true); }
+
+void eval_square_impl(Context& c, const CtBatch& a, CtBatch& out, bool rescale) {
   if (!c.has_relin) fail(HEGPU_ERR_KEY, "square: no relinearisation key");
   const int l = a.level, N = c.N(), B = a.count;
+  if (rescale && l < 2) fail(HEGPU_ERR_CAPACITY, "square: no prime left to drop");
   u64d* d01 = c.alloc((size_t)B * 2 * l * N);
   u64d* d2 = c.alloc((size_t)B * l * N);
   u64d* tmp = c.alloc((size_t)B * l * N);
@@ -1128,9 +1137,10 @@ void eval_square(Context& c, const CtBatch& a, CtBatch& out) {
   ks_inner(c, D, B, l, km, acc);
   DropArgs d{};
   d.src = acc; d.src_b = 2L * (l + 1) * N; d.src_p = (long)(l + 1) * N; d.src_limbs = l + 1;
-  d.dst = out.d; d.dst_b = (long)out.stride(); d.dst_p = (long)l * N;
-  d.pd = c.L(); d.nl = l;
+  d.dst = out.d; d.dst_b = (long)out.stride(); d.dst_p = (long)(rescale ? l - 1 : l) * N;
+  d.pd = c.L(); d.nl = rescale ? l - 1 : l;
   d.add = d01; d.add_b = 2L * l * N; d.add_p = (long)l * N; d.add_mask = 3; d.shifts = nullptr;
+  d.fuse_rescale = rescale ? 1 : 0;
   drop_last_limb(c, B, d, tmpP);
   c.free(d01); c.free(d2); c.free(tmp); c.free(D); c.free(acc); c.free(tmpP);
 }

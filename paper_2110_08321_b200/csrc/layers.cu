@@ -242,11 +242,9 @@ void merge_maps(Context& c, const CtBatch& maps, int nmaps, int64_t w, CtBatch& 
 // ---------------------------------------------------------------- square ----
 void square_layer(Context& c, const CtBatch& a, CtBatch& out) {
   const int B = a.count, l = a.level;
-  CtBatch t{&c, B, l, a.scale * a.scale, c.alloc((size_t)B * 2 * l * c.N())};
-  eval_square(c, a, t);
-  eval_rescale(c, t, out);
+  (void)B;
+  eval_square_rescale(c, a, out);
   out.scale = a.scale * a.scale / (double)c.P->q(l - 1);
-  c.free(t.d);
 }
 
 // -------------------------------------------------------------------- HS ----
@@ -551,16 +549,16 @@ void HsPlan::finish(Context& c, int B, double v_scale, u64d* acc, u64d* cacc, in
     launch_reduce_rows(c, cacc, (size_t)B * 2 * l * N, l, -1);
   }
   u64d* tmpP = c.alloc((size_t)B * 2 * N);
-  CtBatch u{&c, B, l, v_scale * (double)c.P->q(l - 1), c.alloc((size_t)B * 2 * l * N)};
-  // (3) one ModDown of the sum (+ the Q-basis c-part)
+  // (3) one ModDown of the sum (+ the Q-basis c-part) and (4) the rescale by
+  // q_{l-1} (the masks were encoded at exactly that scale), fused into one
+  // drop pass (ntt.cu §4.8; residues equal to ModDown followed by rescale)
   DropArgs d{};
   d.src = acc; d.src_b = 2L * (l + 1) * N; d.src_p = (long)(l + 1) * N; d.src_limbs = l + 1;
-  d.dst = u.d; d.dst_b = (long)u.stride(); d.dst_p = (long)l * N;
-  d.pd = c.L(); d.nl = l;
+  d.dst = out.d; d.dst_b = (long)out.stride(); d.dst_p = (long)(l - 1) * N;
+  d.pd = c.L(); d.nl = l - 1;
   d.add = cacc; d.add_b = 2L * l * N; d.add_p = (long)l * N; d.add_mask = 3; d.shifts = nullptr;
+  d.fuse_rescale = 1;
   drop_last_limb(c, B, d, tmpP);
-  // (4) rescale by q_{l-1}: the masks were encoded at exactly that scale
-  eval_rescale(c, u, out);
   out.scale = v_scale;
   // (5) log-depth fold, matvec.cpp:101-103: s += rot_left(s, m_eff * 2^t)
   // for t = folds-1..0 = sum of rot_left(s, m_eff u) over u < 2^folds, run
@@ -589,7 +587,6 @@ void HsPlan::finish(Context& c, int B, double v_scale, u64d* acc, u64d* cacc, in
     c.free(r.d);
   }
   c.free(tmpP);
-  c.free(u.d);
 }
 
 void HsPlan::run(Context& c, const CtBatch& v, CtBatch& out) {

@@ -415,6 +415,114 @@ __global__ void NTT_BOUNDS k_drop_ntt(TwArgs ta, PrimeTable pt, const u64d* __re
   }
 }
 
+// ------------------------------------------- fused ModDown + rescale (§4.8)
+// The ModDown of an extended-basis accumulator (limbs q_0..q_{l-1}, P) is
+// directly followed by a rescale that drops q_{l-1}.  Two successive drops
+// cost INTT(P) + l NTTs, then INTT(q_{l-1}) + (l-1) NTTs per polynomial;
+// fused they cost INTT(P) + INTT(q_{l-1}) + (l-1) NTTs, with limbs equal to
+// the two-step result residue for residue:
+//   x = INTT_P(acc_P)                        (ModDown's dropped residue)
+//   z = INTT_qd(acc_qd P^-1 + add_qd)         (qd = q_{l-1})
+//   y = z - lift_P(x) P^-1  mod qd           (= INTT of the ModDown's limb qd,
+//                                             by linearity of the INTT)
+//   out_t = (acc_t P^-1 + add_t - NTT_t(lift_P(x) P^-1 + lift_qd(y))) qd^-1
+// Step 1 (k_md_intt): rows (b, p, {P, qd}) -> xz[b][p][{x, z}][N].
+template <int LOGN>
+__global__ void NTT_BOUNDS k_md_intt(TwArgs ta, PrimeTable pt, const u64d* __restrict__ qinv, int np_all, DropArgs a,
+                                     u64d* __restrict__ xz) {
+  extern __shared__ u64d sm[];
+  constexpr int N = 1 << LOGN;
+  const int r = blockIdx.x, which = r & 1, bp = r >> 1, p = bp & 1, b = bp >> 1;
+  const int lq = a.src_limbs - 2;          // limb (and prime index) of q_{l-1}
+  const int pi = which ? lq : a.pd;        // a.pd: prime index of P
+  const u64d* row = a.src + b * a.src_b + p * a.src_p + (size_t)(which ? lq : a.src_limbs - 1) * N;
+  if (which) {
+    const u64d q = pt.p[lq].q;
+    const u64d iv = qinv[((size_t)lq * np_all + a.pd) * 2], ivp = qinv[((size_t)lq * np_all + a.pd) * 2 + 1];
+    const bool add = (a.add_mask >> p) & 1;
+    const u64d* ad = add ? a.add + b * a.add_b + p * a.add_p + (size_t)lq * N : nullptr;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      u64d v = shoup_mul_d(row[i], iv, ivp, q);
+      if (add) v = add_mod_d(v, ad[i], q);
+      sm[pad(__ldg(ta.slot_src + i))] = v;
+    }
+  } else {
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sm[pad(__ldg(ta.slot_src + i))] = row[i];
+  }
+  __syncthreads();
+  StPlain st{xz + ((size_t)bp * 2 + which) * N};
+  inv_transform<LOGN>(sm, st, twi(ta, pi, N), pt.p[pi].q, ta.ninv[2 * pi], ta.ninv[2 * pi + 1]);
+}
+
+// centered lift of a residue mod m (< m) times a constant c (Shoup pair), mod q
+__device__ __forceinline__ u64d lift_mul(u64d v, u64d m, u64d c, u64d cp, u64d q) {
+  const bool neg = v > (m >> 1);
+  const u64d r = shoup_mul_d(neg ? m - v : v, c, cp, q);  // Shoup: any word input, result in [0, q)
+  return (neg && r) ? q - r : r;
+}
+
+// Step 2: rows (b, p, t < nl = l - 1): u = lift_P(x) P^-1 + lift_qd(y) mod
+// q_t, NTT, out_t = (acc_t P^-1 + add_t - NTT(u)) qd^-1; the epilogue's
+// operands are prefetched into shared memory during the transform
+struct LdMd {
+  const u64d* x;
+  const u64d* z;
+  u64d P, qd, q;
+  u64d pv, pvp;    // P^-1 mod q_t
+  u64d pqv, pqvp;  // P^-1 mod qd
+  u64d one_sh;     // floor(2^64 / q_t)
+  __device__ u64d load(int k) const {
+    const u64d xv = x[k];
+    const u64d y = sub_mod_d(z[k], lift_mul(xv, P, pqv, pqvp, qd), qd);
+    return add_mod_d(lift_mul(xv, P, pv, pvp, q), lift_mul(y, qd, 1ull, one_sh, q), q);
+  }
+};
+
+template <int LOGN>
+__global__ void NTT_BOUNDS k_md_ntt(TwArgs ta, PrimeTable pt, const u64d* __restrict__ qinv, int np_all, DropArgs a,
+                                    const u64d* __restrict__ xz) {
+  extern __shared__ u64d sm[];
+  constexpr int N = 1 << LOGN;
+  const int r = blockIdx.x;
+  const int t = r % a.nl, bp = r / a.nl, p = bp % 2, b = bp / 2;
+  const int lq = a.src_limbs - 2;
+  const DevPrime pr = pt.p[t];
+  const u64d q = pr.q;
+  const u64d* in = a.src + b * a.src_b + p * a.src_p + (size_t)t * N;
+  u64d* out = a.dst + b * a.dst_b + p * a.dst_p + (size_t)t * N;
+  const bool add = (a.add_mask >> p) & 1;
+  const u64d* ad = add ? a.add + b * a.add_b + p * a.add_p + (size_t)t * N : nullptr;
+  constexpr bool kPre = drop_prefetch(N);
+  const u64d* in_s = in;
+  const u64d* ad_s = ad;
+  if constexpr (kPre) {
+    u64d* is = sm + (((size_t)N + (N >> 4) + 1 + 1) & ~(size_t)1);
+    u64d* as = is + N;
+    for (int i = threadIdx.x; i < N / 2; i += blockDim.x) {
+      cp_async16_g2s(is + 2 * i, in + 2 * i);
+      if (add) cp_async16_g2s(as + 2 * i, ad + 2 * i);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    in_s = is;
+    ad_s = as;
+  }
+  const u64d pv = qinv[((size_t)t * np_all + a.pd) * 2], pvp = qinv[((size_t)t * np_all + a.pd) * 2 + 1];
+  const u64d qv = qinv[((size_t)t * np_all + lq) * 2], qvp = qinv[((size_t)t * np_all + lq) * 2 + 1];
+  const u64d* X = xz + (size_t)bp * 2 * N;
+  LdMd ld{X, X + N, pt.p[a.pd].q, pt.p[lq].q, q, pv, pvp,
+          qinv[((size_t)lq * np_all + a.pd) * 2], qinv[((size_t)lq * np_all + a.pd) * 2 + 1], pr.one_sh};
+  fwd_transform<LOGN>(sm, ld, twf(ta, t, N), q);
+  if constexpr (kPre) {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+  }
+  ROW_LOOP(pos) {
+    u64d v = shoup_mul_d(in_s[pos], pv, pvp, q);
+    if (add) v = add_mod_d(v, ad_s[pos], q);
+    out[pos] = shoup_mul_d(sub_mod_d(v, sm[pad(__ldg(ta.slot_src + pos))], q), qv, qvp, q);
+  }
+}
+
 // wire (bit-reversed) <-> slot order, optional Montgomery conversion
 __global__ void k_wire_to_slot(const u64d* __restrict__ src, u64d* __restrict__ dst,
                                const uint32_t* __restrict__ slot_src, PrimeTable pt, int N, int to_mont, int nl,
@@ -562,6 +670,41 @@ void NTT_PUB(ks_modup)(Context& c, const u64d* src, long src_stride, int B, int 
 
 void NTT_PUB(drop_last_limb)(Context& c, int B, const DropArgs& a, u64d* tmpP) {
   const int N = c.N();
+  if (a.fuse_rescale) {
+    // ModDown by P and rescale by q_{l-1} in one pass (§4.8): a.nl = l - 1
+    KeyRowMap dummy{};
+    dummy.period = 1;
+    if (a.shifts) fail(HEGPU_ERR_ARG, "fused ModDown + rescale: no shifted add term");
+    u64d* xz = c.alloc((size_t)B * 2 * 2 * N);
+    double _ntt_bytes = 8.0 * N * B * 2 * (2.0 + 1.0 + (a.add_mask ? 1.0 : 0.0) + 2.0);
+    NTT_DISPATCH(c.P->log_n, k_md_intt, B * 4, tw_args(c), c.primes, c.qinv_tab(), c.P->np(), a, xz);
+    if (a.nl > 0) {
+      // read x, z, acc_t (+ add_t), write out_t
+      _ntt_bytes = (32.0 + (a.add_mask ? 8.0 : 0.0)) * N * B * 2 * a.nl;
+#undef NTT_GO
+#define NTT_GO(LG, KERNEL, GRID, ...)                                                               \
+  do {                                                                                              \
+    static PerDeviceOnce prepared;                                                                  \
+    const size_t smb = drop_smem_words(1 << LG) * 8;                                                \
+    if (prepared.first()) prep_kernel(KERNEL<LG>, smb);                                             \
+    LAUNCH_BO(c, #KERNEL, _ntt_bytes, (double)(GRID) * (LG << (LG - 1)),                           \
+              KERNEL<LG><<<(GRID), (1 << LG) >> lr_of(LG), smb, c.stream>>>(__VA_ARGS__));          \
+  } while (0)
+      NTT_DISPATCH(c.P->log_n, k_md_ntt, B * 2 * a.nl, tw_args(c), c.primes, c.qinv_tab(), c.P->np(), a, xz);
+#undef NTT_GO
+#define NTT_GO(LG, KERNEL, GRID, ...)                                                               \
+  do {                                                                                              \
+    static PerDeviceOnce prepared;                                                                  \
+    const size_t smb = ntt_smem(1 << LG);                                                           \
+    if (prepared.first()) prep_kernel(KERNEL<LG>, smb);                                             \
+    LAUNCH_BO(c, #KERNEL, _ntt_bytes, (double)(GRID) * (LG << (LG - 1)),                           \
+              KERNEL<LG><<<(GRID), (1 << LG) >> lr_of(LG), smb, c.stream>>>(__VA_ARGS__));          \
+  } while (0)
+    }
+    c.free(xz);
+    (void)dummy;
+    return;
+  }
   const int pmap[2] = {a.pd, a.pd};
   NTT_PUB(launch_intt_rows)(c, a.src + (size_t)(a.src_limbs - 1) * N, tmpP, B, 2, a.src_b, a.src_p, 2L * N, N, pmap);
   if (a.nl <= 0) return;
@@ -607,6 +750,7 @@ void ks_modup(Context& c, const u64d* src, long src_stride, int B, int l, const 
 }
 void drop_last_limb(Context& c, int B, const DropArgs& a, u64d* tmpP) {
   c.ks[a.pd == c.L() ? KS_MODDOWN : KS_RESCALE] += B;
+  if (a.fuse_rescale) c.ks[KS_RESCALE] += B;
   drop_last_limb_r8(c, B, a, tmpP);
 }
 #endif
