@@ -157,6 +157,8 @@ extern "C" void hegpu_ctx_destroy(hegpu_ctx* h) {
   for (auto& kv : c.rot_keys) cudaFree(kv.second.data);
   if (c.relin.data) cudaFree(c.relin.data);
   cudaFree(c.d_tw);
+  cudaFree(c.d_twd);
+  cudaFree(c.d_fpq);
   cudaFree(c.d_consts);
   cudaFree(c.d_slot_src);
   if (c.stream) cudaStreamDestroy(c.stream);

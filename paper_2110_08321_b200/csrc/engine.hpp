@@ -56,6 +56,8 @@ struct Context {
   cudaStream_t stream = nullptr;
   PrimeTable primes{};
   u64d* d_tw = nullptr;          // [np][2][N] (w, w') pairs: forward, inverse
+  double* d_twd = nullptr;       // [np][2][N] w as doubles (FP64 NTT path, primes < 2^45)
+  double* d_fpq = nullptr;       // [np][2] (q, 1/q), or (0, 0) for primes on the integer path
   u64d* d_consts = nullptr;      // [np]: ninv, ninv' ; then [np][np]: qinv(value, shoup)
   uint32_t* d_slot_src = nullptr;  // [N]
   std::map<int, DeviceKey> rot_keys;  // keyed by left shift in [1, S)
@@ -194,6 +196,7 @@ struct CompactLayout;
 CompactLayout compact_layout(Context& c, int level);
 // twiddle tables [np][fwd, inv][N] of (w, w') pairs -> c.d_tw
 void upload_twiddles(Context& c);
+bool ntt_fp_enabled();
 // coefficient rows -> slot-order NTT rows; row r uses limb r % nl (limb l ->
 // prime l, or P for l == p_limb when p_limb >= 0)
 void launch_ntt_rows(Context& c, const u64d* src, u64d* dst, int rows, int nl, int p_limb);

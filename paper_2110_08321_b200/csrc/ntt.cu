@@ -48,6 +48,8 @@ struct TwArgs {
   const ulonglong2* tw;   // [np][2][N] (w, w') forward then inverse
   const u64d* ninv;       // [np][2]
   const uint32_t* slot_src;
+  const double* twd;      // [np][2][N] w as doubles (FP64 butterflies)
+  const double2* fpq;     // [np] (q, 1/q) for primes on the FP64 path, (0, 0) otherwise
 };
 
 // ------------------------------------------------------------------ forward
@@ -231,6 +233,188 @@ __device__ __forceinline__ void inv_transform(u64d* sm, St& st, const ulonglong2
   inv_passes<LOGN, 0>(x, sm, tw, q, nv, nvp, st);
 }
 
+// ------------------------------------------------- FP64 butterflies (§5.1)
+// For primes q < 2^45 (the 40-bit limbs) the transform runs on the FP64
+// pipe: residues are exact integers in doubles, and a product b*w mod q is
+// formed exactly from the FMA two-product --
+//   hi = fl(b w), lo = b w - hi (exact, one FMA),
+//   k = rint(hi / q) (one FMA against the magic 1.5 * 2^52, one add),
+//   t = (hi - k q) + lo (one FMA, exact since |hi - k q| < q; one add) --
+// so |t| <= 0.52 q and t == b w (mod q) exactly.  Forward (CT) values grow
+// by <= 0.52 q per stage from [0, 4q): after 14 stages |x| < 12 q < 2^49, no
+// lazy reductions needed; inverse (GS) sums double per stage and are
+// re-centred once per register pass.  Six FP64 instructions per product
+// instead of ~20 integer instructions for the 64-bit Shoup multiply, and
+// the integer pipes are left to address arithmetic.  Exact modular
+// arithmetic, so the limbs equal the integer path's bit for bit.
+#ifndef HEGPU_NTT_FP
+#define HEGPU_NTT_FP 1
+#endif
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: x + kMagic - kMagic = rint(x), |x| < 2^51
+constexpr double kTwo52 = 4503599627370496.0;
+
+__device__ __forceinline__ double u2d(u64d x) {  // exact for x < 2^52
+  return __dadd_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)), -kTwo52);
+}
+__device__ __forceinline__ u64d d2u(double r) {  // r an integer in [0, 2^52)
+  return (u64d)__double_as_longlong(__dadd_rn(r, kTwo52)) & 0xFFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ double fp_mulmod(double b, double w, double2 fq) {
+  const double hi = __dmul_rn(b, w);
+  const double lo = __fma_rn(b, w, -hi);
+  const double k = __dadd_rn(__fma_rn(hi, fq.y, kMagic), -kMagic);
+  return __dadd_rn(__fma_rn(-k, fq.x, hi), lo);
+}
+__device__ __forceinline__ double fp_center(double v, double2 fq) {  // -> |v| <= q/2 + eps
+  const double k = __dadd_rn(__fma_rn(v, fq.y, kMagic), -kMagic);
+  return __fma_rn(-k, fq.x, v);
+}
+__device__ __forceinline__ u64d fp_canon(double v, double2 fq) {  // -> [0, q) as a word
+  double r = fp_center(v, fq);
+  if (r < 0.0) r = __dadd_rn(r, fq.x);
+  return d2u(r);
+}
+
+template <int LOGN, int S0, int RR>
+__device__ __forceinline__ void fwd_pass_fp(double (&x)[1 << lr_of(LOGN)], const double* __restrict__ tw, double2 fq) {
+  constexpr int T = (1 << LOGN) / (1 << lr_of(LOGN)), G = (1 << lr_of(LOGN)) >> RR, J = 1 << RR, LOB = LOGN - S0 - RR;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int hi = (g * T + (int)threadIdx.x) >> LOB;
+#pragma unroll
+    for (int u = 0; u < RR; ++u) {
+      const int half = J >> (u + 1);
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        if (j & half) continue;
+        const double W = __ldg(tw + (1 << (S0 + u)) + (hi << u) + (j >> (RR - u)));
+        const double a = x[g * J + j];
+        const double t = fp_mulmod(x[g * J + j + half], W, fq);
+        x[g * J + j] = __dadd_rn(a, t);
+        x[g * J + j + half] = __dadd_rn(a, -t);
+      }
+    }
+  }
+}
+
+template <int LOGN, int S0, int RR>
+__device__ __forceinline__ void fwd_store_d(double* sm, const double (&x)[1 << lr_of(LOGN)]) {
+#pragma unroll
+  for (int g = 0; g < ((1 << lr_of(LOGN)) >> RR); ++g)
+#pragma unroll
+    for (int j = 0; j < (1 << RR); ++j) sm[pad(fwd_idx<LOGN, S0, RR>(g, j))] = x[g * (1 << RR) + j];
+}
+template <int LOGN, int S0, int RR>
+__device__ __forceinline__ void fwd_load_d(const double* sm, double (&x)[1 << lr_of(LOGN)]) {
+#pragma unroll
+  for (int g = 0; g < ((1 << lr_of(LOGN)) >> RR); ++g)
+#pragma unroll
+    for (int j = 0; j < (1 << RR); ++j) x[g * (1 << RR) + j] = sm[pad(fwd_idx<LOGN, S0, RR>(g, j))];
+}
+
+template <int LOGN, int S0>
+__device__ __forceinline__ void fwd_passes_fp(double (&x)[1 << lr_of(LOGN)], u64d* sm, const double* tw, double2 fq) {
+  constexpr int RR = cmin(lr_of(LOGN), LOGN - S0);
+  fwd_pass_fp<LOGN, S0, RR>(x, tw, fq);
+  if constexpr (S0 + RR < LOGN) {
+    constexpr int RN = cmin(lr_of(LOGN), LOGN - S0 - RR);
+    fwd_store_d<LOGN, S0, RR>(reinterpret_cast<double*>(sm), x);
+    __syncthreads();
+    fwd_load_d<LOGN, S0 + RR, RN>(reinterpret_cast<const double*>(sm), x);
+    __syncthreads();
+    fwd_passes_fp<LOGN, S0 + RR>(x, sm, tw, fq);
+  } else {
+#pragma unroll
+    for (int g = 0; g < ((1 << lr_of(LOGN)) >> RR); ++g)
+#pragma unroll
+      for (int j = 0; j < (1 << RR); ++j) sm[pad(fwd_idx<LOGN, S0, RR>(g, j))] = fp_canon(x[g * (1 << RR) + j], fq);
+    __syncthreads();
+  }
+}
+
+template <int LOGN, class Ld>
+__device__ __forceinline__ void fwd_transform_fp(u64d* sm, const Ld& ld, const double* tw, double2 fq) {
+  constexpr int R0 = cmin(lr_of(LOGN), LOGN);
+  double x[1 << lr_of(LOGN)];
+#pragma unroll
+  for (int g = 0; g < ((1 << lr_of(LOGN)) >> R0); ++g)
+#pragma unroll
+    for (int j = 0; j < (1 << R0); ++j) x[g * (1 << R0) + j] = u2d(ld.load(fwd_idx<LOGN, 0, R0>(g, j)));
+  fwd_passes_fp<LOGN, 0>(x, sm, tw, fq);
+}
+
+template <int LOGN, int S0, int RR>
+__device__ __forceinline__ void inv_pass_fp(double (&x)[1 << lr_of(LOGN)], const double* __restrict__ tw, double2 fq) {
+  constexpr int T = (1 << LOGN) / (1 << lr_of(LOGN)), G = (1 << lr_of(LOGN)) >> RR, J = 1 << RR;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int hi = (g * T + (int)threadIdx.x) >> S0;
+#pragma unroll
+    for (int u = 0; u < RR; ++u) {
+      const int dist = 1 << u;
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        if (j & dist) continue;
+        const double W = __ldg(tw + (1 << (LOGN - S0 - u - 1)) + (hi << (RR - u - 1)) + (j >> (u + 1)));
+        const double a = x[g * J + j], b = x[g * J + j + dist];
+        x[g * J + j] = __dadd_rn(a, b);
+        x[g * J + j + dist] = fp_mulmod(__dadd_rn(a, -b), W, fq);
+      }
+    }
+  }
+  // sums grew by up to 2^RR: re-centre every value (|x| <= q/2 + eps)
+#pragma unroll
+  for (int e = 0; e < (1 << lr_of(LOGN)); ++e) x[e] = fp_center(x[e], fq);
+}
+
+template <int LOGN, int S0, int RR>
+__device__ __forceinline__ void inv_store_d(double* sm, const double (&x)[1 << lr_of(LOGN)]) {
+#pragma unroll
+  for (int g = 0; g < ((1 << lr_of(LOGN)) >> RR); ++g)
+#pragma unroll
+    for (int j = 0; j < (1 << RR); ++j) sm[pad(inv_idx<LOGN, S0, RR>(g, j))] = x[g * (1 << RR) + j];
+}
+template <int LOGN, int S0, int RR>
+__device__ __forceinline__ void inv_load_d(const double* sm, double (&x)[1 << lr_of(LOGN)]) {
+#pragma unroll
+  for (int g = 0; g < ((1 << lr_of(LOGN)) >> RR); ++g)
+#pragma unroll
+    for (int j = 0; j < (1 << RR); ++j) x[g * (1 << RR) + j] = sm[pad(inv_idx<LOGN, S0, RR>(g, j))];
+}
+
+template <int LOGN, int S0, class St>
+__device__ __forceinline__ void inv_passes_fp(double (&x)[1 << lr_of(LOGN)], u64d* sm, const double* tw, double2 fq,
+                                              double nv, St& st) {
+  constexpr int RR = cmin(lr_of(LOGN), LOGN - S0);
+  inv_pass_fp<LOGN, S0, RR>(x, tw, fq);
+  if constexpr (S0 + RR < LOGN) {
+    constexpr int RN = cmin(lr_of(LOGN), LOGN - S0 - RR);
+    __syncthreads();
+    inv_store_d<LOGN, S0, RR>(reinterpret_cast<double*>(sm), x);
+    __syncthreads();
+    inv_load_d<LOGN, S0 + RR, RN>(reinterpret_cast<const double*>(sm), x);
+    inv_passes_fp<LOGN, S0 + RR>(x, sm, tw, fq, nv, st);
+  } else {
+#pragma unroll
+    for (int g = 0; g < ((1 << lr_of(LOGN)) >> RR); ++g)
+#pragma unroll
+      for (int j = 0; j < (1 << RR); ++j)
+        st.store(inv_idx<LOGN, S0, RR>(g, j), fp_canon(fp_mulmod(x[g * (1 << RR) + j], nv, fq), fq));
+  }
+}
+
+// input: canonical words scattered into smem (bit-reversed order), synced
+template <int LOGN, class St>
+__device__ __forceinline__ void inv_transform_fp(u64d* sm, St& st, const double* tw, double2 fq, double nv) {
+  constexpr int R0 = cmin(lr_of(LOGN), LOGN);
+  double x[1 << lr_of(LOGN)];
+#pragma unroll
+  for (int g = 0; g < ((1 << lr_of(LOGN)) >> R0); ++g)
+#pragma unroll
+    for (int j = 0; j < (1 << R0); ++j) x[g * (1 << R0) + j] = u2d(sm[pad(inv_idx<LOGN, 0, R0>(g, j))]);
+  inv_passes_fp<LOGN, 0>(x, sm, tw, fq, nv, st);
+}
+
 // ------------------------------------------------------------ functors
 struct LdPlain {
   const u64d* p;
@@ -272,6 +456,33 @@ __device__ __forceinline__ const ulonglong2* twi(const TwArgs& t, int pi, int N)
   return t.tw + ((size_t)pi * 2 + 1) * N;
 }
 
+// forward / inverse transform of prime pi on the FP64 path when the prime
+// allows it (q < 2^45), else on the integer path; same words either way
+template <int LOGN, class Ld>
+__device__ __forceinline__ void fwd_t(u64d* sm, const Ld& ld, const TwArgs& ta, int pi, u64d q) {
+  constexpr int N = 1 << LOGN;
+#if HEGPU_NTT_FP
+  const double2 fq = ta.fpq[pi];
+  if (fq.x != 0.0) {
+    fwd_transform_fp<LOGN>(sm, ld, ta.twd + (size_t)pi * 2 * N, fq);
+    return;
+  }
+#endif
+  fwd_transform<LOGN>(sm, ld, twf(ta, pi, N), q);
+}
+template <int LOGN, class St>
+__device__ __forceinline__ void inv_t(u64d* sm, St& st, const TwArgs& ta, int pi, u64d q) {
+  constexpr int N = 1 << LOGN;
+#if HEGPU_NTT_FP
+  const double2 fq = ta.fpq[pi];
+  if (fq.x != 0.0) {
+    inv_transform_fp<LOGN>(sm, st, ta.twd + ((size_t)pi * 2 + 1) * N, fq, u2d(ta.ninv[2 * pi]));
+    return;
+  }
+#endif
+  inv_transform<LOGN>(sm, st, twi(ta, pi, N), q, ta.ninv[2 * pi], ta.ninv[2 * pi + 1]);
+}
+
 // one pass over a row: R = 2^lr words per thread, compile-time trip count so
 // the loads of all R iterations are issued together (measured: helps the
 // drop-limb epilogue, costs spills in the other row kernels)
@@ -293,7 +504,7 @@ __global__ void NTT_BOUNDS k_ntt_rows(TwArgs ta, PrimeTable pt, const u64d* __re
   constexpr int N = 1 << LOGN;
   const int r = blockIdx.x, limb = r % nl;
   const int pi = (limb == p_limb) ? p_index : limb;
-  fwd_transform<LOGN>(sm, LdPlain{src + (size_t)r * N}, twf(ta, pi, N), pt.p[pi].q);
+  fwd_t<LOGN>(sm, LdPlain{src + (size_t)r * N}, ta, pi, pt.p[pi].q);
   u64d* d = dst + (size_t)r * N;
   for (int p = threadIdx.x; p < N; p += blockDim.x) d[p] = sm[pad(__ldg(ta.slot_src + p))];
 }
@@ -314,7 +525,7 @@ __global__ void NTT_BOUNDS k_intt_rows(TwArgs ta, PrimeTable pt, const u64d* __r
   for (int p = threadIdx.x; p < N; p += blockDim.x) sm[pad(__ldg(ta.slot_src + p))] = s[p];
   __syncthreads();
   StPlain st{dst + o * dox + i * di};
-  inv_transform<LOGN>(sm, st, twi(ta, pi, N), pt.p[pi].q, ta.ninv[2 * pi], ta.ninv[2 * pi + 1]);
+  inv_t<LOGN>(sm, st, ta, pi, pt.p[pi].q);
 }
 
 // KS input: digit j of (shifted) poly b -> coefficient row tmp[b][j]; also
@@ -336,7 +547,7 @@ __global__ void NTT_BOUNDS k_ks_intt(TwArgs ta, PrimeTable pt, const u64d* __res
   }
   __syncthreads();
   StPlain st{tmp + ((size_t)b * l + j) * N};
-  inv_transform<LOGN>(sm, st, twi(ta, j, N), pt.p[j].q, ta.ninv[2 * j], ta.ninv[2 * j + 1]);
+  inv_t<LOGN>(sm, st, ta, j, pt.p[j].q);
 }
 
 // ModUp: rows (b, j, t') with t = t' < j ? t' : t'+1 over the extended basis
@@ -351,7 +562,7 @@ __global__ void NTT_BOUNDS k_ks_modup(TwArgs ta, PrimeTable pt, const u64d* __re
   const int t = tp < j ? tp : tp + 1;
   const int pi = t == l ? P_index : t;
   const DevPrime pr = pt.p[pi];
-  fwd_transform<LOGN>(sm, LdReduce{tmp + ((size_t)b * l + j) * N, pr, pt.p[j].q > pr.q}, twf(ta, pi, N), pr.q);
+  fwd_t<LOGN>(sm, LdReduce{tmp + ((size_t)b * l + j) * N, pr, pt.p[j].q > pr.q}, ta, pi, pr.q);
   u64d* d = D + (((size_t)b * l + j) * (l + 1) + t) * N;
   for (int p = threadIdx.x; p < N; p += blockDim.x) d[p] = sm[pad(__ldg(ta.slot_src + p))];
 }
@@ -401,7 +612,7 @@ __global__ void NTT_BOUNDS k_drop_ntt(TwArgs ta, PrimeTable pt, const u64d* __re
     in_s = is;
     ad_s = as;
   }
-  fwd_transform<LOGN>(sm, LdLift{tmpP + ((size_t)b * 2 + p) * N, pr, qd, (qd >> 1) >= q}, twf(ta, t, N), q);
+  fwd_t<LOGN>(sm, LdLift{tmpP + ((size_t)b * 2 + p) * N, pr, qd, (qd >> 1) >= q}, ta, t, q);
   const u64d iv = qinv[((size_t)t * np_all + a.pd) * 2], ivp = qinv[((size_t)t * np_all + a.pd) * 2 + 1];
   const int sh = (use_shift && p == 0) ? km.shift[b % km.period] : 0;
   if constexpr (kPre) {
@@ -451,7 +662,7 @@ __global__ void NTT_BOUNDS k_md_intt(TwArgs ta, PrimeTable pt, const u64d* __res
   }
   __syncthreads();
   StPlain st{xz + ((size_t)bp * 2 + which) * N};
-  inv_transform<LOGN>(sm, st, twi(ta, pi, N), pt.p[pi].q, ta.ninv[2 * pi], ta.ninv[2 * pi + 1]);
+  inv_t<LOGN>(sm, st, ta, pi, pt.p[pi].q);
 }
 
 // centered lift of a residue mod m (< m) times a constant c (Shoup pair), mod q
@@ -511,7 +722,7 @@ __global__ void NTT_BOUNDS k_md_ntt(TwArgs ta, PrimeTable pt, const u64d* __rest
   const u64d* X = xz + (size_t)bp * 2 * N;
   LdMd ld{X, X + N, pt.p[a.pd].q, pt.p[lq].q, q, pv, pvp,
           qinv[((size_t)lq * np_all + a.pd) * 2], qinv[((size_t)lq * np_all + a.pd) * 2 + 1], pr.one_sh};
-  fwd_transform<LOGN>(sm, ld, twf(ta, t, N), q);
+  fwd_t<LOGN>(sm, ld, ta, t, q);
   if constexpr (kPre) {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
@@ -552,7 +763,9 @@ __global__ void k_slot_to_wire(const u64d* __restrict__ src, u64d* __restrict__ 
   }
 }
 
-TwArgs tw_args(Context& c) { return TwArgs{(const ulonglong2*)c.d_tw, c.ninv_tab(), c.d_slot_src}; }
+TwArgs tw_args(Context& c) {
+  return TwArgs{(const ulonglong2*)c.d_tw, c.ninv_tab(), c.d_slot_src, c.d_twd, (const double2*)c.d_fpq};
+}
 
 size_t ntt_smem(int N) { return (size_t)(N + (N >> 4) + 1) * 8; }
 
@@ -601,6 +814,17 @@ void prep_kernel(K kernel, size_t bytes) {
 #endif
 
 #ifndef HEGPU_NTT_R8_VARIANT
+// HEGPU_NTT_FP=0 keeps every prime on the integer butterflies (A/B switch)
+bool ntt_fp_enabled() {
+  const char* e = getenv("HEGPU_NTT_FP");
+  return !(e && e[0] == '0');
+}
+// HEGPU_NTT_R8=1: every N <= 2^13 entry point on the 8-words-per-thread build
+static bool ntt_all_r8() {
+  const char* e = getenv("HEGPU_NTT_R8");
+  return e && e[0] == '1';
+}
+
 void upload_twiddles(Context& c) {
   const Params& P = *c.P;
   const int np = P.np(), N = P.n;
@@ -617,6 +841,22 @@ void upload_twiddles(Context& c) {
   }
   CK(cudaMalloc((void**)&c.d_tw, tw.size() * 8));
   CK(cudaMemcpy(c.d_tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice));
+  // FP64 butterflies (§5.1) for primes below 2^45: w as exact doubles, (q, 1/q)
+  std::vector<double> twd((size_t)np * 2 * N), fpq((size_t)np * 2, 0.0);
+  for (int i = 0; i < np; ++i) {
+    const Prime& pr = P.primes[i];
+    if (pr.q >= (1ull << 45) || !ntt_fp_enabled()) continue;
+    fpq[2 * i] = (double)pr.q;
+    fpq[2 * i + 1] = 1.0 / (double)pr.q;
+    for (int k = 0; k < N; ++k) {
+      twd[((size_t)i * 2 + 0) * N + k] = (double)pr.w[k];
+      twd[((size_t)i * 2 + 1) * N + k] = (double)pr.iw[k];
+    }
+  }
+  CK(cudaMalloc((void**)&c.d_twd, twd.size() * 8));
+  CK(cudaMemcpy(c.d_twd, twd.data(), twd.size() * 8, cudaMemcpyHostToDevice));
+  CK(cudaMalloc((void**)&c.d_fpq, fpq.size() * 8));
+  CK(cudaMemcpy(c.d_fpq, fpq.data(), fpq.size() * 8, cudaMemcpyHostToDevice));
 }
 
 #endif  // !HEGPU_NTT_R8_VARIANT
@@ -737,7 +977,8 @@ void NTT_PUB(drop_last_limb)(Context& c, int B, const DropArgs& a, u64d* tmpP) {
 #ifndef HEGPU_NTT_R8_VARIANT
 // per-entry-point choice of the thread granularity (see NTT_PUB above)
 void launch_ntt_rows(Context& c, const u64d* src, u64d* dst, int rows, int nl, int p_limb) {
-  launch_ntt_rows_r16(c, src, dst, rows, nl, p_limb);
+  if (ntt_all_r8()) launch_ntt_rows_r8(c, src, dst, rows, nl, p_limb);
+  else launch_ntt_rows_r16(c, src, dst, rows, nl, p_limb);
 }
 void launch_intt_rows(Context& c, const u64d* src, u64d* dst, int n_outer, int n_inner, long so, long si, long dox,
                       long di, const int* prime_of_inner) {
@@ -746,7 +987,8 @@ void launch_intt_rows(Context& c, const u64d* src, u64d* dst, int n_outer, int n
 void ks_modup(Context& c, const u64d* src, long src_stride, int B, int l, const KeyRowMap* shifts, u64d* tmp,
               u64d* D) {
   c.ks[KS_MODUP] += B;
-  ks_modup_r16(c, src, src_stride, B, l, shifts, tmp, D);
+  if (ntt_all_r8()) ks_modup_r8(c, src, src_stride, B, l, shifts, tmp, D);
+  else ks_modup_r16(c, src, src_stride, B, l, shifts, tmp, D);
 }
 void drop_last_limb(Context& c, int B, const DropArgs& a, u64d* tmpP) {
   c.ks[a.pd == c.L() ? KS_MODDOWN : KS_RESCALE] += B;
