@@ -187,17 +187,24 @@ def config3(args, which=3):
     net = H.Net(ctx, cfg, net_weights(cfg, which))
     setup_s = time.perf_counter() - t0
     B = args.batch
-    first = 0 if args.split_hs else rank * B
+    split = args.split_hs or args.split_first
+    first = 0 if split else rank * B
     taps = np.concatenate([net.encrypt_image(net_image(cfg, first + i), nonce=first + i) for i in range(B)])
     dt = ctx.ct(B * net.ntaps, net.top, taps, DELTA)
     out = ctx.ct(B, net.out_level)
-    if args.split_hs and world > 1:
+    # --split-first: Conv1 + Flat1 by output map; --split-hs: HS1 by diagonal
+    # range; both: two partial-sum all-reduces per step
+    layer = (H.split_first_and_dense(0) if args.split_first and args.split_hs
+             else H.SPLIT_FIRST_LAYER if args.split_first else 0)
+    mode = {(True, False): "split-first", (False, True): "split-hs",
+            (True, True): "split-first+hs"}.get((bool(args.split_first), bool(args.split_hs)), "image-shard")
+    if split and world > 1:
         def run():
-            net.run_split(dt, out, 0, rank, world, lambda t: D.reduce_partials(t, world))
+            net.run_split(dt, out, layer, rank, world, lambda t: D.reduce_partials(t, world))
         run()
         ref = ctx.ct(B, net.out_level)
         net.run(dt, ref)
-        assert np.array_equal(out.download(), ref.download()), "split HS differs from the single-GPU run"
+        assert np.array_equal(out.download(), ref.download()), "split run differs from the single-GPU run"
         fn = run
         ctx.reset_meter()
         fn()
@@ -210,12 +217,12 @@ def config3(args, which=3):
         dist.barrier()
     ms = timed(ctx, fn, args.steps, args.warmup)
     ms = D.max_over_ranks(ms, device=f"cuda:{local}")
-    imgs = B if args.split_hs else B * world
+    imgs = B if split else B * world
     if rank == 0:
         print(json.dumps({
-            "config": which, "batch": B, "n_gpus": world, "mode": "split-hs" if args.split_hs else "image-shard",
+            "config": which, "batch": B, "n_gpus": world, "mode": mode,
             "ms_per_step": ms, "inferences_per_s": imgs / (ms / 1e3),
-            "rotations_per_s": tally[4] * (1 if args.split_hs else world) / (ms / 1e3),
+            "rotations_per_s": tally[4] * (1 if split else world) / (ms / 1e3),
             "hops_per_inference": [t / B for t in tally], "setup_s": setup_s}), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -361,6 +368,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--dims", default="64,256,1024,4096", help="config 1 matrix dims (m and n)")
+    ap.add_argument("--split-first", action="store_true",
+                    help="configs 0 / 3 under torchrun: split Conv1 + Flat1 by output map across ranks")
     ap.add_argument("--split-hs", action="store_true",
                     help="configs 1 / 3 under torchrun: split the (first) HS layer's diagonals across ranks")
     ap.add_argument("--hs", action="store_true",

@@ -273,6 +273,17 @@ int hegpu_net_run(hegpu_net* net, const hegpu_ct* taps, hegpu_ct* out);
  * all-reduce; return 0 on success); every rank then finishes the layer and
  * the rest of the net identically.  Bit-identical to hegpu_net_run. */
 typedef int (*hegpu_reduce_fn)(void* dev_words, size_t words, void* user);
+/* layer = HEGPU_SPLIT_FIRST_LAYER splits the first layer instead (reference
+ * first layer only): rank `part` runs the conv-pack MAC + rescale of output
+ * maps [c_out part / nparts, c_out (part+1) / nparts) and their merge
+ * rotations into disjoint slot ranges; the partial (extended-basis key
+ * inner products, Q-basis part) is summed by `reduce`, then every rank runs
+ * the merge's one ModDown per image and the rest of the net (SURVEY.md §8e
+ * config 3: conv/merge by output map).  Bit-identical to hegpu_net_run. */
+#define HEGPU_SPLIT_FIRST_LAYER (-1)
+/* both splits in one run: the first layer and dense layer k (each with its
+ * own reduce call, first layer first) */
+#define HEGPU_SPLIT_FIRST_AND_DENSE(k) (-2 - (k))
 int hegpu_net_run_split(hegpu_net* net, const hegpu_ct* taps, hegpu_ct* out, int layer, int part, int nparts,
                         hegpu_reduce_fn reduce, void* user);
 /* the same on device-resident compact taps (batch x hegpu_net_compact_image_bytes

@@ -319,5 +319,7 @@ void eval_rotate(Context& c, const u64d* a, long a_stride, int B, int l, const K
 void eval_square(Context& c, const CtBatch& a, CtBatch& out);  // tensor + relin, no rescale
 void eval_square_rescale(Context& c, const CtBatch& a, CtBatch& out);  // tensor + relin + rescale (fused)
 void eval_merge(Context& c, const CtBatch& maps, int nmaps, const KeyRowMap& km, CtBatch& out);
+// one rank's share (maps lo .. lo+M-1 per image) of a merge: acc [B][2][l+1][N], C [B][2][l][N]
+void eval_merge_partial(Context& c, const CtBatch& maps, int M, int lo, int64_t w, u64d* acc, u64d* C);
 
 }  // namespace hegpu

@@ -370,6 +370,27 @@ __global__ void k_merge_c(PrimeTable pt, const u64d* __restrict__ maps, int nimg
   C[(size_t)img * st + (size_t)p * l * N + (size_t)t * N + k] = v;
 }
 
+// the Q-basis part of one rank's share of a merge (maps lo..lo+M-1 of an
+// image, map j rotated by its own offset; kc.shift[j] = 0 for global map 0):
+// poly 0 = sum_j sigma_j(c0_j), poly 1 = c1 of global map 0 if this share has it
+__global__ void k_merge_c_part(PrimeTable pt, const u64d* __restrict__ maps, int nimg, int M, int has0, int l, int N,
+                               KeyRowMap kc, u64d* __restrict__ C) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.y % l, p = blockIdx.y / l, img = blockIdx.z;
+  if (k >= N) return;
+  const int S = N >> 1;
+  const u64d q = pt.p[t].q;
+  const size_t st = (size_t)2 * l * N;
+  const u64d* m = maps + (size_t)img * M * st + (size_t)p * l * N + (size_t)t * N;
+  u64d v = 0;
+  if (p == 0) {
+    for (int j = 0; j < M; ++j) v = add_mod_d(v, m[(size_t)j * st + shifted_pos(k, kc.shift[j], S)], q);
+  } else if (has0) {
+    v = m[k];
+  }
+  C[(size_t)img * st + (size_t)p * l * N + (size_t)t * N + k] = v;
+}
+
 #ifndef HEGPU_CONV_CO
 #define HEGPU_CONV_CO 8
 #endif
@@ -1068,20 +1089,9 @@ void eval_rotate(Context& c, const u64d* a, long a_stride, int B, int l, const K
   c.free(tmp); c.free(D); c.free(acc); c.free(tmpP);
 }
 
-// merge_maps with one lazy ModDown per image (DESIGN.md §4.2); km carries
-// the nmaps-1 shifts / keys (period nmaps-1)
-void eval_merge(Context& c, const CtBatch& maps, int nmaps, const KeyRowMap& km, CtBatch& out) {
-  const int B = out.count, l = maps.level, N = c.N(), G = nmaps - 1;
-  const size_t st = maps.stride();
-  u64d* tmp = c.alloc((size_t)B * G * l * N);
-  u64d* D = c.alloc((size_t)B * G * l * (l + 1) * N);
-  u64d* acc = c.alloc((size_t)B * 2 * (l + 1) * N);
-  u64d* C = c.alloc((size_t)B * 2 * l * N);
-  u64d* tmpP = c.alloc((size_t)B * 2 * N);
-  KeyRowMap kg = km;
-  kg.grp = G;
-  kg.grp_stride = (long)(nmaps * st);
-  ks_modup(c, maps.d + st + (size_t)l * N, (long)st, B * G, l, &kg, tmp, D);
+// acc[b] = sum_g <ModUp digits D[b][g], key_g> over G rotated inputs per image
+static void ks_inner_sum(Context& c, const u64d* D, int B, int G, int l, const KeyRowMap& km, u64d* acc) {
+  const int N = c.N();
   c.ks[KS_INNER] += (int64_t)B * G;
   dim3 gi((N + kTpb - 1) / kTpb, l + 1, (B + kKsKT - 1) / kKsKT);
   const double sbytes = 8.0 * N * ((double)B * G * l * (l + 1) + 2.0 * G * l * (l + 1) + 2.0 * B * (l + 1));
@@ -1099,6 +1109,60 @@ void eval_merge(Context& c, const CtBatch& maps, int nmaps, const KeyRowMap& km,
     LAUNCH_BO(c, "k_ks_inner", sbytes, sops,
               k_ks_inner_sum<<<gi, kTpb, 0, c.stream>>>(c.primes, D, B, G, l, c.L(), N, km, acc));
   }
+}
+
+// one rank's share of merge_maps (config 3 across GPUs): maps
+// [B][M] are global maps lo .. lo+M-1 of each image; map j is rotated right
+// by j*w.  acc = the extended-basis key inner products of the share's
+// rotations, C = its Q-basis part (k_merge_c_part).  The element-wise sum of
+// every share's (acc, C), reduced mod q, ModDown(acc) + C is the merged
+// ciphertext -- bit-identical to eval_merge (the sums precede the rounding).
+void eval_merge_partial(Context& c, const CtBatch& maps, int M, int lo, int64_t w, u64d* acc, u64d* C) {
+  const int B = maps.count / M, l = maps.level, N = c.N(), S = c.S();
+  const size_t st = maps.stride();
+  const int first = lo == 0 ? 1 : 0, G = M - first;
+  if (M > HEGPU_MAX_BATCH_PERIOD) fail(HEGPU_ERR_CAPACITY, "merge_maps: too many maps in one share");
+  KeyRowMap kc{};
+  kc.period = M;
+  for (int j = 0; j < M; ++j) kc.shift[j] = (int)((S - ((int64_t)(lo + j) * w) % S) % S);
+  if (G > 0) {
+    KeyRowMap kg{};
+    kg.period = G;
+    for (int g = 0; g < G; ++g) {
+      kg.shift[g] = kc.shift[first + g];
+      kg.key[g] = c.rot_key(kg.shift[g]).data;
+    }
+    kg.grp = G;
+    kg.grp_stride = (long)(M * st);
+    u64d* tmp = c.alloc((size_t)B * G * l * N);
+    u64d* D = c.alloc((size_t)B * G * l * (l + 1) * N);
+    ks_modup(c, maps.d + first * st + (size_t)l * N, (long)st, B * G, l, &kg, tmp, D);
+    ks_inner_sum(c, D, B, G, l, kg, acc);
+    c.free(tmp);
+    c.free(D);
+  } else {
+    CK(cudaMemsetAsync(acc, 0, (size_t)B * 2 * (l + 1) * N * 8, c.stream));
+  }
+  dim3 gc((N + kTpb - 1) / kTpb, 2 * l, B);
+  LAUNCH_B(c, "k_merge_c", 8.0 * N * ((double)B * (M + 1) * l + 2.0 * B * l),
+           k_merge_c_part<<<gc, kTpb, 0, c.stream>>>(c.primes, maps.d, B, M, first, l, N, kc, C));
+}
+
+// merge_maps with one lazy ModDown per image (DESIGN.md §4.2); km carries
+// the nmaps-1 shifts / keys (period nmaps-1)
+void eval_merge(Context& c, const CtBatch& maps, int nmaps, const KeyRowMap& km, CtBatch& out) {
+  const int B = out.count, l = maps.level, N = c.N(), G = nmaps - 1;
+  const size_t st = maps.stride();
+  u64d* tmp = c.alloc((size_t)B * G * l * N);
+  u64d* D = c.alloc((size_t)B * G * l * (l + 1) * N);
+  u64d* acc = c.alloc((size_t)B * 2 * (l + 1) * N);
+  u64d* C = c.alloc((size_t)B * 2 * l * N);
+  u64d* tmpP = c.alloc((size_t)B * 2 * N);
+  KeyRowMap kg = km;
+  kg.grp = G;
+  kg.grp_stride = (long)(nmaps * st);
+  ks_modup(c, maps.d + st + (size_t)l * N, (long)st, B * G, l, &kg, tmp, D);
+  ks_inner_sum(c, D, B, G, l, km, acc);
   dim3 gc((N + kTpb - 1) / kTpb, 2 * l, B);
   LAUNCH_B(c, "k_merge_c", 8.0 * N * ((double)B * (nmaps + 1) * l + 2.0 * B * l),
            k_merge_c<<<gc, kTpb, 0, c.stream>>>(c.primes, maps.d, B, nmaps, l, N, km, C));

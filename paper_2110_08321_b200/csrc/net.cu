@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 
 #include "handles.hpp"
@@ -34,6 +35,10 @@ struct hegpu_net {
   std::unique_ptr<HsPlan> region_sum;
   double tap_scale = 0, out_scale = 0;
   std::unique_ptr<ConvLayer> conv;
+  // the conv weights as given (conv_w [c_out][ntaps], conv_b), kept for the
+  // per-rank output-map slices of hegpu_net_run_split(layer = -1)
+  std::vector<double> conv_w, conv_b;
+  std::map<std::pair<int, int>, std::unique_ptr<ConvLayer>> conv_slices;
   std::vector<HsPlan> plans;
   std::vector<u64d*> bias;   // per dense layer, [level][N] Montgomery
   std::vector<double> bias_scale;
@@ -68,7 +73,8 @@ struct hegpu_net {
   // hegpu_net_run_split: dense layer `layer`'s HS accumulated over part
   // `part` of `nparts` diagonal ranges, partials combined by `reduce`
   struct Split {
-    int layer = -1, part = 0, nparts = 1;
+    static constexpr int kNone = -1000;  // no split (HEGPU_SPLIT_* codes are >= -1 - n_dense)
+    int layer = kNone, part = 0, nparts = 1;
     hegpu_reduce_fn reduce = nullptr;
     void* user = nullptr;
   } split;
@@ -158,10 +164,20 @@ void run_conv(hegpu_net& net, const CtBatch& taps, CtBatch& maps) {
 }
 
 void run_after_conv(hegpu_net& net, const CtBatch& mb, CtBatch& out);
+void run_dense(hegpu_net& net, CtBatch x, CtBatch& out, u64d* cur_p);
+void run_first_split(hegpu_net& net, const CtBatch& taps, CtBatch& x);
 
 void run_net(hegpu_net& net, const CtBatch& taps, CtBatch& out) {
   Context& c = *net.c;
   const int B = taps.count / net.tap_cts;
+  const int sl = net.split.layer;
+  if (sl != hegpu_net::Split::kNone && (sl == HEGPU_SPLIT_FIRST_LAYER || sl <= HEGPU_SPLIT_FIRST_AND_DENSE(0))) {
+    Scratch cur(c, (size_t)B * 2 * (net.top - 1) * c.N());
+    CtBatch x{&c, B, net.top - 1, 0, cur.p};
+    run_first_split(net, taps, x);
+    run_dense(net, x, out, cur.p);
+    return;
+  }
   const int mo = net.conv->out_per_image();
   Scratch maps(c, (size_t)B * mo * 2 * (net.top - 1) * c.N());
   CtBatch mb{&c, B * mo, net.top - 1, 0, maps.p};
@@ -169,12 +185,73 @@ void run_net(hegpu_net& net, const CtBatch& taps, CtBatch& out) {
   run_after_conv(net, mb, out);
 }
 
+// config 3 across GPUs, the first layer: this rank's share
+// lo .. hi-1 of the c_out output maps -- their conv-pack MAC + rescale and
+// their merge rotations (map j rotated right by j d_out^2 into its slot
+// range) -- accumulated as (extended-basis acc, Q-basis C); the caller's
+// reduction sums every rank's share; every rank then reduces mod q and runs
+// the one ModDown per image: the merged ciphertext, bit-identical to the
+// single-GPU Conv1 + Flat1
+void run_first_split(hegpu_net& net, const CtBatch& taps, CtBatch& x) {
+  Context& c = *net.c;
+  const hegpu_net_spec& s = net.spec;
+  const auto& sp = net.split;
+  const int B = x.count, N = c.N(), l = net.top - 1;
+  const int lo = s.c_out * sp.part / sp.nparts, hi = s.c_out * (sp.part + 1) / sp.nparts, M = hi - lo;
+  c.meter.begin(net.conv_label);
+  c.meter.bump(HEGPU_MUL_PC, (int64_t)B * net.ntaps * M);
+  c.meter.bump(HEGPU_ADD_CC, (int64_t)B * (net.ntaps - 1) * M);
+  c.meter.bump(HEGPU_ADD_PC, (int64_t)B * M);
+  const size_t acc_w = (size_t)B * 2 * (l + 1) * N, c_w = (size_t)B * 2 * l * N;
+  Scratch part(c, acc_w + c_w);
+  u64d* acc = part.p;
+  u64d* C = part.p + acc_w;
+  if (M > 0) {
+    auto key = std::make_pair(lo, hi);
+    auto it = net.conv_slices.find(key);
+    if (it == net.conv_slices.end()) {
+      const double* w = net.conv_w.data() + (size_t)lo * net.ntaps;
+      it = net.conv_slices
+               .emplace(key, std::make_unique<ConvLayer>(c, net.ntaps, M, w, net.conv_b.data() + lo, net.w_used,
+                                                         net.top, net.tap_scale))
+               .first;
+    }
+    Scratch maps(c, (size_t)B * M * 2 * l * N);
+    CtBatch mb{&c, B * M, l, 0, maps.p};
+    it->second->run(c, taps, mb);
+    c.meter.begin("Flat1");
+    eval_merge_partial(c, mb, M, lo, net.w_used, acc, C);
+    const int64_t rots = M - (lo == 0 ? 1 : 0);
+    c.meter.bump(HEGPU_ROT, (int64_t)B * rots);
+    c.meter.bump(HEGPU_ADD_CC, (int64_t)B * rots);
+  } else {
+    c.meter.begin("Flat1");
+    CK(cudaMemsetAsync(part.p, 0, (acc_w + c_w) * 8, c.stream));
+  }
+  CK(cudaStreamSynchronize(c.stream));
+  need(sp.reduce(part.p, acc_w + c_w, sp.user) == 0, HEGPU_ERR_CUDA,
+       "net_run_split: the partial-sum reduction failed");
+  if (sp.nparts > 1) {  // sums of nparts reduced residues
+    launch_reduce_rows(c, acc, acc_w, l + 1, l);
+    launch_reduce_rows(c, C, c_w, l, -1);
+  }
+  u64d* tmpP = c.alloc((size_t)B * 2 * N);
+  DropArgs d{};
+  d.src = acc; d.src_b = 2L * (l + 1) * N; d.src_p = (long)(l + 1) * N; d.src_limbs = l + 1;
+  d.dst = x.d; d.dst_b = (long)x.stride(); d.dst_p = (long)l * N;
+  d.pd = c.L(); d.nl = l;
+  d.add = C; d.add_b = 2L * l * N; d.add_p = (long)l * N; d.add_mask = 3; d.shifts = nullptr;
+  drop_last_limb(c, B, d, tmpP);
+  c.free(tmpP);
+  x.scale = taps.scale;
+}
+
 // Flat1 onwards, on the conv-layer maps
 void run_after_conv(hegpu_net& net, const CtBatch& mb, CtBatch& out) {
   Context& c = *net.c;
   const hegpu_net_spec& s = net.spec;
   const int mo = net.conv->out_per_image(), B = mb.count / mo, N = c.N();
-  int l = mb.level;
+  const int l = mb.level;
   // Flat1: Merge (netcompile.cpp:332-347): c_out - 1 key-switched
   // rotations summed lazily with one ModDown per image (eval_merge).  With
   // the fused first layer the maps already sit at their merged offsets (one
@@ -186,6 +263,17 @@ void run_after_conv(hegpu_net& net, const CtBatch& mb, CtBatch& out) {
   merge_maps(c, mb, mo, net.w_used, x);
   c.meter.bump(HEGPU_ROT, (int64_t)B * (s.c_out - 1));
   c.meter.bump(HEGPU_ADD_CC, (int64_t)B * (s.c_out - 1));
+  run_dense(net, x, out, cur.p);
+}
+
+// Square<i> / Dense<i> pairs on the merged ciphertexts x (level top - 1);
+// cur_p is x's buffer, reused for the intermediate layer outputs
+void run_dense(hegpu_net& net, CtBatch x, CtBatch& out, u64d* cur_p) {
+  Context& c = *net.c;
+  const hegpu_net_spec& s = net.spec;
+  const int B = x.count, N = c.N();
+  int l = x.level;
+  struct { u64d* p; } cur{cur_p};
   Scratch nxt(c, (size_t)B * 2 * l * N);
   for (int i = 0; i < s.n_dense; ++i) {
     // Square<i> (netcompile.cpp:348-351)
@@ -201,7 +289,12 @@ void run_after_conv(hegpu_net& net, const CtBatch& mb, CtBatch& out) {
     CtBatch z{&c, B, l - 1, 0, last ? out.d : cur.p};
     const int64_t kept = (int64_t)pl.diag.size();
     int i_lo = 0, i_hi = (int)kept;
-    if (net.split.layer == i) {
+    const int sl = net.split.layer;
+    const int split_dense = sl == hegpu_net::Split::kNone                 ? -1
+                            : sl >= 0                                    ? sl
+                            : sl <= HEGPU_SPLIT_FIRST_AND_DENSE(0)       ? -2 - sl
+                                                                         : -1;
+    if (split_dense == i) {
       // this rank's diagonal range; partial sums combined by the caller's
       // reduction (NCCL all-reduce), then one ModDown / rescale / folds
       const auto& sp = net.split;
@@ -267,6 +360,9 @@ extern "C" int hegpu_net_create(hegpu_ctx* h, const hegpu_net_spec* spec, const 
          "Flat1: group footprint " + std::to_string(s.c_out * net->w_used) + " > n_slots = " + std::to_string(S));
     need(c.L() >= 2 + 2 * s.n_dense, HEGPU_ERR_CAPACITY, "net: Q chain too short for the level schedule");
     net->tap_scale = std::ldexp(1.0, 40);
+    net->conv_w.assign(conv_w, conv_w + (size_t)s.c_out * net->ntaps);
+    if (conv_b) net->conv_b.assign(conv_b, conv_b + s.c_out);
+    else net->conv_b.assign(s.c_out, 0.0);
     net->conv = std::make_unique<ConvLayer>(c, net->ntaps, s.c_out, conv_w, conv_b, net->w_used, net->top,
                                             net->tap_scale);
     std::vector<int64_t> rots;
@@ -355,7 +451,13 @@ extern "C" int hegpu_net_run_split(hegpu_net* net, const hegpu_ct* taps, hegpu_c
   if (!net || !taps || !out || !reduce) return HEGPU_ERR_ARG;
   Context& c = *net->c;
   return guarded(&c, [&] {
-    need(layer >= 0 && layer < net->spec.n_dense, HEGPU_ERR_RANGE, "net_run_split: no such dense layer");
+    need(layer > hegpu_net::Split::kNone, HEGPU_ERR_RANGE, "net_run_split: no such layer");
+    const bool first = layer == HEGPU_SPLIT_FIRST_LAYER || layer <= HEGPU_SPLIT_FIRST_AND_DENSE(0);
+    const int dense = layer >= 0 ? layer : layer <= HEGPU_SPLIT_FIRST_AND_DENSE(0) ? -2 - layer : -1;
+    need(first || dense >= 0, HEGPU_ERR_RANGE, "net_run_split: no such layer");
+    need(dense < net->spec.n_dense, HEGPU_ERR_RANGE, "net_run_split: no such dense layer");
+    need(!first || net->spec.first_layer == HEGPU_FIRST_LAYER_REFERENCE, HEGPU_ERR_ARG,
+         "net_run_split: the first-layer split needs the reference first layer (per-map conv + merge)");
     need(nparts >= 1 && nparts <= 8 && part >= 0 && part < nparts, HEGPU_ERR_RANGE, "net_run_split: bad part");
     need(taps->b.level == net->top && taps->b.count % net->tap_cts == 0, HEGPU_ERR_SHAPE,
          "net_run_split: taps must be B * tap_cts ciphertexts at the top level");

@@ -562,7 +562,10 @@ __global__ void NTT_BOUNDS k_ks_modup(TwArgs ta, PrimeTable pt, const u64d* __re
   const int t = tp < j ? tp : tp + 1;
   const int pi = t == l ? P_index : t;
   const DevPrime pr = pt.p[pi];
-  fwd_t<LOGN>(sm, LdReduce{tmp + ((size_t)b * l + j) * N, pr, pt.p[j].q > pr.q}, ta, pi, pr.q);
+  // the FP64 path takes any word < 4q exactly: a digit of another prime
+  // below 2^45 needs no reduction there (q_j < 2 q_t)
+  const bool need = pt.p[j].q > pr.q && !(HEGPU_NTT_FP && ta.fpq[pi].x != 0.0 && pt.p[j].q < (1ull << 45));
+  fwd_t<LOGN>(sm, LdReduce{tmp + ((size_t)b * l + j) * N, pr, need}, ta, pi, pr.q);
   u64d* d = D + (((size_t)b * l + j) * (l + 1) + t) * N;
   for (int p = threadIdx.x; p < N; p += blockDim.x) d[p] = sm[pad(__ldg(ta.slot_src + p))];
 }

@@ -711,6 +711,14 @@ class Model:
         return spec
 
 
+SPLIT_FIRST_LAYER = -1  # hegpu_net_run_split: split Conv1 + Flat1 by output map
+
+
+def split_first_and_dense(k):
+    """hegpu_net_run_split layer code: the first layer and dense layer k"""
+    return -2 - k
+
+
 class Net:
     """Stage driver (execute, proj/src/netcompile.cpp:291-446) for the
     Conv -> (Square -> Dense)* family on a batch of images."""
@@ -774,8 +782,10 @@ class Net:
 
     def run_split(self, taps_ct, out_ct, layer, part, nparts, reduce):
         """hegpu_net_run_split: dense layer `layer`'s HS over diagonal range
-        `part` of `nparts`; reduce(t) receives the partial accumulator as a
-        CUDA int64 tensor view and must sum it over all parts in place"""
+        `part` of `nparts` (layer = SPLIT_FIRST_LAYER: the conv + merge of
+        output maps share `part`); reduce(t) receives the partial
+        accumulator as a CUDA int64 tensor view and must sum it over all
+        parts in place"""
         import torch
 
         def cb(ptr, words, _user):

@@ -84,3 +84,19 @@ def test_reduce_partials_two_ranks():
 def test_image_ranges_partition_the_batch():
     seen = [i for r in range(4) for i in D.image_range(r, 64)]
     assert seen == list(range(256))
+
+
+def test_launch_ranks_gloo(tmp_path):
+    """the real host launcher (dist.launch_ranks, used by bench.py --gpus N
+    without a torchrun environment): N processes under torch.distributed.run
+    on 127.0.0.1, each joining the group from the environment it sets"""
+    import os
+    import sys
+    out = tmp_path / "r.json"
+    script = os.path.join(os.path.dirname(os.path.abspath(__file__)), "dist_launch_worker.py")
+    rc = D.launch_ranks(2, script, [str(out)], env={"NCCL_DEBUG": "WARN"}, timeout=300)
+    assert rc == 0
+    import json
+    r = json.loads(out.read_text())
+    assert r["world"] == 2 and r["sum"] == 3 and r["tmax"] == 0.5 and r["master"] == "127.0.0.1"
+    assert r["gathered"] == [100] * 4 + [101] * 4

@@ -536,6 +536,80 @@ def test_cfg0_net_run_split_dense1(cfg0):
             assert two[st] == tuple(2 * x for x in one_run[st])
 
 
+@pytest.mark.parametrize("nparts", [2, 3, 5])
+def test_cfg0_net_run_split_first_layer(cfg0, nparts):
+    """config 3's first-layer split: each "rank" runs the
+    conv + merge rotations of its share of the c_out = 5 output maps, the
+    (extended-basis, Q-basis) partials are summed by the reduction (here:
+    earlier parts stashed and added by the last), every rank finishes the
+    merge's ModDown and the rest of the net -- bit-identical to the
+    single-GPU run; Conv1 / Flat1 HOPs of the parts add up to one run's"""
+    cfg, ctx, ck, w, net = cfg0
+    B = 2
+    imgs = [net_image(cfg, 90 + s) for s in range(B)]
+    taps = ctx.ct(B * net.tap_cts, net.top,
+                  np.concatenate([net.encrypt_image(im, nonce=90 + s) for s, im in enumerate(imgs)]), DELTA)
+    ref = ctx.ct(B, net.out_level)
+    ctx.reset_meter()
+    net.run(taps, ref)
+    one_run = dict(ctx.stages())
+    want = ref.download()
+    stash = []
+    ctx.reset_meter()
+    out = ctx.ct(B, net.out_level)
+    for part in range(nparts):
+        def red(t, last=part == nparts - 1):
+            if last:
+                for p in stash:
+                    t.add_(p)
+            else:
+                stash.append(t.clone())
+        net.run_split(taps, out if part == nparts - 1 else ctx.ct(B, net.out_level), H.SPLIT_FIRST_LAYER, part,
+                      nparts, red)
+    assert np.array_equal(out.download(), want)
+    parts = dict(ctx.stages())
+    for st in ("Conv1", "Flat1"):
+        assert parts[st] == one_run[st], st
+    for st in one_run:
+        if st not in ("Conv1", "Flat1"):
+            assert parts[st] == tuple(nparts * x for x in one_run[st])
+    with pytest.raises(H.HegpuError):
+        net.run_split(taps, out, 7, 0, 2, lambda t: None)
+    # both splits in one run (first layer, then HS1): two reductions per run.
+    # Every rank needs the full first-layer sum before its HS1 range, so the
+    # one-GPU emulation first collects each part's first-layer partial (the
+    # run is aborted by a failing reduction), then runs every part with the
+    # first reduction completed from the others' partials
+    first = {}
+    for part in range(nparts):
+        def grab(t, part=part):
+            first[part] = t.clone()
+            raise RuntimeError("stop after the first-layer partial")
+        with pytest.raises(H.HegpuError):
+            net.run_split(taps, ctx.ct(B, net.out_level), H.split_first_and_dense(0), part, nparts, grab)
+    hs1 = []
+    out2 = ctx.ct(B, net.out_level)
+    for part in range(nparts):
+        calls = [0]
+
+        def red2(t, part=part, last=part == nparts - 1):
+            k = calls[0]
+            calls[0] += 1
+            if k == 0:
+                for q, p in first.items():
+                    if q != part:
+                        t.add_(p)
+            elif last:
+                for p in hs1:
+                    t.add_(p)
+            else:
+                hs1.append(t.clone())
+        net.run_split(taps, out2 if part == nparts - 1 else ctx.ct(B, net.out_level), H.split_first_and_dense(0),
+                      part, nparts, red2)
+        assert calls[0] == 2
+    assert np.array_equal(out2.download(), want)
+
+
 def test_cfg0_net_from_model_files(cfg0, tmp_path):
     """hegpu_net_create_from_model: the cfg-0 net described as a model JSON +
     float32 weights file + float32 input file (the reference's formats)
