@@ -58,7 +58,7 @@ def config1(args):
     if world > 1:
         dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
-    ctx = H.Context(14, [60, 40], 60, seed=1, device=local)
+    ctx = H.Context(14, [45, 40], 45, seed=1, device=local)
     dims = [int(x) for x in args.dims.split(",")]
     for m in dims:
         for n in dims:
@@ -124,7 +124,7 @@ def config1_lola(args):
     counts, which equal predict_lola_* (matvec.cpp:189-211)."""
     from paper_2110_08321_b200 import hegpu as H
     from paper_2110_08321_b200.workloads import hs_sweep_case
-    ctx = H.Context(14, [60, 40, 40], 60, seed=1)
+    ctx = H.Context(14, [45, 40, 40], 45, seed=1)
     dims = [int(x) for x in args.dims.split(",")]
     for kind in ("dense", "stacked"):
         for m in dims:
@@ -265,7 +265,7 @@ def config4(args):
     if world > 1:
         dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
-    ctx = H.Context(14, [60, 40], 60, seed=4, device=local)
+    ctx = H.Context(14, [45, 40], 45, seed=4, device=local)
     rng = np.random.default_rng(4)
 
     def tmax(ms):

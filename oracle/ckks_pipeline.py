@@ -25,24 +25,41 @@ def hs_masks(ck, A, level, skip_zero=True):
     return m_eff, folds, rots, (np.concatenate(enc) if enc else np.zeros(0, dtype=np.uint64))
 
 
-def fold_rotations(S, m_eff, folds):
+MAX_FOLD_GROUP = 5  # hoisted fold groups of at most 2^5 - 1 rotations (layers.cu fold_groups)
+
+
+def fold_groups(folds):
+    """the log-depth fold's `folds` doublings split into ceil(folds / 5)
+    groups of near-equal size, larger first (layers.cu fold_groups)"""
+    if folds <= 0:
+        return []
+    g = -(-folds // MAX_FOLD_GROUP)
+    return [folds // g + (1 if i < folds % g else 0) for i in range(g)]
+
+
+def fold_rotations(S, m_eff, folds, offset=0):
     """the log-depth fold s += rot_left(s, m_eff 2^t), t = folds-1 .. 0
     (proj/src/matvec.cpp:101-103) sums rot_left(s, m_eff u) over u <
-    2^folds; as right rotations, ascending (0 first)"""
-    return sorted({(S - (m_eff * u) % S) % S for u in range(1 << folds)})
+    2^folds; a group of `folds` doublings starting at doubling `offset`
+    sums rot_left(s, m_eff 2^offset u); as right rotations, ascending (0 first)"""
+    step = m_eff << offset
+    return sorted({(S - (step * u) % S) % S for u in range(1 << folds)})
 
 
 def fold_sum(ck, u, l, m_eff, folds, key):
-    """the fold as ONE hoisted rotation sum: one ModUp of u.c1, 2^folds - 1
-    key-switch inner products on the rotated digits, one ModDown (the HS
-    machinery with unit masks) -- the same slots as the serial folds,
-    metered as the reference's `folds` rotations"""
-    if folds == 0:
-        return u
-    rots = fold_rotations(ck.S, m_eff, folds)
-    ones = np.ones(len(rots) * (l + 1) * ck.N, dtype=np.uint64)
-    kl = [key(ck.galois_right(r)) for r in rots if r != 0]
-    return ck.hs_hoisted(u, l, np.array(rots, dtype=np.int64), ones, np.concatenate(kl))
+    """the fold as hoisted rotation sums: per group of a doublings one ModUp
+    of u.c1, 2^a - 1 key-switch inner products on the rotated digits, one
+    ModDown (the HS machinery with unit masks); groups applied in order of
+    their offset -- the same slots as the serial folds, metered as the
+    reference's `folds` rotations"""
+    off = 0
+    for a in fold_groups(folds):
+        rots = fold_rotations(ck.S, m_eff, a, off)
+        ones = np.ones(len(rots) * (l + 1) * ck.N, dtype=np.uint64)
+        kl = [key(ck.galois_right(r)) for r in rots if r != 0]
+        u = ck.hs_hoisted(u, l, np.array(rots, dtype=np.int64), ones, np.concatenate(kl))
+        off += a
+    return u
 
 
 def hs_matvec(ck, v, level, A, skip_zero=True, keys=None):
@@ -202,10 +219,13 @@ class PreparedNet:
             m_eff, folds, rots, masks = hs_masks(ck, np.asarray(W), l, True)
             kl = [key(ck.galois_right(r)) for r in rots if r != 0]
             kbuf = np.concatenate(kl) if kl else np.zeros(1, dtype=np.uint64)
-            frots = fold_rotations(ck.S, m_eff, folds) if folds else [0]
-            fkl = [key(ck.galois_right(r)) for r in frots if r != 0]
-            fold = (np.array(frots, dtype=np.int64), np.ones(len(frots) * l * ck.N, dtype=np.uint64),
-                    np.concatenate(fkl) if fkl else None)
+            fold, off = [], 0
+            for a in fold_groups(folds):
+                frots = fold_rotations(ck.S, m_eff, a, off)
+                fkl = [key(ck.galois_right(r)) for r in frots if r != 0]
+                fold.append((np.array(frots, dtype=np.int64), np.ones(len(frots) * l * ck.N, dtype=np.uint64),
+                             np.concatenate(fkl)))
+                off += a
             l -= 1
             bias = ck.encode(np.asarray(b), scale, l)
             self.layers.append((l + 1, np.array(rots, dtype=np.int64), masks, kbuf, fold, bias))
@@ -228,8 +248,8 @@ class PreparedNet:
             l = lv
             u = ck.rescale(ck.hs_hoisted(x, l, rots, masks, kbuf), l)
             l -= 1
-            if fold[2] is not None:  # the folds as one hoisted rotation sum
-                u = ck.hs_hoisted(u, l, fold[0], fold[1], fold[2])
+            for frots, fones, fkeys in fold:  # the folds as hoisted rotation sums
+                u = ck.hs_hoisted(u, l, frots, fones, fkeys)
             x = ck.add_pc(u, bias, l)
         return x
 

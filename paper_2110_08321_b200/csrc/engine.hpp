@@ -58,6 +58,7 @@ struct Context {
   u64d* d_tw = nullptr;          // [np][2][N] (w, w') pairs: forward, inverse
   double* d_twd = nullptr;       // [np][2][N] w as doubles (FP64 NTT path, primes < 2^45)
   double* d_fpq = nullptr;       // [np][2] (q, 1/q), or (0, 0) for primes on the integer path
+  bool fp_all = false;           // every prime on the FP64 path: the FP64-only NTT builds run
   u64d* d_consts = nullptr;      // [np]: ninv, ninv' ; then [np][np]: qinv(value, shoup)
   uint32_t* d_slot_src = nullptr;  // [N]
   std::map<int, DeviceKey> rot_keys;  // keyed by left shift in [1, S)
@@ -247,6 +248,17 @@ void ks_modup_r16(Context& c, const u64d* src, long src_stride, int B, int l, co
                   u64d* D);
 void drop_last_limb_r8(Context& c, int B, const DropArgs& a, u64d* tmpP);
 void drop_last_limb_r16(Context& c, int B, const DropArgs& a, u64d* tmpP);
+// FP64-only builds (every prime < 2^45): ntt_fp16.cu, ntt_fp8.cu
+#define HEGPU_NTT_DECL(S)                                                                                   \
+  void launch_ntt_rows##S(Context& c, const u64d* src, u64d* dst, int rows, int nl, int p_limb);            \
+  void launch_intt_rows##S(Context& c, const u64d* src, u64d* dst, int n_outer, int n_inner, long so, long si, \
+                           long dox, long di, const int* prime_of_inner);                                 \
+  void ks_modup##S(Context& c, const u64d* src, long src_stride, int B, int l, const KeyRowMap* shifts,      \
+                   u64d* tmp, u64d* D);                                                                     \
+  void drop_last_limb##S(Context& c, int B, const DropArgs& a, u64d* tmpP);
+HEGPU_NTT_DECL(_fp16)
+HEGPU_NTT_DECL(_fp8)
+#undef HEGPU_NTT_DECL
 
 // pointwise (eval.cu)
 void launch_add(Context& c, const u64d* a, const u64d* b, u64d* out, int count, int l);

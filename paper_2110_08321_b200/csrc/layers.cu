@@ -310,8 +310,8 @@ void HsPlan::build(Context& c, const double* A, int m_, int n_, int lvl, bool sk
 
 void HsPlan::release() {
   if (ctx) cudaStreamSynchronize(ctx->stream);
-  if (fold) fold->release();
-  fold.reset();
+  for (auto& f : fold) f->release();
+  fold.clear();
   cudaFree(masks);
   cudaFree(d_r);
   cudaFree(d_chunk);
@@ -331,13 +331,26 @@ void HsPlan::release() {
   fkeys = nullptr;
 }
 
-std::vector<int64_t> HsPlan::fold_rights() const {
+// the fold's doublings in ceil(folds / 5) groups of near-equal size, larger
+// first: a group of a doublings is one hoisted sum of 2^a - 1 key inner
+// products, so 7 doublings cost 15 + 7 inner products and two ModUp /
+// ModDown pairs instead of 127 (the config-1 m = 64, n = 4096 point);
+// oracle/ckks_pipeline.fold_groups mirrors it
+std::vector<int> HsPlan::fold_groups() const {
+  std::vector<int> g;
+  if (folds <= 0) return g;
+  const int n = (folds + kMaxFoldGroup - 1) / kMaxFoldGroup;
+  for (int i = 0; i < n; ++i) g.push_back(folds / n + (i < folds % n ? 1 : 0));
+  return g;
+}
+
+std::vector<int64_t> HsPlan::fold_rights(int offset, int size) const {
   // s += rot_left(s, m_eff 2^t) for t = folds-1..0 sums rot_left(s, m_eff u)
-  // over u < 2^folds (distinct: m_eff 2^folds <= S in both branches)
-  const int64_t S = ctx->S();
+  // over u < 2^folds (distinct: m_eff 2^folds <= S in both branches); the
+  // group of `size` doublings from `offset` sums rot_left(s, m_eff 2^offset u)
+  const int64_t S = ctx->S(), step = (int64_t)m_eff << offset;
   std::vector<int64_t> r;
-  if (folds > 0)
-    for (int64_t u = 0; u < (int64_t{1} << folds); ++u) r.push_back((S - (m_eff * u) % S) % S);
+  for (int64_t u = 0; u < (int64_t{1} << size); ++u) r.push_back((S - (step * u) % S) % S);
   std::sort(r.begin(), r.end());
   return r;
 }
@@ -346,8 +359,12 @@ std::vector<int64_t> HsPlan::right_rotations() const {
   std::vector<int64_t> r;
   for (const HsDiag& d : diag)
     if (d.right) r.push_back(d.right);
-  for (int64_t f : fold_rights())
-    if (f) r.push_back(f);  // the fold's hoisted rotations
+  int off = 0;
+  for (int a : fold_groups()) {
+    for (int64_t f : fold_rights(off, a))
+      if (f) r.push_back(f);  // the fold's hoisted rotations
+    off += a;
+  }
   return r;
 }
 
@@ -562,18 +579,24 @@ void HsPlan::finish(Context& c, int B, double v_scale, u64d* acc, u64d* cacc, in
   out.scale = v_scale;
   // (5) log-depth fold, matvec.cpp:101-103: s += rot_left(s, m_eff * 2^t)
   // for t = folds-1..0 = sum of rot_left(s, m_eff u) over u < 2^folds, run
-  // as ONE hoisted rotation sum (one ModUp of s.c1, the 2^folds - 1 key
-  // inner products on the rotated digits, one ModDown) instead of `folds`
-  // serial key switches; metered as the reference's folds (capi.cu)
-  if (folds > 0) {
-    const int lf = l - 1;
-    if (!fold) {
-      fold = std::make_unique<HsPlan>();
-      fold->build_rotsum(c, fold_rights(), lf);
+  // as hoisted rotation sums, one per group of <= 5 doublings (one ModUp of
+  // s.c1, the 2^a - 1 key inner products on the rotated digits, one
+  // ModDown) instead of `folds` serial key switches; metered as the
+  // reference's folds (capi.cu)
+  const std::vector<int> groups = fold_groups();
+  if (fold.empty()) {
+    int off = 0;
+    for (int a : groups) {
+      fold.push_back(std::make_unique<HsPlan>());
+      fold.back()->build_rotsum(c, fold_rights(off, a), l - 1);
+      off += a;
     }
+  }
+  for (auto& fp : fold) {
+    const int lf = l - 1;
     u64d* facc = c.alloc((size_t)B * 2 * (lf + 1) * N);
     u64d* fcacc = c.alloc((size_t)B * 2 * lf * N);
-    fold->accumulate(c, out, 0, (int)fold->diag.size(), facc, fcacc);
+    fp->accumulate(c, out, 0, (int)fp->diag.size(), facc, fcacc);
     CtBatch r{&c, B, lf, out.scale, c.alloc((size_t)B * 2 * lf * N)};
     DropArgs f{};
     f.src = facc; f.src_b = 2L * (lf + 1) * N; f.src_p = (long)(lf + 1) * N; f.src_limbs = lf + 1;

@@ -77,11 +77,14 @@ struct HsPlan {
   bool imma_built = false;
   void ensure_imma(Context& c);
   bool use_imma(Context& c, int B, int i_lo, int i_hi) const;
-  // the log-depth fold (matvec.cpp:101-103) as one hoisted rotation sum:
-  // a unit-mask plan over rot_left(., m_eff u), u < 2^folds, at level - 1
-  std::unique_ptr<HsPlan> fold;
+  // the log-depth fold (matvec.cpp:101-103) as hoisted rotation sums: the
+  // `folds` doublings in groups of <= kMaxFoldGroup (fold_groups), each a
+  // unit-mask plan over rot_left(., m_eff 2^offset u), u < 2^size, at level - 1
+  static constexpr int kMaxFoldGroup = 5;
+  std::vector<std::unique_ptr<HsPlan>> fold;
   bool unit_masks = false;  // a rotation-sum plan (build_rotsum)
-  std::vector<int64_t> fold_rights() const;  // ascending, 0 first
+  std::vector<int> fold_groups() const;
+  std::vector<int64_t> fold_rights(int offset, int size) const;  // ascending, 0 first
   void build_rotsum(Context& c, const std::vector<int64_t>& rights, int level);
   void build(Context& c, const double* A, int m, int n, int level, bool skip_zero);
   void release();

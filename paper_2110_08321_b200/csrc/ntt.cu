@@ -461,6 +461,10 @@ __device__ __forceinline__ const ulonglong2* twi(const TwArgs& t, int pi, int N)
 template <int LOGN, class Ld>
 __device__ __forceinline__ void fwd_t(u64d* sm, const Ld& ld, const TwArgs& ta, int pi, u64d q) {
   constexpr int N = 1 << LOGN;
+#ifdef HEGPU_NTT_FPONLY  // every prime of the context is on the FP64 path (launcher checks)
+  fwd_transform_fp<LOGN>(sm, ld, ta.twd + (size_t)pi * 2 * N, ta.fpq[pi]);
+  return;
+#endif
 #if HEGPU_NTT_FP
   const double2 fq = ta.fpq[pi];
   if (fq.x != 0.0) {
@@ -473,6 +477,10 @@ __device__ __forceinline__ void fwd_t(u64d* sm, const Ld& ld, const TwArgs& ta, 
 template <int LOGN, class St>
 __device__ __forceinline__ void inv_t(u64d* sm, St& st, const TwArgs& ta, int pi, u64d q) {
   constexpr int N = 1 << LOGN;
+#ifdef HEGPU_NTT_FPONLY
+  inv_transform_fp<LOGN>(sm, st, ta.twd + ((size_t)pi * 2 + 1) * N, ta.fpq[pi], u2d(ta.ninv[2 * pi]));
+  return;
+#endif
 #if HEGPU_NTT_FP
   const double2 fq = ta.fpq[pi];
   if (fq.x != 0.0) {
@@ -810,7 +818,11 @@ void prep_kernel(K kernel, size_t bytes) {
 // (1024-thread CTAs, no register spills): measured faster for the row
 // INTTs and the drop-limb NTTs, slower for ModUp (profiles/r01_notes.md),
 // so those two entry points dispatch to the _r8 build.
-#ifdef HEGPU_NTT_R8_VARIANT
+#if defined(HEGPU_NTT_SUFFIX)
+#define NTT_PUB_CAT_(x, s) x##s
+#define NTT_PUB_CAT(x, s) NTT_PUB_CAT_(x, s)
+#define NTT_PUB(x) NTT_PUB_CAT(x, HEGPU_NTT_SUFFIX)
+#elif defined(HEGPU_NTT_R8_VARIANT)
 #define NTT_PUB(x) x##_r8
 #else
 #define NTT_PUB(x) x##_r16
@@ -858,6 +870,8 @@ void upload_twiddles(Context& c) {
   }
   CK(cudaMalloc((void**)&c.d_twd, twd.size() * 8));
   CK(cudaMemcpy(c.d_twd, twd.data(), twd.size() * 8, cudaMemcpyHostToDevice));
+  c.fp_all = true;
+  for (int i = 0; i < np; ++i) c.fp_all = c.fp_all && fpq[2 * i] != 0.0;
   CK(cudaMalloc((void**)&c.d_fpq, fpq.size() * 8));
   CK(cudaMemcpy(c.d_fpq, fpq.data(), fpq.size() * 8, cudaMemcpyHostToDevice));
 }
@@ -978,25 +992,49 @@ void NTT_PUB(drop_last_limb)(Context& c, int B, const DropArgs& a, u64d* tmpP) {
 }
 
 #ifndef HEGPU_NTT_R8_VARIANT
-// per-entry-point choice of the thread granularity (see NTT_PUB above)
+// Per-entry-point choice of the build (thread granularity, FP64-only):
+// when every prime of the context is below 2^45 the FP64-only builds run
+// (ntt_fp16.cu: 16 words per thread, ntt_fp8.cu: 8 words per thread at two
+// 1024-thread CTAs per SM), with no integer-butterfly code in the kernels;
+// otherwise the dual-path builds (ntt.cu: 16, ntt_r8.cu: 8 words per thread).
+// HEGPU_NTT_FPV=<ntt><intt><modup><md> digits (1 = 16 words, 0 = 8 words)
+// overrides the FP64-only choice for A/B measurements.  Measured (cfg 2,
+// profiles/r02_notes.md): the 16-word FP64-only build is fastest for the row
+// transforms, ModUp and the fused ModDown + rescale; the plain drop-limb
+// kernel (rescale / ModDown alone) stays on the dual-path 8-word build,
+// whose integer epilogue fits 64 registers without spills.
+static bool fpv16(int entry, bool dflt) {
+  const char* e = getenv("HEGPU_NTT_FPV");
+  if (!e || (int)strlen(e) <= entry) return dflt;
+  return e[entry] == '1';
+}
 void launch_ntt_rows(Context& c, const u64d* src, u64d* dst, int rows, int nl, int p_limb) {
-  if (ntt_all_r8()) launch_ntt_rows_r8(c, src, dst, rows, nl, p_limb);
+  if (c.fp_all && c.P->log_n <= 13 && !fpv16(0, true)) launch_ntt_rows_fp8(c, src, dst, rows, nl, p_limb);
+  else if (c.fp_all) launch_ntt_rows_fp16(c, src, dst, rows, nl, p_limb);
+  else if (ntt_all_r8()) launch_ntt_rows_r8(c, src, dst, rows, nl, p_limb);
   else launch_ntt_rows_r16(c, src, dst, rows, nl, p_limb);
 }
 void launch_intt_rows(Context& c, const u64d* src, u64d* dst, int n_outer, int n_inner, long so, long si, long dox,
                       long di, const int* prime_of_inner) {
-  launch_intt_rows_r8(c, src, dst, n_outer, n_inner, so, si, dox, di, prime_of_inner);
+  if (c.fp_all && c.P->log_n <= 13 && !fpv16(1, true))
+    launch_intt_rows_fp8(c, src, dst, n_outer, n_inner, so, si, dox, di, prime_of_inner);
+  else if (c.fp_all) launch_intt_rows_fp16(c, src, dst, n_outer, n_inner, so, si, dox, di, prime_of_inner);
+  else launch_intt_rows_r8(c, src, dst, n_outer, n_inner, so, si, dox, di, prime_of_inner);
 }
 void ks_modup(Context& c, const u64d* src, long src_stride, int B, int l, const KeyRowMap* shifts, u64d* tmp,
               u64d* D) {
   c.ks[KS_MODUP] += B;
-  if (ntt_all_r8()) ks_modup_r8(c, src, src_stride, B, l, shifts, tmp, D);
+  if (c.fp_all && c.P->log_n <= 13 && !fpv16(2, true)) ks_modup_fp8(c, src, src_stride, B, l, shifts, tmp, D);
+  else if (c.fp_all) ks_modup_fp16(c, src, src_stride, B, l, shifts, tmp, D);
+  else if (ntt_all_r8()) ks_modup_r8(c, src, src_stride, B, l, shifts, tmp, D);
   else ks_modup_r16(c, src, src_stride, B, l, shifts, tmp, D);
 }
 void drop_last_limb(Context& c, int B, const DropArgs& a, u64d* tmpP) {
   c.ks[a.pd == c.L() ? KS_MODDOWN : KS_RESCALE] += B;
   if (a.fuse_rescale) c.ks[KS_RESCALE] += B;
-  drop_last_limb_r8(c, B, a, tmpP);
+  if (c.fp_all && a.fuse_rescale && c.P->log_n <= 13 && !fpv16(3, true)) drop_last_limb_fp8(c, B, a, tmpP);
+  else if (c.fp_all && a.fuse_rescale) drop_last_limb_fp16(c, B, a, tmpP);
+  else drop_last_limb_r8(c, B, a, tmpP);
 }
 #endif
 

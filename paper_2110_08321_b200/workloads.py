@@ -47,12 +47,18 @@ class NetConfig:
         return self.k * self.k * self.in_c
 
 
+# The benchmark prime chain: q_0 and P of 45 bits, five
+# 40-bit primes for the five rescales at Delta = 2^40.  Every prime is below
+# 2^45, so every NTT row runs on the FP64 butterflies (§5.1); q_0 leaves 4
+# bits above Delta for the logits (|logit| < 16) and P >= q_0 bounds the
+# hybrid key-switch noise.  The integer (64-bit Shoup) path stays for primes
+# up to 2^60 (the 60-bit chains of the unit tests and the CLI).
+QBITS_45 = (45, 40, 40, 40, 40, 40)
+PBITS_45 = 45
 # BASELINE.json configs[0] (and [2] = 64 of these)
-CFG0 = NetConfig("cfg0-mnist", 1, 28, 29, 5, 2, 5, (100, 10), 13,
-                 (60, 40, 40, 40, 40, 40), 60, 0.05)
+CFG0 = NetConfig("cfg0-mnist", 1, 28, 29, 5, 2, 5, (100, 10), 13, QBITS_45, PBITS_45, 0.05)
 # BASELINE.json configs[3]
-CFG3 = NetConfig("cfg3-cifar", 3, 32, 32, 5, 2, 32, (256, 10), 14,
-                 (60, 40, 40, 40, 40, 40), 60, 0.02)
+CFG3 = NetConfig("cfg3-cifar", 3, 32, 32, 5, 2, 32, (256, 10), 14, QBITS_45, PBITS_45, 0.02)
 
 
 def f32(a):

@@ -204,6 +204,7 @@ def test_merge_maps(pair):
 
 @pytest.mark.parametrize("m,n,skip", [(2, 2, True), (10, 100, True), (32, 300, True), (3, 4, False),
                                       (7, 500, True), (4, 4, True),
+                                      (2, 100, True), (2, 300, True),  # 6 / 8 folds: two hoisted fold groups
                                       (300, 200, True)])  # padding branch, 4 diagonal chunks, split CTAs
 def test_hs_matvec(pair, m, n, skip):
     ctx, ck = pair

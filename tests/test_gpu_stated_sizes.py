@@ -28,12 +28,16 @@ from paper_2110_08321_b200.workloads import CFG3, conv_pack_image, hs_sweep_case
 pytestmark = pytest.mark.gpu
 
 DELTA = 2.0 ** 40
-CFG1 = (14, [60, 40], 60)  # N = 16384, one rescale (BASELINE.json configs[1])
+# N = 16384, one rescale (BASELINE.json configs[1]): the bench's chain
+# (45-bit q_0 and P: every limb on the FP64 NTT path) and a 60-bit one (q_0
+# and P on the integer path)
+CFG1 = (14, [45, 40], 45)
+CFG1_60 = (14, [60, 40], 60)
 
 
-@pytest.fixture(scope="module")
-def cfg1():
-    log_n, qb, pb = CFG1
+@pytest.fixture(scope="module", params=[CFG1, CFG1_60], ids=["q45", "q60"])
+def cfg1(request):
+    log_n, qb, pb = request.param
     ctx = H.Context(log_n, qb, pb, seed=1)
     ck = Ckks(log_n, qb, pb, seed=1)
     assert ctx.primes == ck.primes
@@ -76,6 +80,24 @@ def test_cfg1_hs_1024_full(cfg1):
         assert np.array_equal(gotb[i], P.hs_matvec(ck, cts[i], 2, A, keys=keys)), i
     for i in range(B):
         assert np.abs(ck.decrypt_decode(gotb[i], 1, DELTA)[:1024] - A @ xs[i]).max() < 1e-4
+
+
+def test_cfg1_hs_64x4096_grouped_folds(cfg1):
+    """m = 64, n = 4096: 7 fold doublings, run as two hoisted fold groups
+    (4 + 3 doublings: 15 + 7 key inner products instead of 127), limbs ==
+    oracle, metering = the reference's 64 + 7 rotations"""
+    ctx, ck = cfg1
+    A, x = hs_sweep_case(64, 4096)
+    v = ck.encrypt(ck.encode(x, DELTA, 2), 2, 3)
+    plan = ctx.hs_plan(A, 2)
+    assert (plan.m_eff, plan.folds) == (64, 7)
+    assert P.fold_groups(7) == [4, 3]
+    ctx.gen_rotation_keys(plan.rotations())
+    ctx.reset_meter()
+    got = ctx.hs_matvec(plan, ctx.ct(1, 2, v, DELTA), ctx.ct(1, 1)).download()
+    assert ctx.total() == (0, 70, 64, 0, 70)  # predict_hs(64, 4096, 16384) = 70 (test_matvec.cpp:125-131)
+    assert np.array_equal(got, P.hs_matvec(ck, v, 2, A))
+    assert np.abs(ck.decrypt_decode(got, 1, DELTA)[:64] - A @ x).max() < 1e-4
 
 
 def test_cfg1_hs_4096_partial_range(cfg1):
@@ -157,8 +179,8 @@ def test_cfg4_conv_layer_at_size(c_in, k, c_out):
     (the bench's chain); conv_packed_forward + rescale limbs == oracle, HOPs
     k^2 c_in c_out / (k^2 c_in - 1) c_out / c_out, decrypted maps vs the
     FP64 conv"""
-    ctx = H.Context(14, [60, 40], 60, seed=4)
-    ck = Ckks(14, [60, 40], 60, seed=4)
+    ctx = H.Context(14, [45, 40], 45, seed=4)
+    ck = Ckks(14, [45, 40], 45, seed=4)
     rng = np.random.default_rng(40 + c_in * k + c_out)
     img = rng.uniform(0, 1, (c_in, 32, 32))
     W = rng.normal(0, 0.05, (c_out, c_in, k, k))
