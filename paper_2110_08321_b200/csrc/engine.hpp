@@ -269,6 +269,12 @@ void launch_tensor_square(Context& c, const u64d* a, u64d* d01, u64d* d2, int co
 // pair, 4-tap block and lane the A fragment (uint4) of the byte planes of
 // W * 2^(8i) mod q
 bool conv_imma_supported(Context& c);
+// the same MAC on tcgen05 (conv_tc.cu): positions as MMA rows, weight byte
+// planes as accumulator columns; wb from conv_tc_weights
+bool conv_tc_supported(Context& c, int ntaps, int c_out, int l);
+std::vector<uint8_t> conv_tc_weights(Context& c, int ntaps, int c_out, int l, const std::vector<u64>& ws);
+void launch_conv_tc(Context& c, const u64d* taps, int B, int ntaps, int l, const uint8_t* wb, int c_out,
+                    const u64d* bias, u64d* out);
 // limb t packs 3 maps x 5 weight-byte planes per MMA row tile (q_t < 2^40)
 bool conv_imma_triples(Context& c, int t, int c_out);
 void launch_conv_imma(Context& c, const u64d* taps, int B, int ntaps, int l, const uint32_t* wa, int cps, int kbn,

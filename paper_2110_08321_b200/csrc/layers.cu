@@ -83,6 +83,11 @@ ConvLayer::ConvLayer(Context& c, int nt, int co_n, const double* weights, const 
           }
         }
     }
+    if (conv_tc_supported(c, ntaps, c_out, level)) {
+      const std::vector<uint8_t> img = conv_tc_weights(c, ntaps, c_out, level, ws);
+      CK(cudaMalloc((void**)&wtc, img.size()));
+      CK(cudaMemcpy(wtc, img.data(), img.size(), cudaMemcpyHostToDevice));
+    }
     // limbs of primes < 2^40 (5-byte weight digits) pack rows as 3 maps x 5
     // planes (row 15 unused; conv_imma.cu MPT = 3), the others 2 maps x 8
     auto byte_at = [&](int li, int row, int col, int cp, int kb) -> uint32_t {
@@ -179,6 +184,7 @@ ConvLayer::~ConvLayer() {
   cudaFree(w);
   cudaFree(bias);
   cudaFree(wa);
+  cudaFree(wtc);
 }
 
 #ifndef HEGPU_CONV_IMMA
@@ -188,6 +194,7 @@ ConvLayer::~ConvLayer() {
 void ConvLayer::mac(Context& c, const CtBatch& taps, CtBatch& prod) {
   const int B = taps.count / ntaps;
   if (merged) launch_conv_pt(c, taps.d, taps.count / cts_per_image(), ntaps, regions, level, pw, pbias, prod.d);
+  else if (wtc) launch_conv_tc(c, taps.d, B, ntaps, level, wtc, c_out, bias, prod.d);
   else if (HEGPU_CONV_IMMA && conv_imma_supported(c))
     launch_conv_imma(c, taps.d, B, ntaps, level, wa, cps, kbn, c_out, bias, prod.d);
   else
@@ -201,6 +208,7 @@ void ConvLayer::mac_compact(Context& c, const uint8_t* taps, int B, double tap_s
   u64d* full = c.alloc((size_t)B * cts_per_image() * 2 * level * c.N());
   launch_expand_compact(c, taps, B * cts_per_image(), level, full);
   if (merged) launch_conv_pt(c, full, B, ntaps, regions, level, pw, pbias, prod.d);
+  else if (wtc) launch_conv_tc(c, full, B, ntaps, level, wtc, c_out, bias, prod.d);
   else if (HEGPU_CONV_IMMA && conv_imma_supported(c))
     launch_conv_imma(c, full, B, ntaps, level, wa, cps, kbn, c_out, bias, prod.d);
   else

@@ -20,6 +20,7 @@ struct ConvLayer {
   u64d* w = nullptr;     // [c_out][ntaps][level] Montgomery scalars
   u64d* bias = nullptr;  // [c_out][level][N] Montgomery, slot order
   uint32_t* wa = nullptr;  // tensor-core A fragments (launch_conv_imma)
+  uint8_t* wtc = nullptr;  // tcgen05 weight operand images (launch_conv_tc), null if unsupported
   int cps = 0, kbn = 0;    // map pairs, 4-tap blocks
   ConvLayer(Context& c, int ntaps, int c_out, const double* weights, const double* bias_vals, int w_used,
             int level, double tap_scale);
