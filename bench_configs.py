@@ -93,8 +93,13 @@ def config1(args):
                     tally = tt.cpu().numpy()
                     tally[1] -= (world - 1) * B * plan.folds  # the folds run on every rank,
                     tally[4] -= (world - 1) * B * plan.folds  # the reference meters them once
+                # correctness of every sweep point: the first image's decrypted
+                # slots 0..m-1 against the cleartext A x (outside the timed runs)
+                got = ctx.decode(ctx.decrypt(out.download()[: 2 * ctx.N], 1), 1, DELTA)[:m]
+                err = float(np.abs(got - A @ x).max())
+                assert err < 1e-4, f"config 1 m={m} n={n}: decrypted A x off by {err}"
                 kms = kbytes = 0.0
-                for kern in ("k_hs_diag", "k_hs_imma"):
+                for kern in ("k_hs_diag", "k_hs_imma", "k_hs_narrow"):
                     ctx.kernel_timer(kern)
                     run()
                     a, _, b_ = ctx.kernel_timer_read()
@@ -110,6 +115,7 @@ def config1(args):
                         "rotations_per_matvec": rot // B, "mul_pc_per_matvec": int(tally[2]) // B,
                         "m_eff": plan.m_eff, "folds": plan.folds,
                         "hs_kernel_ms": kms, "hs_kernel_gbs": kbytes / (kms / 1e3) / 1e9 if kms else None,
+                        "max_abs_err_vs_Ax": err,
                         "setup_s": setup_s}), flush=True)
             del plan
     if world > 1:
