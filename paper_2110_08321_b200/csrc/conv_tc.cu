@@ -31,7 +31,7 @@ namespace hegpu {
 namespace {
 
 constexpr int kTcM = 128;       // positions per tile (MMA M)
-constexpr int kTcThreads = 256;  // 8 warps: all stage, warps w and w + 4 share TMEM lanes 32 (w % 4)
+constexpr int kTcThreads = 288;  // 9 warps: 4 producers, 1 MMA issuer, 4 epilogue
 constexpr int kTcTiles = 16;     // position tiles per CTA (HEGPU_TC_TILES)
 constexpr int kTcBufs = 3;       // A (tap) tile buffers in flight (HEGPU_TC_BUFS, 2..4)
 
@@ -107,9 +107,15 @@ struct TcArgs {
   int nbufs;          // A tile buffers
 };
 
-__global__ void __launch_bounds__(kTcThreads, 1) k_conv_tc(TcArgs a) {
+// Warp roles (9 warps): 0-3 producers (thread j stages position j of a
+// tile: its tap words by cp.async into the core-matrix rows), 4 the MMA
+// issuer (one lane), 5-8 the epilogue (warp w reads TMEM lanes 32 (w % 4)).
+// mbarriers: full[buf] (128 producer arrivals, after each producer's
+// cp.async.wait + proxy fence), empty[buf] and tfull[tb] (tcgen05.commit),
+// tempty[tb] (128 epilogue arrivals) -- no CTA-wide barrier in the loop.
+__global__ void __launch_bounds__(kTcThreads, 2) k_conv_tc(TcArgs a) {
   extern __shared__ __align__(128) uint8_t tc_smem[];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t bars[2 * 4 + 4];  // full[4], empty[4], tfull[2], tempty[2]
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int N = a.N, l = a.l, KB = a.kb;
@@ -117,101 +123,113 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv_tc(TcArgs a) {
   const int t = row % l, bp = row / l, p = bp & 1, b = bp >> 1;
   const int npad = a.npad[t], PL = a.planes[t];
   const int ntile_all = N / kTcM;
-  const int tile0 = chunk * ntile_all / a.chunks, tile1 = (chunk + 1) * ntile_all / a.chunks;
-  // shared memory: A[kTcBufs] (kTcM x KB bytes each), then B (npad x KB bytes)
+  const int tile0 = chunk * ntile_all / a.chunks, tile1 = (chunk + 1) * ntile_all / a.chunks, nt = tile1 - tile0;
+  const int NBF = a.nbufs;
+  // shared memory: A[NBF] (kTcM x KB bytes each), then B (npad x KB bytes)
   uint8_t* sA = tc_smem;
-  uint8_t* sB = tc_smem + a.nbufs * (size_t)kTcM * KB;
+  uint8_t* sB = tc_smem + NBF * (size_t)kTcM * KB;
   const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
-  const uint32_t bar0 = smem_u32(&bars[0]);
-  if (warp == 0) {
+  const uint32_t full0 = smem_u32(&bars[0]), empty0 = full0 + 32, tfull0 = full0 + 64, tempty0 = full0 + 80;
+  const int npairs = KB / 16;  // tap pairs (16 K bytes each), incl. zero padding
+  if (warp == 4) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_slot)),
                  "r"(a.tcols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
   }
   if (tid == 0) {
-    mbar_init(bar0, 1);
-    mbar_init(bar0 + 8, 1);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(full0 + 8 * i, kTcM);
+      mbar_init(empty0 + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(tfull0 + 8 * i, 1);
+      mbar_init(tempty0 + 8 * i, kTcM);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   // the weight operand of limb t (K-major core-matrix image, npad x KB bytes)
+  // and the zero padding (taps >= ntaps) of every A buffer, written once
   {
     const uint4* src = a.wb + (size_t)t * (KB * 256 / 16);  // images are laid out at npad = 256 stride
     uint4* dst = reinterpret_cast<uint4*>(sB);
     for (int i = tid; i < npad * KB / 16; i += kTcThreads) dst[i] = __ldg(src + i);
+    for (int bf = 0; bf < NBF; ++bf)
+      for (int idx = tid; idx < npairs * kTcM; idx += kTcThreads) {
+        const int sp = idx / kTcM, j = idx % kTcM, s = 2 * sp;
+        uint64_t* r = reinterpret_cast<uint64_t*>(sA + (size_t)bf * kTcM * KB +
+                                                  ((size_t)(sp * 16 + (j >> 3)) * 8 + (j & 7)) * 16);
+        if (s >= a.ntaps) r[0] = 0;
+        if (s + 1 >= a.ntaps) r[1] = 0;
+      }
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
-  const uint32_t idesc = idesc_u8(kTcM, npad);
-  // A core matrices: [K chunk c][position group g (16)][8 rows][16 B]
-  const uint32_t a_lbo = 16 * 128, a_sbo = 128;
-  // B core matrices: [K chunk c][column group (npad / 8)][8 rows][16 B]
-  const uint32_t b_lbo = (uint32_t)(npad / 8) * 128, b_sbo = 128;
   const size_t ct_words = (size_t)2 * l * N;
-  const u64d* tbase = a.taps + (size_t)b * a.ntaps * ct_words + (size_t)p * l * N + (size_t)t * N;
-  const int npairs = KB / 16;  // tap pairs (16 K bytes each), incl. zero padding
-  const DevPrime pr = a.pt.p[t];
-  const int lane_grp = warp & 3;  // TMEM lanes 32 lane_grp .. (this warp's positions)
-  const int pos = 32 * lane_grp + lane;
-  // tile staging: cp.async copies of the tap words straight into the
-  // core-matrix rows (no register round trip), three A buffers in flight;
-  // the zero padding (taps >= ntaps) is written once per buffer
-  const int NBF = a.nbufs;
-  auto a_buf = [&](int k) { return sA + (size_t)(k % NBF) * kTcM * KB; };
-  for (int bf = 0; bf < NBF; ++bf)
-    for (int idx = tid; idx < npairs * kTcM; idx += kTcThreads) {
-      const int sp = idx / kTcM, j = idx % kTcM, s = 2 * sp;
-      uint64_t* row = reinterpret_cast<uint64_t*>(a_buf(bf) + ((size_t)(sp * 16 + (j >> 3)) * 8 + (j & 7)) * 16);
-      if (s >= a.ntaps) row[0] = 0;
-      if (s + 1 >= a.ntaps) row[1] = 0;
-    }
-  auto issue = [&](int it) {
-    if (it < tile1) {
-      uint8_t* A = a_buf(it - tile0);
-      const int k0 = it * kTcM;
-      for (int idx = tid; idx < npairs * kTcM; idx += kTcThreads) {
-        const int sp = idx / kTcM, j = idx % kTcM, s = 2 * sp;
-        const uint32_t dst = smem_u32(A + ((size_t)(sp * 16 + (j >> 3)) * 8 + (j & 7)) * 16);
-        if (s < a.ntaps) cp_async8(dst, tbase + (size_t)s * ct_words + k0 + j);
-        if (s + 1 < a.ntaps) cp_async8(dst + 8, tbase + (size_t)(s + 1) * ct_words + k0 + j);
+  if (warp < 4) {
+    // ---- producers: position j of every tile
+    const int j = tid;
+    const u64d* src0 = a.taps + (size_t)b * a.ntaps * ct_words + (size_t)p * l * N + (size_t)t * N + j;
+    const uint32_t roff = (uint32_t)(((j >> 3) * 8 + (j & 7)) * 16);
+    for (int k = 0; k <= nt; ++k) {
+      if (k < nt) {
+        const int bf = k % NBF;
+        mbar_wait(empty0 + 8 * bf, (uint32_t)(((k / NBF) & 1) ^ 1));  // passes at once on a fresh barrier
+        const uint32_t dst0 = sA_u + (uint32_t)(bf * kTcM * KB) + roff;
+        const u64d* src = src0 + (size_t)(tile0 + k) * kTcM;
+        for (int sp = 0; sp < npairs; ++sp) {
+          const int s = 2 * sp;
+          const uint32_t d = dst0 + (uint32_t)sp * 16 * 128;
+          if (s < a.ntaps) cp_async8(d, src + (size_t)s * ct_words);
+          if (s + 1 < a.ntaps) cp_async8(d + 8, src + (size_t)(s + 1) * ct_words);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+      }
+      if (k >= 1) {
+        // tile k - 1 landed (this thread's rows): publish it to the MMA issuer
+        if (k < nt) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(full0 + 8 * ((k - 1) % NBF)) : "memory");
       }
     }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-  for (int d = 0; d < NBF - 1; ++d) issue(tile0 + d);
-  for (int it = tile0; it <= tile1; ++it) {
-    const int k = it - tile0;
-    if (it < tile1) {
-      // this thread's rows of tile it landed (NBF - 2 later groups may pend)
-      if (NBF == 2) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      else if (NBF == 3) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-      else asm volatile("cp.async.wait_group 2;\n" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    if (it < tile1 && tid == 0) {
-      // ---- MMA issue (one thread): K in steps of 32 bytes = 2 core-matrix chunks
-      const uint32_t a0 = sA_u + (uint32_t)((k % NBF) * kTcM * KB), d = tmem + (uint32_t)((k & 1) * a.nb);
-      for (int ks = 0; ks < KB / 32; ++ks) {
-        const uint64_t ad = umma_desc(a0 + (uint32_t)ks * 2 * a_lbo, a_lbo, a_sbo);
-        const uint64_t bd = umma_desc(sB_u + (uint32_t)ks * 2 * b_lbo, b_lbo, b_sbo);
-        tc_mma_u8(d, ad, bd, idesc, ks > 0);
+  } else if (warp == 4) {
+    // ---- MMA issuer (one lane): K in steps of 32 bytes = 2 core-matrix chunks
+    if (lane == 0) {
+      const uint32_t idesc = idesc_u8(kTcM, npad);
+      const uint32_t a_lbo = 16 * 128, a_sbo = 128;                       // A: [K chunk][16 position groups][8][16 B]
+      const uint32_t b_lbo = (uint32_t)(npad / 8) * 128, b_sbo = 128;     // B: [K chunk][npad / 8 groups][8][16 B]
+      for (int k = 0; k < nt; ++k) {
+        const int bf = k % NBF, tb = k & 1;
+        mbar_wait(full0 + 8 * bf, (uint32_t)((k / NBF) & 1));
+        mbar_wait(tempty0 + 8 * tb, (uint32_t)(((k >> 1) & 1) ^ 1));
+        tc_fence_after();
+        const uint32_t a0 = sA_u + (uint32_t)(bf * kTcM * KB), d = tmem + (uint32_t)(tb * a.nb);
+        for (int ks = 0; ks < KB / 32; ++ks) {
+          const uint64_t ad = umma_desc(a0 + (uint32_t)ks * 2 * a_lbo, a_lbo, a_sbo);
+          const uint64_t bd = umma_desc(sB_u + (uint32_t)ks * 2 * b_lbo, b_lbo, b_sbo);
+          tc_mma_u8(d, ad, bd, idesc, ks > 0);
+        }
+        tc_commit(empty0 + 8 * bf);  // the A buffer may be refilled
+        tc_commit(tfull0 + 8 * tb);  // the accumulator is ready
       }
-      tc_commit(bar0 + 8 * (k & 1));
     }
-    if (k >= 1) {
-      // ---- epilogue of tile it - 1: position pos, maps co = warp / 4 (mod 2)
-      const int kp = k - 1, buf = kp & 1;
-      mbar_wait(bar0 + 8 * buf, (uint32_t)((kp >> 1) & 1));
+    __syncwarp();
+  } else {
+    // ---- epilogue: position pos of each tile, every map
+    const int lane_grp = warp & 3;
+    const int pos = 32 * lane_grp + lane;
+    const DevPrime pr = a.pt.p[t];
+    for (int k = 0; k < nt; ++k) {
+      const int tb = k & 1;
+      mbar_wait(tfull0 + 8 * tb, (uint32_t)((k >> 1) & 1));
       tc_fence_after();
-      const int kpos = (it - 1) * kTcM + pos;
-      const uint32_t lanebase = tmem + ((uint32_t)(32 * lane_grp) << 16) + (uint32_t)(buf * a.nb);
-      for (int co = warp >> 2; co < a.c_out; co += 2) {
+      const int kpos = (tile0 + k) * kTcM + pos;
+      const uint32_t lanebase = tmem + ((uint32_t)(32 * lane_grp) << 16) + (uint32_t)(tb * a.nb);
+      for (int co = 0; co < a.c_out; ++co) {
         uint32_t r[8];
         tc_ld8(lanebase + (uint32_t)(co * PL), r);
         u64d lo = (p == 0 && a.bias) ? __ldg(a.bias + ((size_t)co * l + t) * N + kpos) : 0ull, hi = 0;
@@ -226,14 +244,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv_tc(TcArgs a) {
             mont_reduce128(lo, hi, pr.q, pr.qneg_inv);
       }
       tc_fence_before();
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tempty0 + 8 * tb) : "memory");
     }
-    // refill: buffer (k + NBF - 1) % NBF held tile it - 1, whose MMA the
-    // epilogue above has waited for
-    issue(it + NBF - 1);
   }
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (warp == 4) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(a.tcols) : "memory");
   }

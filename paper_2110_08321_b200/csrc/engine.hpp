@@ -313,6 +313,16 @@ struct HsImmaChunk {
   u64d* wt;
 };
 int hs_imma_chunk_span(int l);
+// the same accumulation on tcgen05 (hs_tc.cu): per chunk of kept diagonals
+// with r in [r_lo, r_hi] (span <= hs_tc_chunk_span), A tables `at` built by
+// launch_hs_tc_tiles (hs_tc_table_bytes); ce [np][8] = 2^(8e) R mod q, pR[t] = P R mod q_t
+bool hs_tc_enabled();
+int hs_tc_chunk_span(int l);
+size_t hs_tc_table_bytes(Context& c, int l, int span);
+void launch_hs_tc_tiles(Context& c, int l, const struct HsDiagTable& t, const u64d* pR, const int* rdiag, int r_lo,
+                        int r_hi, uint8_t* at);
+void launch_hs_tc(Context& c, const u64d* v, int B, int l, const u64d* D, int r_lo, int r_hi, const uint8_t* at,
+                  const u64d* ce, int accumulate, u64d* acc, int keyed, int ndiag);
 bool hs_imma_supported(Context& c, int l);
 size_t hs_imma_tile_words(Context& c, int l, const HsImmaChunk& ch);
 // rdiag[r] = kept diagonal index of right rotation r (or -1); pmod[t] = P mod q_t

@@ -328,6 +328,12 @@ void HsPlan::release() {
   cudaFree(fkeys);
   for (HsImmaChunk& ch : imma) cudaFree(ch.wt);
   imma.clear();
+  for (TcChunk& ch : tc) cudaFree(ch.at);
+  tc.clear();
+  cudaFree(tc_ce);
+  cudaFree(tc_pR);
+  tc_ce = tc_pR = nullptr;
+  tc_built = false;
   cudaFree(imma_ec);
   cudaFree(imma_pmod);
   cudaFree(d_rdiag);
@@ -513,10 +519,70 @@ void HsPlan::ensure_imma(Context& c) {
   imma_built = true;
 }
 
+// the tcgen05 A tables: chunks of kept diagonals whose r span fits the
+// window ring (hs_tc_chunk_span), balanced like the mma.sync chunks
+void HsPlan::ensure_tc(Context& c) {
+  if (tc_built) return;
+  ensure_imma(c);  // rdiag, pmod
+  const int l = level, N = c.N(), np = c.P->np();
+  std::vector<u64> ce((size_t)np * 8);
+  for (int pi = 0; pi < np; ++pi) {
+    const u64 q = c.P->q(pi);
+    u128 w = ((u128)1 << 64) % q;  // R mod q
+    for (int e = 0; e < 8; ++e) {
+      ce[(size_t)pi * 8 + e] = (u64)w;
+      w = (w << 8) % q;
+    }
+  }
+  std::vector<u64> pr(l);
+  for (int t = 0; t < l; ++t) {
+    const u64 q = c.P->q(t);
+    pr[t] = (u64)(((u128)(c.P->q(c.L()) % q) << 64) % q);  // P R mod q_t
+  }
+  CK(cudaMalloc((void**)&tc_ce, ce.size() * 8));
+  CK(cudaMemcpy(tc_ce, ce.data(), ce.size() * 8, cudaMemcpyHostToDevice));
+  CK(cudaMalloc((void**)&tc_pR, pr.size() * 8));
+  CK(cudaMemcpy(tc_pR, pr.data(), pr.size() * 8, cudaMemcpyHostToDevice));
+  const int smax = hs_tc_chunk_span(l), rtot = (int)(diag.back().right - diag[0].right) + 1;
+  const int nch = (rtot + smax - 1) / smax, span = (rtot + nch - 1) / nch;
+  const int first_keyed = diag[0].shift == 0 ? 1 : 0;
+  HsDiagTable tab{(int)diag.size(), 0, d_r, fkeys, (size_t)l * 2 * (l + 1) * N, first_keyed, 1, masks, 0, nullptr};
+  size_t i = 0;
+  while (i < diag.size()) {
+    TcChunk ch{};
+    ch.r_lo = (int)diag[i].right;
+    ch.r_hi = ch.r_lo;
+    while (i < diag.size() && diag[i].right - ch.r_lo < span) {
+      ch.r_hi = (int)diag[i].right;
+      ch.keyed += diag[i].shift != 0;
+      ++ch.ndiag;
+      ++i;
+    }
+    CK(cudaMalloc((void**)&ch.at, hs_tc_table_bytes(c, l, ch.r_hi - ch.r_lo + 1)));
+    launch_hs_tc_tiles(c, l, tab, tc_pR, d_rdiag, ch.r_lo, ch.r_hi, ch.at);
+    tc.push_back(ch);
+  }
+  CK(cudaStreamSynchronize(c.stream));
+  tc_built = true;
+}
+
 void HsPlan::accumulate(Context& c, const CtBatch& v, int i_lo, int i_hi, u64d* acc, u64d* cacc) {
   const int B = v.count, l = level, N = c.N();
   ensure_keys(c);
   for (int i = i_lo; i < i_hi; ++i) c.ks[KS_INNER] += diag[i].shift != 0 ? B : 0;
+  if (use_imma(c, B, i_lo, i_hi) && hs_tc_enabled() && l <= 6) {
+    ensure_tc(c);
+    u64d* tmp = c.alloc((size_t)B * l * N);
+    u64d* D = c.alloc((size_t)B * l * (l + 1) * N);
+    ks_modup(c, v.d + (size_t)l * N, (long)v.stride(), B, l, nullptr, tmp, D);
+    for (size_t ci = 0; ci < tc.size(); ++ci)
+      launch_hs_tc(c, v.d, B, l, D, tc[ci].r_lo, tc[ci].r_hi, tc[ci].at, tc_ce, ci > 0, acc, tc[ci].keyed,
+                   tc[ci].ndiag);
+    launch_hs_cacc(c, v.d, masks, B, l, diag[0].right == 0 ? 1 : 0, cacc);
+    c.free(tmp);
+    c.free(D);
+    return;
+  }
   if (use_imma(c, B, i_lo, i_hi)) {
     ensure_imma(c);
     u64d* tmp = c.alloc((size_t)B * l * N);

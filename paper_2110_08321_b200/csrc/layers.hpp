@@ -77,6 +77,16 @@ struct HsPlan {
   int* d_rdiag = nullptr;     // [S] right rotation -> kept diagonal (or -1)
   bool imma_built = false;
   void ensure_imma(Context& c);
+  // the tcgen05 path (hs_tc.cu): chunks (r_lo, r_hi, keyed, ndiag) with their A tables
+  struct TcChunk {
+    int r_lo, r_hi, keyed, ndiag;
+    uint8_t* at;
+  };
+  std::vector<TcChunk> tc;
+  u64d* tc_ce = nullptr;  // [np][8] 2^(8e) R mod q
+  u64d* tc_pR = nullptr;  // [level] P R mod q_t
+  bool tc_built = false;
+  void ensure_tc(Context& c);
   bool use_imma(Context& c, int B, int i_lo, int i_hi) const;
   // the log-depth fold (matvec.cpp:101-103) as hoisted rotation sums: the
   // `folds` doublings in groups of <= kMaxFoldGroup (fold_groups), each a
