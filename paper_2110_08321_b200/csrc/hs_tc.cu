@@ -23,8 +23,9 @@
 // a stage ring (mbarrier complete_tx); B (the window bytes, byte-plane
 // transposed) is staged from the ModUp digits D and c0 into a shared-memory
 // ring of 16-byte K chunks in core-matrix layout, each element once per
-// strip of consecutive tiles.  Warp roles: 0-3 stage the window and run the
-// epilogue (TMEM lanes 0-127), 4 issues the MMAs (one lane), 5 streams A.
+// strip of consecutive tiles.  Warp roles: 0-7 stage the window and run the
+// epilogue (warp w: TMEM lanes 32 (w % 4), images 8 (w / 4) ..), 8 issues
+// the MMAs (one lane), 9 streams A.
 // Two accumulator buffers: MMA(tile u) overlaps epilogue(u - 1) and the
 // staging of tile u + 1.  Limbs are the same residues as hs_imma.cu / the
 // integer kernel / the oracle.
@@ -45,7 +46,7 @@ constexpr int kN = kNI * 8;      // MMA N (columns (img, d))
 constexpr int kNG = kN / 8;      // column groups of 8 (core matrices along N)
 constexpr int kAStages = 6;      // A K-step stages of 4 KB
 constexpr int kAStep = 4096;     // one K step of A: [2 chunks][16 row groups][8][16 B]
-constexpr int kThreads = 192;    // 6 warps
+constexpr int kThreads = 320;    // 10 warps: 0-7 window staging + epilogue, 8 MMA issuer, 9 A producer
 constexpr int kRCMax = 48;       // ring chunks (16 K bytes x kN columns = 2 KB each)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a) {
   const uint32_t ring_u = smem_u32(ring), ast_u = smem_u32(astage);
   const uint32_t afull0 = smem_u32(&bars[0]), aempty0 = afull0 + 8 * kAStages;
   const uint32_t bfull0 = aempty0 + 8 * kAStages, done0 = bfull0 + 16, tempty0 = bfull0 + 32;
-  if (warp == 4) {
+  if (warp == 8) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_slot)),
                  "r"(2 * kN)
                  : "memory");
@@ -151,9 +152,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a) {
       mbar_init(aempty0 + 8 * i, 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(bfull0 + 8 * i, 128);
+      mbar_init(bfull0 + 8 * i, 256);
       mbar_init(done0 + 8 * i, 1);
-      mbar_init(tempty0 + 8 * i, 128);
+      mbar_init(tempty0 + 8 * i, 256);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -167,10 +168,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a) {
     half = (int)((g / tph) % 2);
     kh0 = (int)(g % tph) * kTP;
   };
-  if (warp < 4) {
-    // ---- window staging + epilogue
+  if (warp < 8) {
+    // ---- window staging (all 8 warps) + epilogue: warp w reads TMEM lanes
+    // 32 (w % 4) (rows m) for images 8 (w / 4) ..
     int cur_seg = -1, c_staged = 0;
-    const int m = tid, kl = m >> 4, p = (m >> 3) & 1, e = m & 7;
+    const int m = 32 * (warp & 3) + lane, kl = m >> 4, p = (m >> 3) & 1, e = m & 7;
+    const int img0 = 8 * (warp >> 2);
     for (int u = 0; u <= nt; ++u) {
       if (u < nt) {
         int t, half, kh0;
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a) {
         const int ng4 = 4 * (c_hi - cfrom), items = ng4 * kNI;
         const u64d* Dt = a.D + (size_t)t * N + (size_t)half * S;
         const u64d* ct = a.v + (size_t)t * N + (size_t)half * S;
-        for (int it = tid; it < items; it += 128) {
+        for (int it = tid; it < items; it += 256) {
           const int img = it / ng4, g4 = 4 * cfrom + it % ng4, b = ig * kNI + img;
           const int k0 = 4 * g4;
           u64d w[4];
@@ -231,23 +234,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a) {
         const int pi = t == LV ? a.L : t;
         const DevPrime pr = a.pt.p[pi];
         const u64d cst = __ldg(a.ce + (size_t)pi * 8 + e);
-        const uint32_t lb = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(tb * kN);
+        const uint32_t lb = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(tb * kN);
         const int k = half * S + kh0 + kl;
 #pragma unroll 1
-        for (int i0 = 0; i0 < kNI; i0 += 4) {
+        for (int i0 = img0; i0 < img0 + 8; i0 += 4) {
           uint32_t r[4][8];
 #pragma unroll
           for (int q = 0; q < 4; ++q) tc_ld8_nowait(lb + (uint32_t)((i0 + q) * 8), r[q]);
           tc_wait_ld();
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            u64d lo = 0, hi = 0;
-#pragma unroll
-            for (int d = 0; d < 8; ++d) {
-              const u64d cv = (u64d)r[q][d];
-              const u64d l_add = cv << (8 * d), h_add = d ? cv >> (64 - 8 * d) : 0ull;
-              asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(l_add), "l"(h_add));
-            }
+            // T = sum_d C_d 2^(8d): two 57-bit partial sums, then one 128-bit add
+            const u64d s0 = (u64d)r[q][0] + ((u64d)r[q][1] << 8) + ((u64d)r[q][2] << 16) + ((u64d)r[q][3] << 24);
+            const u64d s1 = (u64d)r[q][4] + ((u64d)r[q][5] << 8) + ((u64d)r[q][6] << 16) + ((u64d)r[q][7] << 24);
+            u64d lo = s0, hi = s1 >> 32;
+            asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, 0;" : "+l"(lo), "+l"(hi) : "l"(s1 << 32));
             u64d vv = mont_mul(mont_reduce128(lo, hi, pr.q, pr.qneg_inv), cst, pr.q, pr.qneg_inv);
             vv = add_mod_d(vv, __shfl_xor_sync(0xffffffffu, vv, 1), pr.q);
             vv = add_mod_d(vv, __shfl_xor_sync(0xffffffffu, vv, 2), pr.q);
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a) {
         mbar_arrive(tempty0 + 8 * tb);
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == 8) {
     // ---- MMA issuer
     if (lane == 0) {
       const uint32_t idesc = idesc_u8(128, kN);
@@ -311,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a) {
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == 8) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * kN) : "memory");
   }
