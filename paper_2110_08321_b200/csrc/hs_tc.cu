@@ -120,6 +120,7 @@ struct HtArgs {
   const u64d* ce;      // [np][8]: 2^(8e) R mod q (Montgomery form of 2^(8e))
   u64d* acc;           // [B][2][l+1][N]
   int B, L, N, l, nks, r_lo, r_hi, rc, strips, nig, accumulate;
+  int dbg;  // HEGPU_HT_DBG bits (timing probes only, wrong limbs): 1 no epilogue math, 2 no A copies, 4 no staging
 };
 
 template <int J>
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a) {
         const int ng4 = 4 * (c_hi - cfrom), items = ng4 * kNI;
         const u64d* Dt = a.D + (size_t)t * N + (size_t)half * S;
         const u64d* ct = a.v + (size_t)t * N + (size_t)half * S;
-        for (int it = tid; it < items; it += 256) {
+        for (int it = tid; it < ((a.dbg & 4) ? 0 : items); it += 256) {
           const int img = it / ng4, g4 = 4 * cfrom + it % ng4, b = ig * kNI + img;
           const int k0 = 4 * g4;
           u64d w[4];
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a) {
         const uint32_t lb = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(tb * kN);
         const int k = half * S + kh0 + kl;
 #pragma unroll 1
-        for (int i0 = img0; i0 < img0 + 8; i0 += 4) {
+        for (int i0 = img0; i0 < ((a.dbg & 1) ? img0 : img0 + 8); i0 += 4) {
           uint32_t r[4][8];
 #pragma unroll
           for (int q = 0; q < 4; ++q) tc_ld8_nowait(lb + (uint32_t)((i0 + q) * 8), r[q]);
@@ -303,8 +304,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a) {
         for (int ks = 0; ks < NKS; ++ks, ++cnt) {
           const int st = cnt % kAStages;
           mbar_wait(aempty0 + 8 * st, (uint32_t)(((cnt / kAStages) & 1) ^ 1));
-          mbar_expect_tx(afull0 + 8 * st, kAStep);
-          bulk_g2s(ast_u + (uint32_t)(st * kAStep), src + (size_t)ks * kAStep, kAStep, afull0 + 8 * st);
+          if (a.dbg & 2) {
+            mbar_arrive(afull0 + 8 * st);
+          } else {
+            mbar_expect_tx(afull0 + 8 * st, kAStep);
+            bulk_g2s(ast_u + (uint32_t)(st * kAStep), src + (size_t)ks * kAStep, kAStep, afull0 + 8 * st);
+          }
         }
       }
     }
@@ -420,6 +425,8 @@ void launch_hs_tc(Context& c, const u64d* v, int B, int l, const u64d* D, int r_
   a.r_hi = r_hi;
   a.accumulate = accumulate;
   a.nig = (B + kNI - 1) / kNI;
+  const char* dbg = getenv("HEGPU_HT_DBG");
+  a.dbg = dbg ? atoi(dbg) : 0;
   int rc = ((span + kTP) * J + 32 + 15) / 16 + 2 + (kTP * J + 15) / 16 + 1 + 2;
   rc = (rc + 1) / 2 * 2;
   if (rc > kRCMax) fail(HEGPU_ERR_ARG, "hs_tc: chunk span exceeds the window ring");
