@@ -29,6 +29,9 @@
 // Two accumulator buffers: MMA(tile u) overlaps epilogue(u - 1) and the
 // staging of tile u + 1.  Limbs are the same residues as hs_imma.cu / the
 // integer kernel / the oracle.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
@@ -80,6 +83,14 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                "l"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
+// tensor-map TMA: one 4 KB box (256 bytes x 16 rows) of the A table
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_mma_u8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -124,7 +135,7 @@ struct HtArgs {
 };
 
 template <int J>
-__global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a, const __grid_constant__ CUtensorMap amap) {
   constexpr int LV = J - 1;
   extern __shared__ __align__(128) uint8_t ht_smem[];
   __shared__ __align__(8) uint64_t bars[2 * kAStages + 8];
@@ -308,7 +319,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a) {
             mbar_arrive(afull0 + 8 * st);
           } else {
             mbar_expect_tx(afull0 + 8 * st, kAStep);
-            bulk_g2s(ast_u + (uint32_t)(st * kAStep), src + (size_t)ks * kAStep, kAStep, afull0 + 8 * st);
+            // the A table as a 2D tensor [rows of 256 bytes]: this K step's 16 rows
+            const long row = (long)((src - a.at) + (size_t)ks * kAStep) / 256;
+            tma_load_2d(ast_u + (uint32_t)(st * kAStep), &amap, 0, (int)row, afull0 + 8 * st);
           }
         }
       }
@@ -406,6 +419,25 @@ void launch_hs_tc_tiles(Context& c, int l, const HsDiagTable& t, const u64d* pR,
 #undef HT_TILES
 }
 
+// the A table of one chunk as a 2D uint8 tensor map: rows of 256 bytes,
+// boxes of 16 rows (one 4 KB K step); the driver entry point is fetched
+// through the runtime, so the library does not link libcuda directly
+static void make_amap(CUtensorMap* map, const uint8_t* at, size_t bytes) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q{};
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !encode) fail(HEGPU_ERR_CUDA, "hs_tc: cuTensorMapEncodeTiled unavailable");
+  }
+  const cuuint64_t dims[2] = {256, (cuuint64_t)(bytes / 256)};
+  const cuuint64_t strides[1] = {256};
+  const cuuint32_t box[2] = {256, 16}, estr[2] = {1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(at), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(HEGPU_ERR_CUDA, "hs_tc: cuTensorMapEncodeTiled failed");
+}
+
 void launch_hs_tc(Context& c, const u64d* v, int B, int l, const u64d* D, int r_lo, int r_hi, const uint8_t* at,
                   const u64d* ce, int accumulate, u64d* acc, int keyed, int ndiag) {
   const int N = c.N(), J = l + 1, span = r_hi - r_lo + 1;
@@ -437,6 +469,8 @@ void launch_hs_tc(Context& c, const u64d* v, int B, int l, const u64d* D, int r_
   if (strips > T) strips = T;
   a.strips = (int)strips;
   const size_t smem = (size_t)rc * kNG * 128 + (size_t)kAStages * kAStep;
+  alignas(64) CUtensorMap amap;
+  make_amap(&amap, at, hs_tc_table_bytes(c, l, span));
   const double NB = 8.0 * N;
   const double bytes = (double)hs_tc_table_bytes(c, l, span) + NB * B * (l * J + l) + NB * B * 2 * J * (accumulate ? 2 : 1);
   const double ops = (double)N * B * (keyed * l * J * 2.0 + ndiag * l);
@@ -445,7 +479,8 @@ void launch_hs_tc(Context& c, const u64d* v, int B, int l, const u64d* D, int r_
     static PerDeviceOnce prepared;                                                                   \
     if (prepared.first())                                                                            \
       CK(cudaFuncSetAttribute(k_hs_tc<JJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
-    LAUNCH_BO(c, "k_hs_imma", bytes, ops, (k_hs_tc<JJ><<<(unsigned)(a.nig * strips), kThreads, smem, c.stream>>>(a))); \
+    LAUNCH_BO(c, "k_hs_imma", bytes, ops,                                                           \
+              (k_hs_tc<JJ><<<(unsigned)(a.nig * strips), kThreads, smem, c.stream>>>(a, amap)));      \
     break;                                                                                           \
   }
   switch (J) {
