@@ -76,9 +76,16 @@ N_SM = 148
 INT_OPS_IMAD = {"k_hs_diag": 4, "k_hs_narrow": 4, "k_ks_inner": 4, "k_drop_ntt": 6, "k_md_ntt": 6, "k_md_intt": 6,
                 "k_ks_modup": 6,
                 "k_intt_rows": 6, "k_ks_intt": 6, "k_ntt_rows": 6}
-# kernels whose MACs run on IMMA.16832.U8 as 64 byte-plane products each
+# kernels whose MACs run on the tensor cores (tcgen05.mma.kind::i8,
+# conv_tc.cu / hs_tc.cu) as 64 byte-plane products each
 TENSOR_KERNELS = ("k_hs_imma", "k_conv_mac")
-IMMA_POPS = 1.1  # measured legacy mma.sync u8 rate on this B200 (tools/ubench_mma.cu)
+TC_I8_POPS = 4.5  # nominal dense int8 tcgen05 rate of a B200 (2 ops per MAC)
+# the NTT-family kernels run every butterfly of the 40/45-bit benchmark
+# primes on the FP64 pipe: 6 FP64 instructions per product
+# + 2 adds; B200 FP64 = 64 FMA lanes / clk / SM (half the FP32 rate)
+NTT_FP64_KERNELS = ("k_drop_ntt", "k_md_ntt", "k_md_intt", "k_ks_modup", "k_intt_rows", "k_ks_intt", "k_ntt_rows")
+FP64_PER_CLK_SM = 64.0
+FP64_OPS_PER_BUTTERFLY = 8
 
 
 def int_pipe_roofline(name, kd, clk_mhz):
@@ -86,9 +93,16 @@ def int_pipe_roofline(name, kd, clk_mhz):
         return None
     if name in TENSOR_KERNELS:
         ops = kd["modmuls"] * 64 * 2 / (kd["ms_per_step"] / 1e3) / 1e12
-        return {"pipe": "tensor (IMMA u8)", "achieved": ops, "peak": IMMA_POPS * 1e3, "unit": "TOPS (byte-plane)",
-                "frac": ops / (IMMA_POPS * 1e3),
-                "peak_basis": "measured mma.sync m16n8k32 u8 throughput, 64 byte-plane MACs per modular MAC"}
+        return {"pipe": "tensor (tcgen05 i8)", "achieved": ops, "peak": TC_I8_POPS * 1e3, "unit": "TOPS (byte-plane)",
+                "frac": ops / (TC_I8_POPS * 1e3),
+                "peak_basis": "nominal B200 dense int8 tcgen05 rate; 64 byte-plane MACs per modular MAC (useful work "
+                              "only: band / plane padding excluded)"}
+    if name in NTT_FP64_KERNELS:
+        peak = N_SM * FP64_PER_CLK_SM * clk_mhz * 1e6 / FP64_OPS_PER_BUTTERFLY / 1e9
+        return {"pipe": "fp64", "achieved": kd["gmodmul_s"], "peak": peak, "unit": "G butterflies/s",
+                "frac": kd["gmodmul_s"] / peak,
+                "peak_basis": f"{N_SM} SMs x {FP64_PER_CLK_SM:.0f} FP64/clk/SM x {clk_mhz:.0f} MHz / "
+                              f"{FP64_OPS_PER_BUTTERFLY} FP64 instructions per butterfly"}
     per = INT_OPS_IMAD.get(name, 4)
     peak = N_SM * IMAD_WIDE_PER_CLK_SM * clk_mhz * 1e6 / per / 1e9
     return {"pipe": "int (IMAD)", "achieved": kd["gmodmul_s"], "peak": peak,
@@ -382,7 +396,7 @@ def run_gpu(args):
                 "share_of_step": kd["share"],
                 # the NTT-family kernels are bound by the 64-bit multiply issue
                 # rate more than HBM: their integer-pipe roofline
-                "int_pipe": int_pipe_roofline(dom, kd, clk_mhz),
+                "compute": int_pipe_roofline(dom, kd, clk_mhz),
                 "note": "alg bytes / modmuls per launch per DESIGN.md §5 (LAUNCH_B byte models at each launch "
                         "site); achieved = alg bytes / summed CUDA-event launch time on the engine stream; "
                         "traffic = ncu dram bytes per launch of one step (profiles/)"}

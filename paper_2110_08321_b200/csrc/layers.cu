@@ -466,10 +466,12 @@ bool HsPlan::use_imma(Context& c, int B, int i_lo, int i_hi) const {
          4 * (int64_t)diag.size() >= span && hs_imma_supported(c, level);
 }
 
-void HsPlan::ensure_imma(Context& c) {
-  if (imma_built) return;
+// shared by the mma.sync and tcgen05 paths: epilogue constants, P mod q_t,
+// and the right rotation -> kept diagonal map
+void HsPlan::ensure_imma_consts(Context& c) {
+  if (d_rdiag) return;
   ensure_keys(c);
-  const int l = level, N = c.N(), S = c.S(), np = c.P->np(), J = l + 1;
+  const int l = level, S = c.S(), np = c.P->np();
   // epilogue constants 2^(24 g + 32 h) mod q with Shoup companions
   std::vector<u64> ec((size_t)np * 16);
   for (int pi = 0; pi < np; ++pi) {
@@ -492,6 +494,12 @@ void HsPlan::ensure_imma(Context& c) {
   CK(cudaMemcpy(imma_pmod, pm.data(), pm.size() * 8, cudaMemcpyHostToDevice));
   CK(cudaMalloc((void**)&d_rdiag, rd.size() * sizeof(int)));
   CK(cudaMemcpy(d_rdiag, rd.data(), rd.size() * sizeof(int), cudaMemcpyHostToDevice));
+}
+
+void HsPlan::ensure_imma(Context& c) {
+  if (imma_built) return;
+  ensure_imma_consts(c);
+  const int l = level, N = c.N(), J = l + 1;
   // chunks of kept diagonals whose r span fits the kernel's window ring
   // balanced: nchunk = ceil(r span / max span) chunks of about equal r span
   const int smax = hs_imma_chunk_span(l), rtot = (int)(diag.back().right - diag[0].right) + 1;
@@ -523,7 +531,7 @@ void HsPlan::ensure_imma(Context& c) {
 // window ring (hs_tc_chunk_span), balanced like the mma.sync chunks
 void HsPlan::ensure_tc(Context& c) {
   if (tc_built) return;
-  ensure_imma(c);  // rdiag, pmod
+  ensure_imma_consts(c);  // rdiag
   const int l = level, N = c.N(), np = c.P->np();
   std::vector<u64> ce((size_t)np * 8);
   for (int pi = 0; pi < np; ++pi) {

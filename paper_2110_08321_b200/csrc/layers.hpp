@@ -77,6 +77,7 @@ struct HsPlan {
   int* d_rdiag = nullptr;     // [S] right rotation -> kept diagonal (or -1)
   bool imma_built = false;
   void ensure_imma(Context& c);
+  void ensure_imma_consts(Context& c);
   // the tcgen05 path (hs_tc.cu): chunks (r_lo, r_hi, keyed, ndiag) with their A tables
   struct TcChunk {
     int r_lo, r_hi, keyed, ndiag;
