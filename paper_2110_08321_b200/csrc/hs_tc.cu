@@ -47,8 +47,9 @@ constexpr int kTP = 8;           // positions per tile
 constexpr int kNI = 16;          // images per CTA
 constexpr int kN = kNI * 8;      // MMA N (columns (img, d))
 constexpr int kNG = kN / 8;      // column groups of 8 (core matrices along N)
-constexpr int kAStages = 6;      // A K-step stages of 4 KB
+constexpr int kAStages = 3;      // A stages of kKPS K steps
 constexpr int kAStep = 4096;     // one K step of A: [2 chunks][16 row groups][8][16 B]
+constexpr int kKPS = 2;          // K steps per A stage (one TMA box, one commit)
 constexpr int kThreads = 320;    // 10 warps: 0-7 window staging + epilogue, 8 MMA issuer, 9 A producer
 constexpr int kRCMax = 48;       // ring chunks (16 K bytes x kN columns = 2 KB each)
 
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a, const __grid_co
   const long u0 = T * strip / a.strips, u1 = T * (strip + 1) / a.strips;
   const int nt = (int)(u1 - u0);
   uint8_t* ring = ht_smem;                                   // [RC][kNG][8][16]
-  uint8_t* astage = ht_smem + (size_t)RC * kNG * 128;        // [kAStages][4096]
+  uint8_t* astage = ht_smem + (size_t)RC * kNG * 128;        // [kAStages][kKPS * 4096]
   const uint32_t ring_u = smem_u32(ring), ast_u = smem_u32(astage);
   const uint32_t afull0 = smem_u32(&bars[0]), aempty0 = afull0 + 8 * kAStages;
   const uint32_t bfull0 = aempty0 + 8 * kAStages, done0 = bfull0 + 16, tempty0 = bfull0 + 32;
@@ -292,14 +293,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a, const __grid_co
         mbar_wait(tempty0 + 8 * tb, (uint32_t)(((u >> 1) & 1) ^ 1));
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(tb * kN);
-        for (int ks = 0; ks < NKS; ++ks, ++cnt) {
+        for (int ks0 = 0; ks0 < NKS; ks0 += kKPS, ++cnt) {
           const int st = cnt % kAStages;
           mbar_wait(afull0 + 8 * st, (uint32_t)((cnt / kAStages) & 1));
           tc_fence_after();
-          const uint64_t ad = umma_desc(ast_u + (uint32_t)(st * kAStep), 16 * 128, 128);
-          const int slot = (c_lo + 2 * ks) % RC;
-          const uint64_t bd = umma_desc(ring_u + (uint32_t)(slot * kNG * 128), kNG * 128, 128);
-          tc_mma_u8(d, ad, bd, idesc, ks > 0);
+#pragma unroll
+          for (int h = 0; h < kKPS; ++h) {
+            const int ks = ks0 + h;
+            const uint64_t ad = umma_desc(ast_u + (uint32_t)((st * kKPS + h) * kAStep), 16 * 128, 128);
+            const int slot = (c_lo + 2 * ks) % RC;
+            const uint64_t bd = umma_desc(ring_u + (uint32_t)(slot * kNG * 128), kNG * 128, 128);
+            tc_mma_u8(d, ad, bd, idesc, ks > 0);
+          }
           tc_commit(aempty0 + 8 * st);
         }
         tc_commit(done0 + 8 * tb);
@@ -314,16 +319,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_hs_tc(HtArgs a, const __grid_co
         int t, half, kh0;
         decode(u, t, half, kh0);
         const uint8_t* src = a.at + ((((size_t)t * 2 + half) * tph + kh0 / kTP) * NKS) * kAStep;
-        for (int ks = 0; ks < NKS; ++ks, ++cnt) {
+        for (int ks = 0; ks < NKS; ks += kKPS, ++cnt) {
           const int st = cnt % kAStages;
           mbar_wait(aempty0 + 8 * st, (uint32_t)(((cnt / kAStages) & 1) ^ 1));
           if (a.dbg & 2) {
             mbar_arrive(afull0 + 8 * st);
           } else {
-            mbar_expect_tx(afull0 + 8 * st, kAStep);
-            // the A table as a 2D tensor [rows of 256 bytes]: this K step's 16 rows
+            mbar_expect_tx(afull0 + 8 * st, kKPS * kAStep);
+            // the A table as a 2D tensor [rows of 256 bytes]: this stage's kKPS x 16 rows
             const long row = (long)((src - a.at) + (size_t)ks * kAStep) / 256;
-            tma_load_2d(ast_u + (uint32_t)(st * kAStep), &amap, 0, (int)row, afull0 + 8 * st);
+            tma_load_2d(ast_u + (uint32_t)(st * kKPS * kAStep), &amap, 0, (int)row, afull0 + 8 * st);
           }
         }
       }
@@ -396,7 +401,10 @@ int hs_tc_chunk_span(int l) {
   return std::max(1, (room * 16 - 32) / J - kTP);
 }
 
-int hs_tc_nks(int l, int span) { return ((span + kTP) * (l + 1) + 32 + 31) / 32 + 1; }
+int hs_tc_nks(int l, int span) {
+  const int n = ((span + kTP) * (l + 1) + 32 + 31) / 32 + 1;
+  return (n + kKPS - 1) / kKPS * kKPS;  // whole A stages
+}
 
 size_t hs_tc_table_bytes(Context& c, int l, int span) {
   return (size_t)(l + 1) * c.N() / kTP * hs_tc_nks(l, span) * kAStep;
@@ -433,7 +441,7 @@ static void make_amap(CUtensorMap* map, const uint8_t* at, size_t bytes) {
   }
   const cuuint64_t dims[2] = {256, (cuuint64_t)(bytes / 256)};
   const cuuint64_t strides[1] = {256};
-  const cuuint32_t box[2] = {256, 16}, estr[2] = {1, 1};
+  const cuuint32_t box[2] = {256, 16 * kKPS}, estr[2] = {1, 1};
   const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(at), dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -470,7 +478,7 @@ void launch_hs_tc(Context& c, const u64d* v, int B, int l, const u64d* D, int r_
   if (strips < 1) strips = 1;
   if (strips > T) strips = T;
   a.strips = (int)strips;
-  const size_t smem = (size_t)rc * kNG * 128 + (size_t)kAStages * kAStep;
+  const size_t smem = (size_t)rc * kNG * 128 + (size_t)kAStages * kKPS * kAStep;
   alignas(64) CUtensorMap amap;
   make_amap(&amap, at, hs_tc_table_bytes(c, l, span));
   const double NB = 8.0 * N;
