@@ -107,6 +107,8 @@ struct TcArgs {
   int tcols;          // TMEM columns allocated
   int chunks;         // CTAs per (b, p, t) row
   int nbufs;          // A tile buffers
+  int kcb;            // K bytes per A buffer (a K chunk; kb when the whole row fits)
+  int nkc;            // K chunks per tile
 };
 
 // Warp roles (9 warps): 0-3 producers (thread j stages position j of a
@@ -126,13 +128,14 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv_tc(TcArgs a) {
   const int npad = a.npad[t], PL = a.planes[t];
   const int ntile_all = N / kTcM;
   const int tile0 = chunk * ntile_all / a.chunks, tile1 = (chunk + 1) * ntile_all / a.chunks, nt = tile1 - tile0;
-  const int NBF = a.nbufs;
-  // shared memory: A[NBF] (kTcM x KB bytes each), then B (npad x KB bytes)
+  const int NBF = a.nbufs, KCB = a.kcb, NKC = a.nkc, nu = nt * NKC;
+  // shared memory: A[NBF] (kTcM x KCB bytes each: one K chunk of a tile),
+  // then B (npad x KB bytes, the whole K, resident for the CTA)
   uint8_t* sA = tc_smem;
-  uint8_t* sB = tc_smem + NBF * (size_t)kTcM * KB;
+  uint8_t* sB = tc_smem + NBF * (size_t)kTcM * KCB;
   const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
   const uint32_t full0 = smem_u32(&bars[0]), empty0 = full0 + 32, tfull0 = full0 + 64, tempty0 = full0 + 80;
-  const int npairs = KB / 16;  // tap pairs (16 K bytes each), incl. zero padding
+  const int npairs = KB / 16, cpairs = KCB / 16;  // tap pairs (16 K bytes each), incl. zero padding
   if (warp == 4) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_slot)),
                  "r"(a.tcols)
@@ -151,19 +154,10 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv_tc(TcArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   // the weight operand of limb t (K-major core-matrix image, npad x KB bytes)
-  // and the zero padding (taps >= ntaps) of every A buffer, written once
   {
     const uint4* src = a.wb + (size_t)t * (KB * 256 / 16);  // images are laid out at npad = 256 stride
     uint4* dst = reinterpret_cast<uint4*>(sB);
     for (int i = tid; i < npad * KB / 16; i += kTcThreads) dst[i] = __ldg(src + i);
-    for (int bf = 0; bf < NBF; ++bf)
-      for (int idx = tid; idx < npairs * kTcM; idx += kTcThreads) {
-        const int sp = idx / kTcM, j = idx % kTcM, s = 2 * sp;
-        uint64_t* r = reinterpret_cast<uint64_t*>(sA + (size_t)bf * kTcM * KB +
-                                                  ((size_t)(sp * 16 + (j >> 3)) * 8 + (j & 7)) * 16);
-        if (s >= a.ntaps) r[0] = 0;
-        if (s + 1 >= a.ntaps) r[1] = 0;
-      }
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   tc_fence_before();
@@ -176,26 +170,31 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv_tc(TcArgs a) {
     const int j = tid;
     const u64d* src0 = a.taps + (size_t)b * a.ntaps * ct_words + (size_t)p * l * N + (size_t)t * N + j;
     const uint32_t roff = (uint32_t)(((j >> 3) * 8 + (j & 7)) * 16);
-    for (int k = 0; k <= nt; ++k) {
-      if (k < nt) {
-        const int bf = k % NBF;
-        mbar_wait(empty0 + 8 * bf, (uint32_t)(((k / NBF) & 1) ^ 1));  // passes at once on a fresh barrier
-        const uint32_t dst0 = sA_u + (uint32_t)(bf * kTcM * KB) + roff;
+    // unit u = (tile u / NKC, K chunk u % NKC); the buffers cycle over units,
+    // so the zero padding (taps >= ntaps, last chunk only) is rewritten each time
+    for (int u = 0; u <= nu; ++u) {
+      if (u < nu) {
+        const int bf = u % NBF, k = u / NKC, kc = u - k * NKC;
+        mbar_wait(empty0 + 8 * bf, (uint32_t)(((u / NBF) & 1) ^ 1));  // passes at once on a fresh barrier
+        const uint32_t dst0 = sA_u + (uint32_t)(bf * kTcM * KCB) + roff;
         const u64d* src = src0 + (size_t)(tile0 + k) * kTcM;
-        for (int sp = 0; sp < npairs; ++sp) {
+        const int sp0 = kc * cpairs, sp1 = min(npairs, sp0 + cpairs);
+        for (int sp = sp0; sp < sp1; ++sp) {
           const int s = 2 * sp;
-          const uint32_t d = dst0 + (uint32_t)sp * 16 * 128;
+          const uint32_t d = dst0 + (uint32_t)(sp - sp0) * 16 * 128;
           if (s < a.ntaps) cp_async8(d, src + (size_t)s * ct_words);
+          else asm volatile("st.shared.u64 [%0], %1;\n" ::"r"(d), "l"(0ull) : "memory");
           if (s + 1 < a.ntaps) cp_async8(d + 8, src + (size_t)(s + 1) * ct_words);
+          else asm volatile("st.shared.u64 [%0], %1;\n" ::"r"(d + 8), "l"(0ull) : "memory");
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
       }
-      if (k >= 1) {
-        // tile k - 1 landed (this thread's rows): publish it to the MMA issuer
-        if (k < nt) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      if (u >= 1) {
+        // unit u - 1 landed (this thread's rows): publish it to the MMA issuer
+        if (u < nu) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(full0 + 8 * ((k - 1) % NBF)) : "memory");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(full0 + 8 * ((u - 1) % NBF)) : "memory");
       }
     }
   } else if (warp == 4) {
@@ -204,19 +203,20 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv_tc(TcArgs a) {
       const uint32_t idesc = idesc_u8(kTcM, npad);
       const uint32_t a_lbo = 16 * 128, a_sbo = 128;                       // A: [K chunk][16 position groups][8][16 B]
       const uint32_t b_lbo = (uint32_t)(npad / 8) * 128, b_sbo = 128;     // B: [K chunk][npad / 8 groups][8][16 B]
-      for (int k = 0; k < nt; ++k) {
-        const int bf = k % NBF, tb = k & 1;
-        mbar_wait(full0 + 8 * bf, (uint32_t)((k / NBF) & 1));
-        mbar_wait(tempty0 + 8 * tb, (uint32_t)(((k >> 1) & 1) ^ 1));
+      for (int u = 0; u < nu; ++u) {
+        const int bf = u % NBF, k = u / NKC, kc = u - k * NKC, tb = k & 1;
+        mbar_wait(full0 + 8 * bf, (uint32_t)((u / NBF) & 1));
+        if (kc == 0) mbar_wait(tempty0 + 8 * tb, (uint32_t)(((k >> 1) & 1) ^ 1));
         tc_fence_after();
-        const uint32_t a0 = sA_u + (uint32_t)(bf * kTcM * KB), d = tmem + (uint32_t)(tb * a.nb);
-        for (int ks = 0; ks < KB / 32; ++ks) {
-          const uint64_t ad = umma_desc(a0 + (uint32_t)ks * 2 * a_lbo, a_lbo, a_sbo);
+        const uint32_t a0 = sA_u + (uint32_t)(bf * kTcM * KCB), d = tmem + (uint32_t)(tb * a.nb);
+        const int ks0 = kc * (KCB / 32), ks1 = min(KB, (kc + 1) * KCB) / 32;
+        for (int ks = ks0; ks < ks1; ++ks) {
+          const uint64_t ad = umma_desc(a0 + (uint32_t)(ks - ks0) * 2 * a_lbo, a_lbo, a_sbo);
           const uint64_t bd = umma_desc(sB_u + (uint32_t)ks * 2 * b_lbo, b_lbo, b_sbo);
           tc_mma_u8(d, ad, bd, idesc, ks > 0);
         }
-        tc_commit(empty0 + 8 * bf);  // the A buffer may be refilled
-        tc_commit(tfull0 + 8 * tb);  // the accumulator is ready
+        tc_commit(empty0 + 8 * bf);                    // the A buffer may be refilled
+        if (kc == NKC - 1) tc_commit(tfull0 + 8 * tb);  // the accumulator is ready
       }
     }
     __syncwarp();
@@ -263,6 +263,19 @@ int planes_of(u64 q) {
   return n;
 }
 
+constexpr size_t kTcSmem = 200 * 1024;
+
+// K bytes per A buffer: the whole row when A[nbufs] + B fit, else the
+// fewest equal K chunks (multiples of 32 bytes) that do; 0 if even B plus
+// 32-byte chunks does not fit
+int pick_kcb(int kb, int maxn, int nbufs) {
+  const size_t bsz = (size_t)kb * maxn, per32 = (size_t)nbufs * kTcM * 32;
+  if (bsz + per32 > kTcSmem) return 0;
+  const int kcmax = std::min(kb, (int)((kTcSmem - bsz) / per32) * 32);
+  const int nkc = (kb + kcmax - 1) / kcmax;
+  return ((kb + nkc - 1) / nkc + 31) / 32 * 32;
+}
+
 }  // namespace
 
 bool conv_tc_enabled() {
@@ -277,9 +290,9 @@ bool conv_tc_supported(Context& c, int ntaps, int c_out, int l) {
     const int pl = planes_of(c.P->q(t));
     if (c_out * pl > 256) return false;
   }
-  // A buffers + B at the widest limb
-  const size_t sm = kTcBufs * (size_t)kTcM * kb + (size_t)kb * 256;
-  return sm <= 200 * 1024;
+  int maxn = 16;
+  for (int t = 0; t < l; ++t) maxn = std::max(maxn, (c_out * planes_of(c.P->q(t)) + 15) / 16 * 16);
+  return pick_kcb(kb, maxn, kTcBufs) > 0;
 }
 
 // B operand images: per limb, [K chunk][column group][8 rows][16 B] with
@@ -337,14 +350,18 @@ void launch_conv_tc(Context& c, const u64d* taps, int B, int ntaps, int l, const
   const int tiles = et ? std::max(1, atoi(et)) : kTcTiles;
   a.nbufs = eb ? std::min(4, std::max(2, atoi(eb))) : kTcBufs;
   a.chunks = std::max(1, ntile / tiles);
-  size_t sm = (size_t)a.nbufs * kTcM * a.kb + (size_t)a.kb * maxn;
-  if (sm > 200 * 1024) {
+  a.kcb = pick_kcb(a.kb, maxn, a.nbufs);
+  if (a.kcb == 0 || a.kcb < a.kb) {  // the A ring is K-chunked: keep the default buffer count
     a.nbufs = kTcBufs;
-    sm = (size_t)a.nbufs * kTcM * a.kb + (size_t)a.kb * maxn;
+    a.kcb = pick_kcb(a.kb, maxn, a.nbufs);
   }
+  if (const char* ek = getenv("HEGPU_TC_KCB")) a.kcb = std::min(a.kb, std::max(32, atoi(ek) / 32 * 32));
+  const size_t sm = (size_t)a.nbufs * kTcM * a.kcb + (size_t)a.kb * maxn;
+  if (a.kcb == 0 || sm > kTcSmem) fail(HEGPU_ERR_ARG, "conv_tc: operands exceed shared memory");
+  a.nkc = (a.kb + a.kcb - 1) / a.kcb;
   static PerDeviceOnce prepared;
   if (prepared.first())
-    CK(cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem));
   const int N = c.N();
   const double bytes = 8.0 * N * l * (2.0 * B * ntaps + 2.0 * B * c_out + c_out);
   const double ops = 2.0 * N * l * B * ntaps * c_out;

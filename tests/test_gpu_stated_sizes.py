@@ -173,12 +173,17 @@ def _conv_np(img, W, b, s=1):
     return out
 
 
-@pytest.mark.parametrize("c_in,k,c_out", [(32, 5, 64), (3, 3, 18)])
-def test_cfg4_conv_layer_at_size(c_in, k, c_out):
+@pytest.mark.parametrize("c_in,k,c_out,kcb", [(32, 5, 64, None), (3, 3, 18, None), (3, 5, 32, None),
+                                               (3, 3, 18, "32"), (3, 3, 18, "96")])
+def test_cfg4_conv_layer_at_size(c_in, k, c_out, kcb, monkeypatch):
     """config 4: c_in x 32 x 32 U[0,1], stride 1, N = 16384, taps at level 2
     (the bench's chain); conv_packed_forward + rescale limbs == oracle, HOPs
     k^2 c_in c_out / (k^2 c_in - 1) c_out / c_out, decrypted maps vs the
-    FP64 conv"""
+    FP64 conv.  (3, 5, 32) is config 3's first layer (75 taps: the tcgen05
+    conv's tap ring runs in K chunks); kcb forces K chunks of that many bytes
+    on the 27-tap case (HEGPU_TC_KCB)"""
+    if kcb is not None:
+        monkeypatch.setenv("HEGPU_TC_KCB", kcb)
     ctx = H.Context(14, [45, 40], 45, seed=4)
     ck = Ckks(14, [45, 40], 45, seed=4)
     rng = np.random.default_rng(40 + c_in * k + c_out)

@@ -14,8 +14,8 @@ dt = ctx.ct(B * net.ntaps, net.top, taps, 2.0 ** 40)
 out = ctx.ct(B, net.out_level)
 net.run(dt, out); ctx.sync()
 tot = 0
-for k in ["k_hs_diag", "k_drop_ntt", "k_ks_modup", "k_conv_mac", "k_intt_rows", "k_ks_intt", "k_ks_inner",
-          "k_add", "k_tensor_square", "k_add_plain", "k_sum_parts", "k_merge_c"]:
+for k in ["k_hs_diag", "k_hs_imma", "k_drop_ntt", "k_md_ntt", "k_md_intt", "k_ks_modup", "k_conv_mac", "k_intt_rows",
+          "k_ks_intt", "k_ks_inner", "k_add", "k_tensor_square", "k_add_plain", "k_sum_parts", "k_merge_c"]:
     ctx.kernel_timer(k)
     net.run(dt, out)
     ms, n, b, o = ctx.kernel_timer_read_ops()
