@@ -18,7 +18,14 @@
 // instruction), tcgen05.commit arrives on an mbarrier, the epilogue warps
 // read the accumulator with tcgen05.ld.  Two accumulator and three A
 // buffers: the MMA of tile i overlaps the epilogue of tile i - 1 and the
-// cp.async staging of tiles i + 1, i + 2.  Limbs are the same residues as the IMAD / mma.sync paths.
+// cp.async staging of tiles i + 1, i + 2.  When B plus three whole-K A
+// tiles exceed shared memory (config 3's 75-tap first layer: B alone is
+// 117 KB) the A ring holds K chunks instead: a pipeline unit is (tile, K
+// chunk), the chunks of one tile accumulate into the same TMEM buffer, and
+// four buffers with two units in flight per producer keep the loads deep.
+// The epilogue (8 warps, 4 maps per tcgen05.wait::ld) combines the byte
+// planes with 32x32->64 multiply-adds and prefetches the next group's bias
+// words.  Limbs are the same residues as the IMAD / mma.sync paths.
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
@@ -31,9 +38,11 @@ namespace hegpu {
 namespace {
 
 constexpr int kTcM = 128;       // positions per tile (MMA M)
-constexpr int kTcThreads = 288;  // 9 warps: 4 producers, 1 MMA issuer, 4 epilogue
+constexpr int kEpiWarps = 8;     // two epilogue warps per TMEM lane quarter (maps split between them)
+constexpr int kTcThreads = 32 * (5 + kEpiWarps);  // 4 producers, 1 MMA issuer, the epilogue
 constexpr int kTcTiles = 16;     // position tiles per CTA (HEGPU_TC_TILES)
-constexpr int kTcBufs = 3;       // A (tap) tile buffers in flight (HEGPU_TC_BUFS, 2..4)
+constexpr int kTcBufs = 3;       // A (tap) tile buffers in flight (HEGPU_TC_BUFS, 2..kMaxBufs)
+constexpr int kMaxBufs = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -68,6 +77,20 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
 }
 
+// cp.async.wait_group takes an immediate: at most n (0..7) groups left pending
+__device__ __forceinline__ void cp_async_wait_dyn(int n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
+    case 3: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
+    case 4: asm volatile("cp.async.wait_group 4;\n" ::: "memory"); break;
+    case 5: asm volatile("cp.async.wait_group 5;\n" ::: "memory"); break;
+    case 6: asm volatile("cp.async.wait_group 6;\n" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 7;\n" ::: "memory"); break;
+  }
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
@@ -84,13 +107,17 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
                : "memory");
 }
-// 8 consecutive accumulator columns of this thread's TMEM lane
-__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+// 8 consecutive accumulator columns of this thread's TMEM lane (completed by tcgen05.wait::ld)
+__device__ __forceinline__ void tc_ld8_nowait(uint32_t taddr, uint32_t (&r)[8]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+// ties registers loaded by tc_ld8_nowait to a preceding tcgen05.wait::ld
+// (the compiler may not hoist their uses above this volatile asm)
+__device__ __forceinline__ void tc_after_wait(uint32_t (&r)[8]) {
+  asm volatile("" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]));
 }
 
 struct TcArgs {
@@ -109,17 +136,20 @@ struct TcArgs {
   int nbufs;          // A tile buffers
   int kcb;            // K bytes per A buffer (a K chunk; kb when the whole row fits)
   int nkc;            // K chunks per tile
+  int lag;            // units a producer keeps in flight before publishing the oldest (1..nbufs - 1)
 };
 
-// Warp roles (9 warps): 0-3 producers (thread j stages position j of a
+// Warp roles (13 warps): 0-3 producers (thread j stages position j of a
 // tile: its tap words by cp.async into the core-matrix rows), 4 the MMA
-// issuer (one lane), 5-8 the epilogue (warp w reads TMEM lanes 32 (w % 4)).
+// issuer (one lane), 5-12 the epilogue (warp w reads TMEM lanes 32 (w % 4);
+// warps 5-8 take maps 0-3, 8-11, ..., warps 9-12 maps 4-7, 12-15, ...: four
+// maps' columns loaded per tcgen05.wait::ld).
 // mbarriers: full[buf] (128 producer arrivals, after each producer's
 // cp.async.wait + proxy fence), empty[buf] and tfull[tb] (tcgen05.commit),
 // tempty[tb] (128 epilogue arrivals) -- no CTA-wide barrier in the loop.
-__global__ void __launch_bounds__(kTcThreads, 2) k_conv_tc(TcArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 1) k_conv_tc(TcArgs a) {
   extern __shared__ __align__(128) uint8_t tc_smem[];
-  __shared__ __align__(8) uint64_t bars[2 * 4 + 4];  // full[4], empty[4], tfull[2], tempty[2]
+  __shared__ __align__(8) uint64_t bars[2 * kMaxBufs + 4];  // full[], empty[], tfull[2], tempty[2]
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int N = a.N, l = a.l, KB = a.kb;
@@ -134,7 +164,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv_tc(TcArgs a) {
   uint8_t* sA = tc_smem;
   uint8_t* sB = tc_smem + NBF * (size_t)kTcM * KCB;
   const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
-  const uint32_t full0 = smem_u32(&bars[0]), empty0 = full0 + 32, tfull0 = full0 + 64, tempty0 = full0 + 80;
+  const uint32_t full0 = smem_u32(&bars[0]), empty0 = full0 + 8 * kMaxBufs, tfull0 = full0 + 16 * kMaxBufs,
+                 tempty0 = tfull0 + 16;
   const int npairs = KB / 16, cpairs = KCB / 16;  // tap pairs (16 K bytes each), incl. zero padding
   if (warp == 4) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_slot)),
@@ -143,13 +174,13 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv_tc(TcArgs a) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
   }
   if (tid == 0) {
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < kMaxBufs; ++i) {
       mbar_init(full0 + 8 * i, kTcM);
       mbar_init(empty0 + 8 * i, 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull0 + 8 * i, 1);
-      mbar_init(tempty0 + 8 * i, kTcM);
+      mbar_init(tempty0 + 8 * i, 32 * kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -172,29 +203,35 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv_tc(TcArgs a) {
     const uint32_t roff = (uint32_t)(((j >> 3) * 8 + (j & 7)) * 16);
     // unit u = (tile u / NKC, K chunk u % NKC); the buffers cycle over units,
     // so the zero padding (taps >= ntaps, last chunk only) is rewritten each time
-    for (int u = 0; u <= nu; ++u) {
+    const int lag = a.lag;
+    for (int u = 0; u < nu + lag; ++u) {
       if (u < nu) {
         const int bf = u % NBF, k = u / NKC, kc = u - k * NKC;
         mbar_wait(empty0 + 8 * bf, (uint32_t)(((u / NBF) & 1) ^ 1));  // passes at once on a fresh barrier
         const uint32_t dst0 = sA_u + (uint32_t)(bf * kTcM * KCB) + roff;
         const u64d* src = src0 + (size_t)(tile0 + k) * kTcM;
-        const int sp0 = kc * cpairs, sp1 = min(npairs, sp0 + cpairs);
-        for (int sp = sp0; sp < sp1; ++sp) {
+        const int sp0 = kc * cpairs, sp1 = min(npairs, sp0 + cpairs), spf = min(sp1, a.ntaps >> 1);
+        // whole tap pairs: a running source pointer, no predicates
+        uint32_t d = dst0;
+        const u64d* sp_src = src + (size_t)(2 * sp0) * ct_words;
+        for (int sp = sp0; sp < spf; ++sp, d += 16 * 128, sp_src += 2 * ct_words) {
+          cp_async8(d, sp_src);
+          cp_async8(d + 8, sp_src + ct_words);
+        }
+        // the last odd tap and the zero padding up to the 32-byte K step
+        for (int sp = max(sp0, spf); sp < sp1; ++sp, d += 16 * 128) {
           const int s = 2 * sp;
-          const uint32_t d = dst0 + (uint32_t)(sp - sp0) * 16 * 128;
           if (s < a.ntaps) cp_async8(d, src + (size_t)s * ct_words);
           else asm volatile("st.shared.u64 [%0], %1;\n" ::"r"(d), "l"(0ull) : "memory");
-          if (s + 1 < a.ntaps) cp_async8(d + 8, src + (size_t)(s + 1) * ct_words);
-          else asm volatile("st.shared.u64 [%0], %1;\n" ::"r"(d + 8), "l"(0ull) : "memory");
+          asm volatile("st.shared.u64 [%0], %1;\n" ::"r"(d + 8), "l"(0ull) : "memory");
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
       }
-      if (u >= 1) {
-        // unit u - 1 landed (this thread's rows): publish it to the MMA issuer
-        if (u < nu) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-        else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      if (u >= lag) {
+        // unit u - lag landed (this thread's rows): publish it to the MMA issuer
+        cp_async_wait_dyn(min(lag, nu - 1 - (u - lag)));
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(full0 + 8 * ((u - 1) % NBF)) : "memory");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(full0 + 8 * ((u - lag) % NBF)) : "memory");
       }
     }
   } else if (warp == 4) {
@@ -221,29 +258,61 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv_tc(TcArgs a) {
     }
     __syncwarp();
   } else {
-    // ---- epilogue: position pos of each tile, every map
-    const int lane_grp = warp & 3;
+    // ---- epilogue: position pos of each tile, every map.  The bias words
+    // (poly 0) of the next map group are loaded while the current group's
+    // accumulator columns come out of TMEM, so their L2 latency is hidden.
+    const int lane_grp = warp & 3, half = (warp - 5) >> 2;
     const int pos = 32 * lane_grp + lane;
     const DevPrime pr = a.pt.p[t];
+    const u64d* bias_t = (p == 0 && a.bias) ? a.bias + (size_t)t * N + pos : nullptr;
+    const size_t bstride = (size_t)l * N;
+    u64d* obase = a.out + (size_t)b * a.c_out * ct_words + (size_t)p * l * N + (size_t)t * N + (size_t)tile0 * kTcM + pos;
+    auto load_bias = [&](u64d(&o)[4], int k, int c0) {
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        o[g] = (bias_t && k < nt && c0 + g < a.c_out)
+                   ? __ldg(bias_t + (size_t)(c0 + g) * bstride + (size_t)(tile0 + k) * kTcM)
+                   : 0ull;
+    };
+    u64d bcur[4], bnxt[4];
+    load_bias(bcur, 0, 4 * half);
     for (int k = 0; k < nt; ++k) {
       const int tb = k & 1;
       mbar_wait(tfull0 + 8 * tb, (uint32_t)((k >> 1) & 1));
       tc_fence_after();
-      const int kpos = (tile0 + k) * kTcM + pos;
       const uint32_t lanebase = tmem + ((uint32_t)(32 * lane_grp) << 16) + (uint32_t)(tb * a.nb);
-      for (int co = 0; co < a.c_out; ++co) {
-        uint32_t r[8];
-        tc_ld8(lanebase + (uint32_t)(co * PL), r);
-        u64d lo = (p == 0 && a.bias) ? __ldg(a.bias + ((size_t)co * l + t) * N + kpos) : 0ull, hi = 0;
+      for (int c0 = 4 * half; c0 < a.c_out; c0 += 8) {
+        const int ng = min(4, a.c_out - c0);
+        uint32_t r[4][8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          if (e >= PL) break;
-          const u64d v = (u64d)r[e];
-          const u64d l_add = v << (8 * e), h_add = e ? v >> (64 - 8 * e) : 0ull;
-          asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(l_add), "l"(h_add));
+        for (int g = 0; g < 4; ++g)
+          if (g < ng) tc_ld8_nowait(lanebase + (uint32_t)((c0 + g) * PL), r[g]);
+        if (c0 + 8 < a.c_out) load_bias(bnxt, k, c0 + 8);
+        else load_bias(bnxt, k + 1, 4 * half);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          if (g >= ng) break;
+          tc_after_wait(r[g]);
+          const int co = c0 + g;
+          // T = bias R + sum_e C_e 2^(8e): columns >= PL belong to the next map;
+          // x = planes 0-3 and y = planes 4-7 stay below 2^51, T = x + y 2^32
+          uint32_t cv[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) cv[e] = e < PL ? r[g][e] : 0u;
+          u64d x = bcur[g] + (u64d)cv[0];
+          x += (u64d)cv[1] << 8;
+          x += (u64d)cv[2] << 16;
+          x += (u64d)cv[3] << 24;
+          u64d y = (u64d)cv[4];
+          y += (u64d)cv[5] << 8;
+          y += (u64d)cv[6] << 16;
+          y += (u64d)cv[7] << 24;
+          const u64d lo = x + (y << 32), hi = (y >> 32) + (lo < x);
+          obase[(size_t)co * ct_words + (size_t)k * kTcM] = mont_reduce128(lo, hi, pr.q, pr.qneg_inv);
         }
-        a.out[((size_t)b * a.c_out + co) * ct_words + (size_t)p * l * N + (size_t)t * N + kpos] =
-            mont_reduce128(lo, hi, pr.q, pr.qneg_inv);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) bcur[g] = bnxt[g];
       }
       tc_fence_before();
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tempty0 + 8 * tb) : "memory");
@@ -348,14 +417,22 @@ void launch_conv_tc(Context& c, const u64d* taps, int B, int ntaps, int l, const
   const char* et = getenv("HEGPU_TC_TILES");
   const char* eb = getenv("HEGPU_TC_BUFS");
   const int tiles = et ? std::max(1, atoi(et)) : kTcTiles;
-  a.nbufs = eb ? std::min(4, std::max(2, atoi(eb))) : kTcBufs;
+  a.nbufs = eb ? std::min(kMaxBufs, std::max(2, atoi(eb))) : kTcBufs;
   a.chunks = std::max(1, ntile / tiles);
   a.kcb = pick_kcb(a.kb, maxn, a.nbufs);
-  if (a.kcb == 0 || a.kcb < a.kb) {  // the A ring is K-chunked: keep the default buffer count
-    a.nbufs = kTcBufs;
+  bool chunked = a.kcb < a.kb;
+  if (!eb && chunked) {  // K-chunked A ring: shorter units, one more buffer, two units in flight
+    a.nbufs = kTcBufs + 1;
     a.kcb = pick_kcb(a.kb, maxn, a.nbufs);
+    if (a.kcb == 0) {
+      a.nbufs = kTcBufs;
+      a.kcb = pick_kcb(a.kb, maxn, a.nbufs);
+    }
   }
   if (const char* ek = getenv("HEGPU_TC_KCB")) a.kcb = std::min(a.kb, std::max(32, atoi(ek) / 32 * 32));
+  chunked = a.kcb < a.kb;
+  const char* el = getenv("HEGPU_TC_LAG");
+  a.lag = std::min(a.nbufs - 1, std::max(1, el ? atoi(el) : chunked ? 2 : 1));
   const size_t sm = (size_t)a.nbufs * kTcM * a.kcb + (size_t)a.kb * maxn;
   if (a.kcb == 0 || sm > kTcSmem) fail(HEGPU_ERR_ARG, "conv_tc: operands exceed shared memory");
   a.nkc = (a.kb + a.kcb - 1) / a.kcb;
