@@ -646,3 +646,350 @@ def golden_stage_tallies(spec):
         rows[f"Dense{i + 1}"] = (1, add_, mul_, 0, rot)
         n = m
     return rows
+
+
+# ------------------------------------- general lower() / execute() ---------
+# The full stage driver of the reference (SubConv groups, grouped merges,
+# the stand-alone ConvPack repack and the LoLa policies), restated from
+# proj/src/netcompile.cpp:14-446.  Layers are dicts {kind, k, s, out, groups,
+# policy, label} (kind in conv / subconv / avgpool / square / flatten /
+# dense; policy None or convpack / hs / lola_dense / lola_stacked).
+_LINEAR = ("conv", "subconv", "avgpool", "flatten", "dense")
+
+
+def _lget(l, key, default):
+    v = l.get(key, default)
+    return default if v is None else v
+
+
+def _is_standalone_convpack(l):  # netcompile.cpp:21-24
+    return l["kind"] == "conv" and l.get("policy") == "convpack"
+
+
+def _apply_layer(shape, l, where):
+    """netcompile.cpp:34-69; shape = (c, d, flat, flat_len)"""
+    c, d, flat, flat_len = shape
+    kind = l["kind"]
+    if kind in ("conv", "subconv"):
+        if flat:
+            raise ShapeError(where + ": convolution after flatten")
+        g = _lget(l, "groups", 1)
+        if kind == "subconv" and (c % g or l["out"] % g):
+            raise ShapeError(f"{where}: channels not divisible into {g} groups")
+        return (l["out"], (d - l["k"]) // _lget(l, "s", 1) + 1, flat, flat_len)
+    if kind == "avgpool":
+        if flat:
+            raise ShapeError(where + ": pooling after flatten")
+        return (c, (d - l["k"]) // _lget(l, "s", 1) + 1, flat, flat_len)
+    if kind == "flatten":
+        return (c, d, True, _shape_size(shape))
+    if kind == "dense":
+        return (c, d, True, l["out"])
+    return shape
+
+
+def _shape_size(shape):
+    c, d, flat, flat_len = shape
+    return flat_len if flat else c * d * d
+
+
+def _lookahead_groups(layers, frm):  # netcompile.cpp:71-91
+    for j in range(frm, len(layers)):
+        l = layers[j]
+        if l["kind"] == "square":
+            continue
+        if _is_standalone_convpack(l):
+            return 1
+        if l["kind"] == "subconv":
+            return _lget(l, "groups", 1)
+        if l["kind"] in _LINEAR:
+            r = j
+            while r < len(layers) and layers[r]["kind"] in _LINEAR and not _is_standalone_convpack(layers[r]):
+                if layers[r]["kind"] == "subconv":
+                    return _lget(layers[r], "groups", 1)
+                r += 1
+            return 1
+    return 1
+
+
+def lower(model):
+    """proj/src/netcompile.cpp:106-213.  model = dict(name, in_c, in_d,
+    n_slots, layers, default_policy='hs').  Returns the stage list: dicts
+    {kind (convpack / merge / square / repackconv / linear), label,
+    layer_idx, groups, policy}."""
+    layers = model["layers"]
+    N = model["n_slots"]
+    if not layers:
+        raise ShapeError("model has no layers")
+    if not is_power_of_two(N):
+        raise ShapeError("n_slots must be a power of two")
+    stages = []
+    shape = (model["in_c"], model["in_d"], False, 0)
+    idx, flat_n, square_n, linear_n, maps_layout = 0, 0, 0, 0, False
+    l0 = layers[0]
+    if l0["kind"] == "conv" and l0.get("policy") in (None, "convpack"):
+        label = l0.get("label") or "Conv1"
+        nxt = _apply_layer(shape, l0, label)
+        if nxt[1] * nxt[1] > N:
+            raise CapacityError(f"{label}: d_out^2 = {nxt[1] * nxt[1]} > n_slots = {N}")
+        stages.append(dict(kind="convpack", label=label, layer_idx=[0], groups=1, policy="hs"))
+        shape, maps_layout, idx = nxt, True, 1
+    while idx < len(layers):
+        l = layers[idx]
+        if l["kind"] == "square":
+            if maps_layout:
+                flat_n += 1
+                g = _lookahead_groups(layers, idx + 1)
+                label = f"Flat{flat_n}"
+                if shape[0] % g:
+                    raise ShapeError(f"{label}: {shape[0]} maps not divisible into {g} groups")
+                if (shape[0] // g) * shape[1] * shape[1] > N:
+                    raise CapacityError(f"{label}: group footprint {(shape[0] // g) * shape[1] ** 2} > n_slots = {N}")
+                stages.append(dict(kind="merge", label=label, layer_idx=[], groups=g, policy="hs"))
+                maps_layout = False
+            square_n += 1
+            stages.append(dict(kind="square", label=f"Square{square_n}", layer_idx=[idx], groups=1, policy="hs"))
+            idx += 1
+            continue
+        if l["kind"] not in _LINEAR:
+            raise ShapeError(f"unsupported layer kind at index {idx}")
+        if _is_standalone_convpack(l):
+            label = l.get("label") or f"Conv{idx}"
+            stages.append(dict(kind="repackconv", label=label, layer_idx=[idx], groups=1, policy="hs"))
+            shape = _apply_layer(shape, l, label)
+            maps_layout = True
+            idx += 1
+            continue
+        st = dict(kind="linear", label="", layer_idx=[], groups=1, policy=model.get("default_policy", "hs"))
+        j = idx
+        while j < len(layers) and layers[j]["kind"] in _LINEAR and not _is_standalone_convpack(layers[j]):
+            st["layer_idx"].append(j)
+            if layers[j]["kind"] == "subconv":
+                st["groups"] = _lget(layers[j], "groups", 1)
+            if layers[j].get("policy"):
+                st["policy"] = layers[j]["policy"]
+            j += 1
+        linear_n += 1
+        st["label"] = "-".join(layers[r]["label"] for r in st["layer_idx"] if layers[r].get("label")) \
+            or f"Linear{linear_n}"
+        if st["groups"] > 1 and st["policy"] != "hs":
+            raise ShapeError(st["label"] + ": grouped stages require the HS kernel")
+        if maps_layout:
+            flat_n += 1
+            stages.append(dict(kind="merge", label=f"Flat{flat_n}", layer_idx=[], groups=st["groups"], policy="hs"))
+            maps_layout = False
+        run_shape = shape
+        for r in st["layer_idx"]:
+            run_shape = _apply_layer(run_shape, layers[r], st["label"])
+        m, n = _shape_size(run_shape), _shape_size(shape)
+        if m > N or n > N:
+            raise CapacityError(f"{st['label']}: fused {m}x{n} exceeds n_slots = {N}")
+        stages.append(st)
+        shape, idx = run_shape, j
+    return stages
+
+
+def split_model_weights(model, flat):
+    """the float32 weights stream (proj/src/modelio.cpp:169-202) -> per layer
+    (W [out][c][k][k], b) for conv, [(W, b)] * groups for subconv, (W [m][n],
+    b) for dense, None otherwise"""
+    flat = np.asarray(flat, dtype=np.float64)
+    out, o = [], 0
+    shape = (model["in_c"], model["in_d"], False, 0)
+    for l in model["layers"]:
+        c, d = shape[0], shape[1]
+        if l["kind"] == "conv":
+            n = l["out"] * c * l["k"] ** 2
+            out.append((flat[o:o + n].reshape(l["out"], c, l["k"], l["k"]), flat[o + n:o + n + l["out"]]))
+            o += n + l["out"]
+        elif l["kind"] == "subconv":
+            g = _lget(l, "groups", 1)
+            po, pi = l["out"] // g, c // g
+            banks = []
+            for _ in range(g):
+                n = po * pi * l["k"] ** 2
+                banks.append((flat[o:o + n].reshape(po, pi, l["k"], l["k"]), flat[o + n:o + n + po]))
+                o += n + po
+            out.append(banks)
+        elif l["kind"] == "dense":
+            n_in = _shape_size(shape)
+            n = l["out"] * n_in
+            out.append((flat[o:o + n].reshape(l["out"], n_in), flat[o + n:o + n + l["out"]]))
+            o += n + l["out"]
+        else:
+            out.append(None)
+        shape = _apply_layer(shape, l, "shape inference")
+    if o != len(flat):
+        raise ShapeError(f"weights: the model needs {o} values, got {len(flat)}")
+    return out
+
+
+def model_weight_count(model):
+    shape, o = (model["in_c"], model["in_d"], False, 0), 0
+    for l in model["layers"]:
+        c = shape[0]
+        if l["kind"] == "conv":
+            o += l["out"] * c * l["k"] ** 2 + l["out"]
+        elif l["kind"] == "subconv":
+            g = _lget(l, "groups", 1)
+            o += g * ((l["out"] // g) * (c // g) * l["k"] ** 2 + l["out"] // g)
+        elif l["kind"] == "dense":
+            o += l["out"] * _shape_size(shape) + l["out"]
+        shape = _apply_layer(shape, l, "shape inference")
+    return o
+
+
+def compose_group(model, weights, idxs, group, n_groups, shape):
+    """compose_run (proj/src/netcompile.cpp:225-278): the affine map (M, b)
+    of one linear run restricted to channel group `group` of `n_groups`"""
+    c, d = shape[0] // n_groups, shape[1]
+    M, b = None, None
+
+    def fold(A, bias):
+        nonlocal M, b
+        if M is None:
+            M, b = A, np.asarray(bias, dtype=np.float64)
+        else:
+            M, b = A @ M, A @ b + bias
+
+    for i in idxs:
+        l, w = model["layers"][i], weights[i]
+        if l["kind"] in ("conv", "subconv"):
+            W, bias = w[group] if l["kind"] == "subconv" else w
+            cs = ConvShape(d, c, l["k"], _lget(l, "s", 1), np.asarray(W).shape[0])
+            fold(conv_to_matrix(cs, W), conv_bias_vector(cs, bias))
+            c, d = cs.c_out, cs.d_out()
+        elif l["kind"] == "avgpool":
+            s = _lget(l, "s", 1)
+            d_out = (d - l["k"]) // s + 1
+            fold(pool_to_matrix(c, d, l["k"], s), np.zeros(c * d_out * d_out))
+            d = d_out
+        elif l["kind"] == "dense":
+            fold(np.asarray(w[0], dtype=np.float64), np.asarray(w[1], dtype=np.float64))
+        elif l["kind"] != "flatten":
+            raise ShapeError("non-linear layer inside a fused run")
+    if M is None:
+        raise ShapeError("empty linear run")
+    return M, b
+
+
+def execute_program(model, weights, image, ctx, stages=None):
+    """proj/src/netcompile.cpp:291-446.  weights as split_model_weights
+    returns them.  Returns the logits."""
+    stages = lower(model) if stages is None else stages
+    layers, N = model["layers"], model["n_slots"]
+    image = np.asarray(image, dtype=np.float64)
+    shape = (model["in_c"], model["in_d"], False, 0)
+    cts, maps, seeded = [], False, False
+    for st in stages:
+        ctx.begin_stage(st["label"])
+        if not seeded and st["kind"] != "convpack":
+            if _shape_size(shape) > N:
+                raise CapacityError(f"input of {_shape_size(shape)} values exceeds n_slots")
+            cts, seeded = [pack(image.ravel(), N, CIPHERTEXT)], True
+        kind = st["kind"]
+        if kind == "convpack":
+            l = layers[st["layer_idx"][0]]
+            cs = ConvShape(shape[1], shape[0], l["k"], _lget(l, "s", 1), l["out"])
+            W, b = weights[st["layer_idx"][0]]
+            cts = conv_packed_forward(conv_pack(image, cs, N), W, b, cs, ctx)
+            maps, seeded = True, True
+            shape = _apply_layer(shape, l, st["label"])
+        elif kind == "merge":
+            G = st["groups"]
+            per, w = shape[0] // G, shape[1] * shape[1]
+            cts = [merge_maps(cts[g * per:(g + 1) * per], w, ctx) for g in range(G)]
+            maps = False
+        elif kind == "square":
+            cts = [square_layer(ct, ctx) for ct in cts]
+        elif kind == "repackconv":
+            l = layers[st["layer_idx"][0]]
+            if l["k"] != 1:
+                raise ShapeError(st["label"] + ": only 1x1 convolutions support the packed rotation lowering")
+            w = shape[1] * shape[1]
+            if maps:
+                taps = cts
+            else:
+                G = len(cts)
+                per = shape[0] // G
+                taps = [rotate_left(cts[g], j * w, ctx) for g in range(G) for j in range(per)]
+            cs = ConvShape(shape[1], shape[0], 1, 1, l["out"])
+            W, b = weights[st["layer_idx"][0]]
+            cts = conv_packed_forward(taps, W, b, cs, ctx)
+            maps = True
+            shape = _apply_layer(shape, l, st["label"])
+        else:  # linear
+            G = st["groups"]
+            if len(cts) != G:
+                raise ShapeError(f"{st['label']}: expected {G} input ciphertexts, have {len(cts)}")
+            outs = []
+            for g in range(G):
+                M, bias = compose_group(model, weights, st["layer_idx"], g, G, shape)
+                if st["policy"] == "hs":
+                    out = hs_matvec(M, cts[g], ctx)
+                elif st["policy"] == "lola_dense":
+                    out = merge_maps(lola_dense_matvec(M, cts[g], ctx), 1, ctx)
+                elif st["policy"] == "lola_stacked":
+                    res, slot_of_row = lola_stacked_matvec(M, cts[g], ctx)
+                    v = np.zeros(N)
+                    v[:M.shape[0]] = res.slots[np.asarray(slot_of_row)]  # value-level de-interleave (free)
+                    out = SlotVector(v, CIPHERTEXT)
+                else:
+                    raise ShapeError(st["label"] + ": ConvPack is not a matrix-vector kernel")
+                out = add(out, pack(bias, N, PLAINTEXT), ctx)
+                outs.append(out.masked_prefix(M.shape[0]))
+            cts, maps = outs, False
+            for r in st["layer_idx"]:
+                shape = _apply_layer(shape, layers[r], st["label"])
+    if len(cts) != 1:
+        raise ShapeError("program must end in a single output ciphertext")
+    return cts[0].slots[:_shape_size(shape)].copy()
+
+
+def ref_forward_model(model, weights, image):
+    """ref_forward (proj/src/netcompile.cpp:448-503) over a general layer
+    list including SubConv groups"""
+    t = np.asarray(image, dtype=np.float64)
+    for l, w in zip(model["layers"], weights):
+        kind = l["kind"]
+        if kind == "conv":
+            t = ref_conv(t, w[0], w[1], _lget(l, "s", 1))
+        elif kind == "subconv":
+            g = _lget(l, "groups", 1)
+            per = t.shape[0] // g
+            t = np.concatenate([ref_conv(t[i * per:(i + 1) * per], w[i][0], w[i][1], _lget(l, "s", 1))
+                                for i in range(g)])
+        elif kind == "avgpool":
+            t = ref_avgpool(t, l["k"], _lget(l, "s", 1))
+        elif kind == "square":
+            t = ref_square(t)
+        elif kind == "flatten":
+            t = t.ravel()
+        elif kind == "dense":
+            t = ref_dense(np.ravel(t), w[0], w[1])
+    return np.ravel(t)
+
+
+def _L(kind, k=0, s=1, out=0, groups=1, policy=None, label=""):
+    return dict(kind=kind, k=k, s=s, out=out, groups=groups, policy=policy, label=label)
+
+
+def builtin_model(name):
+    """proj/src/netcompile.cpp:567-635"""
+    if name == "cryptonets-hs":
+        return dict(name=name, in_c=1, in_d=29, n_slots=8192, layers=[
+            _L("conv", 5, 2, 5, label="Conv1"), _L("square"), _L("avgpool", 2, 2),
+            _L("conv", 5, 1, 50, label="Conv2"), _L("avgpool", 2, 2), _L("flatten"),
+            _L("dense", out=100, label="Dense1"), _L("square"), _L("dense", out=10, label="Dense2")])
+    if name == "me":
+        return dict(name=name, in_c=1, in_d=30, n_slots=8192, layers=[
+            _L("conv", 3, 1, 5, label="Conv1"), _L("square"), _L("avgpool", 3, 2),
+            _L("conv", 3, 1, 50, label="Conv2"), _L("avgpool", 3, 2), _L("flatten"),
+            _L("dense", out=32, label="Dense1"), _L("square"), _L("dense", out=10, label="Dense2")])
+    if name == "ce":
+        return dict(name=name, in_c=3, in_d=32, n_slots=16384, layers=[
+            _L("conv", 3, 1, 18, label="Conv1"), _L("square"), _L("avgpool", 2, 2, label="Pool1"),
+            _L("subconv", 3, 1, 15, 3, label="Conv2"), _L("conv", 1, 1, 64, policy="convpack", label="Conv3"),
+            _L("square"), _L("avgpool", 2, 2, label="Pool2"), _L("conv", 3, 1, 64), _L("flatten"),
+            _L("dense", out=256, label="Dense1"), _L("square"), _L("dense", out=10, label="Dense2")])
+    return None

@@ -25,7 +25,8 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-I", os.path.join(ROOT, "include"),
 
 
 # translation units that #include another .cu (rebuild when it changes)
-INCLUDED_SOURCES = {"ntt_r8.cu": ["ntt.cu"], "ntt_fp16.cu": ["ntt.cu"], "ntt_fp8.cu": ["ntt.cu"]}
+INCLUDED_SOURCES = {"ntt_r8.cu": ["ntt.cu"], "ntt_fp16.cu": ["ntt.cu"], "ntt_fp8.cu": ["ntt.cu"],
+                    "ntt_fp16n.cu": ["ntt.cu"]}
 
 
 def sources():

@@ -259,6 +259,7 @@ void drop_last_limb_r16(Context& c, int B, const DropArgs& a, u64d* tmpP);
 HEGPU_NTT_DECL(_fp16)
 HEGPU_NTT_DECL(_fp8)
 #undef HEGPU_NTT_DECL
+void drop_last_limb_fp16n(Context& c, int B, const DropArgs& a, u64d* tmpP);  // ntt_fp16n.cu
 
 // pointwise (eval.cu)
 void launch_add(Context& c, const u64d* a, const u64d* b, u64d* out, int count, int l);

@@ -587,7 +587,16 @@ __device__ __forceinline__ void cp_async16_g2s(u64d* dst, const u64d* src) {
 // shared words of the drop-limb kernel: the NTT buffer, then the source limb
 // and the add term of the epilogue (prefetched during the transform)
 // (N <= 2^13: the prefetch buffers fit next to the transform buffer)
-__host__ __device__ constexpr bool drop_prefetch(int N) { return N <= 8192; }
+#ifndef HEGPU_DROP_PRE
+#define HEGPU_DROP_PRE 1
+#endif
+__host__ __device__ constexpr bool drop_prefetch(int N) { return HEGPU_DROP_PRE && N <= 8192; }
+// without the shared-memory staging (two CTAs per SM): pull the epilogue's
+// rows towards L2 while the transform runs
+__device__ __forceinline__ void prefetch_row_l2(const u64d* row, int N) {
+  for (int i = threadIdx.x * 16; i < N; i += blockDim.x * 16)
+    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(row + i));
+}
 __host__ __device__ constexpr size_t drop_smem_words(int N) {
   return ((size_t)(N + (N >> 4) + 1 + 1) & ~(size_t)1) + (drop_prefetch(N) ? 2 * (size_t)N : 0);
 }
@@ -622,6 +631,9 @@ __global__ void NTT_BOUNDS k_drop_ntt(TwArgs ta, PrimeTable pt, const u64d* __re
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     in_s = is;
     ad_s = as;
+  } else {
+    prefetch_row_l2(in, N);
+    if (add) prefetch_row_l2(ad, N);
   }
   fwd_t<LOGN>(sm, LdLift{tmpP + ((size_t)b * 2 + p) * N, pr, qd, (qd >> 1) >= q}, ta, t, q);
   const u64d iv = qinv[((size_t)t * np_all + a.pd) * 2], ivp = qinv[((size_t)t * np_all + a.pd) * 2 + 1];
@@ -727,6 +739,9 @@ __global__ void NTT_BOUNDS k_md_ntt(TwArgs ta, PrimeTable pt, const u64d* __rest
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     in_s = is;
     ad_s = as;
+  } else {
+    prefetch_row_l2(in, N);
+    if (add) prefetch_row_l2(ad, N);
   }
   const u64d pv = qinv[((size_t)t * np_all + a.pd) * 2], pvp = qinv[((size_t)t * np_all + a.pd) * 2 + 1];
   const u64d qv = qinv[((size_t)t * np_all + lq) * 2], qvp = qinv[((size_t)t * np_all + lq) * 2 + 1];
@@ -878,11 +893,13 @@ void upload_twiddles(Context& c) {
 
 #endif  // !HEGPU_NTT_R8_VARIANT
 
+#ifndef HEGPU_NTT_ONLY_DROP
 void NTT_PUB(launch_ntt_rows)(Context& c, const u64d* src, u64d* dst, int rows, int nl, int p_limb) {
   if (rows <= 0) return;
   const double _ntt_bytes = 16.0 * c.N() * rows;  // read + write one limb per row
   NTT_DISPATCH(c.P->log_n, k_ntt_rows, rows, tw_args(c), c.primes, src, dst, nl, p_limb, c.L());
 }
+#endif
 
 void NTT_PUB(launch_intt_rows)(Context& c, const u64d* src, u64d* dst, int n_outer, int n_inner, long so, long si,
                                long dox, long di, const int* prime_of_inner) {
@@ -914,6 +931,7 @@ void launch_slot_to_wire(Context& c, const u64d* src, u64d* dst, size_t rows, in
 
 #endif  // !HEGPU_NTT_R8_VARIANT
 
+#ifndef HEGPU_NTT_ONLY_DROP
 void NTT_PUB(ks_modup)(Context& c, const u64d* src, long src_stride, int B, int l, const KeyRowMap* shifts,
                        u64d* tmp, u64d* D) {
   KeyRowMap dummy{};
@@ -924,6 +942,7 @@ void NTT_PUB(ks_modup)(Context& c, const u64d* src, long src_stride, int B, int 
   _ntt_bytes = 16.0 * c.N() * B * l * l;
   if (B * l * l > 0) NTT_DISPATCH(c.P->log_n, k_ks_modup, B * l * l, tw_args(c), c.primes, tmp, l, c.L(), D);
 }
+#endif
 
 void NTT_PUB(drop_last_limb)(Context& c, int B, const DropArgs& a, u64d* tmpP) {
   const int N = c.N();
@@ -1000,9 +1019,10 @@ void NTT_PUB(drop_last_limb)(Context& c, int B, const DropArgs& a, u64d* tmpP) {
 // HEGPU_NTT_FPV=<ntt><intt><modup><md> digits (1 = 16 words, 0 = 8 words)
 // overrides the FP64-only choice for A/B measurements.  Measured (cfg 2,
 // profiles/r02_notes.md): the 16-word FP64-only build is fastest for the row
-// transforms, ModUp and the fused ModDown + rescale; the plain drop-limb
-// kernel (rescale / ModDown alone) stays on the dual-path 8-word build,
-// whose integer epilogue fits 64 registers without spills.
+// transforms and ModUp; the drop-limb kernels (rescale / ModDown, and the
+// fused ModDown + rescale) run the 16-word build WITHOUT the shared-memory
+// staging of their epilogue operands (ntt_fp16n.cu): 69 KB per CTA keeps two
+// CTAs per SM, where the staged kernels (200 KB) ran one.
 static bool fpv16(int entry, bool dflt) {
   const char* e = getenv("HEGPU_NTT_FPV");
   if (!e || (int)strlen(e) <= entry) return dflt;
@@ -1029,12 +1049,25 @@ void ks_modup(Context& c, const u64d* src, long src_stride, int B, int l, const 
   else if (ntt_all_r8()) ks_modup_r8(c, src, src_stride, B, l, shifts, tmp, D);
   else ks_modup_r16(c, src, src_stride, B, l, shifts, tmp, D);
 }
+// HEGPU_DROP_V=<md><plain>: 0 = r8 dual-path, 1 = fp16 (smem-staged epilogue), 2 = fp16n (no staging;
+// default: two CTAs per SM beat the staged epilogue, cfg 2 drop 0.46 -> 0.40 ms, md_ntt 0.23 -> 0.21 ms)
+static int dropv(int entry, int dflt) {
+  const char* e = getenv("HEGPU_DROP_V");
+  if (!e || (int)strlen(e) <= entry) return dflt;
+  return e[entry] - '0';
+}
 void drop_last_limb(Context& c, int B, const DropArgs& a, u64d* tmpP) {
   c.ks[a.pd == c.L() ? KS_MODDOWN : KS_RESCALE] += B;
   if (a.fuse_rescale) c.ks[KS_RESCALE] += B;
-  if (c.fp_all && a.fuse_rescale && c.P->log_n <= 13 && !fpv16(3, true)) drop_last_limb_fp8(c, B, a, tmpP);
-  else if (c.fp_all && a.fuse_rescale) drop_last_limb_fp16(c, B, a, tmpP);
-  else drop_last_limb_r8(c, B, a, tmpP);
+  if (c.fp_all) {
+    const int v = dropv(a.fuse_rescale ? 0 : 1, 2);
+    if (v == 2) return drop_last_limb_fp16n(c, B, a, tmpP);
+    if (v == 1) {
+      if (a.fuse_rescale && c.P->log_n <= 13 && !fpv16(3, true)) return drop_last_limb_fp8(c, B, a, tmpP);
+      return drop_last_limb_fp16(c, B, a, tmpP);
+    }
+  }
+  drop_last_limb_r8(c, B, a, tmpP);
 }
 #endif
 
