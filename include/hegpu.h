@@ -156,6 +156,14 @@ int hegpu_ct_download(hegpu_ct* ct, uint64_t* host, size_t nwords);
 /* upload `count` compact ciphertexts (hegpu_encrypt_compact) back to back */
 int hegpu_ct_upload_compact(hegpu_ct* ct, const uint8_t* host, size_t nbytes, double scale);
 int hegpu_ct_info(const hegpu_ct* ct, int* count, int* level, double* scale);
+/* a non-owning handle on ciphertexts [first, first + count) of `src` (the
+ * reference slices std::vector<SlotVector>, proj/src/netcompile.cpp:338-342);
+ * valid while `src` lives, released with hegpu_ct_destroy */
+int hegpu_ct_view(hegpu_ct* src, int first, int count, hegpu_ct** out);
+/* device copy between handles of equal count and level (value semantics of
+ * SlotVector assignment) */
+int hegpu_ct_copy(hegpu_ct* dst, const hegpu_ct* src);
+int hegpu_ct_set_scale(hegpu_ct* ct, double scale);
 int hegpu_pt_create(hegpu_ctx* ctx, int count, int level, int with_p, hegpu_pt** out);
 void hegpu_pt_destroy(hegpu_pt* pt);
 int hegpu_pt_upload(hegpu_pt* pt, const uint64_t* host, size_t nwords, double scale);
@@ -349,7 +357,8 @@ int hegpu_model_save_input(hegpu_model* model, const char* path, const double* x
  * (conv / avgpool / flatten / dense), each run's affine map composed on the
  * host (conv_to_matrix, pool_to_matrix, dense; FP64) into one HS layer
  * labelled by its joined layer labels.  HEGPU_ERR_SHAPE outside this family
- * (SubConv groups, RepackConv, LoLa policies).  _net_spec gives the shapes;
+ * (SubConv groups, RepackConv, LoLa policies: those run through hegpu_prog
+ * below).  _net_spec gives the shapes;
  * _compose the composed M (rows x cols, row-major; may be NULL to query the
  * size) and bias b of linear stage `stage` from a flat weights stream. */
 int hegpu_model_net_spec(const hegpu_model* model, hegpu_net_spec* spec);
@@ -359,6 +368,51 @@ int hegpu_net_create_from_model(hegpu_ctx* ctx, hegpu_model* model, const char* 
 /* logits: decrypt + decode output ct (wire) into m_last values */
 int hegpu_net_decrypt_logits(hegpu_net* net, const uint64_t* out_ct, double* logits);
 double hegpu_net_output_scale(const hegpu_net* net);
+
+/* ---- the general stage driver: lower() + execute() for every stage kind ----
+ * (proj/src/netcompile.cpp:106-213 lower, :291-446 execute): ConvPack,
+ * Merge into `groups` ciphertexts, Square, RepackConv (a stand-alone 1x1
+ * conv-pack conv on rotated group ciphertexts, :352-379) and Linear runs
+ * per channel group (SubConv, :380-434) under the HS or LoLa-dense policy;
+ * a model without a first conv-pack conv is seeded with one dense input
+ * ciphertext (:309-319).  One image per run; every stage executes the
+ * C-ABI operators above (conv_plan_run, merge_maps, square, rotate_left,
+ * mul_plain/add/add_plain/rescale with the reference's masked constants,
+ * hs_matvec, lola_matvec) under hegpu_begin_stage(label), so the per-stage
+ * HOP report is the reference's.  LoLa-stacked stages are rejected
+ * (HEGPU_ERR_SHAPE): the reference de-interleaves their result on cleartext
+ * values (:409-417), which has no homomorphic counterpart.
+ * Levels: the context's chain must hold 1 + (primes consumed) limbs:
+ * ConvPack, RepackConv, Square and Linear(HS) consume one prime each,
+ * Linear(LoLa-dense) two (HEGPU_ERR_CAPACITY otherwise); the model's
+ * n_slots must equal the context's slot count. */
+typedef struct hegpu_prog hegpu_prog;
+enum {
+  HEGPU_STAGE_CONVPACK = 0, HEGPU_STAGE_MERGE = 1, HEGPU_STAGE_SQUARE = 2, HEGPU_STAGE_REPACKCONV = 3,
+  HEGPU_STAGE_LINEAR = 4
+};
+/* weights: the flat stream of hegpu_model_load_weights (count values) */
+int hegpu_prog_create(hegpu_ctx* ctx, const hegpu_model* model, const double* weights, size_t count,
+                      hegpu_prog** out);
+void hegpu_prog_destroy(hegpu_prog* prog);
+/* stages, input ciphertexts per image (k^2 c_in conv_pack taps, or 1), the
+ * output level and the number of logits */
+int hegpu_prog_info(const hegpu_prog* prog, int* n_stages, int* input_cts, int* out_level, int* n_logits);
+int hegpu_prog_stage(const hegpu_prog* prog, int i, char* label, int label_len, int* kind, int* groups,
+                     int* policy);
+/* lower() alone (no context): the stage list of a model; label/kind/groups/
+ * policy arrays of capacity cap, returns the stage count or a negative error */
+int hegpu_model_lower(const hegpu_model* model, int cap, char (*labels)[64], int* kinds, int* groups,
+                      int* policies);
+/* client: conv_pack (or the dense input vector) -> encode + encrypt at the
+ * top level; input_cts wire ciphertexts, nonces nonce * input_cts + t */
+int hegpu_prog_encrypt_input(hegpu_prog* prog, const double* image, uint64_t nonce, uint64_t* cts_out);
+/* input: input_cts ciphertexts at the top level; out: 1 ciphertext at out_level */
+int hegpu_prog_run(hegpu_prog* prog, hegpu_ct* input, hegpu_ct* out);
+int hegpu_prog_decrypt_logits(hegpu_prog* prog, const uint64_t* out_ct, double* logits);
+double hegpu_prog_output_scale(const hegpu_prog* prog);
+/* prog == NULL: the last hegpu_prog_create / hegpu_model_lower error of this thread */
+const char* hegpu_prog_last_error(const hegpu_prog* prog);
 
 #ifdef __cplusplus
 }

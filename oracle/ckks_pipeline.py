@@ -337,3 +337,109 @@ def lola_stacked(ck, v, level, A, keys=None):
             g = ck.galois_right(b)
             res = ck.add(res, ck.rotate(u, l2, g, _key(ck, keys, g)), l2)
     return res, slot_of_row
+
+
+# ------------------------------------------------ general stage driver ---
+def repack_conv(ck, taps, level, scale, W, bias, w_used):
+    """conv_packed_forward (proj/src/convlower.cpp:39-74) on ciphertexts whose
+    slots beyond w_used are NOT zero (the RepackConv stage's rotated group
+    ciphertexts, netcompile.cpp:352-379): the reference's masked constant
+    plaintexts pt(w[co,t] on slots < w) at scale q_{level-1}, products summed
+    in tap order, the masked bias at the product scale, one rescale per map."""
+    W = np.asarray(W, dtype=np.float64).reshape(np.asarray(W).shape[0], -1)
+    c_out, ntaps = W.shape
+    qlast = float(ck.primes[level - 1])
+    outs = []
+    for co in range(c_out):
+        acc = None
+        for t in range(ntaps):
+            term = ck.mul_pc(taps[t], ck.encode(np.full(w_used, W[co, t]), qlast, level), level)
+            acc = term if acc is None else ck.add(acc, term, level)
+        acc = ck.add_pc(acc, ck.encode(np.full(w_used, bias[co]), scale * qlast, level), level)
+        outs.append(ck.rescale(acc, level))
+    return outs
+
+
+def run_program(ck, model, weights, image, nonce=0, keys=None):
+    """The reference's execute (proj/src/netcompile.cpp:291-446) over CKKS,
+    stage for stage as hegpu_prog_run evaluates it (csrc/program.cpp):
+    returns (output ct, level, scale, n_logits).  Levels: ConvPack,
+    RepackConv, Square and Linear(HS) consume one prime, Linear(LoLa-dense)
+    two; input scale 2^40 at the top level."""
+    stages = HS.lower(model)
+    layers, S = model["layers"], ck.S
+    if model["n_slots"] != S:
+        raise HS.ShapeError("model n_slots must equal the ring's slot count")
+    keys = keys if keys is not None else {}
+    image = np.asarray(image, dtype=np.float64)
+    scale, l = 2.0 ** 40, ck.L
+    shape = (model["in_c"], model["in_d"], False, 0)
+    cts, maps, seeded, rlk = [], False, False, None
+    for st in stages:
+        kind = st["kind"]
+        if not seeded and kind != "convpack":
+            cts, seeded = [ck.encrypt(ck.encode(image.ravel(), scale, l), l, nonce)], True
+        if kind == "convpack":
+            ly = layers[st["layer_idx"][0]]
+            cs = HS.ConvShape(shape[1], shape[0], ly["k"], ly.get("s") or 1, ly["out"])
+            taps = HS.conv_pack(image, cs, S)
+            w_used, ntaps = cs.d_out() ** 2, len(taps)
+            enc = np.concatenate([ck.encrypt(ck.encode(t.slots[:w_used], scale, l), l, nonce * ntaps + i)
+                                  for i, t in enumerate(taps)])
+            W, b = weights[st["layer_idx"][0]]
+            out = conv_layer(ck, enc, ntaps, l, np.asarray(W).reshape(ly["out"], -1), b, w_used, scale)
+            l -= 1
+            per = 2 * l * ck.N
+            cts = [out[i * per:(i + 1) * per] for i in range(ly["out"])]
+            maps, seeded = True, True
+            shape = HS._apply_layer(shape, ly, st["label"])
+        elif kind == "merge":
+            G = st["groups"]
+            per, w = shape[0] // G, shape[1] * shape[1]
+            cts = [merge(ck, np.concatenate(cts[g * per:(g + 1) * per]), per, l, w, keys) for g in range(G)]
+            maps = False
+        elif kind == "square":
+            rlk = rlk if rlk is not None else ck.relin_key()
+            cts = [square(ck, v, l, rlk) for v in cts]
+            scale = scale * scale / float(ck.primes[l - 1])
+            l -= 1
+        elif kind == "repackconv":
+            ly = layers[st["layer_idx"][0]]
+            w = shape[1] * shape[1]
+            if maps:
+                taps = cts
+            else:
+                G = len(cts)
+                per = shape[0] // G
+                taps = []
+                for g in range(G):
+                    for j in range(per):
+                        if j == 0:
+                            taps.append(cts[g])
+                        else:
+                            gl = ck.galois_left(j * w)
+                            taps.append(ck.rotate(cts[g], l, gl, _key(ck, keys, gl)))
+            W, b = weights[st["layer_idx"][0]]
+            cts = repack_conv(ck, taps, l, scale, W, b, w)
+            l -= 1
+            maps = True
+            shape = HS._apply_layer(shape, ly, st["label"])
+        else:  # linear
+            G = st["groups"]
+            outs = []
+            for g in range(G):
+                M, bias = HS.compose_group(model, weights, st["layer_idx"], g, G, shape)
+                if st["policy"] == "hs":
+                    u, lo = hs_matvec(ck, cts[g], l, M, True, keys), l - 1
+                elif st["policy"] == "lola-dense":
+                    rows = lola_dense(ck, cts[g], l, M, keys)
+                    u, lo = merge(ck, rows, M.shape[0], l - 2, 1, keys), l - 2
+                else:
+                    raise HS.ShapeError(st["label"] + ": policy outside the encrypted stage driver")
+                outs.append(ck.add_pc(u, ck.encode(bias, scale, lo), lo))
+            cts, maps, l = outs, False, lo
+            for r in st["layer_idx"]:
+                shape = HS._apply_layer(shape, layers[r], st["label"])
+    if len(cts) != 1:
+        raise HS.ShapeError("program must end in a single output ciphertext")
+    return cts[0], l, scale, HS._shape_size(shape)

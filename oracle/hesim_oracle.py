@@ -653,7 +653,7 @@ def golden_stage_tallies(spec):
 # the stand-alone ConvPack repack and the LoLa policies), restated from
 # proj/src/netcompile.cpp:14-446.  Layers are dicts {kind, k, s, out, groups,
 # policy, label} (kind in conv / subconv / avgpool / square / flatten /
-# dense; policy None or convpack / hs / lola_dense / lola_stacked).
+# dense; policy None or convpack / hs / lola-dense / lola-stacked).
 _LINEAR = ("conv", "subconv", "avgpool", "flatten", "dense")
 
 
@@ -927,9 +927,9 @@ def execute_program(model, weights, image, ctx, stages=None):
                 M, bias = compose_group(model, weights, st["layer_idx"], g, G, shape)
                 if st["policy"] == "hs":
                     out = hs_matvec(M, cts[g], ctx)
-                elif st["policy"] == "lola_dense":
+                elif st["policy"] == "lola-dense":
                     out = merge_maps(lola_dense_matvec(M, cts[g], ctx), 1, ctx)
-                elif st["policy"] == "lola_stacked":
+                elif st["policy"] == "lola-stacked":
                     res, slot_of_row = lola_stacked_matvec(M, cts[g], ctx)
                     v = np.zeros(N)
                     v[:M.shape[0]] = res.slots[np.asarray(slot_of_row)]  # value-level de-interleave (free)
@@ -993,3 +993,26 @@ def builtin_model(name):
             _L("square"), _L("avgpool", 2, 2, label="Pool2"), _L("conv", 3, 1, 64), _L("flatten"),
             _L("dense", out=256, label="Dense1"), _L("square"), _L("dense", out=10, label="Dense2")])
     return None
+
+
+def model_json(model):
+    """the model as a model file (proj/src/modelio.cpp:106-147 schema)"""
+    import json
+    layers = []
+    for l in model["layers"]:
+        d = {"kind": l["kind"]}
+        if l["kind"] in ("conv", "subconv", "avgpool"):
+            d["k"], d["s"] = l["k"], l.get("s") or 1
+        if l["kind"] in ("conv", "subconv"):
+            d["out_channels"] = l["out"]
+        if l["kind"] == "dense":
+            d["units"] = l["out"]
+        if l["kind"] == "subconv":
+            d["groups"] = l.get("groups") or 1
+        if l.get("policy"):
+            d["policy"] = l["policy"]
+        if l.get("label"):
+            d["label"] = l["label"]
+        layers.append(d)
+    return json.dumps({"name": model["name"], "input": [model["in_c"], model["in_d"], model["in_d"]],
+                       "n_slots": model["n_slots"], "layers": layers})

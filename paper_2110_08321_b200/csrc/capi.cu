@@ -429,10 +429,45 @@ extern "C" int hegpu_ct_create(hegpu_ctx* h, int count, int level, hegpu_ct** ou
 
 extern "C" void hegpu_ct_destroy(hegpu_ct* t) {
   if (!t) return;
+  if (t->view) {
+    delete t;
+    return;
+  }
   try { bind_device(t->b.ctx); } catch (...) {}
   cudaStreamSynchronize(t->b.ctx->stream);
   cudaFree(t->b.d);
   delete t;
+}
+
+extern "C" int hegpu_ct_view(hegpu_ct* src, int first, int count, hegpu_ct** out) {
+  if (!src || !out) return HEGPU_ERR_ARG;
+  Context& c = *src->b.ctx;
+  return guarded(&c, [&] {
+    need(first >= 0 && count >= 1 && first + count <= src->b.count, HEGPU_ERR_RANGE,
+         "ct_view: range outside the source batch");
+    auto* t = new hegpu_ct{CtBatch{&c, count, src->b.level, src->b.scale, src->b.d + (size_t)first * src->b.stride()}};
+    t->view = true;
+    *out = t;
+  });
+}
+
+extern "C" int hegpu_ct_copy(hegpu_ct* dst, const hegpu_ct* src) {
+  if (!dst || !src) return HEGPU_ERR_ARG;
+  Context& c = *src->b.ctx;
+  return guarded(&c, [&] {
+    need(dst->b.ctx == src->b.ctx, HEGPU_ERR_ARG, "ct_copy: handles from different contexts");
+    need(dst->b.count == src->b.count && dst->b.level == src->b.level, HEGPU_ERR_SHAPE,
+         "ct_copy: count/level mismatch");
+    if (dst->b.d != src->b.d)
+      CK(cudaMemcpyAsync(dst->b.d, src->b.d, src->b.words() * 8, cudaMemcpyDeviceToDevice, c.stream));
+    dst->b.scale = src->b.scale;
+  });
+}
+
+extern "C" int hegpu_ct_set_scale(hegpu_ct* t, double scale) {
+  if (!t || !(scale > 0)) return HEGPU_ERR_ARG;
+  t->b.scale = scale;
+  return HEGPU_OK;
 }
 
 extern "C" int hegpu_ct_upload(hegpu_ct* t, const uint64_t* host, size_t nwords, double scale) {

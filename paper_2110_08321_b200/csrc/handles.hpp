@@ -7,6 +7,7 @@ struct hegpu_ctx {
 };
 struct hegpu_ct {
   hegpu::CtBatch b;
+  bool view = false;  // hegpu_ct_view: aliases another handle's device memory (not freed here)
 };
 struct hegpu_pt {
   hegpu::PtBatch b;

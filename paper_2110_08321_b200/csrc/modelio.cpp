@@ -215,9 +215,6 @@ bool exists(const std::string& p) {
 
 }  // namespace
 
-struct hegpu_model : ModelDesc {
-  std::string last_error;
-};
 
 namespace {
 

@@ -176,6 +176,19 @@ def lib():
             "hegpu_net_tap_cts": (i, [vp]),
             "hegpu_net_first_layer": (i, [vp]),
             "hegpu_net_wait": (i, [vp]),
+            "hegpu_ct_view": (i, [vp, i, i, pp]),
+            "hegpu_ct_copy": (i, [vp, vp]),
+            "hegpu_ct_set_scale": (i, [vp, d]),
+            "hegpu_prog_create": (i, [vp, vp, f64p, sz, pp]),
+            "hegpu_prog_destroy": (None, [vp]),
+            "hegpu_prog_info": (i, [vp] + [C.POINTER(i)] * 4),
+            "hegpu_prog_stage": (i, [vp, i, C.c_char_p, i] + [C.POINTER(i)] * 3),
+            "hegpu_model_lower": (i, [vp, i, vp, vp, vp, vp]),
+            "hegpu_prog_encrypt_input": (i, [vp, f64p, u, u64p]),
+            "hegpu_prog_run": (i, [vp, vp, vp]),
+            "hegpu_prog_decrypt_logits": (i, [vp, u64p, f64p]),
+            "hegpu_prog_output_scale": (d, [vp]),
+            "hegpu_prog_last_error": (C.c_char_p, [vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -705,10 +718,84 @@ class Model:
         self._check(lib().hegpu_model_compose(self.h, w, w.size, stage, M.ctypes.data, b.ctypes.data, None, None))
         return M, b
 
+    def lower(self):
+        """lower() (proj/src/netcompile.cpp:106-213): the stage list as dicts
+        {label, kind, groups, policy}"""
+        cap = 64
+        labels = (C.c_char * 64 * cap)()
+        kinds, groups, pols = (C.c_int * cap)(), (C.c_int * cap)(), (C.c_int * cap)()
+        n = lib().hegpu_model_lower(self.h, cap, labels, kinds, groups, pols)
+        if n < 0:
+            msg = lib().hegpu_prog_last_error(None)
+            raise _ERR.get(-n, HegpuError)(-n, msg.decode() if msg else "")
+        return [{"label": labels[k].value.decode(), "kind": STAGE_KINDS[kinds[k]], "groups": groups[k],
+                 "policy": POLICIES[pols[k]]} for k in range(n)]
+
     def net_spec(self):
         spec = NetSpec()
         self._status(lib().hegpu_model_net_spec(self.h, C.byref(spec)), None)
         return spec
+
+
+STAGE_KINDS = ("convpack", "merge", "square", "repackconv", "linear")
+
+
+class Program:
+    """The general stage driver (hegpu_prog, csrc/program.cpp): lower() +
+    execute() (proj/src/netcompile.cpp:106-213, 291-446) with SubConv groups,
+    grouped merges, RepackConv and the HS / LoLa-dense policies."""
+
+    def __init__(self, ctx, model, weights):
+        self.ctx, self.model = ctx, model
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        h = C.c_void_p()
+        rc = lib().hegpu_prog_create(ctx.h, model.h, w, w.size, C.byref(h))
+        if rc:
+            msg = lib().hegpu_prog_last_error(None)
+            raise _ERR.get(rc, HegpuError)(rc, msg.decode() if msg else "")
+        self.h = h
+        v = [C.c_int() for _ in range(4)]
+        self._check(lib().hegpu_prog_info(h, *[C.byref(x) for x in v]))
+        self.n_stages, self.input_cts, self.out_level, self.n_logits = (x.value for x in v)
+        self.top = ctx.L
+        self.stages = []
+        for k in range(self.n_stages):
+            buf = C.create_string_buffer(64)
+            kind, groups, pol = C.c_int(), C.c_int(), C.c_int()
+            self._check(lib().hegpu_prog_stage(h, k, buf, 64, C.byref(kind), C.byref(groups), C.byref(pol)))
+            self.stages.append({"label": buf.value.decode(), "kind": STAGE_KINDS[kind.value],
+                                "groups": groups.value, "policy": POLICIES[pol.value]})
+
+    def _check(self, rc):
+        if rc:
+            msg = lib().hegpu_prog_last_error(self.h)
+            raise _ERR.get(rc, HegpuError)(rc, msg.decode() if msg else "")
+
+    @property
+    def out_scale(self):
+        return lib().hegpu_prog_output_scale(self.h)
+
+    def encrypt_input(self, image, nonce):
+        x = np.ascontiguousarray(image, dtype=np.float64).ravel()
+        out = np.empty(self.input_cts * 2 * self.top * self.ctx.N, dtype=np.uint64)
+        self._check(lib().hegpu_prog_encrypt_input(self.h, x, nonce, out))
+        return out
+
+    def run(self, input_ct, out_ct):
+        self._check(lib().hegpu_prog_run(self.h, input_ct.h, out_ct.h))
+
+    def decrypt_logits(self, out_ct_words):
+        w = np.ascontiguousarray(out_ct_words, dtype=np.uint64)
+        out = np.empty(self.n_logits, dtype=np.float64)
+        self._check(lib().hegpu_prog_decrypt_logits(self.h, w, out))
+        return out
+
+    def __del__(self):
+        try:
+            if _ctx_alive(self) and getattr(self, "h", None):
+                lib().hegpu_prog_destroy(self.h)
+        except Exception:
+            pass
 
 
 SPLIT_FIRST_LAYER = -1  # hegpu_net_run_split: split Conv1 + Flat1 by output map
