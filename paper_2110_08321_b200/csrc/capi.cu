@@ -105,7 +105,7 @@ extern "C" int hegpu_ctx_create(const hegpu_params* p, int device, hegpu_ctx** o
     c.hp = *p;
     c.P = std::make_unique<Params>(*p);
     need(c.P->np() <= HEGPU_MAX_PRIMES, HEGPU_ERR_ARG, "too many primes");
-    need(c.P->n <= 16384, HEGPU_ERR_ARG, "ring degree above 2^14 is not supported by the smem NTT");
+    need(c.P->n <= 32768, HEGPU_ERR_ARG, "ring degree above 2^15 is not supported by the smem NTT");
     c.client = std::make_unique<Client>(*c.P);
     c.device = device;
     if (device == HEGPU_CLIENT_ONLY) return;  // data-owner side: no device state

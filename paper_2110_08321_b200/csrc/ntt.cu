@@ -18,6 +18,8 @@
 //             and the store finishes (x - X) * q_d^{-1} (+ add term);
 //   inverse : key-switch loads apply the Galois shift and emit the shifted
 //             own-prime limb for ModUp; stores multiply by N^{-1}.
+#include <cooperative_groups.h>
+
 #include "engine.hpp"
 
 namespace hegpu {
@@ -31,7 +33,33 @@ namespace {
 #define HEGPU_NTT_LR13 4
 #endif
 __host__ __device__ constexpr int lr_of(int logn) { return logn <= 13 ? HEGPU_NTT_LR13 : 4; }
-constexpr int kMinLogN = 5, kMaxLogN = 14;
+constexpr int kMinLogN = 5, kMaxLogN = 15;
+// N = 2^15 (FP64-only builds): one row is split over the two CTAs of a
+// thread-block cluster, each transforming 2^14 words in its own shared
+// memory.  Forward: both CTAs read the whole row, apply the first
+// Cooley-Tukey stage while loading (CTA h keeps a + (-1)^h w b) and run the
+// remaining 14 stages as an independent sub-transform whose twiddles are
+// the full table's, indexed (2 + h) 2^s + i; its outputs are exactly slot
+// positions [h S, (h + 1) S) (params.cpp: p < S <-> exponent = 1 mod 4 <->
+// bit-reversed index < N / 2).  Inverse: 14 Gentleman-Sande stages per CTA,
+// then the last stage pairs the two halves through distributed shared
+// memory (cluster.map_shared_rank).
+__host__ __device__ constexpr int sub_logn(int logn) { return logn > 14 ? 14 : logn; }
+template <int LOGN>
+struct RowCta {  // which row, which half of it, and the half's first position / index
+  static constexpr int NT = 1 << sub_logn(LOGN);
+  int r, h, base;
+  __device__ __forceinline__ RowCta() {
+    if constexpr (LOGN > 14) {
+      r = (int)(blockIdx.x >> 1);
+      h = (int)(blockIdx.x & 1);
+    } else {
+      r = (int)blockIdx.x;
+      h = 0;
+    }
+    base = h * NT;
+  }
+};
 
 __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
 
@@ -276,7 +304,8 @@ __device__ __forceinline__ u64d fp_canon(double v, double2 fq) {  // -> [0, q) a
 }
 
 template <int LOGN, int S0, int RR>
-__device__ __forceinline__ void fwd_pass_fp(double (&x)[1 << lr_of(LOGN)], const double* __restrict__ tw, double2 fq) {
+__device__ __forceinline__ void fwd_pass_fp(double (&x)[1 << lr_of(LOGN)], const double* __restrict__ tw, double2 fq,
+                                            const int pre = 1) {
   constexpr int T = (1 << LOGN) / (1 << lr_of(LOGN)), G = (1 << lr_of(LOGN)) >> RR, J = 1 << RR, LOB = LOGN - S0 - RR;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -287,7 +316,7 @@ __device__ __forceinline__ void fwd_pass_fp(double (&x)[1 << lr_of(LOGN)], const
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         if (j & half) continue;
-        const double W = __ldg(tw + (1 << (S0 + u)) + (hi << u) + (j >> (RR - u)));
+        const double W = __ldg(tw + (pre << (S0 + u)) + (hi << u) + (j >> (RR - u)));
         const double a = x[g * J + j];
         const double t = fp_mulmod(x[g * J + j + half], W, fq);
         x[g * J + j] = __dadd_rn(a, t);
@@ -313,16 +342,17 @@ __device__ __forceinline__ void fwd_load_d(const double* sm, double (&x)[1 << lr
 }
 
 template <int LOGN, int S0>
-__device__ __forceinline__ void fwd_passes_fp(double (&x)[1 << lr_of(LOGN)], u64d* sm, const double* tw, double2 fq) {
+__device__ __forceinline__ void fwd_passes_fp(double (&x)[1 << lr_of(LOGN)], u64d* sm, const double* tw, double2 fq,
+                                              const int pre = 1) {
   constexpr int RR = cmin(lr_of(LOGN), LOGN - S0);
-  fwd_pass_fp<LOGN, S0, RR>(x, tw, fq);
+  fwd_pass_fp<LOGN, S0, RR>(x, tw, fq, pre);
   if constexpr (S0 + RR < LOGN) {
     constexpr int RN = cmin(lr_of(LOGN), LOGN - S0 - RR);
     fwd_store_d<LOGN, S0, RR>(reinterpret_cast<double*>(sm), x);
     __syncthreads();
     fwd_load_d<LOGN, S0 + RR, RN>(reinterpret_cast<const double*>(sm), x);
     __syncthreads();
-    fwd_passes_fp<LOGN, S0 + RR>(x, sm, tw, fq);
+    fwd_passes_fp<LOGN, S0 + RR>(x, sm, tw, fq, pre);
   } else {
 #pragma unroll
     for (int g = 0; g < ((1 << lr_of(LOGN)) >> RR); ++g)
@@ -343,8 +373,27 @@ __device__ __forceinline__ void fwd_transform_fp(u64d* sm, const Ld& ld, const d
   fwd_passes_fp<LOGN, 0>(x, sm, tw, fq);
 }
 
+// N = 2^15: half h of the row.  `tw` is the full 2^15 table; values stay
+// below 16 q < 2^49 over the 15 stages.
+template <class Ld>
+__device__ __forceinline__ void fwd_transform_fp_split(u64d* sm, const Ld& ld, const double* tw, double2 fq, int h) {
+  constexpr int LS = 14, R = 1 << lr_of(LS), NH = 1 << LS;
+  static_assert(lr_of(LS) <= LS, "one group per thread in the first pass");
+  double x[R];
+  const double w1 = __ldg(tw + 1);
+#pragma unroll
+  for (int e = 0; e < R; ++e) {
+    const int k = fwd_idx<LS, 0, lr_of(LS)>(0, e);
+    const double a = u2d(ld.load(k));
+    const double t = fp_mulmod(u2d(ld.load(k + NH)), w1, fq);
+    x[e] = __dadd_rn(a, h ? -t : t);
+  }
+  fwd_passes_fp<LS, 0>(x, sm, tw, fq, 2 + h);
+}
+
 template <int LOGN, int S0, int RR>
-__device__ __forceinline__ void inv_pass_fp(double (&x)[1 << lr_of(LOGN)], const double* __restrict__ tw, double2 fq) {
+__device__ __forceinline__ void inv_pass_fp(double (&x)[1 << lr_of(LOGN)], const double* __restrict__ tw, double2 fq,
+                                            const int pre = 1) {
   constexpr int T = (1 << LOGN) / (1 << lr_of(LOGN)), G = (1 << lr_of(LOGN)) >> RR, J = 1 << RR;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -355,7 +404,7 @@ __device__ __forceinline__ void inv_pass_fp(double (&x)[1 << lr_of(LOGN)], const
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         if (j & dist) continue;
-        const double W = __ldg(tw + (1 << (LOGN - S0 - u - 1)) + (hi << (RR - u - 1)) + (j >> (u + 1)));
+        const double W = __ldg(tw + (pre << (LOGN - S0 - u - 1)) + (hi << (RR - u - 1)) + (j >> (u + 1)));
         const double a = x[g * J + j], b = x[g * J + j + dist];
         x[g * J + j] = __dadd_rn(a, b);
         x[g * J + j + dist] = fp_mulmod(__dadd_rn(a, -b), W, fq);
@@ -382,18 +431,43 @@ __device__ __forceinline__ void inv_load_d(const double* sm, double (&x)[1 << lr
     for (int j = 0; j < (1 << RR); ++j) x[g * (1 << RR) + j] = sm[pad(inv_idx<LOGN, S0, RR>(g, j))];
 }
 
-template <int LOGN, int S0, class St>
+// SPLIT (N = 2^15): this CTA holds half h; after its 14 stages the last
+// Gentleman-Sande stage pairs coefficient k of the two halves through
+// distributed shared memory: out[k] = (a + b) / N, out[k + N/2] = (a - b) w / N.
+template <int LOGN, int S0, bool SPLIT = false, class St>
 __device__ __forceinline__ void inv_passes_fp(double (&x)[1 << lr_of(LOGN)], u64d* sm, const double* tw, double2 fq,
-                                              double nv, St& st) {
+                                              double nv, St& st, const int pre = 1, const int h = 0) {
   constexpr int RR = cmin(lr_of(LOGN), LOGN - S0);
-  inv_pass_fp<LOGN, S0, RR>(x, tw, fq);
+  inv_pass_fp<LOGN, S0, RR>(x, tw, fq, pre);
   if constexpr (S0 + RR < LOGN) {
     constexpr int RN = cmin(lr_of(LOGN), LOGN - S0 - RR);
     __syncthreads();
     inv_store_d<LOGN, S0, RR>(reinterpret_cast<double*>(sm), x);
     __syncthreads();
     inv_load_d<LOGN, S0 + RR, RN>(reinterpret_cast<const double*>(sm), x);
-    inv_passes_fp<LOGN, S0 + RR>(x, sm, tw, fq, nv, st);
+    inv_passes_fp<LOGN, S0 + RR, SPLIT>(x, sm, tw, fq, nv, st, pre, h);
+  } else if constexpr (SPLIT) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    constexpr int T = (1 << LOGN) / (1 << lr_of(LOGN)), R = 1 << lr_of(LOGN);
+    double* xs = reinterpret_cast<double*>(sm);
+    __syncthreads();  // every thread has loaded its last pass from sm
+#pragma unroll
+    for (int e = 0; e < R; ++e) xs[e * T + (int)threadIdx.x] = x[e];
+    cl.sync();
+    const double* other = cl.map_shared_rank(xs, (unsigned)(h ^ 1));
+    const double wl = __ldg(tw + 1);
+#pragma unroll
+    for (int g = 0; g < (R >> RR); ++g)
+#pragma unroll
+      for (int j = 0; j < (1 << RR); ++j) {
+        const int e = g * (1 << RR) + j;
+        const double o = other[e * T + (int)threadIdx.x];
+        const double v = h ? fp_mulmod(fp_mulmod(__dadd_rn(o, -x[e]), wl, fq), nv, fq)
+                           : fp_mulmod(__dadd_rn(x[e], o), nv, fq);
+        st.store(inv_idx<LOGN, S0, RR>(g, j) + h * (1 << LOGN), fp_canon(v, fq));
+      }
+    cl.sync();  // the partner has read this CTA's half
   } else {
 #pragma unroll
     for (int g = 0; g < ((1 << lr_of(LOGN)) >> RR); ++g)
@@ -413,6 +487,17 @@ __device__ __forceinline__ void inv_transform_fp(u64d* sm, St& st, const double*
 #pragma unroll
     for (int j = 0; j < (1 << R0); ++j) x[g * (1 << R0) + j] = u2d(sm[pad(inv_idx<LOGN, 0, R0>(g, j))]);
   inv_passes_fp<LOGN, 0>(x, sm, tw, fq, nv, st);
+}
+
+// N = 2^15: half h; input: this half's words scattered into smem (sub-index order), synced
+template <class St>
+__device__ __forceinline__ void inv_transform_fp_split(u64d* sm, St& st, const double* tw, double2 fq, double nv,
+                                                       int h) {
+  constexpr int LS = 14, R0 = lr_of(LS);
+  double x[1 << lr_of(LS)];
+#pragma unroll
+  for (int j = 0; j < (1 << R0); ++j) x[j] = u2d(sm[pad(inv_idx<LS, 0, R0>(0, j))]);
+  inv_passes_fp<LS, 0, true>(x, sm, tw, fq, nv, st, 2 + h, h);
 }
 
 // ------------------------------------------------------------ functors
@@ -459,8 +544,12 @@ __device__ __forceinline__ const ulonglong2* twi(const TwArgs& t, int pi, int N)
 // forward / inverse transform of prime pi on the FP64 path when the prime
 // allows it (q < 2^45), else on the integer path; same words either way
 template <int LOGN, class Ld>
-__device__ __forceinline__ void fwd_t(u64d* sm, const Ld& ld, const TwArgs& ta, int pi, u64d q) {
+__device__ __forceinline__ void fwd_t(u64d* sm, const Ld& ld, const TwArgs& ta, int pi, u64d q, int h = 0) {
   constexpr int N = 1 << LOGN;
+  if constexpr (LOGN > 14) {  // split over a CTA pair (FP64-only builds)
+    fwd_transform_fp_split(sm, ld, ta.twd + (size_t)pi * 2 * N, ta.fpq[pi], h);
+    return;
+  }
 #ifdef HEGPU_NTT_FPONLY  // every prime of the context is on the FP64 path (launcher checks)
   fwd_transform_fp<LOGN>(sm, ld, ta.twd + (size_t)pi * 2 * N, ta.fpq[pi]);
   return;
@@ -475,8 +564,12 @@ __device__ __forceinline__ void fwd_t(u64d* sm, const Ld& ld, const TwArgs& ta, 
   fwd_transform<LOGN>(sm, ld, twf(ta, pi, N), q);
 }
 template <int LOGN, class St>
-__device__ __forceinline__ void inv_t(u64d* sm, St& st, const TwArgs& ta, int pi, u64d q) {
+__device__ __forceinline__ void inv_t(u64d* sm, St& st, const TwArgs& ta, int pi, u64d q, int h = 0) {
   constexpr int N = 1 << LOGN;
+  if constexpr (LOGN > 14) {
+    inv_transform_fp_split(sm, st, ta.twd + ((size_t)pi * 2 + 1) * N, ta.fpq[pi], u2d(ta.ninv[2 * pi]), h);
+    return;
+  }
 #ifdef HEGPU_NTT_FPONLY
   inv_transform_fp<LOGN>(sm, st, ta.twd + ((size_t)pi * 2 + 1) * N, ta.fpq[pi], u2d(ta.ninv[2 * pi]));
   return;
@@ -496,25 +589,27 @@ __device__ __forceinline__ void inv_t(u64d* sm, St& st, const TwArgs& ta, int pi
 // drop-limb epilogue, costs spills in the other row kernels)
 #define ROW_LOOP(P)                                         \
   _Pragma("unroll") for (int _e = 0; _e < (1 << lr_of(LOGN)); ++_e) \
-    if (const int P = _e * (N >> lr_of(LOGN)) + (int)threadIdx.x; true)
+    if (const int P = rc.base + _e * (RowCta<LOGN>::NT >> lr_of(LOGN)) + (int)threadIdx.x; true)
 
 // two CTAs per SM for N <= 8192 (<= 64 registers per thread)
 #ifndef HEGPU_NTT_MINB13
 #define HEGPU_NTT_MINB13 2
 #endif
-#define NTT_BOUNDS __launch_bounds__((1 << LOGN) / (1 << lr_of(LOGN)), (LOGN <= 13 ? HEGPU_NTT_MINB13 : 1))
+#define NTT_BOUNDS __launch_bounds__((1 << sub_logn(LOGN)) / (1 << lr_of(LOGN)), (LOGN <= 13 ? HEGPU_NTT_MINB13 : 1))
 
 // ------------------------------------------------------------ kernels
 template <int LOGN>
 __global__ void NTT_BOUNDS k_ntt_rows(TwArgs ta, PrimeTable pt, const u64d* __restrict__ src,
                                       u64d* __restrict__ dst, int nl, int p_limb, int p_index) {
   extern __shared__ u64d sm[];
-  constexpr int N = 1 << LOGN;
-  const int r = blockIdx.x, limb = r % nl;
+  constexpr int N = 1 << LOGN, NT = RowCta<LOGN>::NT;
+  const RowCta<LOGN> rc;
+  const int r = rc.r, limb = r % nl;
   const int pi = (limb == p_limb) ? p_index : limb;
-  fwd_t<LOGN>(sm, LdPlain{src + (size_t)r * N}, ta, pi, pt.p[pi].q);
+  fwd_t<LOGN>(sm, LdPlain{src + (size_t)r * N}, ta, pi, pt.p[pi].q, rc.h);
   u64d* d = dst + (size_t)r * N;
-  for (int p = threadIdx.x; p < N; p += blockDim.x) d[p] = sm[pad(__ldg(ta.slot_src + p))];
+  for (int p = rc.base + threadIdx.x; p < rc.base + NT; p += blockDim.x)
+    d[p] = sm[pad((int)__ldg(ta.slot_src + p) - rc.base)];
 }
 
 struct PMap {
@@ -526,14 +621,16 @@ __global__ void NTT_BOUNDS k_intt_rows(TwArgs ta, PrimeTable pt, const u64d* __r
                                        u64d* __restrict__ dst, int n_inner, long so, long si, long dox, long di,
                                        PMap pm) {
   extern __shared__ u64d sm[];
-  constexpr int N = 1 << LOGN;
-  const int r = blockIdx.x, o = r / n_inner, i = r % n_inner;
+  constexpr int NT = RowCta<LOGN>::NT;
+  const RowCta<LOGN> rc;
+  const int r = rc.r, o = r / n_inner, i = r % n_inner;
   const int pi = pm.p[i];
   const u64d* s = src + o * so + i * si;
-  for (int p = threadIdx.x; p < N; p += blockDim.x) sm[pad(__ldg(ta.slot_src + p))] = s[p];
+  for (int p = rc.base + threadIdx.x; p < rc.base + NT; p += blockDim.x)
+    sm[pad((int)__ldg(ta.slot_src + p) - rc.base)] = s[p];
   __syncthreads();
   StPlain st{dst + o * dox + i * di};
-  inv_t<LOGN>(sm, st, ta, pi, pt.p[pi].q);
+  inv_t<LOGN>(sm, st, ta, pi, pt.p[pi].q, rc.h);
 }
 
 // KS input: digit j of (shifted) poly b -> coefficient row tmp[b][j]; also
@@ -542,20 +639,21 @@ template <int LOGN>
 __global__ void NTT_BOUNDS k_ks_intt(TwArgs ta, PrimeTable pt, const u64d* __restrict__ src, long src_stride, int l,
                                      KeyRowMap km, int use_shift, u64d* __restrict__ tmp, u64d* __restrict__ D) {
   extern __shared__ u64d sm[];
-  constexpr int N = 1 << LOGN, S = N >> 1;
-  const int r = blockIdx.x, b = r / l, j = r % l;
+  constexpr int N = 1 << LOGN, S = N >> 1, NT = RowCta<LOGN>::NT;
+  const RowCta<LOGN> rc;
+  const int r = rc.r, b = r / l, j = r % l;
   const int s = use_shift ? km.shift[b % km.period] : 0;
   const u64d* in = src + (km.grp ? (b / km.grp) * km.grp_stride + (b % km.grp) * src_stride : b * src_stride) +
                    (size_t)j * N;
   u64d* own = D + (((size_t)b * l + j) * (l + 1) + j) * N;
-  for (int p = threadIdx.x; p < N; p += blockDim.x) {
+  for (int p = rc.base + threadIdx.x; p < rc.base + NT; p += blockDim.x) {
     const u64d v = in[s ? shifted(p, s, S) : p];
     own[p] = v;
-    sm[pad(__ldg(ta.slot_src + p))] = v;
+    sm[pad((int)__ldg(ta.slot_src + p) - rc.base)] = v;
   }
   __syncthreads();
   StPlain st{tmp + ((size_t)b * l + j) * N};
-  inv_t<LOGN>(sm, st, ta, j, pt.p[j].q);
+  inv_t<LOGN>(sm, st, ta, j, pt.p[j].q, rc.h);
 }
 
 // ModUp: rows (b, j, t') with t = t' < j ? t' : t'+1 over the extended basis
@@ -564,8 +662,9 @@ template <int LOGN>
 __global__ void NTT_BOUNDS k_ks_modup(TwArgs ta, PrimeTable pt, const u64d* __restrict__ tmp, int l, int P_index,
                                       u64d* __restrict__ D) {
   extern __shared__ u64d sm[];
-  constexpr int N = 1 << LOGN;
-  const int r = blockIdx.x;
+  constexpr int N = 1 << LOGN, NT = RowCta<LOGN>::NT;
+  const RowCta<LOGN> rc;
+  const int r = rc.r;
   const int tp = r % l, bj = r / l, j = bj % l, b = bj / l;
   const int t = tp < j ? tp : tp + 1;
   const int pi = t == l ? P_index : t;
@@ -573,9 +672,10 @@ __global__ void NTT_BOUNDS k_ks_modup(TwArgs ta, PrimeTable pt, const u64d* __re
   // the FP64 path takes any word < 4q exactly: a digit of another prime
   // below 2^45 needs no reduction there (q_j < 2 q_t)
   const bool need = pt.p[j].q > pr.q && !(HEGPU_NTT_FP && ta.fpq[pi].x != 0.0 && pt.p[j].q < (1ull << 45));
-  fwd_t<LOGN>(sm, LdReduce{tmp + ((size_t)b * l + j) * N, pr, need}, ta, pi, pr.q);
+  fwd_t<LOGN>(sm, LdReduce{tmp + ((size_t)b * l + j) * N, pr, need}, ta, pi, pr.q, rc.h);
   u64d* d = D + (((size_t)b * l + j) * (l + 1) + t) * N;
-  for (int p = threadIdx.x; p < N; p += blockDim.x) d[p] = sm[pad(__ldg(ta.slot_src + p))];
+  for (int p = rc.base + threadIdx.x; p < rc.base + NT; p += blockDim.x)
+    d[p] = sm[pad((int)__ldg(ta.slot_src + p) - rc.base)];
 }
 
 __device__ __forceinline__ void cp_async16_g2s(u64d* dst, const u64d* src) {
@@ -609,7 +709,8 @@ __global__ void NTT_BOUNDS k_drop_ntt(TwArgs ta, PrimeTable pt, const u64d* __re
                                       DropArgs a, const u64d* __restrict__ tmpP, KeyRowMap km, int use_shift) {
   extern __shared__ u64d sm[];
   constexpr int N = 1 << LOGN, S = N >> 1;
-  const int r = blockIdx.x;
+  const RowCta<LOGN> rc;
+  const int r = rc.r;
   const int t = r % a.nl, bp = r / a.nl, p = bp % 2, b = bp / 2;
   const DevPrime pr = pt.p[t];
   const u64d q = pr.q;
@@ -635,7 +736,7 @@ __global__ void NTT_BOUNDS k_drop_ntt(TwArgs ta, PrimeTable pt, const u64d* __re
     prefetch_row_l2(in, N);
     if (add) prefetch_row_l2(ad, N);
   }
-  fwd_t<LOGN>(sm, LdLift{tmpP + ((size_t)b * 2 + p) * N, pr, qd, (qd >> 1) >= q}, ta, t, q);
+  fwd_t<LOGN>(sm, LdLift{tmpP + ((size_t)b * 2 + p) * N, pr, qd, (qd >> 1) >= q}, ta, t, q, rc.h);
   const u64d iv = qinv[((size_t)t * np_all + a.pd) * 2], ivp = qinv[((size_t)t * np_all + a.pd) * 2 + 1];
   const int sh = (use_shift && p == 0) ? km.shift[b % km.period] : 0;
   if constexpr (kPre) {
@@ -643,7 +744,7 @@ __global__ void NTT_BOUNDS k_drop_ntt(TwArgs ta, PrimeTable pt, const u64d* __re
     __syncthreads();
   }
   ROW_LOOP(pos) {
-    u64d v = shoup_mul_d(sub_mod_d(in_s[pos], sm[pad(__ldg(ta.slot_src + pos))], q), iv, ivp, q);
+    u64d v = shoup_mul_d(sub_mod_d(in_s[pos], sm[pad((int)__ldg(ta.slot_src + pos) - rc.base)], q), iv, ivp, q);
     if (add) v = add_mod_d(v, ad_s[sh ? shifted(pos, sh, S) : pos], q);
     out[pos] = v;
   }
@@ -665,8 +766,9 @@ template <int LOGN>
 __global__ void NTT_BOUNDS k_md_intt(TwArgs ta, PrimeTable pt, const u64d* __restrict__ qinv, int np_all, DropArgs a,
                                      u64d* __restrict__ xz) {
   extern __shared__ u64d sm[];
-  constexpr int N = 1 << LOGN;
-  const int r = blockIdx.x, which = r & 1, bp = r >> 1, p = bp & 1, b = bp >> 1;
+  constexpr int N = 1 << LOGN, NT = RowCta<LOGN>::NT;
+  const RowCta<LOGN> rc;
+  const int r = rc.r, which = r & 1, bp = r >> 1, p = bp & 1, b = bp >> 1;
   const int lq = a.src_limbs - 2;          // limb (and prime index) of q_{l-1}
   const int pi = which ? lq : a.pd;        // a.pd: prime index of P
   const u64d* row = a.src + b * a.src_b + p * a.src_p + (size_t)(which ? lq : a.src_limbs - 1) * N;
@@ -675,17 +777,18 @@ __global__ void NTT_BOUNDS k_md_intt(TwArgs ta, PrimeTable pt, const u64d* __res
     const u64d iv = qinv[((size_t)lq * np_all + a.pd) * 2], ivp = qinv[((size_t)lq * np_all + a.pd) * 2 + 1];
     const bool add = (a.add_mask >> p) & 1;
     const u64d* ad = add ? a.add + b * a.add_b + p * a.add_p + (size_t)lq * N : nullptr;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    for (int i = rc.base + threadIdx.x; i < rc.base + NT; i += blockDim.x) {
       u64d v = shoup_mul_d(row[i], iv, ivp, q);
       if (add) v = add_mod_d(v, ad[i], q);
-      sm[pad(__ldg(ta.slot_src + i))] = v;
+      sm[pad((int)__ldg(ta.slot_src + i) - rc.base)] = v;
     }
   } else {
-    for (int i = threadIdx.x; i < N; i += blockDim.x) sm[pad(__ldg(ta.slot_src + i))] = row[i];
+    for (int i = rc.base + threadIdx.x; i < rc.base + NT; i += blockDim.x)
+      sm[pad((int)__ldg(ta.slot_src + i) - rc.base)] = row[i];
   }
   __syncthreads();
   StPlain st{xz + ((size_t)bp * 2 + which) * N};
-  inv_t<LOGN>(sm, st, ta, pi, pt.p[pi].q);
+  inv_t<LOGN>(sm, st, ta, pi, pt.p[pi].q, rc.h);
 }
 
 // centered lift of a residue mod m (< m) times a constant c (Shoup pair), mod q
@@ -717,7 +820,8 @@ __global__ void NTT_BOUNDS k_md_ntt(TwArgs ta, PrimeTable pt, const u64d* __rest
                                     const u64d* __restrict__ xz) {
   extern __shared__ u64d sm[];
   constexpr int N = 1 << LOGN;
-  const int r = blockIdx.x;
+  const RowCta<LOGN> rc;
+  const int r = rc.r;
   const int t = r % a.nl, bp = r / a.nl, p = bp % 2, b = bp / 2;
   const int lq = a.src_limbs - 2;
   const DevPrime pr = pt.p[t];
@@ -748,7 +852,7 @@ __global__ void NTT_BOUNDS k_md_ntt(TwArgs ta, PrimeTable pt, const u64d* __rest
   const u64d* X = xz + (size_t)bp * 2 * N;
   LdMd ld{X, X + N, pt.p[a.pd].q, pt.p[lq].q, q, pv, pvp,
           qinv[((size_t)lq * np_all + a.pd) * 2], qinv[((size_t)lq * np_all + a.pd) * 2 + 1], pr.one_sh};
-  fwd_t<LOGN>(sm, ld, ta, t, q);
+  fwd_t<LOGN>(sm, ld, ta, t, q, rc.h);
   if constexpr (kPre) {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
@@ -756,7 +860,7 @@ __global__ void NTT_BOUNDS k_md_ntt(TwArgs ta, PrimeTable pt, const u64d* __rest
   ROW_LOOP(pos) {
     u64d v = shoup_mul_d(in_s[pos], pv, pvp, q);
     if (add) v = add_mod_d(v, ad_s[pos], q);
-    out[pos] = shoup_mul_d(sub_mod_d(v, sm[pad(__ldg(ta.slot_src + pos))], q), qv, qvp, q);
+    out[pos] = shoup_mul_d(sub_mod_d(v, sm[pad((int)__ldg(ta.slot_src + pos) - rc.base)], q), qv, qvp, q);
   }
 }
 
@@ -800,6 +904,38 @@ void prep_kernel(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
+// <<<grid, threads>>> for N <= 2^14; N = 2^15 launches two CTAs per row as
+// a thread-block cluster (the inverse kernels exchange halves through DSMEM)
+template <typename... KA, typename... A>
+void launch_rows(void (*kernel)(KA...), int lg, int grid, size_t smb, cudaStream_t st, A&&... args) {
+  const int threads = (1 << sub_logn(lg)) >> lr_of(lg);
+  if (lg <= 14) {
+    kernel<<<grid, threads, smb, st>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2u * (unsigned)grid);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smb;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kernel, KA(args)...));
+}
+
+// N = 2^15 exists in the 16-word FP64-only builds only (every prime < 2^45)
+#if defined(HEGPU_NTT_FPONLY) && HEGPU_NTT_LR13 == 4
+#define NTT_GO15(KERNEL, GRID, ...) NTT_GO(15, KERNEL, GRID, __VA_ARGS__)
+#else
+#define NTT_GO15(KERNEL, GRID, ...) \
+  fail(HEGPU_ERR_ARG, "N = 2^15 runs on the FP64 NTT only: every prime of the chain must be below 2^45")
+#endif
+
 // one launch per op, dispatched on log2 N
 #define NTT_DISPATCH(logn, KERNEL, GRID, ...)                                                       \
   do {                                                                                              \
@@ -814,17 +950,18 @@ void prep_kernel(K kernel, size_t bytes) {
       case 12: NTT_GO(12, KERNEL, GRID, __VA_ARGS__); break;                                        \
       case 13: NTT_GO(13, KERNEL, GRID, __VA_ARGS__); break;                                        \
       case 14: NTT_GO(14, KERNEL, GRID, __VA_ARGS__); break;                                        \
-      default: fail(HEGPU_ERR_ARG, "NTT: log2 N must be in [5, 14] on the device");                \
+      case 15: NTT_GO15(KERNEL, GRID, __VA_ARGS__); break;                                          \
+      default: fail(HEGPU_ERR_ARG, "NTT: log2 N must be in [5, 15] on the device");                \
     }                                                                                               \
   } while (0)
 
 #define NTT_GO(LG, KERNEL, GRID, ...)                                                               \
   do {                                                                                              \
     static PerDeviceOnce prepared;                                                                  \
-    const size_t smb = ntt_smem(1 << LG);                                                           \
+    const size_t smb = ntt_smem(1 << sub_logn(LG));                                                 \
     if (prepared.first()) prep_kernel(KERNEL<LG>, smb);                                             \
     LAUNCH_BO(c, #KERNEL, _ntt_bytes, (double)(GRID) * (LG << (LG - 1)),                           \
-              KERNEL<LG><<<(GRID), (1 << LG) >> lr_of(LG), smb, c.stream>>>(__VA_ARGS__));          \
+              launch_rows(KERNEL<LG>, LG, (GRID), smb, c.stream, __VA_ARGS__));                     \
   } while (0)
 
 }  // namespace
@@ -858,7 +995,7 @@ static bool ntt_all_r8() {
 void upload_twiddles(Context& c) {
   const Params& P = *c.P;
   const int np = P.np(), N = P.n;
-  if (P.log_n < kMinLogN || P.log_n > kMaxLogN) fail(HEGPU_ERR_ARG, "device NTT supports 2^5 <= N <= 2^14");
+  if (P.log_n < kMinLogN || P.log_n > kMaxLogN) fail(HEGPU_ERR_ARG, "device NTT supports 2^5 <= N <= 2^15");
   std::vector<u64> tw((size_t)np * 2 * N * 2);
   for (int i = 0; i < np; ++i) {
     const Prime& pr = P.primes[i];
@@ -887,6 +1024,8 @@ void upload_twiddles(Context& c) {
   CK(cudaMemcpy(c.d_twd, twd.data(), twd.size() * 8, cudaMemcpyHostToDevice));
   c.fp_all = true;
   for (int i = 0; i < np; ++i) c.fp_all = c.fp_all && fpq[2 * i] != 0.0;
+  if (P.log_n > 14 && !c.fp_all)
+    fail(HEGPU_ERR_ARG, "N = 2^15 runs on the FP64 NTT only: every prime of the chain must be below 2^45");
   CK(cudaMalloc((void**)&c.d_fpq, fpq.size() * 8));
   CK(cudaMemcpy(c.d_fpq, fpq.data(), fpq.size() * 8, cudaMemcpyHostToDevice));
 }
@@ -961,20 +1100,20 @@ void NTT_PUB(drop_last_limb)(Context& c, int B, const DropArgs& a, u64d* tmpP) {
 #define NTT_GO(LG, KERNEL, GRID, ...)                                                               \
   do {                                                                                              \
     static PerDeviceOnce prepared;                                                                  \
-    const size_t smb = drop_smem_words(1 << LG) * 8;                                                \
+    const size_t smb = drop_smem_words(1 << sub_logn(LG)) * 8;                                      \
     if (prepared.first()) prep_kernel(KERNEL<LG>, smb);                                             \
     LAUNCH_BO(c, #KERNEL, _ntt_bytes, (double)(GRID) * (LG << (LG - 1)),                           \
-              KERNEL<LG><<<(GRID), (1 << LG) >> lr_of(LG), smb, c.stream>>>(__VA_ARGS__));          \
+              launch_rows(KERNEL<LG>, LG, (GRID), smb, c.stream, __VA_ARGS__));                     \
   } while (0)
       NTT_DISPATCH(c.P->log_n, k_md_ntt, B * 2 * a.nl, tw_args(c), c.primes, c.qinv_tab(), c.P->np(), a, xz);
 #undef NTT_GO
 #define NTT_GO(LG, KERNEL, GRID, ...)                                                               \
   do {                                                                                              \
     static PerDeviceOnce prepared;                                                                  \
-    const size_t smb = ntt_smem(1 << LG);                                                           \
+    const size_t smb = ntt_smem(1 << sub_logn(LG));                                                 \
     if (prepared.first()) prep_kernel(KERNEL<LG>, smb);                                             \
     LAUNCH_BO(c, #KERNEL, _ntt_bytes, (double)(GRID) * (LG << (LG - 1)),                           \
-              KERNEL<LG><<<(GRID), (1 << LG) >> lr_of(LG), smb, c.stream>>>(__VA_ARGS__));          \
+              launch_rows(KERNEL<LG>, LG, (GRID), smb, c.stream, __VA_ARGS__));                     \
   } while (0)
     }
     c.free(xz);
@@ -992,10 +1131,10 @@ void NTT_PUB(drop_last_limb)(Context& c, int B, const DropArgs& a, u64d* tmpP) {
 #define NTT_GO(LG, KERNEL, GRID, ...)                                                               \
   do {                                                                                              \
     static PerDeviceOnce prepared;                                                                  \
-    const size_t smb = drop_smem_words(1 << LG) * 8;                                                \
+    const size_t smb = drop_smem_words(1 << sub_logn(LG)) * 8;                                      \
     if (prepared.first()) prep_kernel(KERNEL<LG>, smb);                                             \
     LAUNCH_BO(c, #KERNEL, _ntt_bytes, (double)(GRID) * (LG << (LG - 1)),                           \
-              KERNEL<LG><<<(GRID), (1 << LG) >> lr_of(LG), smb, c.stream>>>(__VA_ARGS__));          \
+              launch_rows(KERNEL<LG>, LG, (GRID), smb, c.stream, __VA_ARGS__));                     \
   } while (0)
   NTT_DISPATCH(c.P->log_n, k_drop_ntt, B * 2 * a.nl, tw_args(c), c.primes, c.qinv_tab(), c.P->np(), a, tmpP,
                a.shifts ? *a.shifts : dummy, a.shifts != nullptr);
@@ -1003,10 +1142,10 @@ void NTT_PUB(drop_last_limb)(Context& c, int B, const DropArgs& a, u64d* tmpP) {
 #define NTT_GO(LG, KERNEL, GRID, ...)                                                               \
   do {                                                                                              \
     static PerDeviceOnce prepared;                                                                  \
-    const size_t smb = ntt_smem(1 << LG);                                                           \
+    const size_t smb = ntt_smem(1 << sub_logn(LG));                                                 \
     if (prepared.first()) prep_kernel(KERNEL<LG>, smb);                                             \
     LAUNCH_BO(c, #KERNEL, _ntt_bytes, (double)(GRID) * (LG << (LG - 1)),                           \
-              KERNEL<LG><<<(GRID), (1 << LG) >> lr_of(LG), smb, c.stream>>>(__VA_ARGS__));          \
+              launch_rows(KERNEL<LG>, LG, (GRID), smb, c.stream, __VA_ARGS__));                     \
   } while (0)
 }
 

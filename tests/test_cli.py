@@ -73,6 +73,34 @@ def test_run_count_verify_on_gpu(tmp_path):
 
 
 @pytest.mark.gpu
+def test_run_grouped_model_through_the_general_driver(tmp_path):
+    """a model with SubConv groups and a stand-alone conv-pack repack (ce's
+    stage list, scaled down) runs through hegpu_prog: logits, stage labels
+    and the per-stage HOP rows of the reference's execute"""
+    from test_program import CE_MINI, _weights
+    (tmp_path / "m.json").write_text(HS.model_json(CE_MINI))
+    m = H.Model.parse(HS.model_json(CE_MINI))
+    flat, img = _weights(CE_MINI, 11)
+    m.save_weights(tmp_path / "w.bin", flat)
+    m.save_input(tmp_path / "x.bin", img)
+    r = cli("run", "--model", str(tmp_path / "m.json"), "--weights", str(tmp_path / "w.bin"),
+            "--input", str(tmp_path / "x.bin"), "--report", str(tmp_path / "r.csv"))
+    assert r.returncode == 0, r.stderr
+    logits = np.array([float(l.split(",")[2]) for l in r.stdout.splitlines() if l.startswith("logit,")])
+    w = HS.split_model_weights(CE_MINI, flat)
+    assert np.abs(logits - HS.ref_forward_model(CE_MINI, w, img)).max() < 1e-3
+    mc = HS.MeterContext()
+    HS.execute_program(CE_MINI, w, img, mc)
+    rows = [l.split(",") for l in (tmp_path / "r.csv").read_text().splitlines()[1:]]
+    assert [(r[0], tuple(int(v) for v in r[2:])) for r in rows[:-1]] == \
+        [(lab, (t.add_pc, t.add_cc, t.mul_pc, t.mul_cc, t.rot)) for lab, t in mc.stages]
+    c = cli("count", "--model", "ce-mini", "--seed", "3")
+    assert c.returncode == 0, c.stderr
+    assert "Pool1-Conv2" in c.stdout and "Conv3" in c.stdout
+    assert cli("count", "--model", "ce").returncode == 2  # N = 2^15: CapacityError
+
+
+@pytest.mark.gpu
 def test_verify_negative_control_exits_3():
     """--corrupt-kernel perturbs the expected A x, so verify must report FAIL
     and exit 3 (proj/tools/hesim.cpp:212,237,334-337;
