@@ -45,19 +45,41 @@ constexpr int kMinLogN = 5, kMaxLogN = 15;
 // then the last stage pairs the two halves through distributed shared
 // memory (cluster.map_shared_rank).
 __host__ __device__ constexpr int sub_logn(int logn) { return logn > 14 ? 14 : logn; }
+// HEGPU_NTT_PRIME_MAJOR=1 launches the rows prime-major (the prime index from
+// the slow part of the launch index, so co-resident CTAs share one 64 KB
+// twiddle table in L1).  Measured on cfg 2: no gain (3.134 vs 3.116 ms per
+// step; the digit re-reads spread over the launch cost what the table hits
+// save), so rows stay row-major (profiles/r02_notes.md).
+#ifndef HEGPU_NTT_PRIME_MAJOR
+#define HEGPU_NTT_PRIME_MAJOR 0
+#endif
 template <int LOGN>
 struct RowCta {  // which row, which half of it, and the half's first position / index
   static constexpr int NT = 1 << sub_logn(LOGN);
-  int r, h, base;
+  int r, h, base, rows;
   __device__ __forceinline__ RowCta() {
     if constexpr (LOGN > 14) {
       r = (int)(blockIdx.x >> 1);
       h = (int)(blockIdx.x & 1);
+      rows = (int)(gridDim.x >> 1);
     } else {
       r = (int)blockIdx.x;
       h = 0;
+      rows = (int)gridDim.x;
     }
     base = h * NT;
+  }
+  // split the launch index into (outer, fast) with `nfast` values of the fast
+  // (prime) part: row-major outer * nfast + fast, or prime-major
+  __device__ __forceinline__ int split(int nfast, int& fast) const {
+#if HEGPU_NTT_PRIME_MAJOR
+    const int nouter = rows / nfast;
+    fast = r / nouter;
+    return r - fast * nouter;
+#else
+    fast = r % nfast;
+    return r / nfast;
+#endif
   }
 };
 
@@ -604,7 +626,8 @@ __global__ void NTT_BOUNDS k_ntt_rows(TwArgs ta, PrimeTable pt, const u64d* __re
   extern __shared__ u64d sm[];
   constexpr int N = 1 << LOGN, NT = RowCta<LOGN>::NT;
   const RowCta<LOGN> rc;
-  const int r = rc.r, limb = r % nl;
+  int limb;
+  const int r = rc.split(nl, limb) * nl + limb;
   const int pi = (limb == p_limb) ? p_index : limb;
   fwd_t<LOGN>(sm, LdPlain{src + (size_t)r * N}, ta, pi, pt.p[pi].q, rc.h);
   u64d* d = dst + (size_t)r * N;
@@ -623,7 +646,8 @@ __global__ void NTT_BOUNDS k_intt_rows(TwArgs ta, PrimeTable pt, const u64d* __r
   extern __shared__ u64d sm[];
   constexpr int NT = RowCta<LOGN>::NT;
   const RowCta<LOGN> rc;
-  const int r = rc.r, o = r / n_inner, i = r % n_inner;
+  int i;
+  const int o = rc.split(n_inner, i);
   const int pi = pm.p[i];
   const u64d* s = src + o * so + i * si;
   for (int p = rc.base + threadIdx.x; p < rc.base + NT; p += blockDim.x)
@@ -641,7 +665,8 @@ __global__ void NTT_BOUNDS k_ks_intt(TwArgs ta, PrimeTable pt, const u64d* __res
   extern __shared__ u64d sm[];
   constexpr int N = 1 << LOGN, S = N >> 1, NT = RowCta<LOGN>::NT;
   const RowCta<LOGN> rc;
-  const int r = rc.r, b = r / l, j = r % l;
+  int j;
+  const int b = rc.split(l, j);
   const int s = use_shift ? km.shift[b % km.period] : 0;
   const u64d* in = src + (km.grp ? (b / km.grp) * km.grp_stride + (b % km.grp) * src_stride : b * src_stride) +
                    (size_t)j * N;
@@ -664,8 +689,8 @@ __global__ void NTT_BOUNDS k_ks_modup(TwArgs ta, PrimeTable pt, const u64d* __re
   extern __shared__ u64d sm[];
   constexpr int N = 1 << LOGN, NT = RowCta<LOGN>::NT;
   const RowCta<LOGN> rc;
-  const int r = rc.r;
-  const int tp = r % l, bj = r / l, j = bj % l, b = bj / l;
+  int tp;
+  const int bj = rc.split(l, tp), j = bj % l, b = bj / l;
   const int t = tp < j ? tp : tp + 1;
   const int pi = t == l ? P_index : t;
   const DevPrime pr = pt.p[pi];
@@ -710,8 +735,8 @@ __global__ void NTT_BOUNDS k_drop_ntt(TwArgs ta, PrimeTable pt, const u64d* __re
   extern __shared__ u64d sm[];
   constexpr int N = 1 << LOGN, S = N >> 1;
   const RowCta<LOGN> rc;
-  const int r = rc.r;
-  const int t = r % a.nl, bp = r / a.nl, p = bp % 2, b = bp / 2;
+  int t;
+  const int bp = rc.split(a.nl, t), p = bp % 2, b = bp / 2;
   const DevPrime pr = pt.p[t];
   const u64d q = pr.q;
   const u64d qd = pt.p[a.pd].q;
@@ -768,7 +793,8 @@ __global__ void NTT_BOUNDS k_md_intt(TwArgs ta, PrimeTable pt, const u64d* __res
   extern __shared__ u64d sm[];
   constexpr int N = 1 << LOGN, NT = RowCta<LOGN>::NT;
   const RowCta<LOGN> rc;
-  const int r = rc.r, which = r & 1, bp = r >> 1, p = bp & 1, b = bp >> 1;
+  int which;
+  const int bp = rc.split(2, which), p = bp & 1, b = bp >> 1;
   const int lq = a.src_limbs - 2;          // limb (and prime index) of q_{l-1}
   const int pi = which ? lq : a.pd;        // a.pd: prime index of P
   const u64d* row = a.src + b * a.src_b + p * a.src_p + (size_t)(which ? lq : a.src_limbs - 1) * N;
@@ -821,8 +847,8 @@ __global__ void NTT_BOUNDS k_md_ntt(TwArgs ta, PrimeTable pt, const u64d* __rest
   extern __shared__ u64d sm[];
   constexpr int N = 1 << LOGN;
   const RowCta<LOGN> rc;
-  const int r = rc.r;
-  const int t = r % a.nl, bp = r / a.nl, p = bp % 2, b = bp / 2;
+  int t;
+  const int bp = rc.split(a.nl, t), p = bp % 2, b = bp / 2;
   const int lq = a.src_limbs - 2;
   const DevPrime pr = pt.p[t];
   const u64d q = pr.q;
@@ -1035,6 +1061,7 @@ void upload_twiddles(Context& c) {
 #ifndef HEGPU_NTT_ONLY_DROP
 void NTT_PUB(launch_ntt_rows)(Context& c, const u64d* src, u64d* dst, int rows, int nl, int p_limb) {
   if (rows <= 0) return;
+  if (nl <= 0 || rows % nl) fail(HEGPU_ERR_ARG, "ntt_rows: the row count must be a multiple of the limb count");
   const double _ntt_bytes = 16.0 * c.N() * rows;  // read + write one limb per row
   NTT_DISPATCH(c.P->log_n, k_ntt_rows, rows, tw_args(c), c.primes, src, dst, nl, p_limb, c.L());
 }
