@@ -613,6 +613,20 @@ __device__ __forceinline__ void inv_t(u64d* sm, St& st, const TwArgs& ta, int pi
   _Pragma("unroll") for (int _e = 0; _e < (1 << lr_of(LOGN)); ++_e) \
     if (const int P = rc.base + _e * (RowCta<LOGN>::NT >> lr_of(LOGN)) + (int)threadIdx.x; true)
 
+// the slot-order gathers / scatters around a transform (index load -> shared
+// memory -> global).  HEGPU_NTT_UNROLL_IO=1 unrolls them fully (all R index
+// loads in flight at once); measured on cfg 2: ModUp 0.567 -> 0.591 ms, the
+// row INTTs 0.117 -> 0.109 ms, step 3.118 -> 3.138 ms -- not kept
+// (profiles/r02_notes.md)
+#ifndef HEGPU_NTT_UNROLL_IO
+#define HEGPU_NTT_UNROLL_IO 0
+#endif
+#if HEGPU_NTT_UNROLL_IO
+#define IO_LOOP(P) ROW_LOOP(P)
+#else
+#define IO_LOOP(P) for (int P = rc.base + threadIdx.x; P < rc.base + RowCta<LOGN>::NT; P += blockDim.x)
+#endif
+
 // two CTAs per SM for N <= 8192 (<= 64 registers per thread)
 #ifndef HEGPU_NTT_MINB13
 #define HEGPU_NTT_MINB13 2
@@ -631,8 +645,7 @@ __global__ void NTT_BOUNDS k_ntt_rows(TwArgs ta, PrimeTable pt, const u64d* __re
   const int pi = (limb == p_limb) ? p_index : limb;
   fwd_t<LOGN>(sm, LdPlain{src + (size_t)r * N}, ta, pi, pt.p[pi].q, rc.h);
   u64d* d = dst + (size_t)r * N;
-  for (int p = rc.base + threadIdx.x; p < rc.base + NT; p += blockDim.x)
-    d[p] = sm[pad((int)__ldg(ta.slot_src + p) - rc.base)];
+  IO_LOOP(p) d[p] = sm[pad((int)__ldg(ta.slot_src + p) - rc.base)];
 }
 
 struct PMap {
@@ -650,8 +663,7 @@ __global__ void NTT_BOUNDS k_intt_rows(TwArgs ta, PrimeTable pt, const u64d* __r
   const int o = rc.split(n_inner, i);
   const int pi = pm.p[i];
   const u64d* s = src + o * so + i * si;
-  for (int p = rc.base + threadIdx.x; p < rc.base + NT; p += blockDim.x)
-    sm[pad((int)__ldg(ta.slot_src + p) - rc.base)] = s[p];
+  IO_LOOP(p) sm[pad((int)__ldg(ta.slot_src + p) - rc.base)] = s[p];
   __syncthreads();
   StPlain st{dst + o * dox + i * di};
   inv_t<LOGN>(sm, st, ta, pi, pt.p[pi].q, rc.h);
@@ -671,7 +683,7 @@ __global__ void NTT_BOUNDS k_ks_intt(TwArgs ta, PrimeTable pt, const u64d* __res
   const u64d* in = src + (km.grp ? (b / km.grp) * km.grp_stride + (b % km.grp) * src_stride : b * src_stride) +
                    (size_t)j * N;
   u64d* own = D + (((size_t)b * l + j) * (l + 1) + j) * N;
-  for (int p = rc.base + threadIdx.x; p < rc.base + NT; p += blockDim.x) {
+  IO_LOOP(p) {
     const u64d v = in[s ? shifted(p, s, S) : p];
     own[p] = v;
     sm[pad((int)__ldg(ta.slot_src + p) - rc.base)] = v;
@@ -699,8 +711,7 @@ __global__ void NTT_BOUNDS k_ks_modup(TwArgs ta, PrimeTable pt, const u64d* __re
   const bool need = pt.p[j].q > pr.q && !(HEGPU_NTT_FP && ta.fpq[pi].x != 0.0 && pt.p[j].q < (1ull << 45));
   fwd_t<LOGN>(sm, LdReduce{tmp + ((size_t)b * l + j) * N, pr, need}, ta, pi, pr.q, rc.h);
   u64d* d = D + (((size_t)b * l + j) * (l + 1) + t) * N;
-  for (int p = rc.base + threadIdx.x; p < rc.base + NT; p += blockDim.x)
-    d[p] = sm[pad((int)__ldg(ta.slot_src + p) - rc.base)];
+  IO_LOOP(p) d[p] = sm[pad((int)__ldg(ta.slot_src + p) - rc.base)];
 }
 
 __device__ __forceinline__ void cp_async16_g2s(u64d* dst, const u64d* src) {
@@ -803,14 +814,13 @@ __global__ void NTT_BOUNDS k_md_intt(TwArgs ta, PrimeTable pt, const u64d* __res
     const u64d iv = qinv[((size_t)lq * np_all + a.pd) * 2], ivp = qinv[((size_t)lq * np_all + a.pd) * 2 + 1];
     const bool add = (a.add_mask >> p) & 1;
     const u64d* ad = add ? a.add + b * a.add_b + p * a.add_p + (size_t)lq * N : nullptr;
-    for (int i = rc.base + threadIdx.x; i < rc.base + NT; i += blockDim.x) {
+    IO_LOOP(i) {
       u64d v = shoup_mul_d(row[i], iv, ivp, q);
       if (add) v = add_mod_d(v, ad[i], q);
       sm[pad((int)__ldg(ta.slot_src + i) - rc.base)] = v;
     }
   } else {
-    for (int i = rc.base + threadIdx.x; i < rc.base + NT; i += blockDim.x)
-      sm[pad((int)__ldg(ta.slot_src + i) - rc.base)] = row[i];
+    IO_LOOP(i) sm[pad((int)__ldg(ta.slot_src + i) - rc.base)] = row[i];
   }
   __syncthreads();
   StPlain st{xz + ((size_t)bp * 2 + which) * N};
