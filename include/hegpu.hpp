@@ -20,6 +20,7 @@
 // allocates a fresh result (inputs are never mutated).
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -333,6 +334,96 @@ inline std::vector<double> load_input(const ModelSpec& m, const std::string& pat
   std::vector<double> x((size_t)c * d * d);
   m.check(hegpu_model_load_input(m.get(), path.c_str(), x.data()));
   return x;
+}
+
+
+// ---- lower() / execute() (proj/include/hesim/netcompile.hpp:55-86) ---------
+// The general stage driver: SubConv groups, grouped merges, the conv-pack
+// repack, HS and LoLa-dense linear stages (include/hegpu.h, hegpu_prog_*).
+enum class StageKind { ConvPack, Merge, Square, RepackConv, Linear };
+struct Stage {
+  StageKind kind;
+  std::string label;
+  int groups = 1;
+  int policy = HEGPU_POLICY_HS;
+};
+struct OpReport {
+  std::vector<std::pair<std::string, OpTally>> rows;
+  OpTally total;
+};
+struct ExecResult {
+  std::vector<double> logits;
+  OpReport report;
+};
+
+// lower(model): the stage list alone (no device needed)
+inline std::vector<Stage> lower(const ModelSpec& model) {
+  char labels[64][64];
+  int kinds[64], groups[64], pols[64];
+  const int n = hegpu_model_lower(model.get(), 64, labels, kinds, groups, pols);
+  if (n < 0) throw_status(-n, hegpu_prog_last_error(nullptr));
+  std::vector<Stage> out;
+  for (int i = 0; i < n && i < 64; ++i)
+    out.push_back(Stage{static_cast<StageKind>(kinds[i]), labels[i], groups[i], pols[i]});
+  return out;
+}
+
+// A lowered program bound to a context and its weights (keys, plans and
+// plaintexts are prepared once; execute() evaluates one input).
+class LoweredProgram {
+ public:
+  LoweredProgram(Context& ctx, const ModelSpec& model, const std::vector<double>& weights) : c_(&ctx) {
+    throw_status(hegpu_prog_create(ctx.get(), model.get(), weights.data(), weights.size(), &h_),
+                 hegpu_prog_last_error(nullptr));
+    hegpu_prog_info(h_, &n_stages_, &input_cts_, &out_level_, &n_logits_);
+  }
+  ~LoweredProgram() { hegpu_prog_destroy(h_); }
+  LoweredProgram(const LoweredProgram&) = delete;
+  LoweredProgram& operator=(const LoweredProgram&) = delete;
+  hegpu_prog* get() const { return h_; }
+  Context& ctx() const { return *c_; }
+  int input_cts() const { return input_cts_; }
+  int out_level() const { return out_level_; }
+  int n_logits() const { return n_logits_; }
+  std::vector<Stage> stages() const {
+    std::vector<Stage> out;
+    for (int i = 0; i < n_stages_; ++i) {
+      char label[64];
+      int kind = 0, groups = 1, policy = 0;
+      check(hegpu_prog_stage(h_, i, label, sizeof label, &kind, &groups, &policy));
+      out.push_back(Stage{static_cast<StageKind>(kind), label, groups, policy});
+    }
+    return out;
+  }
+  void check(int rc) const { throw_status(rc, hegpu_prog_last_error(h_)); }
+
+ private:
+  Context* c_;
+  hegpu_prog* h_ = nullptr;
+  int n_stages_ = 0, input_cts_ = 0, out_level_ = 0, n_logits_ = 0;
+};
+
+// execute(program, weights, input, ctx) (netcompile.cpp:291-446): the client
+// side (conv_pack / pack + encrypt, decrypt) is folded in here as in the
+// simulator; `input` is [c][d][d] row-major.  The report is the context's
+// per-stage tally of this run.
+inline ExecResult execute(const LoweredProgram& prog, const std::vector<double>& input, uint64_t nonce = 0) {
+  Context& ctx = prog.ctx();
+  const int L = ctx.levels(), N = ctx.n();
+  std::vector<uint64_t> in((size_t)prog.input_cts() * 2 * L * N);
+  prog.check(hegpu_prog_encrypt_input(prog.get(), input.data(), nonce, in.data()));
+  Ciphertext ci(ctx, prog.input_cts(), L), co(ctx, 1, prog.out_level());
+  ci.upload(in, std::ldexp(1.0, 40));
+  ctx.reset_meter();
+  prog.check(hegpu_prog_run(prog.get(), ci.get(), co.get()));
+  std::vector<uint64_t> out((size_t)2 * prog.out_level() * N);
+  ctx.check(hegpu_ct_download(co.get(), out.data(), out.size()));
+  ExecResult r;
+  r.logits.resize(prog.n_logits());
+  prog.check(hegpu_prog_decrypt_logits(prog.get(), out.data(), r.logits.data()));
+  r.report.rows = ctx.stages();
+  r.report.total = ctx.tally();
+  return r;
 }
 
 }  // namespace hegpu

@@ -148,6 +148,46 @@ int main() {
     CHECK_THROWS_AS(load_weights(m, "/nonexistent/w.bin"), IoError);
   }
 
+  // test_netcompile.cpp:40-54 lower(): stage labels; :74-97 a single 1x1 dense
+  // model costs one multiplication and no rotation; execute() through the
+  // general stage driver (grouped SubConv stages + the conv-pack repack)
+  {
+    const ModelSpec unit = parse_model_json(R"({"name": "unit", "input": [1, 1, 1], "n_slots": 512, "layers": [
+      {"kind": "dense", "units": 1, "label": "D"}]})");
+    const std::vector<Stage> st = lower(unit);
+    CHECK(st.size() == 1 && st[0].kind == StageKind::Linear && st[0].label == "D");
+    Context c2(10, {45, 40}, 45, /*seed=*/5);
+    LoweredProgram prog(c2, unit, {3.0, 1.0});
+    const ExecResult r = execute(prog, {2.0}, 1);
+    CHECK(close(r.logits[0], 7.0, 1e-5));
+    CHECK(r.report.total.mul_pc == 1);
+    CHECK(r.report.total.rot == 0);
+
+    const ModelSpec grouped = parse_model_json(R"({"name": "g", "input": [2, 6, 6], "n_slots": 512, "layers": [
+      {"kind": "conv", "k": 3, "s": 1, "out_channels": 4, "label": "Conv1"}, {"kind": "square"},
+      {"kind": "subconv", "k": 2, "s": 1, "out_channels": 4, "groups": 2, "label": "Conv2"},
+      {"kind": "conv", "k": 1, "s": 1, "out_channels": 3, "policy": "convpack", "label": "Conv3"},
+      {"kind": "square"}, {"kind": "flatten"}, {"kind": "dense", "units": 2, "label": "Dense1"}]})");
+    const std::vector<Stage> gs = lower(grouped);
+    const char* want[] = {"Conv1", "Flat1", "Square1", "Conv2", "Conv3", "Flat2", "Square2", "Dense1"};
+    CHECK(gs.size() == 8);
+    for (size_t i = 0; i < gs.size() && i < 8; ++i) CHECK(gs[i].label == want[i]);
+    CHECK(gs.size() == 8 && gs[1].groups == 2 && gs[3].groups == 2 && gs[4].kind == StageKind::RepackConv);
+    // zero weights give all-zero logits (test_netcompile.cpp:154-171)
+    Context c3(10, {45, 40, 40, 40, 40, 40, 40}, 45, /*seed=*/6);
+    LoweredProgram zp(c3, grouped, std::vector<double>(grouped.weight_floats(), 0.0));
+    std::vector<double> img(2 * 6 * 6);
+    for (size_t i = 0; i < img.size(); ++i) img[i] = 0.01 * (double)(i % 17);
+    const ExecResult z = execute(zp, img, 3);
+    CHECK(z.logits.size() == 2 && close(z.logits[0], 0.0, 1e-5) && close(z.logits[1], 0.0, 1e-5));
+    CHECK(z.report.rows.size() == 8 && z.report.rows[4].first == "Conv3");
+    // a LoLa-stacked stage policy is a ShapeError; a short chain a CapacityError
+    const ModelSpec stacked = parse_model_json(R"({"name": "s", "input": [1, 2, 2], "n_slots": 512, "layers": [
+      {"kind": "flatten"}, {"kind": "dense", "units": 2, "policy": "lola-stacked", "label": "D1"}]})");
+    CHECK_THROWS_AS(LoweredProgram(c2, stacked, std::vector<double>(stacked.weight_floats(), 0.0)), ShapeError);
+    CHECK_THROWS_AS(LoweredProgram(c2, grouped, std::vector<double>(grouped.weight_floats(), 0.0)), CapacityError);
+  }
+
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }

@@ -39,9 +39,12 @@ def test_sweep_matches_predictions():
         assert (int(rot), int(mul)) == (want[0], want[1])
 
 
-def test_exit_codes_without_gpu():
+def test_exit_codes_without_gpu(tmp_path):
     assert cli("run", "--model", "/no/such/model.json").returncode == 1   # IoError
-    assert cli("count", "--model", "ce").returncode == 2                  # SubConv: outside the path
+    bad = tmp_path / "stacked.json"                                       # a LoLa-stacked stage policy: ShapeError
+    bad.write_text('{"name": "s", "input": [1, 4, 4], "n_slots": 512, "layers": [{"kind": "flatten"}, '
+                   '{"kind": "dense", "units": 6, "policy": "lola-stacked", "label": "D1"}]}')
+    assert cli("count", "--model", str(bad)).returncode == 2
     assert cli("frobnicate").returncode == 2
     assert cli("sweep", "--methods", "lola-sparse").returncode == 2
 
@@ -97,7 +100,6 @@ def test_run_grouped_model_through_the_general_driver(tmp_path):
     c = cli("count", "--model", "ce-mini", "--seed", "3")
     assert c.returncode == 0, c.stderr
     assert "Pool1-Conv2" in c.stdout and "Conv3" in c.stdout
-    assert cli("count", "--model", "ce").returncode == 2  # N = 2^15: CapacityError
 
 
 @pytest.mark.gpu

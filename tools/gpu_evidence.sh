@@ -1,7 +1,7 @@
 # round evidence: tests, smoke, bench (both arms), configs 1/3/4, launch list of one step, traffic, ncu of the top kernels
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/ev_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/ev_pytest.log
+timeout 2400 python -m pytest tests -m gpu -x -q --durations=8 > gpurun_out/ev_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/ev_pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev_smoke.log 2>&1
 timeout 600 python bench.py > gpurun_out/ev_bench.json 2> gpurun_out/ev_bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/ev_bench_ref.json 2> gpurun_out/ev_bench_ref.err

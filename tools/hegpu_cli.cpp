@@ -14,6 +14,7 @@
 // random_weights / random_input (mt19937_64, N(0,1), the same scalings).
 // Built by paper_2110_08321_b200/build.py next to libhegpu.so.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -356,7 +357,12 @@ void collect_report(const Ctx& ctx, Report& rep) {
 // models outside the conv -> (square, linear)* family (SubConv groups, the
 // stand-alone conv-pack repack, LoLa-dense stages, a dense first layer): the
 // general stage driver hegpu_prog (execute, netcompile.cpp:291-446)
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 RunResult run_program(const Model& m, const std::vector<double>& w, const std::vector<double>& x, uint64_t seed) {
+  const double t0 = now_s();
   char labels[64][64];
   int kinds[64], groups[64], pols[64];
   const int ns = hegpu_model_lower(m.h, 64, labels, kinds, groups, pols);
@@ -375,13 +381,24 @@ RunResult run_program(const Model& m, const std::vector<double>& w, const std::v
   auto pok = [&](int r) {
     if (r) fail_rc(r, hegpu_prog_last_error(prog));
   };
+  const double t1 = now_s();
   pok(hegpu_prog_encrypt_input(prog, x.data(), seed, in.data()));
   hegpu_ct *di = nullptr, *out = nullptr;
   ctx.ok(hegpu_ct_create(ctx.h, n_in, L, &di));
   ctx.ok(hegpu_ct_upload(di, in.data(), in.size(), std::ldexp(1.0, 40)));
   ctx.ok(hegpu_ct_create(ctx.h, 1, out_level, &out));
   ctx.ok(hegpu_reset_meter(ctx.h));
+  // first run: resolves the plans' fused key tables; the second run is the
+  // steady-state evaluation time of one encrypted inference
+  const double t2 = now_s();
   pok(hegpu_prog_run(prog, di, out));
+  const double t3 = now_s();
+  pok(hegpu_prog_run(prog, di, out));
+  const double t4 = now_s();
+  ctx.ok(hegpu_reset_meter(ctx.h));
+  pok(hegpu_prog_run(prog, di, out));
+  std::fprintf(stderr, "timing: setup (keys, plans) %.2f s, client encrypt %.2f s, first run %.3f s, evaluation %.1f ms\n",
+               t1 - t0, t2 - t1, t3 - t2, (t4 - t3) * 1e3);
   std::vector<uint64_t> o((size_t)2 * out_level * n);
   ctx.ok(hegpu_ct_download(out, o.data(), o.size()));
   RunResult r;

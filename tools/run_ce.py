@@ -57,7 +57,9 @@ def main():
     got = [(x[0], tuple(int(v) for v in x[2:])) for x in rows[:-1]]
     ref = [(lab, (t.add_pc, t.add_cc, t.mul_pc, t.mul_cc, t.rot)) for lab, t in mc.stages]
     err = float(np.abs(logits - want).max())
+    timing = [l for l in r.stderr.splitlines() if l.startswith("timing:")]
     print(json.dumps({"model": a.model, "n_slots": model["n_slots"], "wall_s": round(dt, 1),
+                      "timing": timing[-1][8:] if timing else None,
                       "max_abs_logit_err": err, "logits": [round(float(v), 6) for v in logits],
                       "want": [round(float(v), 6) for v in want], "hops_equal_reference": got == ref,
                       "total": rows[-1][1:], "stages": [x[0] for x in rows[:-1]]}))
