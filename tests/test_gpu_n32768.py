@@ -108,6 +108,30 @@ def test_merge_and_hs(pair):
         assert ctx.total()[4] == HS.predict_hs(m, n, ck.S)[0]
 
 
+def test_batched_hs_and_rotate(pair):
+    """batches of >= 8 ciphertexts take the tcgen05 HS kernel; a batched
+    rotation shares one key"""
+    ctx, ck = pair
+    rng = np.random.default_rng(21)
+    l, B, m, n = 3, 8, 16, 300
+    A = rng.normal(0, 0.05, (m, n))
+    cts = [fresh(ck, rng, l, 300 + i, n=n) for i in range(B)]
+    plan = ctx.hs_plan(A, l, True)
+    ctx.gen_rotation_keys(plan.rotations() + [5])
+    batch = np.concatenate([c for _, c in cts])
+    d = ctx.ct(B, l, batch, DELTA)
+    got = ctx.hs_matvec(plan, d, ctx.ct(B, l - 1)).download().reshape(B, -1)
+    assert np.array_equal(got[0], P.hs_matvec(ck, cts[0][1], l, A, True))
+    one = ctx.hs_matvec(plan, ctx.ct(1, l, cts[B - 1][1], DELTA), ctx.ct(1, l - 1)).download()
+    assert np.array_equal(got[B - 1], one)
+    for i in range(B):
+        assert np.abs(ck.decrypt_decode(got[i], l - 1, DELTA)[:m] - A @ cts[i][0]).max() < 1e-4
+    rot = ctx.rotate_right(d, 5, ctx.ct(B, l)).download().reshape(B, -1)
+    key = ck.galois_key(ck.galois_right(5))
+    for i in (0, B - 1):
+        assert np.array_equal(rot[i], ck.rotate(cts[i][1], l, ck.galois_right(5), key))
+
+
 def test_conv_pack_layer(pair):
     ctx, ck = pair
     rng = np.random.default_rng(12)
