@@ -348,6 +348,11 @@ int hegpu_model_info(const hegpu_model* model, int* in_c, int* in_d, int* n_slot
 /* policy = -1 when the layer names none */
 int hegpu_model_layer(const hegpu_model* model, int i, int* kind, int* k, int* s, int* out, int* groups,
                       int* policy);
+/* ModelSpec::default_policy (netcompile.hpp:33-35; the reference CLI's
+ * --policy, hesim.cpp:43-48): the kernel of linear stages without a per-layer
+ * policy (HEGPU_POLICY_HS / _LOLA_DENSE / _LOLA_STACKED); and --n-slots */
+int hegpu_model_set_default_policy(hegpu_model* model, int policy);
+int hegpu_model_set_n_slots(hegpu_model* model, int n_slots);
 int hegpu_model_load_weights(hegpu_model* model, const char* path, double* out, size_t count); /* load_weights */
 int hegpu_model_save_weights(hegpu_model* model, const char* path, const double* w, size_t count);
 int hegpu_model_load_input(hegpu_model* model, const char* path, double* out);   /* load_input */

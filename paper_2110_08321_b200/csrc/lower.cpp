@@ -95,6 +95,7 @@ Lowered lower_model(const ModelDesc& m, const double* w, size_t wcount) {
     fail(HEGPU_ERR_SHAPE, "model \"" + m.name + "\" is outside the GPU path (" + why + ")");
   };
   const auto& L = m.layers;
+  if (m.default_policy != HEGPU_POLICY_HS) bad("a non-HS default policy (the general driver runs it)");
   if (L.empty() || L[0].kind != HEGPU_LAYER_CONV) bad("the first layer must be a conv-pack conv");
   if (L[0].groups != 1 || (L[0].policy != -1 && L[0].policy != HEGPU_POLICY_CONVPACK))
     bad("the first conv must be a plain conv-pack layer");
@@ -325,7 +326,7 @@ std::vector<ProgStage> lower_program(const ModelDesc& m) {
     }
     ProgStage st;  // maximal fused linear run
     st.kind = HEGPU_STAGE_LINEAR;
-    st.policy = HEGPU_POLICY_HS;
+    st.policy = m.default_policy;  // netcompile.cpp:178
     size_t j = idx;
     for (; j < L.size() && is_linear_kind(L[j].kind) && !is_standalone_convpack(L[j]); ++j) {
       st.layer_idx.push_back((int)j);

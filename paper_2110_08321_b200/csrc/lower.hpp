@@ -18,6 +18,7 @@ struct ModelLayer {
 struct ModelDesc {
   std::string name;
   int in_c = 0, in_d = 0, n_slots = 0;
+  int default_policy = 1;  // HEGPU_POLICY_HS: linear stages without a per-layer policy (netcompile.hpp:33-35)
   std::vector<ModelLayer> layers;
   std::pair<int, int> shape_before(size_t idx) const;  // (channels, side) entering layer idx
   size_t weight_count() const;                         // float32 values in the weights stream

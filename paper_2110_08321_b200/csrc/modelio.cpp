@@ -334,6 +334,18 @@ extern "C" int hegpu_model_info(const hegpu_model* m, int* in_c, int* in_d, int*
   return HEGPU_OK;
 }
 
+extern "C" int hegpu_model_set_default_policy(hegpu_model* m, int policy) {
+  if (!m || policy < HEGPU_POLICY_HS || policy > HEGPU_POLICY_LOLA_STACKED) return HEGPU_ERR_ARG;
+  m->default_policy = policy;
+  return HEGPU_OK;
+}
+
+extern "C" int hegpu_model_set_n_slots(hegpu_model* m, int n_slots) {
+  if (!m || n_slots < 1) return HEGPU_ERR_ARG;
+  m->n_slots = n_slots;
+  return HEGPU_OK;
+}
+
 extern "C" int hegpu_model_layer(const hegpu_model* m, int i, int* kind, int* k, int* s, int* out, int* groups,
                                  int* policy) {
   if (!m || i < 0 || i >= (int)m->layers.size()) return HEGPU_ERR_RANGE;

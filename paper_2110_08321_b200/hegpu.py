@@ -176,6 +176,8 @@ def lib():
             "hegpu_net_tap_cts": (i, [vp]),
             "hegpu_net_first_layer": (i, [vp]),
             "hegpu_net_wait": (i, [vp]),
+            "hegpu_model_set_default_policy": (i, [vp, i]),
+            "hegpu_model_set_n_slots": (i, [vp, i]),
             "hegpu_ct_view": (i, [vp, i, i, pp]),
             "hegpu_ct_copy": (i, [vp, vp]),
             "hegpu_ct_set_scale": (i, [vp, d]),
@@ -717,6 +719,14 @@ class Model:
         b = np.empty(r.value)
         self._check(lib().hegpu_model_compose(self.h, w, w.size, stage, M.ctypes.data, b.ctypes.data, None, None))
         return M, b
+
+    def set_default_policy(self, policy):
+        """ModelSpec::default_policy (netcompile.hpp:33-35): 'hs', 'lola-dense' or 'lola-stacked'"""
+        self._check(lib().hegpu_model_set_default_policy(self.h, POLICIES.index(policy)))
+
+    def set_n_slots(self, n_slots):
+        self._check(lib().hegpu_model_set_n_slots(self.h, n_slots))
+        self.n_slots = n_slots
 
     def lower(self):
         """lower() (proj/src/netcompile.cpp:106-213): the stage list as dicts

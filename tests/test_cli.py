@@ -103,6 +103,34 @@ def test_run_grouped_model_through_the_general_driver(tmp_path):
 
 
 @pytest.mark.gpu
+def test_policy_flag_changes_the_accounting(tmp_path):
+    """--policy lola-dense (hesim.cpp:43-48): me's linear stages run the
+    LoLa-dense kernel -- more rotations than the 56 of the HS pipeline, the
+    same logits (proj/tests/test_netcompile.cpp:190-205)"""
+    me = HS.builtin_model("me")
+    (tmp_path / "m.json").write_text(HS.model_json(me))
+    m = H.Model.parse(HS.model_json(me))
+    rng = np.random.default_rng(3)
+    flat = rng.normal(0, 0.05, HS.model_weight_count(me)).astype(np.float32).astype(np.float64)
+    img = rng.uniform(0, 1, (1, 30, 30)).astype(np.float32).astype(np.float64)
+    m.save_weights(tmp_path / "w.bin", flat)
+    m.save_input(tmp_path / "x.bin", img)
+    r = cli("run", "--model", str(tmp_path / "m.json"), "--weights", str(tmp_path / "w.bin"),
+            "--input", str(tmp_path / "x.bin"), "--report", str(tmp_path / "r.csv"), "--policy", "lola-dense")
+    assert r.returncode == 0, r.stderr
+    logits = np.array([float(l.split(",")[2]) for l in r.stdout.splitlines() if l.startswith("logit,")])
+    w = HS.split_model_weights(me, flat)
+    assert np.abs(logits - HS.ref_forward_model(me, w, img)).max() < 1e-3
+    mc = HS.MeterContext()
+    HS.execute_program(dict(me, default_policy="lola-dense"), w, img, mc)
+    rows = [l.split(",") for l in (tmp_path / "r.csv").read_text().splitlines()[1:]]
+    assert [(x[0], tuple(int(v) for v in x[2:])) for x in rows[:-1]] == \
+        [(lab, (t.add_pc, t.add_cc, t.mul_pc, t.mul_cc, t.rot)) for lab, t in mc.stages]
+    assert int(rows[-1][6]) > 56
+    assert cli("count", "--model", "me", "--policy", "lola-stacked").returncode == 2
+
+
+@pytest.mark.gpu
 def test_verify_negative_control_exits_3():
     """--corrupt-kernel perturbs the expected A x, so verify must report FAIL
     and exit 3 (proj/tools/hesim.cpp:212,237,334-337;

@@ -121,6 +121,33 @@ def test_cpp_lowering_equals_the_restatement():
         assert H.Model.parse(HS.model_json(model)).weight_floats == HS.model_weight_count(model)
 
 
+def test_default_policy_changes_the_linear_stages():
+    """ModelSpec::default_policy (netcompile.hpp:33-35, netcompile.cpp:178;
+    test_netcompile.cpp:190-205): stages without a per-layer policy take it"""
+    from paper_2110_08321_b200 import hegpu as H
+    me = dict(HS.builtin_model("me"), default_policy="lola-dense")
+    want = HS.lower(me)
+    assert [s["policy"] for s in want if s["kind"] == "linear"] == ["lola-dense", "lola-dense"]
+    m = H.Model.parse(HS.model_json(me))
+    assert [s["policy"] for s in m.lower() if s["kind"] == "linear"] == ["hs", "hs"]
+    m.set_default_policy("lola-dense")
+    assert [(s["label"], s["policy"]) for s in m.lower() if s["kind"] == "linear"] == \
+        [(s["label"], s["policy"]) for s in want if s["kind"] == "linear"]
+    with pytest.raises(H.ShapeError):
+        m.net_spec()   # the batched net is HS only; the general driver takes this model
+    flat, img = _weights(me, 3, 0.05)
+    w = HS.split_model_weights(me, flat)
+    mc = HS.MeterContext()
+    lg = HS.execute_program(me, w, img, mc)
+    assert mc.tally.rot > 56
+    assert np.abs(lg - HS.ref_forward_model(me, w, img)).max() < 1e-7
+    m.set_n_slots(16)   # test_netcompile.cpp:207-211: an undersized slot count is a stage-named CapacityError
+    with pytest.raises(H.CapacityError):
+        m.lower()
+    with pytest.raises(HS.CapacityError):
+        HS.lower(dict(me, n_slots=16))
+
+
 def test_cpp_lowering_errors():
     from paper_2110_08321_b200 import hegpu as H
     bad = dict(CE_MINI, n_slots=1024)  # Pool1-Conv2: fused 150 x 1176 exceeds n_slots

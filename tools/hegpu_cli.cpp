@@ -254,6 +254,8 @@ std::vector<double> ref_forward(const Model& m, const std::vector<double>& w, co
 
 struct Args {
   std::string cmd, model, weights, input, report, out, methods = "hs,lola-dense,lola-stacked";
+  std::string policy;   // run / count: ModelSpec::default_policy (hesim.cpp:43-48)
+  int model_slots = 0;  // run / count: --n-slots override of the model's slot count
   uint64_t seed = 0;
   bool seed_set = false, measure = false;
   bool corrupt_kernel = false;  // verify's negative control (hesim.cpp:212,237,334-337)
@@ -285,11 +287,13 @@ Args parse(int argc, char** argv) {
     else if (k == "--methods") a.methods = val();
     else if (k == "--measure") a.measure = true;
     else if (k == "--corrupt-kernel") a.corrupt_kernel = true;
+    else if (k == "--policy") a.policy = val();
     else if (k == "--n-slots") {
       a.slots.clear();
       std::stringstream ss(val());
       std::string tok;
       while (std::getline(ss, tok, ',')) a.slots.push_back(std::stoi(tok));
+      if (a.slots.size() == 1) a.model_slots = a.slots[0];
     } else throw Fail{kExitCapacity, "unknown option " + k};
   }
   if (!a.seed_set && a.cmd == "verify") a.seed = 1;
@@ -483,6 +487,16 @@ int cmd_run(const Args& a, bool table) {
   if (a.model.empty()) throw Fail{kExitCapacity, "--model is required"};
   Model m;
   load_model(a.model, m);
+  if (!a.policy.empty()) {  // configured_model, hesim.cpp:43-48
+    const int pol = a.policy == "hs" ? HEGPU_POLICY_HS : a.policy == "lola-dense" ? HEGPU_POLICY_LOLA_DENSE
+                    : a.policy == "lola-stacked" ? HEGPU_POLICY_LOLA_STACKED : -1;
+    if (pol < 0) throw Fail{kExitCapacity, "unknown policy " + a.policy};
+    check(hegpu_model_set_default_policy(m.h, pol), "set_default_policy");
+  }
+  if (a.model_slots > 0) {
+    check(hegpu_model_set_n_slots(m.h, a.model_slots), "set_n_slots");
+    m.n_slots = a.model_slots;
+  }
   std::vector<double> w, x;
   inputs(a, m, w, x);
   const RunResult r = run_model(m, w, x, a.seed, a.weights);
