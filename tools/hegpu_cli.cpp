@@ -258,6 +258,7 @@ struct Args {
   int model_slots = 0;  // run / count: --n-slots override of the model's slot count
   uint64_t seed = 0;
   bool seed_set = false, measure = false;
+  bool worked = false;  // sweep --worked-example (hesim.cpp:152-165)
   bool corrupt_kernel = false;  // verify's negative control (hesim.cpp:212,237,334-337)
   int cases = 20, n_min = 16, n_max = 4096, m_min = 4, m_max = 512;
   std::vector<int> slots = {4096, 16384};
@@ -286,6 +287,7 @@ Args parse(int argc, char** argv) {
     else if (k == "--m-max") a.m_max = std::stoi(val());
     else if (k == "--methods") a.methods = val();
     else if (k == "--measure") a.measure = true;
+    else if (k == "--worked-example") a.worked = true;
     else if (k == "--corrupt-kernel") a.corrupt_kernel = true;
     else if (k == "--policy") a.policy = val();
     else if (k == "--n-slots") {
@@ -605,6 +607,17 @@ int cmd_sweep(const Args& a) {
   for (const auto& m : methods)
     if (m != "hs" && m != "lola-dense" && m != "lola-stacked") throw Fail{kExitCapacity, "--methods: unknown method " + m};
   std::ostringstream os;
+  if (a.worked) {  // the m = 64, n = 4096, N = 16384 example of section 3.2 (matvec.hpp:74-83)
+    const int m = 64, n = 4096, N = 16384;
+    os << "method,n,m,N,rotations,multiplications\n";
+    const auto hs = predict_hs(m, n, N), dn = predict_lola(false, m, n, N), st = predict_lola(true, m, n, N);
+    os << "hs," << n << "," << m << "," << N << "," << hs.first << "," << hs.second << "\n";
+    os << "lola-dense," << n << "," << m << "," << N << "," << dn.first << "," << dn.second << "\n";
+    os << "lola-stacked," << n << "," << m << "," << N << "," << st.first << "," << st.second << "\n";
+    os << "# prose reference: hs rotations 77, lola-stacked rotations 1023, lola-stacked multiplications 64\n";
+    emit(a.out, os.str());
+    return kExitOk;
+  }
   os << "method,n,m,N,rotations,multiplications";
   if (a.measure) os << ",measured_rotations,measured_multiplications";
   os << "\n";
@@ -615,8 +628,8 @@ int cmd_sweep(const Args& a) {
           if (n > N || m > N) continue;
           const auto p = method == "hs" ? predict_hs(m, n, N) : predict_lola(method == "lola-stacked", m, n, N);
           os << method << "," << n << "," << m << "," << N << "," << p.first << "," << p.second;
-          if (a.measure && log2i(2 * N) > 14) {
-            os << ",,";  // ring degree 2N above the device NTT's 2^14
+          if (a.measure && log2i(2 * N) > 15) {
+            os << ",,";  // ring degree 2N above the device NTT's 2^15
           } else if (a.measure) {
             const auto g = measure_gpu(method, m, n, N, a.seed);
             os << "," << g.first << "," << g.second;
