@@ -6,6 +6,8 @@ measures the headline config 2).  One JSON line per measured point.
   python bench_configs.py --config 1 --method lola   # the LoLa comparators on the same grid
   python bench_configs.py --config 3   # CIFAR-shaped net, N=16384, 5 rescales
   python bench_configs.py --config 4 [--hs]  # conv layer sweep, N=16384 (torchrun: shard by output channel)
+  python bench_configs.py --model ce --batch 8   # a reference builtin (cryptonets-hs / me / ce) or ce-mini
+                                                 # through the general stage driver, B images per run
 
 Device time with CUDA events on the engine's stream after warm-up; inputs are
 fresh seeded encryptions (synthetic, BASELINE.json shapes/distributions).
@@ -234,6 +236,48 @@ def config3(args, which=3):
         dist.destroy_process_group()
 
 
+def builtin_program(args):
+    """A reference builtin (proj/src/netcompile.cpp:567-628) through the
+    general stage driver hegpu_prog: B encrypted images per run; ce runs at
+    its declared n_slots = 16384 (N = 2^15, ~140 GB of keys and tables).
+    The logits of every image are checked against the FP64 forward pass."""
+    from oracle import hesim_oracle as HS   # the checker (logits, HOP rows)
+    from paper_2110_08321_b200 import hegpu as H
+    if args.model == "ce-mini":
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from test_program import CE_MINI as model
+    else:
+        model = HS.builtin_model(args.model)
+    stages = HS.lower(model)
+    depth = sum(0 if s["kind"] == "merge" else 2 if s["policy"] == "lola-dense" and s["kind"] == "linear" else 1
+                for s in stages)
+    log_n = (2 * model["n_slots"]).bit_length() - 1
+    t0 = time.perf_counter()
+    ctx = H.Context(log_n, [45] + [40] * depth, 45, seed=11, device=0)
+    rng = np.random.default_rng(5)
+    flat = rng.normal(0, 0.05, HS.model_weight_count(model)).astype(np.float32).astype(np.float64)
+    prog = H.Program(ctx, H.Model.parse(HS.model_json(model)), flat)
+    B = args.batch
+    imgs = rng.uniform(0, 1, (B, model["in_c"], model["in_d"], model["in_d"]))
+    cts = np.concatenate([prog.encrypt_input(imgs[b], nonce=b) for b in range(B)])
+    din, out = ctx.ct(B * prog.input_cts, prog.top, cts, DELTA), ctx.ct(B, prog.out_level)
+    prog.run(din, out)   # resolves the plans' fused key tables
+    setup = time.perf_counter() - t0
+    ctx.reset_meter()
+    prog.run(din, out)
+    rows = ctx.stages()
+    total = ctx.total()
+    ms = timed(ctx, lambda: prog.run(din, out), args.steps, args.warmup)
+    got = out.download().reshape(B, -1)
+    w = HS.split_model_weights(model, flat)
+    err = max(np.abs(prog.decrypt_logits(got[b]) - HS.ref_forward_model(model, w, imgs[b])).max() for b in range(B))
+    assert err < 1e-3, err
+    print(json.dumps({"model": model["name"], "n_slots": model["n_slots"], "log_n": log_n, "levels": depth + 1,
+                      "batch": B, "ms_per_run": ms, "inferences_per_s": B / ms * 1e3,
+                      "rotations_per_s": total[4] / ms * 1e3, "hops_per_inference": [v / B for v in total],
+                      "stages": [r[0] for r in rows], "max_abs_logit_err": float(err), "setup_s": setup}))
+
+
 def _dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -367,7 +411,9 @@ def hs_formulation(ctx, W, b, img, world, rank, local, args):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", type=int, required=True, choices=[0, 1, 3, 4])
+    ap.add_argument("--config", type=int, choices=[0, 1, 3, 4])
+    ap.add_argument("--model", choices=["cryptonets-hs", "me", "ce", "ce-mini"],
+                    help="run a builtin model through the general stage driver instead of a config")
     ap.add_argument("--method", default="hs", choices=["hs", "lola"],
                     help="config 1: the HS matvec (default) or the two LoLa comparators")
     ap.add_argument("--steps", type=int, default=5)
@@ -381,6 +427,10 @@ def main():
     ap.add_argument("--hs", action="store_true",
                     help="config 4: also run the Halevi-Shoup formulation where it fits one ciphertext")
     args = ap.parse_args()
+    if args.model:
+        return builtin_program(args)
+    if args.config is None:
+        ap.error("--config or --model is required")
     if args.config == 1 and args.method == "lola":
         return config1_lola(args)
     {0: config0, 1: config1, 3: config3, 4: config4}[args.config](args)

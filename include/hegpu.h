@@ -380,7 +380,7 @@ double hegpu_net_output_scale(const hegpu_net* net);
  * conv-pack conv on rotated group ciphertexts, :352-379) and Linear runs
  * per channel group (SubConv, :380-434) under the HS or LoLa-dense policy;
  * a model without a first conv-pack conv is seeded with one dense input
- * ciphertext (:309-319).  One image per run; every stage executes the
+ * ciphertext (:309-319).  Every stage executes the
  * C-ABI operators above (conv_plan_run, merge_maps, square, rotate_left,
  * mul_plain/add/add_plain/rescale with the reference's masked constants,
  * hs_matvec, lola_matvec) under hegpu_begin_stage(label), so the per-stage
@@ -412,7 +412,9 @@ int hegpu_model_lower(const hegpu_model* model, int cap, char (*labels)[64], int
 /* client: conv_pack (or the dense input vector) -> encode + encrypt at the
  * top level; input_cts wire ciphertexts, nonces nonce * input_cts + t */
 int hegpu_prog_encrypt_input(hegpu_prog* prog, const double* image, uint64_t nonce, uint64_t* cts_out);
-/* input: input_cts ciphertexts at the top level; out: 1 ciphertext at out_level */
+/* input: B x input_cts ciphertexts (image-major, as hegpu_prog_encrypt_input
+ * writes them image after image) at the top level; out: B ciphertexts at
+ * out_level.  Grouped stages run one batched operator call per group. */
 int hegpu_prog_run(hegpu_prog* prog, hegpu_ct* input, hegpu_ct* out);
 int hegpu_prog_decrypt_logits(hegpu_prog* prog, const uint64_t* out_ct, double* logits);
 double hegpu_prog_output_scale(const hegpu_prog* prog);

@@ -300,71 +300,104 @@ void build(hegpu_prog& P, const double* w, size_t count) {
   if (any_square) ok(h, hegpu_gen_relin_key(h), "gen_relin_key");
 }
 
+// One pass over a batch of B images.  Layouts of the intermediate batch:
+// ConvPack leaves maps image-major [b][map]; every other stage keeps its
+// ciphertexts UNIT-MAJOR [unit][b] (unit = channel group after a Merge /
+// Linear stage, map after a RepackConv), so the B ciphertexts a stage
+// operator works on are contiguous and run as one batched C-ABI call (the
+// grouped HS stages take the tensor-core kernel from B = 8 on).
 void run(hegpu_prog& P, hegpu_ct* input, hegpu_ct* out) {
   hegpu_ctx* h = P.h;
   int cnt = 0, lvl = 0;
   ok(h, hegpu_ct_info(input, &cnt, &lvl, nullptr), "ct_info");
-  if (cnt != P.input_cts || lvl != P.top)
-    fail(HEGPU_ERR_SHAPE, "prog_run: input must be " + std::to_string(P.input_cts) + " ciphertexts at the top level");
+  if (cnt < P.input_cts || cnt % P.input_cts != 0 || lvl != P.top)
+    fail(HEGPU_ERR_SHAPE, "prog_run: input must be B x " + std::to_string(P.input_cts) +
+                              " ciphertexts at the top level");
+  const int B = cnt / P.input_cts;
   ok(h, hegpu_ct_info(out, &cnt, &lvl, nullptr), "ct_info");
-  if (cnt != 1 || lvl != P.out_level) fail(HEGPU_ERR_SHAPE, "prog_run: bad output handle");
+  if (cnt != B || lvl != P.out_level) fail(HEGPU_ERR_SHAPE, "prog_run: the output handle must hold B ciphertexts at the output level");
   ok(h, hegpu_ct_set_scale(input, P.in_scale), "ct_set_scale");
-  CtH cur;            // owned intermediate batch (empty while the state is the caller's input)
-  hegpu_ct* x = input;  // current state: pl.n_in ciphertexts at pl.level_in
+  CtH cur;              // owned intermediate batch (empty while the state is the caller's input)
+  hegpu_ct* x = input;  // current state: pl.n_in units x B ciphertexts at pl.level_in
+  bool image_major = true;  // [b][unit] (the input taps, ConvPack's maps) vs [unit][b]
+  auto sub = [&](hegpu_ct* src, int first, int count) {
+    hegpu_ct* v = nullptr;
+    ok(h, hegpu_ct_view(src, first, count, &v), "ct_view");
+    return CtH(v);
+  };
   for (size_t si = 0; si < P.stages.size(); ++si) {
     const ProgStage& st = P.stages[si];
     const StagePlan& pl = P.plans[si];
     ok(h, hegpu_begin_stage(h, st.label.c_str()), "begin_stage");
     CtH nxt;
+    bool nxt_image_major = false;
     switch (st.kind) {
       case HEGPU_STAGE_CONVPACK: {
-        nxt = make_ct(h, pl.n_out, pl.level_out);
+        nxt = make_ct(h, B * pl.n_out, pl.level_out);
         ok(h, hegpu_conv_plan_run(h, pl.conv, x, nxt.p), st.label.c_str());
+        nxt_image_major = true;
         break;
       }
       case HEGPU_STAGE_MERGE: {
-        const int G = st.groups, per = pl.shape_in.c / G;
+        const int G = st.groups, C = pl.shape_in.c, per = C / G;
         const int64_t wd = (int64_t)pl.shape_in.d * pl.shape_in.d;
-        nxt = make_ct(h, G, pl.level_out);
-        for (int g = 0; g < G; ++g) {
-          hegpu_ct* in_g = nullptr;
-          ok(h, hegpu_ct_view(x, g * per, per, &in_g), "ct_view");
-          CtH ig(in_g), og = view(h, nxt, g, 1);
-          ok(h, hegpu_merge_maps(h, ig.p, per, wd, og.p), st.label.c_str());
-        }
+        nxt = make_ct(h, G * B, pl.level_out);
+        CtH gather;  // map-major input: one group's maps of one image, made contiguous
+        if (!image_major) gather = make_ct(h, per, pl.level_in);
+        for (int b = 0; b < B; ++b)
+          for (int g = 0; g < G; ++g) {
+            CtH og = sub(nxt.p, g * B + b, 1);
+            if (image_major) {
+              CtH ig = sub(x, b * C + g * per, per);
+              ok(h, hegpu_merge_maps(h, ig.p, per, wd, og.p), st.label.c_str());
+            } else {
+              for (int j = 0; j < per; ++j) {
+                CtH src = sub(x, (g * per + j) * B + b, 1), dst = sub(gather.p, j, 1);
+                ok(h, hegpu_ct_copy(dst.p, src.p), "ct_copy");
+              }
+              ok(h, hegpu_merge_maps(h, gather.p, per, wd, og.p), st.label.c_str());
+            }
+          }
         break;
       }
       case HEGPU_STAGE_SQUARE: {
-        nxt = make_ct(h, pl.n_in, pl.level_out);
+        nxt = make_ct(h, B * pl.n_in, pl.level_out);
         ok(h, hegpu_square(h, x, nxt.p), st.label.c_str());
+        nxt_image_major = image_major;
         break;
       }
       case HEGPU_STAGE_REPACKCONV: {
         const int c_in = pl.shape_in.c, c_out = pl.n_out, l = pl.level_in;
         const int64_t wd = (int64_t)pl.shape_in.d * pl.shape_in.d;
+        // taps, tap-major [t][b]: the maps themselves, or rotate_left(group
+        // ct, j w) (netcompile.cpp:366-373; one batched rotation per (g, j))
         CtH rot;
         hegpu_ct* taps = x;
-        if (!pl.maps_in) {  // taps = rotate_left(group ct, j w), netcompile.cpp:366-373
+        if (pl.maps_in && image_major) {  // ConvPack maps [b][t] -> [t][b]
+          rot = make_ct(h, c_in * B, l);
+          for (int b = 0; b < B; ++b)
+            for (int t = 0; t < c_in; ++t) {
+              CtH src = sub(x, b * c_in + t, 1), dst = sub(rot.p, t * B + b, 1);
+              ok(h, hegpu_ct_copy(dst.p, src.p), "ct_copy");
+            }
+          taps = rot.p;
+        } else if (!pl.maps_in) {
           const int G = pl.n_in, per = c_in / G;
-          rot = make_ct(h, c_in, l);
+          rot = make_ct(h, c_in * B, l);
           for (int g = 0; g < G; ++g) {
-            hegpu_ct* src = nullptr;
-            ok(h, hegpu_ct_view(x, g, 1, &src), "ct_view");
-            CtH sg(src);
+            CtH sg = sub(x, g * B, B);
             for (int j = 0; j < per; ++j) {
-              CtH dst = view(h, rot, g * per + j, 1);
+              CtH dst = sub(rot.p, (g * per + j) * B, B);
               ok(h, hegpu_rotate_left(h, sg.p, (int64_t)j * wd % P.S, dst.p), st.label.c_str());
             }
           }
           taps = rot.p;
         }
-        CtH prod = make_ct(h, c_out, l), tmp = make_ct(h, 1, l);
+        CtH prod = make_ct(h, c_out * B, l), tmp = make_ct(h, B, l);
         for (int co = 0; co < c_out; ++co) {
-          CtH acc = view(h, prod, co, 1);
+          CtH acc = sub(prod.p, co * B, B);
           for (int t = 0; t < c_in; ++t) {
-            hegpu_ct* tv = nullptr;
-            ok(h, hegpu_ct_view(taps, t, 1, &tv), "ct_view");
-            CtH tap(tv);
+            CtH tap = sub(taps, t * B, B);
             ok(h, hegpu_ct_set_scale(tap.p, pl.scale_in), "ct_set_scale");
             if (t == 0) {
               ok(h, hegpu_mul_plain(h, tap.p, pl.rp_w[(size_t)co * c_in], acc.p), st.label.c_str());
@@ -375,22 +408,20 @@ void run(hegpu_prog& P, hegpu_ct* input, hegpu_ct* out) {
           }
           ok(h, hegpu_add_plain(h, acc.p, pl.rp_b[co], acc.p), st.label.c_str());
         }
-        nxt = make_ct(h, c_out, pl.level_out);
+        nxt = make_ct(h, c_out * B, pl.level_out);
         ok(h, hegpu_rescale(h, prod.p, nxt.p), st.label.c_str());
         break;
       }
       case HEGPU_STAGE_LINEAR: {
         const int G = st.groups;
-        nxt = make_ct(h, G, pl.level_out);
+        nxt = make_ct(h, G * B, pl.level_out);
         for (int g = 0; g < G; ++g) {
-          hegpu_ct* in_g = nullptr;
-          ok(h, hegpu_ct_view(x, g, 1, &in_g), "ct_view");
-          CtH ig(in_g), og = view(h, nxt, g, 1);
+          CtH ig = sub(x, g * B, B), og = sub(nxt.p, g * B, B);
           ok(h, hegpu_ct_set_scale(ig.p, pl.scale_in), "ct_set_scale");
           if (st.policy == HEGPU_POLICY_HS) {
             ok(h, hegpu_hs_matvec(h, pl.hs[g], ig.p, og.p), st.label.c_str());
-          } else {  // lola_dense_matvec rows, then merge_maps(rows, 1) (netcompile.cpp:402-405)
-            CtH rows = make_ct(h, pl.rows, pl.level_out);
+          } else {  // lola_dense_matvec rows [b][row], then merge_maps(rows, 1) (netcompile.cpp:402-405)
+            CtH rows = make_ct(h, B * pl.rows, pl.level_out);
             ok(h, hegpu_lola_matvec(h, pl.lola[g], ig.p, rows.p), st.label.c_str());
             ok(h, hegpu_merge_maps(h, rows.p, pl.rows, 1, og.p), st.label.c_str());
           }
@@ -402,6 +433,7 @@ void run(hegpu_prog& P, hegpu_ct* input, hegpu_ct* out) {
     ok(h, hegpu_ct_set_scale(nxt.p, pl.scale_out), "ct_set_scale");
     cur = std::move(nxt);
     x = cur.p;
+    image_major = nxt_image_major;
   }
   ok(h, hegpu_ct_copy(out, x), "ct_copy");
   ok(h, hegpu_sync(h), "sync");

@@ -219,6 +219,42 @@ def test_prog_lola_dense_dense_seed():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("model,qbits,log_n,B", [(CE_MINI, CE_MINI_QBITS, 12, 3), (CE_MINI, CE_MINI_QBITS, 12, 8),
+                                                 (LD_MINI, LD_MINI_QBITS, 10, 5)])
+def test_prog_batches_match_single_image_runs(model, qbits, log_n, B):
+    """B images per run (unit-major batches; from B = 8 the grouped HS stages
+    take the tensor-core kernel): every image's limbs equal its own
+    single-image run and the CPU oracle, the HOP report is B times one run's"""
+    from oracle import ckks_pipeline as P
+    from oracle.ckks import Ckks
+    from paper_2110_08321_b200 import hegpu as H
+    flat, _ = _weights(model, 5)
+    w = HS.split_model_weights(model, flat)
+    rng = np.random.default_rng(77)
+    imgs = rng.uniform(0, 1, (B, model["in_c"], model["in_d"], model["in_d"]))
+    ctx = H.Context(log_n, qbits, 45, seed=7, device=0)
+    prog = H.Program(ctx, H.Model.parse(HS.model_json(model)), flat)
+    cts = np.concatenate([prog.encrypt_input(imgs[b], nonce=10 + b) for b in range(B)])
+    out = ctx.ct(B, prog.out_level)
+    ctx.reset_meter()
+    prog.run(ctx.ct(B * prog.input_cts, prog.top, cts, 2.0 ** 40), out)
+    batch_rows = ctx.stages()
+    got = out.download().reshape(B, -1)
+    per = prog.input_cts * 2 * prog.top * ctx.N
+    for b in (0, B - 1):
+        one = ctx.ct(1, prog.out_level)
+        ctx.reset_meter()
+        prog.run(ctx.ct(prog.input_cts, prog.top, cts[b * per:(b + 1) * per], 2.0 ** 40), one)
+        assert np.array_equal(got[b], one.download()), b
+    assert batch_rows == [(lab, tuple(B * v for v in t)) for lab, t in ctx.stages()]
+    ck = Ckks(log_n, qbits, 45, seed=7)
+    want, _, _, _ = P.run_program(ck, model, w, imgs[B // 2], nonce=10 + B // 2)
+    assert np.array_equal(got[B // 2], want)
+    for b in range(B):
+        assert np.abs(prog.decrypt_logits(got[b]) - HS.ref_forward_model(model, w, imgs[b])).max() < 1e-3
+
+
+@pytest.mark.gpu
 def test_prog_rejections():
     from paper_2110_08321_b200 import hegpu as H
     flat, _ = _weights(LD_MINI, 1)
