@@ -147,7 +147,10 @@ struct TcArgs {
 // mbarriers: full[buf] (128 producer arrivals, after each producer's
 // cp.async.wait + proxy fence), empty[buf] and tfull[tb] (tcgen05.commit),
 // tempty[tb] (128 epilogue arrivals) -- no CTA-wide barrier in the loop.
-__global__ void __launch_bounds__(kTcThreads, 1) k_conv_tc(TcArgs a) {
+#ifndef HEGPU_TC_MINB
+#define HEGPU_TC_MINB 1  // CTAs per SM the register allocation allows (2: <= 78 registers)
+#endif
+__global__ void __launch_bounds__(kTcThreads, HEGPU_TC_MINB) k_conv_tc(TcArgs a) {
   extern __shared__ __align__(128) uint8_t tc_smem[];
   __shared__ __align__(8) uint64_t bars[2 * kMaxBufs + 4];  // full[], empty[], tfull[2], tempty[2]
   __shared__ uint32_t tmem_slot;
