@@ -10,6 +10,10 @@ ckks_small.json -- CKKS limb fixtures at N = 2^10 from the CPU oracle
     sha256 of each op's output limbs + decrypted slots.  tests/test_golden.py
     checks the oracle against them on CPU and the CUDA path against them on
     the GPU, so GPU parity does not depend on the oracle at run time.
+ckks_programs.json -- the general stage driver: the reference's lowering
+    KATs (stage labels, the `ce` totals) and, from the CPU oracle, the output
+    ciphertext hash, logits and per-stage HOP rows of the scaled-down `ce`
+    and the LoLa-dense model (tests/test_program.py).
 """
 import hashlib
 import json
@@ -98,7 +102,43 @@ def ckks_fixtures():
     return out
 
 
+def program_fixtures():
+    """the general stage driver (SubConv groups, RepackConv, LoLa-dense): the
+    CPU oracle's output ciphertext of the scaled-down `ce` and the LoLa-dense
+    model of tests/test_program.py, plus the reference KATs of the lowering
+    (proj/tests/test_netcompile.cpp:40-54, :139-152)"""
+    from oracle import ckks_pipeline as P
+    from oracle import hesim_oracle as HS
+    from oracle.ckks import Ckks
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import test_program as T
+    out = {"lowering_kats": {
+        "src": "proj/tests/test_netcompile.cpp:40-54,139-152",
+        "cryptonets-hs": ["Conv1", "Flat1", "Square1", "Conv2-Dense1", "Square2", "Dense2"],
+        "me_stages": 6,
+        "ce": ["Conv1", "Flat1", "Square1", "Pool1-Conv2", "Conv3", "Flat2", "Square2", "Pool2-Dense1", "Square3",
+               "Dense2"],
+        "ce_conv1": [18, 468, 486, 0, 0],
+        "ce_published_totals": {"total": 11134, "add_pc": 85, "add_cc": 4092, "mul_pc": 4080, "mul_cc": 5,
+                                "rot": 2872, "tolerance_pct": 5}}}
+    for name, model, qbits, log_n, seed in (("ce_mini", T.CE_MINI, T.CE_MINI_QBITS, 12, 5),
+                                            ("ld_mini", T.LD_MINI, T.LD_MINI_QBITS, 10, 6)):
+        flat, img = T._weights(model, seed)
+        w = HS.split_model_weights(model, flat)
+        ck = Ckks(log_n, qbits, 45, seed=7)
+        ct, l, scale, n = P.run_program(ck, model, w, img, nonce=2)
+        mc = HS.MeterContext()
+        HS.execute_program(model, w, img, mc)
+        out[name] = {"log_n": log_n, "qbits": qbits, "pbits": 45, "ctx_seed": 7, "weights_seed": seed, "nonce": 2,
+                     "level": l, "scale": scale, "n_logits": n, "out_ct": sha(ct),
+                     "logits": [float(x) for x in np.real(ck.decrypt_decode(ct, l, scale)[:n])],
+                     "stages": [[lab, [t.add_pc, t.add_cc, t.mul_pc, t.mul_cc, t.rot]] for lab, t in mc.stages]}
+    return out
+
+
 if __name__ == "__main__":
+    with open(os.path.join(HERE, "ckks_programs.json"), "w") as f:
+        json.dump(program_fixtures(), f, indent=1)
     with open(os.path.join(HERE, "reference_kats.json"), "w") as f:
         json.dump(reference_kats(), f, indent=1)
     with open(os.path.join(HERE, "ckks_small.json"), "w") as f:
