@@ -427,6 +427,7 @@ def run_gpu(args):
         "ntts_per_s": ntt_rows * world / sec, "ntts_per_step": ntt_rows,
         "hops_per_inference": {k: v / B for k, v in zip(H.TALLY_FIELDS, tally)},
         "cuda_graph": bool(args.graph),
+        "step_streams": (int(os.environ.get("HEGPU_NET_STREAMS", "2")) if B >= 64 else 1),
         "gpu_launches": ref["launches_per_step"] * args.steps,
         "roofline": roofline,
         "kernels": kernels,

@@ -443,6 +443,32 @@ def test_cfg0_net_batch_tensor_core_hs(cfg0):
         assert np.abs(net.decrypt_logits(got[b]) - HS.ref_forward(spec, w, imgs[b])).max() < 1e-3
 
 
+def test_cfg0_net_batch64_two_streams(cfg0):
+    """a 64-image batch (config 2's step) runs as two 32-image parts on two
+    streams (net.cu run_net), also inside a CUDA-graph capture: every image's
+    limbs equal its single-image run"""
+    cfg, ctx, ck, w, net = cfg0
+    t = [net.encrypt_image(net_image(cfg, 70 + s), nonce=70 + s) for s in range(3)]
+    singles = []
+    for k in range(3):
+        o = ctx.ct(1, net.out_level)
+        net.run(ctx.ct(net.tap_cts, net.top, t[k], DELTA), o)
+        singles.append(o.download())
+    order = [(b * 7 + b // 32) % 3 for b in range(64)]   # a different pattern in each half
+    din = ctx.ct(64 * net.tap_cts, net.top, np.concatenate([t[k] for k in order]), DELTA)
+    out = ctx.ct(64, net.out_level)
+    net.run(din, out)
+    got = out.download().reshape(64, -1)
+    for b in range(64):
+        assert np.array_equal(got[b], singles[order[b]]), b
+    out2 = ctx.ct(64, net.out_level)
+    graph = ctx.capture(lambda: net.run(din, out2))
+    graph()
+    graph()
+    ctx.sync()
+    assert np.array_equal(out2.download().reshape(64, -1), got)
+
+
 def test_cfg0_run_host_matches_device_run(cfg0):
     cfg, ctx, ck, w, net = cfg0
     B = 3
