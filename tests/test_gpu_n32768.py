@@ -132,6 +132,26 @@ def test_batched_hs_and_rotate(pair):
         assert np.array_equal(rot[i], ck.rotate(cts[i][1], l, ck.galois_right(5), key))
 
 
+def test_cluster_kernels_are_deterministic(pair):
+    """the DSMEM exchange of the split inverse transform and the two-CTA
+    forward halves: 12 repeated key switches / squares of a 16-ciphertext
+    batch (enough rows to fill the GPU several times) give identical limbs"""
+    ctx, ck = pair
+    rng = np.random.default_rng(31)
+    l, B = 4, 16
+    cts = np.concatenate([fresh(ck, rng, l, 400 + i)[1] for i in range(B)])
+    ctx.gen_rotation_keys([123])
+    ctx.gen_relin_key()
+    d = ctx.ct(B, l, cts, DELTA)
+    rot0 = ctx.rotate_right(d, 123, ctx.ct(B, l)).download()
+    sq0 = ctx.square(d, ctx.ct(B, l - 1)).download()
+    assert np.array_equal(rot0.reshape(B, -1)[3], ck.rotate(cts.reshape(B, -1)[3], l, ck.galois_right(123),
+                                                             ck.galois_key(ck.galois_right(123))))
+    for _ in range(12):
+        assert np.array_equal(ctx.rotate_right(d, 123, ctx.ct(B, l)).download(), rot0)
+        assert np.array_equal(ctx.square(d, ctx.ct(B, l - 1)).download(), sq0)
+
+
 def test_conv_pack_layer(pair):
     ctx, ck = pair
     rng = np.random.default_rng(12)
