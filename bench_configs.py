@@ -241,22 +241,19 @@ def builtin_program(args):
     general stage driver hegpu_prog: B encrypted images per run; ce runs at
     its declared n_slots = 16384 (N = 2^15, ~140 GB of keys and tables).
     The logits of every image are checked against the FP64 forward pass."""
-    from oracle import hesim_oracle as HS   # the checker (logits, HOP rows)
     from paper_2110_08321_b200 import hegpu as H
-    if args.model == "ce-mini":
-        sys.path.insert(0, os.path.join(ROOT, "tests"))
-        from test_program import CE_MINI as model
-    else:
-        model = HS.builtin_model(args.model)
-    stages = HS.lower(model)
+    from paper_2110_08321_b200.workloads import BUILTIN_MODEL_JSON, model_forward
+    m = H.Model.parse(BUILTIN_MODEL_JSON[args.model])
+    model = {"name": args.model, "n_slots": m.n_slots, "in_c": m.in_c, "in_d": m.in_d}
+    stages = m.lower()
     depth = sum(0 if s["kind"] == "merge" else 2 if s["policy"] == "lola-dense" and s["kind"] == "linear" else 1
                 for s in stages)
     log_n = (2 * model["n_slots"]).bit_length() - 1
     t0 = time.perf_counter()
     ctx = H.Context(log_n, [45] + [40] * depth, 45, seed=11, device=0)
     rng = np.random.default_rng(5)
-    flat = rng.normal(0, 0.05, HS.model_weight_count(model)).astype(np.float32).astype(np.float64)
-    prog = H.Program(ctx, H.Model.parse(HS.model_json(model)), flat)
+    flat = rng.normal(0, 0.05, m.weight_floats).astype(np.float32).astype(np.float64)
+    prog = H.Program(ctx, m, flat)
     B = args.batch
     imgs = rng.uniform(0, 1, (B, model["in_c"], model["in_d"], model["in_d"]))
     cts = np.concatenate([prog.encrypt_input(imgs[b], nonce=b) for b in range(B)])
@@ -269,8 +266,8 @@ def builtin_program(args):
     total = ctx.total()
     ms = timed(ctx, lambda: prog.run(din, out), args.steps, args.warmup)
     got = out.download().reshape(B, -1)
-    w = HS.split_model_weights(model, flat)
-    err = max(np.abs(prog.decrypt_logits(got[b]) - HS.ref_forward_model(model, w, imgs[b])).max() for b in range(B))
+    err = max(np.abs(prog.decrypt_logits(got[b]) - model_forward(m.layers, m.in_c, m.in_d, flat, imgs[b])).max()
+              for b in range(B))
     assert err < 1e-3, err
     print(json.dumps({"model": model["name"], "n_slots": model["n_slots"], "log_n": log_n, "levels": depth + 1,
                       "batch": B, "ms_per_run": ms, "inferences_per_s": B / ms * 1e3,

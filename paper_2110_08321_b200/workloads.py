@@ -143,3 +143,91 @@ def plain_forward(cfg: NetConfig, weights, image):
     for Wd, bd in weights["dense"]:
         flat = np.asarray(Wd) @ (flat * flat) + np.asarray(bd)
     return flat
+
+
+# ---- the reference's builtin layer lists (proj/src/netcompile.cpp:567-628) as
+# model files, plus ce-mini (ce's ten stages scaled to N = 4096) -------------
+BUILTIN_MODEL_JSON = {
+    "cryptonets-hs": """{"name": "cryptonets-hs", "input": [1, 29, 29], "n_slots": 8192, "layers": [
+        {"kind": "conv", "k": 5, "s": 2, "out_channels": 5, "label": "Conv1"}, {"kind": "square"},
+        {"kind": "avgpool", "k": 2, "s": 2}, {"kind": "conv", "k": 5, "s": 1, "out_channels": 50, "label": "Conv2"},
+        {"kind": "avgpool", "k": 2, "s": 2}, {"kind": "flatten"}, {"kind": "dense", "units": 100, "label": "Dense1"},
+        {"kind": "square"}, {"kind": "dense", "units": 10, "label": "Dense2"}]}""",
+    "me": """{"name": "me", "input": [1, 30, 30], "n_slots": 8192, "layers": [
+        {"kind": "conv", "k": 3, "s": 1, "out_channels": 5, "label": "Conv1"}, {"kind": "square"},
+        {"kind": "avgpool", "k": 3, "s": 2}, {"kind": "conv", "k": 3, "s": 1, "out_channels": 50, "label": "Conv2"},
+        {"kind": "avgpool", "k": 3, "s": 2}, {"kind": "flatten"}, {"kind": "dense", "units": 32, "label": "Dense1"},
+        {"kind": "square"}, {"kind": "dense", "units": 10, "label": "Dense2"}]}""",
+    "ce": """{"name": "ce", "input": [3, 32, 32], "n_slots": 16384, "layers": [
+        {"kind": "conv", "k": 3, "s": 1, "out_channels": 18, "label": "Conv1"}, {"kind": "square"},
+        {"kind": "avgpool", "k": 2, "s": 2, "label": "Pool1"},
+        {"kind": "subconv", "k": 3, "s": 1, "out_channels": 15, "groups": 3, "label": "Conv2"},
+        {"kind": "conv", "k": 1, "s": 1, "out_channels": 64, "policy": "convpack", "label": "Conv3"},
+        {"kind": "square"}, {"kind": "avgpool", "k": 2, "s": 2, "label": "Pool2"},
+        {"kind": "conv", "k": 3, "s": 1, "out_channels": 64}, {"kind": "flatten"},
+        {"kind": "dense", "units": 256, "label": "Dense1"}, {"kind": "square"},
+        {"kind": "dense", "units": 10, "label": "Dense2"}]}""",
+    "ce-mini": """{"name": "ce-mini", "input": [3, 16, 16], "n_slots": 2048, "layers": [
+        {"kind": "conv", "k": 3, "s": 1, "out_channels": 6, "label": "Conv1"}, {"kind": "square"},
+        {"kind": "avgpool", "k": 2, "s": 2, "label": "Pool1"},
+        {"kind": "subconv", "k": 3, "s": 1, "out_channels": 6, "groups": 3, "label": "Conv2"},
+        {"kind": "conv", "k": 1, "s": 1, "out_channels": 8, "policy": "convpack", "label": "Conv3"},
+        {"kind": "square"}, {"kind": "avgpool", "k": 2, "s": 2, "label": "Pool2"},
+        {"kind": "conv", "k": 2, "s": 1, "out_channels": 12}, {"kind": "flatten"},
+        {"kind": "dense", "units": 16, "label": "Dense1"}, {"kind": "square"},
+        {"kind": "dense", "units": 10, "label": "Dense2"}]}""",
+}
+
+
+def _conv_fp64(x, W, b, s):
+    c_out, c_in, k, _ = W.shape
+    d = (x.shape[1] - k) // s + 1
+    out = np.empty((c_out, d, d))
+    o = np.arange(d) * s
+    for co in range(c_out):
+        acc = np.full((d, d), float(b[co]))
+        for ci in range(c_in):
+            for ky in range(k):
+                for kx in range(k):
+                    acc += W[co, ci, ky, kx] * x[ci][np.ix_(o + ky, o + kx)]
+        out[co] = acc
+    return out
+
+
+def model_forward(layers, in_c, in_d, flat_weights, image):
+    """the cleartext forward pass of a model's layer list (conv / subconv /
+    avgpool / square / flatten / dense; the float32-stream weight order of
+    proj/src/modelio.cpp:169-202) in FP64 -- the sanity check on decrypted
+    logits of bench_configs.py --model (the reference-order oracle lives under
+    oracle/ and is for tests); layers as paper_2110_08321_b200.hegpu.Model.layers"""
+    w = np.asarray(flat_weights, dtype=np.float64)
+    t = np.asarray(image, dtype=np.float64).reshape(in_c, in_d, in_d)
+    o = 0
+    for l in layers:
+        kind = l["kind"]
+        if kind in ("conv", "subconv"):
+            g = max(1, l.get("groups") or 1) if kind == "subconv" else 1
+            ci, co, k = t.shape[0] // g, l["out"] // g, l["k"]
+            parts = []
+            for i in range(g):
+                n = co * ci * k * k
+                parts.append(_conv_fp64(t[i * ci:(i + 1) * ci], w[o:o + n].reshape(co, ci, k, k), w[o + n:o + n + co],
+                                        l.get("s") or 1))
+                o += n + co
+            t = np.concatenate(parts)
+        elif kind == "avgpool":
+            k, s = l["k"], l.get("s") or 1
+            d = (t.shape[1] - k) // s + 1
+            idx = np.arange(d) * s
+            t = sum(t[:, idx + ky][:, :, idx + kx] for ky in range(k) for kx in range(k)) / (k * k)
+        elif kind == "square":
+            t = t * t
+        elif kind == "flatten":
+            t = t.reshape(-1)
+        elif kind == "dense":
+            x = t.reshape(-1)
+            n = l["out"] * x.size
+            t = w[o:o + n].reshape(l["out"], x.size) @ x + w[o + n:o + n + l["out"]]
+            o += n + l["out"]
+    assert o == w.size
+    return np.asarray(t).reshape(-1)

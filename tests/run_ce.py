@@ -3,7 +3,7 @@ n_slots = 16384 -> N = 2^15, SubConv groups, the 1x1 conv-pack repack, ten
 stages) encrypted through `hegpu_cli run` and compare the logits with the
 FP64 forward pass and the per-stage HOP report with the slot-level execute.
 
-    python tools/run_ce.py [--model ce] [--seed 1] [--sigma 0.05]
+    python tests/run_ce.py [--model ce] [--seed 1] [--sigma 0.05]
 
 Needs a GPU with ~150 GB free (about 1200 rotation keys of 47 MB and the
 fused key x mask tables of the 845-diagonal grouped HS stages)."""

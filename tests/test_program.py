@@ -148,6 +148,26 @@ def test_default_policy_changes_the_linear_stages():
         HS.lower(dict(me, n_slots=16))
 
 
+def test_workload_builtins_and_forward_match_the_restatement():
+    """the product-side builtin model files and FP64 forward used by
+    bench_configs.py --model (paper_2110_08321_b200/workloads.py) against the
+    restated reference builtins and ref_forward"""
+    from paper_2110_08321_b200 import hegpu as H
+    from paper_2110_08321_b200.workloads import BUILTIN_MODEL_JSON, model_forward
+    for name in ("cryptonets-hs", "me", "ce"):
+        m = H.Model.parse(BUILTIN_MODEL_JSON[name])
+        ref = H.Model.parse(HS.model_json(HS.builtin_model(name)))
+        assert (m.in_c, m.in_d, m.n_slots, m.layers) == (ref.in_c, ref.in_d, ref.n_slots, ref.layers)
+    mini = H.Model.parse(BUILTIN_MODEL_JSON["ce-mini"])
+    assert mini.layers == H.Model.parse(HS.model_json(CE_MINI)).layers
+    for model in (CE_MINI, HS.builtin_model("me"), LD_MINI):
+        flat, img = _weights(model, 8, 0.1)
+        m = H.Model.parse(HS.model_json(model))
+        got = model_forward(m.layers, m.in_c, m.in_d, flat, img)
+        want = HS.ref_forward_model(model, HS.split_model_weights(model, flat), img)
+        assert np.abs(got - want).max() < 1e-9
+
+
 def test_cpp_lowering_errors():
     from paper_2110_08321_b200 import hegpu as H
     bad = dict(CE_MINI, n_slots=1024)  # Pool1-Conv2: fused 150 x 1176 exceeds n_slots

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.gpu
 def test_ce_builtin_runs_encrypted():
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "run_ce.py"), "--model", "ce"],
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "run_ce.py"), "--model", "ce"],
                        capture_output=True, text=True, timeout=1500)
     assert r.returncode == 0, r.stdout + r.stderr
     d = json.loads(r.stdout.strip().splitlines()[-1])

@@ -687,7 +687,7 @@ int cmd_verify(const Args& a) {
     std::printf("kernel-vs-oracle: %d cases, max relative error %.3g\n", a.cases, max_err);
   }
   double e2e = 0.0;
-  for (const char* name : {"cryptonets-hs", "me", "ce-mini"}) {  // ce itself: tools/run_ce.py (58 GB of keys)
+  for (const char* name : {"cryptonets-hs", "me", "ce-mini"}) {  // ce itself: tests/run_ce.py (58 GB of keys)
     Model m;
     load_model(name, m);
     const int draws = std::max(1, std::min(a.cases, 3));
@@ -702,7 +702,7 @@ int cmd_verify(const Args& a) {
     }
     std::printf("end-to-end %s: %d draws, max relative error %.3g\n", name, draws, e2e);
   }
-  std::printf("end-to-end ce: not part of verify (N = 2^15 with ~1200 rotation keys; see tools/run_ce.py); ce-mini runs its stages\n");
+  std::printf("end-to-end ce: not part of verify (N = 2^15 with ~1200 rotation keys; see tests/run_ce.py); ce-mini runs its stages\n");
   if (e2e >= 1e-3) ok = false;
   std::printf("max observed error: %.3g\n", std::max(max_err, e2e));
   std::printf("%s\n", ok ? "verify: PASS" : "verify: FAIL");
