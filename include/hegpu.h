@@ -201,6 +201,17 @@ void hegpu_conv_plan_destroy(hegpu_conv_plan* plan);
 int hegpu_conv_plan_run(hegpu_ctx* ctx, const hegpu_conv_plan* plan, const hegpu_ct* taps, hegpu_ct* maps_out);
 /* merge_maps (convlower.cpp:145-160): maps count B*c ordered [b][j];
  * out count B; CapacityError if c*w > S */
+/* conv_packed_forward with the reference's masked constant plaintexts
+ * pt(w[co,t] on slots < w_used) (convlower.cpp:55-63) for taps that are NOT
+ * zero beyond w_used -- the RepackConv stage's rotated group ciphertexts
+ * (netcompile.cpp:352-379).  taps: ntaps * B ciphertexts TAP-MAJOR [t][b] at
+ * `level`; maps: c_out * B MAP-MAJOR [co][b] at level - 1 (MAC + masked bias
+ * + rescale, one kernel over every map); metered as conv_packed_forward */
+typedef struct hegpu_masked_conv hegpu_masked_conv;
+int hegpu_masked_conv_create(hegpu_ctx* ctx, int ntaps, const double* weights, int c_out, const double* bias,
+                             int w_used, int level, double tap_scale, hegpu_masked_conv** out);
+void hegpu_masked_conv_destroy(hegpu_masked_conv* plan);
+int hegpu_masked_conv_run(hegpu_ctx* ctx, const hegpu_masked_conv* plan, const hegpu_ct* taps, hegpu_ct* maps);
 int hegpu_merge_maps(hegpu_ctx* ctx, const hegpu_ct* maps, int c, int64_t w, hegpu_ct* out);
 /* extract_diagonals (matvec.cpp:45-65) + encode, once per matrix (offline);
  * A is m x n row-major, input ciphertexts at `level` */

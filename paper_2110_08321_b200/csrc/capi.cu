@@ -749,6 +749,51 @@ extern "C" int hegpu_conv_plan_run(hegpu_ctx* h, const hegpu_conv_plan* p, const
   });
 }
 
+struct hegpu_masked_conv {
+  std::unique_ptr<MaskedConv> layer;
+};
+
+extern "C" int hegpu_masked_conv_create(hegpu_ctx* h, int ntaps, const double* weights, int c_out, const double* bias,
+                                        int w_used, int level, double tap_scale, hegpu_masked_conv** out) {
+  if (!h || !weights || !out) return HEGPU_ERR_ARG;
+  Context& c = h->c;
+  return guarded(&c, [&] {
+    need_gpu(c);
+    need(ntaps >= 1 && c_out >= 1, HEGPU_ERR_SHAPE, "masked_conv: bad shape");
+    auto* p = new hegpu_masked_conv{nullptr};
+    try {
+      p->layer = std::make_unique<MaskedConv>(c, ntaps, c_out, weights, bias, w_used, level, tap_scale);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
+extern "C" void hegpu_masked_conv_destroy(hegpu_masked_conv* p) {
+  if (!p) return;
+  try { bind_device(p->layer ? p->layer->ctx : nullptr); } catch (...) {}
+  delete p;
+}
+
+extern "C" int hegpu_masked_conv_run(hegpu_ctx* h, const hegpu_masked_conv* p, const hegpu_ct* taps, hegpu_ct* maps) {
+  if (!h || !p || !taps || !maps) return HEGPU_ERR_ARG;
+  Context& c = h->c;
+  return guarded(&c, [&] {
+    const int ntaps = p->layer->ntaps, c_out = p->layer->c_out;
+    need(taps->b.level == p->layer->level && taps->b.count % ntaps == 0, HEGPU_ERR_SHAPE,
+         "masked_conv_run: taps must be ntaps * B at the plan level");
+    const int B = taps->b.count / ntaps;
+    need(maps->b.count == B * c_out && maps->b.level == taps->b.level - 1, HEGPU_ERR_SHAPE,
+         "masked_conv_run: maps must be c_out * B at level - 1");
+    p->layer->run(c, taps->b, maps->b);
+    c.meter.bump(HEGPU_MUL_PC, (int64_t)B * ntaps * c_out);
+    c.meter.bump(HEGPU_ADD_CC, (int64_t)B * (ntaps - 1) * c_out);
+    c.meter.bump(HEGPU_ADD_PC, (int64_t)B * c_out);
+  });
+}
+
 extern "C" int hegpu_merge_maps(hegpu_ctx* h, const hegpu_ct* maps, int nmaps, int64_t w, hegpu_ct* out) {
   if (!h || !maps || !out) return HEGPU_ERR_ARG;
   Context& c = h->c;

@@ -284,6 +284,11 @@ void launch_conv_imma(Context& c, const u64d* taps, int B, int ntaps, int l, con
 // weights (the merged first layer), pw split-31 Montgomery, pbias standard
 void launch_conv_pt(Context& c, const u64d* taps, int B, int ntaps, int regions, int l, const u64d* pw,
                     const u64d* pbias, u64d* out);
+// masked-constant conv over every output map in one launch: taps [ntaps][B]
+// (tap-major), pw [c_out][ntaps][l][N] split-31 Montgomery, pbias [c_out][l][N]
+// standard form, out [c_out][B] (map-major), all at level l
+void launch_conv_masked(Context& c, const u64d* taps, int B, int ntaps, int c_out, int l, const u64d* pw,
+                        const u64d* pbias, u64d* out);
 void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, const u64d* wmont /*[c_out][ntaps][l]*/,
                      int c_out, const u64d* bias /*[c_out][l][N] mont*/, u64d* out);
 struct HsDiagTable {

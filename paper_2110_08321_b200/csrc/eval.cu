@@ -273,6 +273,25 @@ __global__ void __launch_bounds__(kTpb) k_conv_pt(PrimeTable pt, const u64d* __r
   out[(size_t)b * ct + (size_t)p * l * N + (size_t)t * N + k] = v;
 }
 
+// masked-constant conv (the RepackConv stage, proj/src/netcompile.cpp:352-379):
+//   out[co][b][p][t][k] = sum_s tap[s][b][p][t][k] * P[co][s][t][k] (+ bias[co] on part 0)
+// taps tap-major [s][b], outputs map-major [co][b]; one thread per output word
+__global__ void __launch_bounds__(kTpb) k_conv_masked(PrimeTable pt, const u64d* __restrict__ taps, int B, int G,
+                                                      int l, int N, const u64d* __restrict__ pw,
+                                                      const u64d* __restrict__ pbias, u64d* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.y % l, p = blockIdx.y / l, b = blockIdx.z % B, co = blockIdx.z / B;
+  if (k >= N) return;
+  const DevPrime pr = pt.p[t];
+  const size_t ct = (size_t)2 * l * N;
+  const u64d* x = taps + (size_t)b * ct + (size_t)p * l * N + (size_t)t * N + k;
+  const u64d* w = pw + (size_t)co * G * l * N + (size_t)t * N + k;
+  u64d v = pr.q >> 40 ? conv_pt_mac<AccC>(x, w, G, (size_t)B * ct, (size_t)l * N, pr)
+                      : conv_pt_mac<Acc20>(x, w, G, (size_t)B * ct, (size_t)l * N, pr);
+  if (p == 0) v = add_mod_d(v, __ldg(pbias + ((size_t)co * l + t) * N + k), pr.q);
+  out[((size_t)co * B + b) * ct + (size_t)p * l * N + (size_t)t * N + k] = v;
+}
+
 // merge inner product, summed over the G rotated maps of each image:
 //   acc[img][p][t] = sum_j sum_d D[img*G + j][d][t] * key_j[d][p][pi(t)]
 __global__ void __launch_bounds__(kTpb) k_ks_inner_sum(PrimeTable pt, const u64d* __restrict__ D, int nimg, int G,
@@ -991,6 +1010,17 @@ void launch_conv_pt(Context& c, const u64d* taps, int B, int ntaps, int regions,
   const double bytes = 8.0 * N * l * (2.0 * B * G + G + 1 + 2.0 * B);
   LAUNCH_BO(c, "k_conv_mac", bytes, 2.0 * N * l * B * G,
             k_conv_pt<<<grid, kTpb, 0, c.stream>>>(c.primes, taps, G, l, N, pw, pbias, out));
+}
+
+void launch_conv_masked(Context& c, const u64d* taps, int B, int ntaps, int c_out, int l, const u64d* pw,
+                        const u64d* pbias, u64d* out) {
+  const int N = c.N();
+  if ((size_t)B * c_out > 65535) fail(HEGPU_ERR_ARG, "conv_masked: batch * maps exceeds the grid");
+  dim3 grid((N + kTpb - 1) / kTpb, 2 * l, B * c_out);
+  // per output word: the taps and the map's plaintexts once, the output once
+  const double bytes = 8.0 * N * l * (2.0 * B * ntaps * c_out + (double)ntaps * c_out + c_out + 2.0 * B * c_out);
+  LAUNCH_BO(c, "k_conv_mac", bytes, 2.0 * N * l * B * ntaps * c_out,
+            k_conv_masked<<<grid, kTpb, 0, c.stream>>>(c.primes, taps, B, ntaps, l, N, pw, pbias, out));
 }
 
 void launch_conv_mac(Context& c, const u64d* taps, int B, int ntaps, int l, const u64d* w, int c_out,

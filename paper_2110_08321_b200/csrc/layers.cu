@@ -177,6 +177,52 @@ void ConvLayer::make_merged(Context& c, const double* weights, const double* bia
   merged = true;
 }
 
+MaskedConv::MaskedConv(Context& c, int ntaps_, int c_out_, const double* weights, const double* bias_vals,
+                       int w_used, int level_, double tap_scale)
+    : ntaps(ntaps_), c_out(c_out_), level(level_), ctx(&c) {
+  const int N = c.N();
+  need(w_used >= 0 && w_used <= c.S(), HEGPU_ERR_CAPACITY, "masked conv: w exceeds the slots");
+  need(level >= 2 && level <= c.L(), HEGPU_ERR_CAPACITY, "masked conv: level must leave a prime to rescale");
+  const double qlast = (double)c.P->q(level - 1);
+  const size_t rows = (size_t)c_out * ntaps;
+  std::vector<u64> wire(rows * level * N), bw((size_t)c_out * level * N);
+#pragma omp parallel for schedule(dynamic)
+  for (long r = 0; r < (long)rows; ++r) {
+    std::vector<double> z(w_used, weights[r]);
+    c.client->encode(z.data(), w_used, qlast, level, false, wire.data() + (size_t)r * level * N);
+  }
+#pragma omp parallel for schedule(dynamic)
+  for (int co = 0; co < c_out; ++co) {
+    std::vector<double> z(w_used, bias_vals ? bias_vals[co] : 0.0);
+    c.client->encode(z.data(), w_used, tap_scale * qlast, level, false, bw.data() + (size_t)co * level * N);
+  }
+  CK(cudaMalloc((void**)&pw, wire.size() * 8));
+  upload_mont(c, wire, pw, rows * level, level, -1);
+  launch_split31(c, pw, wire.size());
+  CK(cudaMalloc((void**)&pbias, bw.size() * 8));
+  u64d* stage = c.alloc(bw.size());
+  CK(cudaMemcpyAsync(stage, bw.data(), bw.size() * 8, cudaMemcpyHostToDevice, c.stream));
+  launch_wire_to_slot(c, stage, pbias, (size_t)c_out * level, 0, level, -1);  // standard form
+  c.free(stage);
+  CK(cudaStreamSynchronize(c.stream));
+}
+
+MaskedConv::~MaskedConv() {
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(pw);
+  cudaFree(pbias);
+}
+
+void MaskedConv::run(Context& c, const CtBatch& taps, CtBatch& maps) {
+  const int B = taps.count / ntaps, N = c.N();
+  u64d* prod = c.alloc((size_t)B * c_out * 2 * level * N);
+  launch_conv_masked(c, taps.d, B, ntaps, c_out, level, pw, pbias, prod);
+  CtBatch pb{&c, B * c_out, level, taps.scale * (double)c.P->q(level - 1), prod};
+  eval_rescale(c, pb, maps);
+  maps.scale = taps.scale;
+  c.free(prod);
+}
+
 ConvLayer::~ConvLayer() {
   cudaStreamSynchronize(ctx->stream);
   cudaFree(pw);

@@ -49,6 +49,24 @@ struct ConvLayer {
   Context* ctx;
 };
 
+// conv_packed_forward with the reference's MASKED constant plaintexts
+// pt(w[co,t] on slots < w_used) (convlower.cpp:55-63) for taps whose slots
+// beyond w_used are not zero -- the RepackConv stage's rotated group
+// ciphertexts (netcompile.cpp:352-379).  taps [ntaps][B] tap-major at
+// `level`, maps [c_out][B] map-major at level - 1 (MAC + bias + rescale).
+struct MaskedConv {
+  int ntaps = 0, c_out = 0, level = 0;
+  u64d* pw = nullptr;     // [c_out][ntaps][level][N] split-31 Montgomery, scale q_{level-1}
+  u64d* pbias = nullptr;  // [c_out][level][N] standard form, scale tap_scale * q_{level-1}
+  Context* ctx = nullptr;
+  MaskedConv(Context& c, int ntaps, int c_out, const double* weights, const double* bias_vals, int w_used, int level,
+             double tap_scale);
+  ~MaskedConv();
+  MaskedConv(const MaskedConv&) = delete;
+  MaskedConv& operator=(const MaskedConv&) = delete;
+  void run(Context& c, const CtBatch& taps, CtBatch& maps);
+};
+
 void merge_maps(Context& c, const CtBatch& maps, int nmaps, int64_t w, CtBatch& out);
 void square_layer(Context& c, const CtBatch& a, CtBatch& out);  // tensor + relin + rescale
 

@@ -13,7 +13,10 @@
 // Linear(LoLa-dense): two primes.  masked_prefix (netcompile.cpp:424) is
 // elided as in net.cu: every consumer's plaintexts are zero beyond the valid
 // prefix (HS masks, LoLa rows, the RepackConv's masked constants).
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -52,8 +55,8 @@ struct StagePlan {
   bool maps_in = false;
   // ConvPack
   hegpu_conv_plan* conv = nullptr;
-  // RepackConv: masked constants [c_out][c_in] and biases [c_out]
-  std::vector<hegpu_pt*> rp_w, rp_b;
+  // RepackConv: the masked-constant conv over every map (hegpu_masked_conv)
+  hegpu_masked_conv* repack = nullptr;
   // Linear, per group
   std::vector<hegpu_hs_plan*> hs;
   std::vector<hegpu_lola_plan*> lola;
@@ -75,8 +78,7 @@ struct hegpu_prog {
   ~hegpu_prog() {
     for (auto& p : plans) {
       hegpu_conv_plan_destroy(p.conv);
-      for (auto* x : p.rp_w) hegpu_pt_destroy(x);
-      for (auto* x : p.rp_b) hegpu_pt_destroy(x);
+      hegpu_masked_conv_destroy(p.repack);
       for (auto* x : p.hs) hegpu_hs_plan_destroy(x);
       for (auto* x : p.lola) hegpu_lola_plan_destroy(x);
       for (auto* x : p.bias) hegpu_pt_destroy(x);
@@ -227,17 +229,8 @@ void build(hegpu_prog& P, const double* w, size_t count) {
           for (int j = 1; j < per; ++j) rots.push_back((S - (int64_t)j * wd % S) % S);  // rotate_left(j w)
         }
         const double* W = w + off[st.layer_idx[0]];
-        const double* B = W + (size_t)c_out * c_in;
-        const double qlast = (double)primes[l - 1];
-        std::vector<double> z(wd);
-        for (int co = 0; co < c_out; ++co) {
-          for (int t = 0; t < c_in; ++t) {
-            std::fill(z.begin(), z.end(), W[(size_t)co * c_in + t]);
-            pl.rp_w.push_back(make_pt(h, z.data(), wd, qlast, l, P.N));
-          }
-          std::fill(z.begin(), z.end(), B[co]);
-          pl.rp_b.push_back(make_pt(h, z.data(), wd, scale * qlast, l, P.N));
-        }
+        ok(h, hegpu_masked_conv_create(h, c_in, W, c_out, W + (size_t)c_out * c_in, wd, l, scale, &pl.repack),
+           st.label.c_str());
         shape = prog_apply_layer(shape, ly, st.label);
         ncts = c_out;
         --l;
@@ -325,10 +318,17 @@ void run(hegpu_prog& P, hegpu_ct* input, hegpu_ct* out) {
     ok(h, hegpu_ct_view(src, first, count, &v), "ct_view");
     return CtH(v);
   };
+  // HEGPU_PROG_TIMING=1: synchronise after every stage and print its wall time (diagnostics)
+  static const bool timing = [] {
+    const char* e = std::getenv("HEGPU_PROG_TIMING");
+    return e && e[0] == '1';
+  }();
+  auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   for (size_t si = 0; si < P.stages.size(); ++si) {
     const ProgStage& st = P.stages[si];
     const StagePlan& pl = P.plans[si];
     ok(h, hegpu_begin_stage(h, st.label.c_str()), "begin_stage");
+    const double t_stage = timing ? (hegpu_sync(h), now()) : 0.0;
     CtH nxt;
     bool nxt_image_major = false;
     switch (st.kind) {
@@ -393,23 +393,11 @@ void run(hegpu_prog& P, hegpu_ct* input, hegpu_ct* out) {
           }
           taps = rot.p;
         }
-        CtH prod = make_ct(h, c_out * B, l), tmp = make_ct(h, B, l);
-        for (int co = 0; co < c_out; ++co) {
-          CtH acc = sub(prod.p, co * B, B);
-          for (int t = 0; t < c_in; ++t) {
-            CtH tap = sub(taps, t * B, B);
-            ok(h, hegpu_ct_set_scale(tap.p, pl.scale_in), "ct_set_scale");
-            if (t == 0) {
-              ok(h, hegpu_mul_plain(h, tap.p, pl.rp_w[(size_t)co * c_in], acc.p), st.label.c_str());
-            } else {
-              ok(h, hegpu_mul_plain(h, tap.p, pl.rp_w[(size_t)co * c_in + t], tmp.p), st.label.c_str());
-              ok(h, hegpu_add(h, acc.p, tmp.p, acc.p), st.label.c_str());
-            }
-          }
-          ok(h, hegpu_add_plain(h, acc.p, pl.rp_b[co], acc.p), st.label.c_str());
-        }
+        // the masked-constant MAC over every map, the masked bias and the
+        // rescale in one operator (maps map-major [co][b])
+        ok(h, hegpu_ct_set_scale(taps, pl.scale_in), "ct_set_scale");
         nxt = make_ct(h, c_out * B, pl.level_out);
-        ok(h, hegpu_rescale(h, prod.p, nxt.p), st.label.c_str());
+        ok(h, hegpu_masked_conv_run(h, pl.repack, taps, nxt.p), st.label.c_str());
         break;
       }
       case HEGPU_STAGE_LINEAR: {
@@ -431,6 +419,10 @@ void run(hegpu_prog& P, hegpu_ct* input, hegpu_ct* out) {
       }
     }
     ok(h, hegpu_ct_set_scale(nxt.p, pl.scale_out), "ct_set_scale");
+    if (timing) {
+      hegpu_sync(h);
+      std::fprintf(stderr, "prog stage %-14s B=%d  %.3f ms\n", st.label.c_str(), B, (now() - t_stage) * 1e3);
+    }
     cur = std::move(nxt);
     x = cur.p;
     image_major = nxt_image_major;

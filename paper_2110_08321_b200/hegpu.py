@@ -178,6 +178,9 @@ def lib():
             "hegpu_net_wait": (i, [vp]),
             "hegpu_model_set_default_policy": (i, [vp, i]),
             "hegpu_model_set_n_slots": (i, [vp, i]),
+            "hegpu_masked_conv_create": (i, [vp, i, f64p, i, vp, i, i, d, pp]),
+            "hegpu_masked_conv_destroy": (None, [vp]),
+            "hegpu_masked_conv_run": (i, [vp, vp, vp, vp]),
             "hegpu_ct_view": (i, [vp, i, i, pp]),
             "hegpu_ct_copy": (i, [vp, vp]),
             "hegpu_ct_set_scale": (i, [vp, d]),
