@@ -323,6 +323,7 @@ int hs_imma_chunk_span(int l);
 // with r in [r_lo, r_hi] (span <= hs_tc_chunk_span), A tables `at` built by
 // launch_hs_tc_tiles (hs_tc_table_bytes); ce [np][8] = 2^(8e) R mod q, pR[t] = P R mod q_t
 bool hs_tc_enabled();
+constexpr int kHsTcMaxLevel = 8;  // k_hs_tc<J> is instantiated for J = l + 1 <= 9
 int hs_tc_chunk_span(int l);
 size_t hs_tc_table_bytes(Context& c, int l, int span);
 void launch_hs_tc_tiles(Context& c, int l, const struct HsDiagTable& t, const u64d* pR, const int* rdiag, int r_lo,

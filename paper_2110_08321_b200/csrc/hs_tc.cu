@@ -423,7 +423,7 @@ void launch_hs_tc_tiles(Context& c, int l, const HsDiagTable& t, const u64d* pR,
                                                          pR, c.L(), c.N(), nks, r_lo, r_hi, a4));              \
     break;
   switch (l + 1) {
-    HT_TILES(2) HT_TILES(3) HT_TILES(4) HT_TILES(5) HT_TILES(6) HT_TILES(7)
+    HT_TILES(2) HT_TILES(3) HT_TILES(4) HT_TILES(5) HT_TILES(6) HT_TILES(7) HT_TILES(8) HT_TILES(9)
     default: fail(HEGPU_ERR_ARG, "hs_tc: level out of range");
   }
 #undef HT_TILES
@@ -494,7 +494,7 @@ void launch_hs_tc(Context& c, const u64d* v, int B, int l, const u64d* D, int r_
     break;                                                                                           \
   }
   switch (J) {
-    HT_GO(2) HT_GO(3) HT_GO(4) HT_GO(5) HT_GO(6) HT_GO(7)
+    HT_GO(2) HT_GO(3) HT_GO(4) HT_GO(5) HT_GO(6) HT_GO(7) HT_GO(8) HT_GO(9)
     default: fail(HEGPU_ERR_ARG, "hs_tc: level out of range");
   }
 #undef HT_GO

@@ -508,8 +508,11 @@ bool HsPlan::use_imma(Context& c, int B, int i_lo, int i_hi) const {
   const int64_t span = diag.back().right - diag.front().right + 1;
   // dense bands only: the fragments cover the whole rotation span (a sparse
   // band -- e.g. a convolution's matrix -- would store mostly zero tiles)
+  // the tcgen05 kernel is instantiated up to level 8 (J = l + 1 <= 9), the mma.sync one up to 6
+  const bool level_ok = hs_imma_supported(c, level) ||
+                        (hs_tc_enabled() && level >= 1 && level <= kHsTcMaxLevel && hs_imma_supported(c, 6));
   return B >= hs_imma_min_batch() && i_lo == 0 && i_hi == (int)diag.size() && span >= hs_imma_min_span() &&
-         4 * (int64_t)diag.size() >= span && hs_imma_supported(c, level);
+         4 * (int64_t)diag.size() >= span && level_ok;
 }
 
 // shared by the mma.sync and tcgen05 paths: epilogue constants, P mod q_t,
@@ -575,10 +578,22 @@ void HsPlan::ensure_imma(Context& c) {
 
 // the tcgen05 A tables: chunks of kept diagonals whose r span fits the
 // window ring (hs_tc_chunk_span), balanced like the mma.sync chunks
-void HsPlan::ensure_tc(Context& c) {
-  if (tc_built) return;
-  ensure_imma_consts(c);  // rdiag
+bool HsPlan::ensure_tc(Context& c) {
+  if (tc_built) return true;
+  if (tc_unfit) return false;
   const int l = level, N = c.N(), np = c.P->np();
+  {  // the A tables are as large again as the fused keys: build them only if they fit
+    const int smax0 = hs_tc_chunk_span(l), rtot0 = (int)(diag.back().right - diag[0].right) + 1;
+    const int nch0 = (rtot0 + smax0 - 1) / smax0, span0 = (rtot0 + nch0 - 1) / nch0;
+    const size_t need_bytes = (size_t)nch0 * hs_tc_table_bytes(c, l, span0);
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    if (need_bytes + (total_b >> 4) > free_b) {  // keep 1/16 of the device for the working set
+      tc_unfit = true;
+      return false;
+    }
+  }
+  ensure_imma_consts(c);  // rdiag
   std::vector<u64> ce((size_t)np * 8);
   for (int pi = 0; pi < np; ++pi) {
     const u64 q = c.P->q(pi);
@@ -618,14 +633,14 @@ void HsPlan::ensure_tc(Context& c) {
   }
   CK(cudaStreamSynchronize(c.stream));
   tc_built = true;
+  return true;
 }
 
 void HsPlan::accumulate(Context& c, const CtBatch& v, int i_lo, int i_hi, u64d* acc, u64d* cacc) {
   const int B = v.count, l = level, N = c.N();
   ensure_keys(c);
   for (int i = i_lo; i < i_hi; ++i) c.ks[KS_INNER] += diag[i].shift != 0 ? B : 0;
-  if (use_imma(c, B, i_lo, i_hi) && hs_tc_enabled() && l <= 6) {
-    ensure_tc(c);
+  if (use_imma(c, B, i_lo, i_hi) && hs_tc_enabled() && l <= kHsTcMaxLevel && ensure_tc(c)) {
     u64d* tmp = c.alloc((size_t)B * l * N);
     u64d* D = c.alloc((size_t)B * l * (l + 1) * N);
     ks_modup(c, v.d + (size_t)l * N, (long)v.stride(), B, l, nullptr, tmp, D);
@@ -637,7 +652,7 @@ void HsPlan::accumulate(Context& c, const CtBatch& v, int i_lo, int i_hi, u64d* 
     c.free(D);
     return;
   }
-  if (use_imma(c, B, i_lo, i_hi)) {
+  if (use_imma(c, B, i_lo, i_hi) && hs_imma_supported(c, level)) {
     ensure_imma(c);
     u64d* tmp = c.alloc((size_t)B * l * N);
     u64d* D = c.alloc((size_t)B * l * (l + 1) * N);

@@ -104,8 +104,10 @@ struct HsPlan {
   std::vector<TcChunk> tc;
   u64d* tc_ce = nullptr;  // [np][8] 2^(8e) R mod q
   u64d* tc_pR = nullptr;  // [level] P R mod q_t
-  bool tc_built = false;
-  void ensure_tc(Context& c);
+  bool tc_built = false, tc_unfit = false;
+  // builds the A tables on first use; false if they do not fit the free
+  // device memory (the caller falls back to the integer kernels)
+  bool ensure_tc(Context& c);
   bool use_imma(Context& c, int B, int i_lo, int i_hi) const;
   // the log-depth fold (matvec.cpp:101-103) as hoisted rotation sums: the
   // `folds` doublings in groups of <= kMaxFoldGroup (fold_groups), each a

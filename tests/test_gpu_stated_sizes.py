@@ -208,3 +208,31 @@ def test_cfg4_conv_layer_at_size(c_in, k, c_out, kcb, monkeypatch):
     for co in (0, c_out // 2, c_out - 1):
         dec = ck.decrypt_decode(got[co * per:(co + 1) * per], 1, DELTA)[:w_used]
         assert np.abs(dec - ref[co].ravel()).max() < 1e-5, co
+
+
+@pytest.mark.parametrize("l", [7, 8])
+def test_hs_tensor_core_at_levels_7_and_8(l):
+    """the grouped HS stages of the `ce` builtin run at level 7 (L = 9): the
+    tcgen05 HS kernel is instantiated up to level 8 (J = l + 1 <= 9); a
+    batch of 8 images equals the single-ciphertext (integer kernel) runs and
+    the CPU oracle"""
+    from oracle import ckks_pipeline as P
+    from oracle.ckks import Ckks
+    from paper_2110_08321_b200 import hegpu as H
+    qb = [45] + [40] * 8
+    ctx = H.Context(11, qb, 45, seed=19)
+    ck = Ckks(11, qb, 45, seed=19)
+    rng = np.random.default_rng(100 + l)
+    m, n, B = 48, 300, 8
+    A = rng.normal(0, 0.05, (m, n))
+    zs = [rng.uniform(-1, 1, n) for _ in range(B)]
+    cts = [ck.encrypt(ck.encode(z, 2.0 ** 40, l), l, 900 + i) for i, z in enumerate(zs)]
+    plan = ctx.hs_plan(A, l, True)
+    ctx.gen_rotation_keys(plan.rotations())
+    got = ctx.hs_matvec(plan, ctx.ct(B, l, np.concatenate(cts), 2.0 ** 40), ctx.ct(B, l - 1)).download().reshape(B, -1)
+    for i in (0, B - 1):
+        one = ctx.hs_matvec(plan, ctx.ct(1, l, cts[i], 2.0 ** 40), ctx.ct(1, l - 1)).download()
+        assert np.array_equal(got[i], one), i
+    assert np.array_equal(got[3], P.hs_matvec(ck, cts[3], l, A, True))
+    for i in range(B):
+        assert np.abs(ck.decrypt_decode(got[i], l - 1, 2.0 ** 40)[:m] - A @ zs[i]).max() < 1e-4
