@@ -420,9 +420,15 @@ extern "C" int hegpu_ct_create(hegpu_ctx* h, int count, int level, hegpu_ct** ou
   return guarded(&c, [&] {
     need_gpu(c);
     need(count >= 1 && level >= 1 && level <= c.L(), HEGPU_ERR_ARG, "ct_create: bad count/level");
+    // from the context's stream-ordered pool: handles that live for one
+    // stage of a driver loop (hegpu_prog) cost no cudaMalloc / cudaFree
     auto* t = new hegpu_ct{CtBatch{&c, count, level, 1.0, nullptr}};
-    cudaError_t e = cudaMalloc((void**)&t->b.d, t->b.words() * 8);
-    if (e != cudaSuccess) { delete t; CK(e); }
+    try {
+      t->b.d = c.alloc(t->b.words());
+    } catch (...) {
+      delete t;
+      throw;
+    }
     *out = t;
   });
 }
@@ -433,9 +439,11 @@ extern "C" void hegpu_ct_destroy(hegpu_ct* t) {
     delete t;
     return;
   }
-  try { bind_device(t->b.ctx); } catch (...) {}
-  cudaStreamSynchronize(t->b.ctx->stream);
-  cudaFree(t->b.d);
+  try {
+    bind_device(t->b.ctx);
+    t->b.ctx->free(t->b.d);  // stream-ordered: after everything enqueued so far
+  } catch (...) {
+  }
   delete t;
 }
 
