@@ -63,7 +63,9 @@ typedef struct hegpu_net hegpu_net;
 #define HEGPU_MAX_Q 15
 
 typedef struct {
-  int log_n;                 /* ring degree N = 2^log_n, slots S = N/2 */
+  int log_n;                 /* ring degree N = 2^log_n, slots S = N/2; the device evaluator takes
+                              * 5 <= log_n <= 15 (log_n = 15 needs every prime below 2^45: those rows
+                              * run on the FP64 NTT, split over two-CTA clusters) */
   int n_q;                   /* Q chain length L (L-1 rescales) */
   int q_bits[HEGPU_MAX_Q];   /* bit sizes of q_0..q_{L-1} (<= 60) */
   int p_bits;                /* special prime P (<= 60) */
