@@ -165,6 +165,9 @@ int hegpu_ct_view(hegpu_ct* src, int first, int count, hegpu_ct** out);
 /* device copy between handles of equal count and level (value semantics of
  * SlotVector assignment) */
 int hegpu_ct_copy(hegpu_ct* dst, const hegpu_ct* src);
+/* dst[dst_first + i] = src[src_first + i * src_stride], i < count (one strided
+ * device copy): regroups a batch between image-major and unit-major order */
+int hegpu_ct_gather(hegpu_ct* dst, int dst_first, const hegpu_ct* src, int src_first, int src_stride, int count);
 int hegpu_ct_set_scale(hegpu_ct* ct, double scale);
 int hegpu_pt_create(hegpu_ctx* ctx, int count, int level, int with_p, hegpu_pt** out);
 void hegpu_pt_destroy(hegpu_pt* pt);

@@ -472,6 +472,23 @@ extern "C" int hegpu_ct_copy(hegpu_ct* dst, const hegpu_ct* src) {
   });
 }
 
+extern "C" int hegpu_ct_gather(hegpu_ct* dst, int dst_first, const hegpu_ct* src, int src_first, int src_stride,
+                               int count) {
+  if (!dst || !src) return HEGPU_ERR_ARG;
+  Context& c = *src->b.ctx;
+  return guarded(&c, [&] {
+    need(dst->b.ctx == src->b.ctx, HEGPU_ERR_ARG, "ct_gather: handles from different contexts");
+    need(dst->b.level == src->b.level, HEGPU_ERR_SHAPE, "ct_gather: level mismatch");
+    need(count >= 1 && src_stride >= 1 && dst_first >= 0 && src_first >= 0 && dst_first + count <= dst->b.count &&
+             src_first + (int64_t)(count - 1) * src_stride < src->b.count,
+         HEGPU_ERR_RANGE, "ct_gather: range outside a batch");
+    const size_t ct = src->b.stride() * 8;
+    CK(cudaMemcpy2DAsync(dst->b.d + (size_t)dst_first * dst->b.stride(), ct,
+                         src->b.d + (size_t)src_first * src->b.stride(), ct * (size_t)src_stride, ct, (size_t)count,
+                         cudaMemcpyDeviceToDevice, c.stream));
+  });
+}
+
 extern "C" int hegpu_ct_set_scale(hegpu_ct* t, double scale) {
   if (!t || !(scale > 0)) return HEGPU_ERR_ARG;
   t->b.scale = scale;

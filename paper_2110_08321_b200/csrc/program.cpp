@@ -339,25 +339,24 @@ void run(hegpu_prog& P, hegpu_ct* input, hegpu_ct* out) {
         break;
       }
       case HEGPU_STAGE_MERGE: {
+        // per group: its maps of every image gathered image-major [b][j]
+        // (one strided copy per image), then ONE batched merge_maps over the
+        // B images into the group's B contiguous outputs
         const int G = st.groups, C = pl.shape_in.c, per = C / G;
         const int64_t wd = (int64_t)pl.shape_in.d * pl.shape_in.d;
         nxt = make_ct(h, G * B, pl.level_out);
-        CtH gather;  // map-major input: one group's maps of one image, made contiguous
-        if (!image_major) gather = make_ct(h, per, pl.level_in);
-        for (int b = 0; b < B; ++b)
-          for (int g = 0; g < G; ++g) {
-            CtH og = sub(nxt.p, g * B + b, 1);
-            if (image_major) {
-              CtH ig = sub(x, b * C + g * per, per);
-              ok(h, hegpu_merge_maps(h, ig.p, per, wd, og.p), st.label.c_str());
-            } else {
-              for (int j = 0; j < per; ++j) {
-                CtH src = sub(x, (g * per + j) * B + b, 1), dst = sub(gather.p, j, 1);
-                ok(h, hegpu_ct_copy(dst.p, src.p), "ct_copy");
-              }
-              ok(h, hegpu_merge_maps(h, gather.p, per, wd, og.p), st.label.c_str());
-            }
+        CtH gather = make_ct(h, B * per, pl.level_in);
+        for (int g = 0; g < G; ++g) {
+          for (int b = 0; b < B; ++b) {
+            if (image_major)  // [b][c] -> maps g*per .. of image b
+              ok(h, hegpu_ct_gather(gather.p, b * per, x, b * C + g * per, 1, per), "ct_gather");
+            else              // [c][b] -> the same maps, stride B
+              ok(h, hegpu_ct_gather(gather.p, b * per, x, g * per * B + b, B, per), "ct_gather");
           }
+          ok(h, hegpu_ct_set_scale(gather.p, pl.scale_in), "ct_set_scale");
+          CtH og = sub(nxt.p, g * B, B);
+          ok(h, hegpu_merge_maps(h, gather.p, per, wd, og.p), st.label.c_str());
+        }
         break;
       }
       case HEGPU_STAGE_SQUARE: {

@@ -183,6 +183,7 @@ def lib():
             "hegpu_masked_conv_run": (i, [vp, vp, vp, vp]),
             "hegpu_ct_view": (i, [vp, i, i, pp]),
             "hegpu_ct_copy": (i, [vp, vp]),
+            "hegpu_ct_gather": (i, [vp, i, vp, i, i, i]),
             "hegpu_ct_set_scale": (i, [vp, d]),
             "hegpu_prog_create": (i, [vp, vp, f64p, sz, pp]),
             "hegpu_prog_destroy": (None, [vp]),
