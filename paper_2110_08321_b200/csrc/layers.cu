@@ -588,7 +588,7 @@ bool HsPlan::ensure_tc(Context& c) {
     const size_t need_bytes = (size_t)nch0 * hs_tc_table_bytes(c, l, span0);
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    if (need_bytes + (total_b >> 4) > free_b) {  // keep 1/16 of the device for the working set
+    if (need_bytes + (total_b >> 3) > free_b) {  // keep 1/8 of the device for the working set
       tc_unfit = true;
       return false;
     }

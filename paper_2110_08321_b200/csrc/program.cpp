@@ -13,6 +13,7 @@
 // Linear(LoLa-dense): two primes.  masked_prefix (netcompile.cpp:424) is
 // elided as in net.cu: every consumer's plaintexts are zero beyond the valid
 // prefix (HS masks, LoLa rows, the RepackConv's masked constants).
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -345,18 +346,22 @@ void run(hegpu_prog& P, hegpu_ct* input, hegpu_ct* out) {
         const int G = st.groups, C = pl.shape_in.c, per = C / G;
         const int64_t wd = (int64_t)pl.shape_in.d * pl.shape_in.d;
         nxt = make_ct(h, G * B, pl.level_out);
-        CtH gather = make_ct(h, B * per, pl.level_in);
-        for (int g = 0; g < G; ++g) {
-          for (int b = 0; b < B; ++b) {
-            if (image_major)  // [b][c] -> maps g*per .. of image b
-              ok(h, hegpu_ct_gather(gather.p, b * per, x, b * C + g * per, 1, per), "ct_gather");
-            else              // [c][b] -> the same maps, stride B
-              ok(h, hegpu_ct_gather(gather.p, b * per, x, g * per * B + b, B, per), "ct_gather");
+        // at most ~256 maps per merge call (its ModUp digits are (per - 1) l (l + 1) limbs per image)
+        const int bc = std::max(1, std::min(B, 256 / std::max(1, per)));
+        CtH gather = make_ct(h, bc * per, pl.level_in);
+        for (int g = 0; g < G; ++g)
+          for (int b0 = 0; b0 < B; b0 += bc) {
+            const int nb = std::min(bc, B - b0);
+            for (int b = b0; b < b0 + nb; ++b) {
+              if (image_major)  // [b][c] -> maps g*per .. of image b
+                ok(h, hegpu_ct_gather(gather.p, (b - b0) * per, x, b * C + g * per, 1, per), "ct_gather");
+              else              // [c][b] -> the same maps, stride B
+                ok(h, hegpu_ct_gather(gather.p, (b - b0) * per, x, g * per * B + b, B, per), "ct_gather");
+            }
+            ok(h, hegpu_ct_set_scale(gather.p, pl.scale_in), "ct_set_scale");
+            CtH gv = sub(gather.p, 0, nb * per), og = sub(nxt.p, g * B + b0, nb);
+            ok(h, hegpu_merge_maps(h, gv.p, per, wd, og.p), st.label.c_str());
           }
-          ok(h, hegpu_ct_set_scale(gather.p, pl.scale_in), "ct_set_scale");
-          CtH og = sub(nxt.p, g * B, B);
-          ok(h, hegpu_merge_maps(h, gather.p, per, wd, og.p), st.label.c_str());
-        }
         break;
       }
       case HEGPU_STAGE_SQUARE: {
