@@ -101,11 +101,6 @@ CtH make_ct(hegpu_ctx* h, int count, int level) {
   ok(h, hegpu_ct_create(h, count, level, &p), "ct_create");
   return CtH(p);
 }
-CtH view(hegpu_ctx* h, const CtH& src, int first, int count) {
-  hegpu_ct* p = nullptr;
-  ok(h, hegpu_ct_view(src.p, first, count, &p), "ct_view");
-  return CtH(p);
-}
 
 // pack(values on slots [0, len), n_slots, Plaintext) encoded at `scale`, uploaded
 hegpu_pt* make_pt(hegpu_ctx* h, const double* z, int len, double scale, int level, int N) {
