@@ -110,15 +110,16 @@ def int_pipe_roofline(name, kd, clk_mhz):
             "peak_basis": f"{N_SM} SMs x {IMAD_WIDE_PER_CLK_SM} IMAD.WIDE.U32/clk/SM x {clk_mhz:.0f} MHz / {per}"}
 
 
-def ncu_traffic(kernel):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
-    from the newest committed ncu --set full capture of one step (profiles/),
-    or None"""
+def ncu_traffic(kernel, launches):
+    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` over one step
+    (the newest committed ncu capture, profiles/), per launch of the timer
+    run's `launches` per step (the ncu'd step runs as two 32-image parts, so
+    it has twice the launches at half the rows each), or None"""
     for name in ("r02_traffic_step.json", "r01_traffic_step.json"):
         try:
             with open(os.path.join(ROOT, "profiles", name)) as f:
                 t = json.load(f)
-            return float(t[kernel]["per_launch_bytes"]), name
+            return float(t[kernel]["dram_bytes"]) / max(1, launches), name
         except Exception:
             continue
     return None, None
@@ -384,7 +385,7 @@ def run_gpu(args):
         kd["compute_roofline"] = int_pipe_roofline(name, kd, clk_mhz)
     dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
     kd = kernels[dom]
-    traffic, traffic_src = ncu_traffic(dom)
+    traffic, traffic_src = ncu_traffic(dom, kd["launches"])
     ms_max = ref["ms"]
     sec = ms_max / 1e3
     ntt_rows = sum(kernels[k]["modmuls"] for k in NTT_KERNELS if k in kernels) / ((1 << (cfg.log_n - 1)) * cfg.log_n)
@@ -399,7 +400,7 @@ def run_gpu(args):
                 "compute": int_pipe_roofline(dom, kd, clk_mhz),
                 "note": "alg bytes / modmuls per launch per DESIGN.md §5 (LAUNCH_B byte models at each launch "
                         "site); achieved = alg bytes / summed CUDA-event launch time on the engine stream; "
-                        "traffic = ncu dram bytes per launch of one step (profiles/)"}
+                        "traffic = ncu dram bytes of the kernel over one step (profiles/) / launches_per_step"}
     tally, ks = ref["tally"], ref["ks"]
     line = {
         "metric": METRIC, "value": ref["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
